@@ -1,0 +1,204 @@
+"""TEST INFRASTRUCTURE ONLY — ctypes bindings for the CPU oracles.
+
+* ``Oracle``    : oracle/liboracle.so, the plain-C restatement (oracle.c).
+* ``Reference`` : oracle/_ref/libqref.so, the unmodified reference library
+                  (/root/reference/proj/src/*.cpp) behind ref_shim.cpp.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+``--impl reference`` legs may import this module, and only as the checker or
+the timed CPU baseline.  The product package never imports it.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "liboracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libqref.so")
+
+_u32p = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")
+_f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
+_u64p = np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS")
+
+KIND = {"quesadilla": 0, "topk": 1, "radix": 2, "comparison": 3}
+
+
+class OracleError(Exception):
+    def __init__(self, code: int, msg: str = ""):
+        super().__init__(f"status {code}: {msg}")
+        self.code = code
+
+
+def _u32(a):
+    return np.ascontiguousarray(a, dtype=np.uint32)
+
+
+class Oracle:
+    """The C restatement (oracle/oracle.c)."""
+
+    def __init__(self, path: str = ORACLE_SO):
+        self.lib = C.CDLL(path)
+        L = self.lib
+        L.qo_plan.argtypes = [_u32p, C.c_uint32, C.c_uint32, _u32p, C.c_uint32,
+                              C.POINTER(C.c_uint32)]
+        L.qo_partial_sort.argtypes = [C.c_uint32, _u32p, C.c_uint64, _u32p, _f64p,
+                                      _u32p, C.c_uint32, C.c_uint32]
+        L.qo_transpose.argtypes = [C.c_uint32, _u32p, C.c_uint64, _u32p, _f64p,
+                                   _u32p, C.c_int, C.c_uint32, C.c_int, _u32p,
+                                   C.c_uint32, C.POINTER(C.c_uint32)]
+        L.qo_bucket_starts.argtypes = [C.c_uint32, C.c_uint64, _u32p, _u32p,
+                                       C.c_uint32, _u64p]
+        L.qo_bucket_starts.restype = C.c_uint64
+        L.qo_is_sorted.argtypes = [C.c_uint32, C.c_uint64, _u32p, _u32p]
+
+    def plan(self, target, want: int = 0):
+        t = _u32(target)
+        steps = np.zeros(256, np.uint32)
+        n = C.c_uint32(0)
+        s = self.lib.qo_plan(t, len(t), want, steps, 128, C.byref(n))
+        if s:
+            raise OracleError(s)
+        return [(int(steps[2 * i]), int(steps[2 * i + 1])) for i in range(n.value)]
+
+    def partial_sort(self, dims, coords, values, prefix, mode):
+        dims = _u32(dims)
+        c = _u32(coords).copy()
+        v = np.ascontiguousarray(values, np.float64).copy()
+        p = _u32(prefix) if len(prefix) else np.zeros(1, np.uint32)
+        s = self.lib.qo_partial_sort(len(dims), dims, len(v), c, v, p, len(prefix), mode)
+        if s:
+            raise OracleError(s)
+        return c, v
+
+    def transpose(self, dims, coords, values, target, strategy="quesadilla", k=0,
+                  verify_input=False):
+        dims = _u32(dims)
+        c = _u32(coords).copy()
+        v = np.ascontiguousarray(values, np.float64).copy()
+        steps = np.zeros(256, np.uint32)
+        n = C.c_uint32(0)
+        s = self.lib.qo_transpose(len(dims), dims, len(v), c, v, _u32(target),
+                                  KIND[strategy], k, int(verify_input), steps, 128,
+                                  C.byref(n))
+        if s:
+            raise OracleError(s)
+        return c, v, [(int(steps[2 * i]), int(steps[2 * i + 1])) for i in range(n.value)]
+
+    def bucket_starts(self, rank, coords, modes):
+        c = _u32(coords)
+        nnz = len(c) // rank if rank else 0
+        out = np.zeros(max(nnz, 1), np.uint64)
+        m = _u32(modes) if len(modes) else np.zeros(1, np.uint32)
+        n = self.lib.qo_bucket_starts(rank, nnz, c, m, len(modes), out)
+        return out[:n].copy()
+
+    def is_sorted(self, rank, coords, order):
+        c = _u32(coords)
+        return bool(self.lib.qo_is_sorted(rank, len(c) // rank, c, _u32(order)))
+
+
+class Reference:
+    """The reference library itself (oracle/_ref/libqref.so)."""
+
+    def __init__(self, path: str = REF_SO):
+        self.lib = C.CDLL(path)
+        L = self.lib
+        L.qref_last_error.restype = C.c_char_p
+        L.qref_transpose.argtypes = [C.c_uint32, _u32p, C.c_uint64, _u32p, _f64p,
+                                     _u32p, C.c_int, C.c_uint32, C.c_uint32, C.c_int,
+                                     _u32p, C.c_uint32, C.POINTER(C.c_uint32)]
+        L.qref_partial_sort.argtypes = [C.c_uint32, _u32p, C.c_uint64, _u32p, _f64p,
+                                        _u32p, C.c_uint32, C.c_uint32, C.c_uint32]
+        L.qref_plan.argtypes = [_u32p, C.c_uint32, C.c_uint32, _u32p, C.c_uint32,
+                                C.POINTER(C.c_uint32)]
+        L.qref_min_plan_bruteforce.argtypes = [_u32p, C.c_uint32, C.POINTER(C.c_int),
+                                               C.POINTER(C.c_int)]
+        L.qref_required_sort_count.argtypes = [_u32p, _u32p, C.c_uint32,
+                                               C.POINTER(C.c_int)]
+        L.qref_pass_histogram.argtypes = [C.c_uint32, np.ctypeslib.ndpointer(
+            np.int64, flags="C_CONTIGUOUS"), C.c_uint32]
+        L.qref_generate.argtypes = [C.c_uint32, _u32p, C.c_uint64, C.c_uint64, C.c_int,
+                                    _u32p, _f64p]
+        L.qref_bucket_starts.argtypes = [C.c_uint32, _u32p, C.c_uint64, _u32p, _f64p,
+                                         _u32p, C.c_uint32, _u64p,
+                                         C.POINTER(C.c_uint64)]
+        L.qref_is_sorted.argtypes = [C.c_uint32, _u32p, C.c_uint64, _u32p, _f64p,
+                                     _u32p, C.POINTER(C.c_int)]
+        L.qref_ctx_create.restype = C.c_void_p
+        L.qref_ctx_create.argtypes = [C.c_uint32, _u32p, C.c_uint64, _u32p, _f64p]
+        L.qref_ctx_destroy.argtypes = [C.c_void_p]
+        L.qref_ctx_reset.argtypes = [C.c_void_p, _u32p, _f64p]
+        L.qref_ctx_transpose.argtypes = [C.c_void_p, _u32p, C.c_uint32]
+        L.qref_ctx_read.argtypes = [C.c_void_p, _u32p, _f64p]
+        L.qref_default_workers.restype = C.c_uint
+
+    def _check(self, s):
+        if s:
+            raise OracleError(s, self.lib.qref_last_error().decode())
+
+    def transpose(self, dims, coords, values, target, strategy="quesadilla", k=0,
+                  workers=1, verify_input=False):
+        dims = _u32(dims)
+        c = _u32(coords).copy()
+        v = np.ascontiguousarray(values, np.float64).copy()
+        steps = np.zeros(256, np.uint32)
+        n = C.c_uint32(0)
+        self._check(self.lib.qref_transpose(len(dims), dims, len(v), c, v, _u32(target),
+                                            KIND[strategy], k, workers, int(verify_input),
+                                            steps, 128, C.byref(n)))
+        return c, v, [(int(steps[2 * i]), int(steps[2 * i + 1])) for i in range(n.value)]
+
+    def partial_sort(self, dims, coords, values, prefix, mode, workers=1):
+        dims = _u32(dims)
+        c = _u32(coords).copy()
+        v = np.ascontiguousarray(values, np.float64).copy()
+        p = _u32(prefix) if len(prefix) else np.zeros(1, np.uint32)
+        self._check(self.lib.qref_partial_sort(len(dims), dims, len(v), c, v, p,
+                                               len(prefix), mode, workers))
+        return c, v
+
+    def plan(self, target, want: int = 0):
+        t = _u32(target)
+        steps = np.zeros(256, np.uint32)
+        n = C.c_uint32(0)
+        self._check(self.lib.qref_plan(t, len(t), want, steps, 128, C.byref(n)))
+        return [(int(steps[2 * i]), int(steps[2 * i + 1])) for i in range(n.value)]
+
+    def min_plan_bruteforce(self, target):
+        a, b = C.c_int(0), C.c_int(0)
+        t = _u32(target)
+        self._check(self.lib.qref_min_plan_bruteforce(t, len(t), C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+    def pass_histogram(self, rank):
+        h = np.zeros(16, np.int64)
+        self._check(self.lib.qref_pass_histogram(rank, h, 16))
+        return {i: int(x) for i, x in enumerate(h) if x}
+
+    def generate(self, dims, nnz, seed, distinct=False):
+        dims = _u32(dims)
+        c = np.zeros(nnz * len(dims), np.uint32)
+        v = np.zeros(nnz, np.float64)
+        self._check(self.lib.qref_generate(len(dims), dims, nnz, seed, int(distinct), c, v))
+        return c, v
+
+    def bucket_starts(self, dims, coords, values, modes):
+        dims = _u32(dims)
+        c = _u32(coords)
+        v = np.ascontiguousarray(values, np.float64)
+        out = np.zeros(max(len(v), 1), np.uint64)
+        n = C.c_uint64(0)
+        m = _u32(modes) if len(modes) else np.zeros(1, np.uint32)
+        self._check(self.lib.qref_bucket_starts(len(dims), dims, len(v), c, v, m,
+                                                len(modes), out, C.byref(n)))
+        return out[: n.value].copy()
+
+    def default_workers(self):
+        return int(self.lib.qref_default_workers())
+
+
+def reference_available() -> bool:
+    return os.path.exists(REF_SO)
