@@ -1,0 +1,176 @@
+/* quesadilla_b200 — C ABI of the B200-native Quesadilla COO transpose.
+ *
+ * The drop-in boundary for the reference's transpose path
+ * (arxiv 2005.10427 artifact, /root/reference/proj).  Plain pointers and
+ * sizes only; no C++ or torch types cross this boundary; no exceptions cross
+ * it either — every reference exception maps to a status code:
+ *
+ *   QD_INVALID_ARGUMENT  <-> std::invalid_argument
+ *   QD_OUT_OF_RANGE      <-> std::out_of_range   (coordinate >= dimension)
+ *   QD_CUDA_ERROR / QD_NO_DEVICE: device failures (no CPU fallback exists).
+ *
+ * Layout (identical to quesadilla::CooTensor, coo.hpp:16-24):
+ *   coords : nnz * rank uint32, row-major AoS (row j, mode m at j*rank+m)
+ *   values : nnz float64
+ *   dims   : rank uint32, each >= 1
+ * A target ordering is a permutation of 0..rank-1, highest priority first
+ * (quesadilla::Ordering, ordering.hpp:38-61).
+ *
+ * Semantics are bit-exact with the reference: the output rows are exactly
+ * what quesadilla::transpose_inplace produces (stable; values only moved).
+ * Functions are synchronous with respect to the host (like the reference);
+ * the *_device variants enqueue on `stream` (a cudaStream_t, may be NULL for
+ * the legacy stream) and synchronise it before returning the status.
+ */
+#ifndef QUESADILLA_B200_H
+#define QUESADILLA_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QD_ABI_VERSION 1
+#define QD_MAX_RANK 64 /* quesadilla::kMaxRank, ordering.hpp:14 */
+
+typedef enum qd_status {
+  QD_OK = 0,
+  QD_INVALID_ARGUMENT = 1,
+  QD_OUT_OF_RANGE = 2,
+  QD_CUDA_ERROR = 3,
+  QD_NCCL_ERROR = 4,
+  QD_NO_DEVICE = 5
+} qd_status;
+
+/* quesadilla::SortStrategy::Kind, transpose.hpp:22. */
+typedef enum qd_strategy_kind {
+  QD_QUESADILLA = 0,
+  QD_TOPK = 1,
+  QD_FULL_RADIX = 2,
+  QD_COMPARISON_SORT = 3
+} qd_strategy_kind;
+
+/* quesadilla::PlanStep, plan.hpp:13-20. */
+typedef struct qd_plan_step {
+  uint32_t prefix_len;
+  uint32_t mode;
+} qd_plan_step;
+
+/* quesadilla::TransposeOptions, transpose.hpp:45-54, plus device extras. */
+typedef struct qd_options {
+  int verify_input;            /* throw invalid_argument unless simply sorted */
+  uint32_t workers;            /* ParallelConfig::workers; 0 rejected like the
+                                  reference (parallel.cpp:161-163), otherwise
+                                  the GPU uses all of its SMs */
+  qd_plan_step* pass_log;      /* optional: receives the executed LOGICAL steps */
+  uint32_t pass_log_capacity;
+  uint32_t* pass_log_len;      /* out: number of steps executed */
+  /* optional: output segment/pos boundaries = start rows of the maximal runs
+   * of the leading target mode in the output (detail::bucket_starts(out,
+   * {target[0]}), sort.cpp:136-147) followed by nnz.  Host pointer for the
+   * host API, device pointer for the device API; capacity nnz + 1. */
+  uint64_t* boundaries;
+  uint64_t* n_boundaries;      /* out: number of entries written (incl. nnz) */
+} qd_options;
+
+typedef struct qd_workspace qd_workspace; /* quesadilla::Workspace, sort.hpp:14-21 */
+
+/* ---- runtime ------------------------------------------------------------ */
+int qd_abi_version(void);
+const char* qd_last_error(void);          /* thread-local message */
+/* Row / mode of the last QD_OUT_OF_RANGE (input row index). */
+void qd_last_error_detail(uint64_t* row, uint32_t* mode);
+
+qd_status qd_workspace_create(int device, qd_workspace** out);
+void qd_workspace_destroy(qd_workspace* ws);
+/* Bytes of device memory currently held by the workspace. */
+uint64_t qd_workspace_bytes(const qd_workspace* ws);
+/* Number of CUDA kernels this workspace has launched since creation. */
+uint64_t qd_workspace_launches(const qd_workspace* ws);
+
+/* ---- planner (host; planner.hpp:13-55, plan.hpp:27-36) ------------------ */
+qd_status qd_quesadilla_plan(const uint32_t* target, uint32_t rank,
+                             qd_plan_step* steps, uint32_t capacity,
+                             uint32_t* n_steps);
+qd_status qd_prefix_plan(const uint32_t* target, uint32_t rank,
+                         uint32_t prefix_len, qd_plan_step* steps,
+                         uint32_t capacity, uint32_t* n_steps);
+qd_status qd_required_sort_count(const uint32_t* source, const uint32_t* target,
+                                 uint32_t rank, int* out);
+qd_status qd_apply_transition(const uint32_t* current, uint32_t rank,
+                              qd_plan_step step, uint32_t* next);
+qd_status qd_strategy_pass_cost(qd_strategy_kind kind, uint32_t k,
+                                const uint32_t* target, uint32_t rank,
+                                int* total, int* bucketed);
+
+/* ---- transpose (transpose.hpp:59-80) ------------------------------------ */
+
+/* Host buffers, in place: quesadilla::transpose_inplace (transpose.cpp:79-112).
+ * Copies H2D, runs the planned passes on the GPU, copies D2H.  Pinned host
+ * buffers give full link bandwidth.  On error the host buffers are left
+ * unmodified (strong guarantee; the reference gives the basic one). */
+qd_status qd_transpose_inplace(uint32_t rank, const uint32_t* dims, uint64_t nnz,
+                               uint32_t* coords, double* values,
+                               const uint32_t* target, qd_strategy_kind kind,
+                               uint32_t k, const qd_options* opts,
+                               qd_workspace* ws);
+
+/* Device-resident, out of place (in and out must not overlap). */
+qd_status qd_transpose_device(uint32_t rank, const uint32_t* dims, uint64_t nnz,
+                              const uint32_t* d_coords_in,
+                              const double* d_values_in, uint32_t* d_coords_out,
+                              double* d_values_out, const uint32_t* target,
+                              qd_strategy_kind kind, uint32_t k,
+                              const qd_options* opts, qd_workspace* ws,
+                              void* stream);
+
+/* ---- one partial sort (sort.hpp:32-33, parallel.hpp:35-37) -------------- */
+qd_status qd_partial_sort(uint32_t rank, const uint32_t* dims, uint64_t nnz,
+                          uint32_t* coords, double* values,
+                          const uint32_t* prefix, uint32_t prefix_len,
+                          uint32_t mode, qd_workspace* ws);
+qd_status qd_partial_sort_device(uint32_t rank, const uint32_t* dims,
+                                 uint64_t nnz, const uint32_t* d_coords_in,
+                                 const double* d_values_in,
+                                 uint32_t* d_coords_out, double* d_values_out,
+                                 const uint32_t* prefix, uint32_t prefix_len,
+                                 uint32_t mode, qd_workspace* ws, void* stream);
+
+/* ---- checks and boundaries ---------------------------------------------- */
+/* is_sorted_under (coo.cpp:32-49) on device coords; *out = 0/1. */
+qd_status qd_is_sorted_device(uint32_t rank, uint64_t nnz,
+                              const uint32_t* d_coords, const uint32_t* order,
+                              int* out, qd_workspace* ws, void* stream);
+/* detail::bucket_starts (sort.cpp:136-147) on device coords, followed by nnz:
+ * d_starts (device, capacity nnz + 1) receives the run starts + nnz. */
+qd_status qd_bucket_starts_device(uint32_t rank, uint64_t nnz,
+                                  const uint32_t* d_coords,
+                                  const uint32_t* modes, uint32_t n_modes,
+                                  uint64_t* d_starts, uint64_t* n_starts,
+                                  qd_workspace* ws, void* stream);
+
+/* ---- multi-GPU sharding helpers (device) -------------- */
+/* Histogram of mode `mode` over rows (device, n_bins = dims[mode] counters,
+ * uint64), accumulated into d_hist. */
+qd_status qd_mode_histogram_device(uint32_t rank, uint64_t nnz,
+                                   const uint32_t* d_coords, uint32_t mode,
+                                   uint32_t dim, uint64_t* d_hist,
+                                   qd_workspace* ws, void* stream);
+/* Stable partition of rows into n_parts destination parts by
+ * part = lookup[coords[row*rank+mode]] (d_lookup: dim uint32 entries < n_parts).
+ * Writes the rows grouped by part, input order kept inside each part, and
+ * part_counts[n_parts] (host). */
+qd_status qd_partition_rows_device(uint32_t rank, uint64_t nnz,
+                                   const uint32_t* d_coords_in,
+                                   const double* d_values_in, uint32_t mode,
+                                   uint32_t dim, const uint32_t* d_lookup,
+                                   uint32_t n_parts, uint32_t* d_coords_out,
+                                   double* d_values_out, uint64_t* part_counts,
+                                   qd_workspace* ws, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QUESADILLA_B200_H */

@@ -1,0 +1,274 @@
+// extern "C" layer: the drop-in boundary (include/quesadilla_b200.h).
+// Validation mirrors the reference's argument checks so the same calls fail
+// with the same exception class (mapped to qd_status):
+//   transpose.cpp:83-89 (rank, verify_input), transpose.cpp:101-103 (top-K),
+//   sort.cpp:153-166 (partial_sort args), parallel.cpp:161-163 (workers).
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "internal.hpp"
+
+using namespace qb200;
+
+namespace {
+
+thread_local std::string g_msg;
+thread_local uint64_t g_row = 0;
+thread_local uint32_t g_mode = 0;
+
+template <class F>
+qd_status guard(F&& f) {
+  try {
+    f();
+    g_msg.clear();
+    return QD_OK;
+  } catch (const Error& e) {
+    g_msg = e.what();
+    g_row = e.row;
+    g_mode = e.mode;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_msg = "host allocation failed";
+    return QD_CUDA_ERROR;
+  } catch (const std::exception& e) {
+    g_msg = e.what();
+    return QD_CUDA_ERROR;
+  }
+}
+
+void check_tensor(uint32_t rank, const uint32_t* dims, uint64_t nnz, const void* c,
+                  const void* v) {
+  if (rank == 0 || rank > QD_MAX_RANK) invalid("tensor rank must be in 1..64");
+  if (!dims) invalid("dims is null");
+  for (uint32_t m = 0; m < rank; ++m)
+    if (dims[m] == 0) invalid("dimension of mode " + std::to_string(m) + " must be positive");
+  if (nnz && (!c || !v)) invalid("coordinate or value buffer is null");
+  if (nnz >= (uint64_t{1} << 32))
+    invalid("nnz must be below 2^32 (the reference's u32 counters, sort.hpp:15-18)");
+}
+
+void log_steps(const qd_options* o, const std::vector<Step>& steps) {
+  if (!o || !o->pass_log_len) return;
+  *o->pass_log_len = static_cast<uint32_t>(steps.size());
+  if (!o->pass_log) return;
+  for (size_t i = 0; i < steps.size() && i < o->pass_log_capacity; ++i)
+    o->pass_log[i] = {steps[i].prefix_len, steps[i].mode};
+}
+
+// ParallelConfig{0} is rejected where the reference would reach
+// parallel_partial_sort (any executed step, parallel.cpp:161-163) or the
+// top-K bucket phase (parallel.cpp:194-196); elsewhere it is never read.
+void check_workers(const qd_options* o, qd_strategy_kind kind, const std::vector<Step>& steps) {
+  if (o && o->workers == 0 && (!steps.empty() || kind == QD_TOPK))
+    invalid("worker count must be at least 1");
+}
+
+void copy_steps(const std::vector<Step>& s, qd_plan_step* out, uint32_t cap, uint32_t* n) {
+  if (n) *n = static_cast<uint32_t>(s.size());
+  for (size_t i = 0; i < s.size() && i < cap && out; ++i) out[i] = {s[i].prefix_len, s[i].mode};
+}
+
+std::vector<Group> partial_sort_group(uint32_t rank, const uint32_t* prefix, uint32_t plen,
+                                      uint32_t mode) {
+  // validate_sort_args, sort.cpp:153-166
+  if (mode >= rank) invalid("sort mode out of range");
+  if (plen >= rank) invalid("prefix length out of range");
+  for (uint32_t i = 0; i < plen; ++i) {
+    if (prefix[i] >= rank) invalid("prefix mode out of range");
+    if (prefix[i] == mode) invalid("sort mode lies inside the bucketing prefix");
+  }
+  Group g;
+  g.prefix.assign(prefix, prefix + plen);
+  g.keys = {mode};
+  g.n_steps = 1;
+  return {g};
+}
+
+}  // namespace
+
+extern "C" {
+
+int qd_abi_version(void) { return QD_ABI_VERSION; }
+const char* qd_last_error(void) { return g_msg.c_str(); }
+void qd_last_error_detail(uint64_t* row, uint32_t* mode) {
+  if (row) *row = g_row;
+  if (mode) *mode = g_mode;
+}
+
+qd_status qd_workspace_create(int device, qd_workspace** out) {
+  return guard([&] {
+    if (!out) invalid("out is null");
+    *out = reinterpret_cast<qd_workspace*>(workspace_create(device));
+  });
+}
+void qd_workspace_destroy(qd_workspace* ws) {
+  workspace_destroy(reinterpret_cast<Workspace*>(ws));
+}
+uint64_t qd_workspace_bytes(const qd_workspace* ws) {
+  return ws ? workspace_bytes(reinterpret_cast<const Workspace*>(ws)) : 0;
+}
+uint64_t qd_workspace_launches(const qd_workspace* ws) {
+  return ws ? workspace_launches(reinterpret_cast<const Workspace*>(ws)) : 0;
+}
+
+qd_status qd_quesadilla_plan(const uint32_t* target, uint32_t rank, qd_plan_step* steps,
+                             uint32_t capacity, uint32_t* n_steps) {
+  return guard([&] { copy_steps(plan_to_prefix(target, rank, rank), steps, capacity, n_steps); });
+}
+
+qd_status qd_prefix_plan(const uint32_t* target, uint32_t rank, uint32_t prefix_len,
+                         qd_plan_step* steps, uint32_t capacity, uint32_t* n_steps) {
+  return guard([&] {
+    check_ordering(target, rank);
+    if (prefix_len < 1 || prefix_len > rank) invalid("prefix length must be in 1..rank");
+    copy_steps(plan_to_prefix(target, rank, prefix_len), steps, capacity, n_steps);
+  });
+}
+
+qd_status qd_required_sort_count(const uint32_t* source, const uint32_t* target, uint32_t rank,
+                                 int* out) {
+  return guard([&] { *out = required_sort_count(source, target, rank); });
+}
+
+qd_status qd_apply_transition(const uint32_t* current, uint32_t rank, qd_plan_step step,
+                              uint32_t* next) {
+  return guard([&] {
+    auto v = apply_transition(current, rank, Step{step.prefix_len, step.mode});
+    std::memcpy(next, v.data(), rank * sizeof(uint32_t));
+  });
+}
+
+qd_status qd_strategy_pass_cost(qd_strategy_kind kind, uint32_t k, const uint32_t* target,
+                                uint32_t rank, int* total, int* bucketed) {
+  return guard([&] {
+    std::vector<Step> steps;
+    if (kind == QD_TOPK && (k < 1 || k > rank)) invalid("prefix length must be in 1..rank");
+    strategy_groups(target, rank, kind, k, &steps);
+    int b = 0;
+    for (auto& s : steps) b += s.prefix_len > 0;
+    *total = static_cast<int>(steps.size());
+    *bucketed = b;
+  });
+}
+
+qd_status qd_transpose_inplace(uint32_t rank, const uint32_t* dims, uint64_t nnz,
+                               uint32_t* coords, double* values, const uint32_t* target,
+                               qd_strategy_kind kind, uint32_t k, const qd_options* opts,
+                               qd_workspace* ws) {
+  return guard([&] {
+    if (!ws) invalid("workspace is null");
+    check_tensor(rank, dims, nnz, coords, values);
+    check_ordering(target, rank);
+    std::vector<Step> steps;
+    auto groups = strategy_groups(target, rank, kind, k, &steps);
+    check_workers(opts, kind, steps);
+    TensorView t{rank, dims, nnz};
+    run_groups_host(*reinterpret_cast<Workspace*>(ws), t, coords, values, groups,
+                    opts && opts->verify_input, opts ? opts->boundaries : nullptr,
+                    opts ? opts->n_boundaries : nullptr, target[0]);
+    log_steps(opts, steps);
+  });
+}
+
+qd_status qd_transpose_device(uint32_t rank, const uint32_t* dims, uint64_t nnz,
+                              const uint32_t* d_coords_in, const double* d_values_in,
+                              uint32_t* d_coords_out, double* d_values_out,
+                              const uint32_t* target, qd_strategy_kind kind, uint32_t k,
+                              const qd_options* opts, qd_workspace* ws, void* stream) {
+  return guard([&] {
+    if (!ws) invalid("workspace is null");
+    check_tensor(rank, dims, nnz, d_coords_in, d_values_in);
+    if (nnz && (!d_coords_out || !d_values_out)) invalid("output buffer is null");
+    if (nnz && (d_coords_out == d_coords_in || d_values_out == d_values_in))
+      invalid("device transpose is out of place: input and output must differ");
+    check_ordering(target, rank);
+    std::vector<Step> steps;
+    auto groups = strategy_groups(target, rank, kind, k, &steps);
+    check_workers(opts, kind, steps);
+    TensorView t{rank, dims, nnz};
+    run_groups(*reinterpret_cast<Workspace*>(ws), t, d_coords_in, d_values_in, d_coords_out,
+               d_values_out, groups, opts && opts->verify_input,
+               opts ? opts->boundaries : nullptr, opts ? opts->n_boundaries : nullptr, target[0],
+               stream);
+    log_steps(opts, steps);
+  });
+}
+
+qd_status qd_partial_sort(uint32_t rank, const uint32_t* dims, uint64_t nnz, uint32_t* coords,
+                          double* values, const uint32_t* prefix, uint32_t prefix_len,
+                          uint32_t mode, qd_workspace* ws) {
+  return guard([&] {
+    if (!ws) invalid("workspace is null");
+    check_tensor(rank, dims, nnz, coords, values);
+    auto groups = partial_sort_group(rank, prefix, prefix_len, mode);
+    TensorView t{rank, dims, nnz};
+    run_groups_host(*reinterpret_cast<Workspace*>(ws), t, coords, values, groups, false, nullptr,
+                    nullptr, 0);
+  });
+}
+
+qd_status qd_partial_sort_device(uint32_t rank, const uint32_t* dims, uint64_t nnz,
+                                 const uint32_t* d_coords_in, const double* d_values_in,
+                                 uint32_t* d_coords_out, double* d_values_out,
+                                 const uint32_t* prefix, uint32_t prefix_len, uint32_t mode,
+                                 qd_workspace* ws, void* stream) {
+  return guard([&] {
+    if (!ws) invalid("workspace is null");
+    check_tensor(rank, dims, nnz, d_coords_in, d_values_in);
+    if (nnz && (d_coords_out == d_coords_in || d_values_out == d_values_in))
+      invalid("device partial sort is out of place: input and output must differ");
+    auto groups = partial_sort_group(rank, prefix, prefix_len, mode);
+    TensorView t{rank, dims, nnz};
+    run_groups(*reinterpret_cast<Workspace*>(ws), t, d_coords_in, d_values_in, d_coords_out,
+               d_values_out, groups, false, nullptr, nullptr, 0, stream);
+  });
+}
+
+qd_status qd_is_sorted_device(uint32_t rank, uint64_t nnz, const uint32_t* d_coords,
+                              const uint32_t* order, int* out, qd_workspace* ws, void* stream) {
+  return guard([&] {
+    if (!ws || !out) invalid("null argument");
+    check_ordering(order, rank);
+    *out = is_sorted_device(*reinterpret_cast<Workspace*>(ws), rank, nnz, d_coords, order, stream);
+  });
+}
+
+qd_status qd_bucket_starts_device(uint32_t rank, uint64_t nnz, const uint32_t* d_coords,
+                                  const uint32_t* modes, uint32_t n_modes, uint64_t* d_starts,
+                                  uint64_t* n_starts, qd_workspace* ws, void* stream) {
+  return guard([&] {
+    if (!ws) invalid("workspace is null");
+    for (uint32_t i = 0; i < n_modes; ++i)
+      if (modes[i] >= rank) invalid("mode out of range");
+    const uint64_t n = bucket_starts_device(*reinterpret_cast<Workspace*>(ws), rank, nnz,
+                                            d_coords, modes, n_modes, d_starts, stream);
+    if (n_starts) *n_starts = n;
+  });
+}
+
+qd_status qd_mode_histogram_device(uint32_t rank, uint64_t nnz, const uint32_t* d_coords,
+                                   uint32_t mode, uint32_t dim, uint64_t* d_hist,
+                                   qd_workspace* ws, void* stream) {
+  return guard([&] {
+    if (!ws) invalid("workspace is null");
+    if (mode >= rank) invalid("mode out of range");
+    mode_histogram_device(*reinterpret_cast<Workspace*>(ws), rank, nnz, d_coords, mode, dim,
+                          d_hist, stream);
+  });
+}
+
+qd_status qd_partition_rows_device(uint32_t rank, uint64_t nnz, const uint32_t* d_coords_in,
+                                   const double* d_values_in, uint32_t mode, uint32_t dim,
+                                   const uint32_t* d_lookup, uint32_t n_parts,
+                                   uint32_t* d_coords_out, double* d_values_out,
+                                   uint64_t* part_counts, qd_workspace* ws, void* stream) {
+  return guard([&] {
+    if (!ws) invalid("workspace is null");
+    partition_rows_device(*reinterpret_cast<Workspace*>(ws), rank, nnz, d_coords_in, d_values_in,
+                          mode, dim, d_lookup, n_parts, d_coords_out, d_values_out, part_counts,
+                          stream);
+  });
+}
+
+}  // extern "C"

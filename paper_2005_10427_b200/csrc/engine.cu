@@ -1,0 +1,1448 @@
+// B200 (sm_100a) device engine of the Quesadilla COO transpose.
+//
+// Every logical plan group (internal.hpp: a run of same-prefix plan steps)
+// is one SEGMENTED STABLE SORT: rows are cut into maximal runs agreeing on
+// the group's prefix modes (Alg. 2's "buckets", sort.cpp:80-134), and each
+// run is stably sorted by the group's combined key (Alg. 1 when the prefix is
+// empty, sort.cpp:54-78; consecutive same-prefix steps compose LSD-wise into
+// one combined key).  Device work per group:
+//
+//   k_heads / scan / k_compact   segment discovery (bucket_starts, sort.cpp:136)
+//   k_classify / k_gen_tiles     small runs -> local chunks, large runs -> tiles
+//   k_hist                       per-run digit histograms of every pass in one
+//                                read, + range check (count_keys, sort.cpp:54-64)
+//   k_onesweep  (D passes)       stable counting pass of one radix digit per
+//                                tile: warp-match ranking in shared memory,
+//                                decoupled look-back across the tiles of a run,
+//                                coalesced scatter of whole rows (AoS coords +
+//                                f64 value) staged through shared memory
+//   k_local                      runs that fit one CTA: loaded once, fully
+//                                sorted in shared memory, written once
+//
+// Rows are always moved whole (the reference's scatter_rows), so there is no
+// separate gather.  No CPU fallback exists: every path here is a kernel.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <string>
+
+#include "internal.hpp"
+
+namespace qb200 {
+
+#define QD_CUDA(x)                                                              \
+  do {                                                                          \
+    cudaError_t e_ = (x);                                                       \
+    if (e_ != cudaSuccess)                                                      \
+      throw Error(QD_CUDA_ERROR, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kRadixLog = 8;
+constexpr int kBins = 1 << kRadixLog;
+constexpr int kMaxTerms = 12;
+constexpr int kMaxKeys = QD_MAX_RANK;
+constexpr int kHistPasses = 8;  // passes histogrammed per k_hist launch
+
+// ---------------------------------------------------------------------------
+// kernel parameter blocks
+// ---------------------------------------------------------------------------
+
+// Digit of one pass: bits [lo, lo+b) of the combined key, gathered from at
+// most kMaxTerms mode fields.
+struct DigitSpec {
+  uint32_t n;
+  uint8_t mode[kMaxTerms], rsh[kMaxTerms], bits[kMaxTerms], lsh[kMaxTerms];
+  // lookup digit (stable partition): digit = lookup[row[lookup_mode]]
+  const uint32_t* lookup;
+  uint32_t lookup_mode, lookup_dim;
+};
+
+// Combined key of a group: keys[0] most significant; field i occupies
+// [off[i], off[i] + width[i]).
+struct KeySpec {
+  uint32_t n;
+  uint32_t total_bits;
+  int check;  // range-check key coordinates against dim
+  uint8_t mode[kMaxKeys], width[kMaxKeys];
+  uint16_t off[kMaxKeys];
+  uint32_t dim[kMaxKeys];
+};
+
+struct ErrBlock {
+  unsigned int flags;  // bit0 out_of_range, bit1 not simply sorted
+  unsigned int pad;
+  unsigned long long rowmode;  // min over (row << 6 | mode)
+};
+
+struct TileDesc {
+  unsigned long long row_begin;
+  unsigned int len;
+  unsigned int li_first;  // (large-run index << 1) | first-tile-of-run
+};
+
+struct PassArgs {
+  const uint32_t* in_c;
+  const double* in_v;
+  uint32_t* out_c;
+  double* out_v;
+  uint32_t rank;
+  uint64_t nnz;
+  uint32_t T;                               // rows per tile
+  const TileDesc* tiles;                    // nullptr: uniform tiles of [0,nnz)
+  uint32_t num_tiles;
+  const unsigned long long* run_start;      // [li]; nullptr: run 0 starts at 0
+  const uint32_t* hist;                     // [li][pass][kBins], this pass
+  uint32_t hist_stride;                     // D * kBins
+  unsigned long long* status;               // [tile][kBins]
+  uint32_t epoch;
+  uint32_t* tile_counter;
+  DigitSpec dig;
+};
+
+struct HistArgs {
+  const uint32_t* in_c;
+  uint32_t rank;
+  uint64_t nnz;
+  uint32_t T;
+  const TileDesc* tiles;
+  uint32_t num_tiles;
+  uint32_t tiles_per_cta;
+  uint32_t np;                              // passes in this launch
+  uint32_t pass0;
+  uint32_t* hist;
+  uint32_t hist_stride;
+  DigitSpec dig[kHistPasses];
+  KeySpec key;
+  int do_check;
+  ErrBlock* err;
+};
+
+struct LocalArgs {
+  const uint32_t* in_c;
+  const double* in_v;
+  uint32_t* out_c;
+  double* out_v;
+  uint32_t rank;
+  uint64_t nnz;
+  uint32_t TL;  // chunk span; runs with len <= TL are "small"
+  uint32_t cap; // rows per chunk buffer (>= 2*TL, or nnz for a single run)
+  const unsigned long long* seg_start;  // S+1 entries; nullptr: one run [0,nnz)
+  uint64_t nseg;
+  KeySpec key;
+  ErrBlock* err;
+};
+
+// ---------------------------------------------------------------------------
+// device helpers
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ uint32_t digit_of(const uint32_t* row, const DigitSpec& d) {
+  if (d.lookup) {
+    uint32_t c = row[d.lookup_mode];
+    return c < d.lookup_dim ? __ldg(d.lookup + c) : 0u;
+  }
+  uint32_t v = 0;
+#pragma unroll 1
+  for (uint32_t i = 0; i < d.n; ++i)
+    v |= ((row[d.mode[i]] >> d.rsh[i]) & ((1u << d.bits[i]) - 1u)) << d.lsh[i];
+  return v;
+}
+
+__device__ __forceinline__ uint64_t full_key(const uint32_t* row, const KeySpec& k) {
+  uint64_t v = 0;
+#pragma unroll 1
+  for (uint32_t i = 0; i < k.n; ++i) {
+    const uint32_t w = k.width[i];
+    if (w) v |= (uint64_t)(row[k.mode[i]] & (uint32_t)((1ull << w) - 1ull)) << k.off[i];
+  }
+  return v;
+}
+
+__device__ __forceinline__ void check_row(const uint32_t* row, const KeySpec& k,
+                                          uint64_t grow, ErrBlock* e) {
+#pragma unroll 1
+  for (uint32_t i = 0; i < k.n; ++i) {
+    if (row[k.mode[i]] >= k.dim[i]) {
+      atomicOr(&e->flags, 1u);
+      atomicMin(&e->rowmode, (unsigned long long)((grow << 6) | k.mode[i]));
+    }
+  }
+}
+
+__device__ __forceinline__ void st_relaxed(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+constexpr unsigned long long kFlagAgg = 1ull << 62;
+constexpr unsigned long long kFlagPre = 2ull << 62;
+constexpr unsigned long long kValMask = (1ull << 48) - 1ull;
+
+__device__ __forceinline__ unsigned long long enc(unsigned long long flag, uint32_t epoch,
+                                                  unsigned long long v) {
+  return flag | ((unsigned long long)(epoch & 0x3FFFu) << 48) | v;
+}
+
+// Exclusive scan across the block of one value per thread.
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_tmp,
+                                                    uint32_t* total = nullptr) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_tmp[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    uint32_t t = lane < kWarps ? s_tmp[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t y = __shfl_up_sync(0xFFFFFFFFu, t, o);
+      if (lane >= o) t += y;
+    }
+    if (lane < kWarps) s_tmp[lane] = t;  // inclusive warp totals
+  }
+  __syncthreads();
+  const uint32_t before = w ? s_tmp[w - 1] : 0;
+  const uint32_t tot = s_tmp[kWarps - 1];
+  __syncthreads();
+  if (total) *total = tot;
+  return before + x - v;
+}
+
+// Same for 64-bit values.
+__device__ __forceinline__ unsigned long long block_excl_scan64(unsigned long long v,
+                                                                unsigned long long* s_tmp) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  unsigned long long x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    unsigned long long y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_tmp[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    unsigned long long t = lane < kWarps ? s_tmp[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      unsigned long long y = __shfl_up_sync(0xFFFFFFFFu, t, o);
+      if (lane >= o) t += y;
+    }
+    if (lane < kWarps) s_tmp[lane] = t;
+  }
+  __syncthreads();
+  const unsigned long long before = w ? s_tmp[w - 1] : 0;
+  __syncthreads();
+  return before + x - v;
+}
+
+// Stable per-warp ranking of positions [0, n): positions are cut into kWarps
+// contiguous stripes of `ipw`; warp w walks its stripe in rounds of 32, so
+// rank order = position order.  s_rank[p] = rank of p among equal digits
+// earlier in its stripe; s_whist[w][d] = count of digit d in stripe w.
+template <class F>
+__device__ __forceinline__ void warp_rank(F get_digit, uint32_t n, uint32_t ipw,
+                                          uint16_t* s_rank, uint32_t* s_whist) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t* wh = s_whist + w * kBins;
+  const uint32_t lo = w * ipw;
+  const uint32_t hi = min(n, lo + ipw);
+  for (uint32_t base = lo; base < hi; base += 32) {
+    const uint32_t p = base + lane;
+    const bool valid = p < hi;
+    const uint32_t d = valid ? get_digit(p) : 0xFFFFFFFFu;
+    const unsigned peers = __match_any_sync(0xFFFFFFFFu, d);
+    const int leader = __ffs(peers) - 1;
+    uint32_t b = 0;
+    if (valid && lane == leader) {
+      b = wh[d];
+      wh[d] = b + __popc(peers);
+    }
+    b = __shfl_sync(0xFFFFFFFFu, b, leader);
+    if (valid) s_rank[p] = (uint16_t)(b + __popc(peers & ((1u << lane) - 1u)));
+  }
+}
+
+// Turn per-warp counts into per-bin warp-exclusive offsets; s_cnt[b] = total.
+__device__ __forceinline__ void bin_totals(uint32_t* s_whist, uint32_t* s_cnt) {
+  for (int b = threadIdx.x; b < kBins; b += kThreads) {
+    uint32_t run = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+      const uint32_t c = s_whist[w * kBins + b];
+      s_whist[w * kBins + b] = run;
+      run += c;
+    }
+    s_cnt[b] = run;
+  }
+}
+
+// Load words [a, a+nw) of g into s_raw so that word a+k lands at
+// s_raw[(a & 3) + k]; 16-byte vector loads for the aligned body.
+__device__ __forceinline__ void load_words(uint32_t* s_raw, const uint32_t* g,
+                                           unsigned long long a, uint32_t nw) {
+  const uint32_t h = (uint32_t)(a & 3ull);
+  const uint32_t* gb = g + (a - h);
+  const uint32_t total = h + nw;
+  const uint32_t nvec = total >> 2;
+  const uint4* gv = reinterpret_cast<const uint4*>(gb);
+  uint4* sv = reinterpret_cast<uint4*>(s_raw);
+  for (uint32_t v = threadIdx.x; v < nvec; v += kThreads) sv[v] = __ldcs(gv + v);
+  for (uint32_t w = (nvec << 2) + threadIdx.x; w < total; w += kThreads) s_raw[w] = __ldcs(gb + w);
+}
+
+// Same for doubles: element a+k lands at s_raw[(a & 1) + k].
+__device__ __forceinline__ void load_doubles(double* s_raw, const double* g,
+                                             unsigned long long a, uint32_t n) {
+  const uint32_t h = (uint32_t)(a & 1ull);
+  const double* gb = g + (a - h);
+  const uint32_t total = h + n;
+  const uint32_t nvec = total >> 1;
+  const double2* gv = reinterpret_cast<const double2*>(gb);
+  double2* sv = reinterpret_cast<double2*>(s_raw);
+  for (uint32_t v = threadIdx.x; v < nvec; v += kThreads) sv[v] = __ldcs(gv + v);
+  for (uint32_t w = (nvec << 1) + threadIdx.x; w < total; w += kThreads) s_raw[w] = __ldcs(gb + w);
+}
+
+__device__ __forceinline__ void store_row(uint32_t* out_c, double* out_v, uint32_t rank,
+                                          unsigned long long dst, const uint32_t* srow,
+                                          double v) {
+  uint32_t* o = out_c + dst * rank;
+#pragma unroll 4
+  for (uint32_t m = 0; m < rank; ++m) __stcs(o + m, srow[m]);
+  __stcs(out_v + dst, v);
+}
+
+__host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+
+// Shared-memory layout of k_onesweep for T rows of `rank` coordinates.
+struct SweepLayout {
+  size_t c, v, dig, rnk, sorted, whist, cnt, start, gbase, tmp, total;
+  __host__ __device__ SweepLayout(uint32_t T, uint32_t rank) {
+    size_t o = 0;
+    c = o; o += align16((size_t(T) * rank + 4) * 4);
+    v = o; o += align16((size_t(T) + 2) * 8);
+    dig = o; o += align16(size_t(T) * 2);
+    rnk = o; o += align16(size_t(T) * 2);
+    sorted = o; o += align16(size_t(T) * 2);
+    whist = o; o += align16(size_t(kWarps) * kBins * 4);
+    cnt = o; o += align16(kBins * 4);
+    start = o; o += align16(kBins * 4);
+    gbase = o; o += align16(kBins * 8);
+    tmp = o; o += align16(64 * 8);
+    total = o;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// k_onesweep: one stable counting pass over one radix digit
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) k_onesweep(PassArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const SweepLayout L(a.T, a.rank);
+  uint32_t* s_craw = reinterpret_cast<uint32_t*>(smem + L.c);
+  double* s_vraw = reinterpret_cast<double*>(smem + L.v);
+  uint16_t* s_dig = reinterpret_cast<uint16_t*>(smem + L.dig);
+  uint16_t* s_rank = reinterpret_cast<uint16_t*>(smem + L.rnk);
+  uint16_t* s_sorted = reinterpret_cast<uint16_t*>(smem + L.sorted);
+  uint32_t* s_whist = reinterpret_cast<uint32_t*>(smem + L.whist);
+  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(smem + L.cnt);
+  uint32_t* s_start = reinterpret_cast<uint32_t*>(smem + L.start);
+  long long* s_gbase = reinterpret_cast<long long*>(smem + L.gbase);
+  unsigned long long* s_tmp = reinterpret_cast<unsigned long long*>(smem + L.tmp);
+  __shared__ uint32_t s_tile;
+
+  if (threadIdx.x == 0) s_tile = atomicAdd(a.tile_counter, 1u);
+  for (int k = threadIdx.x; k < kWarps * kBins; k += kThreads) s_whist[k] = 0;
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  if (tile >= a.num_tiles) return;
+
+  unsigned long long rb;
+  uint32_t n, li;
+  bool first;
+  if (a.tiles) {
+    const TileDesc d = a.tiles[tile];
+    rb = d.row_begin;
+    n = d.len;
+    li = d.li_first >> 1;
+    first = d.li_first & 1u;
+  } else {
+    rb = (unsigned long long)tile * a.T;
+    n = (uint32_t)min((unsigned long long)a.T, a.nnz - rb);
+    li = 0;
+    first = tile == 0;
+  }
+  const uint32_t R = a.rank;
+  const uint32_t ch = (uint32_t)((rb * R) & 3ull), vh = (uint32_t)(rb & 1ull);
+  load_words(s_craw, a.in_c, rb * R, n * R);
+  load_doubles(s_vraw, a.in_v, rb, n);
+  __syncthreads();
+  const uint32_t* s_c = s_craw + ch;
+  const double* s_v = s_vraw + vh;
+
+  for (uint32_t i = threadIdx.x; i < n; i += kThreads)
+    s_dig[i] = (uint16_t)digit_of(s_c + (size_t)i * R, a.dig);
+  __syncthreads();
+
+  const uint32_t ipw = a.T / kWarps;
+  warp_rank([&](uint32_t p) { return (uint32_t)s_dig[p]; }, n, ipw, s_rank, s_whist);
+  __syncthreads();
+  bin_totals(s_whist, s_cnt);
+  __syncthreads();
+
+  // Publish this tile's per-digit counts as early as possible.
+  unsigned long long* st = a.status + (size_t)tile * kBins;
+  for (int b = threadIdx.x; b < kBins; b += kThreads)
+    st_relaxed(st + b, enc(first ? kFlagPre : kFlagAgg, a.epoch, s_cnt[b]));
+
+  // Tile-local and run-level exclusive digit offsets.
+  const uint32_t cnt = s_cnt[threadIdx.x];
+  const uint32_t start = block_excl_scan(cnt, reinterpret_cast<uint32_t*>(s_tmp));
+  s_start[threadIdx.x] = start;
+  const uint32_t h = a.hist[(size_t)li * a.hist_stride + threadIdx.x];
+  const unsigned long long run_off = block_excl_scan64(h, s_tmp);
+  const unsigned long long base = a.run_start ? a.run_start[li] : 0ull;
+
+  // Decoupled look-back over the preceding tiles of the same run.
+  {
+    const int b = threadIdx.x;
+    unsigned long long excl = 0;
+    if (!first) {
+      long long p = (long long)tile - 1;
+      for (;;) {
+        const unsigned long long s = ld_relaxed(a.status + (size_t)p * kBins + b);
+        const unsigned long long flag = s & (3ull << 62);
+        if (flag == 0 || ((s >> 48) & 0x3FFFu) != (a.epoch & 0x3FFFu)) {
+          __nanosleep(32);
+          continue;
+        }
+        excl += s & kValMask;
+        if (flag == kFlagPre) break;
+        --p;
+      }
+      st_relaxed(st + b, enc(kFlagPre, a.epoch, excl + cnt));
+    }
+    s_gbase[b] = (long long)(base + run_off + excl) - (long long)start;
+  }
+  __syncthreads();
+
+  for (uint32_t i = threadIdx.x; i < n; i += kThreads) {
+    const uint32_t d = s_dig[i];
+    const uint32_t pos = s_start[d] + s_whist[(i / ipw) * kBins + d] + s_rank[i];
+    s_sorted[pos] = (uint16_t)i;
+  }
+  __syncthreads();
+
+  for (uint32_t j = threadIdx.x; j < n; j += kThreads) {
+    const uint32_t i = s_sorted[j];
+    const unsigned long long dst = (unsigned long long)(s_gbase[s_dig[i]] + j);
+    store_row(a.out_c, a.out_v, R, dst, s_c + (size_t)i * R, s_v[i]);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_hist: per-run digit histograms of np passes + range check
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) k_hist(HistArgs a) {
+  __shared__ uint32_t s_h[kHistPasses * kBins];
+  for (int k = threadIdx.x; k < kHistPasses * kBins; k += kThreads) s_h[k] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  int cur_li = -1;
+  auto flush = [&](int li) {
+    __syncthreads();
+    if (li >= 0) {
+      uint32_t* g = a.hist + (size_t)li * a.hist_stride + (size_t)a.pass0 * kBins;
+      for (uint32_t k = threadIdx.x; k < a.np * kBins; k += kThreads) {
+        const uint32_t v = s_h[k];
+        if (v) atomicAdd(g + k, v);
+        s_h[k] = 0;
+      }
+    }
+    __syncthreads();
+  };
+  auto count_rows = [&](unsigned long long rb, uint32_t n) {
+    // whole warps iterate together so __match_any_sync sees full masks
+    for (uint32_t base = 0; base < n; base += kThreads) {
+      const uint32_t i = base + threadIdx.x;
+      const bool valid = i < n;
+      const uint32_t* row = a.in_c + (size_t)(rb + (valid ? i : 0)) * a.rank;
+      if (valid && a.do_check) check_row(row, a.key, rb + i, a.err);
+      for (uint32_t q = 0; q < a.np; ++q) {
+        const uint32_t d = valid ? digit_of(row, a.dig[q]) : 0xFFFFFFFFu;
+        const unsigned peers = __match_any_sync(0xFFFFFFFFu, d);
+        if (valid && lane == __ffs(peers) - 1) atomicAdd(&s_h[q * kBins + d], __popc(peers));
+      }
+    }
+  };
+  if (a.tiles == nullptr) {
+    // one run [0, nnz): contiguous row chunks per CTA
+    const unsigned long long per = (a.nnz + gridDim.x - 1) / gridDim.x;
+    const unsigned long long b = per * blockIdx.x;
+    const unsigned long long e = min((unsigned long long)a.nnz, b + per);
+    for (unsigned long long r = b; r < e; r += 65536ull)
+      count_rows(r, (uint32_t)min(65536ull, e - r));
+    flush(0);
+    return;
+  }
+  const uint32_t t0 = blockIdx.x * a.tiles_per_cta;
+  const uint32_t t1 = min(a.num_tiles, t0 + a.tiles_per_cta);
+  for (uint32_t t = t0; t < t1; ++t) {
+    const TileDesc d = a.tiles[t];
+    const int li = (int)(d.li_first >> 1);
+    if (li != cur_li) {
+      flush(cur_li);
+      cur_li = li;
+    }
+    count_rows(d.row_begin, d.len);
+  }
+  flush(cur_li);
+}
+
+// ---------------------------------------------------------------------------
+// k_local: small runs, fully sorted inside one CTA
+// ---------------------------------------------------------------------------
+struct LocalLayout {
+  size_t c, v, key, perm0, perm1, rnk, whist, cnt, start, seg, tmp, total;
+  __host__ __device__ LocalLayout(uint32_t cap, uint32_t rank, uint32_t TL) {
+    size_t o = 0;
+    c = o; o += align16((size_t(cap) * rank + 4) * 4);
+    v = o; o += align16((size_t(cap) + 2) * 8);
+    key = o; o += align16(size_t(cap) * 8);
+    perm0 = o; o += align16(size_t(cap) * 2);
+    perm1 = o; o += align16(size_t(cap) * 2);
+    rnk = o; o += align16(size_t(cap) * 2);
+    whist = o; o += align16(size_t(kWarps) * kBins * 4);
+    cnt = o; o += align16(kBins * 4);
+    start = o; o += align16(kBins * 4);
+    seg = o; o += align16((size_t(TL) + 2) * 8);
+    tmp = o; o += align16(64 * 8);
+    total = o;
+  }
+};
+
+__device__ __forceinline__ uint32_t ceil_log2_dev(uint64_t x) {
+  return x <= 1 ? 0u : 64u - (uint32_t)__clzll((long long)(x - 1));
+}
+
+__global__ void __launch_bounds__(kThreads) k_local(LocalArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const LocalLayout L(a.cap, a.rank, a.TL);
+  uint32_t* s_craw = reinterpret_cast<uint32_t*>(smem + L.c);
+  double* s_vraw = reinterpret_cast<double*>(smem + L.v);
+  unsigned long long* s_key = reinterpret_cast<unsigned long long*>(smem + L.key);
+  uint16_t* s_p0 = reinterpret_cast<uint16_t*>(smem + L.perm0);
+  uint16_t* s_p1 = reinterpret_cast<uint16_t*>(smem + L.perm1);
+  uint16_t* s_rank = reinterpret_cast<uint16_t*>(smem + L.rnk);
+  uint32_t* s_whist = reinterpret_cast<uint32_t*>(smem + L.whist);
+  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(smem + L.cnt);
+  uint32_t* s_start = reinterpret_cast<uint32_t*>(smem + L.start);
+  unsigned long long* s_seg = reinterpret_cast<unsigned long long*>(smem + L.seg);
+  uint32_t* s_tmp = reinterpret_cast<uint32_t*>(smem + L.tmp);
+  __shared__ unsigned long long s_sa;
+  __shared__ uint32_t s_nsl;
+
+  unsigned long long r0, r1;
+  uint32_t nsl;
+  if (a.seg_start == nullptr) {
+    r0 = 0;
+    r1 = a.nnz;
+    nsl = 1;
+    if (threadIdx.x == 0) {
+      s_seg[0] = 0;
+      s_seg[1] = a.nnz;
+    }
+  } else {
+    const unsigned long long lo = (unsigned long long)blockIdx.x * a.TL;
+    const unsigned long long hi = min((unsigned long long)a.nnz, lo + (unsigned long long)a.TL);
+    const uint64_t S = a.nseg;  // seg_start has S+1 entries
+    if (threadIdx.x == 0) {
+      // first run starting at or after lo
+      uint64_t l = 0, h = S;
+      while (l < h) {
+        const uint64_t m = (l + h) >> 1;
+        if (a.seg_start[m] < lo) l = m + 1; else h = m;
+      }
+      s_sa = l;
+      s_nsl = 0xFFFFFFFFu;
+    }
+    __syncthreads();
+    const uint64_t sa = s_sa;
+    // runs sa .. sa+k starting in [lo, hi) and small; at most TL of them
+    for (uint32_t k = threadIdx.x; k <= a.TL; k += kThreads) {
+      const uint64_t s = sa + k;
+      bool stop = true;
+      if (s < S) {
+        const unsigned long long b = a.seg_start[s], e = a.seg_start[s + 1];
+        s_seg[k] = b;
+        stop = b >= hi || (e - b) > a.TL;
+        if (!stop) s_seg[k + 1] = e;
+      }
+      if (stop) atomicMin(&s_nsl, k);
+    }
+    __syncthreads();
+    nsl = min(s_nsl, a.TL + 1);
+    if (nsl == 0) return;
+    r0 = s_seg[0];
+    r1 = s_seg[nsl];
+  }
+  __syncthreads();
+  const uint32_t n = (uint32_t)(r1 - r0);
+  const uint32_t R = a.rank;
+  load_words(s_craw, a.in_c, r0 * R, n * R);
+  load_doubles(s_vraw, a.in_v, r0, n);
+  __syncthreads();
+  const uint32_t* s_c = s_craw + (uint32_t)((r0 * R) & 3ull);
+  const double* s_v = s_vraw + (uint32_t)(r0 & 1ull);
+
+  const uint32_t kb = a.key.total_bits;
+  for (uint32_t i = threadIdx.x; i < n; i += kThreads) {
+    const uint32_t* row = s_c + (size_t)i * R;
+    if (a.key.check) check_row(row, a.key, r0 + i, a.err);
+    unsigned long long k = full_key(row, a.key);
+    if (nsl > 1) {
+      // local run index: last run start <= row
+      uint32_t l = 0, h = nsl;  // s_seg[0..nsl]
+      const unsigned long long g = r0 + i;
+      while (h - l > 1) {
+        const uint32_t m = (l + h) >> 1;
+        if (s_seg[m] <= g) l = m; else h = m;
+      }
+      k |= (unsigned long long)l << kb;
+    }
+    s_key[i] = k;
+    s_p0[i] = (uint16_t)i;
+  }
+  const uint32_t nbits = kb + ceil_log2_dev(nsl);
+  const uint32_t passes = (nbits + kRadixLog - 1) / kRadixLog;
+  const uint32_t ipw = (n + kWarps - 1) / kWarps;
+  uint16_t* cur = s_p0;
+  uint16_t* nxt = s_p1;
+  for (uint32_t q = 0; q < passes; ++q) {
+    const uint32_t sh = q * kRadixLog;
+    for (int k = threadIdx.x; k < kWarps * kBins; k += kThreads) s_whist[k] = 0;
+    __syncthreads();
+    warp_rank([&](uint32_t p) { return (uint32_t)((s_key[cur[p]] >> sh) & (kBins - 1)); }, n,
+              ipw, s_rank, s_whist);
+    __syncthreads();
+    bin_totals(s_whist, s_cnt);
+    __syncthreads();
+    s_start[threadIdx.x] = block_excl_scan(s_cnt[threadIdx.x], s_tmp);
+    __syncthreads();
+    for (uint32_t p = threadIdx.x; p < n; p += kThreads) {
+      const uint32_t it = cur[p];
+      const uint32_t d = (uint32_t)((s_key[it] >> sh) & (kBins - 1));
+      nxt[s_start[d] + s_whist[(p / ipw) * kBins + d] + s_rank[p]] = (uint16_t)it;
+    }
+    __syncthreads();
+    uint16_t* t = cur;
+    cur = nxt;
+    nxt = t;
+  }
+  for (uint32_t j = threadIdx.x; j < n; j += kThreads) {
+    const uint32_t i = cur[j];
+    store_row(a.out_c, a.out_v, R, r0 + j, s_c + (size_t)i * R, s_v[i]);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// segment discovery
+// ---------------------------------------------------------------------------
+constexpr uint32_t kHeadRows = 4096;  // rows per k_heads CTA (128 words)
+
+struct ModeList {
+  uint32_t n;
+  uint8_t m[kMaxKeys];
+};
+
+// head bit of row i = 1 iff i == 0 or row i differs from row i-1 on `modes`.
+__global__ void __launch_bounds__(kThreads) k_heads(const uint32_t* c, uint32_t rank,
+                                                    uint64_t nnz, ModeList modes,
+                                                    uint32_t* words, uint32_t* block_cnt) {
+  const unsigned long long r0 = (unsigned long long)blockIdx.x * kHeadRows;
+  uint32_t cnt = 0;
+  for (uint32_t k = 0; k < kHeadRows / kThreads; ++k) {
+    const unsigned long long i = r0 + k * kThreads + threadIdx.x;
+    bool head = false;
+    if (i < nnz) {
+      if (i == 0) {
+        head = true;
+      } else {
+        const uint32_t* x = c + i * rank;
+        const uint32_t* y = x - rank;
+        for (uint32_t j = 0; j < modes.n; ++j)
+          if (x[modes.m[j]] != y[modes.m[j]]) { head = true; break; }
+      }
+    }
+    const unsigned bits = __ballot_sync(0xFFFFFFFFu, head);
+    if ((threadIdx.x & 31) == 0 && r0 + k * kThreads + threadIdx.x < nnz)
+      words[(r0 + k * kThreads + threadIdx.x) >> 5] = bits;
+    cnt += head;
+  }
+  __shared__ uint32_t s_tmp[64];
+  uint32_t tot;
+  block_excl_scan(cnt, s_tmp, &tot);
+  if (threadIdx.x == 0) block_cnt[blockIdx.x] = tot;
+}
+
+// Write seg_start[off + rank] = row for every head; the last CTA also writes
+// seg_start[S] = nnz.
+__global__ void __launch_bounds__(kThreads) k_compact(const uint32_t* words, uint64_t nnz,
+                                                      const unsigned long long* block_off,
+                                                      uint32_t nblocks,
+                                                      unsigned long long* seg_start,
+                                                      const unsigned long long* total) {
+  const unsigned long long w0 = (unsigned long long)blockIdx.x * (kHeadRows / 32);
+  const unsigned long long nwords = (nnz + 31) / 32;
+  __shared__ uint32_t s_tmp[64];
+  // kHeadRows/32 = 128 words per CTA; threads 0..127 own one word each
+  const unsigned long long wi = w0 + threadIdx.x;
+  uint32_t word = 0;
+  if (threadIdx.x < kHeadRows / 32 && wi < nwords) word = words[wi];
+  const uint32_t pre = block_excl_scan(__popc(word), s_tmp);
+  unsigned long long out = block_off[blockIdx.x] + pre;
+  while (word) {
+    const int b = __ffs(word) - 1;
+    word &= word - 1;
+    seg_start[out++] = wi * 32 + b;
+  }
+  if (blockIdx.x == nblocks - 1 && threadIdx.x == 0) seg_start[*total] = nnz;
+}
+
+// Per run: large flag and its tile count.
+__global__ void k_classify(const unsigned long long* seg_start, const unsigned long long* S_ptr,
+                           uint32_t TL, uint32_t T, uint32_t* is_large, uint32_t* ntiles) {
+  const unsigned long long S = *S_ptr;
+  for (unsigned long long s = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; s < S;
+       s += (unsigned long long)gridDim.x * blockDim.x) {
+    const unsigned long long len = seg_start[s + 1] - seg_start[s];
+    const bool large = len > TL;
+    is_large[s] = large;
+    ntiles[s] = large ? (uint32_t)((len + T - 1) / T) : 0u;
+  }
+}
+
+__global__ void k_gen_tiles(const unsigned long long* seg_start, const unsigned long long* S_ptr,
+                            uint32_t T, const uint32_t* is_large,
+                            const unsigned long long* large_off, const unsigned long long* tile_off,
+                            TileDesc* tiles, unsigned long long* run_start) {
+  const unsigned long long S = *S_ptr;
+  for (unsigned long long s = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; s < S;
+       s += (unsigned long long)gridDim.x * blockDim.x) {
+    if (!is_large[s]) continue;
+    const unsigned long long b = seg_start[s], e = seg_start[s + 1];
+    const uint32_t li = (uint32_t)large_off[s];
+    run_start[li] = b;
+    unsigned long long t = tile_off[s];
+    for (unsigned long long r = b; r < e; r += T, ++t) {
+      TileDesc d;
+      d.row_begin = r;
+      d.len = (uint32_t)min((unsigned long long)T, e - r);
+      d.li_first = (li << 1) | (r == b ? 1u : 0u);
+      tiles[t] = d;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// generic exclusive scan (u32 in -> u64 out), 3 phases
+// ---------------------------------------------------------------------------
+constexpr uint32_t kScanItems = 8;
+constexpr uint32_t kScanTile = kThreads * kScanItems;
+
+__global__ void k_scan_reduce(const uint32_t* in, unsigned long long n, unsigned long long* part) {
+  const unsigned long long b = (unsigned long long)blockIdx.x * kScanTile;
+  unsigned long long s = 0;
+  for (uint32_t k = 0; k < kScanItems; ++k) {
+    const unsigned long long i = b + k * kThreads + threadIdx.x;
+    if (i < n) s += in[i];
+  }
+  __shared__ unsigned long long s_tmp[64];
+  const unsigned long long ex = block_excl_scan64(s, s_tmp);
+  if (threadIdx.x == kThreads - 1) part[blockIdx.x] = ex + s;
+}
+
+// single CTA: exclusive scan of part[0..np) in place, total to *total
+__global__ void k_scan_parts(unsigned long long* part, uint32_t np, unsigned long long* total) {
+  __shared__ unsigned long long s_tmp[64];
+  unsigned long long carry = 0;
+  for (uint32_t b = 0; b < np; b += kThreads) {
+    const uint32_t i = b + threadIdx.x;
+    const unsigned long long v = i < np ? part[i] : 0;
+    const unsigned long long ex = block_excl_scan64(v, s_tmp);
+    if (i < np) part[i] = carry + ex;
+    __shared__ unsigned long long s_last;
+    if (threadIdx.x == kThreads - 1) s_last = ex + v;
+    __syncthreads();
+    carry += s_last;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *total = carry;
+}
+
+__global__ void k_scan_down(const uint32_t* in, unsigned long long n, const unsigned long long* part,
+                            unsigned long long* out) {
+  const unsigned long long b = (unsigned long long)blockIdx.x * kScanTile;
+  // each thread owns kScanItems consecutive elements
+  unsigned long long v[kScanItems];
+  unsigned long long s = 0;
+  for (uint32_t k = 0; k < kScanItems; ++k) {
+    const unsigned long long i = b + threadIdx.x * kScanItems + k;
+    v[k] = i < n ? in[i] : 0;
+    s += v[k];
+  }
+  __shared__ unsigned long long s_tmp[64];
+  unsigned long long run = part[blockIdx.x] + block_excl_scan64(s, s_tmp);
+  for (uint32_t k = 0; k < kScanItems; ++k) {
+    const unsigned long long i = b + threadIdx.x * kScanItems + k;
+    if (i < n) out[i] = run;
+    run += v[k];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// small utility kernels
+// ---------------------------------------------------------------------------
+__global__ void k_copy_check(const uint32_t* in_c, const double* in_v, uint32_t* out_c,
+                             double* out_v, uint32_t rank, uint64_t nnz, KeySpec key,
+                             ErrBlock* err) {
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < nnz;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const uint32_t* row = in_c + i * rank;
+    if (key.check) check_row(row, key, i, err);
+    for (uint32_t m = 0; m < rank; ++m) out_c[i * rank + m] = row[m];
+    out_v[i] = in_v[i];
+  }
+}
+
+// flags bit1 unless rows are non-decreasing under `order` (coo.cpp:32-49)
+__global__ void k_is_sorted(const uint32_t* c, uint32_t rank, uint64_t nnz, ModeList order,
+                            ErrBlock* err) {
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x + 1;
+       i < nnz; i += (unsigned long long)gridDim.x * blockDim.x) {
+    const uint32_t* x = c + i * rank;
+    const uint32_t* y = x - rank;
+    for (uint32_t j = 0; j < order.n; ++j) {
+      const uint32_t a = y[order.m[j]], b = x[order.m[j]];
+      if (a != b) {
+        if (a > b) atomicOr(&err->flags, 2u);
+        break;
+      }
+    }
+  }
+}
+
+__global__ void k_mode_max(const uint32_t* c, uint32_t rank, uint64_t nnz, ModeList modes,
+                           uint32_t* mx) {
+  __shared__ uint32_t s_mx[kMaxKeys];
+  for (uint32_t j = threadIdx.x; j < modes.n; j += blockDim.x) s_mx[j] = 0;
+  __syncthreads();
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < nnz;
+       i += (unsigned long long)gridDim.x * blockDim.x)
+    for (uint32_t j = 0; j < modes.n; ++j) atomicMax(&s_mx[j], c[i * rank + modes.m[j]]);
+  __syncthreads();
+  for (uint32_t j = threadIdx.x; j < modes.n; j += blockDim.x) atomicMax(&mx[j], s_mx[j]);
+}
+
+__global__ void k_mode_hist(const uint32_t* c, uint32_t rank, uint64_t nnz, uint32_t mode,
+                            uint32_t dim, unsigned long long* hist) {
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < nnz;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const uint32_t k = c[i * rank + mode];
+    if (k < dim) atomicAdd(hist + k, 1ull);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+struct Workspace {
+  int device = 0;
+  int num_sms = 148;
+  size_t smem_optin = 227 * 1024;
+  std::map<std::string, DevBuf> bufs;
+  uint32_t epoch = 0;
+  uint64_t launches = 0;
+  ErrBlock* h_err = nullptr;  // pinned
+  uint64_t* h_small = nullptr;  // pinned scratch for small D2H reads
+  void* status_clean = nullptr;  // look-back buffer known to hold no stale flags
+
+  template <class T>
+  T* get(const std::string& name, size_t count) {
+    const size_t bytes = std::max<size_t>(count * sizeof(T), 256);
+    DevBuf& b = bufs[name];
+    if (b.bytes < bytes) {
+      if (b.p) QD_CUDA(cudaFree(b.p));
+      b.p = nullptr;
+      b.bytes = 0;
+      const size_t want = bytes + bytes / 8;  // headroom against regrowth
+      QD_CUDA(cudaMalloc(&b.p, want));
+      b.bytes = want;
+    }
+    return static_cast<T*>(b.p);
+  }
+};
+
+Workspace* workspace_create(int device) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+    throw Error(QD_NO_DEVICE, "no CUDA device visible (this library has no CPU path)");
+  if (device < 0 || device >= n) invalid("device index out of range");
+  QD_CUDA(cudaSetDevice(device));
+  auto* ws = new Workspace;
+  ws->device = device;
+  QD_CUDA(cudaDeviceGetAttribute(&ws->num_sms, cudaDevAttrMultiProcessorCount, device));
+  int optin = 0;
+  QD_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+  ws->smem_optin = optin;
+  QD_CUDA(cudaMallocHost(&ws->h_err, sizeof(ErrBlock)));
+  QD_CUDA(cudaMallocHost(&ws->h_small, 64 * sizeof(uint64_t)));
+  QD_CUDA(cudaFuncSetAttribute(k_onesweep, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+  QD_CUDA(cudaFuncSetAttribute(k_local, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+  return ws;
+}
+
+void workspace_destroy(Workspace* ws) {
+  if (!ws) return;
+  cudaSetDevice(ws->device);
+  for (auto& kv : ws->bufs)
+    if (kv.second.p) cudaFree(kv.second.p);
+  if (ws->h_err) cudaFreeHost(ws->h_err);
+  if (ws->h_small) cudaFreeHost(ws->h_small);
+  delete ws;
+}
+
+uint64_t workspace_bytes(const Workspace* ws) {
+  uint64_t b = 0;
+  for (auto& kv : ws->bufs) b += kv.second.bytes;
+  return b;
+}
+uint64_t workspace_launches(const Workspace* ws) { return ws->launches; }
+
+namespace {
+
+uint32_t ceil_log2(uint64_t x) {
+  uint32_t b = 0;
+  while ((uint64_t{1} << b) < x && b < 64) ++b;
+  return b;
+}
+
+struct Ctx {
+  Workspace& ws;
+  cudaStream_t st;
+  ErrBlock* err;       // device
+  uint32_t* counters;  // device, tile counters
+  uint32_t next_counter = 0;
+  void launched() {
+    ++ws.launches;
+    QD_CUDA(cudaGetLastError());
+  }
+};
+
+constexpr uint32_t kCounters = 4096;
+
+// Rows per onesweep tile / local chunk for a given rank, from the smem budget.
+uint32_t sweep_tile_rows(const Workspace& ws, uint32_t rank) {
+  const size_t budget = std::min<size_t>(ws.smem_optin, 112 * 1024);  // 2 CTAs/SM
+  uint32_t T = 4096;
+  while (T > 256 && SweepLayout(T, rank).total > budget) T -= 256;
+  return T;
+}
+uint32_t local_span(const Workspace& ws, uint32_t rank) {
+  const size_t budget = std::min<size_t>(ws.smem_optin, 112 * 1024);
+  uint32_t TL = 2048;
+  while (TL > 32 && LocalLayout(2 * TL, rank, TL).total > budget) TL -= 32;
+  return TL;
+}
+
+void scan_exclusive(Ctx& c, const uint32_t* in, uint64_t n, unsigned long long* out,
+                    unsigned long long* d_total) {
+  const uint32_t nb = (uint32_t)((n + kScanTile - 1) / kScanTile);
+  auto* part = c.ws.get<unsigned long long>("scan_part", nb + 1);
+  if (n == 0) {
+    QD_CUDA(cudaMemsetAsync(d_total, 0, sizeof(unsigned long long), c.st));
+    return;
+  }
+  k_scan_reduce<<<nb, kThreads, 0, c.st>>>(in, n, part);
+  c.launched();
+  k_scan_parts<<<1, kThreads, 0, c.st>>>(part, nb, d_total);
+  c.launched();
+  k_scan_down<<<nb, kThreads, 0, c.st>>>(in, n, part, out);
+  c.launched();
+}
+
+// Segment discovery on `coords` with respect to `modes`: fills seg_start[0..S]
+// (device, seg_start[S] = nnz) and returns S (host sync).
+uint64_t find_runs(Ctx& c, const uint32_t* coords, uint32_t rank, uint64_t nnz,
+                   const std::vector<uint32_t>& modes, unsigned long long** seg_out) {
+  ModeList ml{};
+  ml.n = (uint32_t)modes.size();
+  for (uint32_t i = 0; i < ml.n; ++i) ml.m[i] = (uint8_t)modes[i];
+  const uint32_t nb = (uint32_t)((nnz + kHeadRows - 1) / kHeadRows);
+  auto* words = c.ws.get<uint32_t>("head_words", (nnz + 31) / 32 + 1);
+  auto* bcnt = c.ws.get<uint32_t>("head_bcnt", nb + 1);
+  auto* boff = c.ws.get<unsigned long long>("head_boff", nb + 1);
+  auto* tot = c.ws.get<unsigned long long>("head_total", 1);
+  k_heads<<<nb, kThreads, 0, c.st>>>(coords, rank, nnz, ml, words, bcnt);
+  c.launched();
+  scan_exclusive(c, bcnt, nb, boff, tot);
+  QD_CUDA(cudaMemcpyAsync(c.ws.h_small, tot, 8, cudaMemcpyDeviceToHost, c.st));
+  QD_CUDA(cudaStreamSynchronize(c.st));
+  const uint64_t S = c.ws.h_small[0];
+  auto* seg = c.ws.get<unsigned long long>("seg_start", S + 1);
+  k_compact<<<nb, kThreads, 0, c.st>>>(words, nnz, boff, nb, seg, tot);
+  c.launched();
+  *seg_out = seg;
+  return S;
+}
+
+KeySpec make_keyspec(const std::vector<uint32_t>& keys, const std::vector<uint32_t>& widths,
+                     const uint32_t* dims, bool check) {
+  KeySpec k{};
+  k.n = (uint32_t)keys.size();
+  k.check = check;
+  uint32_t off = 0;
+  for (int i = (int)k.n - 1; i >= 0; --i) {
+    k.mode[i] = (uint8_t)keys[i];
+    k.width[i] = (uint8_t)widths[i];
+    k.off[i] = (uint16_t)off;
+    k.dim[i] = dims[keys[i]];
+    off += widths[i];
+  }
+  k.total_bits = off;
+  return k;
+}
+
+DigitSpec make_digit(const KeySpec& k, uint32_t lo, uint32_t hi) {
+  DigitSpec d{};
+  for (uint32_t i = 0; i < k.n; ++i) {
+    const uint32_t fb = k.off[i], fe = k.off[i] + k.width[i];
+    const uint32_t b = std::max(fb, lo), e = std::min(fe, hi);
+    if (b >= e) continue;
+    if (d.n == kMaxTerms) throw Error(QD_INVALID_ARGUMENT, "digit spans too many modes");
+    d.mode[d.n] = k.mode[i];
+    d.rsh[d.n] = (uint8_t)(b - fb);
+    d.bits[d.n] = (uint8_t)(e - b);
+    d.lsh[d.n] = (uint8_t)(b - lo);
+    ++d.n;
+  }
+  return d;
+}
+
+// Look-back status words; freshly (re)allocated memory is cleared once, after
+// that the per-pass epoch in every word makes stale entries harmless.
+unsigned long long* status_buffer(Ctx& c, uint64_t num_tiles) {
+  auto* status = c.ws.get<unsigned long long>("status", num_tiles * kBins);
+  if (c.ws.status_clean != status) {
+    QD_CUDA(cudaMemsetAsync(status, 0, c.ws.bufs["status"].bytes, c.st));
+    c.ws.status_clean = status;
+  }
+  return status;
+}
+
+void launch_pass(Ctx& c, PassArgs& a) {
+  if (a.num_tiles == 0) return;
+  Workspace& ws = c.ws;
+  if (++ws.epoch >= 0x3FFFu) {
+    ws.epoch = 1;
+    QD_CUDA(cudaMemsetAsync(a.status, 0, ws.bufs["status"].bytes, c.st));
+  }
+  a.epoch = ws.epoch;
+  if (c.next_counter >= kCounters) {
+    QD_CUDA(cudaMemsetAsync(c.counters, 0, kCounters * 4, c.st));
+    c.next_counter = 0;
+  }
+  a.tile_counter = c.counters + c.next_counter++;
+  const size_t smem = SweepLayout(a.T, a.rank).total;
+  k_onesweep<<<a.num_tiles, kThreads, smem, c.st>>>(a);
+  c.launched();
+}
+
+// One segmented stable sort (a plan group), src -> dst, with tmp scratch.
+void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const double* src_v,
+                    uint32_t* dst_c, double* dst_v, uint32_t* tmp_c, double* tmp_v,
+                    const Group& g) {
+  Workspace& ws = c.ws;
+  const uint64_t N = t.nnz;
+  const uint32_t R = t.rank;
+  if (N == 0) return;
+
+  // key field widths
+  std::vector<uint32_t> widths(g.keys.size());
+  if (g.check_range) {
+    for (size_t i = 0; i < g.keys.size(); ++i) widths[i] = ceil_log2(t.dims[g.keys[i]]);
+  } else {
+    ModeList ml{};
+    ml.n = (uint32_t)g.keys.size();
+    for (uint32_t i = 0; i < ml.n; ++i) ml.m[i] = (uint8_t)g.keys[i];
+    auto* mx = ws.get<uint32_t>("mode_max", kMaxKeys);
+    QD_CUDA(cudaMemsetAsync(mx, 0, kMaxKeys * 4, c.st));
+    const uint32_t grid = (uint32_t)std::min<uint64_t>((N + kThreads - 1) / kThreads, ws.num_sms * 8);
+    k_mode_max<<<grid, kThreads, 0, c.st>>>(src_c, R, N, ml, mx);
+    c.launched();
+    uint32_t* h = reinterpret_cast<uint32_t*>(ws.h_small);
+    QD_CUDA(cudaMemcpyAsync(h, mx, kMaxKeys * 4, cudaMemcpyDeviceToHost, c.st));
+    QD_CUDA(cudaStreamSynchronize(c.st));
+    for (size_t i = 0; i < g.keys.size(); ++i) widths[i] = ceil_log2((uint64_t)h[i] + 1);
+  }
+  const KeySpec key = make_keyspec(g.keys, widths, t.dims, g.check_range);
+  const uint32_t bits = key.total_bits;
+
+  if (bits == 0 || N == 1) {
+    // nothing to reorder; still the histogram pass's range check
+    const uint32_t grid = (uint32_t)std::min<uint64_t>((N + kThreads - 1) / kThreads, ws.num_sms * 8);
+    k_copy_check<<<grid, kThreads, 0, c.st>>>(src_c, src_v, dst_c, dst_v, R, N, key, c.err);
+    c.launched();
+    return;
+  }
+
+  const uint32_t D = (bits + kRadixLog - 1) / kRadixLog;
+  const uint32_t per = (bits + D - 1) / D;
+  std::vector<DigitSpec> digs(D);
+  for (uint32_t q = 0; q < D; ++q) digs[q] = make_digit(key, q * per, std::min(bits, (q + 1) * per));
+
+  const uint32_t T = sweep_tile_rows(ws, R);
+  uint32_t TL = local_span(ws, R);
+  if (bits + ceil_log2(TL) + 1 > 64) TL = 0;  // local key would not fit 64 bits
+
+  const TileDesc* tiles = nullptr;
+  const unsigned long long* run_start = nullptr;
+  uint64_t num_tiles = 0, num_large = 0;
+  unsigned long long* seg = nullptr;
+  uint64_t S = 0;
+
+  if (g.prefix.empty()) {
+    if (TL && N <= TL) {
+      LocalArgs la{src_c, src_v, dst_c, dst_v, R, N, TL, (uint32_t)N, nullptr, 1, key, c.err};
+      const size_t smem = LocalLayout((uint32_t)N, R, TL).total;
+      k_local<<<1, kThreads, smem, c.st>>>(la);
+      c.launched();
+      return;
+    }
+    num_tiles = (N + T - 1) / T;
+    num_large = 1;
+  } else {
+    S = find_runs(c, src_c, R, N, g.prefix, &seg);
+    auto* is_large = ws.get<uint32_t>("run_large", S + 1);
+    auto* ntl = ws.get<uint32_t>("run_ntiles", S + 1);
+    auto* loff = ws.get<unsigned long long>("run_loff", S + 1);
+    auto* toff = ws.get<unsigned long long>("run_toff", S + 1);
+    auto* totals = ws.get<unsigned long long>("run_totals", 2);
+    auto* S_dev = ws.get<unsigned long long>("run_S", 1);
+    ws.h_small[0] = S;
+    QD_CUDA(cudaMemcpyAsync(S_dev, ws.h_small, 8, cudaMemcpyHostToDevice, c.st));
+    const uint32_t grid = (uint32_t)std::min<uint64_t>((S + kThreads - 1) / kThreads, ws.num_sms * 8);
+    k_classify<<<grid, kThreads, 0, c.st>>>(seg, S_dev, TL, T, is_large, ntl);
+    c.launched();
+    scan_exclusive(c, is_large, S, loff, totals);
+    scan_exclusive(c, ntl, S, toff, totals + 1);
+    QD_CUDA(cudaMemcpyAsync(ws.h_small + 1, totals, 16, cudaMemcpyDeviceToHost, c.st));
+    QD_CUDA(cudaStreamSynchronize(c.st));
+    num_large = ws.h_small[1];
+    num_tiles = ws.h_small[2];
+    if (num_tiles) {
+      auto* td = ws.get<TileDesc>("tiles", num_tiles);
+      auto* rs = ws.get<unsigned long long>("run_start", num_large);
+      k_gen_tiles<<<grid, kThreads, 0, c.st>>>(seg, S_dev, T, is_large, loff, toff, td, rs);
+      c.launched();
+      tiles = td;
+      run_start = rs;
+    }
+    if (S > num_large) {
+      // small runs: chunks of runs starting in [c*TL, (c+1)*TL)
+      LocalArgs la{src_c, src_v, dst_c, dst_v, R, N, TL, 2 * TL, seg, S, key, c.err};
+      const size_t smem = LocalLayout(2 * TL, R, TL).total;
+      const uint64_t chunks = (N + TL - 1) / TL;
+      k_local<<<(uint32_t)chunks, kThreads, smem, c.st>>>(la);
+      c.launched();
+    }
+  }
+  if (num_tiles == 0) return;
+
+  // per-run digit histograms for all passes (+ range check of large-run rows)
+  const uint32_t stride = D * kBins;
+  auto* hist = ws.get<uint32_t>("hist", num_large * stride);
+  QD_CUDA(cudaMemsetAsync(hist, 0, num_large * stride * 4, c.st));
+  for (uint32_t p0 = 0; p0 < D; p0 += kHistPasses) {
+    HistArgs h{};
+    h.in_c = src_c;
+    h.rank = R;
+    h.nnz = N;
+    h.T = T;
+    h.tiles = tiles;
+    h.num_tiles = (uint32_t)num_tiles;
+    h.np = std::min<uint32_t>(kHistPasses, D - p0);
+    h.pass0 = p0;
+    h.hist = hist;
+    h.hist_stride = stride;
+    for (uint32_t q = 0; q < h.np; ++q) h.dig[q] = digs[p0 + q];
+    h.key = key;
+    h.do_check = p0 == 0 && key.check;
+    h.err = c.err;
+    uint32_t grid = ws.num_sms * 4;
+    if (tiles) {
+      h.tiles_per_cta = (uint32_t)std::max<uint64_t>(1, (num_tiles + grid - 1) / grid);
+      grid = (uint32_t)((num_tiles + h.tiles_per_cta - 1) / h.tiles_per_cta);
+    } else {
+      grid = (uint32_t)std::min<uint64_t>(grid, (N + 4095) / 4096);
+    }
+    k_hist<<<grid, kThreads, 0, c.st>>>(h);
+    c.launched();
+  }
+
+  auto* status = status_buffer(c, num_tiles);
+
+  const uint32_t* in_c = src_c;
+  const double* in_v = src_v;
+  for (uint32_t q = 0; q < D; ++q) {
+    const bool to_dst = ((D - 1 - q) % 2) == 0;
+    uint32_t* oc = to_dst ? dst_c : tmp_c;
+    double* ov = to_dst ? dst_v : tmp_v;
+    PassArgs a{};
+    a.in_c = in_c;
+    a.in_v = in_v;
+    a.out_c = oc;
+    a.out_v = ov;
+    a.rank = R;
+    a.nnz = N;
+    a.T = T;
+    a.tiles = tiles;
+    a.num_tiles = (uint32_t)num_tiles;
+    a.run_start = run_start;
+    a.hist = hist + (size_t)q * kBins;
+    a.hist_stride = stride;
+    a.status = status;
+    a.dig = digs[q];
+    launch_pass(c, a);
+    in_c = oc;
+    in_v = ov;
+  }
+}
+
+}  // namespace
+
+static void check_errors(Ctx& c) {
+  QD_CUDA(cudaMemcpyAsync(c.ws.h_err, c.err, sizeof(ErrBlock), cudaMemcpyDeviceToHost, c.st));
+  QD_CUDA(cudaStreamSynchronize(c.st));
+  const ErrBlock e = *c.ws.h_err;
+  if (e.flags & 2u) invalid("input tensor is not sorted under the simple ordering");
+  if (e.flags & 1u) {
+    Error err(QD_OUT_OF_RANGE, "coordinate in row " + std::to_string(e.rowmode >> 6) +
+                                   " exceeds the dimension of mode " +
+                                   std::to_string(e.rowmode & 63));
+    err.row = e.rowmode >> 6;
+    err.mode = (uint32_t)(e.rowmode & 63);
+    throw err;
+  }
+}
+
+static Ctx make_ctx(Workspace& ws, void* stream) {
+  QD_CUDA(cudaSetDevice(ws.device));
+  Ctx c{ws, static_cast<cudaStream_t>(stream), nullptr, nullptr};
+  c.err = ws.get<ErrBlock>("err", 1);
+  c.counters = ws.get<uint32_t>("counters", kCounters);
+  ErrBlock init{0u, 0u, ~0ull};
+  *ws.h_err = init;
+  QD_CUDA(cudaMemcpyAsync(c.err, ws.h_err, sizeof(ErrBlock), cudaMemcpyHostToDevice, c.st));
+  QD_CUDA(cudaMemsetAsync(c.counters, 0, kCounters * 4, c.st));
+  return c;
+}
+
+void run_groups(Workspace& ws, const TensorView& t, const uint32_t* d_c_in, const double* d_v_in,
+                uint32_t* d_c_out, double* d_v_out, const std::vector<Group>& groups,
+                bool verify_input, uint64_t* d_boundaries, uint64_t* n_boundaries,
+                uint32_t boundary_mode, void* stream) {
+  Ctx c = make_ctx(ws, stream);
+  const uint64_t N = t.nnz;
+  const uint32_t R = t.rank;
+  if (verify_input && N > 1) {
+    ModeList ml{};
+    ml.n = R;
+    for (uint32_t i = 0; i < R; ++i) ml.m[i] = (uint8_t)i;
+    const uint32_t grid = (uint32_t)std::min<uint64_t>((N + kThreads - 1) / kThreads, ws.num_sms * 8);
+    k_is_sorted<<<grid, kThreads, 0, c.st>>>(d_c_in, R, N, ml, c.err);
+    c.launched();
+  }
+  const size_t G = groups.size();
+  if (G == 0 || N == 0) {
+    if (N && d_c_out != d_c_in) {
+      QD_CUDA(cudaMemcpyAsync(d_c_out, d_c_in, N * R * 4, cudaMemcpyDeviceToDevice, c.st));
+      QD_CUDA(cudaMemcpyAsync(d_v_out, d_v_in, N * 8, cudaMemcpyDeviceToDevice, c.st));
+    }
+  } else {
+    uint32_t* Ac = ws.get<uint32_t>("rowsA_c", N * R);
+    double* Av = ws.get<double>("rowsA_v", N);
+    uint32_t* Bc = G >= 2 ? ws.get<uint32_t>("rowsB_c", N * R) : nullptr;
+    double* Bv = G >= 2 ? ws.get<double>("rowsB_v", N) : nullptr;
+    const uint32_t* sc = d_c_in;
+    const double* sv = d_v_in;
+    for (size_t gi = 0; gi < G; ++gi) {
+      const bool last = gi + 1 == G;
+      uint32_t *dc, *tc;
+      double *dv, *tv;
+      // chain: in -> A -> B -> A ... -> out
+      uint32_t* Xc = (gi % 2 == 0) ? Ac : Bc;
+      double* Xv = (gi % 2 == 0) ? Av : Bv;
+      if (last) {
+        dc = d_c_out;
+        dv = d_v_out;
+        if (sc == Ac) { tc = Bc; tv = Bv; } else { tc = Ac; tv = Av; }
+      } else {
+        dc = Xc;
+        dv = Xv;
+        tc = d_c_out;  // not yet written by anyone
+        tv = d_v_out;
+      }
+      segmented_sort(c, t, sc, sv, dc, dv, tc, tv, groups[gi]);
+      sc = dc;
+      sv = dv;
+    }
+  }
+  if (d_boundaries && N > 0) {
+    unsigned long long* seg = nullptr;
+    const uint64_t S = find_runs(c, d_c_out, R, N, {boundary_mode}, &seg);
+    QD_CUDA(cudaMemcpyAsync(d_boundaries, seg, (S + 1) * 8, cudaMemcpyDeviceToDevice, c.st));
+    if (n_boundaries) *n_boundaries = S + 1;
+  } else if (n_boundaries) {
+    *n_boundaries = 0;
+  }
+  check_errors(c);
+}
+
+void run_groups_host(Workspace& ws, const TensorView& t, uint32_t* coords, double* values,
+                     const std::vector<Group>& groups, bool verify_input, uint64_t* h_boundaries,
+                     uint64_t* n_boundaries, uint32_t boundary_mode) {
+  QD_CUDA(cudaSetDevice(ws.device));
+  const uint64_t N = t.nnz;
+  const uint32_t R = t.rank;
+  uint32_t* ic = ws.get<uint32_t>("host_in_c", N * R);
+  double* iv = ws.get<double>("host_in_v", N);
+  uint32_t* oc = ws.get<uint32_t>("host_out_c", N * R);
+  double* ov = ws.get<double>("host_out_v", N);
+  uint64_t* db = h_boundaries ? ws.get<uint64_t>("host_bounds", N + 1) : nullptr;
+  cudaStream_t st = nullptr;
+  if (N) {
+    QD_CUDA(cudaMemcpyAsync(ic, coords, N * R * 4, cudaMemcpyHostToDevice, st));
+    QD_CUDA(cudaMemcpyAsync(iv, values, N * 8, cudaMemcpyHostToDevice, st));
+  }
+  uint64_t nb = 0;
+  run_groups(ws, t, ic, iv, oc, ov, groups, verify_input, db, &nb, boundary_mode, st);
+  if (N) {
+    QD_CUDA(cudaMemcpyAsync(coords, oc, N * R * 4, cudaMemcpyDeviceToHost, st));
+    QD_CUDA(cudaMemcpyAsync(values, ov, N * 8, cudaMemcpyDeviceToHost, st));
+    if (db && nb) QD_CUDA(cudaMemcpyAsync(h_boundaries, db, nb * 8, cudaMemcpyDeviceToHost, st));
+    QD_CUDA(cudaStreamSynchronize(st));
+  }
+  if (n_boundaries) *n_boundaries = nb;
+}
+
+bool is_sorted_device(Workspace& ws, uint32_t rank, uint64_t nnz, const uint32_t* d_coords,
+                      const uint32_t* order, void* stream) {
+  Ctx c = make_ctx(ws, stream);
+  ModeList ml{};
+  ml.n = rank;
+  for (uint32_t i = 0; i < rank; ++i) ml.m[i] = (uint8_t)order[i];
+  if (nnz > 1) {
+    const uint32_t grid = (uint32_t)std::min<uint64_t>((nnz + kThreads - 1) / kThreads, ws.num_sms * 8);
+    k_is_sorted<<<grid, kThreads, 0, c.st>>>(d_coords, rank, nnz, ml, c.err);
+    c.launched();
+  }
+  QD_CUDA(cudaMemcpyAsync(ws.h_err, c.err, sizeof(ErrBlock), cudaMemcpyDeviceToHost, c.st));
+  QD_CUDA(cudaStreamSynchronize(c.st));
+  return (ws.h_err->flags & 2u) == 0;
+}
+
+uint64_t bucket_starts_device(Workspace& ws, uint32_t rank, uint64_t nnz, const uint32_t* d_coords,
+                              const uint32_t* modes, uint32_t n_modes, uint64_t* d_starts,
+                              void* stream) {
+  Ctx c = make_ctx(ws, stream);
+  if (nnz == 0) return 0;
+  unsigned long long* seg = nullptr;
+  const uint64_t S = find_runs(c, d_coords, rank, nnz,
+                               std::vector<uint32_t>(modes, modes + n_modes), &seg);
+  QD_CUDA(cudaMemcpyAsync(d_starts, seg, (S + 1) * 8, cudaMemcpyDeviceToDevice, c.st));
+  QD_CUDA(cudaStreamSynchronize(c.st));
+  return S + 1;
+}
+
+void mode_histogram_device(Workspace& ws, uint32_t rank, uint64_t nnz, const uint32_t* d_coords,
+                           uint32_t mode, uint32_t dim, uint64_t* d_hist, void* stream) {
+  Ctx c = make_ctx(ws, stream);
+  if (nnz) {
+    const uint32_t grid = (uint32_t)std::min<uint64_t>((nnz + kThreads - 1) / kThreads, ws.num_sms * 8);
+    k_mode_hist<<<grid, kThreads, 0, c.st>>>(d_coords, rank, nnz, mode, dim,
+                                              reinterpret_cast<unsigned long long*>(d_hist));
+    c.launched();
+  }
+  QD_CUDA(cudaStreamSynchronize(c.st));
+}
+
+void partition_rows_device(Workspace& ws, uint32_t rank, uint64_t nnz, const uint32_t* d_c_in,
+                           const double* d_v_in, uint32_t mode, uint32_t dim,
+                           const uint32_t* d_lookup, uint32_t n_parts, uint32_t* d_c_out,
+                           double* d_v_out, uint64_t* part_counts, void* stream) {
+  if (n_parts == 0 || n_parts > (uint32_t)kBins) invalid("n_parts must be in 1..256");
+  if (mode >= rank) invalid("partition mode out of range");
+  Ctx c = make_ctx(ws, stream);
+  for (uint32_t p = 0; p < n_parts; ++p) part_counts[p] = 0;
+  if (nnz == 0) return;
+  const uint32_t T = sweep_tile_rows(ws, rank);
+  const uint64_t num_tiles = (nnz + T - 1) / T;
+  DigitSpec dig{};
+  dig.lookup = d_lookup;
+  dig.lookup_mode = mode;
+  dig.lookup_dim = dim;
+  auto* hist = ws.get<uint32_t>("hist", kBins);
+  QD_CUDA(cudaMemsetAsync(hist, 0, kBins * 4, c.st));
+  HistArgs h{};
+  h.in_c = d_c_in;
+  h.rank = rank;
+  h.nnz = nnz;
+  h.T = T;
+  h.np = 1;
+  h.hist = hist;
+  h.hist_stride = kBins;
+  h.dig[0] = dig;
+  h.err = c.err;
+  const uint32_t grid = (uint32_t)std::min<uint64_t>(ws.num_sms * 4, (nnz + 4095) / 4096);
+  k_hist<<<grid, kThreads, 0, c.st>>>(h);
+  c.launched();
+  auto* status = status_buffer(c, num_tiles);
+  PassArgs a{};
+  a.in_c = d_c_in;
+  a.in_v = d_v_in;
+  a.out_c = d_c_out;
+  a.out_v = d_v_out;
+  a.rank = rank;
+  a.nnz = nnz;
+  a.T = T;
+  a.num_tiles = (uint32_t)num_tiles;
+  a.hist = hist;
+  a.hist_stride = kBins;
+  a.status = status;
+  a.dig = dig;
+  launch_pass(c, a);
+  uint32_t* h_counts = reinterpret_cast<uint32_t*>(ws.h_small);
+  QD_CUDA(cudaMemcpyAsync(h_counts, hist, n_parts * 4, cudaMemcpyDeviceToHost, c.st));
+  QD_CUDA(cudaStreamSynchronize(c.st));
+  for (uint32_t p = 0; p < n_parts; ++p) part_counts[p] = h_counts[p];
+}
+
+}  // namespace qb200

@@ -1,0 +1,104 @@
+// Internal interfaces of libquesadilla_b200 (host C++; not part of the ABI).
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "quesadilla_b200.h"
+
+namespace qb200 {
+
+// Error carrying a C-ABI status; thrown inside the library, caught at the
+// extern "C" boundary (capi.cpp) and turned into a qd_status.
+struct Error : std::runtime_error {
+  qd_status code;
+  uint64_t row = 0;
+  uint32_t mode = 0;
+  Error(qd_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void invalid(const std::string& m) {
+  throw Error(QD_INVALID_ARGUMENT, m);
+}
+
+// ---- planner (planner.cpp) -------------------------------------------------
+struct Step {
+  uint32_t prefix_len;
+  uint32_t mode;
+};
+
+void check_ordering(const uint32_t* ord, uint32_t rank);  // ordering.cpp:13-31
+std::vector<Step> plan_to_prefix(const uint32_t* target, uint32_t rank,
+                                 uint32_t want);          // planner.cpp:37-56
+int required_sort_count(const uint32_t* source, const uint32_t* target,
+                        uint32_t rank);                   // planner.cpp:19-29
+std::vector<uint32_t> apply_transition(const uint32_t* cur, uint32_t rank,
+                                       Step s);           // plan.cpp:7-27
+
+// One device "group": a segmented stable sort.  Rows are partitioned into
+// maximal runs agreeing on `prefix` (in the current order; empty prefix =
+// one run) and each run is stably sorted by the combined key `keys`
+// (priority order, keys[0] most significant).  A run of consecutive plan
+// steps with the same prefix_len is exactly one group (LSD composition).
+struct Group {
+  std::vector<uint32_t> prefix;
+  std::vector<uint32_t> keys;
+  uint32_t first_step = 0, n_steps = 0;  // logical plan steps it covers
+  // Histogram passes range-check their key (sort.cpp:26-30 -> out_of_range);
+  // comparison phases (sort_rows_by) do not, and then key widths come from
+  // the data instead of the dimensions.
+  bool check_range = true;
+};
+
+// Groups for a whole strategy (transpose.cpp:79-112): the LOGICAL steps go to
+// `steps` (pass_log semantics), the device work to the returned groups.
+std::vector<Group> strategy_groups(const uint32_t* target, uint32_t rank,
+                                   qd_strategy_kind kind, uint32_t k,
+                                   std::vector<Step>* steps);
+
+// ---- device engine (engine.cu) ----------------------------------------------
+struct Workspace;
+Workspace* workspace_create(int device);
+void workspace_destroy(Workspace* ws);
+uint64_t workspace_bytes(const Workspace* ws);
+uint64_t workspace_launches(const Workspace* ws);
+
+struct TensorView {
+  uint32_t rank;
+  const uint32_t* dims;  // host
+  uint64_t nnz;
+};
+
+// Runs the groups in order, src -> dst (device pointers, distinct).  Checks
+// verify_input (simple order) first when asked.  Synchronises `stream` and
+// throws Error on invalid input / out-of-range coordinates / CUDA errors.
+void run_groups(Workspace& ws, const TensorView& t, const uint32_t* d_c_in,
+                const double* d_v_in, uint32_t* d_c_out, double* d_v_out,
+                const std::vector<Group>& groups, bool verify_input,
+                uint64_t* d_boundaries, uint64_t* n_boundaries,
+                uint32_t boundary_mode, void* stream);
+
+// Host-buffer convenience: H2D, run_groups, D2H (only on success).
+void run_groups_host(Workspace& ws, const TensorView& t, uint32_t* coords,
+                     double* values, const std::vector<Group>& groups,
+                     bool verify_input, uint64_t* h_boundaries,
+                     uint64_t* n_boundaries, uint32_t boundary_mode);
+
+bool is_sorted_device(Workspace& ws, uint32_t rank, uint64_t nnz,
+                      const uint32_t* d_coords, const uint32_t* order,
+                      void* stream);
+uint64_t bucket_starts_device(Workspace& ws, uint32_t rank, uint64_t nnz,
+                              const uint32_t* d_coords, const uint32_t* modes,
+                              uint32_t n_modes, uint64_t* d_starts, void* stream);
+void mode_histogram_device(Workspace& ws, uint32_t rank, uint64_t nnz,
+                           const uint32_t* d_coords, uint32_t mode, uint32_t dim,
+                           uint64_t* d_hist, void* stream);
+void partition_rows_device(Workspace& ws, uint32_t rank, uint64_t nnz,
+                           const uint32_t* d_c_in, const double* d_v_in,
+                           uint32_t mode, uint32_t dim, const uint32_t* d_lookup,
+                           uint32_t n_parts, uint32_t* d_c_out, double* d_v_out,
+                           uint64_t* part_counts, void* stream);
+
+}  // namespace qb200

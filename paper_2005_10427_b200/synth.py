@@ -1,0 +1,129 @@
+"""Seeded synthetic COO tensors standing in for the paper's FROSTT inputs
+(the datasets are not available offline; BASELINE.json configs 2-5 give the
+shapes and value distributions, SURVEY.md §8(d) the generator rules).
+
+* Coordinates are drawn per mode (Zipf(s) over ranks 1..n -> index rank-1,
+  uniform, or clustered Gaussian), from numpy's counter-based Philox
+  generator keyed by the seed.
+* The unique set is the first N distinct coordinate rows in draw order (the
+  reference generate()'s Distinct semantics, io.cpp:187-196), topped up with
+  more draws when duplicates leave it short.
+* Values are U[0,1) (or lognormal(0,1) for the clustered config), drawn per
+  accepted row; rows are then sorted into the simple order (0, 1, ..., r-1).
+
+This is harness code (inputs for tests and bench.py), not the measured path.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+
+@dataclass
+class Config:
+    name: str
+    dims: List[int]
+    nnz: int
+    dist: List[str]           # per mode: "zipf", "uniform", "cluster"
+    s: float = 1.0            # Zipf exponent
+    values: str = "uniform"   # or "lognormal"
+    seed: int = 0
+    targets: List[List[int]] = field(default_factory=list)
+    clusters: int = 0
+    sigma: float = 0.0
+
+
+CONFIGS = {
+    "c1": Config("c1", [1000, 1000, 1000], 1_000_000, ["uniform"] * 3, seed=1,
+                 targets=[[2, 1, 0]]),
+    "c2": Config("c2", [12092, 9184, 28818], 76_879_419, ["zipf"] * 3, s=1.1, seed=2,
+                 targets=[[0, 2, 1], [1, 0, 2], [1, 2, 0], [2, 0, 1], [2, 1, 0]]),
+    "c3": Config("c3", [532924, 17262471, 2480308, 1443], 140_126_220,
+                 ["zipf", "zipf", "zipf", "uniform"], s=1.2, seed=3,
+                 targets=[[3, 2, 1, 0], [1, 0, 2, 3], [0, 3, 1, 2]]),
+    "c4": Config("c4", [1605, 4198, 1631, 4209, 868131], 1_698_825, ["cluster"] * 5,
+                 values="lognormal", seed=4, targets=[[4, 3, 2, 1, 0], [0, 1, 4, 2, 3]],
+                 clusters=10_000, sigma=0.02),
+    "c5": Config("c5", [4821207, 1774269, 1805187], 1_741_809_018, ["zipf"] * 3, s=1.05,
+                 seed=5, targets=[[1, 0, 2], [0, 2, 1]]),
+}
+
+
+def _zipf_cdf(n: int, s: float) -> np.ndarray:
+    w = np.arange(1, n + 1, dtype=np.float64) ** (-s)
+    c = np.cumsum(w)
+    c /= c[-1]
+    return c
+
+
+def _bits(d: int) -> int:
+    return max(1, int(d - 1).bit_length())
+
+
+def _draw(cfg: Config, rng: np.random.Generator, m: int, cdfs, centres) -> np.ndarray:
+    r = len(cfg.dims)
+    out = np.empty((m, r), np.uint32)
+    if "cluster" in cfg.dist:
+        pick = rng.integers(0, cfg.clusters, m)
+    for j, (d, kind) in enumerate(zip(cfg.dims, cfg.dist)):
+        if kind == "zipf":
+            out[:, j] = np.minimum(np.searchsorted(cdfs[j], rng.random(m), side="right"), d - 1)
+        elif kind == "uniform":
+            out[:, j] = rng.integers(0, d, m)
+        elif kind == "cluster":
+            x = centres[pick, j] + rng.normal(0.0, cfg.sigma * d, m)
+            out[:, j] = np.clip(np.rint(x), 0, d - 1).astype(np.uint32)
+        else:
+            raise ValueError(kind)
+    return out
+
+
+def _pack(rows: np.ndarray, dims: Sequence[int]) -> np.ndarray:
+    """Lexicographic key (mode 0 most significant); needs sum of bits <= 64."""
+    key = np.zeros(len(rows), np.uint64)
+    for j, d in enumerate(dims):
+        key = (key << np.uint64(_bits(d))) | rows[:, j].astype(np.uint64)
+    return key
+
+
+def generate(cfg: Config, nnz: Optional[int] = None, seed: Optional[int] = None):
+    """Returns (coords uint32[N*r], values f64[N]) simply sorted, N unique rows."""
+    n = cfg.nnz if nnz is None else int(nnz)
+    seed = cfg.seed if seed is None else seed
+    rng = np.random.Generator(np.random.Philox(seed))
+    r = len(cfg.dims)
+    cdfs = [(_zipf_cdf(d, cfg.s) if k == "zipf" else None) for d, k in zip(cfg.dims, cfg.dist)]
+    centres = None
+    if "cluster" in cfg.dist:
+        centres = np.stack([rng.uniform(0, d, cfg.clusters) for d in cfg.dims], 1)
+    packable = sum(_bits(d) for d in cfg.dims) <= 64
+    drawn = []
+    total = 0
+    m = int(n * 1.25) + 1024
+    while True:
+        drawn.append(_draw(cfg, rng, m, cdfs, centres))
+        total += m
+        rows = np.concatenate(drawn) if len(drawn) > 1 else drawn[0]
+        if packable:
+            _, first = np.unique(_pack(rows, cfg.dims), return_index=True)
+        else:
+            v = np.ascontiguousarray(rows).view(np.dtype((np.void, 4 * r))).ravel()
+            _, first = np.unique(v, return_index=True)
+        if len(first) >= n:
+            break
+        deficit = n - len(first)
+        m = int(deficit * max(2.0, total / max(1, len(first)))) + 1024
+    chosen = np.sort(first)[:n]            # draw indices of the first n distinct rows
+    sel = rows[chosen]
+    if cfg.values == "lognormal":
+        values = np.exp(rng.normal(0.0, 1.0, n))
+    else:
+        values = rng.random(n)
+    if packable:
+        perm = np.argsort(_pack(sel, cfg.dims), kind="stable")
+    else:
+        perm = np.lexsort(sel.T[::-1])
+    sel, values = sel[perm], values[perm]
+    return np.ascontiguousarray(sel).reshape(-1), values

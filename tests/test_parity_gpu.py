@@ -1,0 +1,323 @@
+"""GPU parity: the CUDA path through the C ABI versus the oracle, bit for bit
+(coords by value, values by raw f64 bits).  Mirrors the reference's own test
+strategy (proj/tests/test_sort.cpp, test_parallel.cpp, acceptance.cpp)."""
+import itertools
+
+import numpy as np
+import pytest
+
+import paper_2005_10427_b200 as qd
+from golden_util import cases, golden
+from pyoracle import Oracle, OracleError, Reference, reference_available
+
+pytestmark = pytest.mark.gpu
+
+ORC = Oracle()
+STRATS = {"quesadilla": qd.SortStrategy.quesadilla(), "radix": qd.SortStrategy.full_radix(),
+          "comparison": qd.SortStrategy.comparison_sort()}
+
+
+@pytest.fixture(scope="module")
+def ws():
+    w = qd.Workspace(0)
+    yield w
+    w.close()
+
+
+def same(out: qd.CooTensor, c, v):
+    return np.array_equal(out.coords, c) and np.array_equal(out.values.view(np.uint64),
+                                                            np.asarray(v).view(np.uint64))
+
+
+def strategy(name, k):
+    return qd.SortStrategy.top_k(k) if name == "topk" else STRATS[name]
+
+
+def rand_tensor(rng, dims, nnz, sort=True, distinct=False):
+    c = np.stack([rng.integers(0, d, nnz) for d in dims], 1).astype(np.uint32)
+    if distinct:
+        c = np.unique(c, axis=0)
+    if sort:
+        c = c[np.lexsort(c.T[::-1])]
+    v = rng.random(len(c))
+    return qd.CooTensor(dims, c.ravel(), v)
+
+
+# --- the reference's worked example -----------------------------------------
+
+def test_golden_example(ws):
+    g = golden()["golden"]
+    t = qd.CooTensor(g["dims"], g["input_coords"], g["input_values"])
+    log = []
+    out = qd.transpose(t, g["target"], qd.SortStrategy.quesadilla(),
+                       qd.TransposeOptions(verify_input=True, pass_log=log), ws)
+    assert out.coords.tolist() == g["output_coords"]
+    assert out.values.tolist() == g["output_values"]
+    assert log == [qd.PlanStep(2, 3)]
+
+
+def test_golden_step1_and_bucketed_call(ws):
+    g = golden()["golden"]
+    t = qd.CooTensor(g["dims"], g["input_coords"], g["input_values"])
+    s = t.copy()
+    qd.partial_sort(s, [], 3, ws)
+    assert s.coords.tolist() == g["step1_mode3_coords"]
+    assert s.values.tolist() == g["step1_mode3_values"]
+    b = t.copy()
+    qd.partial_sort(b, [0, 1], 3, ws)
+    assert b.coords.tolist() == g["output_coords"]
+    assert qd.is_sorted_under(b, g["target"])
+
+
+# --- committed reference cases (all strategies) --------------------------------
+
+@pytest.mark.parametrize("case", cases(), ids=lambda c: f"case{c['i']}")
+def test_reference_cases(case, ws):
+    t = qd.CooTensor(case["dims"], case["c_in"], case["v_in"])
+    log = []
+    out = qd.transpose(t, case["target"], strategy(case["strategy"], case["k"]),
+                       qd.TransposeOptions(pass_log=log), ws)
+    assert same(out, case["c_out"], case["v_out"])
+    assert [[s.prefix_len, s.mode] for s in log] == case["pass_log"]
+
+
+# --- randomised equivalence with the oracle ----------------------------------
+
+def test_every_strategy_random(ws):
+    rng = np.random.default_rng(1234)
+    n_cases = 0
+    for r in range(1, 6):
+        for i in range(6):
+            dims = [int(x) for x in rng.integers(1, 12 if i % 2 else 3000, r)]
+            t = rand_tensor(rng, dims, int(rng.integers(0, 6000)))
+            target = [int(x) for x in rng.permutation(r)]
+            for name, k in [("quesadilla", 0), ("radix", 0), ("comparison", 0),
+                            ("topk", 1), ("topk", r)]:
+                out = qd.transpose(t, target, strategy(name, k), None, ws)
+                c, v, _ = ORC.transpose(dims, t.coords, t.values, target, name, k)
+                assert same(out, c, v), (dims, target, name, k)
+                n_cases += 1
+    assert n_cases >= 150
+
+
+def test_all_targets_rank4_pass_log(ws):
+    rng = np.random.default_rng(99)
+    t = rand_tensor(rng, [7, 5, 6, 4], 300)
+    for target in itertools.permutations(range(4)):
+        log = []
+        out = qd.transpose(t, list(target), qd.SortStrategy.quesadilla(),
+                           qd.TransposeOptions(pass_log=log), ws)
+        c, v, olog = ORC.transpose(t.dims, t.coords, t.values, list(target))
+        assert same(out, c, v)
+        assert [(s.prefix_len, s.mode) for s in log] == olog
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_partial_sort_any_prefix_any_order(ws, seed):
+    # Alg. 2 semantics on arbitrary (even unsorted) inputs: buckets are maximal runs.
+    rng = np.random.default_rng(seed)
+    for _ in range(10):
+        r = int(rng.integers(2, 6))
+        dims = [int(x) for x in rng.integers(1, 40, r)]
+        t = rand_tensor(rng, dims, int(rng.integers(1, 20000)), sort=bool(rng.integers(0, 2)))
+        perm = [int(x) for x in rng.permutation(r)]
+        mode = perm[-1]
+        prefix = perm[: int(rng.integers(0, r))]
+        s = t.copy()
+        qd.partial_sort(s, prefix, mode, ws)
+        c, v = ORC.partial_sort(dims, t.coords, t.values, prefix, mode)
+        assert same(s, c, v), (dims, prefix, mode)
+
+
+# --- shapes that exercise every kernel path -----------------------------------
+
+@pytest.mark.parametrize("shape", [
+    # (dims, nnz, target): large single run (uniform tiles), multi-digit keys
+    ([50, 4000, 70000], 300_000, [2, 1, 0]),
+    ([50, 4000, 70000], 300_000, [1, 0, 2]),
+    # huge buckets (few prefix values) -> look-back across many tiles per run
+    ([3, 5000, 900], 400_000, [0, 2, 1]),
+    # tiny buckets -> local CTA sorts
+    ([20000, 40, 9000], 200_000, [0, 2, 1]),
+    # mixture of large and small buckets (skewed)
+    ("zipf", 400_000, [0, 2, 1]),
+    # rank 5, multi-step bucketed plan
+    ([30, 20, 40, 25, 900], 250_000, [0, 1, 4, 2, 3]),
+    ([30, 20, 40, 25, 900], 250_000, [4, 3, 2, 1, 0]),
+    # 1-bit and extent-1 modes
+    ([1, 2, 1, 3000], 50_000, [3, 1, 0, 2]),
+])
+def test_kernel_paths(ws, shape):
+    dims, nnz, target = shape
+    rng = np.random.default_rng(7)
+    if dims == "zipf":
+        from paper_2005_10427_b200 import synth
+        cfg = synth.CONFIGS["c2"]
+        c, v = synth.generate(cfg, nnz, seed=11)
+        t = qd.CooTensor(cfg.dims, c, v)
+        dims = cfg.dims
+    else:
+        t = rand_tensor(rng, dims, nnz)
+    for name in ("quesadilla", "radix"):
+        out = qd.transpose(t, target, STRATS[name], None, ws)
+        c, v, _ = ORC.transpose(dims, t.coords, t.values, target, name)
+        assert same(out, c, v), (dims, target, name)
+
+
+# --- edge cases the reference tests ------------------------------------------
+
+def test_rank1_and_extent1(ws):
+    t = qd.CooTensor([3], [2, 0, 1], [1.0, 2.0, 3.0])
+    s = t.copy()
+    qd.partial_sort(s, [], 0, ws)
+    assert s.coords.tolist() == [0, 1, 2] and s.values.tolist() == [2.0, 3.0, 1.0]
+    u = qd.CooTensor([1, 3], [0, 2, 0, 0, 0, 1], [1.0, 2.0, 3.0])
+    s = u.copy()
+    qd.partial_sort(s, [], 0, ws)
+    assert s == u  # every key 0: stable, order kept
+    e = qd.CooTensor([1, 3], [0, 0, 0, 1, 0, 2], [1.0, 2.0, 3.0])
+    for target in ([0, 1], [1, 0]):
+        assert qd.transpose(e, target, ws=ws) == qd.comparison_transpose(e, target, ws=ws)
+
+
+def test_empty_tensor(ws):
+    t = qd.CooTensor([4, 4], np.zeros(0, np.uint32), np.zeros(0))
+    qd.partial_sort(t, [], 1, ws)
+    qd.partial_sort(t, [0], 1, ws)
+    out = qd.transpose(t, [1, 0], ws=ws)
+    assert out.nnz() == 0
+
+
+def test_identity_is_zero_pass_noop(ws):
+    rng = np.random.default_rng(21)
+    t = rand_tensor(rng, [8, 8, 8], 300)
+    log = []
+    out = qd.transpose(t, [0, 1, 2], qd.SortStrategy.quesadilla(),
+                       qd.TransposeOptions(pass_log=log), ws)
+    assert out == t and log == []
+
+
+def test_argument_errors(ws):
+    t = qd.CooTensor([2, 2], [0, 1], [1.0])
+    with pytest.raises(qd.InvalidArgument):
+        qd.partial_sort(t, [1], 1, ws)
+    with pytest.raises(qd.InvalidArgument):
+        qd.partial_sort(t, [], 2, ws)
+    with pytest.raises(qd.InvalidArgument):
+        qd.topk_transpose(t, [1, 0], 0, ws=ws)
+    with pytest.raises(qd.InvalidArgument):
+        qd.topk_transpose(t, [1, 0], 3, ws=ws)
+    with pytest.raises(qd.InvalidArgument):
+        qd.transpose(t, [1, 0], qd.SortStrategy.quesadilla(),
+                     qd.TransposeOptions(parallel=qd.ParallelConfig(0)), ws)
+
+
+def test_out_of_range_detected_and_tensor_untouched(ws):
+    t = qd.CooTensor([4, 4], [0, 1, 1, 0], [1.0, 2.0])
+    t.coords[1] = 9
+    before = t.copy()
+    with pytest.raises(qd.OutOfRange) as e:
+        qd.partial_sort(t, [], 1, ws)
+    assert t == before and e.value.mode == 1 and e.value.row == 0
+    # a mode the plan never sorts is never checked (as in the reference)
+    u = qd.CooTensor([4, 4], [9, 1, 9, 3], [1.0, 2.0])
+    with pytest.raises(OracleError):
+        ORC.partial_sort(u.dims, u.coords, u.values, [], 0)
+    out = qd.transpose(u, [0, 1], ws=ws)  # identity: zero passes
+    assert out == u
+    # larger tensor, bad coordinate deep inside a large run
+    rng = np.random.default_rng(3)
+    big = rand_tensor(rng, [5, 3000, 3000], 200_000)
+    big.coords[3 * 150_000 + 2] = 3000
+    with pytest.raises(qd.OutOfRange):
+        qd.transpose(big, [2, 1, 0], ws=ws)
+    with pytest.raises(qd.OutOfRange):
+        qd.transpose(big, [0, 2, 1], ws=ws)
+
+
+def test_verify_input(ws):
+    t = qd.CooTensor([3, 3], [2, 0, 0, 1], [1.0, 2.0])
+    with pytest.raises(qd.InvalidArgument):
+        qd.transpose(t, [1, 0], qd.SortStrategy.quesadilla(),
+                     qd.TransposeOptions(verify_input=True), ws)
+
+
+def test_stability_with_duplicates(ws):
+    # test_sort.cpp:259-278: identical coordinates keep their value order
+    t = qd.CooTensor([3, 3, 3], [0, 1, 2, 1, 2, 0, 1, 2, 0, 2, 0, 1], [10, 20, 30, 40])
+    for target in itertools.permutations(range(3)):
+        for s in (qd.SortStrategy.quesadilla(), qd.SortStrategy.full_radix(),
+                  qd.SortStrategy.top_k(1), qd.SortStrategy.top_k(2)):
+            out = qd.transpose(t, list(target), s, None, ws)
+            j = list(out.values).index(20.0)
+            assert out.values[j + 1] == 30.0
+    # duplicate-heavy tensor (test_parallel.cpp:347-362)
+    rng = np.random.default_rng(5)
+    d = rand_tensor(rng, [2, 2, 3], 20_000)
+    for target in itertools.permutations(range(3)):
+        out = qd.transpose(d, list(target), ws=ws)
+        c, v, _ = ORC.transpose(d.dims, d.coords, d.values, list(target), "comparison")
+        assert same(out, c, v)
+
+
+def test_determinism(ws):
+    rng = np.random.default_rng(8)
+    t = rand_tensor(rng, [100, 3000, 500], 500_000)
+    a = qd.transpose(t, [2, 0, 1], ws=ws)
+    for _ in range(3):
+        assert qd.transpose(t, [2, 0, 1], ws=ws) == a
+
+
+# --- against the reference library itself ------------------------------------
+
+@pytest.mark.skipif(not reference_available(), reason="oracle/_ref not built")
+def test_config1_against_reference(ws):
+    ref = Reference()
+    c, v = ref.generate([1000, 1000, 1000], 1_000_000, 1, distinct=True)
+    t = qd.CooTensor([1000, 1000, 1000], c, v)
+    bounds = []
+    log = []
+    out = qd.transpose(t, [2, 1, 0], qd.SortStrategy.quesadilla(),
+                       qd.TransposeOptions(pass_log=log, boundaries=bounds), ws)
+    rc, rv, rlog = ref.transpose(t.dims, c, v, [2, 1, 0], workers=4)
+    assert same(out, rc, rv)
+    assert [(s.prefix_len, s.mode) for s in log] == rlog == [(0, 1), (0, 2)]
+    starts = ref.bucket_starts(t.dims, rc, rv, [2])
+    assert bounds == list(starts) + [t.nnz()]
+
+
+@pytest.mark.skipif(not reference_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("cfg_name,n", [("c2", 2_000_000), ("c3", 1_000_000), ("c4", None)])
+def test_configs_scaled_against_reference(ws, cfg_name, n):
+    from paper_2005_10427_b200 import synth
+    cfg = synth.CONFIGS[cfg_name]
+    c, v = synth.generate(cfg, n)
+    t = qd.CooTensor(cfg.dims, c, v)
+    ref = Reference()
+    for target in cfg.targets:
+        out = qd.transpose(t, target, qd.SortStrategy.quesadilla(), None, ws)
+        rc, rv, _ = ref.transpose(cfg.dims, c, v, target, workers=8)
+        assert same(out, rc, rv), (cfg_name, target)
+
+
+# --- device API -------------------------------------------------------------------
+
+def test_device_api_with_torch(ws):
+    import torch
+    rng = np.random.default_rng(4)
+    t = rand_tensor(rng, [64, 2000, 5000], 300_000)
+    ci = torch.from_numpy(t.coords.view(np.int32)).cuda()
+    vi = torch.from_numpy(t.values).cuda()
+    co = torch.empty_like(ci)
+    vo = torch.empty_like(vi)
+    b = torch.empty(t.nnz() + 1, dtype=torch.int64, device="cuda")
+    nb = qd.transpose_device_boundaries(3, t.dims, t.nnz(), ci.data_ptr(), vi.data_ptr(),
+                                        co.data_ptr(), vo.data_ptr(), [1, 0, 2], b.data_ptr(),
+                                        ws=ws, stream=torch.cuda.current_stream().cuda_stream)
+    c, v, _ = ORC.transpose(t.dims, t.coords, t.values, [1, 0, 2])
+    assert np.array_equal(co.cpu().numpy().view(np.uint32), c)
+    assert np.array_equal(vo.cpu().numpy().view(np.uint64), v.view(np.uint64))
+    starts = ORC.bucket_starts(3, c, [1])
+    assert b[:nb].cpu().numpy().tolist() == list(starts) + [t.nnz()]
+    assert qd.is_sorted_device(3, t.nnz(), co.data_ptr(), [1, 0, 2], ws=ws)
+    assert not qd.is_sorted_device(3, t.nnz(), co.data_ptr(), [0, 1, 2], ws=ws)
