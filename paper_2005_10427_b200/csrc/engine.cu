@@ -914,8 +914,15 @@ Workspace* workspace_create(int device) {
   ws->smem_optin = optin;
   QD_CUDA(cudaMallocHost(&ws->h_err, sizeof(ErrBlock)));
   QD_CUDA(cudaMallocHost(&ws->h_small, 64 * sizeof(uint64_t)));
-  QD_CUDA(cudaFuncSetAttribute(k_onesweep, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
-  QD_CUDA(cudaFuncSetAttribute(k_local, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+  auto allow_smem = [&](const void* fn) {
+    cudaFuncAttributes fa{};
+    QD_CUDA(cudaFuncGetAttributes(&fa, fn));
+    QD_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 optin - (int)fa.sharedSizeBytes));
+  };
+  allow_smem(reinterpret_cast<const void*>(k_onesweep));
+  allow_smem(reinterpret_cast<const void*>(k_local));
+  ws->smem_optin = optin - 1024;  // dynamic budget below the static usage
   return ws;
 }
 
