@@ -90,6 +90,16 @@ uint64_t qd_workspace_bytes(const qd_workspace* ws);
 /* Number of CUDA kernels this workspace has launched since creation. */
 uint64_t qd_workspace_launches(const qd_workspace* ws);
 
+/* Live per-kernel-class timing with CUDA events recorded on the launch
+ * stream (off by default).  Classes: 0 onesweep digit pass, 1 histogram,
+ * 2 local (in-CTA) run sort, 3 run discovery / scans, 4 other.  bytes is the
+ * algorithmic traffic of the class (rows moved x 2 x row bytes for
+ * classes 0 and 2, coordinates read for class 1). */
+void qd_profile_enable(qd_workspace* ws, int enable);
+void qd_profile_reset(qd_workspace* ws);
+qd_status qd_profile_get(const qd_workspace* ws, int kernel_class,
+                         uint64_t* launches, double* total_ms, double* bytes);
+
 /* ---- planner (host; planner.hpp:13-55, plan.hpp:27-36) ------------------ */
 qd_status qd_quesadilla_plan(const uint32_t* target, uint32_t rank,
                              qd_plan_step* steps, uint32_t capacity,

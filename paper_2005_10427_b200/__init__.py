@@ -101,6 +101,10 @@ def lib():
         L.qd_workspace_bytes.restype = C.c_uint64
         L.qd_workspace_launches.argtypes = [C.c_void_p]
         L.qd_workspace_launches.restype = C.c_uint64
+        L.qd_profile_enable.argtypes = [C.c_void_p, C.c_int]
+        L.qd_profile_reset.argtypes = [C.c_void_p]
+        L.qd_profile_get.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_uint64),
+                                     C.POINTER(C.c_double), C.POINTER(C.c_double)]
         L.qd_last_error_detail.argtypes = [C.POINTER(C.c_uint64), C.POINTER(C.c_uint32)]
         L.qd_quesadilla_plan.argtypes = [_u32p, C.c_uint32, C.POINTER(PlanStepC), C.c_uint32, _u32p]
         L.qd_prefix_plan.argtypes = [_u32p, C.c_uint32, C.c_uint32, C.POINTER(PlanStepC),
@@ -453,6 +457,23 @@ class Workspace:
 
     def launches(self) -> int:
         return int(lib().qd_workspace_launches(self._h))
+
+    PROFILE_CLASSES = ("onesweep", "hist", "local", "runs", "other")
+
+    def profile(self, enable: bool = True):
+        """Live per-kernel-class CUDA-event timing inside the library."""
+        lib().qd_profile_enable(self._h, int(enable))
+
+    def profile_reset(self):
+        lib().qd_profile_reset(self._h)
+
+    def profile_stats(self) -> dict:
+        out = {}
+        for i, name in enumerate(self.PROFILE_CLASSES):
+            n, ms, b = C.c_uint64(0), C.c_double(0), C.c_double(0)
+            _check(lib().qd_profile_get(self._h, i, C.byref(n), C.byref(ms), C.byref(b)))
+            out[name] = {"launches": n.value, "ms": ms.value, "bytes": b.value}
+        return out
 
     def close(self):
         if self._h:

@@ -112,6 +112,22 @@ uint64_t qd_workspace_launches(const qd_workspace* ws) {
   return ws ? workspace_launches(reinterpret_cast<const Workspace*>(ws)) : 0;
 }
 
+void qd_profile_enable(qd_workspace* ws, int enable) {
+  if (ws) workspace_profile(reinterpret_cast<Workspace*>(ws), enable);
+}
+void qd_profile_reset(qd_workspace* ws) {
+  if (ws) workspace_profile_reset(reinterpret_cast<Workspace*>(ws));
+}
+qd_status qd_profile_get(const qd_workspace* ws, int kernel_class, uint64_t* launches,
+                         double* total_ms, double* bytes) {
+  return guard([&] {
+    if (!ws || !launches || !total_ms || !bytes) invalid("null argument");
+    if (!workspace_profile_get(reinterpret_cast<const Workspace*>(ws), kernel_class, launches,
+                               total_ms, bytes))
+      invalid("kernel class must be in 0..4");
+  });
+}
+
 qd_status qd_quesadilla_plan(const uint32_t* target, uint32_t rank, qd_plan_step* steps,
                              uint32_t capacity, uint32_t* n_steps) {
   return guard([&] { copy_steps(plan_to_prefix(target, rank, rank), steps, capacity, n_steps); });

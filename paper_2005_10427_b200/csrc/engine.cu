@@ -72,10 +72,13 @@ struct KeySpec {
   uint32_t dim[kMaxKeys];
 };
 
+constexpr int kMaxGroups = 64;
+
 struct ErrBlock {
   unsigned int flags;  // bit0 out_of_range, bit1 not simply sorted
   unsigned int pad;
   unsigned long long rowmode;  // min over (row << 6 | mode)
+  unsigned long long rows[kMaxGroups];  // rows of large runs, per group (profiling)
 };
 
 struct TileDesc {
@@ -119,6 +122,7 @@ struct HistArgs {
   KeySpec key;
   int do_check;
   ErrBlock* err;
+  unsigned long long* rows_counter;  // += rows histogrammed (pass0 == 0 only)
 };
 
 struct LocalArgs {
@@ -474,6 +478,7 @@ __global__ void __launch_bounds__(kThreads) k_hist(HistArgs a) {
     __syncthreads();
   };
   auto count_rows = [&](unsigned long long rb, uint32_t n) {
+    if (threadIdx.x == 0 && a.rows_counter) atomicAdd(a.rows_counter, (unsigned long long)n);
     // whole warps iterate together so __match_any_sync sees full masks
     for (uint32_t base = 0; base < n; base += kThreads) {
       const uint32_t i = base + threadIdx.x;
@@ -883,6 +888,23 @@ struct Workspace {
   ErrBlock* h_err = nullptr;  // pinned
   uint64_t* h_small = nullptr;  // pinned scratch for small D2H reads
   void* status_clean = nullptr;  // look-back buffer known to hold no stale flags
+  // live per-kernel-class timing (CUDA events on the launch stream)
+  bool prof = false;
+  struct ProfStat {
+    uint64_t launches = 0;
+    double ms = 0, bytes = 0;
+  } prof_stats[5];
+  std::vector<cudaEvent_t> ev_pool;
+  cudaEvent_t event() {
+    if (ev_pool.empty()) {
+      cudaEvent_t e;
+      QD_CUDA(cudaEventCreate(&e));
+      return e;
+    }
+    cudaEvent_t e = ev_pool.back();
+    ev_pool.pop_back();
+    return e;
+  }
 
   template <class T>
   T* get(const std::string& name, size_t count) {
@@ -933,6 +955,7 @@ void workspace_destroy(Workspace* ws) {
     if (kv.second.p) cudaFree(kv.second.p);
   if (ws->h_err) cudaFreeHost(ws->h_err);
   if (ws->h_small) cudaFreeHost(ws->h_small);
+  for (auto e : ws->ev_pool) cudaEventDestroy(e);
   delete ws;
 }
 
@@ -943,6 +966,22 @@ uint64_t workspace_bytes(const Workspace* ws) {
 }
 uint64_t workspace_launches(const Workspace* ws) { return ws->launches; }
 
+void workspace_profile(Workspace* ws, int enable) {
+  ws->prof = enable != 0;
+}
+void workspace_profile_reset(Workspace* ws) {
+  for (auto& p : ws->prof_stats) p = Workspace::ProfStat{};
+}
+bool workspace_profile_get(const Workspace* ws, int cls, uint64_t* launches, double* ms,
+                           double* bytes) {
+  if (cls < 0 || cls >= 5) return false;
+  const auto& p = ws->prof_stats[cls];
+  *launches = p.launches;
+  *ms = p.ms;
+  *bytes = p.bytes;
+  return true;
+}
+
 namespace {
 
 uint32_t ceil_log2(uint64_t x) {
@@ -951,15 +990,62 @@ uint32_t ceil_log2(uint64_t x) {
   return b;
 }
 
+// kernel classes for profiling
+enum { kSweep = 0, kHistK = 1, kLocalK = 2, kSegK = 3, kOtherK = 4 };
+
 struct Ctx {
   Workspace& ws;
   cudaStream_t st;
   ErrBlock* err;       // device
   uint32_t* counters;  // device, tile counters
   uint32_t next_counter = 0;
-  void launched() {
+  // profiling records, resolved after the call's final synchronisation
+  struct Rec {
+    int cls;
+    cudaEvent_t a, b;
+    int group;
+    int all_rows;  // local: 1 = every row of the group, 0 = rows outside large runs
+  };
+  std::vector<Rec> recs;
+  cudaEvent_t pending = nullptr;
+  int group = 0;
+  uint64_t nnz = 0;
+  uint32_t rank = 0;
+  void pre() {
+    if (ws.prof) {
+      pending = ws.event();
+      QD_CUDA(cudaEventRecord(pending, st));
+    }
+  }
+  void launched(int cls = kOtherK, int all_rows = 0) {
     ++ws.launches;
     QD_CUDA(cudaGetLastError());
+    if (ws.prof && pending) {
+      cudaEvent_t b = ws.event();
+      QD_CUDA(cudaEventRecord(b, st));
+      recs.push_back({cls, pending, b, std::min(group, kMaxGroups - 1), all_rows});
+      pending = nullptr;
+    }
+  }
+  // after the final stream sync: fold the records into ws.prof_stats
+  void resolve(const ErrBlock& e) {
+    const double row_bytes = 4.0 * rank + 8.0;
+    for (auto& r : recs) {
+      float ms = 0;
+      QD_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+      const double large = (double)e.rows[r.group];
+      double bytes = 0;
+      if (r.cls == kSweep) bytes = large * 2 * row_bytes;
+      else if (r.cls == kHistK) bytes = large * 4.0 * rank;
+      else if (r.cls == kLocalK) bytes = (r.all_rows ? (double)nnz : (double)nnz - large) * 2 * row_bytes;
+      auto& p = ws.prof_stats[r.cls];
+      ++p.launches;
+      p.ms += ms;
+      p.bytes += bytes;
+      ws.ev_pool.push_back(r.a);
+      ws.ev_pool.push_back(r.b);
+    }
+    recs.clear();
   }
 };
 
@@ -987,12 +1073,15 @@ void scan_exclusive(Ctx& c, const uint32_t* in, uint64_t n, unsigned long long* 
     QD_CUDA(cudaMemsetAsync(d_total, 0, sizeof(unsigned long long), c.st));
     return;
   }
+  c.pre();
   k_scan_reduce<<<nb, kThreads, 0, c.st>>>(in, n, part);
-  c.launched();
+  c.launched(kSegK);
+  c.pre();
   k_scan_parts<<<1, kThreads, 0, c.st>>>(part, nb, d_total);
-  c.launched();
+  c.launched(kSegK);
+  c.pre();
   k_scan_down<<<nb, kThreads, 0, c.st>>>(in, n, part, out);
-  c.launched();
+  c.launched(kSegK);
 }
 
 // Segment discovery on `coords` with respect to `modes`: fills seg_start[0..S]
@@ -1007,15 +1096,17 @@ uint64_t find_runs(Ctx& c, const uint32_t* coords, uint32_t rank, uint64_t nnz,
   auto* bcnt = c.ws.get<uint32_t>("head_bcnt", nb + 1);
   auto* boff = c.ws.get<unsigned long long>("head_boff", nb + 1);
   auto* tot = c.ws.get<unsigned long long>("head_total", 1);
+  c.pre();
   k_heads<<<nb, kThreads, 0, c.st>>>(coords, rank, nnz, ml, words, bcnt);
-  c.launched();
+  c.launched(kSegK);
   scan_exclusive(c, bcnt, nb, boff, tot);
   QD_CUDA(cudaMemcpyAsync(c.ws.h_small, tot, 8, cudaMemcpyDeviceToHost, c.st));
   QD_CUDA(cudaStreamSynchronize(c.st));
   const uint64_t S = c.ws.h_small[0];
   auto* seg = c.ws.get<unsigned long long>("seg_start", S + 1);
+  c.pre();
   k_compact<<<nb, kThreads, 0, c.st>>>(words, nnz, boff, nb, seg, tot);
-  c.launched();
+  c.launched(kSegK);
   *seg_out = seg;
   return S;
 }
@@ -1078,8 +1169,9 @@ void launch_pass(Ctx& c, PassArgs& a) {
   }
   a.tile_counter = c.counters + c.next_counter++;
   const size_t smem = SweepLayout(a.T, a.rank).total;
+  c.pre();
   k_onesweep<<<a.num_tiles, kThreads, smem, c.st>>>(a);
-  c.launched();
+  c.launched(kSweep);
 }
 
 // One segmented stable sort (a plan group), src -> dst, with tmp scratch.
@@ -1102,8 +1194,9 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
     auto* mx = ws.get<uint32_t>("mode_max", kMaxKeys);
     QD_CUDA(cudaMemsetAsync(mx, 0, kMaxKeys * 4, c.st));
     const uint32_t grid = (uint32_t)std::min<uint64_t>((N + kThreads - 1) / kThreads, ws.num_sms * 8);
+    c.pre();
     k_mode_max<<<grid, kThreads, 0, c.st>>>(src_c, R, N, ml, mx);
-    c.launched();
+    c.launched(kOtherK);
     uint32_t* h = reinterpret_cast<uint32_t*>(ws.h_small);
     QD_CUDA(cudaMemcpyAsync(h, mx, kMaxKeys * 4, cudaMemcpyDeviceToHost, c.st));
     QD_CUDA(cudaStreamSynchronize(c.st));
@@ -1115,8 +1208,9 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
   if (bits == 0 || N == 1) {
     // nothing to reorder; still the histogram pass's range check
     const uint32_t grid = (uint32_t)std::min<uint64_t>((N + kThreads - 1) / kThreads, ws.num_sms * 8);
+    c.pre();
     k_copy_check<<<grid, kThreads, 0, c.st>>>(src_c, src_v, dst_c, dst_v, R, N, key, c.err);
-    c.launched();
+    c.launched(kOtherK);
     return;
   }
 
@@ -1139,8 +1233,9 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
     if (TL && N <= TL) {
       LocalArgs la{src_c, src_v, dst_c, dst_v, R, N, TL, (uint32_t)N, nullptr, 1, key, c.err};
       const size_t smem = LocalLayout((uint32_t)N, R, TL).total;
+      c.pre();
       k_local<<<1, kThreads, smem, c.st>>>(la);
-      c.launched();
+      c.launched(kLocalK, 1);
       return;
     }
     num_tiles = (N + T - 1) / T;
@@ -1156,8 +1251,9 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
     ws.h_small[0] = S;
     QD_CUDA(cudaMemcpyAsync(S_dev, ws.h_small, 8, cudaMemcpyHostToDevice, c.st));
     const uint32_t grid = (uint32_t)std::min<uint64_t>((S + kThreads - 1) / kThreads, ws.num_sms * 8);
+    c.pre();
     k_classify<<<grid, kThreads, 0, c.st>>>(seg, S_dev, TL, T, is_large, ntl);
-    c.launched();
+    c.launched(kSegK);
     scan_exclusive(c, is_large, S, loff, totals);
     scan_exclusive(c, ntl, S, toff, totals + 1);
     QD_CUDA(cudaMemcpyAsync(ws.h_small + 1, totals, 16, cudaMemcpyDeviceToHost, c.st));
@@ -1167,8 +1263,9 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
     if (num_tiles) {
       auto* td = ws.get<TileDesc>("tiles", num_tiles);
       auto* rs = ws.get<unsigned long long>("run_start", num_large);
+      c.pre();
       k_gen_tiles<<<grid, kThreads, 0, c.st>>>(seg, S_dev, T, is_large, loff, toff, td, rs);
-      c.launched();
+      c.launched(kSegK);
       tiles = td;
       run_start = rs;
     }
@@ -1177,8 +1274,9 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
       LocalArgs la{src_c, src_v, dst_c, dst_v, R, N, TL, 2 * TL, seg, S, key, c.err};
       const size_t smem = LocalLayout(2 * TL, R, TL).total;
       const uint64_t chunks = (N + TL - 1) / TL;
+      c.pre();
       k_local<<<(uint32_t)chunks, kThreads, smem, c.st>>>(la);
-      c.launched();
+      c.launched(kLocalK);
     }
   }
   if (num_tiles == 0) return;
@@ -1203,6 +1301,7 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
     h.key = key;
     h.do_check = p0 == 0 && key.check;
     h.err = c.err;
+    h.rows_counter = p0 == 0 ? &c.err->rows[std::min(c.group, kMaxGroups - 1)] : nullptr;
     uint32_t grid = ws.num_sms * 4;
     if (tiles) {
       h.tiles_per_cta = (uint32_t)std::max<uint64_t>(1, (num_tiles + grid - 1) / grid);
@@ -1210,8 +1309,9 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
     } else {
       grid = (uint32_t)std::min<uint64_t>(grid, (N + 4095) / 4096);
     }
+    c.pre();
     k_hist<<<grid, kThreads, 0, c.st>>>(h);
-    c.launched();
+    c.launched(kHistK);
   }
 
   auto* status = status_buffer(c, num_tiles);
@@ -1249,6 +1349,7 @@ static void check_errors(Ctx& c) {
   QD_CUDA(cudaMemcpyAsync(c.ws.h_err, c.err, sizeof(ErrBlock), cudaMemcpyDeviceToHost, c.st));
   QD_CUDA(cudaStreamSynchronize(c.st));
   const ErrBlock e = *c.ws.h_err;
+  c.resolve(e);
   if (e.flags & 2u) invalid("input tensor is not sorted under the simple ordering");
   if (e.flags & 1u) {
     Error err(QD_OUT_OF_RANGE, "coordinate in row " + std::to_string(e.rowmode >> 6) +
@@ -1265,8 +1366,8 @@ static Ctx make_ctx(Workspace& ws, void* stream) {
   Ctx c{ws, static_cast<cudaStream_t>(stream), nullptr, nullptr};
   c.err = ws.get<ErrBlock>("err", 1);
   c.counters = ws.get<uint32_t>("counters", kCounters);
-  ErrBlock init{0u, 0u, ~0ull};
-  *ws.h_err = init;
+  std::memset(ws.h_err, 0, sizeof(ErrBlock));
+  ws.h_err->rowmode = ~0ull;
   QD_CUDA(cudaMemcpyAsync(c.err, ws.h_err, sizeof(ErrBlock), cudaMemcpyHostToDevice, c.st));
   QD_CUDA(cudaMemsetAsync(c.counters, 0, kCounters * 4, c.st));
   return c;
@@ -1279,13 +1380,16 @@ void run_groups(Workspace& ws, const TensorView& t, const uint32_t* d_c_in, cons
   Ctx c = make_ctx(ws, stream);
   const uint64_t N = t.nnz;
   const uint32_t R = t.rank;
+  c.nnz = N;
+  c.rank = R;
   if (verify_input && N > 1) {
     ModeList ml{};
     ml.n = R;
     for (uint32_t i = 0; i < R; ++i) ml.m[i] = (uint8_t)i;
     const uint32_t grid = (uint32_t)std::min<uint64_t>((N + kThreads - 1) / kThreads, ws.num_sms * 8);
+    c.pre();
     k_is_sorted<<<grid, kThreads, 0, c.st>>>(d_c_in, R, N, ml, c.err);
-    c.launched();
+    c.launched(kOtherK);
   }
   const size_t G = groups.size();
   if (G == 0 || N == 0) {
@@ -1317,6 +1421,7 @@ void run_groups(Workspace& ws, const TensorView& t, const uint32_t* d_c_in, cons
         tc = d_c_out;  // not yet written by anyone
         tv = d_v_out;
       }
+      c.group = (int)gi;
       segmented_sort(c, t, sc, sv, dc, dv, tc, tv, groups[gi]);
       sc = dc;
       sv = dv;
@@ -1368,8 +1473,9 @@ bool is_sorted_device(Workspace& ws, uint32_t rank, uint64_t nnz, const uint32_t
   for (uint32_t i = 0; i < rank; ++i) ml.m[i] = (uint8_t)order[i];
   if (nnz > 1) {
     const uint32_t grid = (uint32_t)std::min<uint64_t>((nnz + kThreads - 1) / kThreads, ws.num_sms * 8);
+    c.pre();
     k_is_sorted<<<grid, kThreads, 0, c.st>>>(d_coords, rank, nnz, ml, c.err);
-    c.launched();
+    c.launched(kOtherK);
   }
   QD_CUDA(cudaMemcpyAsync(ws.h_err, c.err, sizeof(ErrBlock), cudaMemcpyDeviceToHost, c.st));
   QD_CUDA(cudaStreamSynchronize(c.st));
@@ -1394,9 +1500,10 @@ void mode_histogram_device(Workspace& ws, uint32_t rank, uint64_t nnz, const uin
   Ctx c = make_ctx(ws, stream);
   if (nnz) {
     const uint32_t grid = (uint32_t)std::min<uint64_t>((nnz + kThreads - 1) / kThreads, ws.num_sms * 8);
+    c.pre();
     k_mode_hist<<<grid, kThreads, 0, c.st>>>(d_coords, rank, nnz, mode, dim,
                                               reinterpret_cast<unsigned long long*>(d_hist));
-    c.launched();
+    c.launched(kOtherK);
   }
   QD_CUDA(cudaStreamSynchronize(c.st));
 }
@@ -1429,8 +1536,9 @@ void partition_rows_device(Workspace& ws, uint32_t rank, uint64_t nnz, const uin
   h.dig[0] = dig;
   h.err = c.err;
   const uint32_t grid = (uint32_t)std::min<uint64_t>(ws.num_sms * 4, (nnz + 4095) / 4096);
+  c.pre();
   k_hist<<<grid, kThreads, 0, c.st>>>(h);
-  c.launched();
+  c.launched(kHistK);
   auto* status = status_buffer(c, num_tiles);
   PassArgs a{};
   a.in_c = d_c_in;

@@ -64,6 +64,10 @@ Workspace* workspace_create(int device);
 void workspace_destroy(Workspace* ws);
 uint64_t workspace_bytes(const Workspace* ws);
 uint64_t workspace_launches(const Workspace* ws);
+void workspace_profile(Workspace* ws, int enable);
+void workspace_profile_reset(Workspace* ws);
+bool workspace_profile_get(const Workspace* ws, int cls, uint64_t* launches, double* ms,
+                           double* bytes);
 
 struct TensorView {
   uint32_t rank;

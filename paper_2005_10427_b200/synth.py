@@ -127,3 +127,81 @@ def generate(cfg: Config, nnz: Optional[int] = None, seed: Optional[int] = None)
         perm = np.lexsort(sel.T[::-1])
     sel, values = sel[perm], values[perm]
     return np.ascontiguousarray(sel).reshape(-1), values
+
+
+def generate_torch(cfg: Config, nnz: Optional[int] = None, seed: Optional[int] = None,
+                   device: str = "cuda"):
+    """Same rules as generate(), drawn with torch's Philox generator on `device`
+    (fast for the 77M-1.7B row configs).  Returns (coords int32 [N*r],
+    values float64 [N]) as device tensors.  The stream differs from the numpy
+    one, so tests feed the SAME generated bytes to both implementations."""
+    import torch
+
+    n = cfg.nnz if nnz is None else int(nnz)
+    seed = cfg.seed if seed is None else seed
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    r = len(cfg.dims)
+    cdfs = [torch.from_numpy(_zipf_cdf(d, cfg.s)).to(device) if k == "zipf" else None
+            for d, k in zip(cfg.dims, cfg.dist)]
+    centres = None
+    if "cluster" in cfg.dist:
+        centres = torch.stack([torch.rand(cfg.clusters, generator=g, device=device,
+                                          dtype=torch.float64) * d for d in cfg.dims], 1)
+    prod = 1
+    for d in cfg.dims:
+        prod *= d
+    mixed = prod < 2**63
+
+    def draw(m):
+        out = torch.empty((m, r), dtype=torch.int64, device=device)
+        if centres is not None:
+            pick = torch.randint(0, cfg.clusters, (m,), generator=g, device=device)
+        for j, (d, kind) in enumerate(zip(cfg.dims, cfg.dist)):
+            if kind == "zipf":
+                u = torch.rand(m, generator=g, device=device, dtype=torch.float64)
+                out[:, j] = torch.searchsorted(cdfs[j], u, right=True).clamp_(max=d - 1)
+            elif kind == "uniform":
+                out[:, j] = torch.randint(0, d, (m,), generator=g, device=device)
+            else:
+                x = centres[pick, j] + torch.randn(m, generator=g, device=device,
+                                                   dtype=torch.float64) * (cfg.sigma * d)
+                out[:, j] = torch.round(x).clamp_(0, d - 1).to(torch.int64)
+        return out
+
+    def lex_order(rows):
+        """Stable permutation sorting rows lexicographically (mode 0 first)."""
+        if mixed:
+            key = torch.zeros(len(rows), dtype=torch.int64, device=device)
+            for j, d in enumerate(cfg.dims):
+                key = key * d + rows[:, j]
+            return torch.sort(key, stable=True).indices, key
+        perm = torch.arange(len(rows), device=device)
+        for j in reversed(range(r)):
+            perm = perm[torch.sort(rows[perm, j], stable=True).indices]
+        return perm, None
+
+    rows = draw(int(n * 1.3) + 1024)
+    while True:
+        perm, key = lex_order(rows)
+        s = rows[perm]
+        if key is not None:
+            ks = key[perm]
+            head = torch.ones(len(ks), dtype=torch.bool, device=device)
+            head[1:] = ks[1:] != ks[:-1]
+        else:
+            head = torch.ones(len(s), dtype=torch.bool, device=device)
+            head[1:] = (s[1:] != s[:-1]).any(1)
+        first = perm[head]          # draw index of each distinct row (stable sort)
+        if len(first) >= n:
+            break
+        rows = torch.cat([rows, draw(int((n - len(first)) * 2) + 1024)])
+    chosen = torch.sort(first).values[:n]
+    sel = rows[chosen]
+    if cfg.values == "lognormal":
+        values = torch.randn(n, generator=g, device=device, dtype=torch.float64).exp_()
+    else:
+        values = torch.rand(n, generator=g, device=device, dtype=torch.float64)
+    perm, _ = lex_order(sel)
+    sel, values = sel[perm], values[perm]
+    return sel.to(torch.int32).reshape(-1).contiguous(), values.contiguous()
