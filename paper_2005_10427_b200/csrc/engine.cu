@@ -39,8 +39,10 @@ namespace qb200 {
       throw Error(QD_CUDA_ERROR, std::string(#x) + ": " + cudaGetErrorString(e_)); \
   } while (0)
 
-constexpr int kThreads = 256;
+constexpr int kThreads = 256;       // utility kernels
 constexpr int kWarps = kThreads / 32;
+constexpr int kSortThreads = 512;   // k_onesweep / k_local
+constexpr int kSortWarps = kSortThreads / 32;
 constexpr int kRadixLog = 8;
 constexpr int kBins = 1 << kRadixLog;
 constexpr int kMaxTerms = 12;
@@ -149,9 +151,9 @@ __device__ __forceinline__ uint32_t digit_of(const uint32_t* row, const DigitSpe
     uint32_t c = row[d.lookup_mode];
     return c < d.lookup_dim ? __ldg(d.lookup + c) : 0u;
   }
-  uint32_t v = 0;
+  uint32_t v = ((row[d.mode[0]] >> d.rsh[0]) & ((1u << d.bits[0]) - 1u)) << d.lsh[0];
 #pragma unroll 1
-  for (uint32_t i = 0; i < d.n; ++i)
+  for (uint32_t i = 1; i < d.n; ++i)
     v |= ((row[d.mode[i]] >> d.rsh[i]) & ((1u << d.bits[i]) - 1u)) << d.lsh[i];
   return v;
 }
@@ -195,9 +197,11 @@ __device__ __forceinline__ unsigned long long enc(unsigned long long flag, uint3
   return flag | ((unsigned long long)(epoch & 0x3FFFu) << 48) | v;
 }
 
-// Exclusive scan across the block of one value per thread.
+// Exclusive scan across the block of one value per thread (NT threads).
+template <int NT = kThreads>
 __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_tmp,
                                                     uint32_t* total = nullptr) {
+  constexpr int kWarps = NT / 32;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   uint32_t x = v;
 #pragma unroll
@@ -225,8 +229,10 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_tmp,
 }
 
 // Same for 64-bit values.
+template <int NT = kThreads>
 __device__ __forceinline__ unsigned long long block_excl_scan64(unsigned long long v,
                                                                 unsigned long long* s_tmp) {
+  constexpr int kWarps = NT / 32;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   unsigned long long x = v;
 #pragma unroll
@@ -251,7 +257,21 @@ __device__ __forceinline__ unsigned long long block_excl_scan64(unsigned long lo
   return before + x - v;
 }
 
-// Stable per-warp ranking of positions [0, n): positions are cut into kWarps
+// Lanes of the warp whose digit equals this lane's (digits < 2^BITS), by
+// BITS ballots; cheaper than MATCH.ANY on sm_100.  Only lanes in `valid` count.
+template <int BITS = kRadixLog>
+__device__ __forceinline__ unsigned warp_peers(uint32_t d, unsigned valid) {
+  unsigned m = valid;
+#pragma unroll
+  for (int b = 0; b < BITS; ++b) {
+    const unsigned bit = (d >> b) & 1u;
+    const unsigned v = __ballot_sync(0xFFFFFFFFu, bit);
+    m &= bit ? v : ~v;
+  }
+  return m;
+}
+
+// Stable per-warp ranking of positions [0, n): positions are cut into NW
 // contiguous stripes of `ipw`; warp w walks its stripe in rounds of 32, so
 // rank order = position order.  s_rank[p] = rank of p among equal digits
 // earlier in its stripe; s_whist[w][d] = count of digit d in stripe w.
@@ -262,25 +282,29 @@ __device__ __forceinline__ void warp_rank(F get_digit, uint32_t n, uint32_t ipw,
   uint32_t* wh = s_whist + w * kBins;
   const uint32_t lo = w * ipw;
   const uint32_t hi = min(n, lo + ipw);
+  const unsigned below = (1u << lane) - 1u;
   for (uint32_t base = lo; base < hi; base += 32) {
     const uint32_t p = base + lane;
     const bool valid = p < hi;
-    const uint32_t d = valid ? get_digit(p) : 0xFFFFFFFFu;
-    const unsigned peers = __match_any_sync(0xFFFFFFFFu, d);
+    const uint32_t d = valid ? get_digit(p) : 0u;
+    unsigned peers = warp_peers(d, __ballot_sync(0xFFFFFFFFu, valid));
+    if (!valid) peers = 1u << lane;
     const int leader = __ffs(peers) - 1;
     uint32_t b = 0;
     if (valid && lane == leader) {
       b = wh[d];
       wh[d] = b + __popc(peers);
     }
-    b = __shfl_sync(0xFFFFFFFFu, b, leader);
-    if (valid) s_rank[p] = (uint16_t)(b + __popc(peers & ((1u << lane) - 1u)));
+    b = __shfl_sync(0xFFFFFFFFu, b, leader);  // leader's old count
+    if (valid) s_rank[p] = (uint16_t)(b + __popc(peers & below));
   }
 }
 
 // Turn per-warp counts into per-bin warp-exclusive offsets; s_cnt[b] = total.
+template <int NT = kThreads>
 __device__ __forceinline__ void bin_totals(uint32_t* s_whist, uint32_t* s_cnt) {
-  for (int b = threadIdx.x; b < kBins; b += kThreads) {
+  constexpr int kWarps = NT / 32;
+  for (int b = threadIdx.x; b < kBins; b += NT) {
     uint32_t run = 0;
 #pragma unroll
     for (int w = 0; w < kWarps; ++w) {
@@ -294,6 +318,7 @@ __device__ __forceinline__ void bin_totals(uint32_t* s_whist, uint32_t* s_cnt) {
 
 // Load words [a, a+nw) of g into s_raw so that word a+k lands at
 // s_raw[(a & 3) + k]; 16-byte vector loads for the aligned body.
+template <int NT = kThreads>
 __device__ __forceinline__ void load_words(uint32_t* s_raw, const uint32_t* g,
                                            unsigned long long a, uint32_t nw) {
   const uint32_t h = (uint32_t)(a & 3ull);
@@ -302,11 +327,13 @@ __device__ __forceinline__ void load_words(uint32_t* s_raw, const uint32_t* g,
   const uint32_t nvec = total >> 2;
   const uint4* gv = reinterpret_cast<const uint4*>(gb);
   uint4* sv = reinterpret_cast<uint4*>(s_raw);
-  for (uint32_t v = threadIdx.x; v < nvec; v += kThreads) sv[v] = __ldcs(gv + v);
-  for (uint32_t w = (nvec << 2) + threadIdx.x; w < total; w += kThreads) s_raw[w] = __ldcs(gb + w);
+#pragma unroll 4
+  for (uint32_t v = threadIdx.x; v < nvec; v += NT) sv[v] = __ldcs(gv + v);
+  for (uint32_t w = (nvec << 2) + threadIdx.x; w < total; w += NT) s_raw[w] = __ldcs(gb + w);
 }
 
 // Same for doubles: element a+k lands at s_raw[(a & 1) + k].
+template <int NT = kThreads>
 __device__ __forceinline__ void load_doubles(double* s_raw, const double* g,
                                              unsigned long long a, uint32_t n) {
   const uint32_t h = (uint32_t)(a & 1ull);
@@ -315,8 +342,9 @@ __device__ __forceinline__ void load_doubles(double* s_raw, const double* g,
   const uint32_t nvec = total >> 1;
   const double2* gv = reinterpret_cast<const double2*>(gb);
   double2* sv = reinterpret_cast<double2*>(s_raw);
-  for (uint32_t v = threadIdx.x; v < nvec; v += kThreads) sv[v] = __ldcs(gv + v);
-  for (uint32_t w = (nvec << 1) + threadIdx.x; w < total; w += kThreads) s_raw[w] = __ldcs(gb + w);
+#pragma unroll 4
+  for (uint32_t v = threadIdx.x; v < nvec; v += NT) sv[v] = __ldcs(gv + v);
+  for (uint32_t w = (nvec << 1) + threadIdx.x; w < total; w += NT) s_raw[w] = __ldcs(gb + w);
 }
 
 __device__ __forceinline__ void store_row(uint32_t* out_c, double* out_v, uint32_t rank,
@@ -340,7 +368,7 @@ struct SweepLayout {
     dig = o; o += align16(size_t(T) * 2);
     rnk = o; o += align16(size_t(T) * 2);
     sorted = o; o += align16(size_t(T) * 2);
-    whist = o; o += align16(size_t(kWarps) * kBins * 4);
+    whist = o; o += align16(size_t(kSortWarps) * kBins * 4);
     cnt = o; o += align16(kBins * 4);
     start = o; o += align16(kBins * 4);
     gbase = o; o += align16(kBins * 8);
@@ -352,7 +380,7 @@ struct SweepLayout {
 // ---------------------------------------------------------------------------
 // k_onesweep: one stable counting pass over one radix digit
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kThreads) k_onesweep(PassArgs a) {
+__global__ void __launch_bounds__(kSortThreads) k_onesweep(PassArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const SweepLayout L(a.T, a.rank);
   uint32_t* s_craw = reinterpret_cast<uint32_t*>(smem + L.c);
@@ -368,7 +396,7 @@ __global__ void __launch_bounds__(kThreads) k_onesweep(PassArgs a) {
   __shared__ uint32_t s_tile;
 
   if (threadIdx.x == 0) s_tile = atomicAdd(a.tile_counter, 1u);
-  for (int k = threadIdx.x; k < kWarps * kBins; k += kThreads) s_whist[k] = 0;
+  for (int k = threadIdx.x; k < kSortWarps * kBins; k += kSortThreads) s_whist[k] = 0;
   __syncthreads();
   const uint32_t tile = s_tile;
   if (tile >= a.num_tiles) return;
@@ -390,37 +418,38 @@ __global__ void __launch_bounds__(kThreads) k_onesweep(PassArgs a) {
   }
   const uint32_t R = a.rank;
   const uint32_t ch = (uint32_t)((rb * R) & 3ull), vh = (uint32_t)(rb & 1ull);
-  load_words(s_craw, a.in_c, rb * R, n * R);
-  load_doubles(s_vraw, a.in_v, rb, n);
+  load_words<kSortThreads>(s_craw, a.in_c, rb * R, n * R);
+  load_doubles<kSortThreads>(s_vraw, a.in_v, rb, n);
   __syncthreads();
   const uint32_t* s_c = s_craw + ch;
   const double* s_v = s_vraw + vh;
 
-  for (uint32_t i = threadIdx.x; i < n; i += kThreads)
+  for (uint32_t i = threadIdx.x; i < n; i += kSortThreads)
     s_dig[i] = (uint16_t)digit_of(s_c + (size_t)i * R, a.dig);
   __syncthreads();
 
-  const uint32_t ipw = a.T / kWarps;
+  const uint32_t ipw = a.T / kSortWarps;
   warp_rank([&](uint32_t p) { return (uint32_t)s_dig[p]; }, n, ipw, s_rank, s_whist);
   __syncthreads();
-  bin_totals(s_whist, s_cnt);
+  bin_totals<kSortThreads>(s_whist, s_cnt);
   __syncthreads();
 
   // Publish this tile's per-digit counts as early as possible.
   unsigned long long* st = a.status + (size_t)tile * kBins;
-  for (int b = threadIdx.x; b < kBins; b += kThreads)
+  for (int b = threadIdx.x; b < kBins; b += kSortThreads)
     st_relaxed(st + b, enc(first ? kFlagPre : kFlagAgg, a.epoch, s_cnt[b]));
 
   // Tile-local and run-level exclusive digit offsets.
-  const uint32_t cnt = s_cnt[threadIdx.x];
-  const uint32_t start = block_excl_scan(cnt, reinterpret_cast<uint32_t*>(s_tmp));
-  s_start[threadIdx.x] = start;
-  const uint32_t h = a.hist[(size_t)li * a.hist_stride + threadIdx.x];
-  const unsigned long long run_off = block_excl_scan64(h, s_tmp);
+  const bool binthr = threadIdx.x < kBins;
+  const uint32_t cnt = binthr ? s_cnt[threadIdx.x] : 0u;
+  const uint32_t start = block_excl_scan<kSortThreads>(cnt, reinterpret_cast<uint32_t*>(s_tmp));
+  if (binthr) s_start[threadIdx.x] = start;
+  const uint32_t h = binthr ? a.hist[(size_t)li * a.hist_stride + threadIdx.x] : 0u;
+  const unsigned long long run_off = block_excl_scan64<kSortThreads>(h, s_tmp);
   const unsigned long long base = a.run_start ? a.run_start[li] : 0ull;
 
   // Decoupled look-back over the preceding tiles of the same run.
-  {
+  if (binthr) {
     const int b = threadIdx.x;
     unsigned long long excl = 0;
     if (!first) {
@@ -442,14 +471,14 @@ __global__ void __launch_bounds__(kThreads) k_onesweep(PassArgs a) {
   }
   __syncthreads();
 
-  for (uint32_t i = threadIdx.x; i < n; i += kThreads) {
+  for (uint32_t i = threadIdx.x; i < n; i += kSortThreads) {
     const uint32_t d = s_dig[i];
     const uint32_t pos = s_start[d] + s_whist[(i / ipw) * kBins + d] + s_rank[i];
     s_sorted[pos] = (uint16_t)i;
   }
   __syncthreads();
 
-  for (uint32_t j = threadIdx.x; j < n; j += kThreads) {
+  for (uint32_t j = threadIdx.x; j < n; j += kSortThreads) {
     const uint32_t i = s_sorted[j];
     const unsigned long long dst = (unsigned long long)(s_gbase[s_dig[i]] + j);
     store_row(a.out_c, a.out_v, R, dst, s_c + (size_t)i * R, s_v[i]);
@@ -460,35 +489,47 @@ __global__ void __launch_bounds__(kThreads) k_onesweep(PassArgs a) {
 // k_hist: per-run digit histograms of np passes + range check
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads) k_hist(HistArgs a) {
-  __shared__ uint32_t s_h[kHistPasses * kBins];
-  for (int k = threadIdx.x; k < kHistPasses * kBins; k += kThreads) s_h[k] = 0;
+  // per-warp private histograms [kWarps][np][kBins]: one leader per digit per
+  // round updates them, so no atomics; folded into global at each flush
+  extern __shared__ uint32_t s_h[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t per_warp = a.np * kBins;
+  for (uint32_t k = threadIdx.x; k < kWarps * per_warp; k += kThreads) s_h[k] = 0;
   __syncthreads();
-  const int lane = threadIdx.x & 31;
+  uint32_t* wh = s_h + w * per_warp;
   int cur_li = -1;
   auto flush = [&](int li) {
     __syncthreads();
     if (li >= 0) {
       uint32_t* g = a.hist + (size_t)li * a.hist_stride + (size_t)a.pass0 * kBins;
-      for (uint32_t k = threadIdx.x; k < a.np * kBins; k += kThreads) {
-        const uint32_t v = s_h[k];
+      for (uint32_t k = threadIdx.x; k < per_warp; k += kThreads) {
+        uint32_t v = 0;
+#pragma unroll
+        for (int x = 0; x < kWarps; ++x) {
+          v += s_h[x * per_warp + k];
+          s_h[x * per_warp + k] = 0;
+        }
         if (v) atomicAdd(g + k, v);
-        s_h[k] = 0;
       }
     }
     __syncthreads();
   };
   auto count_rows = [&](unsigned long long rb, uint32_t n) {
     if (threadIdx.x == 0 && a.rows_counter) atomicAdd(a.rows_counter, (unsigned long long)n);
-    // whole warps iterate together so __match_any_sync sees full masks
-    for (uint32_t base = 0; base < n; base += kThreads) {
-      const uint32_t i = base + threadIdx.x;
+    for (uint32_t g = w * 32; g < n; g += kThreads) {  // warp-uniform
+      const uint32_t i = g + lane;
       const bool valid = i < n;
       const uint32_t* row = a.in_c + (size_t)(rb + (valid ? i : 0)) * a.rank;
       if (valid && a.do_check) check_row(row, a.key, rb + i, a.err);
-      for (uint32_t q = 0; q < a.np; ++q) {
-        const uint32_t d = valid ? digit_of(row, a.dig[q]) : 0xFFFFFFFFu;
-        const unsigned peers = __match_any_sync(0xFFFFFFFFu, d);
-        if (valid && lane == __ffs(peers) - 1) atomicAdd(&s_h[q * kBins + d], __popc(peers));
+      const unsigned vmask = __ballot_sync(0xFFFFFFFFu, valid);
+#pragma unroll
+      for (int q = 0; q < kHistPasses; ++q) {
+        if (q < (int)a.np) {
+          const uint32_t d = valid ? digit_of(row, a.dig[q]) : 0u;
+          const unsigned peers = warp_peers(d, vmask);
+          if (valid && lane == __ffs(peers) - 1) wh[q * kBins + d] += __popc(peers);
+          __syncwarp();
+        }
       }
     }
   };
@@ -529,7 +570,7 @@ struct LocalLayout {
     perm0 = o; o += align16(size_t(cap) * 2);
     perm1 = o; o += align16(size_t(cap) * 2);
     rnk = o; o += align16(size_t(cap) * 2);
-    whist = o; o += align16(size_t(kWarps) * kBins * 4);
+    whist = o; o += align16(size_t(kSortWarps) * kBins * 4);
     cnt = o; o += align16(kBins * 4);
     start = o; o += align16(kBins * 4);
     seg = o; o += align16((size_t(TL) + 2) * 8);
@@ -542,7 +583,7 @@ __device__ __forceinline__ uint32_t ceil_log2_dev(uint64_t x) {
   return x <= 1 ? 0u : 64u - (uint32_t)__clzll((long long)(x - 1));
 }
 
-__global__ void __launch_bounds__(kThreads) k_local(LocalArgs a) {
+__global__ void __launch_bounds__(kSortThreads) k_local(LocalArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const LocalLayout L(a.cap, a.rank, a.TL);
   uint32_t* s_craw = reinterpret_cast<uint32_t*>(smem + L.c);
@@ -586,7 +627,7 @@ __global__ void __launch_bounds__(kThreads) k_local(LocalArgs a) {
     __syncthreads();
     const uint64_t sa = s_sa;
     // runs sa .. sa+k starting in [lo, hi) and small; at most TL of them
-    for (uint32_t k = threadIdx.x; k <= a.TL; k += kThreads) {
+    for (uint32_t k = threadIdx.x; k <= a.TL; k += kSortThreads) {
       const uint64_t s = sa + k;
       bool stop = true;
       if (s < S) {
@@ -606,14 +647,14 @@ __global__ void __launch_bounds__(kThreads) k_local(LocalArgs a) {
   __syncthreads();
   const uint32_t n = (uint32_t)(r1 - r0);
   const uint32_t R = a.rank;
-  load_words(s_craw, a.in_c, r0 * R, n * R);
-  load_doubles(s_vraw, a.in_v, r0, n);
+  load_words<kSortThreads>(s_craw, a.in_c, r0 * R, n * R);
+  load_doubles<kSortThreads>(s_vraw, a.in_v, r0, n);
   __syncthreads();
   const uint32_t* s_c = s_craw + (uint32_t)((r0 * R) & 3ull);
   const double* s_v = s_vraw + (uint32_t)(r0 & 1ull);
 
   const uint32_t kb = a.key.total_bits;
-  for (uint32_t i = threadIdx.x; i < n; i += kThreads) {
+  for (uint32_t i = threadIdx.x; i < n; i += kSortThreads) {
     const uint32_t* row = s_c + (size_t)i * R;
     if (a.key.check) check_row(row, a.key, r0 + i, a.err);
     unsigned long long k = full_key(row, a.key);
@@ -632,21 +673,25 @@ __global__ void __launch_bounds__(kThreads) k_local(LocalArgs a) {
   }
   const uint32_t nbits = kb + ceil_log2_dev(nsl);
   const uint32_t passes = (nbits + kRadixLog - 1) / kRadixLog;
-  const uint32_t ipw = (n + kWarps - 1) / kWarps;
+  const uint32_t ipw = (n + kSortWarps - 1) / kSortWarps;
   uint16_t* cur = s_p0;
   uint16_t* nxt = s_p1;
   for (uint32_t q = 0; q < passes; ++q) {
     const uint32_t sh = q * kRadixLog;
-    for (int k = threadIdx.x; k < kWarps * kBins; k += kThreads) s_whist[k] = 0;
+    for (int k = threadIdx.x; k < kSortWarps * kBins; k += kSortThreads) s_whist[k] = 0;
     __syncthreads();
     warp_rank([&](uint32_t p) { return (uint32_t)((s_key[cur[p]] >> sh) & (kBins - 1)); }, n,
               ipw, s_rank, s_whist);
     __syncthreads();
-    bin_totals(s_whist, s_cnt);
+    bin_totals<kSortThreads>(s_whist, s_cnt);
     __syncthreads();
-    s_start[threadIdx.x] = block_excl_scan(s_cnt[threadIdx.x], s_tmp);
+    {
+      const uint32_t st = block_excl_scan<kSortThreads>(threadIdx.x < kBins ? s_cnt[threadIdx.x] : 0u,
+                                                        s_tmp);
+      if (threadIdx.x < kBins) s_start[threadIdx.x] = st;
+    }
     __syncthreads();
-    for (uint32_t p = threadIdx.x; p < n; p += kThreads) {
+    for (uint32_t p = threadIdx.x; p < n; p += kSortThreads) {
       const uint32_t it = cur[p];
       const uint32_t d = (uint32_t)((s_key[it] >> sh) & (kBins - 1));
       nxt[s_start[d] + s_whist[(p / ipw) * kBins + d] + s_rank[p]] = (uint16_t)it;
@@ -656,7 +701,7 @@ __global__ void __launch_bounds__(kThreads) k_local(LocalArgs a) {
     cur = nxt;
     nxt = t;
   }
-  for (uint32_t j = threadIdx.x; j < n; j += kThreads) {
+  for (uint32_t j = threadIdx.x; j < n; j += kSortThreads) {
     const uint32_t i = cur[j];
     store_row(a.out_c, a.out_v, R, r0 + j, s_c + (size_t)i * R, s_v[i]);
   }
@@ -944,6 +989,7 @@ Workspace* workspace_create(int device) {
   };
   allow_smem(reinterpret_cast<const void*>(k_onesweep));
   allow_smem(reinterpret_cast<const void*>(k_local));
+  allow_smem(reinterpret_cast<const void*>(k_hist));
   ws->smem_optin = optin - 1024;  // dynamic budget below the static usage
   return ws;
 }
@@ -1170,7 +1216,7 @@ void launch_pass(Ctx& c, PassArgs& a) {
   a.tile_counter = c.counters + c.next_counter++;
   const size_t smem = SweepLayout(a.T, a.rank).total;
   c.pre();
-  k_onesweep<<<a.num_tiles, kThreads, smem, c.st>>>(a);
+  k_onesweep<<<a.num_tiles, kSortThreads, smem, c.st>>>(a);
   c.launched(kSweep);
 }
 
@@ -1234,7 +1280,7 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
       LocalArgs la{src_c, src_v, dst_c, dst_v, R, N, TL, (uint32_t)N, nullptr, 1, key, c.err};
       const size_t smem = LocalLayout((uint32_t)N, R, TL).total;
       c.pre();
-      k_local<<<1, kThreads, smem, c.st>>>(la);
+      k_local<<<1, kSortThreads, smem, c.st>>>(la);
       c.launched(kLocalK, 1);
       return;
     }
@@ -1275,7 +1321,7 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
       const size_t smem = LocalLayout(2 * TL, R, TL).total;
       const uint64_t chunks = (N + TL - 1) / TL;
       c.pre();
-      k_local<<<(uint32_t)chunks, kThreads, smem, c.st>>>(la);
+      k_local<<<(uint32_t)chunks, kSortThreads, smem, c.st>>>(la);
       c.launched(kLocalK);
     }
   }
@@ -1307,10 +1353,10 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
       h.tiles_per_cta = (uint32_t)std::max<uint64_t>(1, (num_tiles + grid - 1) / grid);
       grid = (uint32_t)((num_tiles + h.tiles_per_cta - 1) / h.tiles_per_cta);
     } else {
-      grid = (uint32_t)std::min<uint64_t>(grid, (N + 4095) / 4096);
+      grid = (uint32_t)std::min<uint64_t>(ws.num_sms * 8, (N + 4095) / 4096);
     }
     c.pre();
-    k_hist<<<grid, kThreads, 0, c.st>>>(h);
+    k_hist<<<grid, kThreads, (size_t)kWarps * h.np * kBins * 4, c.st>>>(h);
     c.launched(kHistK);
   }
 
@@ -1537,7 +1583,7 @@ void partition_rows_device(Workspace& ws, uint32_t rank, uint64_t nnz, const uin
   h.err = c.err;
   const uint32_t grid = (uint32_t)std::min<uint64_t>(ws.num_sms * 4, (nnz + 4095) / 4096);
   c.pre();
-  k_hist<<<grid, kThreads, 0, c.st>>>(h);
+  k_hist<<<grid, kThreads, (size_t)kWarps * h.np * kBins * 4, c.st>>>(h);
   c.launched(kHistK);
   auto* status = status_buffer(c, num_tiles);
   PassArgs a{};
