@@ -125,6 +125,10 @@ struct HistArgs {
   int do_check;
   ErrBlock* err;
   unsigned long long* rows_counter;  // += rows histogrammed (pass0 == 0 only)
+  // fast path (combined key fits 64 bits, no lookup digit): digit q of a row
+  // is (full_key >> shift[q]) & mask[q]
+  int fast;
+  uint32_t shift[kHistPasses], mask[kHistPasses];
 };
 
 struct LocalArgs {
@@ -277,9 +281,9 @@ __device__ __forceinline__ unsigned warp_peers(uint32_t d, unsigned valid) {
 // earlier in its stripe; s_whist[w][d] = count of digit d in stripe w.
 template <class F>
 __device__ __forceinline__ void warp_rank(F get_digit, uint32_t n, uint32_t ipw,
-                                          uint16_t* s_rank, uint32_t* s_whist) {
+                                          uint16_t* s_rank, uint16_t* s_whist) {
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint32_t* wh = s_whist + w * kBins;
+  uint16_t* wh = s_whist + w * kBins;
   const uint32_t lo = w * ipw;
   const uint32_t hi = min(n, lo + ipw);
   const unsigned below = (1u << lane) - 1u;
@@ -293,7 +297,7 @@ __device__ __forceinline__ void warp_rank(F get_digit, uint32_t n, uint32_t ipw,
     uint32_t b = 0;
     if (valid && lane == leader) {
       b = wh[d];
-      wh[d] = b + __popc(peers);
+      wh[d] = (uint16_t)(b + __popc(peers));
     }
     b = __shfl_sync(0xFFFFFFFFu, b, leader);  // leader's old count
     if (valid) s_rank[p] = (uint16_t)(b + __popc(peers & below));
@@ -302,14 +306,14 @@ __device__ __forceinline__ void warp_rank(F get_digit, uint32_t n, uint32_t ipw,
 
 // Turn per-warp counts into per-bin warp-exclusive offsets; s_cnt[b] = total.
 template <int NT = kThreads>
-__device__ __forceinline__ void bin_totals(uint32_t* s_whist, uint32_t* s_cnt) {
+__device__ __forceinline__ void bin_totals(uint16_t* s_whist, uint32_t* s_cnt) {
   constexpr int kWarps = NT / 32;
   for (int b = threadIdx.x; b < kBins; b += NT) {
     uint32_t run = 0;
 #pragma unroll
     for (int w = 0; w < kWarps; ++w) {
       const uint32_t c = s_whist[w * kBins + b];
-      s_whist[w * kBins + b] = run;
+      s_whist[w * kBins + b] = (uint16_t)run;
       run += c;
     }
     s_cnt[b] = run;
@@ -358,130 +362,240 @@ __device__ __forceinline__ void store_row(uint32_t* out_c, double* out_v, uint32
 
 __host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
-// Shared-memory layout of k_onesweep for T rows of `rank` coordinates.
+// ---- TMA bulk copies (cp.async.bulk) completing on an mbarrier ----------
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "QD_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra QD_WAIT_%=;\n}" ::"r"(smem_addr(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+
+// A byte span [g, g+len) of global memory staged at dst so that byte g+k
+// lands at dst[head + k]: 16-byte aligned bulk body + (< 16 B) tail.
+struct Stage {
+  const char* gal;  // 16-byte aligned start
+  uint32_t head;    // g - gal
+  uint32_t bulk;    // bytes moved by TMA from gal
+  uint32_t tail;    // bytes after the bulk body, loaded by threads
+};
+__device__ __forceinline__ Stage make_stage(const void* g, uint32_t len) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(g);
+  Stage s;
+  s.gal = reinterpret_cast<const char*>(a & ~uintptr_t(15));
+  s.head = (uint32_t)(a & 15);
+  const uint32_t total = s.head + len;
+  s.bulk = total & ~15u;
+  s.tail = total - s.bulk;
+  return s;
+}
+
+// Shared-memory layout of k_onesweep: two row buffers (double buffering) of T
+// rows plus the ranking / offset scratch.
 struct SweepLayout {
-  size_t c, v, dig, rnk, sorted, whist, cnt, start, gbase, tmp, total;
+  size_t cbuf, vbuf, c0, v0, dig, rnk, sorted, whist, cnt, start, gbase, tmp, bar, total;
   __host__ __device__ SweepLayout(uint32_t T, uint32_t rank) {
     size_t o = 0;
-    c = o; o += align16((size_t(T) * rank + 4) * 4);
-    v = o; o += align16((size_t(T) + 2) * 8);
+    cbuf = align16(size_t(T) * rank * 4 + 32);
+    vbuf = align16(size_t(T) * 8 + 32);
+    c0 = o; o += 2 * cbuf;  // coordinate buffers 0, 1
+    v0 = o; o += 2 * vbuf;  // value buffers 0, 1
     dig = o; o += align16(size_t(T) * 2);
     rnk = o; o += align16(size_t(T) * 2);
     sorted = o; o += align16(size_t(T) * 2);
-    whist = o; o += align16(size_t(kSortWarps) * kBins * 4);
+    whist = o; o += align16(size_t(kSortWarps) * kBins * 2);
     cnt = o; o += align16(kBins * 4);
     start = o; o += align16(kBins * 4);
     gbase = o; o += align16(kBins * 8);
     tmp = o; o += align16(64 * 8);
+    bar = o; o += 16;
     total = o;
   }
 };
 
+struct TileInfo {
+  unsigned long long rb;
+  uint32_t n, li, first;
+};
+
+__device__ __forceinline__ TileInfo tile_info(const PassArgs& a, uint32_t tile) {
+  TileInfo t;
+  if (a.tiles) {
+    const TileDesc d = a.tiles[tile];
+    t.rb = d.row_begin;
+    t.n = d.len;
+    t.li = d.li_first >> 1;
+    t.first = d.li_first & 1u;
+  } else {
+    t.rb = (unsigned long long)tile * a.T;
+    t.n = (uint32_t)min((unsigned long long)a.T, a.nnz - t.rb);
+    t.li = 0;
+    t.first = tile == 0;
+  }
+  return t;
+}
+
 // ---------------------------------------------------------------------------
-// k_onesweep: one stable counting pass over one radix digit
+// k_onesweep: one stable counting pass over one radix digit.  Persistent CTAs
+// take tiles in order from a global counter; thread 0 prefetches the NEXT
+// tile's rows with TMA bulk copies into the other buffer while the CTA ranks,
+// looks back and scatters the current one.  RT = compile-time rank (0: any).
 // ---------------------------------------------------------------------------
+template <int RT>
 __global__ void __launch_bounds__(kSortThreads) k_onesweep(PassArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const SweepLayout L(a.T, a.rank);
-  uint32_t* s_craw = reinterpret_cast<uint32_t*>(smem + L.c);
-  double* s_vraw = reinterpret_cast<double*>(smem + L.v);
+  const uint32_t R = RT ? RT : a.rank;
+  const SweepLayout L(a.T, R);
   uint16_t* s_dig = reinterpret_cast<uint16_t*>(smem + L.dig);
   uint16_t* s_rank = reinterpret_cast<uint16_t*>(smem + L.rnk);
   uint16_t* s_sorted = reinterpret_cast<uint16_t*>(smem + L.sorted);
-  uint32_t* s_whist = reinterpret_cast<uint32_t*>(smem + L.whist);
+  uint16_t* s_whist = reinterpret_cast<uint16_t*>(smem + L.whist);
   uint32_t* s_cnt = reinterpret_cast<uint32_t*>(smem + L.cnt);
   uint32_t* s_start = reinterpret_cast<uint32_t*>(smem + L.start);
   long long* s_gbase = reinterpret_cast<long long*>(smem + L.gbase);
   unsigned long long* s_tmp = reinterpret_cast<unsigned long long*>(smem + L.tmp);
-  __shared__ uint32_t s_tile;
+  unsigned long long* s_bar = reinterpret_cast<unsigned long long*>(smem + L.bar);
+  __shared__ uint32_t s_next;
 
-  if (threadIdx.x == 0) s_tile = atomicAdd(a.tile_counter, 1u);
-  for (int k = threadIdx.x; k < kSortWarps * kBins; k += kSortThreads) s_whist[k] = 0;
-  __syncthreads();
-  const uint32_t tile = s_tile;
-  if (tile >= a.num_tiles) return;
+  // thread 0: claim the next tile and start its bulk loads into buffer b
+  auto prefetch = [&](uint32_t b) {
+    const uint32_t t = atomicAdd(a.tile_counter, 1u);
+    s_next = t;
+    if (t < a.num_tiles) {
+      const TileInfo ti = tile_info(a, t);
+      const Stage sc = make_stage(a.in_c + ti.rb * R, ti.n * R * 4);
+      const Stage sv = make_stage(a.in_v + ti.rb, ti.n * 8);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect_tx(&s_bar[b], sc.bulk + sv.bulk);
+      if (sc.bulk) bulk_g2s(smem + L.c0 + b * L.cbuf, sc.gal, sc.bulk, &s_bar[b]);
+      if (sv.bulk) bulk_g2s(smem + L.v0 + b * L.vbuf, sv.gal, sv.bulk, &s_bar[b]);
+    }
+  };
 
-  unsigned long long rb;
-  uint32_t n, li;
-  bool first;
-  if (a.tiles) {
-    const TileDesc d = a.tiles[tile];
-    rb = d.row_begin;
-    n = d.len;
-    li = d.li_first >> 1;
-    first = d.li_first & 1u;
-  } else {
-    rb = (unsigned long long)tile * a.T;
-    n = (uint32_t)min((unsigned long long)a.T, a.nnz - rb);
-    li = 0;
-    first = tile == 0;
+  if (threadIdx.x == 0) {
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  const uint32_t R = a.rank;
-  const uint32_t ch = (uint32_t)((rb * R) & 3ull), vh = (uint32_t)(rb & 1ull);
-  load_words<kSortThreads>(s_craw, a.in_c, rb * R, n * R);
-  load_doubles<kSortThreads>(s_vraw, a.in_v, rb, n);
   __syncthreads();
-  const uint32_t* s_c = s_craw + ch;
-  const double* s_v = s_vraw + vh;
-
-  for (uint32_t i = threadIdx.x; i < n; i += kSortThreads)
-    s_dig[i] = (uint16_t)digit_of(s_c + (size_t)i * R, a.dig);
+  if (threadIdx.x == 0) prefetch(0);
   __syncthreads();
 
   const uint32_t ipw = a.T / kSortWarps;
-  warp_rank([&](uint32_t p) { return (uint32_t)s_dig[p]; }, n, ipw, s_rank, s_whist);
-  __syncthreads();
-  bin_totals<kSortThreads>(s_whist, s_cnt);
-  __syncthreads();
+  uint32_t phases = 0u;  // bit b: parity of buffer b's barrier
+  for (uint32_t it = 0;; ++it) {
+    const uint32_t b = it & 1u;
+    const uint32_t tile = s_next;
+    if (tile >= a.num_tiles) break;
+    __syncthreads();  // everyone has read s_next
+    if (threadIdx.x == 0) prefetch(b ^ 1u);
+    for (int k = threadIdx.x; k < kSortWarps * kBins; k += kSortThreads) s_whist[k] = 0;
 
-  // Publish this tile's per-digit counts as early as possible.
-  unsigned long long* st = a.status + (size_t)tile * kBins;
-  for (int b = threadIdx.x; b < kBins; b += kSortThreads)
-    st_relaxed(st + b, enc(first ? kFlagPre : kFlagAgg, a.epoch, s_cnt[b]));
+    const TileInfo ti = tile_info(a, tile);
+    const uint32_t n = ti.n;
+    const Stage sc = make_stage(a.in_c + ti.rb * R, n * R * 4);
+    const Stage sv = make_stage(a.in_v + ti.rb, n * 8);
+    mbar_wait(&s_bar[b], (phases >> b) & 1u);
+    phases ^= 1u << b;
+    // sub-16-byte tails of the spans
+    if (threadIdx.x < sc.tail / 4)
+      reinterpret_cast<uint32_t*>(smem + L.c0 + b * L.cbuf + sc.bulk)[threadIdx.x] =
+          reinterpret_cast<const uint32_t*>(sc.gal + sc.bulk)[threadIdx.x];
+    if (threadIdx.x == 32 && sv.tail)
+      *reinterpret_cast<double*>(smem + L.v0 + b * L.vbuf + sv.bulk) =
+          *reinterpret_cast<const double*>(sv.gal + sv.bulk);
+    const uint32_t* s_c = reinterpret_cast<const uint32_t*>(smem + L.c0 + b * L.cbuf + sc.head);
+    const double* s_v = reinterpret_cast<const double*>(smem + L.v0 + b * L.vbuf + sv.head);
+    __syncthreads();
 
-  // Tile-local and run-level exclusive digit offsets.
-  const bool binthr = threadIdx.x < kBins;
-  const uint32_t cnt = binthr ? s_cnt[threadIdx.x] : 0u;
-  const uint32_t start = block_excl_scan<kSortThreads>(cnt, reinterpret_cast<uint32_t*>(s_tmp));
-  if (binthr) s_start[threadIdx.x] = start;
-  const uint32_t h = binthr ? a.hist[(size_t)li * a.hist_stride + threadIdx.x] : 0u;
-  const unsigned long long run_off = block_excl_scan64<kSortThreads>(h, s_tmp);
-  const unsigned long long base = a.run_start ? a.run_start[li] : 0ull;
+    for (uint32_t i = threadIdx.x; i < n; i += kSortThreads)
+      s_dig[i] = (uint16_t)digit_of(s_c + (size_t)i * R, a.dig);
+    __syncthreads();
 
-  // Decoupled look-back over the preceding tiles of the same run.
-  if (binthr) {
-    const int b = threadIdx.x;
-    unsigned long long excl = 0;
-    if (!first) {
-      long long p = (long long)tile - 1;
-      for (;;) {
-        const unsigned long long s = ld_relaxed(a.status + (size_t)p * kBins + b);
-        const unsigned long long flag = s & (3ull << 62);
-        if (flag == 0 || ((s >> 48) & 0x3FFFu) != (a.epoch & 0x3FFFu)) {
-          __nanosleep(32);
-          continue;
+    warp_rank([&](uint32_t p) { return (uint32_t)s_dig[p]; }, n, ipw, s_rank, s_whist);
+    __syncthreads();
+    bin_totals<kSortThreads>(s_whist, s_cnt);
+    __syncthreads();
+
+    // Publish this tile's per-digit counts as early as possible.
+    unsigned long long* st = a.status + (size_t)tile * kBins;
+    const bool binthr = threadIdx.x < kBins;
+    const uint32_t cnt = binthr ? s_cnt[threadIdx.x] : 0u;
+    if (binthr) st_relaxed(st + threadIdx.x, enc(ti.first ? kFlagPre : kFlagAgg, a.epoch, cnt));
+
+    // Tile-local and run-level exclusive digit offsets.
+    const uint32_t start = block_excl_scan<kSortThreads>(cnt, reinterpret_cast<uint32_t*>(s_tmp));
+    if (binthr) s_start[threadIdx.x] = start;
+    const uint32_t h = binthr ? a.hist[(size_t)ti.li * a.hist_stride + threadIdx.x] : 0u;
+    const unsigned long long run_off = block_excl_scan64<kSortThreads>(h, s_tmp);
+    const unsigned long long base = a.run_start ? a.run_start[ti.li] : 0ull;
+
+    // Decoupled look-back over the preceding tiles of the same run.
+    if (binthr) {
+      const int bb = threadIdx.x;
+      unsigned long long excl = 0;
+      if (!ti.first) {
+        long long p = (long long)tile - 1;
+        for (;;) {
+          const unsigned long long sw = ld_relaxed(a.status + (size_t)p * kBins + bb);
+          const unsigned long long flag = sw & (3ull << 62);
+          if (flag == 0 || ((sw >> 48) & 0x3FFFu) != (a.epoch & 0x3FFFu)) {
+            __nanosleep(20);
+            continue;
+          }
+          excl += sw & kValMask;
+          if (flag == kFlagPre) break;
+          --p;
         }
-        excl += s & kValMask;
-        if (flag == kFlagPre) break;
-        --p;
+        st_relaxed(st + bb, enc(kFlagPre, a.epoch, excl + cnt));
       }
-      st_relaxed(st + b, enc(kFlagPre, a.epoch, excl + cnt));
+      s_gbase[bb] = (long long)(base + run_off + excl) - (long long)start;
     }
-    s_gbase[b] = (long long)(base + run_off + excl) - (long long)start;
-  }
-  __syncthreads();
+    __syncthreads();
 
-  for (uint32_t i = threadIdx.x; i < n; i += kSortThreads) {
-    const uint32_t d = s_dig[i];
-    const uint32_t pos = s_start[d] + s_whist[(i / ipw) * kBins + d] + s_rank[i];
-    s_sorted[pos] = (uint16_t)i;
-  }
-  __syncthreads();
+    for (uint32_t i = threadIdx.x; i < n; i += kSortThreads) {
+      const uint32_t d = s_dig[i];
+      const uint32_t pos = s_start[d] + s_whist[(i / ipw) * kBins + d] + s_rank[i];
+      s_sorted[pos] = (uint16_t)i;
+    }
+    __syncthreads();
 
-  for (uint32_t j = threadIdx.x; j < n; j += kSortThreads) {
-    const uint32_t i = s_sorted[j];
-    const unsigned long long dst = (unsigned long long)(s_gbase[s_dig[i]] + j);
-    store_row(a.out_c, a.out_v, R, dst, s_c + (size_t)i * R, s_v[i]);
+    for (uint32_t j = threadIdx.x; j < n; j += kSortThreads) {
+      const uint32_t i = s_sorted[j];
+      const unsigned long long dst = (unsigned long long)(s_gbase[s_dig[i]] + j);
+      const uint32_t* src = s_c + (size_t)i * R;
+      uint32_t* o = a.out_c + dst * R;
+      if (RT) {
+#pragma unroll
+        for (int m = 0; m < RT; ++m) __stcs(o + m, src[m]);
+      } else {
+        for (uint32_t m = 0; m < R; ++m) __stcs(o + m, src[m]);
+      }
+      __stcs(a.out_v + dst, s_v[i]);
+    }
+    __syncthreads();  // buffer b and the scratch are free again
   }
 }
 
@@ -489,8 +603,8 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(PassArgs a) {
 // k_hist: per-run digit histograms of np passes + range check
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads) k_hist(HistArgs a) {
-  // per-warp private histograms [kWarps][np][kBins]: one leader per digit per
-  // round updates them, so no atomics; folded into global at each flush
+  // per-warp private histograms [kWarps][np][kBins] (shared-memory atomics
+  // only among one warp's run heads), folded into global at each flush
   extern __shared__ uint32_t s_h[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t per_warp = a.np * kBins;
@@ -514,22 +628,48 @@ __global__ void __launch_bounds__(kThreads) k_hist(HistArgs a) {
     }
     __syncthreads();
   };
+  // Runs of equal digits among the warp's 32 consecutive rows are counted by
+  // their head lane (sorted inputs make long runs common: Zipf heads).
+  auto add_runs = [&](uint32_t* h, uint32_t d, bool valid, uint32_t nvalid) {
+    const uint32_t prev = __shfl_up_sync(0xFFFFFFFFu, d, 1);
+    const bool head = valid && (lane == 0 || prev != d);
+    const unsigned heads = __ballot_sync(0xFFFFFFFFu, head);
+    if (head) {
+      const unsigned after = heads & ~((2u << lane) - 1u);
+      const uint32_t end = after ? (uint32_t)(__ffs(after) - 1) : nvalid;
+      atomicAdd(h + d, end - lane);
+    }
+  };
   auto count_rows = [&](unsigned long long rb, uint32_t n) {
     if (threadIdx.x == 0 && a.rows_counter) atomicAdd(a.rows_counter, (unsigned long long)n);
     for (uint32_t g = w * 32; g < n; g += kThreads) {  // warp-uniform
       const uint32_t i = g + lane;
       const bool valid = i < n;
+      const uint32_t nvalid = min(32u, n - g);
       const uint32_t* row = a.in_c + (size_t)(rb + (valid ? i : 0)) * a.rank;
-      if (valid && a.do_check) check_row(row, a.key, rb + i, a.err);
-      const unsigned vmask = __ballot_sync(0xFFFFFFFFu, valid);
-#pragma unroll
-      for (int q = 0; q < kHistPasses; ++q) {
-        if (q < (int)a.np) {
-          const uint32_t d = valid ? digit_of(row, a.dig[q]) : 0u;
-          const unsigned peers = warp_peers(d, vmask);
-          if (valid && lane == __ffs(peers) - 1) wh[q * kBins + d] += __popc(peers);
-          __syncwarp();
+      if (a.fast) {
+        // one pass over the key fields: range check + combined key
+        unsigned long long key = 0;
+#pragma unroll 1
+        for (uint32_t k = 0; k < a.key.n; ++k) {
+          const uint32_t c = valid ? __ldg(row + a.key.mode[k]) : 0u;
+          if (a.do_check && c >= a.key.dim[k]) {
+            atomicOr(&a.err->flags, 1u);
+            atomicMin(&a.err->rowmode, (unsigned long long)(((rb + i) << 6) | a.key.mode[k]));
+          }
+          const uint32_t wd = a.key.width[k];
+          key |= (unsigned long long)(c & (uint32_t)((1ull << wd) - 1ull)) << a.key.off[k];
         }
+#pragma unroll
+        for (int q = 0; q < kHistPasses; ++q)
+          if (q < (int)a.np)
+            add_runs(wh + q * kBins, (uint32_t)(key >> a.shift[q]) & a.mask[q], valid, nvalid);
+      } else {
+        if (valid && a.do_check) check_row(row, a.key, rb + i, a.err);
+#pragma unroll
+        for (int q = 0; q < kHistPasses; ++q)
+          if (q < (int)a.np)
+            add_runs(wh + q * kBins, valid ? digit_of(row, a.dig[q]) : 0u, valid, nvalid);
       }
     }
   };
@@ -570,7 +710,7 @@ struct LocalLayout {
     perm0 = o; o += align16(size_t(cap) * 2);
     perm1 = o; o += align16(size_t(cap) * 2);
     rnk = o; o += align16(size_t(cap) * 2);
-    whist = o; o += align16(size_t(kSortWarps) * kBins * 4);
+    whist = o; o += align16(size_t(kSortWarps) * kBins * 2);
     cnt = o; o += align16(kBins * 4);
     start = o; o += align16(kBins * 4);
     seg = o; o += align16((size_t(TL) + 2) * 8);
@@ -592,7 +732,7 @@ __global__ void __launch_bounds__(kSortThreads) k_local(LocalArgs a) {
   uint16_t* s_p0 = reinterpret_cast<uint16_t*>(smem + L.perm0);
   uint16_t* s_p1 = reinterpret_cast<uint16_t*>(smem + L.perm1);
   uint16_t* s_rank = reinterpret_cast<uint16_t*>(smem + L.rnk);
-  uint32_t* s_whist = reinterpret_cast<uint32_t*>(smem + L.whist);
+  uint16_t* s_whist = reinterpret_cast<uint16_t*>(smem + L.whist);
   uint32_t* s_cnt = reinterpret_cast<uint32_t*>(smem + L.cnt);
   uint32_t* s_start = reinterpret_cast<uint32_t*>(smem + L.start);
   unsigned long long* s_seg = reinterpret_cast<unsigned long long*>(smem + L.seg);
@@ -987,7 +1127,11 @@ Workspace* workspace_create(int device) {
     QD_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  optin - (int)fa.sharedSizeBytes));
   };
-  allow_smem(reinterpret_cast<const void*>(k_onesweep));
+  allow_smem(reinterpret_cast<const void*>(k_onesweep<0>));
+  allow_smem(reinterpret_cast<const void*>(k_onesweep<2>));
+  allow_smem(reinterpret_cast<const void*>(k_onesweep<3>));
+  allow_smem(reinterpret_cast<const void*>(k_onesweep<4>));
+  allow_smem(reinterpret_cast<const void*>(k_onesweep<5>));
   allow_smem(reinterpret_cast<const void*>(k_local));
   allow_smem(reinterpret_cast<const void*>(k_hist));
   ws->smem_optin = optin - 1024;  // dynamic budget below the static usage
@@ -1101,7 +1245,8 @@ constexpr uint32_t kCounters = 4096;
 uint32_t sweep_tile_rows(const Workspace& ws, uint32_t rank) {
   const size_t budget = std::min<size_t>(ws.smem_optin, 112 * 1024);  // 2 CTAs/SM
   uint32_t T = 4096;
-  while (T > 256 && SweepLayout(T, rank).total > budget) T -= 256;
+  while (T > 512 && SweepLayout(T, rank).total > budget) T -= 512;
+  while (T > 32 && SweepLayout(T, rank).total > budget) T -= 32;
   return T;
 }
 uint32_t local_span(const Workspace& ws, uint32_t rank) {
@@ -1215,8 +1360,20 @@ void launch_pass(Ctx& c, PassArgs& a) {
   }
   a.tile_counter = c.counters + c.next_counter++;
   const size_t smem = SweepLayout(a.T, a.rank).total;
+  void (*fn)(PassArgs) = k_onesweep<0>;
+  switch (a.rank) {
+    case 2: fn = k_onesweep<2>; break;
+    case 3: fn = k_onesweep<3>; break;
+    case 4: fn = k_onesweep<4>; break;
+    case 5: fn = k_onesweep<5>; break;
+    default: break;
+  }
+  int per_sm = 0;
+  QD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kSortThreads, smem));
+  const uint32_t grid =
+      (uint32_t)std::min<uint64_t>(a.num_tiles, (uint64_t)std::max(1, per_sm) * ws.num_sms);
   c.pre();
-  k_onesweep<<<a.num_tiles, kSortThreads, smem, c.st>>>(a);
+  fn<<<grid, kSortThreads, smem, c.st>>>(a);
   c.launched(kSweep);
 }
 
@@ -1343,7 +1500,13 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
     h.pass0 = p0;
     h.hist = hist;
     h.hist_stride = stride;
-    for (uint32_t q = 0; q < h.np; ++q) h.dig[q] = digs[p0 + q];
+    for (uint32_t q = 0; q < h.np; ++q) {
+      h.dig[q] = digs[p0 + q];
+      const uint32_t lo = (p0 + q) * per, hi = std::min(bits, lo + per);
+      h.shift[q] = lo;
+      h.mask[q] = (1u << (hi - lo)) - 1u;
+    }
+    h.fast = bits <= 64;
     h.key = key;
     h.do_check = p0 == 0 && key.check;
     h.err = c.err;
