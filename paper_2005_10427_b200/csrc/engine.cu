@@ -7,17 +7,22 @@
 // empty, sort.cpp:54-78; consecutive same-prefix steps compose LSD-wise into
 // one combined key).  Device work per group:
 //
-//   k_heads / scan / k_compact   segment discovery (bucket_starts, sort.cpp:136)
-//   k_classify / k_gen_tiles     small runs -> local chunks, large runs -> tiles
-//   k_hist                       per-run digit histograms of every pass in one
-//                                read, + range check (count_keys, sort.cpp:54-64)
-//   k_onesweep  (D passes)       stable counting pass of one radix digit per
-//                                tile: warp-match ranking in shared memory,
-//                                decoupled look-back across the tiles of a run,
-//                                coalesced scatter of whole rows (AoS coords +
-//                                f64 value) staged through shared memory
-//   k_local                      runs that fit one CTA: loaded once, fully
-//                                sorted in shared memory, written once
+//   k_heads / scan / k_compact     run discovery (bucket_starts, sort.cpp:136)
+//   k_classify_chunks/k_gen_chunks small runs -> local CTA sorts, large runs ->
+//                                  chunks of contiguous rows
+//   per radix digit (LSD, 8 bits):
+//     k_chunk_hist                 digit histogram of every chunk (+ range
+//                                  check on the first digit: count_keys)
+//     scan                         (run, bin, chunk) exclusive scan = every
+//                                  chunk's output cursor per bin: the
+//                                  (key, worker) order of parallel.cpp:88-100
+//     k_scatter                    chunk-ordered stable scatter of whole rows:
+//                                  TMA bulk-copy double buffering, warp-ballot
+//                                  ranking in shared memory, coalesced stores;
+//                                  intermediates in SoA so the next histogram
+//                                  reads only the key column
+//   k_local                        runs that fit one CTA: loaded once, fully
+//                                  sorted in shared memory, written once
 //
 // Rows are always moved whole (the reference's scatter_rows), so there is no
 // separate gather.  No CPU fallback exists: every path here is a kernel.
@@ -41,13 +46,14 @@ namespace qb200 {
 
 constexpr int kThreads = 256;       // utility kernels
 constexpr int kWarps = kThreads / 32;
-constexpr int kSortThreads = 512;   // k_onesweep / k_local
+constexpr int kSortThreads = 512;   // k_scatter / k_local
 constexpr int kSortWarps = kSortThreads / 32;
 constexpr int kRadixLog = 8;
 constexpr int kBins = 1 << kRadixLog;
 constexpr int kMaxTerms = 12;
 constexpr int kMaxKeys = QD_MAX_RANK;
 constexpr int kHistPasses = 8;  // passes histogrammed per k_hist launch
+constexpr uint32_t kChunkTiles = 16;  // tiles per scatter chunk
 
 // ---------------------------------------------------------------------------
 // kernel parameter blocks
@@ -83,54 +89,6 @@ struct ErrBlock {
   unsigned long long rows[kMaxGroups];  // rows of large runs, per group (profiling)
 };
 
-struct TileDesc {
-  unsigned long long row_begin;
-  unsigned int len;
-  unsigned int li_first;  // (large-run index << 1) | first-tile-of-run
-};
-
-struct PassArgs {
-  const uint32_t* in_c;
-  const double* in_v;
-  uint32_t* out_c;
-  double* out_v;
-  uint32_t rank;
-  uint64_t nnz;
-  uint32_t T;                               // rows per tile
-  const TileDesc* tiles;                    // nullptr: uniform tiles of [0,nnz)
-  uint32_t num_tiles;
-  const unsigned long long* run_start;      // [li]; nullptr: run 0 starts at 0
-  const uint32_t* hist;                     // [li][pass][kBins], this pass
-  uint32_t hist_stride;                     // D * kBins
-  unsigned long long* status;               // [tile][kBins]
-  uint32_t epoch;
-  uint32_t* tile_counter;
-  DigitSpec dig;
-};
-
-struct HistArgs {
-  const uint32_t* in_c;
-  uint32_t rank;
-  uint64_t nnz;
-  uint32_t T;
-  const TileDesc* tiles;
-  uint32_t num_tiles;
-  uint32_t tiles_per_cta;
-  uint32_t np;                              // passes in this launch
-  uint32_t pass0;
-  uint32_t* hist;
-  uint32_t hist_stride;
-  DigitSpec dig[kHistPasses];
-  KeySpec key;
-  int do_check;
-  ErrBlock* err;
-  unsigned long long* rows_counter;  // += rows histogrammed (pass0 == 0 only)
-  // fast path (combined key fits 64 bits, no lookup digit): digit q of a row
-  // is (full_key >> shift[q]) & mask[q]
-  int fast;
-  uint32_t shift[kHistPasses], mask[kHistPasses];
-};
-
 struct LocalArgs {
   const uint32_t* in_c;
   const double* in_v;
@@ -144,6 +102,60 @@ struct LocalArgs {
   uint64_t nseg;
   KeySpec key;
   ErrBlock* err;
+};
+
+// A chunk: a contiguous row range inside one run, processed by one CTA in
+// input order; the (bin, chunk) exclusive scan gives every chunk its own
+// output cursor per bin (parallel.cpp:88-100's (key, worker) order, with CTA
+// chunks as the workers), so no inter-CTA waiting is needed.
+struct ChunkDesc {
+  unsigned long long row_begin;
+  unsigned int len;
+  unsigned int li;          // large-run index
+  unsigned int cidx;        // chunk index inside its run
+  unsigned int nchunks;     // chunks in its run
+  unsigned long long coff;  // global index of the run's first chunk
+};
+
+// Row storage: AoS = coords[N*R] (row-major, the API layout) + values[N];
+// SoA = column m at coords + m*N (intermediate passes) + values[N].
+struct Rows {
+  const uint32_t* c;
+  const double* v;
+  int soa;
+};
+struct RowsOut {
+  uint32_t* c;
+  double* v;
+  int soa;
+};
+
+struct ChunkHistArgs {
+  Rows in;
+  uint32_t rank;
+  uint64_t nnz;
+  const ChunkDesc* chunks;
+  uint32_t num_chunks;
+  uint32_t* flat;  // [(coff + c) * kBins layout: coff*kBins + b*nchunks + cidx]
+  DigitSpec dig;
+  KeySpec key;
+  int do_check;
+  ErrBlock* err;
+  unsigned long long* rows_counter;
+};
+
+struct ScatterArgs {
+  Rows in;
+  RowsOut out;
+  uint32_t rank;
+  uint64_t nnz;
+  uint32_t T;  // rows per tile
+  const ChunkDesc* chunks;
+  uint32_t num_chunks;
+  const unsigned long long* offs;       // exclusive scan of the chunk-hist flat array
+  const unsigned long long* run_start;  // [li]; nullptr: 0
+  uint32_t* chunk_counter;
+  DigitSpec dig;
 };
 
 // ---------------------------------------------------------------------------
@@ -181,24 +193,6 @@ __device__ __forceinline__ void check_row(const uint32_t* row, const KeySpec& k,
       atomicMin(&e->rowmode, (unsigned long long)((grow << 6) | k.mode[i]));
     }
   }
-}
-
-__device__ __forceinline__ void st_relaxed(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-
-constexpr unsigned long long kFlagAgg = 1ull << 62;
-constexpr unsigned long long kFlagPre = 2ull << 62;
-constexpr unsigned long long kValMask = (1ull << 48) - 1ull;
-
-__device__ __forceinline__ unsigned long long enc(unsigned long long flag, uint32_t epoch,
-                                                  unsigned long long v) {
-  return flag | ((unsigned long long)(epoch & 0x3FFFu) << 48) | v;
 }
 
 // Exclusive scan across the block of one value per thread (NT threads).
@@ -412,289 +406,290 @@ __device__ __forceinline__ Stage make_stage(const void* g, uint32_t len) {
   return s;
 }
 
-// Shared-memory layout of k_onesweep: two row buffers (double buffering) of T
-// rows plus the ranking / offset scratch.
-struct SweepLayout {
-  size_t cbuf, vbuf, c0, v0, dig, rnk, sorted, whist, cnt, start, gbase, tmp, bar, total;
-  __host__ __device__ SweepLayout(uint32_t T, uint32_t rank) {
+// Digit of the row whose coordinate of mode m is get(m).
+template <class G>
+__device__ __forceinline__ uint32_t digit_by(G get, const DigitSpec& d) {
+  if (d.lookup) {
+    const uint32_t c = get(d.lookup_mode);
+    return c < d.lookup_dim ? __ldg(d.lookup + c) : 0u;
+  }
+  uint32_t v = ((get(d.mode[0]) >> d.rsh[0]) & ((1u << d.bits[0]) - 1u)) << d.lsh[0];
+#pragma unroll 1
+  for (uint32_t i = 1; i < d.n; ++i)
+    v |= ((get(d.mode[i]) >> d.rsh[i]) & ((1u << d.bits[i]) - 1u)) << d.lsh[i];
+  return v;
+}
+
+// Warp-aggregated counting of 32 consecutive rows' digits into a per-warp
+// histogram: each run of equal digits is added once by its head lane (sorted
+// inputs make long runs common).
+__device__ __forceinline__ void add_runs(uint32_t* h, uint32_t d, bool valid, uint32_t nvalid) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t prev = __shfl_up_sync(0xFFFFFFFFu, d, 1);
+  const bool head = valid && (lane == 0 || prev != d);
+  const unsigned heads = __ballot_sync(0xFFFFFFFFu, head);
+  if (head) {
+    const unsigned after = heads & ~((2u << lane) - 1u);
+    const uint32_t end = after ? (uint32_t)(__ffs(after) - 1) : nvalid;
+    atomicAdd(h + d, end - lane);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_chunk_hist: digit histogram of every chunk (one pass), written into the
+// (run, bin, chunk) flat array that the scan turns into output cursors.
+// Pass 0 also range-checks the key coordinates (count_keys, sort.cpp:54-64).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) k_chunk_hist(ChunkHistArgs a) {
+  __shared__ uint32_t s_h[kWarps * kBins];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t R = a.rank;
+  const uint64_t N = a.nnz;
+  for (uint32_t ci = blockIdx.x; ci < a.num_chunks; ci += gridDim.x) {
+    for (int k = threadIdx.x; k < kWarps * kBins; k += kThreads) s_h[k] = 0;
+    __syncthreads();
+    const ChunkDesc cd = a.chunks[ci];
+    if (threadIdx.x == 0 && a.rows_counter) atomicAdd(a.rows_counter, (unsigned long long)cd.len);
+    for (uint32_t g = w * 32; g < cd.len; g += kThreads) {  // warp-uniform
+      const uint32_t i = g + lane;
+      const bool valid = i < cd.len;
+      const uint32_t nvalid = min(32u, cd.len - g);
+      const unsigned long long r = cd.row_begin + (valid ? i : 0u);
+      uint32_t d = 0;
+      if (a.in.soa) {
+        if (valid) d = digit_by([&](uint32_t m) { return __ldcs(a.in.c + m * N + r); }, a.dig);
+      } else {
+        const uint32_t* row = a.in.c + r * R;
+        if (valid) {
+          if (a.do_check) check_row(row, a.key, r, a.err);
+          d = digit_by([&](uint32_t m) { return __ldg(row + m); }, a.dig);
+        }
+      }
+      add_runs(s_h + w * kBins, d, valid, nvalid);
+    }
+    __syncthreads();
+    uint32_t* f = a.flat + cd.coff * kBins + cd.cidx;
+    for (int b = threadIdx.x; b < kBins; b += kThreads) {
+      uint32_t v = 0;
+#pragma unroll
+      for (int x = 0; x < kWarps; ++x) v += s_h[x * kBins + b];
+      f[(size_t)b * cd.nchunks] = v;
+    }
+    __syncthreads();
+  }
+}
+
+// Shared-memory layout of k_scatter: two staging buffers (TMA double
+// buffering) of T rows, plus ranking scratch and per-bin cursors.
+struct ScatterLayout {
+  size_t cspan, cbuf, vbuf, c0, v0, dig, rnk, sorted, whist, cnt, start, run, gbase, tmp, ofs,
+      bar, total;
+  __host__ __device__ ScatterLayout(uint32_t T, uint32_t rank, bool soa) {
     size_t o = 0;
-    cbuf = align16(size_t(T) * rank * 4 + 32);
+    cspan = align16(size_t(T) * 4 + 32);  // one SoA column span
+    cbuf = soa ? cspan * rank : align16(size_t(T) * rank * 4 + 32);
     vbuf = align16(size_t(T) * 8 + 32);
-    c0 = o; o += 2 * cbuf;  // coordinate buffers 0, 1
-    v0 = o; o += 2 * vbuf;  // value buffers 0, 1
+    c0 = o; o += 2 * cbuf;
+    v0 = o; o += 2 * vbuf;
     dig = o; o += align16(size_t(T) * 2);
     rnk = o; o += align16(size_t(T) * 2);
     sorted = o; o += align16(size_t(T) * 2);
     whist = o; o += align16(size_t(kSortWarps) * kBins * 2);
     cnt = o; o += align16(kBins * 4);
     start = o; o += align16(kBins * 4);
+    run = o; o += align16(kBins * 8);
     gbase = o; o += align16(kBins * 8);
     tmp = o; o += align16(64 * 8);
+    ofs = o; o += align16(2 * 66 * 4);  // per buffer: R column heads + value head
     bar = o; o += 16;
     total = o;
   }
 };
 
-struct TileInfo {
-  unsigned long long rb;
-  uint32_t n, li, first;
-};
-
-__device__ __forceinline__ TileInfo tile_info(const PassArgs& a, uint32_t tile) {
-  TileInfo t;
-  if (a.tiles) {
-    const TileDesc d = a.tiles[tile];
-    t.rb = d.row_begin;
-    t.n = d.len;
-    t.li = d.li_first >> 1;
-    t.first = d.li_first & 1u;
-  } else {
-    t.rb = (unsigned long long)tile * a.T;
-    t.n = (uint32_t)min((unsigned long long)a.T, a.nnz - t.rb);
-    t.li = 0;
-    t.first = tile == 0;
-  }
-  return t;
-}
-
 // ---------------------------------------------------------------------------
-// k_onesweep: one stable counting pass over one radix digit.  Persistent CTAs
-// take tiles in order from a global counter; thread 0 prefetches the NEXT
-// tile's rows with TMA bulk copies into the other buffer while the CTA ranks,
-// looks back and scatters the current one.  RT = compile-time rank (0: any).
+// k_scatter: one stable counting pass over one radix digit, chunk-ordered.
+// Persistent CTAs claim chunks; inside a chunk, tiles are processed in order
+// and thread 0 prefetches the next tile with TMA bulk copies (cp.async.bulk,
+// mbarrier completion) into the other buffer while the CTA ranks the current
+// tile (warp ballots), and scatters it coalesced through shared memory.
+// RT: compile-time rank (0 = runtime); IN_SOA / OUT_SOA: row formats.
 // ---------------------------------------------------------------------------
-template <int RT>
-__global__ void __launch_bounds__(kSortThreads) k_onesweep(PassArgs a) {
-  extern __shared__ __align__(16) unsigned char smem[];
+template <int RT, bool IN_SOA, bool OUT_SOA>
+__global__ void __launch_bounds__(kSortThreads, 2) k_scatter(ScatterArgs a) {
+  extern __shared__ __align__(128) unsigned char smem[];
   const uint32_t R = RT ? RT : a.rank;
-  const SweepLayout L(a.T, R);
+  const uint64_t N = a.nnz;
+  const ScatterLayout L(a.T, R, IN_SOA);
   uint16_t* s_dig = reinterpret_cast<uint16_t*>(smem + L.dig);
   uint16_t* s_rank = reinterpret_cast<uint16_t*>(smem + L.rnk);
   uint16_t* s_sorted = reinterpret_cast<uint16_t*>(smem + L.sorted);
   uint16_t* s_whist = reinterpret_cast<uint16_t*>(smem + L.whist);
   uint32_t* s_cnt = reinterpret_cast<uint32_t*>(smem + L.cnt);
   uint32_t* s_start = reinterpret_cast<uint32_t*>(smem + L.start);
+  unsigned long long* s_run = reinterpret_cast<unsigned long long*>(smem + L.run);
   long long* s_gbase = reinterpret_cast<long long*>(smem + L.gbase);
   unsigned long long* s_tmp = reinterpret_cast<unsigned long long*>(smem + L.tmp);
+  uint32_t* s_ofs = reinterpret_cast<uint32_t*>(smem + L.ofs);  // [2][66] byte offsets
   unsigned long long* s_bar = reinterpret_cast<unsigned long long*>(smem + L.bar);
-  __shared__ uint32_t s_next;
+  __shared__ uint32_t s_chunk, s_tile;  // next (chunk, tile-in-chunk) to process
 
-  // thread 0: claim the next tile and start its bulk loads into buffer b
-  auto prefetch = [&](uint32_t b) {
-    const uint32_t t = atomicAdd(a.tile_counter, 1u);
-    s_next = t;
-    if (t < a.num_tiles) {
-      const TileInfo ti = tile_info(a, t);
-      const Stage sc = make_stage(a.in_c + ti.rb * R, ti.n * R * 4);
-      const Stage sv = make_stage(a.in_v + ti.rb, ti.n * 8);
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_expect_tx(&s_bar[b], sc.bulk + sv.bulk);
-      if (sc.bulk) bulk_g2s(smem + L.c0 + b * L.cbuf, sc.gal, sc.bulk, &s_bar[b]);
-      if (sv.bulk) bulk_g2s(smem + L.v0 + b * L.vbuf, sv.gal, sv.bulk, &s_bar[b]);
+  // global address + byte length of span k of rows [rb, rb+n)
+  auto span = [&](uint32_t k, unsigned long long rb, uint32_t n, const void*& g, uint32_t& len) {
+    if (k == R) {
+      g = a.in.v + rb;
+      len = n * 8;
+    } else if (IN_SOA) {
+      g = a.in.c + (size_t)k * N + rb;
+      len = n * 4;
+    } else {
+      g = a.in.c + rb * R;
+      len = n * R * 4;
     }
+  };
+  auto nspans = [&]() { return IN_SOA ? R + 1 : 2u; };
+  auto span_index = [&](uint32_t j) { return (!IN_SOA && j == 1) ? R : j; };
+  auto span_dst = [&](uint32_t b, uint32_t k) -> unsigned char* {
+    if (k == R) return smem + L.v0 + b * L.vbuf;
+    return smem + L.c0 + b * L.cbuf + (IN_SOA ? k * L.cspan : 0);
+  };
+
+  // thread 0: issue the bulk loads of tile (ci, ti) into buffer b
+  auto load_tile = [&](uint32_t b, uint32_t ci, uint32_t ti) {
+    const ChunkDesc cd = a.chunks[ci];
+    const unsigned long long rb = cd.row_begin + (unsigned long long)ti * a.T;
+    const uint32_t n = (uint32_t)min((unsigned long long)a.T, cd.row_begin + cd.len - rb);
+    const uint32_t ns = nspans();
+    uint32_t total = 0;
+    for (uint32_t j = 0; j < ns; ++j) {
+      const void* g;
+      uint32_t len;
+      span(span_index(j), rb, n, g, len);
+      const Stage st = make_stage(g, len);
+      total += st.bulk;
+      s_ofs[b * 66 + span_index(j)] = st.head;
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect_tx(&s_bar[b], total);
+    for (uint32_t j = 0; j < ns; ++j) {
+      const void* g;
+      uint32_t len;
+      span(span_index(j), rb, n, g, len);
+      const Stage st = make_stage(g, len);
+      if (st.bulk) bulk_g2s(span_dst(b, span_index(j)), st.gal, st.bulk, &s_bar[b]);
+    }
+  };
+  // thread 0: pick the tile after (ci, ti), publish it in s_chunk/s_tile and
+  // start loading it into buffer b
+  auto advance = [&](uint32_t b, uint32_t ci, uint32_t ti, bool start) {
+    uint32_t nc = ci, nt = ti + 1;
+    if (start || nt * (unsigned long long)a.T >= a.chunks[ci].len) {
+      nc = atomicAdd(a.chunk_counter, 1u);
+      nt = 0;
+    }
+    s_chunk = nc;
+    s_tile = nt;
+    if (nc < a.num_chunks) load_tile(b, nc, nt);
   };
 
   if (threadIdx.x == 0) {
     mbar_init(&s_bar[0], 1);
     mbar_init(&s_bar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    advance(0, 0, 0, true);
   }
   __syncthreads();
-  if (threadIdx.x == 0) prefetch(0);
-  __syncthreads();
 
-  const uint32_t ipw = a.T / kSortWarps;
-  uint32_t phases = 0u;  // bit b: parity of buffer b's barrier
+  uint32_t phases = 0u;
   for (uint32_t it = 0;; ++it) {
     const uint32_t b = it & 1u;
-    const uint32_t tile = s_next;
-    if (tile >= a.num_tiles) break;
-    __syncthreads();  // everyone has read s_next
-    if (threadIdx.x == 0) prefetch(b ^ 1u);
+    const uint32_t ci = s_chunk, ti = s_tile;
+    if (ci >= a.num_chunks) break;
+    __syncthreads();  // everyone has read s_chunk / s_tile
+    if (threadIdx.x == 0) advance(b ^ 1u, ci, ti, false);
+    const ChunkDesc cd = a.chunks[ci];
+    const unsigned long long rb = cd.row_begin + (unsigned long long)ti * a.T;
+    const uint32_t n = (uint32_t)min((unsigned long long)a.T, cd.row_begin + cd.len - rb);
+    if (ti == 0 && threadIdx.x < kBins) {
+      // this chunk's cursor per bin: scanned (run, bin, chunk) offset
+      const unsigned long long base0 = a.offs[cd.coff * kBins];
+      const unsigned long long rs = a.run_start ? a.run_start[cd.li] : 0ull;
+      s_run[threadIdx.x] =
+          a.offs[cd.coff * kBins + (size_t)threadIdx.x * cd.nchunks + cd.cidx] - base0 + rs;
+    }
     for (int k = threadIdx.x; k < kSortWarps * kBins; k += kSortThreads) s_whist[k] = 0;
-
-    const TileInfo ti = tile_info(a, tile);
-    const uint32_t n = ti.n;
-    const Stage sc = make_stage(a.in_c + ti.rb * R, n * R * 4);
-    const Stage sv = make_stage(a.in_v + ti.rb, n * 8);
     mbar_wait(&s_bar[b], (phases >> b) & 1u);
     phases ^= 1u << b;
-    // sub-16-byte tails of the spans
-    if (threadIdx.x < sc.tail / 4)
-      reinterpret_cast<uint32_t*>(smem + L.c0 + b * L.cbuf + sc.bulk)[threadIdx.x] =
-          reinterpret_cast<const uint32_t*>(sc.gal + sc.bulk)[threadIdx.x];
-    if (threadIdx.x == 32 && sv.tail)
-      *reinterpret_cast<double*>(smem + L.v0 + b * L.vbuf + sv.bulk) =
-          *reinterpret_cast<const double*>(sv.gal + sv.bulk);
-    const uint32_t* s_c = reinterpret_cast<const uint32_t*>(smem + L.c0 + b * L.cbuf + sc.head);
-    const double* s_v = reinterpret_cast<const double*>(smem + L.v0 + b * L.vbuf + sv.head);
+    {  // sub-16-byte tails of every span: warp j loads span j's tail
+      const uint32_t j = threadIdx.x >> 5, lane = threadIdx.x & 31;
+      if (j < nspans()) {
+        const uint32_t k = span_index(j);
+        const void* g;
+        uint32_t len;
+        span(k, rb, n, g, len);
+        const Stage st = make_stage(g, len);
+        if (lane < st.tail / 4)
+          reinterpret_cast<uint32_t*>(span_dst(b, k) + st.bulk)[lane] =
+              reinterpret_cast<const uint32_t*>(st.gal + st.bulk)[lane];
+      }
+    }
     __syncthreads();
+    const uint32_t* sc = reinterpret_cast<const uint32_t*>(smem + L.c0 + b * L.cbuf);
+    const double* s_v = reinterpret_cast<const double*>(span_dst(b, R) + s_ofs[b * 66 + R]);
+    const uint32_t* s_ofsb = s_ofs + b * 66;
+    auto coord = [&](uint32_t i, uint32_t m) -> uint32_t {
+      if (IN_SOA)
+        return *reinterpret_cast<const uint32_t*>(reinterpret_cast<const unsigned char*>(sc) +
+                                                  m * L.cspan + s_ofsb[m] + i * 4);
+      return *reinterpret_cast<const uint32_t*>(reinterpret_cast<const unsigned char*>(sc) +
+                                                s_ofsb[0] + (i * R + m) * 4);
+    };
 
     for (uint32_t i = threadIdx.x; i < n; i += kSortThreads)
-      s_dig[i] = (uint16_t)digit_of(s_c + (size_t)i * R, a.dig);
+      s_dig[i] = (uint16_t)digit_by([&](uint32_t m) { return coord(i, m); }, a.dig);
     __syncthreads();
-
+    const uint32_t ipw = (n + kSortWarps - 1) / kSortWarps;
     warp_rank([&](uint32_t p) { return (uint32_t)s_dig[p]; }, n, ipw, s_rank, s_whist);
     __syncthreads();
     bin_totals<kSortThreads>(s_whist, s_cnt);
     __syncthreads();
-
-    // Publish this tile's per-digit counts as early as possible.
-    unsigned long long* st = a.status + (size_t)tile * kBins;
     const bool binthr = threadIdx.x < kBins;
     const uint32_t cnt = binthr ? s_cnt[threadIdx.x] : 0u;
-    if (binthr) st_relaxed(st + threadIdx.x, enc(ti.first ? kFlagPre : kFlagAgg, a.epoch, cnt));
-
-    // Tile-local and run-level exclusive digit offsets.
     const uint32_t start = block_excl_scan<kSortThreads>(cnt, reinterpret_cast<uint32_t*>(s_tmp));
-    if (binthr) s_start[threadIdx.x] = start;
-    const uint32_t h = binthr ? a.hist[(size_t)ti.li * a.hist_stride + threadIdx.x] : 0u;
-    const unsigned long long run_off = block_excl_scan64<kSortThreads>(h, s_tmp);
-    const unsigned long long base = a.run_start ? a.run_start[ti.li] : 0ull;
-
-    // Decoupled look-back over the preceding tiles of the same run.
     if (binthr) {
-      const int bb = threadIdx.x;
-      unsigned long long excl = 0;
-      if (!ti.first) {
-        long long p = (long long)tile - 1;
-        for (;;) {
-          const unsigned long long sw = ld_relaxed(a.status + (size_t)p * kBins + bb);
-          const unsigned long long flag = sw & (3ull << 62);
-          if (flag == 0 || ((sw >> 48) & 0x3FFFu) != (a.epoch & 0x3FFFu)) {
-            __nanosleep(20);
-            continue;
-          }
-          excl += sw & kValMask;
-          if (flag == kFlagPre) break;
-          --p;
-        }
-        st_relaxed(st + bb, enc(kFlagPre, a.epoch, excl + cnt));
-      }
-      s_gbase[bb] = (long long)(base + run_off + excl) - (long long)start;
+      s_start[threadIdx.x] = start;
+      const unsigned long long r0 = s_run[threadIdx.x];
+      s_gbase[threadIdx.x] = (long long)r0 - (long long)start;
+      s_run[threadIdx.x] = r0 + cnt;
     }
     __syncthreads();
-
     for (uint32_t i = threadIdx.x; i < n; i += kSortThreads) {
       const uint32_t d = s_dig[i];
-      const uint32_t pos = s_start[d] + s_whist[(i / ipw) * kBins + d] + s_rank[i];
-      s_sorted[pos] = (uint16_t)i;
+      s_sorted[s_start[d] + s_whist[(i / ipw) * kBins + d] + s_rank[i]] = (uint16_t)i;
     }
     __syncthreads();
-
     for (uint32_t j = threadIdx.x; j < n; j += kSortThreads) {
       const uint32_t i = s_sorted[j];
       const unsigned long long dst = (unsigned long long)(s_gbase[s_dig[i]] + j);
-      const uint32_t* src = s_c + (size_t)i * R;
-      uint32_t* o = a.out_c + dst * R;
-      if (RT) {
+      if (OUT_SOA) {
+        if (RT) {
 #pragma unroll
-        for (int m = 0; m < RT; ++m) __stcs(o + m, src[m]);
+          for (int m = 0; m < RT; ++m) __stcs(a.out.c + (size_t)m * N + dst, coord(i, m));
+        } else {
+          for (uint32_t m = 0; m < R; ++m) __stcs(a.out.c + (size_t)m * N + dst, coord(i, m));
+        }
       } else {
-        for (uint32_t m = 0; m < R; ++m) __stcs(o + m, src[m]);
+        uint32_t* o = a.out.c + dst * R;
+        if (RT) {
+#pragma unroll
+          for (int m = 0; m < RT; ++m) __stcs(o + m, coord(i, m));
+        } else {
+          for (uint32_t m = 0; m < R; ++m) __stcs(o + m, coord(i, m));
+        }
       }
-      __stcs(a.out_v + dst, s_v[i]);
+      __stcs(a.out.v + dst, s_v[i]);
     }
     __syncthreads();  // buffer b and the scratch are free again
   }
-}
-
-// ---------------------------------------------------------------------------
-// k_hist: per-run digit histograms of np passes + range check
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kThreads) k_hist(HistArgs a) {
-  // per-warp private histograms [kWarps][np][kBins] (shared-memory atomics
-  // only among one warp's run heads), folded into global at each flush
-  extern __shared__ uint32_t s_h[];
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t per_warp = a.np * kBins;
-  for (uint32_t k = threadIdx.x; k < kWarps * per_warp; k += kThreads) s_h[k] = 0;
-  __syncthreads();
-  uint32_t* wh = s_h + w * per_warp;
-  int cur_li = -1;
-  auto flush = [&](int li) {
-    __syncthreads();
-    if (li >= 0) {
-      uint32_t* g = a.hist + (size_t)li * a.hist_stride + (size_t)a.pass0 * kBins;
-      for (uint32_t k = threadIdx.x; k < per_warp; k += kThreads) {
-        uint32_t v = 0;
-#pragma unroll
-        for (int x = 0; x < kWarps; ++x) {
-          v += s_h[x * per_warp + k];
-          s_h[x * per_warp + k] = 0;
-        }
-        if (v) atomicAdd(g + k, v);
-      }
-    }
-    __syncthreads();
-  };
-  // Runs of equal digits among the warp's 32 consecutive rows are counted by
-  // their head lane (sorted inputs make long runs common: Zipf heads).
-  auto add_runs = [&](uint32_t* h, uint32_t d, bool valid, uint32_t nvalid) {
-    const uint32_t prev = __shfl_up_sync(0xFFFFFFFFu, d, 1);
-    const bool head = valid && (lane == 0 || prev != d);
-    const unsigned heads = __ballot_sync(0xFFFFFFFFu, head);
-    if (head) {
-      const unsigned after = heads & ~((2u << lane) - 1u);
-      const uint32_t end = after ? (uint32_t)(__ffs(after) - 1) : nvalid;
-      atomicAdd(h + d, end - lane);
-    }
-  };
-  auto count_rows = [&](unsigned long long rb, uint32_t n) {
-    if (threadIdx.x == 0 && a.rows_counter) atomicAdd(a.rows_counter, (unsigned long long)n);
-    for (uint32_t g = w * 32; g < n; g += kThreads) {  // warp-uniform
-      const uint32_t i = g + lane;
-      const bool valid = i < n;
-      const uint32_t nvalid = min(32u, n - g);
-      const uint32_t* row = a.in_c + (size_t)(rb + (valid ? i : 0)) * a.rank;
-      if (a.fast) {
-        // one pass over the key fields: range check + combined key
-        unsigned long long key = 0;
-#pragma unroll 1
-        for (uint32_t k = 0; k < a.key.n; ++k) {
-          const uint32_t c = valid ? __ldg(row + a.key.mode[k]) : 0u;
-          if (a.do_check && c >= a.key.dim[k]) {
-            atomicOr(&a.err->flags, 1u);
-            atomicMin(&a.err->rowmode, (unsigned long long)(((rb + i) << 6) | a.key.mode[k]));
-          }
-          const uint32_t wd = a.key.width[k];
-          key |= (unsigned long long)(c & (uint32_t)((1ull << wd) - 1ull)) << a.key.off[k];
-        }
-#pragma unroll
-        for (int q = 0; q < kHistPasses; ++q)
-          if (q < (int)a.np)
-            add_runs(wh + q * kBins, (uint32_t)(key >> a.shift[q]) & a.mask[q], valid, nvalid);
-      } else {
-        if (valid && a.do_check) check_row(row, a.key, rb + i, a.err);
-#pragma unroll
-        for (int q = 0; q < kHistPasses; ++q)
-          if (q < (int)a.np)
-            add_runs(wh + q * kBins, valid ? digit_of(row, a.dig[q]) : 0u, valid, nvalid);
-      }
-    }
-  };
-  if (a.tiles == nullptr) {
-    // one run [0, nnz): contiguous row chunks per CTA
-    const unsigned long long per = (a.nnz + gridDim.x - 1) / gridDim.x;
-    const unsigned long long b = per * blockIdx.x;
-    const unsigned long long e = min((unsigned long long)a.nnz, b + per);
-    for (unsigned long long r = b; r < e; r += 65536ull)
-      count_rows(r, (uint32_t)min(65536ull, e - r));
-    flush(0);
-    return;
-  }
-  const uint32_t t0 = blockIdx.x * a.tiles_per_cta;
-  const uint32_t t1 = min(a.num_tiles, t0 + a.tiles_per_cta);
-  for (uint32_t t = t0; t < t1; ++t) {
-    const TileDesc d = a.tiles[t];
-    const int li = (int)(d.li_first >> 1);
-    if (li != cur_li) {
-      flush(cur_li);
-      cur_li = li;
-    }
-    count_rows(d.row_begin, d.len);
-  }
-  flush(cur_li);
 }
 
 // ---------------------------------------------------------------------------
@@ -911,23 +906,25 @@ __global__ void __launch_bounds__(kThreads) k_compact(const uint32_t* words, uin
   if (blockIdx.x == nblocks - 1 && threadIdx.x == 0) seg_start[*total] = nnz;
 }
 
-// Per run: large flag and its tile count.
-__global__ void k_classify(const unsigned long long* seg_start, const unsigned long long* S_ptr,
-                           uint32_t TL, uint32_t T, uint32_t* is_large, uint32_t* ntiles) {
+// Per run: large flag and its chunk count (CH rows per chunk).
+__global__ void k_classify_chunks(const unsigned long long* seg_start,
+                                  const unsigned long long* S_ptr, uint32_t TL, uint32_t CH,
+                                  uint32_t* is_large, uint32_t* nchunks) {
   const unsigned long long S = *S_ptr;
   for (unsigned long long s = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; s < S;
        s += (unsigned long long)gridDim.x * blockDim.x) {
     const unsigned long long len = seg_start[s + 1] - seg_start[s];
     const bool large = len > TL;
     is_large[s] = large;
-    ntiles[s] = large ? (uint32_t)((len + T - 1) / T) : 0u;
+    nchunks[s] = large ? (uint32_t)((len + CH - 1) / CH) : 0u;
   }
 }
 
-__global__ void k_gen_tiles(const unsigned long long* seg_start, const unsigned long long* S_ptr,
-                            uint32_t T, const uint32_t* is_large,
-                            const unsigned long long* large_off, const unsigned long long* tile_off,
-                            TileDesc* tiles, unsigned long long* run_start) {
+__global__ void k_gen_chunks(const unsigned long long* seg_start, const unsigned long long* S_ptr,
+                             uint32_t CH, const uint32_t* is_large,
+                             const unsigned long long* large_off,
+                             const unsigned long long* chunk_off, ChunkDesc* chunks,
+                             unsigned long long* run_start) {
   const unsigned long long S = *S_ptr;
   for (unsigned long long s = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; s < S;
        s += (unsigned long long)gridDim.x * blockDim.x) {
@@ -935,15 +932,40 @@ __global__ void k_gen_tiles(const unsigned long long* seg_start, const unsigned 
     const unsigned long long b = seg_start[s], e = seg_start[s + 1];
     const uint32_t li = (uint32_t)large_off[s];
     run_start[li] = b;
-    unsigned long long t = tile_off[s];
-    for (unsigned long long r = b; r < e; r += T, ++t) {
-      TileDesc d;
-      d.row_begin = r;
-      d.len = (uint32_t)min((unsigned long long)T, e - r);
-      d.li_first = (li << 1) | (r == b ? 1u : 0u);
-      tiles[t] = d;
+    const unsigned long long c0 = chunk_off[s];
+    const uint32_t nc = (uint32_t)((e - b + CH - 1) / CH);
+    for (uint32_t k = 0; k < nc; ++k) {
+      ChunkDesc d;
+      d.row_begin = b + (unsigned long long)k * CH;
+      d.len = (uint32_t)min((unsigned long long)CH, e - d.row_begin);
+      d.li = li;
+      d.cidx = k;
+      d.nchunks = nc;
+      d.coff = c0;
+      chunks[c0 + k] = d;
     }
   }
+}
+
+// One run [0, nnz) cut into chunks of CH rows.
+__global__ void k_uniform_chunks(uint64_t nnz, uint32_t CH, uint32_t nc, ChunkDesc* chunks) {
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < nc; k += gridDim.x * blockDim.x) {
+    ChunkDesc d;
+    d.row_begin = (unsigned long long)k * CH;
+    d.len = (uint32_t)min((unsigned long long)CH, nnz - d.row_begin);
+    d.li = 0;
+    d.cidx = k;
+    d.nchunks = nc;
+    d.coff = 0;
+    chunks[k] = d;
+  }
+}
+
+// out[i] = in[i * stride] for i < n (reads a column of the scanned offsets)
+__global__ void k_gather_stride(const unsigned long long* in, uint64_t stride, uint32_t n,
+                                unsigned long long* out) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    out[i] = in[i * stride];
 }
 
 // ---------------------------------------------------------------------------
@@ -1068,11 +1090,9 @@ struct Workspace {
   int num_sms = 148;
   size_t smem_optin = 227 * 1024;
   std::map<std::string, DevBuf> bufs;
-  uint32_t epoch = 0;
   uint64_t launches = 0;
   ErrBlock* h_err = nullptr;  // pinned
   uint64_t* h_small = nullptr;  // pinned scratch for small D2H reads
-  void* status_clean = nullptr;  // look-back buffer known to hold no stale flags
   // live per-kernel-class timing (CUDA events on the launch stream)
   bool prof = false;
   struct ProfStat {
@@ -1107,6 +1127,26 @@ struct Workspace {
   }
 };
 
+using ScatterFn = void (*)(ScatterArgs);
+template <int RT>
+ScatterFn scatter_kernel_fmt(int fmt) {
+  switch (fmt) {
+    case 0: return k_scatter<RT, false, false>;
+    case 1: return k_scatter<RT, false, true>;
+    case 2: return k_scatter<RT, true, false>;
+    default: return k_scatter<RT, true, true>;
+  }
+}
+ScatterFn scatter_kernel(int rt, int fmt) {
+  switch (rt) {
+    case 2: return scatter_kernel_fmt<2>(fmt);
+    case 3: return scatter_kernel_fmt<3>(fmt);
+    case 4: return scatter_kernel_fmt<4>(fmt);
+    case 5: return scatter_kernel_fmt<5>(fmt);
+    default: return scatter_kernel_fmt<0>(fmt);
+  }
+}
+
 Workspace* workspace_create(int device) {
   int n = 0;
   if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
@@ -1120,20 +1160,16 @@ Workspace* workspace_create(int device) {
   QD_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
   ws->smem_optin = optin;
   QD_CUDA(cudaMallocHost(&ws->h_err, sizeof(ErrBlock)));
-  QD_CUDA(cudaMallocHost(&ws->h_small, 64 * sizeof(uint64_t)));
+  QD_CUDA(cudaMallocHost(&ws->h_small, 512 * sizeof(uint64_t)));
   auto allow_smem = [&](const void* fn) {
     cudaFuncAttributes fa{};
     QD_CUDA(cudaFuncGetAttributes(&fa, fn));
     QD_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  optin - (int)fa.sharedSizeBytes));
   };
-  allow_smem(reinterpret_cast<const void*>(k_onesweep<0>));
-  allow_smem(reinterpret_cast<const void*>(k_onesweep<2>));
-  allow_smem(reinterpret_cast<const void*>(k_onesweep<3>));
-  allow_smem(reinterpret_cast<const void*>(k_onesweep<4>));
-  allow_smem(reinterpret_cast<const void*>(k_onesweep<5>));
+  for (int rt : {0, 2, 3, 4, 5})
+    for (int fmt = 0; fmt < 4; ++fmt) allow_smem(reinterpret_cast<const void*>(scatter_kernel(rt, fmt)));
   allow_smem(reinterpret_cast<const void*>(k_local));
-  allow_smem(reinterpret_cast<const void*>(k_hist));
   ws->smem_optin = optin - 1024;  // dynamic budget below the static usage
   return ws;
 }
@@ -1244,9 +1280,12 @@ constexpr uint32_t kCounters = 4096;
 // Rows per onesweep tile / local chunk for a given rank, from the smem budget.
 uint32_t sweep_tile_rows(const Workspace& ws, uint32_t rank) {
   const size_t budget = std::min<size_t>(ws.smem_optin, 112 * 1024);  // 2 CTAs/SM
+  auto need = [&](uint32_t T) {
+    return std::max(ScatterLayout(T, rank, false).total, ScatterLayout(T, rank, true).total);
+  };
   uint32_t T = 4096;
-  while (T > 512 && SweepLayout(T, rank).total > budget) T -= 512;
-  while (T > 32 && SweepLayout(T, rank).total > budget) T -= 32;
+  while (T > 512 && need(T) > budget) T -= 512;
+  while (T > 32 && need(T) > budget) T -= 32;
   return T;
 }
 uint32_t local_span(const Workspace& ws, uint32_t rank) {
@@ -1335,46 +1374,65 @@ DigitSpec make_digit(const KeySpec& k, uint32_t lo, uint32_t hi) {
   return d;
 }
 
-// Look-back status words; freshly (re)allocated memory is cleared once, after
-// that the per-pass epoch in every word makes stale entries harmless.
-unsigned long long* status_buffer(Ctx& c, uint64_t num_tiles) {
-  auto* status = c.ws.get<unsigned long long>("status", num_tiles * kBins);
-  if (c.ws.status_clean != status) {
-    QD_CUDA(cudaMemsetAsync(status, 0, c.ws.bufs["status"].bytes, c.st));
-    c.ws.status_clean = status;
-  }
-  return status;
-}
-
-void launch_pass(Ctx& c, PassArgs& a) {
-  if (a.num_tiles == 0) return;
+// One stable counting pass of digit `dig` over the chunks: chunk histograms,
+// (run, bin, chunk) exclusive scan, chunk-ordered scatter.
+void run_pass(Ctx& c, uint32_t R, uint64_t N, uint32_t T, Rows in, RowsOut out,
+              const ChunkDesc* chunks, uint64_t num_chunks,
+              const unsigned long long* run_start, const DigitSpec& dig, const KeySpec& key,
+              bool check, unsigned long long** offs_out = nullptr) {
   Workspace& ws = c.ws;
-  if (++ws.epoch >= 0x3FFFu) {
-    ws.epoch = 1;
-    QD_CUDA(cudaMemsetAsync(a.status, 0, ws.bufs["status"].bytes, c.st));
-  }
-  a.epoch = ws.epoch;
+  const uint64_t nflat = num_chunks * kBins;
+  auto* flat = ws.get<uint32_t>("chunk_flat", nflat);
+  auto* offs = ws.get<unsigned long long>("chunk_offs", nflat);
+  auto* tot = ws.get<unsigned long long>("chunk_total", 1);
+  ChunkHistArgs h{};
+  h.in = in;
+  h.rank = R;
+  h.nnz = N;
+  h.chunks = chunks;
+  h.num_chunks = (uint32_t)num_chunks;
+  h.flat = flat;
+  h.dig = dig;
+  h.key = key;
+  h.do_check = check;
+  h.err = c.err;
+  h.rows_counter = check ? &c.err->rows[std::min(c.group, kMaxGroups - 1)] : nullptr;
+  c.pre();
+  k_chunk_hist<<<(uint32_t)std::min<uint64_t>(num_chunks, (uint64_t)ws.num_sms * 8), kThreads, 0,
+                 c.st>>>(h);
+  c.launched(kHistK);
+  scan_exclusive(c, flat, nflat, offs, tot);
+
+  ScatterArgs a{};
+  a.in = in;
+  a.out = out;
+  a.rank = R;
+  a.nnz = N;
+  a.T = T;
+  a.chunks = chunks;
+  a.num_chunks = (uint32_t)num_chunks;
+  a.offs = offs;
+  a.run_start = run_start;
+  a.dig = dig;
   if (c.next_counter >= kCounters) {
     QD_CUDA(cudaMemsetAsync(c.counters, 0, kCounters * 4, c.st));
     c.next_counter = 0;
   }
-  a.tile_counter = c.counters + c.next_counter++;
-  const size_t smem = SweepLayout(a.T, a.rank).total;
-  void (*fn)(PassArgs) = k_onesweep<0>;
-  switch (a.rank) {
-    case 2: fn = k_onesweep<2>; break;
-    case 3: fn = k_onesweep<3>; break;
-    case 4: fn = k_onesweep<4>; break;
-    case 5: fn = k_onesweep<5>; break;
-    default: break;
-  }
+  a.chunk_counter = c.counters + c.next_counter++;
+  const size_t smem = ScatterLayout(T, R, in.soa != 0).total;
+  using Fn = void (*)(ScatterArgs);
+  Fn fn = nullptr;
+  const int rt = (R >= 2 && R <= 5) ? (int)R : 0;
+  const int fmt = (in.soa ? 2 : 0) | (out.soa ? 1 : 0);
+  fn = scatter_kernel(rt, fmt);
   int per_sm = 0;
   QD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kSortThreads, smem));
   const uint32_t grid =
-      (uint32_t)std::min<uint64_t>(a.num_tiles, (uint64_t)std::max(1, per_sm) * ws.num_sms);
+      (uint32_t)std::min<uint64_t>(num_chunks, (uint64_t)std::max(1, per_sm) * ws.num_sms);
   c.pre();
   fn<<<grid, kSortThreads, smem, c.st>>>(a);
   c.launched(kSweep);
+  if (offs_out) *offs_out = offs;
 }
 
 // One segmented stable sort (a plan group), src -> dst, with tmp scratch.
@@ -1426,11 +1484,13 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
   uint32_t TL = local_span(ws, R);
   if (bits + ceil_log2(TL) + 1 > 64) TL = 0;  // local key would not fit 64 bits
 
-  const TileDesc* tiles = nullptr;
+  const uint32_t CH = T * kChunkTiles;
+  ChunkDesc* chunks = ws.get<ChunkDesc>("chunks", 1);
   const unsigned long long* run_start = nullptr;
-  uint64_t num_tiles = 0, num_large = 0;
+  uint64_t num_chunks = 0;
   unsigned long long* seg = nullptr;
-  uint64_t S = 0;
+  uint64_t S = 0, num_large = 0;
+  bool small_runs = false;
 
   if (g.prefix.empty()) {
     if (TL && N <= TL) {
@@ -1441,114 +1501,63 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
       c.launched(kLocalK, 1);
       return;
     }
-    num_tiles = (N + T - 1) / T;
-    num_large = 1;
+    num_chunks = (N + CH - 1) / CH;
+    chunks = ws.get<ChunkDesc>("chunks", num_chunks);
+    c.pre();
+    k_uniform_chunks<<<(uint32_t)((num_chunks + kThreads - 1) / kThreads), kThreads, 0, c.st>>>(
+        N, CH, (uint32_t)num_chunks, chunks);
+    c.launched(kSegK);
   } else {
     S = find_runs(c, src_c, R, N, g.prefix, &seg);
     auto* is_large = ws.get<uint32_t>("run_large", S + 1);
-    auto* ntl = ws.get<uint32_t>("run_ntiles", S + 1);
+    auto* nch = ws.get<uint32_t>("run_nchunks", S + 1);
     auto* loff = ws.get<unsigned long long>("run_loff", S + 1);
-    auto* toff = ws.get<unsigned long long>("run_toff", S + 1);
+    auto* coff = ws.get<unsigned long long>("run_coff", S + 1);
     auto* totals = ws.get<unsigned long long>("run_totals", 2);
     auto* S_dev = ws.get<unsigned long long>("run_S", 1);
     ws.h_small[0] = S;
     QD_CUDA(cudaMemcpyAsync(S_dev, ws.h_small, 8, cudaMemcpyHostToDevice, c.st));
     const uint32_t grid = (uint32_t)std::min<uint64_t>((S + kThreads - 1) / kThreads, ws.num_sms * 8);
     c.pre();
-    k_classify<<<grid, kThreads, 0, c.st>>>(seg, S_dev, TL, T, is_large, ntl);
+    k_classify_chunks<<<grid, kThreads, 0, c.st>>>(seg, S_dev, TL, CH, is_large, nch);
     c.launched(kSegK);
     scan_exclusive(c, is_large, S, loff, totals);
-    scan_exclusive(c, ntl, S, toff, totals + 1);
+    scan_exclusive(c, nch, S, coff, totals + 1);
     QD_CUDA(cudaMemcpyAsync(ws.h_small + 1, totals, 16, cudaMemcpyDeviceToHost, c.st));
     QD_CUDA(cudaStreamSynchronize(c.st));
     num_large = ws.h_small[1];
-    num_tiles = ws.h_small[2];
-    if (num_tiles) {
-      auto* td = ws.get<TileDesc>("tiles", num_tiles);
+    num_chunks = ws.h_small[2];
+    small_runs = S > num_large;
+    if (num_chunks) {
+      chunks = ws.get<ChunkDesc>("chunks", num_chunks);
       auto* rs = ws.get<unsigned long long>("run_start", num_large);
       c.pre();
-      k_gen_tiles<<<grid, kThreads, 0, c.st>>>(seg, S_dev, T, is_large, loff, toff, td, rs);
+      k_gen_chunks<<<grid, kThreads, 0, c.st>>>(seg, S_dev, CH, is_large, loff, coff, chunks, rs);
       c.launched(kSegK);
-      tiles = td;
       run_start = rs;
     }
-    if (S > num_large) {
-      // small runs: chunks of runs starting in [c*TL, (c+1)*TL)
-      LocalArgs la{src_c, src_v, dst_c, dst_v, R, N, TL, 2 * TL, seg, S, key, c.err};
-      const size_t smem = LocalLayout(2 * TL, R, TL).total;
-      const uint64_t chunks = (N + TL - 1) / TL;
-      c.pre();
-      k_local<<<(uint32_t)chunks, kSortThreads, smem, c.st>>>(la);
-      c.launched(kLocalK);
+  }
+
+  if (num_chunks) {
+    Rows in{src_c, src_v, 0};
+    for (uint32_t q = 0; q < D; ++q) {
+      const bool last = q + 1 == D;
+      const bool to_dst = ((D - 1 - q) % 2) == 0;
+      RowsOut out{to_dst ? dst_c : tmp_c, to_dst ? dst_v : tmp_v, last ? 0 : 1};
+      run_pass(c, R, N, T, in, out, chunks, num_chunks, run_start, digs[q], key,
+               q == 0 && key.check);
+      in = Rows{out.c, out.v, out.soa};
     }
   }
-  if (num_tiles == 0) return;
-
-  // per-run digit histograms for all passes (+ range check of large-run rows)
-  const uint32_t stride = D * kBins;
-  auto* hist = ws.get<uint32_t>("hist", num_large * stride);
-  QD_CUDA(cudaMemsetAsync(hist, 0, num_large * stride * 4, c.st));
-  for (uint32_t p0 = 0; p0 < D; p0 += kHistPasses) {
-    HistArgs h{};
-    h.in_c = src_c;
-    h.rank = R;
-    h.nnz = N;
-    h.T = T;
-    h.tiles = tiles;
-    h.num_tiles = (uint32_t)num_tiles;
-    h.np = std::min<uint32_t>(kHistPasses, D - p0);
-    h.pass0 = p0;
-    h.hist = hist;
-    h.hist_stride = stride;
-    for (uint32_t q = 0; q < h.np; ++q) {
-      h.dig[q] = digs[p0 + q];
-      const uint32_t lo = (p0 + q) * per, hi = std::min(bits, lo + per);
-      h.shift[q] = lo;
-      h.mask[q] = (1u << (hi - lo)) - 1u;
-    }
-    h.fast = bits <= 64;
-    h.key = key;
-    h.do_check = p0 == 0 && key.check;
-    h.err = c.err;
-    h.rows_counter = p0 == 0 ? &c.err->rows[std::min(c.group, kMaxGroups - 1)] : nullptr;
-    uint32_t grid = ws.num_sms * 4;
-    if (tiles) {
-      h.tiles_per_cta = (uint32_t)std::max<uint64_t>(1, (num_tiles + grid - 1) / grid);
-      grid = (uint32_t)((num_tiles + h.tiles_per_cta - 1) / h.tiles_per_cta);
-    } else {
-      grid = (uint32_t)std::min<uint64_t>(ws.num_sms * 8, (N + 4095) / 4096);
-    }
+  if (small_runs) {
+    // small runs: chunks of runs starting in [c*TL, (c+1)*TL); after the
+    // passes, whose SoA intermediates may use dst's storage
+    LocalArgs la{src_c, src_v, dst_c, dst_v, R, N, TL, 2 * TL, seg, S, key, c.err};
+    const size_t smem = LocalLayout(2 * TL, R, TL).total;
+    const uint64_t nloc = (N + TL - 1) / TL;
     c.pre();
-    k_hist<<<grid, kThreads, (size_t)kWarps * h.np * kBins * 4, c.st>>>(h);
-    c.launched(kHistK);
-  }
-
-  auto* status = status_buffer(c, num_tiles);
-
-  const uint32_t* in_c = src_c;
-  const double* in_v = src_v;
-  for (uint32_t q = 0; q < D; ++q) {
-    const bool to_dst = ((D - 1 - q) % 2) == 0;
-    uint32_t* oc = to_dst ? dst_c : tmp_c;
-    double* ov = to_dst ? dst_v : tmp_v;
-    PassArgs a{};
-    a.in_c = in_c;
-    a.in_v = in_v;
-    a.out_c = oc;
-    a.out_v = ov;
-    a.rank = R;
-    a.nnz = N;
-    a.T = T;
-    a.tiles = tiles;
-    a.num_tiles = (uint32_t)num_tiles;
-    a.run_start = run_start;
-    a.hist = hist + (size_t)q * kBins;
-    a.hist_stride = stride;
-    a.status = status;
-    a.dig = digs[q];
-    launch_pass(c, a);
-    in_c = oc;
-    in_v = ov;
+    k_local<<<(uint32_t)nloc, kSortThreads, smem, c.st>>>(la);
+    c.launched(kLocalK);
   }
 }
 
@@ -1727,46 +1736,35 @@ void partition_rows_device(Workspace& ws, uint32_t rank, uint64_t nnz, const uin
   for (uint32_t p = 0; p < n_parts; ++p) part_counts[p] = 0;
   if (nnz == 0) return;
   const uint32_t T = sweep_tile_rows(ws, rank);
-  const uint64_t num_tiles = (nnz + T - 1) / T;
+  const uint32_t CH = T * kChunkTiles;
+  const uint64_t nc = (nnz + CH - 1) / CH;
+  ChunkDesc* chunks = ws.get<ChunkDesc>("chunks", nc);
+  c.pre();
+  k_uniform_chunks<<<(uint32_t)((nc + kThreads - 1) / kThreads), kThreads, 0, c.st>>>(
+      nnz, CH, (uint32_t)nc, chunks);
+  c.launched(kSegK);
   DigitSpec dig{};
   dig.lookup = d_lookup;
   dig.lookup_mode = mode;
   dig.lookup_dim = dim;
-  auto* hist = ws.get<uint32_t>("hist", kBins);
-  QD_CUDA(cudaMemsetAsync(hist, 0, kBins * 4, c.st));
-  HistArgs h{};
-  h.in_c = d_c_in;
-  h.rank = rank;
-  h.nnz = nnz;
-  h.T = T;
-  h.np = 1;
-  h.hist = hist;
-  h.hist_stride = kBins;
-  h.dig[0] = dig;
-  h.err = c.err;
-  const uint32_t grid = (uint32_t)std::min<uint64_t>(ws.num_sms * 4, (nnz + 4095) / 4096);
+  KeySpec key{};
+  unsigned long long* offs = nullptr;
+  run_pass(c, rank, nnz, T, Rows{d_c_in, d_v_in, 0}, RowsOut{d_c_out, d_v_out, 0}, chunks, nc,
+           nullptr, dig, key, false, &offs);
+  // part p starts at offs[p * nc] (bin-major flat layout of one run)
+  const uint32_t nb = std::min<uint32_t>(n_parts + 1, kBins);
+  auto* starts = ws.get<unsigned long long>("part_starts", kBins + 1);
   c.pre();
-  k_hist<<<grid, kThreads, (size_t)kWarps * h.np * kBins * 4, c.st>>>(h);
-  c.launched(kHistK);
-  auto* status = status_buffer(c, num_tiles);
-  PassArgs a{};
-  a.in_c = d_c_in;
-  a.in_v = d_v_in;
-  a.out_c = d_c_out;
-  a.out_v = d_v_out;
-  a.rank = rank;
-  a.nnz = nnz;
-  a.T = T;
-  a.num_tiles = (uint32_t)num_tiles;
-  a.hist = hist;
-  a.hist_stride = kBins;
-  a.status = status;
-  a.dig = dig;
-  launch_pass(c, a);
-  uint32_t* h_counts = reinterpret_cast<uint32_t*>(ws.h_small);
-  QD_CUDA(cudaMemcpyAsync(h_counts, hist, n_parts * 4, cudaMemcpyDeviceToHost, c.st));
+  k_gather_stride<<<1, kThreads, 0, c.st>>>(offs, nc, nb, starts);
+  c.launched(kOtherK);
+  QD_CUDA(cudaMemcpyAsync(ws.h_small, starts, nb * 8, cudaMemcpyDeviceToHost, c.st));
   QD_CUDA(cudaStreamSynchronize(c.st));
-  for (uint32_t p = 0; p < n_parts; ++p) part_counts[p] = h_counts[p];
+  for (uint32_t p = 0; p < n_parts; ++p) {
+    const uint64_t b = ws.h_small[p];
+    const uint64_t e = p + 1 < nb ? ws.h_small[p + 1] : nnz;
+    part_counts[p] = e - b;
+  }
+  check_errors(c);
 }
 
 }  // namespace qb200
