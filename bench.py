@@ -266,7 +266,7 @@ def main():
     value = units / (ms / 1e3) / 1e6
 
     # roofline of the dominant kernel class
-    top = max(("onesweep", "local", "hist"), key=lambda k: prof[k]["ms"])
+    top = max(("scatter", "local", "hist"), key=lambda k: prof[k]["ms"])
     p = prof[top]
     peak, peak_kind = peaks()
     achieved = (p["bytes"] / p["launches"]) / (p["ms"] / p["launches"] / 1e3) / 1e9 if p["ms"] else 0
@@ -318,8 +318,8 @@ def main():
         "vs_baseline": None, "dtype": "u32 coords + f64 values (moved, not computed)",
         "data": "synthetic (seeded Zipf stand-in for nell-2; FROSTT files unavailable offline)",
         "config": workload_config(cfg, n),
-        "roofline": {"bound": "hbm", "kernel": {"onesweep": "k_onesweep", "local": "k_local",
-                                                "hist": "k_hist"}[top],
+        "roofline": {"bound": "hbm", "kernel": {"scatter": "k_scatter", "local": "k_local",
+                                                "hist": "k_chunk_hist"}[top],
                      "achieved": round(achieved, 1), "peak": peak, "peak_kind": peak_kind,
                      "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                      "launches": p["launches"],

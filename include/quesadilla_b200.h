@@ -91,7 +91,7 @@ uint64_t qd_workspace_bytes(const qd_workspace* ws);
 uint64_t qd_workspace_launches(const qd_workspace* ws);
 
 /* Live per-kernel-class timing with CUDA events recorded on the launch
- * stream (off by default).  Classes: 0 onesweep digit pass, 1 histogram,
+ * stream (off by default).  Classes: 0 chunk-ordered digit scatter, 1 chunk histogram,
  * 2 local (in-CTA) run sort, 3 run discovery / scans, 4 other.  bytes is the
  * algorithmic traffic of the class (rows moved x 2 x row bytes for
  * classes 0 and 2, coordinates read for class 1). */

@@ -458,7 +458,7 @@ class Workspace:
     def launches(self) -> int:
         return int(lib().qd_workspace_launches(self._h))
 
-    PROFILE_CLASSES = ("onesweep", "hist", "local", "runs", "other")
+    PROFILE_CLASSES = ("scatter", "hist", "local", "runs", "other")
 
     def profile(self, enable: bool = True):
         """Live per-kernel-class CUDA-event timing inside the library."""

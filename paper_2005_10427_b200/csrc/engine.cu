@@ -388,21 +388,20 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }
 
 // A byte span [g, g+len) of global memory staged at dst so that byte g+k
-// lands at dst[head + k]: 16-byte aligned bulk body + (< 16 B) tail.
+// lands at dst[head + k]: the enclosing 16-byte-aligned blocks are copied
+// whole (a 16-byte block holding a valid byte never crosses a page, so the
+// few extra bytes are always readable; they are never used).
 struct Stage {
   const char* gal;  // 16-byte aligned start
   uint32_t head;    // g - gal
-  uint32_t bulk;    // bytes moved by TMA from gal
-  uint32_t tail;    // bytes after the bulk body, loaded by threads
+  uint32_t bulk;    // bytes moved by TMA from gal (multiple of 16)
 };
 __device__ __forceinline__ Stage make_stage(const void* g, uint32_t len) {
   const uintptr_t a = reinterpret_cast<uintptr_t>(g);
   Stage s;
   s.gal = reinterpret_cast<const char*>(a & ~uintptr_t(15));
   s.head = (uint32_t)(a & 15);
-  const uint32_t total = s.head + len;
-  s.bulk = total & ~15u;
-  s.tail = total - s.bulk;
+  s.bulk = (s.head + len + 15u) & ~15u;
   return s;
 }
 
@@ -417,6 +416,31 @@ __device__ __forceinline__ uint32_t digit_by(G get, const DigitSpec& d) {
 #pragma unroll 1
   for (uint32_t i = 1; i < d.n; ++i)
     v |= ((get(d.mode[i]) >> d.rsh[i]) & ((1u << d.bits[i]) - 1u)) << d.lsh[i];
+  return v;
+}
+
+// Register copy of a digit with at most two mode fields (the common case:
+// 8-bit digits rarely straddle more than one field boundary).
+struct Dig2 {
+  uint32_t two, m0, r0, k0, l0, m1, r1, k1, l1;
+};
+__device__ __forceinline__ Dig2 dig2_of(const DigitSpec& d) {
+  Dig2 f;
+  f.two = d.n > 1;
+  f.m0 = d.mode[0];
+  f.r0 = d.rsh[0];
+  f.k0 = (1u << d.bits[0]) - 1u;
+  f.l0 = d.lsh[0];
+  f.m1 = d.n > 1 ? d.mode[1] : d.mode[0];
+  f.r1 = d.n > 1 ? d.rsh[1] : 0u;
+  f.k1 = d.n > 1 ? (1u << d.bits[1]) - 1u : 0u;
+  f.l1 = d.n > 1 ? d.lsh[1] : 0u;
+  return f;
+}
+template <class G>
+__device__ __forceinline__ uint32_t digit2(G get, const Dig2& f) {
+  uint32_t v = ((get(f.m0) >> f.r0) & f.k0) << f.l0;
+  if (f.two) v |= ((get(f.m1) >> f.r1) & f.k1) << f.l1;
   return v;
 }
 
@@ -445,6 +469,8 @@ __global__ void __launch_bounds__(kThreads) k_chunk_hist(ChunkHistArgs a) {
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t R = a.rank;
   const uint64_t N = a.nnz;
+  const bool fast_dig = a.dig.lookup == nullptr && a.dig.n <= 2;
+  const Dig2 dg = dig2_of(a.dig);
   for (uint32_t ci = blockIdx.x; ci < a.num_chunks; ci += gridDim.x) {
     for (int k = threadIdx.x; k < kWarps * kBins; k += kThreads) s_h[k] = 0;
     __syncthreads();
@@ -457,12 +483,16 @@ __global__ void __launch_bounds__(kThreads) k_chunk_hist(ChunkHistArgs a) {
       const unsigned long long r = cd.row_begin + (valid ? i : 0u);
       uint32_t d = 0;
       if (a.in.soa) {
-        if (valid) d = digit_by([&](uint32_t m) { return __ldcs(a.in.c + m * N + r); }, a.dig);
+        if (valid) {
+          auto get = [&](uint32_t m) { return __ldcs(a.in.c + m * N + r); };
+          d = fast_dig ? digit2(get, dg) : digit_by(get, a.dig);
+        }
       } else {
         const uint32_t* row = a.in.c + r * R;
         if (valid) {
           if (a.do_check) check_row(row, a.key, r, a.err);
-          d = digit_by([&](uint32_t m) { return __ldg(row + m); }, a.dig);
+          auto get = [&](uint32_t m) { return __ldg(row + m); };
+          d = fast_dig ? digit2(get, dg) : digit_by(get, a.dig);
         }
       }
       add_runs(s_h + w * kBins, d, valid, nvalid);
@@ -532,6 +562,7 @@ __global__ void __launch_bounds__(kSortThreads, 2) k_scatter(ScatterArgs a) {
   uint32_t* s_ofs = reinterpret_cast<uint32_t*>(smem + L.ofs);  // [2][66] byte offsets
   unsigned long long* s_bar = reinterpret_cast<unsigned long long*>(smem + L.bar);
   __shared__ uint32_t s_chunk, s_tile;  // next (chunk, tile-in-chunk) to process
+  __shared__ ChunkDesc s_cd[2];          // descriptor of the chunk staged in buffer b
 
   // global address + byte length of span k of rows [rb, rb+n)
   auto span = [&](uint32_t k, unsigned long long rb, uint32_t n, const void*& g, uint32_t& len) {
@@ -556,6 +587,7 @@ __global__ void __launch_bounds__(kSortThreads, 2) k_scatter(ScatterArgs a) {
   // thread 0: issue the bulk loads of tile (ci, ti) into buffer b
   auto load_tile = [&](uint32_t b, uint32_t ci, uint32_t ti) {
     const ChunkDesc cd = a.chunks[ci];
+    s_cd[b] = cd;
     const unsigned long long rb = cd.row_begin + (unsigned long long)ti * a.T;
     const uint32_t n = (uint32_t)min((unsigned long long)a.T, cd.row_begin + cd.len - rb);
     const uint32_t ns = nspans();
@@ -582,7 +614,7 @@ __global__ void __launch_bounds__(kSortThreads, 2) k_scatter(ScatterArgs a) {
   // start loading it into buffer b
   auto advance = [&](uint32_t b, uint32_t ci, uint32_t ti, bool start) {
     uint32_t nc = ci, nt = ti + 1;
-    if (start || nt * (unsigned long long)a.T >= a.chunks[ci].len) {
+    if (start || nt * (unsigned long long)a.T >= s_cd[b ^ 1u].len) {
       nc = atomicAdd(a.chunk_counter, 1u);
       nt = 0;
     }
@@ -599,14 +631,16 @@ __global__ void __launch_bounds__(kSortThreads, 2) k_scatter(ScatterArgs a) {
   }
   __syncthreads();
 
+  const bool fast_dig = a.dig.lookup == nullptr && a.dig.n <= 2;
+  const Dig2 dg = dig2_of(a.dig);
   uint32_t phases = 0u;
   for (uint32_t it = 0;; ++it) {
     const uint32_t b = it & 1u;
     const uint32_t ci = s_chunk, ti = s_tile;
     if (ci >= a.num_chunks) break;
     __syncthreads();  // everyone has read s_chunk / s_tile
+    const ChunkDesc cd = s_cd[b];  // thread 0 only refills the other slot
     if (threadIdx.x == 0) advance(b ^ 1u, ci, ti, false);
-    const ChunkDesc cd = a.chunks[ci];
     const unsigned long long rb = cd.row_begin + (unsigned long long)ti * a.T;
     const uint32_t n = (uint32_t)min((unsigned long long)a.T, cd.row_begin + cd.len - rb);
     if (ti == 0 && threadIdx.x < kBins) {
@@ -617,22 +651,8 @@ __global__ void __launch_bounds__(kSortThreads, 2) k_scatter(ScatterArgs a) {
           a.offs[cd.coff * kBins + (size_t)threadIdx.x * cd.nchunks + cd.cidx] - base0 + rs;
     }
     for (int k = threadIdx.x; k < kSortWarps * kBins; k += kSortThreads) s_whist[k] = 0;
-    mbar_wait(&s_bar[b], (phases >> b) & 1u);
+    mbar_wait(&s_bar[b], (phases >> b) & 1u);  // each thread observes the TMA completion
     phases ^= 1u << b;
-    {  // sub-16-byte tails of every span: warp j loads span j's tail
-      const uint32_t j = threadIdx.x >> 5, lane = threadIdx.x & 31;
-      if (j < nspans()) {
-        const uint32_t k = span_index(j);
-        const void* g;
-        uint32_t len;
-        span(k, rb, n, g, len);
-        const Stage st = make_stage(g, len);
-        if (lane < st.tail / 4)
-          reinterpret_cast<uint32_t*>(span_dst(b, k) + st.bulk)[lane] =
-              reinterpret_cast<const uint32_t*>(st.gal + st.bulk)[lane];
-      }
-    }
-    __syncthreads();
     const uint32_t* sc = reinterpret_cast<const uint32_t*>(smem + L.c0 + b * L.cbuf);
     const double* s_v = reinterpret_cast<const double*>(span_dst(b, R) + s_ofs[b * 66 + R]);
     const uint32_t* s_ofsb = s_ofs + b * 66;
@@ -644,8 +664,13 @@ __global__ void __launch_bounds__(kSortThreads, 2) k_scatter(ScatterArgs a) {
                                                 s_ofsb[0] + (i * R + m) * 4);
     };
 
-    for (uint32_t i = threadIdx.x; i < n; i += kSortThreads)
-      s_dig[i] = (uint16_t)digit_by([&](uint32_t m) { return coord(i, m); }, a.dig);
+    if (fast_dig) {
+      for (uint32_t i = threadIdx.x; i < n; i += kSortThreads)
+        s_dig[i] = (uint16_t)digit2([&](uint32_t m) { return coord(i, m); }, dg);
+    } else {
+      for (uint32_t i = threadIdx.x; i < n; i += kSortThreads)
+        s_dig[i] = (uint16_t)digit_by([&](uint32_t m) { return coord(i, m); }, a.dig);
+    }
     __syncthreads();
     const uint32_t ipw = (n + kSortWarps - 1) / kSortWarps;
     warp_rank([&](uint32_t p) { return (uint32_t)s_dig[p]; }, n, ipw, s_rank, s_whist);
@@ -662,9 +687,14 @@ __global__ void __launch_bounds__(kSortThreads, 2) k_scatter(ScatterArgs a) {
       s_run[threadIdx.x] = r0 + cnt;
     }
     __syncthreads();
-    for (uint32_t i = threadIdx.x; i < n; i += kSortThreads) {
-      const uint32_t d = s_dig[i];
-      s_sorted[s_start[d] + s_whist[(i / ipw) * kBins + d] + s_rank[i]] = (uint16_t)i;
+    {  // sorted position of every row, warp by warp over its own stripe
+      const uint32_t w = threadIdx.x >> 5;
+      const uint32_t hi = min(n, (w + 1) * ipw);
+      const uint16_t* wh = s_whist + w * kBins;
+      for (uint32_t i = w * ipw + (threadIdx.x & 31); i < hi; i += 32) {
+        const uint32_t d = s_dig[i];
+        s_sorted[s_start[d] + wh[d] + s_rank[i]] = (uint16_t)i;
+      }
     }
     __syncthreads();
     for (uint32_t j = threadIdx.x; j < n; j += kSortThreads) {
@@ -826,10 +856,15 @@ __global__ void __launch_bounds__(kSortThreads) k_local(LocalArgs a) {
       if (threadIdx.x < kBins) s_start[threadIdx.x] = st;
     }
     __syncthreads();
-    for (uint32_t p = threadIdx.x; p < n; p += kSortThreads) {
-      const uint32_t it = cur[p];
-      const uint32_t d = (uint32_t)((s_key[it] >> sh) & (kBins - 1));
-      nxt[s_start[d] + s_whist[(p / ipw) * kBins + d] + s_rank[p]] = (uint16_t)it;
+    {
+      const uint32_t w = threadIdx.x >> 5;
+      const uint32_t hi = min(n, (w + 1) * ipw);
+      const uint16_t* wh = s_whist + w * kBins;
+      for (uint32_t p = w * ipw + (threadIdx.x & 31); p < hi; p += 32) {
+        const uint32_t it = cur[p];
+        const uint32_t d = (uint32_t)((s_key[it] >> sh) & (kBins - 1));
+        nxt[s_start[d] + wh[d] + s_rank[p]] = (uint16_t)it;
+      }
     }
     __syncthreads();
     uint16_t* t = cur;
