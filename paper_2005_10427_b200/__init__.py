@@ -42,7 +42,7 @@ from typing import List, Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libquesadilla_b200.so")
+LIB_PATH = os.environ.get("QD_LIB_PATH") or os.path.join(_HERE, "lib", "libquesadilla_b200.so")
 
 QD_OK, QD_INVALID_ARGUMENT, QD_OUT_OF_RANGE, QD_CUDA_ERROR, QD_NCCL_ERROR, QD_NO_DEVICE = range(6)
 KINDS = {"quesadilla": 0, "topk": 1, "radix": 2, "comparison": 3}

@@ -29,6 +29,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <string>
@@ -46,7 +48,10 @@ namespace qb200 {
 
 constexpr int kThreads = 256;       // utility kernels
 constexpr int kWarps = kThreads / 32;
-constexpr int kSortThreads = 512;   // k_scatter / k_local
+#ifndef QD_SORT_THREADS
+#define QD_SORT_THREADS 512
+#endif
+constexpr int kSortThreads = QD_SORT_THREADS;  // k_scatter / k_local
 constexpr int kSortWarps = kSortThreads / 32;
 constexpr int kRadixLog = 8;
 constexpr int kBins = 1 << kRadixLog;
@@ -54,6 +59,7 @@ constexpr int kMaxTerms = 12;
 constexpr int kMaxKeys = QD_MAX_RANK;
 constexpr int kHistPasses = 8;  // passes histogrammed per k_hist launch
 constexpr uint32_t kChunkTiles = 16;  // tiles per scatter chunk
+constexpr int kMaxRounds = 4096 / kSortThreads;  // 32-row rounds per warp per tile (T <= 4096)
 
 // ---------------------------------------------------------------------------
 // kernel parameter blocks
@@ -145,6 +151,8 @@ struct ChunkHistArgs {
 };
 
 struct ScatterArgs {
+  int dbg;  // experiment switches (QD_SCATTER_DBG): 1 = skip global stores
+  unsigned long long* dbg_t;  // QD_SCATTER_DBG & 2: per-phase clock totals
   Rows in;
   RowsOut out;
   uint32_t rank;
@@ -259,6 +267,9 @@ __device__ __forceinline__ unsigned long long block_excl_scan64(unsigned long lo
 // BITS ballots; cheaper than MATCH.ANY on sm_100.  Only lanes in `valid` count.
 template <int BITS = kRadixLog>
 __device__ __forceinline__ unsigned warp_peers(uint32_t d, unsigned valid) {
+#ifdef QD_MATCH_ANY
+  return __match_any_sync(0xFFFFFFFFu, d) & valid;
+#endif
   unsigned m = valid;
 #pragma unroll
   for (int b = 0; b < BITS; ++b) {
@@ -545,7 +556,7 @@ struct ScatterLayout {
 // RT: compile-time rank (0 = runtime); IN_SOA / OUT_SOA: row formats.
 // ---------------------------------------------------------------------------
 template <int RT, bool IN_SOA, bool OUT_SOA>
-__global__ void __launch_bounds__(kSortThreads, 2) k_scatter(ScatterArgs a) {
+__global__ void __launch_bounds__(kSortThreads, 1024 / kSortThreads) k_scatter(ScatterArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   const uint32_t R = RT ? RT : a.rank;
   const uint64_t N = a.nnz;
@@ -584,9 +595,13 @@ __global__ void __launch_bounds__(kSortThreads, 2) k_scatter(ScatterArgs a) {
     return smem + L.c0 + b * L.cbuf + (IN_SOA ? k * L.cspan : 0);
   };
 
-  // thread 0: issue the bulk loads of tile (ci, ti) into buffer b
-  auto load_tile = [&](uint32_t b, uint32_t ci, uint32_t ti) {
-    const ChunkDesc cd = a.chunks[ci];
+  // The advancer thread (lane 0 of the last warp, idle while the first
+  // kBins threads fold the bin counts) issues the bulk loads of the next tile.
+  // Chunks are assigned statically (blockIdx.x + k*gridDim.x): no atomics,
+  // and the next chunk's descriptor is loaded one chunk ahead.
+  constexpr uint32_t kAdv = kSortThreads - 32;
+  ChunkDesc pre{};  // advancer only: descriptor of this CTA's next chunk
+  auto load_tile = [&](uint32_t b, const ChunkDesc& cd, uint32_t ti) {
     s_cd[b] = cd;
     const unsigned long long rb = cd.row_begin + (unsigned long long)ti * a.T;
     const uint32_t n = (uint32_t)min((unsigned long long)a.T, cd.row_begin + cd.len - rb);
@@ -600,7 +615,8 @@ __global__ void __launch_bounds__(kSortThreads, 2) k_scatter(ScatterArgs a) {
       total += st.bulk;
       s_ofs[b * 66 + span_index(j)] = st.head;
     }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    // No proxy fence: the buffer was only READ by the generic proxy, and the
+    // CTA barrier that ended its last use orders those reads before this.
     mbar_expect_tx(&s_bar[b], total);
     for (uint32_t j = 0; j < ns; ++j) {
       const void* g;
@@ -610,37 +626,53 @@ __global__ void __launch_bounds__(kSortThreads, 2) k_scatter(ScatterArgs a) {
       if (st.bulk) bulk_g2s(span_dst(b, span_index(j)), st.gal, st.bulk, &s_bar[b]);
     }
   };
-  // thread 0: pick the tile after (ci, ti), publish it in s_chunk/s_tile and
-  // start loading it into buffer b
-  auto advance = [&](uint32_t b, uint32_t ci, uint32_t ti, bool start) {
+  // advancer: pick the tile after (ci, ti) (whose chunk is in slot b^1),
+  // publish it in s_chunk/s_tile and start loading it into buffer b
+  auto advance = [&](uint32_t b, uint32_t ci, uint32_t ti) {
     uint32_t nc = ci, nt = ti + 1;
-    if (start || nt * (unsigned long long)a.T >= s_cd[b ^ 1u].len) {
-      nc = atomicAdd(a.chunk_counter, 1u);
+    ChunkDesc cd = s_cd[b ^ 1u];
+    if (nt * (unsigned long long)a.T >= cd.len) {
+      nc = ci + gridDim.x;
       nt = 0;
+      cd = pre;
+      if (nc + gridDim.x < a.num_chunks) pre = a.chunks[nc + gridDim.x];
     }
     s_chunk = nc;
     s_tile = nt;
-    if (nc < a.num_chunks) load_tile(b, nc, nt);
+    if (nc < a.num_chunks) load_tile(b, cd, nt);
   };
 
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == kAdv) {
     mbar_init(&s_bar[0], 1);
     mbar_init(&s_bar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    advance(0, 0, 0, true);
+    const uint32_t c0 = blockIdx.x;
+    s_chunk = c0;
+    s_tile = 0;
+    if (c0 < a.num_chunks) {
+      if (c0 + gridDim.x < a.num_chunks) pre = a.chunks[c0 + gridDim.x];
+      load_tile(0, a.chunks[c0], 0);
+    }
   }
   __syncthreads();
 
   const bool fast_dig = a.dig.lookup == nullptr && a.dig.n <= 2;
   const Dig2 dg = dig2_of(a.dig);
   uint32_t phases = 0u;
+  long long t_last = clock64();
+#define QD_TMARK(ph)                                           \
+  if (a.dbg_t && threadIdx.x == 0) {                           \
+    const long long t_now = clock64();                         \
+    atomicAdd(a.dbg_t + (ph), (unsigned long long)(t_now - t_last)); \
+    t_last = t_now;                                            \
+  }
   for (uint32_t it = 0;; ++it) {
     const uint32_t b = it & 1u;
     const uint32_t ci = s_chunk, ti = s_tile;
     if (ci >= a.num_chunks) break;
     __syncthreads();  // everyone has read s_chunk / s_tile
-    const ChunkDesc cd = s_cd[b];  // thread 0 only refills the other slot
-    if (threadIdx.x == 0) advance(b ^ 1u, ci, ti, false);
+    QD_TMARK(1);
+    const ChunkDesc cd = s_cd[b];  // the advancer only refills the other slot
     const unsigned long long rb = cd.row_begin + (unsigned long long)ti * a.T;
     const uint32_t n = (uint32_t)min((unsigned long long)a.T, cd.row_begin + cd.len - rb);
     if (ti == 0 && threadIdx.x < kBins) {
@@ -650,33 +682,76 @@ __global__ void __launch_bounds__(kSortThreads, 2) k_scatter(ScatterArgs a) {
       s_run[threadIdx.x] =
           a.offs[cd.coff * kBins + (size_t)threadIdx.x * cd.nchunks + cd.cidx] - base0 + rs;
     }
-    for (int k = threadIdx.x; k < kSortWarps * kBins; k += kSortThreads) s_whist[k] = 0;
+    {  // each warp clears its own histogram (no block barrier before ranking)
+      uint16_t* whz = s_whist + (threadIdx.x >> 5) * kBins;
+      for (int k = threadIdx.x & 31; k < kBins; k += 32) whz[k] = 0;
+      __syncwarp();
+    }
     mbar_wait(&s_bar[b], (phases >> b) & 1u);  // each thread observes the TMA completion
+    QD_TMARK(2);
     phases ^= 1u << b;
     const uint32_t* sc = reinterpret_cast<const uint32_t*>(smem + L.c0 + b * L.cbuf);
     const double* s_v = reinterpret_cast<const double*>(span_dst(b, R) + s_ofs[b * 66 + R]);
     const uint32_t* s_ofsb = s_ofs + b * 66;
+    const unsigned char* scb = reinterpret_cast<const unsigned char*>(sc);
+    // byte offset of (row 0, mode m) in the staged tile, and the row stride
+    const uint32_t rstride = IN_SOA ? 4u : R * 4u;
+    auto mbase = [&](uint32_t m) -> uint32_t {
+      return IN_SOA ? m * (uint32_t)L.cspan + s_ofsb[m] : s_ofsb[0] + m * 4u;
+    };
     auto coord = [&](uint32_t i, uint32_t m) -> uint32_t {
-      if (IN_SOA)
-        return *reinterpret_cast<const uint32_t*>(reinterpret_cast<const unsigned char*>(sc) +
-                                                  m * L.cspan + s_ofsb[m] + i * 4);
-      return *reinterpret_cast<const uint32_t*>(reinterpret_cast<const unsigned char*>(sc) +
-                                                s_ofsb[0] + (i * R + m) * 4);
+      return *reinterpret_cast<const uint32_t*>(scb + mbase(m) + i * rstride);
+    };
+    // the digit's (at most two) fields, resolved once per tile
+    const uint32_t dbase0 = fast_dig ? mbase(dg.m0) : 0u;
+    const uint32_t dbase1 = fast_dig ? mbase(dg.m1) : 0u;
+    auto digit_at = [&](uint32_t i) -> uint32_t {
+      if (!fast_dig) return digit_by([&](uint32_t m) { return coord(i, m); }, a.dig);
+      const uint32_t x0 = *reinterpret_cast<const uint32_t*>(scb + dbase0 + i * rstride);
+      uint32_t v = ((x0 >> dg.r0) & dg.k0) << dg.l0;
+      if (dg.two) {
+        const uint32_t x1 = *reinterpret_cast<const uint32_t*>(scb + dbase1 + i * rstride);
+        v |= ((x1 >> dg.r1) & dg.k1) << dg.l1;
+      }
+      return v;
     };
 
-    if (fast_dig) {
-      for (uint32_t i = threadIdx.x; i < n; i += kSortThreads)
-        s_dig[i] = (uint16_t)digit2([&](uint32_t m) { return coord(i, m); }, dg);
-    } else {
-      for (uint32_t i = threadIdx.x; i < n; i += kSortThreads)
-        s_dig[i] = (uint16_t)digit_by([&](uint32_t m) { return coord(i, m); }, a.dig);
+    // Digits and stable warp ranks, kept in registers: warp w owns rows
+    // [w*ipw, (w+1)*ipw) and walks them in rounds of 32 (rank order = row
+    // order); packed[r] = (rank within the warp's equal digits << 8) | digit.
+    const uint32_t w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t ipw = (n + kSortWarps - 1) / kSortWarps;
+    const uint32_t lo = w * ipw, hi = min(n, lo + ipw);
+    uint16_t* wh = s_whist + w * kBins;
+    const unsigned below = (1u << lane) - 1u;
+    uint32_t packed[kMaxRounds];
+#pragma unroll
+    for (int r = 0; r < kMaxRounds; ++r) {
+      const uint32_t p = lo + r * 32 + lane;
+      if (lo + r * 32 >= hi) break;  // warp-uniform
+      const bool valid = p < hi;
+      uint32_t d = 0;
+      if (valid) {
+        d = digit_at(p);
+        s_dig[p] = (uint16_t)d;
+      }
+      unsigned peers = warp_peers(d, __ballot_sync(0xFFFFFFFFu, valid));
+      if (!valid) peers = 1u << lane;
+      const int leader = __ffs(peers) - 1;
+      uint32_t bcount = 0;
+      if (valid && lane == leader) {
+        bcount = wh[d];
+        wh[d] = (uint16_t)(bcount + __popc(peers));
+      }
+      bcount = __shfl_sync(0xFFFFFFFFu, bcount, leader);
+      packed[r] = ((bcount + __popc(peers & below)) << 8) | d;
     }
     __syncthreads();
-    const uint32_t ipw = (n + kSortWarps - 1) / kSortWarps;
-    warp_rank([&](uint32_t p) { return (uint32_t)s_dig[p]; }, n, ipw, s_rank, s_whist);
-    __syncthreads();
+    QD_TMARK(3);
+    if (threadIdx.x == kAdv) advance(b ^ 1u, ci, ti);  // overlaps bin_totals
     bin_totals<kSortThreads>(s_whist, s_cnt);
     __syncthreads();
+    QD_TMARK(4);
     const bool binthr = threadIdx.x < kBins;
     const uint32_t cnt = binthr ? s_cnt[threadIdx.x] : 0u;
     const uint32_t start = block_excl_scan<kSortThreads>(cnt, reinterpret_cast<uint32_t*>(s_tmp));
@@ -687,38 +762,43 @@ __global__ void __launch_bounds__(kSortThreads, 2) k_scatter(ScatterArgs a) {
       s_run[threadIdx.x] = r0 + cnt;
     }
     __syncthreads();
-    {  // sorted position of every row, warp by warp over its own stripe
-      const uint32_t w = threadIdx.x >> 5;
-      const uint32_t hi = min(n, (w + 1) * ipw);
-      const uint16_t* wh = s_whist + w * kBins;
-      for (uint32_t i = w * ipw + (threadIdx.x & 31); i < hi; i += 32) {
-        const uint32_t d = s_dig[i];
-        s_sorted[s_start[d] + wh[d] + s_rank[i]] = (uint16_t)i;
+    QD_TMARK(5);
+#pragma unroll
+    for (int r = 0; r < kMaxRounds; ++r) {  // sorted position of every row
+      const uint32_t p = lo + r * 32 + lane;
+      if (lo + r * 32 >= hi) break;
+      if (p < hi) {
+        const uint32_t d = packed[r] & 0xFFu;
+        s_sorted[s_start[d] + wh[d] + (packed[r] >> 8)] = (uint16_t)p;
       }
     }
     __syncthreads();
+    QD_TMARK(6);
+    uint32_t cb[RT > 0 ? RT : 1];
+    if (RT) {
+#pragma unroll
+      for (int m = 0; m < (RT > 0 ? RT : 1); ++m) cb[m] = mbase(m);
+    }
+    const uint32_t vbase = (uint32_t)(span_dst(b, R) - scb) + s_ofsb[R];
     for (uint32_t j = threadIdx.x; j < n; j += kSortThreads) {
       const uint32_t i = s_sorted[j];
       const unsigned long long dst = (unsigned long long)(s_gbase[s_dig[i]] + j);
-      if (OUT_SOA) {
-        if (RT) {
+      if (a.dbg & 1) continue;
+      const double v = *reinterpret_cast<const double*>(scb + vbase + i * 8u);
+      if (RT) {
 #pragma unroll
-          for (int m = 0; m < RT; ++m) __stcs(a.out.c + (size_t)m * N + dst, coord(i, m));
-        } else {
-          for (uint32_t m = 0; m < R; ++m) __stcs(a.out.c + (size_t)m * N + dst, coord(i, m));
+        for (int m = 0; m < (RT > 0 ? RT : 1); ++m) {
+          const uint32_t x = *reinterpret_cast<const uint32_t*>(scb + cb[m] + i * rstride);
+          __stcs(OUT_SOA ? a.out.c + (size_t)m * N + dst : a.out.c + dst * RT + m, x);
         }
       } else {
-        uint32_t* o = a.out.c + dst * R;
-        if (RT) {
-#pragma unroll
-          for (int m = 0; m < RT; ++m) __stcs(o + m, coord(i, m));
-        } else {
-          for (uint32_t m = 0; m < R; ++m) __stcs(o + m, coord(i, m));
-        }
+        for (uint32_t m = 0; m < R; ++m)
+          __stcs(OUT_SOA ? a.out.c + (size_t)m * N + dst : a.out.c + dst * R + m, coord(i, m));
       }
-      __stcs(a.out.v + dst, s_v[i]);
+      __stcs(a.out.v + dst, v);
     }
     __syncthreads();  // buffer b and the scratch are free again
+    QD_TMARK(7);
   }
 }
 
@@ -1314,7 +1394,9 @@ constexpr uint32_t kCounters = 4096;
 
 // Rows per onesweep tile / local chunk for a given rank, from the smem budget.
 uint32_t sweep_tile_rows(const Workspace& ws, uint32_t rank) {
-  const size_t budget = std::min<size_t>(ws.smem_optin, 112 * 1024);  // 2 CTAs/SM
+  if (const char* e = getenv("QD_TILE_ROWS")) return (uint32_t)atoi(e);
+  size_t budget = std::min<size_t>(ws.smem_optin, 112 * 1024);  // 2 CTAs/SM
+  if (const char* e = getenv("QD_SMEM_BUDGET")) budget = (size_t)atoi(e) * 1024;
   auto need = [&](uint32_t T) {
     return std::max(ScatterLayout(T, rank, false).total, ScatterLayout(T, rank, true).total);
   };
@@ -1409,6 +1491,11 @@ DigitSpec make_digit(const KeySpec& k, uint32_t lo, uint32_t hi) {
   return d;
 }
 
+uint32_t chunk_tiles() {
+  if (const char* e = getenv("QD_CHUNK_TILES")) return (uint32_t)atoi(e);
+  return kChunkTiles;
+}
+
 // One stable counting pass of digit `dig` over the chunks: chunk histograms,
 // (run, bin, chunk) exclusive scan, chunk-ordered scatter.
 void run_pass(Ctx& c, uint32_t R, uint64_t N, uint32_t T, Rows in, RowsOut out,
@@ -1449,6 +1536,11 @@ void run_pass(Ctx& c, uint32_t R, uint64_t N, uint32_t T, Rows in, RowsOut out,
   a.offs = offs;
   a.run_start = run_start;
   a.dig = dig;
+  if (const char* e = getenv("QD_SCATTER_DBG")) a.dbg = atoi(e);
+  if (a.dbg & 2) {
+    a.dbg_t = ws.get<unsigned long long>("dbg_t", 16);
+    QD_CUDA(cudaMemsetAsync(a.dbg_t, 0, 128, c.st));
+  }
   if (c.next_counter >= kCounters) {
     QD_CUDA(cudaMemsetAsync(c.counters, 0, kCounters * 4, c.st));
     c.next_counter = 0;
@@ -1467,6 +1559,14 @@ void run_pass(Ctx& c, uint32_t R, uint64_t N, uint32_t T, Rows in, RowsOut out,
   c.pre();
   fn<<<grid, kSortThreads, smem, c.st>>>(a);
   c.launched(kSweep);
+  if (a.dbg & 2) {
+    unsigned long long h[16];
+    QD_CUDA(cudaMemcpyAsync(h, a.dbg_t, 128, cudaMemcpyDeviceToHost, c.st));
+    QD_CUDA(cudaStreamSynchronize(c.st));
+    fprintf(stderr, "scatter phases (Mcycles, thread0 sum over CTAs): grid %u", grid);
+    for (int i = 1; i < 9; ++i) fprintf(stderr, " p%d=%.2f", i, h[i] / 1e6);
+    fprintf(stderr, "\n");
+  }
   if (offs_out) *offs_out = offs;
 }
 
@@ -1519,7 +1619,7 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
   uint32_t TL = local_span(ws, R);
   if (bits + ceil_log2(TL) + 1 > 64) TL = 0;  // local key would not fit 64 bits
 
-  const uint32_t CH = T * kChunkTiles;
+  const uint32_t CH = T * chunk_tiles();
   ChunkDesc* chunks = ws.get<ChunkDesc>("chunks", 1);
   const unsigned long long* run_start = nullptr;
   uint64_t num_chunks = 0;
@@ -1771,7 +1871,7 @@ void partition_rows_device(Workspace& ws, uint32_t rank, uint64_t nnz, const uin
   for (uint32_t p = 0; p < n_parts; ++p) part_counts[p] = 0;
   if (nnz == 0) return;
   const uint32_t T = sweep_tile_rows(ws, rank);
-  const uint32_t CH = T * kChunkTiles;
+  const uint32_t CH = T * chunk_tiles();
   const uint64_t nc = (nnz + CH - 1) / CH;
   ChunkDesc* chunks = ws.get<ChunkDesc>("chunks", nc);
   c.pre();
