@@ -267,8 +267,8 @@ __device__ __forceinline__ unsigned long long block_excl_scan64(unsigned long lo
 // BITS ballots; cheaper than MATCH.ANY on sm_100.  Only lanes in `valid` count.
 template <int BITS = kRadixLog>
 __device__ __forceinline__ unsigned warp_peers(uint32_t d, unsigned valid) {
-#ifdef QD_MATCH_ANY
-  return __match_any_sync(0xFFFFFFFFu, d) & valid;
+#ifndef QD_BALLOT_MATCH
+  return __match_any_sync(0xFFFFFFFFu, d) & valid;  // MATCH.ANY: one instruction
 #endif
   unsigned m = valid;
 #pragma unroll
@@ -487,6 +487,29 @@ __global__ void __launch_bounds__(kThreads) k_chunk_hist(ChunkHistArgs a) {
     __syncthreads();
     const ChunkDesc cd = a.chunks[ci];
     if (threadIdx.x == 0 && a.rows_counter) atomicAdd(a.rows_counter, (unsigned long long)cd.len);
+    if (a.in.soa && fast_dig && !dg.two) {
+      // SoA column, one-field digit: 16-byte loads of 4 rows per thread and
+      // per-warp shared-memory atomics (intermediate order has few runs)
+      const uint32_t* col = a.in.c + (size_t)dg.m0 * N + cd.row_begin;
+      const uint32_t head = (uint32_t)min((unsigned long long)cd.len,
+                                          (unsigned long long)((4u - ((uintptr_t)col >> 2)) & 3u));
+      uint32_t* wh = s_h + w * kBins;
+      if (threadIdx.x < head) atomicAdd(wh + ((col[threadIdx.x] >> dg.r0) & dg.k0), 1u);
+      const uint32_t nv = (cd.len - head) >> 2;
+      const uint4* vcol = reinterpret_cast<const uint4*>(col + head);
+#pragma unroll 2
+      for (uint32_t v = threadIdx.x; v < nv; v += kThreads) {
+        const uint4 x = __ldcs(vcol + v);
+        atomicAdd(wh + ((x.x >> dg.r0) & dg.k0), 1u);
+        atomicAdd(wh + ((x.y >> dg.r0) & dg.k0), 1u);
+        atomicAdd(wh + ((x.z >> dg.r0) & dg.k0), 1u);
+        atomicAdd(wh + ((x.w >> dg.r0) & dg.k0), 1u);
+      }
+      for (uint32_t k = head + nv * 4 + threadIdx.x; k < cd.len; k += kThreads)
+        atomicAdd(wh + ((col[k] >> dg.r0) & dg.k0), 1u);
+      __syncthreads();
+      goto flush;
+    }
     for (uint32_t g = w * 32; g < cd.len; g += kThreads) {  // warp-uniform
       const uint32_t i = g + lane;
       const bool valid = i < cd.len;
@@ -509,6 +532,7 @@ __global__ void __launch_bounds__(kThreads) k_chunk_hist(ChunkHistArgs a) {
       add_runs(s_h + w * kBins, d, valid, nvalid);
     }
     __syncthreads();
+    flush:
     uint32_t* f = a.flat + cd.coff * kBins + cd.cidx;
     for (int b = threadIdx.x; b < kBins; b += kThreads) {
       uint32_t v = 0;
@@ -555,7 +579,7 @@ struct ScatterLayout {
 // tile (warp ballots), and scatters it coalesced through shared memory.
 // RT: compile-time rank (0 = runtime); IN_SOA / OUT_SOA: row formats.
 // ---------------------------------------------------------------------------
-template <int RT, bool IN_SOA, bool OUT_SOA>
+template <int RT, bool IN_SOA, bool OUT_SOA, int DM>
 __global__ void __launch_bounds__(kSortThreads, 1024 / kSortThreads) k_scatter(ScatterArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   const uint32_t R = RT ? RT : a.rank;
@@ -601,32 +625,33 @@ __global__ void __launch_bounds__(kSortThreads, 1024 / kSortThreads) k_scatter(S
   // and the next chunk's descriptor is loaded one chunk ahead.
   constexpr uint32_t kAdv = kSortThreads - 32;
   ChunkDesc pre{};  // advancer only: descriptor of this CTA's next chunk
+  // called by the whole advancer warp: lane j issues span j's bulk copy
   auto load_tile = [&](uint32_t b, const ChunkDesc& cd, uint32_t ti) {
-    s_cd[b] = cd;
+    const uint32_t lane = threadIdx.x & 31;
+    if (lane == 0) s_cd[b] = cd;
     const unsigned long long rb = cd.row_begin + (unsigned long long)ti * a.T;
     const uint32_t n = (uint32_t)min((unsigned long long)a.T, cd.row_begin + cd.len - rb);
     const uint32_t ns = nspans();
-    uint32_t total = 0;
-    for (uint32_t j = 0; j < ns; ++j) {
+    uint32_t bulk = 0;
+    Stage st{};
+    if (lane < ns) {
       const void* g;
       uint32_t len;
-      span(span_index(j), rb, n, g, len);
-      const Stage st = make_stage(g, len);
-      total += st.bulk;
-      s_ofs[b * 66 + span_index(j)] = st.head;
+      span(span_index(lane), rb, n, g, len);
+      st = make_stage(g, len);
+      bulk = st.bulk;
+      s_ofs[b * 66 + span_index(lane)] = st.head;
     }
+    uint32_t total = bulk;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) total += __shfl_xor_sync(0xFFFFFFFFu, total, o);
     // No proxy fence: the buffer was only READ by the generic proxy, and the
     // CTA barrier that ended its last use orders those reads before this.
-    mbar_expect_tx(&s_bar[b], total);
-    for (uint32_t j = 0; j < ns; ++j) {
-      const void* g;
-      uint32_t len;
-      span(span_index(j), rb, n, g, len);
-      const Stage st = make_stage(g, len);
-      if (st.bulk) bulk_g2s(span_dst(b, span_index(j)), st.gal, st.bulk, &s_bar[b]);
-    }
+    if (lane == 0) mbar_expect_tx(&s_bar[b], total);
+    __syncwarp();
+    if (lane < ns && st.bulk) bulk_g2s(span_dst(b, span_index(lane)), st.gal, st.bulk, &s_bar[b]);
   };
-  // advancer: pick the tile after (ci, ti) (whose chunk is in slot b^1),
+  // advancer warp: pick the tile after (ci, ti) (whose chunk is in slot b^1),
   // publish it in s_chunk/s_tile and start loading it into buffer b
   auto advance = [&](uint32_t b, uint32_t ci, uint32_t ti) {
     uint32_t nc = ci, nt = ti + 1;
@@ -637,8 +662,10 @@ __global__ void __launch_bounds__(kSortThreads, 1024 / kSortThreads) k_scatter(S
       cd = pre;
       if (nc + gridDim.x < a.num_chunks) pre = a.chunks[nc + gridDim.x];
     }
-    s_chunk = nc;
-    s_tile = nt;
+    if ((threadIdx.x & 31) == 0) {
+      s_chunk = nc;
+      s_tile = nt;
+    }
     if (nc < a.num_chunks) load_tile(b, cd, nt);
   };
 
@@ -646,9 +673,14 @@ __global__ void __launch_bounds__(kSortThreads, 1024 / kSortThreads) k_scatter(S
     mbar_init(&s_bar[0], 1);
     mbar_init(&s_bar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x >= kAdv) {  // the advancer warp
     const uint32_t c0 = blockIdx.x;
-    s_chunk = c0;
-    s_tile = 0;
+    if (threadIdx.x == kAdv) {
+      s_chunk = c0;
+      s_tile = 0;
+    }
     if (c0 < a.num_chunks) {
       if (c0 + gridDim.x < a.num_chunks) pre = a.chunks[c0 + gridDim.x];
       load_tile(0, a.chunks[c0], 0);
@@ -703,15 +735,16 @@ __global__ void __launch_bounds__(kSortThreads, 1024 / kSortThreads) k_scatter(S
       return *reinterpret_cast<const uint32_t*>(scb + mbase(m) + i * rstride);
     };
     // the digit's (at most two) fields, resolved once per tile
-    const uint32_t dbase0 = fast_dig ? mbase(dg.m0) : 0u;
-    const uint32_t dbase1 = fast_dig ? mbase(dg.m1) : 0u;
+    const uint32_t dbase0 = DM ? mbase(dg.m0) : 0u;
+    const uint32_t dbase1 = DM == 2 ? mbase(dg.m1) : 0u;
+    // DM: 1 = digit inside one key field, 2 = spans two fields, 0 = general
     auto digit_at = [&](uint32_t i) -> uint32_t {
-      if (!fast_dig) return digit_by([&](uint32_t m) { return coord(i, m); }, a.dig);
+      if (DM == 0) return digit_by([&](uint32_t m) { return coord(i, m); }, a.dig);
       const uint32_t x0 = *reinterpret_cast<const uint32_t*>(scb + dbase0 + i * rstride);
-      uint32_t v = ((x0 >> dg.r0) & dg.k0) << dg.l0;
-      if (dg.two) {
+      uint32_t v = (x0 >> dg.r0) & dg.k0;
+      if (DM == 2) {
         const uint32_t x1 = *reinterpret_cast<const uint32_t*>(scb + dbase1 + i * rstride);
-        v |= ((x1 >> dg.r1) & dg.k1) << dg.l1;
+        v = (v << dg.l0) | (((x1 >> dg.r1) & dg.k1) << dg.l1);
       }
       return v;
     };
@@ -748,7 +781,7 @@ __global__ void __launch_bounds__(kSortThreads, 1024 / kSortThreads) k_scatter(S
     }
     __syncthreads();
     QD_TMARK(3);
-    if (threadIdx.x == kAdv) advance(b ^ 1u, ci, ti);  // overlaps bin_totals
+    if (threadIdx.x >= kAdv) advance(b ^ 1u, ci, ti);  // warp-wide; overlaps bin_totals
     bin_totals<kSortThreads>(s_whist, s_cnt);
     __syncthreads();
     QD_TMARK(4);
@@ -1243,22 +1276,29 @@ struct Workspace {
 };
 
 using ScatterFn = void (*)(ScatterArgs);
-template <int RT>
+template <int RT, int DM>
 ScatterFn scatter_kernel_fmt(int fmt) {
   switch (fmt) {
-    case 0: return k_scatter<RT, false, false>;
-    case 1: return k_scatter<RT, false, true>;
-    case 2: return k_scatter<RT, true, false>;
-    default: return k_scatter<RT, true, true>;
+    case 0: return k_scatter<RT, false, false, DM>;
+    case 1: return k_scatter<RT, false, true, DM>;
+    case 2: return k_scatter<RT, true, false, DM>;
+    default: return k_scatter<RT, true, true, DM>;
   }
 }
-ScatterFn scatter_kernel(int rt, int fmt) {
+template <int RT>
+ScatterFn scatter_kernel_dm(int dm, int fmt) {
+  switch (dm) {
+    case 1: return scatter_kernel_fmt<RT, 1>(fmt);
+    case 2: return scatter_kernel_fmt<RT, 2>(fmt);
+    default: return scatter_kernel_fmt<RT, 0>(fmt);
+  }
+}
+// rt: compile-time rank (3, 4 or 0 = runtime); dm: digit mode; fmt: in/out SoA bits
+ScatterFn scatter_kernel(int rt, int dm, int fmt) {
   switch (rt) {
-    case 2: return scatter_kernel_fmt<2>(fmt);
-    case 3: return scatter_kernel_fmt<3>(fmt);
-    case 4: return scatter_kernel_fmt<4>(fmt);
-    case 5: return scatter_kernel_fmt<5>(fmt);
-    default: return scatter_kernel_fmt<0>(fmt);
+    case 3: return scatter_kernel_dm<3>(dm, fmt);
+    case 4: return scatter_kernel_dm<4>(dm, fmt);
+    default: return scatter_kernel_dm<0>(dm, fmt);
   }
 }
 
@@ -1282,8 +1322,10 @@ Workspace* workspace_create(int device) {
     QD_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  optin - (int)fa.sharedSizeBytes));
   };
-  for (int rt : {0, 2, 3, 4, 5})
-    for (int fmt = 0; fmt < 4; ++fmt) allow_smem(reinterpret_cast<const void*>(scatter_kernel(rt, fmt)));
+  for (int rt : {0, 3, 4})
+    for (int dm = 0; dm < 3; ++dm)
+      for (int fmt = 0; fmt < 4; ++fmt)
+        allow_smem(reinterpret_cast<const void*>(scatter_kernel(rt, dm, fmt)));
   allow_smem(reinterpret_cast<const void*>(k_local));
   ws->smem_optin = optin - 1024;  // dynamic budget below the static usage
   return ws;
@@ -1491,9 +1533,13 @@ DigitSpec make_digit(const KeySpec& k, uint32_t lo, uint32_t hi) {
   return d;
 }
 
-uint32_t chunk_tiles() {
+// Tiles per chunk: chunks are statically dealt to the resident CTAs, so aim
+// for ~8 chunks per CTA (good balance) but at most kChunkTiles tiles each.
+uint32_t chunk_tiles(const Workspace& ws, uint64_t rows, uint32_t T) {
   if (const char* e = getenv("QD_CHUNK_TILES")) return (uint32_t)atoi(e);
-  return kChunkTiles;
+  const uint64_t ctas = (uint64_t)ws.num_sms * 2;
+  const uint64_t tiles = (rows + T - 1) / T;
+  return (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(kChunkTiles, tiles / (8 * ctas)));
 }
 
 // One stable counting pass of digit `dig` over the chunks: chunk histograms,
@@ -1549,9 +1595,10 @@ void run_pass(Ctx& c, uint32_t R, uint64_t N, uint32_t T, Rows in, RowsOut out,
   const size_t smem = ScatterLayout(T, R, in.soa != 0).total;
   using Fn = void (*)(ScatterArgs);
   Fn fn = nullptr;
-  const int rt = (R >= 2 && R <= 5) ? (int)R : 0;
+  const int rt = (R == 3 || R == 4) ? (int)R : 0;
   const int fmt = (in.soa ? 2 : 0) | (out.soa ? 1 : 0);
-  fn = scatter_kernel(rt, fmt);
+  const int dm = dig.lookup ? 0 : (dig.n == 1 ? 1 : (dig.n == 2 ? 2 : 0));
+  fn = scatter_kernel(rt, dm, fmt);
   int per_sm = 0;
   QD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kSortThreads, smem));
   const uint32_t grid =
@@ -1619,7 +1666,7 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
   uint32_t TL = local_span(ws, R);
   if (bits + ceil_log2(TL) + 1 > 64) TL = 0;  // local key would not fit 64 bits
 
-  const uint32_t CH = T * chunk_tiles();
+  const uint32_t CH = T * chunk_tiles(ws, N, T);
   ChunkDesc* chunks = ws.get<ChunkDesc>("chunks", 1);
   const unsigned long long* run_start = nullptr;
   uint64_t num_chunks = 0;
@@ -1871,7 +1918,7 @@ void partition_rows_device(Workspace& ws, uint32_t rank, uint64_t nnz, const uin
   for (uint32_t p = 0; p < n_parts; ++p) part_counts[p] = 0;
   if (nnz == 0) return;
   const uint32_t T = sweep_tile_rows(ws, rank);
-  const uint32_t CH = T * chunk_tiles();
+  const uint32_t CH = T * chunk_tiles(ws, nnz, T);
   const uint64_t nc = (nnz + CH - 1) / CH;
   ChunkDesc* chunks = ws.get<ChunkDesc>("chunks", nc);
   c.pre();
