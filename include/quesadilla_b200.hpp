@@ -1,0 +1,269 @@
+// quesadilla_b200.hpp — C++ drop-in for the reference's transpose API
+// (arxiv 2005.10427 artifact, proj/include/quesadilla/*.hpp), header-only
+// over the C ABI in quesadilla_b200.h.  Same names, argument meaning and
+// exception classes as namespace quesadilla; a caller switches by changing
+// the namespace (and linking libquesadilla_b200.so).  Every transpose runs as
+// sm_100a kernels; there is no CPU path.
+//
+//   reference                                  here
+//   quesadilla::Ordering (ordering.hpp:38)     quesadilla_b200::Ordering
+//   quesadilla::CooTensor (coo.hpp:16)         quesadilla_b200::CooTensor
+//   quesadilla::PlanStep / SortPlan (plan.hpp) quesadilla_b200::PlanStep / SortPlan
+//   quesadilla_plan / prefix_plan (planner.hpp:27-34)
+//   SortStrategy / TransposeOptions (transpose.hpp:18-54)
+//   Workspace (sort.hpp:14)                    device workspace (one GPU)
+//   transpose_inplace / transpose (transpose.hpp:59-66)
+//   partial_sort (sort.hpp:32) / parallel_partial_sort (parallel.hpp:35)
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "quesadilla_b200.h"
+
+namespace quesadilla_b200 {
+
+using Mode = std::uint32_t;
+inline constexpr Mode kMaxRank = QD_MAX_RANK;
+
+namespace detail {
+inline void check(qd_status s) {
+  switch (s) {
+    case QD_OK: return;
+    case QD_INVALID_ARGUMENT: throw std::invalid_argument(qd_last_error());
+    case QD_OUT_OF_RANGE: throw std::out_of_range(qd_last_error());
+    default: throw std::runtime_error(std::string("quesadilla_b200: ") + qd_last_error());
+  }
+}
+}  // namespace detail
+
+class Ordering {
+ public:
+  explicit Ordering(std::vector<Mode> modes) : modes_(std::move(modes)) {
+    const std::size_t r = modes_.size();
+    if (r == 0 || r > kMaxRank) throw std::invalid_argument("ordering rank must be in 1..64");
+    std::uint64_t seen = 0;
+    for (Mode m : modes_) {
+      if (m >= r) throw std::invalid_argument("ordering contains mode outside 0..r-1");
+      if (seen & (std::uint64_t{1} << m)) throw std::invalid_argument("ordering repeats a mode");
+      seen |= std::uint64_t{1} << m;
+    }
+  }
+  static Ordering simple(Mode rank) {
+    std::vector<Mode> m(rank);
+    for (Mode i = 0; i < rank; ++i) m[i] = i;
+    return Ordering(std::move(m));
+  }
+  Mode rank() const { return static_cast<Mode>(modes_.size()); }
+  Mode at(std::size_t i) const { return modes_[i]; }
+  const std::vector<Mode>& modes() const { return modes_; }
+  bool is_simple() const {
+    for (std::size_t i = 0; i < modes_.size(); ++i)
+      if (modes_[i] != i) return false;
+    return true;
+  }
+  friend bool operator==(const Ordering&, const Ordering&) = default;
+
+ private:
+  std::vector<Mode> modes_;
+};
+
+struct PlanStep {
+  Mode prefix_len = 0;
+  Mode mode = 0;
+  bool bucketed() const { return prefix_len > 0; }
+  friend bool operator==(const PlanStep&, const PlanStep&) = default;
+};
+
+struct SortPlan {
+  Ordering target;
+  std::vector<PlanStep> steps;
+};
+
+struct PlanCost {
+  int total_passes = 0;
+  int bucketed_passes = 0;
+  friend bool operator==(const PlanCost&, const PlanCost&) = default;
+};
+
+struct CooTensor {
+  std::vector<std::uint32_t> dims;
+  std::vector<std::uint32_t> coords;  // nnz * rank, row-major
+  std::vector<double> values;         // nnz
+  Mode rank() const { return static_cast<Mode>(dims.size()); }
+  std::size_t nnz() const { return values.size(); }
+  std::uint32_t coord(std::size_t row, Mode mode) const { return coords[row * dims.size() + mode]; }
+  friend bool operator==(const CooTensor&, const CooTensor&) = default;
+};
+
+namespace detail {
+inline SortPlan plan_call(const Ordering& target, Mode want) {
+  std::vector<qd_plan_step> buf(4096);
+  std::uint32_t n = 0;
+  if (want == 0)
+    check(qd_quesadilla_plan(target.modes().data(), target.rank(), buf.data(), 4096, &n));
+  else
+    check(qd_prefix_plan(target.modes().data(), target.rank(), want, buf.data(), 4096, &n));
+  SortPlan p{target, {}};
+  for (std::uint32_t i = 0; i < n; ++i) p.steps.push_back({buf[i].prefix_len, buf[i].mode});
+  return p;
+}
+}  // namespace detail
+
+inline SortPlan quesadilla_plan(const Ordering& target) { return detail::plan_call(target, 0); }
+inline SortPlan prefix_plan(const Ordering& target, Mode prefix_len) {
+  if (prefix_len < 1 || prefix_len > target.rank())
+    throw std::invalid_argument("prefix length must be in 1..rank");
+  return detail::plan_call(target, prefix_len);
+}
+inline int required_sort_count(const Ordering& source, const Ordering& target) {
+  if (source.rank() != target.rank()) throw std::invalid_argument("source and target ranks differ");
+  int out = 0;
+  detail::check(qd_required_sort_count(source.modes().data(), target.modes().data(),
+                                       target.rank(), &out));
+  return out;
+}
+inline Ordering apply_transition(const Ordering& current, const PlanStep& step) {
+  std::vector<Mode> next(current.rank());
+  detail::check(qd_apply_transition(current.modes().data(), current.rank(),
+                                    qd_plan_step{step.prefix_len, step.mode}, next.data()));
+  return Ordering(std::move(next));
+}
+inline Ordering simulate_plan(const SortPlan& plan) {
+  Ordering o = Ordering::simple(plan.target.rank());
+  for (const PlanStep& s : plan.steps) o = apply_transition(o, s);
+  return o;
+}
+inline PlanCost plan_cost(const SortPlan& plan) {
+  PlanCost c;
+  c.total_passes = static_cast<int>(plan.steps.size());
+  for (const PlanStep& s : plan.steps) c.bucketed_passes += s.bucketed();
+  return c;
+}
+
+struct SortStrategy {
+  enum class Kind { Quesadilla, TopK, FullRadix, ComparisonSort };
+  Kind kind = Kind::Quesadilla;
+  Mode k = 0;
+  static SortStrategy quesadilla() { return {Kind::Quesadilla, 0}; }
+  static SortStrategy top_k(Mode k) { return {Kind::TopK, k}; }
+  static SortStrategy splatt_style() { return top_k(1); }
+  static SortStrategy full_radix() { return {Kind::FullRadix, 0}; }
+  static SortStrategy comparison_sort() { return {Kind::ComparisonSort, 0}; }
+  std::string name() const {
+    switch (kind) {
+      case Kind::Quesadilla: return "quesadilla";
+      case Kind::TopK: return "top" + std::to_string(k);
+      case Kind::FullRadix: return "radix";
+      case Kind::ComparisonSort: return "comparison";
+    }
+    return "?";
+  }
+  qd_strategy_kind c_kind() const {
+    switch (kind) {
+      case Kind::Quesadilla: return QD_QUESADILLA;
+      case Kind::TopK: return QD_TOPK;
+      case Kind::FullRadix: return QD_FULL_RADIX;
+      default: return QD_COMPARISON_SORT;
+    }
+  }
+  friend bool operator==(const SortStrategy&, const SortStrategy&) = default;
+};
+
+inline PlanCost strategy_pass_cost(const SortStrategy& s, const Ordering& target) {
+  PlanCost c;
+  detail::check(qd_strategy_pass_cost(s.c_kind(), s.k, target.modes().data(), target.rank(),
+                                      &c.total_passes, &c.bucketed_passes));
+  return c;
+}
+
+struct ParallelConfig {
+  unsigned workers = 1;  // accepted for API parity; 0 is rejected like the reference
+  static ParallelConfig serial() { return {}; }
+  static ParallelConfig with_workers(unsigned p) { return {p}; }
+};
+
+struct TransposeOptions {
+  bool verify_input = false;
+  ParallelConfig parallel = ParallelConfig::serial();
+  std::vector<PlanStep>* pass_log = nullptr;
+  // device extra: the output's leading-mode run starts + nnz (CSF pos array)
+  std::vector<std::uint64_t>* boundaries = nullptr;
+};
+
+// Device workspace (cached HBM buffers on one GPU); reuse across calls,
+// never concurrently.
+class Workspace {
+ public:
+  explicit Workspace(int device = 0) { detail::check(qd_workspace_create(device, &ws_)); }
+  ~Workspace() { qd_workspace_destroy(ws_); }
+  Workspace(const Workspace&) = delete;
+  Workspace& operator=(const Workspace&) = delete;
+  qd_workspace* get() const { return ws_; }
+
+ private:
+  qd_workspace* ws_ = nullptr;
+};
+
+inline void transpose_inplace(CooTensor& t, const Ordering& target, const SortStrategy& s,
+                              Workspace& ws, const TransposeOptions& opts = {}) {
+  if (target.rank() != t.rank())
+    throw std::invalid_argument("target ordering rank does not match tensor");
+  std::vector<qd_plan_step> log(4096);
+  std::uint32_t nlog = 0;
+  std::vector<std::uint64_t> bounds;
+  std::uint64_t nb = 0;
+  qd_options o{};
+  o.verify_input = opts.verify_input;
+  o.workers = opts.parallel.workers;
+  o.pass_log = log.data();
+  o.pass_log_capacity = 4096;
+  o.pass_log_len = &nlog;
+  if (opts.boundaries) {
+    bounds.resize(t.nnz() + 1);
+    o.boundaries = bounds.data();
+    o.n_boundaries = &nb;
+  }
+  detail::check(qd_transpose_inplace(t.rank(), t.dims.data(), t.nnz(), t.coords.data(),
+                                     t.values.data(), target.modes().data(), s.c_kind(), s.k, &o,
+                                     ws.get()));
+  if (opts.pass_log)
+    for (std::uint32_t i = 0; i < nlog; ++i) opts.pass_log->push_back({log[i].prefix_len, log[i].mode});
+  if (opts.boundaries) opts.boundaries->assign(bounds.begin(), bounds.begin() + nb);
+}
+
+inline CooTensor transpose(const CooTensor& t, const Ordering& target, const SortStrategy& s,
+                           const TransposeOptions& opts = {}) {
+  CooTensor out = t;
+  Workspace ws;
+  transpose_inplace(out, target, s, ws, opts);
+  return out;
+}
+
+inline CooTensor full_radix_transpose(const CooTensor& t, const Ordering& target,
+                                      const TransposeOptions& opts = {}) {
+  return transpose(t, target, SortStrategy::full_radix(), opts);
+}
+inline CooTensor comparison_transpose(const CooTensor& t, const Ordering& target) {
+  return transpose(t, target, SortStrategy::comparison_sort());
+}
+inline CooTensor topk_transpose(const CooTensor& t, const Ordering& target, Mode k,
+                                const TransposeOptions& opts = {}) {
+  return transpose(t, target, SortStrategy::top_k(k), opts);
+}
+
+inline void partial_sort(CooTensor& t, const std::vector<Mode>& prefix, Mode mode, Workspace& ws) {
+  detail::check(qd_partial_sort(t.rank(), t.dims.data(), t.nnz(), t.coords.data(),
+                                t.values.data(), prefix.data(),
+                                static_cast<std::uint32_t>(prefix.size()), mode, ws.get()));
+}
+inline void parallel_partial_sort(CooTensor& t, const std::vector<Mode>& prefix, Mode mode,
+                                  Workspace& ws, const ParallelConfig& cfg) {
+  if (cfg.workers == 0) throw std::invalid_argument("worker count must be at least 1");
+  partial_sort(t, prefix, mode, ws);
+}
+
+}  // namespace quesadilla_b200

@@ -1,0 +1,221 @@
+"""Multi-GPU transpose: one process per GPU, sharded by the range of the
+output's leading mode sigma1.
+
+Every rank holds a contiguous slice of the input rows (the global input is
+sorted in the simple order, slices in rank order).  The output of rank g is
+the slice of the global output whose sigma1 values fall in rank g's range, so
+the concatenation of the rank outputs in rank order is exactly the reference
+transpose of the global tensor:
+
+* sigma1 == 0 (the plan's first step is bucketed, e.g. (0,2,1)): the slices
+  are already sigma1-aligned when no mode-0 run straddles two ranks
+  (``aligned_bounds`` produces such slices) — every rank transposes its own
+  rows, no communication (the GPU lift of parallel.cpp:125-139).
+* otherwise (e.g. (1,0,2)): one exchange.  Global histogram of sigma1
+  (all_reduce of each rank's ``qd_mode_histogram_device``), splitters that
+  balance rows at sigma1-value boundaries, a stable device partition of the
+  local rows into destination parts (``qd_partition_rows_device``), one
+  all_to_all over NCCL/NVLink, and the received parts concatenated in SOURCE
+  RANK order — a subsequence of the simply sorted input, hence still simply
+  sorted — then the full local Quesadilla plan.
+
+The local work goes through a backend: ``GpuBackend`` (the CUDA library) in
+the product; tests substitute a CPU backend to check the host logic with
+world_size 2 over gloo.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import List, Sequence
+
+import numpy as np
+
+
+def splitters(hist: np.ndarray, parts: int) -> np.ndarray:
+    """Cut sigma1 values 0..dim-1 into `parts` contiguous value ranges with
+    balanced row counts; returns part id per sigma1 value (uint32[dim])."""
+    hist = np.asarray(hist, np.int64)
+    dim = len(hist)
+    total = int(hist.sum())
+    cum = np.cumsum(hist)
+    lookup = np.zeros(dim, np.uint32)
+    if total == 0 or parts == 1:
+        return lookup
+    # value v goes to part floor(rows strictly before v's end * parts / total)
+    # using the midpoint of v's rows so an indivisible head value lands once
+    mid = cum - hist / 2.0
+    lookup[:] = np.minimum(parts - 1, np.floor(mid * parts / total)).astype(np.uint32)
+    # monotone by construction (cum is non-decreasing)
+    return lookup
+
+
+def aligned_bounds(mode0: np.ndarray, parts: int) -> List[int]:
+    """Row bounds of `parts` contiguous slices of a simply sorted tensor with
+    no mode-0 run split across slices (parallel.cpp:125-139)."""
+    n = len(mode0)
+    b = [0]
+    for p in range(1, parts):
+        j = n * p // parts
+        while 0 < j < n and mode0[j] == mode0[j - 1]:
+            j += 1
+        b.append(max(j, b[-1]))
+    b.append(n)
+    return b
+
+
+@dataclass
+class LocalRows:
+    """A rank's rows: coords (int32/uint32, n*rank) and values (f64, n) on the
+    backend's device."""
+    coords: object
+    values: object
+
+    def nnz(self) -> int:
+        return int(self.values.shape[0])
+
+
+class GpuBackend:
+    """Local work on this rank's GPU through the C ABI."""
+
+    def __init__(self, device: int, ws=None):
+        import torch
+
+        import paper_2005_10427_b200 as qd
+        self.qd, self.torch = qd, torch
+        self.device = torch.device("cuda", device)
+        self.ws = ws or qd.Workspace(device)
+
+    def stream(self):
+        return self.torch.cuda.current_stream(self.device).cuda_stream
+
+    def zeros_like_rows(self, n, rank):
+        t = self.torch
+        return LocalRows(t.empty(n * rank, dtype=t.int32, device=self.device),
+                         t.empty(n, dtype=t.float64, device=self.device))
+
+    def mode_hist(self, rows: LocalRows, rank: int, mode: int, dim: int):
+        t = self.torch
+        h = t.zeros(dim, dtype=t.int64, device=self.device)
+        if rows.nnz():
+            self.qd.mode_histogram_device(rank, rows.nnz(), rows.coords.data_ptr(), mode, dim,
+                                          h.data_ptr(), self.ws, self.stream())
+        return h
+
+    def partition(self, rows: LocalRows, rank: int, mode: int, lookup: np.ndarray, parts: int):
+        t = self.torch
+        out = self.zeros_like_rows(rows.nnz(), rank)
+        lk = t.from_numpy(np.ascontiguousarray(lookup).view(np.int32)).to(self.device)
+        counts = self.qd.partition_rows_device(rank, rows.nnz(), rows.coords.data_ptr(),
+                                               rows.values.data_ptr(), mode, len(lookup),
+                                               lk.data_ptr(), parts, out.coords.data_ptr(),
+                                               out.values.data_ptr(), self.ws, self.stream())
+        return out, counts
+
+    def transpose(self, rows: LocalRows, dims, target) -> LocalRows:
+        out = self.zeros_like_rows(rows.nnz(), len(dims))
+        if rows.nnz():
+            self.qd.transpose_device(len(dims), dims, rows.nnz(), rows.coords.data_ptr(),
+                                     rows.values.data_ptr(), out.coords.data_ptr(),
+                                     out.values.data_ptr(), target,
+                                     self.qd.SortStrategy.quesadilla(), self.ws, self.stream())
+        return out
+
+    def to_numpy_i64(self, h):
+        return h.cpu().numpy()
+
+    def from_numpy_i64(self, a):
+        return self.torch.from_numpy(np.asarray(a, np.int64)).to(self.device)
+
+
+def exchange(dist, be, rows: LocalRows, counts: Sequence[int], rank_modes: int) -> LocalRows:
+    """all_to_all of the partitioned rows; part p of every rank goes to rank p
+    and the received parts are concatenated in source-rank order."""
+    world = dist.get_world_size()
+    send = be.from_numpy_i64(np.asarray(counts, np.int64))
+    recv = be.from_numpy_i64(np.zeros(world, np.int64))
+    dist.all_to_all_single(recv, send)
+    rc = [int(x) for x in be.to_numpy_i64(recv)]
+    out = be.zeros_like_rows(sum(rc), rank_modes)
+    dist.all_to_all_single(out.coords, rows.coords, [c * rank_modes for c in rc],
+                           [int(c) * rank_modes for c in counts])
+    dist.all_to_all_single(out.values, rows.values, rc, [int(c) for c in counts])
+    return out
+
+
+def sharded_transpose(dist, be, rows: LocalRows, dims: Sequence[int], target: Sequence[int]):
+    """Transpose the global tensor whose rank-ordered slices are `rows`;
+    returns this rank's slice of the global output (and whether an exchange
+    was needed).  For target[0] == 0 the input slices must be mode-0 aligned
+    (see aligned_bounds)."""
+    r = len(dims)
+    target = [int(x) for x in target]
+    world = dist.get_world_size()
+    if world == 1 or target[0] == 0:
+        return be.transpose(rows, dims, target), False
+    s1 = target[0]
+    h = be.mode_hist(rows, r, s1, dims[s1])
+    dist.all_reduce(h)
+    lookup = splitters(be.to_numpy_i64(h), world)
+    parts, counts = be.partition(rows, r, s1, lookup, world)
+    recv = exchange(dist, be, parts, counts, r)
+    return be.transpose(recv, dims, target), True
+
+
+def bench_sharded(args, cfg, dist, rank, world, local):
+    """bench.py --gpus N: weak scaling.  Each rank generates its own
+    c2-shaped slice with mode-0 values offset by rank, so the global tensor
+    (dims[0] * N) x dims[1] x dims[2] is the rank-ordered concatenation, simply
+    sorted; every step transposes it to all 5 targets (the (0,2,1) target
+    without communication, the others with one all_to_all)."""
+    import json
+    import time
+
+    import torch
+
+    from paper_2005_10427_b200 import synth
+    torch.cuda.set_device(local)
+    ci, vi = synth.generate_torch(cfg, args.nnz, seed=cfg.seed + 1000 * rank, device="cuda")
+    r = len(cfg.dims)
+    dims = list(cfg.dims)
+    ci = ci.view(-1, r)
+    ci[:, 0] += rank * dims[0]
+    ci = ci.reshape(-1).contiguous()
+    gdims = [dims[0] * world] + dims[1:]
+    be = GpuBackend(local)
+    rows = LocalRows(ci, vi)
+    n_local = vi.numel()
+
+    def step():
+        for t in cfg.targets:
+            sharded_transpose(dist, be, rows, gdims, t)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    dist.barrier()
+    ms = torch.tensor([e0.elapsed_time(e1)], device="cuda")
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    total = torch.tensor([n_local], device="cuda", dtype=torch.int64)
+    dist.all_reduce(total)
+    if rank == 0:
+        units = int(total.item()) * len(cfg.targets) * args.steps
+        v = units / (ms.item() / 1e3) / 1e6
+        print(json.dumps({
+            "metric": "nonzeros transposed/sec (Mnnz/s)", "value": round(v, 3), "unit": "Mnnz/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms.item() / args.steps, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None,
+            "dtype": "u32 coords + f64 values (moved, not computed)",
+            "data": "synthetic (seeded Zipf, per-rank slices of one global tensor)",
+            "config": {"workload": f"c2 x {world}: {gdims[0]}x{gdims[1]}x{gdims[2]}, "
+                                   f"{int(total.item())} nnz, 5 targets",
+                       "parallelism": f"shard{world} (sigma1 ranges; all_to_all over NCCL)"},
+        }))
+    dist.destroy_process_group()

@@ -2,6 +2,7 @@
 (coords by value, values by raw f64 bits).  Mirrors the reference's own test
 strategy (proj/tests/test_sort.cpp, test_parallel.cpp, acceptance.cpp)."""
 import itertools
+import os
 
 import numpy as np
 import pytest
@@ -321,3 +322,45 @@ def test_device_api_with_torch(ws):
     assert b[:nb].cpu().numpy().tolist() == list(starts) + [t.nnz()]
     assert qd.is_sorted_device(3, t.nnz(), co.data_ptr(), [1, 0, 2], ws=ws)
     assert not qd.is_sorted_device(3, t.nnz(), co.data_ptr(), [0, 1, 2], ws=ws)
+
+
+# --- multi-GPU building blocks on one GPU ---------------------------------------
+
+def test_partition_rows_and_mode_hist(ws):
+    import torch
+    from paper_2005_10427_b200 import shard
+    rng = np.random.default_rng(12)
+    t = rand_tensor(rng, [50, 700, 90], 300_000)
+    be = shard.GpuBackend(0, ws)
+    rows = shard.LocalRows(torch.from_numpy(t.coords.view(np.int32)).cuda(),
+                           torch.from_numpy(t.values).cuda())
+    h = be.to_numpy_i64(be.mode_hist(rows, 3, 1, 700))
+    c = t.coords.reshape(-1, 3)
+    assert np.array_equal(h, np.bincount(c[:, 1], minlength=700))
+    for parts in (1, 2, 5, 8):
+        lk = shard.splitters(h, parts)
+        out, counts = be.partition(rows, 3, 1, lk, parts)
+        part = lk[c[:, 1]]
+        order = np.argsort(part, kind="stable")  # stable partition = reference order inside parts
+        assert counts == np.bincount(part, minlength=parts).tolist()
+        assert np.array_equal(out.coords.cpu().numpy().view(np.uint32).reshape(-1, 3), c[order])
+        assert np.array_equal(out.values.cpu().numpy(), t.values[order])
+
+
+def test_sharded_single_rank_is_plain_transpose(ws):
+    import torch
+    import torch.distributed as dist
+    from paper_2005_10427_b200 import shard
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        dist.init_process_group("gloo", rank=0, world_size=1)
+    rng = np.random.default_rng(13)
+    t = rand_tensor(rng, [40, 300, 500], 100_000)
+    be = shard.GpuBackend(0, ws)
+    rows = shard.LocalRows(torch.from_numpy(t.coords.view(np.int32)).cuda(),
+                           torch.from_numpy(t.values).cuda())
+    for target in ([1, 0, 2], [0, 2, 1]):
+        out, _ = shard.sharded_transpose(dist, be, rows, t.dims.tolist(), target)
+        c, v, _ = ORC.transpose(t.dims, t.coords, t.values, target)
+        assert np.array_equal(out.coords.cpu().numpy().view(np.uint32), c)
