@@ -125,15 +125,26 @@ struct ChunkDesc {
 
 // Row storage: AoS = coords[N*R] (row-major, the API layout) + values[N];
 // SoA = column m at coords + m*N (intermediate passes) + values[N].
+// Row formats.  AoS: coords[N*R] + values[N] (the API layout).  SoA: column m
+// at coords + m*N, values[N].  PK: 16-byte rows {u64 packed coordinates, f64
+// value} where the packed word holds the group's combined key in its low
+// bits (digit q = shift + mask) and the other modes above it.
+enum { kAoS = 0, kSoA = 1, kPK = 2 };
 struct Rows {
-  const uint32_t* c;
+  const uint32_t* c;  // PK: the 16-byte rows
   const double* v;
-  int soa;
+  int fmt;
 };
 struct RowsOut {
   uint32_t* c;
   double* v;
-  int soa;
+  int fmt;
+};
+
+// Packed coordinate layout: mode m at bits [off[m], off[m] + width[m]).
+struct PackSpec {
+  uint32_t rank;
+  uint8_t off[kMaxKeys], width[kMaxKeys];
 };
 
 struct ChunkHistArgs {
@@ -148,6 +159,9 @@ struct ChunkHistArgs {
   int do_check;
   ErrBlock* err;
   unsigned long long* rows_counter;
+  uint32_t pk_shift, pk_mask;  // digit of a PK row
+  int check_pack;              // flag bit2 if a coordinate would not pack losslessly
+  PackSpec pack;
 };
 
 struct ScatterArgs {
@@ -164,6 +178,8 @@ struct ScatterArgs {
   const unsigned long long* run_start;  // [li]; nullptr: 0
   uint32_t* chunk_counter;
   DigitSpec dig;
+  uint32_t pk_shift, pk_mask;  // digit of a PK row
+  PackSpec pack;
 };
 
 // ---------------------------------------------------------------------------
@@ -487,7 +503,17 @@ __global__ void __launch_bounds__(kThreads) k_chunk_hist(ChunkHistArgs a) {
     __syncthreads();
     const ChunkDesc cd = a.chunks[ci];
     if (threadIdx.x == 0 && a.rows_counter) atomicAdd(a.rows_counter, (unsigned long long)cd.len);
-    if (a.in.soa && fast_dig && !dg.two) {
+    if (a.in.fmt == kPK) {
+      // 16-byte rows: digit from the packed word
+      const ulonglong2* rows = reinterpret_cast<const ulonglong2*>(a.in.c) + cd.row_begin;
+      uint32_t* wh = s_h + w * kBins;
+#pragma unroll 4
+      for (uint32_t k = threadIdx.x; k < cd.len; k += kThreads)
+        atomicAdd(wh + ((uint32_t)(__ldcs(rows + k).x >> a.pk_shift) & a.pk_mask), 1u);
+      __syncthreads();
+      goto flush;
+    }
+    if (a.in.fmt == kSoA && fast_dig && !dg.two) {
       // SoA column, one-field digit: 16-byte loads of 4 rows per thread and
       // per-warp shared-memory atomics (intermediate order has few runs)
       const uint32_t* col = a.in.c + (size_t)dg.m0 * N + cd.row_begin;
@@ -516,7 +542,7 @@ __global__ void __launch_bounds__(kThreads) k_chunk_hist(ChunkHistArgs a) {
       const uint32_t nvalid = min(32u, cd.len - g);
       const unsigned long long r = cd.row_begin + (valid ? i : 0u);
       uint32_t d = 0;
-      if (a.in.soa) {
+      if (a.in.fmt == kSoA) {
         if (valid) {
           auto get = [&](uint32_t m) { return __ldcs(a.in.c + m * N + r); };
           d = fast_dig ? digit2(get, dg) : digit_by(get, a.dig);
@@ -525,6 +551,11 @@ __global__ void __launch_bounds__(kThreads) k_chunk_hist(ChunkHistArgs a) {
         const uint32_t* row = a.in.c + r * R;
         if (valid) {
           if (a.do_check) check_row(row, a.key, r, a.err);
+          if (a.check_pack) {
+            uint32_t bad = 0;
+            for (uint32_t m = 0; m < R; ++m) bad |= a.pack.width[m] >= 32 ? 0u : (row[m] >> a.pack.width[m]);
+            if (bad) atomicOr(&a.err->flags, 4u);
+          }
           auto get = [&](uint32_t m) { return __ldg(row + m); };
           d = fast_dig ? digit2(get, dg) : digit_by(get, a.dig);
         }
@@ -549,15 +580,20 @@ __global__ void __launch_bounds__(kThreads) k_chunk_hist(ChunkHistArgs a) {
 struct ScatterLayout {
   size_t cspan, cbuf, vbuf, c0, v0, dig, rnk, sorted, whist, cnt, start, run, gbase, tmp, ofs,
       bar, total;
-  __host__ __device__ ScatterLayout(uint32_t T, uint32_t rank, bool soa) {
+  __host__ __device__ ScatterLayout(uint32_t T, uint32_t rank, int fmt) {
     size_t o = 0;
     cspan = align16(size_t(T) * 4 + 32);  // one SoA column span
-    cbuf = soa ? cspan * rank : align16(size_t(T) * rank * 4 + 32);
-    vbuf = align16(size_t(T) * 8 + 32);
+    if (fmt == kPK) {
+      cbuf = align16(size_t(T) * 16 + 32);
+      vbuf = 0;
+    } else {
+      cbuf = fmt == kSoA ? cspan * rank : align16(size_t(T) * rank * 4 + 32);
+      vbuf = align16(size_t(T) * 8 + 32);
+    }
     c0 = o; o += 2 * cbuf;
     v0 = o; o += 2 * vbuf;
     dig = o; o += align16(size_t(T) * 2);
-    rnk = o; o += align16(size_t(T) * 2);
+    rnk = o; o += 0;  // ranks live in registers
     sorted = o; o += align16(size_t(T) * 2);
     whist = o; o += align16(size_t(kSortWarps) * kBins * 2);
     cnt = o; o += align16(kBins * 4);
@@ -573,20 +609,21 @@ struct ScatterLayout {
 
 // ---------------------------------------------------------------------------
 // k_scatter: one stable counting pass over one radix digit, chunk-ordered.
-// Persistent CTAs claim chunks; inside a chunk, tiles are processed in order
-// and thread 0 prefetches the next tile with TMA bulk copies (cp.async.bulk,
-// mbarrier completion) into the other buffer while the CTA ranks the current
-// tile (warp ballots), and scatters it coalesced through shared memory.
-// RT: compile-time rank (0 = runtime); IN_SOA / OUT_SOA: row formats.
+// Persistent CTAs take chunks (statically dealt); inside a chunk, tiles are
+// processed in order and the advancer warp prefetches the next tile with TMA
+// bulk copies (cp.async.bulk, mbarrier completion) into the other buffer
+// while the CTA ranks the current tile (MATCH.ANY per 32-row round) and
+// scatters it coalesced through shared memory.
+// RT: compile-time rank (0 = runtime); IN/OUT: row formats (kAoS/kSoA/kPK);
+// DM: digit of an AoS/SoA row inside 1 or 2 key fields (0 = general).
 // ---------------------------------------------------------------------------
-template <int RT, bool IN_SOA, bool OUT_SOA, int DM>
+template <int RT, int IN, int OUT, int DM>
 __global__ void __launch_bounds__(kSortThreads, 1024 / kSortThreads) k_scatter(ScatterArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   const uint32_t R = RT ? RT : a.rank;
   const uint64_t N = a.nnz;
-  const ScatterLayout L(a.T, R, IN_SOA);
+  const ScatterLayout L(a.T, R, IN);
   uint16_t* s_dig = reinterpret_cast<uint16_t*>(smem + L.dig);
-  uint16_t* s_rank = reinterpret_cast<uint16_t*>(smem + L.rnk);
   uint16_t* s_sorted = reinterpret_cast<uint16_t*>(smem + L.sorted);
   uint16_t* s_whist = reinterpret_cast<uint16_t*>(smem + L.whist);
   uint32_t* s_cnt = reinterpret_cast<uint32_t*>(smem + L.cnt);
@@ -599,12 +636,19 @@ __global__ void __launch_bounds__(kSortThreads, 1024 / kSortThreads) k_scatter(S
   __shared__ uint32_t s_chunk, s_tile;  // next (chunk, tile-in-chunk) to process
   __shared__ ChunkDesc s_cd[2];          // descriptor of the chunk staged in buffer b
 
-  // global address + byte length of span k of rows [rb, rb+n)
+  // spans of a tile: AoS {coords, values}, SoA {column 0..R-1, values},
+  // PK {rows}.  Span index R always means "values".
+  constexpr bool kSoAIn = IN == kSoA;
+  auto nspans = [&]() { return IN == kPK ? 1u : (kSoAIn ? R + 1 : 2u); };
+  auto span_index = [&](uint32_t j) { return (IN == kAoS && j == 1) ? R : j; };
   auto span = [&](uint32_t k, unsigned long long rb, uint32_t n, const void*& g, uint32_t& len) {
-    if (k == R) {
+    if (IN == kPK) {
+      g = reinterpret_cast<const ulonglong2*>(a.in.c) + rb;
+      len = n * 16;
+    } else if (k == R) {
       g = a.in.v + rb;
       len = n * 8;
-    } else if (IN_SOA) {
+    } else if (kSoAIn) {
       g = a.in.c + (size_t)k * N + rb;
       len = n * 4;
     } else {
@@ -612,17 +656,15 @@ __global__ void __launch_bounds__(kSortThreads, 1024 / kSortThreads) k_scatter(S
       len = n * R * 4;
     }
   };
-  auto nspans = [&]() { return IN_SOA ? R + 1 : 2u; };
-  auto span_index = [&](uint32_t j) { return (!IN_SOA && j == 1) ? R : j; };
   auto span_dst = [&](uint32_t b, uint32_t k) -> unsigned char* {
-    if (k == R) return smem + L.v0 + b * L.vbuf;
-    return smem + L.c0 + b * L.cbuf + (IN_SOA ? k * L.cspan : 0);
+    if (IN != kPK && k == R) return smem + L.v0 + b * L.vbuf;
+    return smem + L.c0 + b * L.cbuf + (kSoAIn ? k * L.cspan : 0);
   };
 
-  // The advancer thread (lane 0 of the last warp, idle while the first
-  // kBins threads fold the bin counts) issues the bulk loads of the next tile.
-  // Chunks are assigned statically (blockIdx.x + k*gridDim.x): no atomics,
-  // and the next chunk's descriptor is loaded one chunk ahead.
+  // The advancer warp (the last one, idle while the first kBins threads fold
+  // the bin counts) issues the bulk loads of the next tile.  Chunks are
+  // assigned statically (blockIdx.x + k*gridDim.x): no atomics, and the next
+  // chunk's descriptor is loaded one chunk ahead.
   constexpr uint32_t kAdv = kSortThreads - 32;
   ChunkDesc pre{};  // advancer only: descriptor of this CTA's next chunk
   // called by the whole advancer warp: lane j issues span j's bulk copy
@@ -688,7 +730,6 @@ __global__ void __launch_bounds__(kSortThreads, 1024 / kSortThreads) k_scatter(S
   }
   __syncthreads();
 
-  const bool fast_dig = a.dig.lookup == nullptr && a.dig.n <= 2;
   const Dig2 dg = dig2_of(a.dig);
   uint32_t phases = 0u;
   long long t_last = clock64();
@@ -722,23 +763,22 @@ __global__ void __launch_bounds__(kSortThreads, 1024 / kSortThreads) k_scatter(S
     mbar_wait(&s_bar[b], (phases >> b) & 1u);  // each thread observes the TMA completion
     QD_TMARK(2);
     phases ^= 1u << b;
-    const uint32_t* sc = reinterpret_cast<const uint32_t*>(smem + L.c0 + b * L.cbuf);
-    const double* s_v = reinterpret_cast<const double*>(span_dst(b, R) + s_ofs[b * 66 + R]);
+    const unsigned char* scb = smem + L.c0 + b * L.cbuf;
     const uint32_t* s_ofsb = s_ofs + b * 66;
-    const unsigned char* scb = reinterpret_cast<const unsigned char*>(sc);
+    const ulonglong2* s_pk = reinterpret_cast<const ulonglong2*>(scb);  // PK rows
     // byte offset of (row 0, mode m) in the staged tile, and the row stride
-    const uint32_t rstride = IN_SOA ? 4u : R * 4u;
+    const uint32_t rstride = kSoAIn ? 4u : R * 4u;
     auto mbase = [&](uint32_t m) -> uint32_t {
-      return IN_SOA ? m * (uint32_t)L.cspan + s_ofsb[m] : s_ofsb[0] + m * 4u;
+      return kSoAIn ? m * (uint32_t)L.cspan + s_ofsb[m] : s_ofsb[0] + m * 4u;
     };
     auto coord = [&](uint32_t i, uint32_t m) -> uint32_t {
       return *reinterpret_cast<const uint32_t*>(scb + mbase(m) + i * rstride);
     };
     // the digit's (at most two) fields, resolved once per tile
-    const uint32_t dbase0 = DM ? mbase(dg.m0) : 0u;
-    const uint32_t dbase1 = DM == 2 ? mbase(dg.m1) : 0u;
-    // DM: 1 = digit inside one key field, 2 = spans two fields, 0 = general
+    const uint32_t dbase0 = (IN != kPK && DM) ? mbase(dg.m0) : 0u;
+    const uint32_t dbase1 = (IN != kPK && DM == 2) ? mbase(dg.m1) : 0u;
     auto digit_at = [&](uint32_t i) -> uint32_t {
+      if (IN == kPK) return (uint32_t)(s_pk[i].x >> a.pk_shift) & a.pk_mask;
       if (DM == 0) return digit_by([&](uint32_t m) { return coord(i, m); }, a.dig);
       const uint32_t x0 = *reinterpret_cast<const uint32_t*>(scb + dbase0 + i * rstride);
       uint32_t v = (x0 >> dg.r0) & dg.k0;
@@ -807,26 +847,62 @@ __global__ void __launch_bounds__(kSortThreads, 1024 / kSortThreads) k_scatter(S
     }
     __syncthreads();
     QD_TMARK(6);
+    // ---- scatter, in sorted order so consecutive threads write consecutive rows
     uint32_t cb[RT > 0 ? RT : 1];
-    if (RT) {
+    if (IN != kPK && RT) {
 #pragma unroll
       for (int m = 0; m < (RT > 0 ? RT : 1); ++m) cb[m] = mbase(m);
     }
-    const uint32_t vbase = (uint32_t)(span_dst(b, R) - scb) + s_ofsb[R];
+    const uint32_t vbase = IN == kPK ? 0u : (uint32_t)(span_dst(b, R) - scb) + s_ofsb[R];
     for (uint32_t j = threadIdx.x; j < n; j += kSortThreads) {
       const uint32_t i = s_sorted[j];
       const unsigned long long dst = (unsigned long long)(s_gbase[s_dig[i]] + j);
       if (a.dbg & 1) continue;
+      if (IN == kPK) {
+        const ulonglong2 row = s_pk[i];
+        if (OUT == kPK) {
+          __stcs(reinterpret_cast<ulonglong2*>(a.out.c) + dst, row);
+        } else {  // unpack into AoS
+          uint32_t* o = a.out.c + dst * R;
+          if (RT) {
+#pragma unroll
+            for (int m = 0; m < (RT > 0 ? RT : 1); ++m)
+              __stcs(o + m, (uint32_t)(row.x >> a.pack.off[m]) &
+                                (uint32_t)((1ull << a.pack.width[m]) - 1ull));
+          } else {
+            for (uint32_t m = 0; m < R; ++m)
+              __stcs(o + m, (uint32_t)(row.x >> a.pack.off[m]) &
+                                (uint32_t)((1ull << a.pack.width[m]) - 1ull));
+          }
+          __stcs(a.out.v + dst, __longlong_as_double((long long)row.y));
+        }
+        continue;
+      }
       const double v = *reinterpret_cast<const double*>(scb + vbase + i * 8u);
+      if (OUT == kPK) {  // pack (first pass)
+        unsigned long long pk = 0;
+        if (RT) {
+#pragma unroll
+          for (int m = 0; m < (RT > 0 ? RT : 1); ++m)
+            pk |= (unsigned long long)*reinterpret_cast<const uint32_t*>(scb + cb[m] + i * rstride)
+                  << a.pack.off[m];
+        } else {
+          for (uint32_t m = 0; m < R; ++m)
+            pk |= (unsigned long long)coord(i, m) << a.pack.off[m];
+        }
+        __stcs(reinterpret_cast<ulonglong2*>(a.out.c) + dst,
+               make_ulonglong2(pk, (unsigned long long)__double_as_longlong(v)));
+        continue;
+      }
       if (RT) {
 #pragma unroll
         for (int m = 0; m < (RT > 0 ? RT : 1); ++m) {
           const uint32_t x = *reinterpret_cast<const uint32_t*>(scb + cb[m] + i * rstride);
-          __stcs(OUT_SOA ? a.out.c + (size_t)m * N + dst : a.out.c + dst * RT + m, x);
+          __stcs(OUT == kSoA ? a.out.c + (size_t)m * N + dst : a.out.c + dst * RT + m, x);
         }
       } else {
         for (uint32_t m = 0; m < R; ++m)
-          __stcs(OUT_SOA ? a.out.c + (size_t)m * N + dst : a.out.c + dst * R + m, coord(i, m));
+          __stcs(OUT == kSoA ? a.out.c + (size_t)m * N + dst : a.out.c + dst * R + m, coord(i, m));
       }
       __stcs(a.out.v + dst, v);
     }
@@ -1241,6 +1317,7 @@ struct Workspace {
   uint64_t launches = 0;
   ErrBlock* h_err = nullptr;  // pinned
   uint64_t* h_small = nullptr;  // pinned scratch for small D2H reads
+  bool allow_pack = true;  // packed intermediates (cleared for a lossy-pack redo)
   // live per-kernel-class timing (CUDA events on the launch stream)
   bool prof = false;
   struct ProfStat {
@@ -1276,29 +1353,32 @@ struct Workspace {
 };
 
 using ScatterFn = void (*)(ScatterArgs);
+// (in, out) format pairs used: AoS->AoS, AoS->SoA, SoA->SoA, SoA->AoS (any
+// group), AoS->PK, PK->PK, PK->AoS (packed groups)
 template <int RT, int DM>
-ScatterFn scatter_kernel_fmt(int fmt) {
-  switch (fmt) {
-    case 0: return k_scatter<RT, false, false, DM>;
-    case 1: return k_scatter<RT, false, true, DM>;
-    case 2: return k_scatter<RT, true, false, DM>;
-    default: return k_scatter<RT, true, true, DM>;
-  }
+ScatterFn scatter_kernel_fmt(int in, int out) {
+  if (in == kAoS && out == kAoS) return k_scatter<RT, kAoS, kAoS, DM>;
+  if (in == kAoS && out == kSoA) return k_scatter<RT, kAoS, kSoA, DM>;
+  if (in == kSoA && out == kSoA) return k_scatter<RT, kSoA, kSoA, DM>;
+  if (in == kSoA && out == kAoS) return k_scatter<RT, kSoA, kAoS, DM>;
+  if (in == kAoS && out == kPK) return k_scatter<RT, kAoS, kPK, DM>;
+  return nullptr;
 }
 template <int RT>
-ScatterFn scatter_kernel_dm(int dm, int fmt) {
+ScatterFn scatter_kernel_rt(int dm, int in, int out) {
+  if (in == kPK) return out == kPK ? k_scatter<RT, kPK, kPK, 0> : k_scatter<RT, kPK, kAoS, 0>;
   switch (dm) {
-    case 1: return scatter_kernel_fmt<RT, 1>(fmt);
-    case 2: return scatter_kernel_fmt<RT, 2>(fmt);
-    default: return scatter_kernel_fmt<RT, 0>(fmt);
+    case 1: return scatter_kernel_fmt<RT, 1>(in, out);
+    case 2: return scatter_kernel_fmt<RT, 2>(in, out);
+    default: return scatter_kernel_fmt<RT, 0>(in, out);
   }
 }
-// rt: compile-time rank (3, 4 or 0 = runtime); dm: digit mode; fmt: in/out SoA bits
-ScatterFn scatter_kernel(int rt, int dm, int fmt) {
+// rt: compile-time rank (3, 4 or 0 = runtime); dm: digit mode; in/out formats
+ScatterFn scatter_kernel(int rt, int dm, int in, int out) {
   switch (rt) {
-    case 3: return scatter_kernel_dm<3>(dm, fmt);
-    case 4: return scatter_kernel_dm<4>(dm, fmt);
-    default: return scatter_kernel_dm<0>(dm, fmt);
+    case 3: return scatter_kernel_rt<3>(dm, in, out);
+    case 4: return scatter_kernel_rt<4>(dm, in, out);
+    default: return scatter_kernel_rt<0>(dm, in, out);
   }
 }
 
@@ -1324,8 +1404,10 @@ Workspace* workspace_create(int device) {
   };
   for (int rt : {0, 3, 4})
     for (int dm = 0; dm < 3; ++dm)
-      for (int fmt = 0; fmt < 4; ++fmt)
-        allow_smem(reinterpret_cast<const void*>(scatter_kernel(rt, dm, fmt)));
+      for (int in = 0; in < 3; ++in)
+        for (int out = 0; out < 3; ++out)
+          if (ScatterFn f = scatter_kernel(rt, dm, in, out))
+            allow_smem(reinterpret_cast<const void*>(f));
   allow_smem(reinterpret_cast<const void*>(k_local));
   ws->smem_optin = optin - 1024;  // dynamic budget below the static usage
   return ws;
@@ -1440,7 +1522,8 @@ uint32_t sweep_tile_rows(const Workspace& ws, uint32_t rank) {
   size_t budget = std::min<size_t>(ws.smem_optin, 112 * 1024);  // 2 CTAs/SM
   if (const char* e = getenv("QD_SMEM_BUDGET")) budget = (size_t)atoi(e) * 1024;
   auto need = [&](uint32_t T) {
-    return std::max(ScatterLayout(T, rank, false).total, ScatterLayout(T, rank, true).total);
+    return std::max({ScatterLayout(T, rank, kAoS).total, ScatterLayout(T, rank, kSoA).total,
+                     ScatterLayout(T, rank, kPK).total});
   };
   uint32_t T = 4096;
   while (T > 512 && need(T) > budget) T -= 512;
@@ -1547,7 +1630,8 @@ uint32_t chunk_tiles(const Workspace& ws, uint64_t rows, uint32_t T) {
 void run_pass(Ctx& c, uint32_t R, uint64_t N, uint32_t T, Rows in, RowsOut out,
               const ChunkDesc* chunks, uint64_t num_chunks,
               const unsigned long long* run_start, const DigitSpec& dig, const KeySpec& key,
-              bool check, unsigned long long** offs_out = nullptr) {
+              bool check, unsigned long long** offs_out = nullptr, const PackSpec* pack = nullptr,
+              uint32_t pk_shift = 0, uint32_t pk_mask = 0) {
   Workspace& ws = c.ws;
   const uint64_t nflat = num_chunks * kBins;
   auto* flat = ws.get<uint32_t>("chunk_flat", nflat);
@@ -1565,6 +1649,12 @@ void run_pass(Ctx& c, uint32_t R, uint64_t N, uint32_t T, Rows in, RowsOut out,
   h.do_check = check;
   h.err = c.err;
   h.rows_counter = check ? &c.err->rows[std::min(c.group, kMaxGroups - 1)] : nullptr;
+  h.pk_shift = pk_shift;
+  h.pk_mask = pk_mask;
+  if (pack) {
+    h.pack = *pack;
+    h.check_pack = in.fmt == kAoS && out.fmt == kPK;
+  }
   c.pre();
   k_chunk_hist<<<(uint32_t)std::min<uint64_t>(num_chunks, (uint64_t)ws.num_sms * 8), kThreads, 0,
                  c.st>>>(h);
@@ -1582,6 +1672,9 @@ void run_pass(Ctx& c, uint32_t R, uint64_t N, uint32_t T, Rows in, RowsOut out,
   a.offs = offs;
   a.run_start = run_start;
   a.dig = dig;
+  a.pk_shift = pk_shift;
+  a.pk_mask = pk_mask;
+  if (pack) a.pack = *pack;
   if (const char* e = getenv("QD_SCATTER_DBG")) a.dbg = atoi(e);
   if (a.dbg & 2) {
     a.dbg_t = ws.get<unsigned long long>("dbg_t", 16);
@@ -1592,13 +1685,11 @@ void run_pass(Ctx& c, uint32_t R, uint64_t N, uint32_t T, Rows in, RowsOut out,
     c.next_counter = 0;
   }
   a.chunk_counter = c.counters + c.next_counter++;
-  const size_t smem = ScatterLayout(T, R, in.soa != 0).total;
-  using Fn = void (*)(ScatterArgs);
-  Fn fn = nullptr;
+  const size_t smem = ScatterLayout(T, R, in.fmt).total;
   const int rt = (R == 3 || R == 4) ? (int)R : 0;
-  const int fmt = (in.soa ? 2 : 0) | (out.soa ? 1 : 0);
   const int dm = dig.lookup ? 0 : (dig.n == 1 ? 1 : (dig.n == 2 ? 2 : 0));
-  fn = scatter_kernel(rt, dm, fmt);
+  ScatterFn fn = scatter_kernel(rt, dm, in.fmt, out.fmt);
+  if (!fn) throw Error(QD_CUDA_ERROR, "no scatter kernel for this row format pair");
   int per_sm = 0;
   QD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kSortThreads, smem));
   const uint32_t grid =
@@ -1721,14 +1812,49 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
   }
 
   if (num_chunks) {
-    Rows in{src_c, src_v, 0};
+    // Intermediate rows: packed 16-byte rows when every coordinate packs into
+    // one u64 (key fields at their key offsets, so a digit is shift + mask),
+    // else SoA columns.  A coordinate that would not pack losslessly (only
+    // possible for modes the plan never range-checks) is flagged by the
+    // first histogram and the whole call is redone unpacked (run_groups).
+    PackSpec pack{};
+    uint32_t pbits = key.total_bits;
+    bool packed = ws.allow_pack && g.check_range && D > 1;
+    if (packed) {
+      pack.rank = R;
+      for (uint32_t k = 0; k < key.n; ++k) {
+        pack.off[key.mode[k]] = (uint8_t)key.off[k];
+        pack.width[key.mode[k]] = key.width[k];
+      }
+      for (uint32_t m = 0; m < R && packed; ++m) {
+        bool is_key = false;
+        for (uint32_t k = 0; k < key.n; ++k) is_key |= key.mode[k] == m;
+        if (is_key) continue;
+        const uint32_t wdt = ceil_log2(t.dims[m]);
+        pack.off[m] = (uint8_t)pbits;
+        pack.width[m] = (uint8_t)wdt;
+        pbits += wdt;
+      }
+      packed = pbits <= 64;
+    }
+    // packed intermediates ping-pong in workspace buffers of 16 bytes/row
+    uint32_t* pk[2] = {nullptr, nullptr};
+    if (packed) {
+      pk[0] = ws.get<uint32_t>("pkA", N * 4);
+      if (D > 2) pk[1] = ws.get<uint32_t>("pkB", N * 4);
+    }
+    Rows in{src_c, src_v, kAoS};
     for (uint32_t q = 0; q < D; ++q) {
       const bool last = q + 1 == D;
       const bool to_dst = ((D - 1 - q) % 2) == 0;
-      RowsOut out{to_dst ? dst_c : tmp_c, to_dst ? dst_v : tmp_v, last ? 0 : 1};
+      const int ofmt = last ? kAoS : (packed ? kPK : kSoA);
+      RowsOut out{to_dst ? dst_c : tmp_c, to_dst ? dst_v : tmp_v, ofmt};
+      if (ofmt == kPK) out = RowsOut{pk[q % 2], nullptr, kPK};
+      const uint32_t lo = q * per, hi = std::min(bits, lo + per);
       run_pass(c, R, N, T, in, out, chunks, num_chunks, run_start, digs[q], key,
-               q == 0 && key.check);
-      in = Rows{out.c, out.v, out.soa};
+               q == 0 && key.check, nullptr, packed ? &pack : nullptr, lo,
+               (1u << (hi - lo)) - 1u);
+      in = Rows{out.c, out.v, out.fmt};
     }
   }
   if (small_runs) {
@@ -1745,7 +1871,9 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
 
 }  // namespace
 
-static void check_errors(Ctx& c) {
+// Synchronise, fold profiling records, and throw the first error found.
+// Returns the error flags (bit2 = a coordinate did not pack losslessly).
+static unsigned check_errors(Ctx& c) {
   QD_CUDA(cudaMemcpyAsync(c.ws.h_err, c.err, sizeof(ErrBlock), cudaMemcpyDeviceToHost, c.st));
   QD_CUDA(cudaStreamSynchronize(c.st));
   const ErrBlock e = *c.ws.h_err;
@@ -1759,6 +1887,7 @@ static void check_errors(Ctx& c) {
     err.mode = (uint32_t)(e.rowmode & 63);
     throw err;
   }
+  return e.flags;
 }
 
 static Ctx make_ctx(Workspace& ws, void* stream) {
@@ -1773,10 +1902,11 @@ static Ctx make_ctx(Workspace& ws, void* stream) {
   return c;
 }
 
-void run_groups(Workspace& ws, const TensorView& t, const uint32_t* d_c_in, const double* d_v_in,
-                uint32_t* d_c_out, double* d_v_out, const std::vector<Group>& groups,
-                bool verify_input, uint64_t* d_boundaries, uint64_t* n_boundaries,
-                uint32_t boundary_mode, void* stream) {
+static void run_groups_once(Workspace& ws, const TensorView& t, const uint32_t* d_c_in,
+                            const double* d_v_in, uint32_t* d_c_out, double* d_v_out,
+                            const std::vector<Group>& groups, bool verify_input,
+                            uint64_t* d_boundaries, uint64_t* n_boundaries,
+                            uint32_t boundary_mode, void* stream, unsigned* flags) {
   Ctx c = make_ctx(ws, stream);
   const uint64_t N = t.nnz;
   const uint32_t R = t.rank;
@@ -1835,7 +1965,29 @@ void run_groups(Workspace& ws, const TensorView& t, const uint32_t* d_c_in, cons
   } else if (n_boundaries) {
     *n_boundaries = 0;
   }
-  check_errors(c);
+  *flags = check_errors(c);
+}
+
+void run_groups(Workspace& ws, const TensorView& t, const uint32_t* d_c_in, const double* d_v_in,
+                uint32_t* d_c_out, double* d_v_out, const std::vector<Group>& groups,
+                bool verify_input, uint64_t* d_boundaries, uint64_t* n_boundaries,
+                uint32_t boundary_mode, void* stream) {
+  unsigned flags = 0;
+  run_groups_once(ws, t, d_c_in, d_v_in, d_c_out, d_v_out, groups, verify_input, d_boundaries,
+                  n_boundaries, boundary_mode, stream, &flags);
+  if (flags & 4u) {
+    // a coordinate of a mode the plan never range-checks does not fit its
+    // packed field: redo the call with unpacked (SoA) intermediates
+    ws.allow_pack = false;
+    try {
+      run_groups_once(ws, t, d_c_in, d_v_in, d_c_out, d_v_out, groups, verify_input,
+                      d_boundaries, n_boundaries, boundary_mode, stream, &flags);
+    } catch (...) {
+      ws.allow_pack = true;
+      throw;
+    }
+    ws.allow_pack = true;
+  }
 }
 
 void run_groups_host(Workspace& ws, const TensorView& t, uint32_t* coords, double* values,

@@ -364,3 +364,16 @@ def test_sharded_single_rank_is_plain_transpose(ws):
         out, _ = shard.sharded_transpose(dist, be, rows, t.dims.tolist(), target)
         c, v, _ = ORC.transpose(t.dims, t.coords, t.values, target)
         assert np.array_equal(out.coords.cpu().numpy().view(np.uint32), c)
+
+
+def test_unchecked_mode_out_of_range_is_moved_not_truncated(ws):
+    # Mode 0 is never a key of the (2,1,0) plan, so the reference never
+    # range-checks it (sort.cpp:26-30 only checks the sorted mode) and just
+    # moves the value 9 along; the packed intermediate cannot hold it, so the
+    # library must detect that and redo the call unpacked.
+    rng = np.random.default_rng(17)
+    t = rand_tensor(rng, [4, 3000, 3000], 100_000)
+    t.coords[3 * 5000] = 9
+    c, v, _ = ORC.transpose(t.dims, t.coords, t.values, [2, 1, 0])
+    out = qd.transpose(t, [2, 1, 0], ws=ws)
+    assert same(out, c, v)
