@@ -108,6 +108,7 @@ struct LocalArgs {
   uint64_t nseg;
   KeySpec key;
   ErrBlock* err;
+  const uint32_t* chunk_list;  // chunk ids holding small runs (blockIdx.x -> chunk)
 };
 
 // A chunk: a contiguous row range inside one run, processed by one CTA in
@@ -533,6 +534,32 @@ __global__ void __launch_bounds__(kThreads) k_chunk_hist(ChunkHistArgs a) {
       }
       for (uint32_t k = head + nv * 4 + threadIdx.x; k < cd.len; k += kThreads)
         atomicAdd(wh + ((col[k] >> dg.r0) & dg.k0), 1u);
+      __syncthreads();
+      goto flush;
+    }
+    if (a.in.fmt == kAoS && R == 3 && fast_dig) {
+      // AoS rank-3 rows (the common first pass): coordinates in registers,
+      // range + pack checks from them, run-aggregated counting
+      const uint32_t dm0 = dg.m0, dm1 = dg.m1;
+      for (uint32_t g = w * 32; g < cd.len; g += kThreads) {  // warp-uniform
+        const uint32_t i = g + lane;
+        const bool valid = i < cd.len;
+        const uint32_t nvalid = min(32u, cd.len - g);
+        const unsigned long long r = cd.row_begin + (valid ? i : 0u);
+        const uint32_t* row = a.in.c + r * 3;
+        const uint32_t c0 = __ldcs(row), c1 = __ldcs(row + 1), c2 = __ldcs(row + 2);
+        auto cm = [&](uint32_t m) { return m == 0 ? c0 : (m == 1 ? c1 : c2); };
+        uint32_t d = 0;
+        if (valid) {
+          if (a.do_check) check_row(row, a.key, r, a.err);
+          if (a.check_pack &&
+              ((c0 >> a.pack.width[0]) | (c1 >> a.pack.width[1]) | (c2 >> a.pack.width[2])))
+            atomicOr(&a.err->flags, 4u);
+          d = ((cm(dm0) >> dg.r0) & dg.k0) << dg.l0;
+          if (dg.two) d |= ((cm(dm1) >> dg.r1) & dg.k1) << dg.l1;
+        }
+        add_runs(s_h + w * kBins, d, valid, nvalid);
+      }
       __syncthreads();
       goto flush;
     }
@@ -965,7 +992,8 @@ __global__ void __launch_bounds__(kSortThreads) k_local(LocalArgs a) {
       s_seg[1] = a.nnz;
     }
   } else {
-    const unsigned long long lo = (unsigned long long)blockIdx.x * a.TL;
+    const uint32_t chunk = a.chunk_list ? a.chunk_list[blockIdx.x] : blockIdx.x;
+    const unsigned long long lo = (unsigned long long)chunk * a.TL;
     const unsigned long long hi = min((unsigned long long)a.nnz, lo + (unsigned long long)a.TL);
     const uint64_t S = a.nseg;  // seg_start has S+1 entries
     if (threadIdx.x == 0) {
@@ -1133,7 +1161,7 @@ __global__ void __launch_bounds__(kThreads) k_compact(const uint32_t* words, uin
 // Per run: large flag and its chunk count (CH rows per chunk).
 __global__ void k_classify_chunks(const unsigned long long* seg_start,
                                   const unsigned long long* S_ptr, uint32_t TL, uint32_t CH,
-                                  uint32_t* is_large, uint32_t* nchunks) {
+                                  uint32_t* is_large, uint32_t* nchunks, uint32_t* local_flag) {
   const unsigned long long S = *S_ptr;
   for (unsigned long long s = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; s < S;
        s += (unsigned long long)gridDim.x * blockDim.x) {
@@ -1141,7 +1169,16 @@ __global__ void k_classify_chunks(const unsigned long long* seg_start,
     const bool large = len > TL;
     is_large[s] = large;
     nchunks[s] = large ? (uint32_t)((len + CH - 1) / CH) : 0u;
+    if (!large && TL) local_flag[seg_start[s] / TL] = 1u;  // a local chunk has work
   }
+}
+
+// list[pos[c]] = c for every flagged c
+__global__ void k_compact_flags(const uint32_t* flag, const unsigned long long* pos, uint64_t n,
+                                uint32_t* list) {
+  for (unsigned long long c = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; c < n;
+       c += (unsigned long long)gridDim.x * blockDim.x)
+    if (flag[c]) list[pos[c]] = (uint32_t)c;
 }
 
 __global__ void k_gen_chunks(const unsigned long long* seg_start, const unsigned long long* S_ptr,
@@ -1762,12 +1799,14 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
   const unsigned long long* run_start = nullptr;
   uint64_t num_chunks = 0;
   unsigned long long* seg = nullptr;
-  uint64_t S = 0, num_large = 0;
+  uint64_t S = 0, num_large = 0, local_chunks = 0;
+  const uint32_t* local_list = nullptr;
   bool small_runs = false;
 
   if (g.prefix.empty()) {
     if (TL && N <= TL) {
-      LocalArgs la{src_c, src_v, dst_c, dst_v, R, N, TL, (uint32_t)N, nullptr, 1, key, c.err};
+      LocalArgs la{src_c, src_v, dst_c, dst_v, R, N, TL, (uint32_t)N, nullptr, 1, key, c.err,
+                   nullptr};
       const size_t smem = LocalLayout((uint32_t)N, R, TL).total;
       c.pre();
       k_local<<<1, kSortThreads, smem, c.st>>>(la);
@@ -1786,20 +1825,36 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
     auto* nch = ws.get<uint32_t>("run_nchunks", S + 1);
     auto* loff = ws.get<unsigned long long>("run_loff", S + 1);
     auto* coff = ws.get<unsigned long long>("run_coff", S + 1);
-    auto* totals = ws.get<unsigned long long>("run_totals", 2);
+    auto* totals = ws.get<unsigned long long>("run_totals", 3);
     auto* S_dev = ws.get<unsigned long long>("run_S", 1);
+    const uint64_t nloc = TL ? (N + TL - 1) / TL : 0;
+    auto* lflag = ws.get<uint32_t>("local_flag", nloc + 1);
+    auto* lpos = ws.get<unsigned long long>("local_pos", nloc + 1);
+    auto* llist = ws.get<uint32_t>("local_list", nloc + 1);
+    if (nloc) QD_CUDA(cudaMemsetAsync(lflag, 0, nloc * 4, c.st));
     ws.h_small[0] = S;
     QD_CUDA(cudaMemcpyAsync(S_dev, ws.h_small, 8, cudaMemcpyHostToDevice, c.st));
     const uint32_t grid = (uint32_t)std::min<uint64_t>((S + kThreads - 1) / kThreads, ws.num_sms * 8);
     c.pre();
-    k_classify_chunks<<<grid, kThreads, 0, c.st>>>(seg, S_dev, TL, CH, is_large, nch);
+    k_classify_chunks<<<grid, kThreads, 0, c.st>>>(seg, S_dev, TL, CH, is_large, nch, lflag);
     c.launched(kSegK);
     scan_exclusive(c, is_large, S, loff, totals);
     scan_exclusive(c, nch, S, coff, totals + 1);
-    QD_CUDA(cudaMemcpyAsync(ws.h_small + 1, totals, 16, cudaMemcpyDeviceToHost, c.st));
+    if (nloc) {
+      scan_exclusive(c, lflag, nloc, lpos, totals + 2);
+      c.pre();
+      k_compact_flags<<<(uint32_t)std::min<uint64_t>((nloc + kThreads - 1) / kThreads, ws.num_sms * 8),
+                        kThreads, 0, c.st>>>(lflag, lpos, nloc, llist);
+      c.launched(kSegK);
+    } else {
+      QD_CUDA(cudaMemsetAsync(totals + 2, 0, 8, c.st));
+    }
+    QD_CUDA(cudaMemcpyAsync(ws.h_small + 1, totals, 24, cudaMemcpyDeviceToHost, c.st));
     QD_CUDA(cudaStreamSynchronize(c.st));
     num_large = ws.h_small[1];
     num_chunks = ws.h_small[2];
+    local_chunks = ws.h_small[3];
+    local_list = llist;
     small_runs = S > num_large;
     if (num_chunks) {
       chunks = ws.get<ChunkDesc>("chunks", num_chunks);
@@ -1857,14 +1912,14 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
       in = Rows{out.c, out.v, out.fmt};
     }
   }
-  if (small_runs) {
-    // small runs: chunks of runs starting in [c*TL, (c+1)*TL); after the
-    // passes, whose SoA intermediates may use dst's storage
-    LocalArgs la{src_c, src_v, dst_c, dst_v, R, N, TL, 2 * TL, seg, S, key, c.err};
+  if (small_runs && local_chunks) {
+    // small runs: chunks of runs starting in [c*TL, (c+1)*TL), only the
+    // chunks that hold some (compact list); after the passes, whose
+    // intermediates may use dst's storage
+    LocalArgs la{src_c, src_v, dst_c, dst_v, R, N, TL, 2 * TL, seg, S, key, c.err, local_list};
     const size_t smem = LocalLayout(2 * TL, R, TL).total;
-    const uint64_t nloc = (N + TL - 1) / TL;
     c.pre();
-    k_local<<<(uint32_t)nloc, kSortThreads, smem, c.st>>>(la);
+    k_local<<<(uint32_t)local_chunks, kSortThreads, smem, c.st>>>(la);
     c.launched(kLocalK);
   }
 }
