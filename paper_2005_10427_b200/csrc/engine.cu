@@ -59,6 +59,8 @@ constexpr int kMaxTerms = 12;
 constexpr int kMaxKeys = QD_MAX_RANK;
 constexpr int kHistPasses = 8;  // passes histogrammed per k_hist launch
 constexpr uint32_t kChunkTiles = 16;  // tiles per scatter chunk
+constexpr double kRunSortMinAvg = 2.5;       // mean run length that pays for a run sort
+constexpr uint64_t kRunSortMinRows = 1u << 20;  // below this, not worth a probe
 constexpr int kMaxRounds = 4096 / kSortThreads;  // 32-row rounds per warp per tile (T <= 4096)
 
 // ---------------------------------------------------------------------------
@@ -1339,6 +1341,135 @@ __global__ void k_mode_hist(const uint32_t* c, uint32_t rank, uint64_t nnz, uint
 }
 
 // ---------------------------------------------------------------------------
+// run-level sort: when the rows to sort by key k come in long runs of equal
+// (prefix, key) — the input's existing order (e.g. (i0,i1) fibers when sorting
+// by i1) — a stable sort moves each run as a block.  Runs become records
+// {key, start << 32 | len}, the records are sorted with the same engine, and
+// k_move_runs copies every run to its place.
+// ---------------------------------------------------------------------------
+__global__ void k_run_records(const uint32_t* c, uint32_t rank, uint32_t mode, uint32_t dim,
+                              const unsigned long long* seg, uint64_t S, uint32_t* rkey,
+                              double* rval, ErrBlock* err) {
+  for (unsigned long long s = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; s < S;
+       s += (unsigned long long)gridDim.x * blockDim.x) {
+    const unsigned long long b = seg[s], e = seg[s + 1];
+    const uint32_t key = c[b * rank + mode];
+    if (key >= dim) {  // every row of the run has this key (count_keys check)
+      atomicOr(&err->flags, 1u);
+      atomicMin(&err->rowmode, (b << 6) | mode);
+    }
+    rkey[s] = key;
+    rval[s] = __longlong_as_double((long long)((b << 32) | (e - b)));
+  }
+}
+
+__global__ void k_run_lens(const double* rval, uint64_t S, uint32_t* lens) {
+  for (unsigned long long s = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; s < S;
+       s += (unsigned long long)gridDim.x * blockDim.x)
+    lens[s] = (uint32_t)((unsigned long long)__double_as_longlong(rval[s]) & 0xFFFFFFFFull);
+}
+
+constexpr uint32_t kMoveRows = 4096;  // output rows per k_move_runs CTA
+
+// Output rows [p0, p0 + kMoveRows): each comes from the sorted run that
+// covers it (dsto = run output offsets, rval = {start << 32 | len}).
+__global__ void __launch_bounds__(kSortThreads, 1) k_move_runs(
+    const uint32_t* in_c, const double* in_v, uint32_t* out_c, double* out_v, uint32_t rank,
+    uint64_t N, const double* rval, const unsigned long long* dsto, uint64_t S) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  unsigned long long* s_dst = reinterpret_cast<unsigned long long*>(smem);
+  unsigned long long* s_src = s_dst + kMoveRows + 1;
+  __shared__ unsigned long long s_j0;
+  __shared__ uint32_t s_nr;
+  const unsigned long long p0 = (unsigned long long)blockIdx.x * kMoveRows;
+  const unsigned long long p1 = min((unsigned long long)N, p0 + kMoveRows);
+  if (threadIdx.x == 0) {  // last run starting at or before p0
+    uint64_t l = 0, h = S;
+    while (h - l > 1) {
+      const uint64_t m = (l + h) >> 1;
+      if (dsto[m] <= p0) l = m; else h = m;
+    }
+    s_j0 = l;
+    s_nr = 0xFFFFFFFFu;
+  }
+  __syncthreads();
+  const uint64_t j0 = s_j0;
+  for (uint32_t k = threadIdx.x; k <= kMoveRows; k += blockDim.x) {
+    const uint64_t j = j0 + k;
+    if (j < S && (k == 0 || dsto[j] < p1)) {
+      s_dst[k] = dsto[j];
+      s_src[k] = (unsigned long long)__double_as_longlong(rval[j]) >> 32;
+    } else {
+      atomicMin(&s_nr, k);
+    }
+  }
+  __syncthreads();
+  const uint32_t nr = min(s_nr, kMoveRows + 1);
+  // every thread resolves its kMoveRows/blockDim rows together (independent
+  // binary searches interleaved), then issues all their loads, then stores
+  constexpr int K = kMoveRows / kSortThreads;
+  unsigned long long src[K];
+  uint32_t lo[K], hi[K];
+#pragma unroll
+  for (int q = 0; q < K; ++q) {
+    lo[q] = 0;
+    hi[q] = nr;
+  }
+  for (int it = 0; it < 13; ++it) {  // 2^13 > kMoveRows + 1 entries
+#pragma unroll
+    for (int q = 0; q < K; ++q) {
+      const unsigned long long p = p0 + threadIdx.x + q * kSortThreads;
+      if (hi[q] - lo[q] > 1) {
+        const uint32_t m = (lo[q] + hi[q]) >> 1;
+        if (s_dst[m] <= p) lo[q] = m; else hi[q] = m;
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < K; ++q) {
+    const unsigned long long p = p0 + threadIdx.x + q * kSortThreads;
+    src[q] = s_src[lo[q]] + (p - s_dst[lo[q]]);
+  }
+  if (rank == 3) {
+    uint32_t x[K][3];
+    double v[K];
+#pragma unroll
+    for (int q = 0; q < K; ++q) {
+      const unsigned long long p = p0 + threadIdx.x + q * kSortThreads;
+      if (p < p1) {
+        const uint32_t* ic = in_c + src[q] * 3;
+        x[q][0] = __ldg(ic);
+        x[q][1] = __ldg(ic + 1);
+        x[q][2] = __ldg(ic + 2);
+        v[q] = __ldg(in_v + src[q]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < K; ++q) {
+      const unsigned long long p = p0 + threadIdx.x + q * kSortThreads;
+      if (p < p1) {
+        uint32_t* oc = out_c + p * 3;
+        __stcs(oc, x[q][0]);
+        __stcs(oc + 1, x[q][1]);
+        __stcs(oc + 2, x[q][2]);
+        __stcs(out_v + p, v[q]);
+      }
+    }
+    return;
+  }
+#pragma unroll
+  for (int q = 0; q < K; ++q) {
+    const unsigned long long p = p0 + threadIdx.x + q * kSortThreads;
+    if (p < p1) {
+      const uint32_t* ic = in_c + src[q] * rank;
+      uint32_t* oc = out_c + p * rank;
+      for (uint32_t m = 0; m < rank; ++m) __stcs(oc + m, __ldg(ic + m));
+      __stcs(out_v + p, __ldg(in_v + src[q]));
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
 struct DevBuf {
@@ -1446,6 +1577,7 @@ Workspace* workspace_create(int device) {
           if (ScatterFn f = scatter_kernel(rt, dm, in, out))
             allow_smem(reinterpret_cast<const void*>(f));
   allow_smem(reinterpret_cast<const void*>(k_local));
+  allow_smem(reinterpret_cast<const void*>(k_move_runs));
   ws->smem_optin = optin - 1024;  // dynamic budget below the static usage
   return ws;
 }
@@ -1924,6 +2056,98 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
   }
 }
 
+
+// Run-level stable sort by mode k (empty prefix): see k_run_records.  Returns
+// false (nothing written) when the runs are too short to pay off.
+bool try_run_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const double* src_v,
+                  uint32_t* dst_c, double* dst_v, uint32_t k) {
+  Workspace& ws = c.ws;
+  const uint64_t N = t.nnz;
+  const uint32_t R = t.rank;
+  unsigned long long* seg = nullptr;
+  const uint64_t S = find_runs(c, src_c, R, N, {k}, &seg);
+  if (S == 0 || (double)N / (double)S < kRunSortMinAvg) return false;
+  auto* rk0 = ws.get<uint32_t>("run_rk0", S);
+  auto* rv0 = ws.get<double>("run_rv0", S);
+  auto* rk1 = ws.get<uint32_t>("run_rk1", S);
+  auto* rv1 = ws.get<double>("run_rv1", S);
+  auto* rkt = ws.get<uint32_t>("run_rkt", S);
+  auto* rvt = ws.get<double>("run_rvt", S);
+  const uint32_t grid = (uint32_t)std::min<uint64_t>((S + kThreads - 1) / kThreads, ws.num_sms * 8);
+  c.pre();
+  k_run_records<<<grid, kThreads, 0, c.st>>>(src_c, R, k, t.dims[k], seg, S, rk0, rv0, c.err);
+  c.launched(kSegK);
+  // the records are a rank-1 tensor: sort them by their key with the engine
+  const uint32_t rdim = t.dims[k];
+  TensorView rt{1, &rdim, S};
+  Group rg;
+  rg.keys = {0};
+  segmented_sort(c, rt, rk0, rv0, rk1, rv1, rkt, rvt, rg);
+  auto* lens = ws.get<uint32_t>("run_lens", S);
+  auto* dsto = ws.get<unsigned long long>("run_dsto", S + 1);
+  auto* tot = ws.get<unsigned long long>("run_tot", 1);
+  c.pre();
+  k_run_lens<<<grid, kThreads, 0, c.st>>>(rv1, S, lens);
+  c.launched(kSegK);
+  scan_exclusive(c, lens, S, dsto, tot);
+  const size_t smem = (size_t)(kMoveRows + 1) * 16;
+  c.pre();
+  k_move_runs<<<(uint32_t)((N + kMoveRows - 1) / kMoveRows), kSortThreads, smem, c.st>>>(
+      src_c, src_v, dst_c, dst_v, R, N, rv1, dsto, S);
+  c.launched(kSweep);
+  return true;
+}
+
+// One plan group, possibly decomposed: a stable sort by keys (k1..km) within
+// prefix runs equals [sort by k1, then by (k2..km) within (prefix, k1) runs]
+// (MSD) and [sort by km, then by (k1..km-1)] (LSD).  When the first such step
+// can be a run-level sort (its key's runs are long), use that chain.
+void exec_group(Ctx& c, const TensorView& t, const uint32_t* src_c, const double* src_v,
+                uint32_t* dst_c, double* dst_v, uint32_t* tmp_c, double* tmp_v, const Group& g) {
+  Workspace& ws = c.ws;
+  const uint64_t N = t.nnz;
+  const uint32_t R = t.rank;
+  // Off by default: the move of short runs (gather of ~6-row runs) does not
+  // yet beat two chunk passes on the c2 data; QD_RUN_SORT=1 enables it.
+  const bool disabled = getenv("QD_RUN_SORT") == nullptr;
+  uint64_t min_rows = kRunSortMinRows;
+  if (const char* e = getenv("QD_RUN_SORT_MIN_ROWS")) min_rows = strtoull(e, nullptr, 10);
+  // candidates: the key mode is not the last mode (its runs would be single
+  // rows of a duplicate-free tensor) and every prefix mode precedes it
+  auto candidate = [&](uint32_t k) {
+    if (k + 1 >= R) return false;
+    for (uint32_t p : g.prefix)
+      if (p > k) return false;
+    return true;
+  };
+  const size_t m = g.keys.size();
+  if (!disabled && g.check_range && g.prefix.empty() && m >= 1 && N >= min_rows) {
+    auto* xc = m >= 2 ? ws.get<uint32_t>("rowsC_c", N * R) : nullptr;
+    auto* xv = m >= 2 ? ws.get<double>("rowsC_v", N) : nullptr;
+    const uint32_t k1 = g.keys[0], km = g.keys[m - 1];
+    if (candidate(k1)) {
+      if (try_run_sort(c, t, src_c, src_v, m == 1 ? dst_c : xc, m == 1 ? dst_v : xv, k1)) {
+        if (m >= 2) {
+          Group rest;
+          rest.prefix = g.prefix;
+          rest.prefix.push_back(k1);
+          rest.keys.assign(g.keys.begin() + 1, g.keys.end());
+          segmented_sort(c, t, xc, xv, dst_c, dst_v, tmp_c, tmp_v, rest);
+        }
+        return;
+      }
+    } else if (m >= 2 && candidate(km)) {
+      if (try_run_sort(c, t, src_c, src_v, xc, xv, km)) {
+        Group rest;
+        rest.prefix = g.prefix;
+        rest.keys.assign(g.keys.begin(), g.keys.end() - 1);
+        segmented_sort(c, t, xc, xv, dst_c, dst_v, tmp_c, tmp_v, rest);
+        return;
+      }
+    }
+  }
+  segmented_sort(c, t, src_c, src_v, dst_c, dst_v, tmp_c, tmp_v, g);
+}
 }  // namespace
 
 // Synchronise, fold profiling records, and throw the first error found.
@@ -2007,7 +2231,7 @@ static void run_groups_once(Workspace& ws, const TensorView& t, const uint32_t* 
         tv = d_v_out;
       }
       c.group = (int)gi;
-      segmented_sort(c, t, sc, sv, dc, dv, tc, tv, groups[gi]);
+      exec_group(c, t, sc, sv, dc, dv, tc, tv, groups[gi]);
       sc = dc;
       sv = dv;
     }

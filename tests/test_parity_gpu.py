@@ -377,3 +377,38 @@ def test_unchecked_mode_out_of_range_is_moved_not_truncated(ws):
     c, v, _ = ORC.transpose(t.dims, t.coords, t.values, [2, 1, 0])
     out = qd.transpose(t, [2, 1, 0], ws=ws)
     assert same(out, c, v)
+
+
+@pytest.mark.parametrize("target", [[1, 0, 2], [2, 1, 0], [1, 2, 0], [0, 2, 1], [2, 0, 1]])
+@pytest.mark.parametrize("skew", [False, True])
+def test_run_level_sort_chains(ws, target, skew):
+    # long runs of equal (i0, i1) make the run-level sort (and the MSD/LSD
+    # chains that start with it) kick in; forced on at this size via env
+    os.environ["QD_RUN_SORT_MIN_ROWS"] = "1"
+    os.environ["QD_RUN_SORT"] = "1"
+    try:
+        rng = np.random.default_rng(31 + skew)
+        if skew:
+            from paper_2005_10427_b200 import synth
+            cfg = synth.Config("t", [60, 80, 20000], 400_000, ["zipf"] * 3, s=1.3, seed=5)
+            c, v = synth.generate(cfg)
+            t = qd.CooTensor(cfg.dims, c, v)
+        else:
+            t = rand_tensor(rng, [20, 50, 20000], 300_000)
+        out = qd.transpose(t, target, ws=ws)
+        c, v, _ = ORC.transpose(t.dims, t.coords, t.values, target)
+        assert same(out, c, v)
+        # an out-of-range mode-1 coordinate: found through the run records
+        # when mode 1 is sorted by the plan, moved untouched otherwise
+        bad = t.copy()
+        bad.coords[3 * 1000 + 1] = 50 if not skew else 80
+        sorted_modes = {s.mode for s in qd.quesadilla_plan(target).steps}
+        if 1 in sorted_modes:
+            with pytest.raises(qd.OutOfRange):
+                qd.transpose(bad, target, ws=ws)
+        else:
+            c, v, _ = ORC.transpose(bad.dims, bad.coords, bad.values, target)
+            assert same(qd.transpose(bad, target, ws=ws), c, v)
+    finally:
+        del os.environ["QD_RUN_SORT_MIN_ROWS"]
+        del os.environ["QD_RUN_SORT"]
