@@ -196,6 +196,25 @@ def run_reference(args, cfg, rank):
     }))
 
 
+def survey_bytes(dims, target, n):
+    """SURVEY.md §8(d) algorithmic byte model B_total for one transpose."""
+    import paper_2005_10427_b200 as qd
+    r = len(dims)
+    steps = qd.quesadilla_plan(target).steps
+    if not steps:
+        return 0
+    used = set()
+    for st in steps:
+        used.add(st.mode)
+        used.update(target[: st.prefix_len])
+    b = n * (4 * r + 4 * len(used))
+    for i, st in enumerate(steps):
+        l = st.prefix_len
+        b += n * (4 + 4 + 4 * (i > 0) + (4 * l + 8 if l > 0 else 0)) + 8 * (dims[st.mode] + 1)
+    b += n * (4 + 2 * (4 * r + 8)) + 4 * (dims[target[0]] + 1)
+    return b
+
+
 def workload_config(cfg, n, world=1):
     return {"workload": f"{cfg.name}: {'x'.join(map(str, cfg.dims))}, {n} unique nnz "
                         f"({cfg.dist[0]} s={cfg.s}), targets "
@@ -279,6 +298,25 @@ def main():
     step_ms = ms / args.steps
     share = {k: round(v["ms"] / args.steps / step_ms, 4) for k, v in prof.items()}
 
+    # per-target device time (one extra untimed-for-value round) and the
+    # SURVEY §8(d) byte-model roofline fraction of each
+    per_target = {}
+    model_bytes = 0
+    for t in cfg.targets:
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        qd.transpose_device(r, cfg.dims, n, ci.data_ptr(), vi.data_ptr(), co.data_ptr(),
+                            vo.data_ptr(), t, qd.SortStrategy.quesadilla(), ws, sp)
+        a1.record(stream)
+        torch.cuda.synchronize()
+        tms = a0.elapsed_time(a1)
+        mb = survey_bytes(cfg.dims, t, n)
+        model_bytes += mb
+        per_target["".join(str(x) for x in t)] = {
+            "ms": round(tms, 4), "Mnnz_s": round(n / tms / 1e3, 1),
+            "model_GB": round(mb / 1e9, 3),
+            "model_frac": round(mb / (tms / 1e3) / 1e9 / peaks()[0], 4)}
+
     # end to end through the host C-ABI entry, pinned host buffers
     e2e = None
     if not args.no_e2e:
@@ -327,6 +365,11 @@ def main():
                      "bytes_per_launch": round(p["bytes"] / max(1, p["launches"])),
                      "avg_launch_us": round(p["ms"] / max(1, p["launches"]) * 1e3, 2),
                      "step_share": share},
+        "model_roofline": {"note": "SURVEY.md §8(d) B_total byte model per step over the 5 targets",
+                           "bytes_per_step": model_bytes,
+                           "achieved_GBs": round(model_bytes / (step_ms / 1e3) / 1e9, 1),
+                           "frac": round(model_bytes / (step_ms / 1e3) / 1e9 / peaks()[0], 4),
+                           "per_target": per_target},
         "e2e": e2e,
         "gpu_launches": launches,
         "clocks": clk.summary(),
