@@ -165,6 +165,7 @@ struct ChunkHistArgs {
   uint32_t pk_shift, pk_mask;  // digit of a PK row
   int check_pack;              // flag bit2 if a coordinate would not pack losslessly
   PackSpec pack;
+  const uint8_t* digits;       // this pass's digit per row, written by the previous scatter
 };
 
 struct ScatterArgs {
@@ -183,6 +184,8 @@ struct ScatterArgs {
   DigitSpec dig;
   uint32_t pk_shift, pk_mask;  // digit of a PK row
   PackSpec pack;
+  uint8_t* next_dig;           // PK output: next pass's digit per row (side channel)
+  uint32_t nd_shift, nd_mask;
 };
 
 // ---------------------------------------------------------------------------
@@ -506,6 +509,32 @@ __global__ void __launch_bounds__(kThreads) k_chunk_hist(ChunkHistArgs a) {
     __syncthreads();
     const ChunkDesc cd = a.chunks[ci];
     if (threadIdx.x == 0 && a.rows_counter) atomicAdd(a.rows_counter, (unsigned long long)cd.len);
+    if (a.digits) {
+      // digit bytes left by the previous pass's scatter: 16 rows per load
+      const uint8_t* dg8 = a.digits + cd.row_begin;
+      uint32_t* wh = s_h + w * kBins;
+      const uint32_t head = (uint32_t)min((unsigned long long)cd.len,
+                                          (unsigned long long)((16u - ((uintptr_t)dg8 & 15u)) & 15u));
+      if (threadIdx.x < head) atomicAdd(wh + dg8[threadIdx.x], 1u);
+      const uint32_t nv = (cd.len - head) >> 4;
+      const uint4* v4 = reinterpret_cast<const uint4*>(dg8 + head);
+#pragma unroll 2
+      for (uint32_t v = threadIdx.x; v < nv; v += kThreads) {
+        const uint4 x = __ldcs(v4 + v);
+        const uint32_t wd[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          atomicAdd(wh + (wd[q] & 0xFFu), 1u);
+          atomicAdd(wh + ((wd[q] >> 8) & 0xFFu), 1u);
+          atomicAdd(wh + ((wd[q] >> 16) & 0xFFu), 1u);
+          atomicAdd(wh + (wd[q] >> 24), 1u);
+        }
+      }
+      for (uint32_t k = head + nv * 16 + threadIdx.x; k < cd.len; k += kThreads)
+        atomicAdd(wh + dg8[k], 1u);
+      __syncthreads();
+      goto flush;
+    }
     if (a.in.fmt == kPK) {
       // 16-byte rows: digit from the packed word
       const ulonglong2* rows = reinterpret_cast<const ulonglong2*>(a.in.c) + cd.row_begin;
@@ -891,6 +920,7 @@ __global__ void __launch_bounds__(kSortThreads, 1024 / kSortThreads) k_scatter(S
         const ulonglong2 row = s_pk[i];
         if (OUT == kPK) {
           __stcs(reinterpret_cast<ulonglong2*>(a.out.c) + dst, row);
+          if (a.next_dig) __stcs(a.next_dig + dst, (uint8_t)((row.x >> a.nd_shift) & a.nd_mask));
         } else {  // unpack into AoS
           uint32_t* o = a.out.c + dst * R;
           if (RT) {
@@ -921,6 +951,7 @@ __global__ void __launch_bounds__(kSortThreads, 1024 / kSortThreads) k_scatter(S
         }
         __stcs(reinterpret_cast<ulonglong2*>(a.out.c) + dst,
                make_ulonglong2(pk, (unsigned long long)__double_as_longlong(v)));
+        if (a.next_dig) __stcs(a.next_dig + dst, (uint8_t)((pk >> a.nd_shift) & a.nd_mask));
         continue;
       }
       if (RT) {
@@ -1800,7 +1831,8 @@ void run_pass(Ctx& c, uint32_t R, uint64_t N, uint32_t T, Rows in, RowsOut out,
               const ChunkDesc* chunks, uint64_t num_chunks,
               const unsigned long long* run_start, const DigitSpec& dig, const KeySpec& key,
               bool check, unsigned long long** offs_out = nullptr, const PackSpec* pack = nullptr,
-              uint32_t pk_shift = 0, uint32_t pk_mask = 0) {
+              uint32_t pk_shift = 0, uint32_t pk_mask = 0, const uint8_t* digits_in = nullptr,
+              uint8_t* digits_out = nullptr, uint32_t nd_shift = 0, uint32_t nd_mask = 0) {
   Workspace& ws = c.ws;
   const uint64_t nflat = num_chunks * kBins;
   auto* flat = ws.get<uint32_t>("chunk_flat", nflat);
@@ -1820,6 +1852,7 @@ void run_pass(Ctx& c, uint32_t R, uint64_t N, uint32_t T, Rows in, RowsOut out,
   h.rows_counter = check ? &c.err->rows[std::min(c.group, kMaxGroups - 1)] : nullptr;
   h.pk_shift = pk_shift;
   h.pk_mask = pk_mask;
+  h.digits = digits_in;
   if (pack) {
     h.pack = *pack;
     h.check_pack = in.fmt == kAoS && out.fmt == kPK;
@@ -1844,6 +1877,9 @@ void run_pass(Ctx& c, uint32_t R, uint64_t N, uint32_t T, Rows in, RowsOut out,
   a.pk_shift = pk_shift;
   a.pk_mask = pk_mask;
   if (pack) a.pack = *pack;
+  a.next_dig = digits_out;
+  a.nd_shift = nd_shift;
+  a.nd_mask = nd_mask;
   if (const char* e = getenv("QD_SCATTER_DBG")) a.dbg = atoi(e);
   if (a.dbg & 2) {
     a.dbg_t = ws.get<unsigned long long>("dbg_t", 16);
@@ -2026,9 +2062,11 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
     }
     // packed intermediates ping-pong in workspace buffers of 16 bytes/row
     uint32_t* pk[2] = {nullptr, nullptr};
+    uint8_t* digbuf = nullptr;
     if (packed) {
       pk[0] = ws.get<uint32_t>("pkA", N * 4);
       if (D > 2) pk[1] = ws.get<uint32_t>("pkB", N * 4);
+      digbuf = ws.get<uint8_t>("digits", N + 16);
     }
     Rows in{src_c, src_v, kAoS};
     for (uint32_t q = 0; q < D; ++q) {
@@ -2038,9 +2076,14 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
       RowsOut out{to_dst ? dst_c : tmp_c, to_dst ? dst_v : tmp_v, ofmt};
       if (ofmt == kPK) out = RowsOut{pk[q % 2], nullptr, kPK};
       const uint32_t lo = q * per, hi = std::min(bits, lo + per);
+      // packed passes hand the next pass its digit bytes (1 B/row instead of
+      // re-reading 16 B rows for the next histogram)
+      const uint8_t* dig_in = (packed && q > 0) ? digbuf : nullptr;
+      uint8_t* dig_out = (packed && !last) ? digbuf : nullptr;
+      const uint32_t nlo = (q + 1) * per, nhi = std::min(bits, nlo + per);
       run_pass(c, R, N, T, in, out, chunks, num_chunks, run_start, digs[q], key,
                q == 0 && key.check, nullptr, packed ? &pack : nullptr, lo,
-               (1u << (hi - lo)) - 1u);
+               (1u << (hi - lo)) - 1u, dig_in, dig_out, nlo, last ? 0u : (1u << (nhi - nlo)) - 1u);
       in = Rows{out.c, out.v, out.fmt};
     }
   }
