@@ -241,7 +241,7 @@ def main():
     import paper_2005_10427_b200 as qd
     torch.cuda.set_device(local)
     dist = None
-    if world > 1:
+    if world > 1 or os.environ.get("QD_FORCE_SHARDED"):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         from paper_2005_10427_b200 import shard

@@ -193,20 +193,69 @@ def bench_sharded(args, cfg, dist, rank, world, local):
         step()
     torch.cuda.synchronize()
     dist.barrier()
+    import bench as B  # the driver-side helpers (clock sampler, peaks)
+    be.ws.profile(True)
+    be.ws.profile_reset()
+    l0 = be.ws.launches()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(args.steps):
-        step()
-    e1.record()
-    torch.cuda.synchronize()
+    with B.ClockSampler(local) as clk:
+        e0.record()
+        for _ in range(args.steps):
+            step()
+        e1.record()
+        torch.cuda.synchronize()
     dist.barrier()
+    launches = be.ws.launches() - l0
+    prof = be.ws.profile_stats()
+    be.ws.profile(False)
     ms = torch.tensor([e0.elapsed_time(e1)], device="cuda")
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     total = torch.tensor([n_local], device="cuda", dtype=torch.int64)
     dist.all_reduce(total)
+
+    # end to end: every rank copies its slice in from pinned host memory,
+    # runs the sharded transpose and copies its output slice back
+    hc = torch.empty(ci.shape, dtype=ci.dtype).pin_memory()
+    hv = torch.empty(vi.shape, dtype=vi.dtype).pin_memory()
+    hc.copy_(ci)
+    hv.copy_(vi)
+    dc, dv = torch.empty_like(ci), torch.empty_like(vi)
+    # output slices may be larger than the input slice after the exchange
+    cap = 2 * n_local + 1024
+    oc = torch.empty(cap * r, dtype=ci.dtype).pin_memory()
+    ov = torch.empty(cap, dtype=vi.dtype).pin_memory()
+    torch.cuda.synchronize()
+    dist.barrier()
+    k_e2e = max(1, min(args.steps, 3))
+    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    h2d = d2h = 0
+    a0.record()
+    for _ in range(k_e2e):
+        for t in cfg.targets:
+            dc.copy_(hc, non_blocking=True)
+            dv.copy_(hv, non_blocking=True)
+            out, _ = sharded_transpose(dist, be, LocalRows(dc, dv), gdims, t)
+            n_out = out.values.numel()
+            if n_out > ov.numel():
+                oc = torch.empty(n_out * r, dtype=ci.dtype).pin_memory()
+                ov = torch.empty(n_out, dtype=vi.dtype).pin_memory()
+            oc[:n_out * r].copy_(out.coords, non_blocking=True)
+            ov[:n_out].copy_(out.values, non_blocking=True)
+            h2d += dc.numel() * 4 + dv.numel() * 8
+            d2h += n_out * (4 * r + 8)
+    a1.record()
+    torch.cuda.synchronize()
+    e2e_ms = torch.tensor([a0.elapsed_time(a1)], device="cuda")
+    dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
     if rank == 0:
         units = int(total.item()) * len(cfg.targets) * args.steps
         v = units / (ms.item() / 1e3) / 1e6
+        top = max(("scatter", "local", "hist"), key=lambda k: prof[k]["ms"])
+        p = prof[top]
+        peak, peak_kind = B.peaks()
+        achieved = (p["bytes"] / p["launches"]) / (p["ms"] / p["launches"] / 1e3) / 1e9 \
+            if p["ms"] and p["launches"] else 0.0
+        e2e_units = int(total.item()) * len(cfg.targets) * k_e2e
         print(json.dumps({
             "metric": "nonzeros transposed/sec (Mnnz/s)", "value": round(v, 3), "unit": "Mnnz/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -216,6 +265,17 @@ def bench_sharded(args, cfg, dist, rank, world, local):
             "data": "synthetic (seeded Zipf, per-rank slices of one global tensor)",
             "config": {"workload": f"c2 x {world}: {gdims[0]}x{gdims[1]}x{gdims[2]}, "
                                    f"{int(total.item())} nnz, 5 targets",
-                       "parallelism": f"shard{world} (sigma1 ranges; all_to_all over NCCL)"},
+                       "parallelism": f"shard{world} (sigma1 ranges; all_to_all over NCCL)",
+                       "l2": "inputs larger than L2; no flush needed"},
+            "roofline": {"bound": "hbm", "kernel": {"scatter": "k_scatter", "local": "k_local",
+                                                    "hist": "k_chunk_hist"}[top],
+                         "achieved": round(achieved, 1), "peak": peak, "peak_kind": peak_kind,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+                         "rank": 0},
+            "e2e": {"value": round(e2e_units / (e2e_ms.item() / 1e3) / 1e6, 3), "unit": "Mnnz/s",
+                    "h2d_bytes_per_step": h2d // k_e2e, "d2h_bytes_per_step": d2h // k_e2e,
+                    "note": "rank 0's bytes; every rank moves its own slice"},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
         }))
     dist.destroy_process_group()
