@@ -571,25 +571,55 @@ __global__ void __launch_bounds__(kThreads) k_chunk_hist(ChunkHistArgs a) {
     if (a.in.fmt == kAoS && R == 3 && fast_dig) {
       // AoS rank-3 rows (the common first pass): coordinates in registers,
       // range + pack checks from them, run-aggregated counting
+      // Each warp takes 128 rows at a time: the loads of its four 32-row
+      // rounds are issued together (enough bytes in flight per SM to cover
+      // HBM latency), then the rounds are counted.
       const uint32_t dm0 = dg.m0, dm1 = dg.m1;
-      for (uint32_t g = w * 32; g < cd.len; g += kThreads) {  // warp-uniform
-        const uint32_t i = g + lane;
-        const bool valid = i < cd.len;
-        const uint32_t nvalid = min(32u, cd.len - g);
-        const unsigned long long r = cd.row_begin + (valid ? i : 0u);
-        const uint32_t* row = a.in.c + r * 3;
-        const uint32_t c0 = __ldcs(row), c1 = __ldcs(row + 1), c2 = __ldcs(row + 2);
-        auto cm = [&](uint32_t m) { return m == 0 ? c0 : (m == 1 ? c1 : c2); };
-        uint32_t d = 0;
-        if (valid) {
-          if (a.do_check) check_row(row, a.key, r, a.err);
-          if (a.check_pack &&
-              ((c0 >> a.pack.width[0]) | (c1 >> a.pack.width[1]) | (c2 >> a.pack.width[2])))
-            atomicOr(&a.err->flags, 4u);
-          d = ((cm(dm0) >> dg.r0) & dg.k0) << dg.l0;
-          if (dg.two) d |= ((cm(dm1) >> dg.r1) & dg.k1) << dg.l1;
+      // per-mode limits: range check (dim for key modes) and pack check
+      // (2^width) folded into one compare per coordinate
+      uint32_t lim[3];
+#pragma unroll
+      for (int m = 0; m < 3; ++m) {
+        lim[m] = 0xFFFFFFFFu;
+        if (a.do_check)
+          for (uint32_t k = 0; k < a.key.n; ++k)
+            if (a.key.mode[k] == m) lim[m] = a.key.dim[k];
+        if (a.check_pack && a.pack.width[m] < 32) lim[m] = min(lim[m], 1u << a.pack.width[m]);
+      }
+      constexpr int kQ = 4;
+      for (uint32_t g = w * 32 * kQ; g < cd.len; g += kThreads * kQ) {  // warp-uniform
+        uint32_t c[kQ][3];
+#pragma unroll
+        for (int q = 0; q < kQ; ++q) {
+          const uint32_t i = g + q * 32 + lane;
+          const uint32_t* row = a.in.c + (cd.row_begin + (i < cd.len ? i : 0u)) * 3;
+          c[q][0] = __ldcs(row);
+          c[q][1] = __ldcs(row + 1);
+          c[q][2] = __ldcs(row + 2);
         }
-        add_runs(s_h + w * kBins, d, valid, nvalid);
+#pragma unroll
+        for (int q = 0; q < kQ; ++q) {
+          if (g + q * 32 >= cd.len) break;  // warp-uniform
+          const uint32_t i = g + q * 32 + lane;
+          const bool valid = i < cd.len;
+          const uint32_t nvalid = min(32u, cd.len - (g + q * 32));
+          const uint32_t x0 = dm0 == 0 ? c[q][0] : (dm0 == 1 ? c[q][1] : c[q][2]);
+          uint32_t d = ((x0 >> dg.r0) & dg.k0) << dg.l0;
+          if (dg.two) {
+            const uint32_t x1 = dm1 == 0 ? c[q][0] : (dm1 == 1 ? c[q][1] : c[q][2]);
+            d |= ((x1 >> dg.r1) & dg.k1) << dg.l1;
+          }
+          if (valid && (c[q][0] >= lim[0] || c[q][1] >= lim[1] || c[q][2] >= lim[2])) {
+            // rare: the exact checks (range: first (row, mode); pack: flag)
+            const uint32_t* row = a.in.c + (cd.row_begin + i) * 3;
+            if (a.do_check) check_row(row, a.key, cd.row_begin + i, a.err);
+            if (a.check_pack && ((c[q][0] >> a.pack.width[0]) | (c[q][1] >> a.pack.width[1]) |
+                                 (c[q][2] >> a.pack.width[2])))
+              atomicOr(&a.err->flags, 4u);
+          }
+          if (!valid) d = 0;
+          add_runs(s_h + w * kBins, d, valid, nvalid);
+        }
       }
       __syncthreads();
       goto flush;
