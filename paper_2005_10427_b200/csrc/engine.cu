@@ -1173,6 +1173,33 @@ __global__ void __launch_bounds__(kThreads) k_heads(const uint32_t* c, uint32_t 
                                                     uint32_t* words, uint32_t* block_cnt) {
   const unsigned long long r0 = (unsigned long long)blockIdx.x * kHeadRows;
   uint32_t cnt = 0;
+  if (modes.n == 1) {
+    // one prefix mode: each row's coordinate is loaded once (all rounds'
+    // loads in flight together); the previous row's comes from lane - 1
+    constexpr int kQ = 8;
+    const uint32_t m = modes.m[0];
+    const int lane = threadIdx.x & 31;
+#pragma unroll 1
+    for (uint32_t k0 = 0; k0 < kHeadRows / kThreads; k0 += kQ) {
+      uint32_t x[kQ], y0[kQ];
+#pragma unroll
+      for (int k = 0; k < kQ; ++k) {
+        const unsigned long long i = r0 + (k0 + k) * kThreads + threadIdx.x;
+        x[k] = i < nnz ? __ldcs(c + i * rank + m) : 0u;
+        y0[k] = (lane == 0 && i > 0 && i < nnz) ? __ldg(c + (i - 1) * rank + m) : 0u;
+      }
+#pragma unroll
+      for (int k = 0; k < kQ; ++k) {
+        const unsigned long long i = r0 + (k0 + k) * kThreads + threadIdx.x;
+        const uint32_t up = __shfl_up_sync(0xFFFFFFFFu, x[k], 1);
+        const uint32_t y = lane == 0 ? y0[k] : up;
+        const bool head = i < nnz && (i == 0 || x[k] != y);
+        const unsigned bits = __ballot_sync(0xFFFFFFFFu, head);
+        if (lane == 0 && i < nnz) words[i >> 5] = bits;
+        cnt += head;
+      }
+    }
+  } else
   for (uint32_t k = 0; k < kHeadRows / kThreads; ++k) {
     const unsigned long long i = r0 + k * kThreads + threadIdx.x;
     bool head = false;
