@@ -317,34 +317,42 @@ def main():
             "model_GB": round(mb / 1e9, 3),
             "model_frac": round(mb / (tms / 1e3) / 1e9 / peaks()[0], 4)}
 
-    # end to end through the host C-ABI entry, pinned host buffers
+    # end to end through the host C-ABI entry, pinned host buffers: every
+    # step transposes a fresh host copy of the input to each target with
+    # qd_transpose_inplace_async (one call per target, as the reference CLI's
+    # bench loop makes) and waits for the last output copy; the input copy of
+    # call i+1 overlaps the output copy of call i (full-duplex PCIe).  Wall
+    # clock around the whole step: H2D + device work + D2H of all targets.
     e2e = None
     if not args.no_e2e:
         hc0 = ci.cpu().numpy().view(np.uint32)
         hv0 = vi.cpu().numpy()
-        pin_c = torch.empty(hc0.shape, dtype=torch.int32).pin_memory()
-        pin_v = torch.empty(hv0.shape, dtype=torch.float64).pin_memory()
-        hc = pin_c.numpy().view(np.uint32)
-        hv = pin_v.numpy()
-        e2e_ms = 0.0
-        k_e2e = max(1, min(args.steps, 5))
+        pins = [(torch.empty(hc0.shape, dtype=torch.int32).pin_memory(),
+                 torch.empty(hv0.shape, dtype=torch.float64).pin_memory()) for _ in cfg.targets]
+        bufs = [(pc.numpy().view(np.uint32), pv.numpy()) for pc, pv in pins]
+        e2e_s = 0.0
+        k_e2e = max(1, min(args.steps, 3))
         for it in range(k_e2e + 1):
-            for t in cfg.targets:
+            tens = []
+            for hc, hv in bufs:
                 np.copyto(hc, hc0)
                 np.copyto(hv, hv0)
-                tens = qd.CooTensor(cfg.dims, hc, hv)  # wraps the pinned buffers, no copy
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                torch.cuda.synchronize()
-                a.record()
-                qd.transpose_inplace(tens, t, qd.SortStrategy.quesadilla(), ws)
-                b.record()
-                torch.cuda.synchronize()
-                if it > 0:  # first round is warm-up (workspace growth)
-                    e2e_ms += a.elapsed_time(b)
-        e2e = {"value": round(n * len(cfg.targets) * k_e2e / (e2e_ms / 1e3) / 1e6, 3),
+                tens.append(qd.CooTensor(cfg.dims, hc, hv))  # wraps the pinned buffers
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for tn, t in zip(tens, cfg.targets):
+                qd.transpose_inplace_async(tn, t, qd.SortStrategy.quesadilla(), ws)
+            ws.synchronize()
+            dt = time.perf_counter() - t0
+            if it > 0:  # first round is warm-up (workspace growth)
+                e2e_s += dt
+        e2e = {"value": round(n * len(cfg.targets) * k_e2e / e2e_s / 1e6, 3),
                "unit": "Mnnz/s", "h2d_bytes_per_step": n * (4 * r + 8) * len(cfg.targets),
                "d2h_bytes_per_step": n * (4 * r + 8) * len(cfg.targets),
-               "steps": k_e2e, "api": "qd_transpose_inplace (host buffers, pinned)"}
+               "steps": k_e2e, "timing": "host wall clock per step (all copies + device work)",
+               "api": "qd_transpose_inplace_async x targets + qd_workspace_synchronize "
+                      "(host buffers, pinned)"}
+        del pins, bufs
 
     cpu = None
     if not args.no_cpu_baseline:

@@ -127,6 +127,24 @@ qd_status qd_transpose_inplace(uint32_t rank, const uint32_t* dims, uint64_t nnz
                                uint32_t k, const qd_options* opts,
                                qd_workspace* ws);
 
+/* Asynchronous form of qd_transpose_inplace for pipelines of host-buffer
+ * calls (e.g. the CLI bench's loop over targets, main.cpp:198-213): the
+ * host->device copy, the device transpose and the device->host copy of
+ * consecutive calls run on the workspace's own streams, so call i's output
+ * copy overlaps call i+1's input copy (PCIe is full duplex).  The call
+ * returns once its rows are sorted on the device (so out_of_range /
+ * invalid_argument are reported by the call itself, host buffers untouched);
+ * (coords, values) hold the result after qd_workspace_synchronize.  The
+ * buffers must stay valid (and should be pinned) until then; bucket
+ * boundaries are not reported by this form. */
+qd_status qd_transpose_inplace_async(uint32_t rank, const uint32_t* dims, uint64_t nnz,
+                                     uint32_t* coords, double* values,
+                                     const uint32_t* target, qd_strategy_kind kind,
+                                     uint32_t k, const qd_options* opts,
+                                     qd_workspace* ws);
+/* Wait for every asynchronous call on this workspace. */
+qd_status qd_workspace_synchronize(qd_workspace* ws);
+
 /* Device-resident, out of place (in and out must not overlap). */
 qd_status qd_transpose_device(uint32_t rank, const uint32_t* dims, uint64_t nnz,
                               const uint32_t* d_coords_in,

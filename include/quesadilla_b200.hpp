@@ -203,10 +203,37 @@ class Workspace {
   Workspace(const Workspace&) = delete;
   Workspace& operator=(const Workspace&) = delete;
   qd_workspace* get() const { return ws_; }
+  // wait for every transpose_inplace_async on this workspace
+  void synchronize() { detail::check(qd_workspace_synchronize(ws_)); }
 
  private:
   qd_workspace* ws_ = nullptr;
 };
+
+// transpose_inplace whose device->host copy completes at ws.synchronize();
+// consecutive calls overlap one's output copy with the next one's input copy.
+// Errors throw from the call itself (tensor untouched); t must outlive the
+// synchronize.  No bucket boundaries in this form.
+inline void transpose_inplace_async(CooTensor& t, const Ordering& target, const SortStrategy& s,
+                                    Workspace& ws, const TransposeOptions& opts = {}) {
+  if (target.rank() != t.rank())
+    throw std::invalid_argument("target ordering rank does not match tensor");
+  if (opts.boundaries)
+    throw std::invalid_argument("bucket boundaries are only reported by transpose_inplace");
+  std::vector<qd_plan_step> log(4096);
+  std::uint32_t nlog = 0;
+  qd_options o{};
+  o.verify_input = opts.verify_input;
+  o.workers = opts.parallel.workers;
+  o.pass_log = log.data();
+  o.pass_log_capacity = 4096;
+  o.pass_log_len = &nlog;
+  detail::check(qd_transpose_inplace_async(t.rank(), t.dims.data(), t.nnz(), t.coords.data(),
+                                           t.values.data(), target.modes().data(), s.c_kind(),
+                                           s.k, &o, ws.get()));
+  if (opts.pass_log)
+    for (std::uint32_t i = 0; i < nlog; ++i) opts.pass_log->push_back({log[i].prefix_len, log[i].mode});
+}
 
 inline void transpose_inplace(CooTensor& t, const Ordering& target, const SortStrategy& s,
                               Workspace& ws, const TransposeOptions& opts = {}) {

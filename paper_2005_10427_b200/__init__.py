@@ -115,6 +115,8 @@ def lib():
                                             C.POINTER(C.c_int), C.POINTER(C.c_int)]
         L.qd_transpose_inplace.argtypes = [C.c_uint32, _u32p, C.c_uint64, _u32p, _f64p, _u32p,
                                            C.c_int, C.c_uint32, C.POINTER(OptionsC), C.c_void_p]
+        L.qd_transpose_inplace_async.argtypes = L.qd_transpose_inplace.argtypes
+        L.qd_workspace_synchronize.argtypes = [C.c_void_p]
         L.qd_transpose_device.argtypes = [C.c_uint32, _u32p, C.c_uint64, C.c_void_p, C.c_void_p,
                                           C.c_void_p, C.c_void_p, _u32p, C.c_int, C.c_uint32,
                                           C.POINTER(OptionsC), C.c_void_p, C.c_void_p]
@@ -475,6 +477,11 @@ class Workspace:
             out[name] = {"launches": n.value, "ms": ms.value, "bytes": b.value}
         return out
 
+    def synchronize(self):
+        """Wait for this workspace's asynchronous calls (transpose_inplace_async)."""
+        _check(lib().qd_workspace_synchronize(self._h))
+        self._pending = []
+
     def close(self):
         if self._h:
             lib().qd_workspace_destroy(self._h)
@@ -548,6 +555,29 @@ def transpose_inplace(tensor: CooTensor, target, strategy: SortStrategy = SortSt
         tensor.values.ctypes.data_as(_f64p), _ptr_u32(t), KINDS[strategy.kind], strategy.k,
         C.byref(o), w.handle))
     _finish_options(opts, keep)
+
+
+def transpose_inplace_async(tensor: CooTensor, target, strategy: SortStrategy = SortStrategy(),
+                            ws: Optional[Workspace] = None,
+                            opts: Optional[TransposeOptions] = None) -> None:
+    """transpose_inplace whose device->host copy completes at ws.synchronize();
+    consecutive calls overlap one call's output copy with the next one's input
+    copy.  Errors are raised by the call itself (tensor untouched).  The
+    tensor's arrays must stay alive (and should be pinned) until then."""
+    target = _ord(target)
+    if target.rank() != tensor.rank():
+        raise InvalidArgument("target ordering rank does not match tensor")
+    w = _ws(ws)
+    o, keep = _options(opts, tensor.nnz())
+    t = _arr_u32(target.modes())
+    _check(lib().qd_transpose_inplace_async(
+        tensor.rank(), _ptr_u32(tensor.dims), tensor.nnz(), _ptr_u32(tensor.coords),
+        tensor.values.ctypes.data_as(_f64p), _ptr_u32(t), KINDS[strategy.kind], strategy.k,
+        C.byref(o), w.handle))
+    _finish_options(opts, keep)
+    if not hasattr(w, "_pending"):
+        w._pending = []
+    w._pending.append(tensor)  # keep the host arrays alive until synchronize()
 
 
 def transpose(tensor: CooTensor, target, strategy: SortStrategy = SortStrategy(),

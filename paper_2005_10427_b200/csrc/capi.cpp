@@ -187,6 +187,33 @@ qd_status qd_transpose_inplace(uint32_t rank, const uint32_t* dims, uint64_t nnz
   });
 }
 
+qd_status qd_transpose_inplace_async(uint32_t rank, const uint32_t* dims, uint64_t nnz,
+                                     uint32_t* coords, double* values, const uint32_t* target,
+                                     qd_strategy_kind kind, uint32_t k, const qd_options* opts,
+                                     qd_workspace* ws) {
+  return guard([&] {
+    if (!ws) invalid("workspace is null");
+    check_tensor(rank, dims, nnz, coords, values);
+    check_ordering(target, rank);
+    if (opts && (opts->boundaries || opts->n_boundaries))
+      invalid("bucket boundaries are only reported by the synchronous calls");
+    std::vector<Step> steps;
+    auto groups = strategy_groups(target, rank, kind, k, &steps);
+    check_workers(opts, kind, steps);
+    TensorView t{rank, dims, nnz};
+    run_groups_host_async(*reinterpret_cast<Workspace*>(ws), t, coords, values, groups,
+                          opts && opts->verify_input);
+    log_steps(opts, steps);
+  });
+}
+
+qd_status qd_workspace_synchronize(qd_workspace* ws) {
+  return guard([&] {
+    if (!ws) invalid("workspace is null");
+    workspace_synchronize(reinterpret_cast<Workspace*>(ws));
+  });
+}
+
 qd_status qd_transpose_device(uint32_t rank, const uint32_t* dims, uint64_t nnz,
                               const uint32_t* d_coords_in, const double* d_values_in,
                               uint32_t* d_coords_out, double* d_values_out,

@@ -1574,6 +1574,20 @@ struct Workspace {
   ErrBlock* h_err = nullptr;  // pinned
   uint64_t* h_small = nullptr;  // pinned scratch for small D2H reads
   bool allow_pack = true;  // packed intermediates (cleared for a lossy-pack redo)
+  // asynchronous host-buffer transposes (qd_transpose_inplace_async): two
+  // device slots; the H2D, device and D2H work of consecutive calls runs on
+  // separate non-blocking streams so one call's output copy overlaps the
+  // next call's input copy (PCIe is full duplex)
+  cudaStream_t s_in = nullptr, s_comp = nullptr, s_out = nullptr;
+  cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_comp[2] = {nullptr, nullptr},
+              ev_out[2] = {nullptr, nullptr};
+  int slot = 0;
+  struct HostSpan {
+    const void* c = nullptr;
+    size_t nc = 0;
+    const void* v = nullptr;
+    size_t nv = 0;
+  } last_host;  // host bytes the latest async call writes back
   // live per-kernel-class timing (CUDA events on the launch stream)
   bool prof = false;
   struct ProfStat {
@@ -1673,6 +1687,14 @@ Workspace* workspace_create(int device) {
 void workspace_destroy(Workspace* ws) {
   if (!ws) return;
   cudaSetDevice(ws->device);
+  for (cudaStream_t st : {ws->s_in, ws->s_comp, ws->s_out})
+    if (st) {
+      cudaStreamSynchronize(st);
+      cudaStreamDestroy(st);
+    }
+  for (int i = 0; i < 2; ++i)
+    for (cudaEvent_t e : {ws->ev_in[i], ws->ev_comp[i], ws->ev_out[i]})
+      if (e) cudaEventDestroy(e);
   for (auto& kv : ws->bufs)
     if (kv.second.p) cudaFree(kv.second.p);
   if (ws->h_err) cudaFreeHost(ws->h_err);
@@ -2394,6 +2416,61 @@ void run_groups_host(Workspace& ws, const TensorView& t, uint32_t* coords, doubl
     QD_CUDA(cudaStreamSynchronize(st));
   }
   if (n_boundaries) *n_boundaries = nb;
+}
+
+void run_groups_host_async(Workspace& ws, const TensorView& t, uint32_t* coords, double* values,
+                           const std::vector<Group>& groups, bool verify_input) {
+  QD_CUDA(cudaSetDevice(ws.device));
+  if (!ws.s_in) {
+    for (cudaStream_t* st : {&ws.s_in, &ws.s_comp, &ws.s_out})
+      QD_CUDA(cudaStreamCreateWithFlags(st, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i)
+      for (cudaEvent_t* e : {&ws.ev_in[i], &ws.ev_comp[i], &ws.ev_out[i]}) {
+        QD_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+        QD_CUDA(cudaEventRecord(*e, ws.s_in));  // "done" until first use
+      }
+  }
+  const uint64_t N = t.nnz;
+  const uint32_t R = t.rank;
+  const int sl = ws.slot;
+  const std::string tag = std::to_string(sl);
+  uint32_t* ic = ws.get<uint32_t>("async_in_c" + tag, N * R);
+  double* iv = ws.get<double>("async_in_v" + tag, N);
+  uint32_t* oc = ws.get<uint32_t>("async_out_c" + tag, N * R);
+  double* ov = ws.get<double>("async_out_v" + tag, N);
+  // the slot's buffers are free once its previous output copy has drained;
+  // and if this call reads host bytes the previous call is still writing
+  // (chained in-place calls), its output copy must land first
+  QD_CUDA(cudaStreamWaitEvent(ws.s_in, ws.ev_out[sl], 0));
+  auto overlaps = [](const void* a, size_t na, const void* b, size_t nb) {
+    const char *x = static_cast<const char*>(a), *y = static_cast<const char*>(b);
+    return na && nb && x < y + nb && y < x + na;
+  };
+  const Workspace::HostSpan cur{coords, N * R * 4, values, N * 8};
+  const Workspace::HostSpan& prev = ws.last_host;
+  if (overlaps(cur.c, cur.nc, prev.c, prev.nc) || overlaps(cur.c, cur.nc, prev.v, prev.nv) ||
+      overlaps(cur.v, cur.nv, prev.c, prev.nc) || overlaps(cur.v, cur.nv, prev.v, prev.nv))
+    QD_CUDA(cudaStreamWaitEvent(ws.s_in, ws.ev_out[sl ^ 1], 0));
+  QD_CUDA(cudaMemcpyAsync(ic, coords, N * R * 4, cudaMemcpyHostToDevice, ws.s_in));
+  QD_CUDA(cudaMemcpyAsync(iv, values, N * 8, cudaMemcpyHostToDevice, ws.s_in));
+  QD_CUDA(cudaEventRecord(ws.ev_in[sl], ws.s_in));
+  QD_CUDA(cudaStreamWaitEvent(ws.s_comp, ws.ev_in[sl], 0));
+  // device work; its internal host syncs return once this call's rows are
+  // sorted (and report out_of_range before any host byte is written)
+  run_groups(ws, t, ic, iv, oc, ov, groups, verify_input, nullptr, nullptr, 0, ws.s_comp);
+  QD_CUDA(cudaEventRecord(ws.ev_comp[sl], ws.s_comp));
+  QD_CUDA(cudaStreamWaitEvent(ws.s_out, ws.ev_comp[sl], 0));
+  QD_CUDA(cudaMemcpyAsync(coords, oc, N * R * 4, cudaMemcpyDeviceToHost, ws.s_out));
+  QD_CUDA(cudaMemcpyAsync(values, ov, N * 8, cudaMemcpyDeviceToHost, ws.s_out));
+  QD_CUDA(cudaEventRecord(ws.ev_out[sl], ws.s_out));
+  ws.slot = sl ^ 1;
+  ws.last_host = cur;
+}
+
+void workspace_synchronize(Workspace* ws) {
+  QD_CUDA(cudaSetDevice(ws->device));
+  for (cudaStream_t st : {ws->s_in, ws->s_comp, ws->s_out})
+    if (st) QD_CUDA(cudaStreamSynchronize(st));
 }
 
 bool is_sorted_device(Workspace& ws, uint32_t rank, uint64_t nnz, const uint32_t* d_coords,

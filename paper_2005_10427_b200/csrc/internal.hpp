@@ -85,6 +85,9 @@ void run_groups(Workspace& ws, const TensorView& t, const uint32_t* d_c_in,
                 uint32_t boundary_mode, void* stream);
 
 // Host-buffer convenience: H2D, run_groups, D2H (only on success).
+void run_groups_host_async(Workspace& ws, const TensorView& t, uint32_t* coords, double* values,
+                           const std::vector<Group>& groups, bool verify_input);
+void workspace_synchronize(Workspace* ws);
 void run_groups_host(Workspace& ws, const TensorView& t, uint32_t* coords,
                      double* values, const std::vector<Group>& groups,
                      bool verify_input, uint64_t* h_boundaries,

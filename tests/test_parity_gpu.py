@@ -412,3 +412,57 @@ def test_run_level_sort_chains(ws, target, skew):
     finally:
         del os.environ["QD_RUN_SORT_MIN_ROWS"]
         del os.environ["QD_RUN_SORT"]
+
+
+# --- asynchronous host-buffer calls (qd_transpose_inplace_async) ------------
+
+def test_async_pipeline_matches_oracle(ws):
+    """A pipeline of async calls (one tensor copy per target, as the CLI bench
+    loop does) gives every call the oracle's output once synchronized."""
+    rng = np.random.default_rng(11)
+    base = rand_tensor(rng, [300, 200, 500], 400_000, distinct=True)
+    targets = [[0, 2, 1], [1, 0, 2], [1, 2, 0], [2, 0, 1], [2, 1, 0]]
+    copies = [base.copy() for _ in targets]
+    logs = [[] for _ in targets]
+    for t, tgt, lg in zip(copies, targets, logs):
+        qd.transpose_inplace_async(t, tgt, qd.SortStrategy.quesadilla(), ws,
+                                   qd.TransposeOptions(pass_log=lg))
+    ws.synchronize()
+    for t, tgt, lg in zip(copies, targets, logs):
+        c, v, steps = ORC.transpose(base.dims, base.coords, base.values, tgt)
+        assert same(t, c, v), tgt
+        assert [(s.prefix_len, s.mode) for s in lg] == [tuple(x) for x in steps]
+
+
+def test_async_chained_on_same_buffers(ws):
+    """Chained in-place async calls on ONE tensor: the second call's input copy
+    must wait for the first call's output copy."""
+    rng = np.random.default_rng(12)
+    base = rand_tensor(rng, [60, 70, 80], 150_000)
+    t = base.copy()
+    qd.transpose_inplace_async(t, [0, 2, 1], qd.SortStrategy.quesadilla(), ws)
+    # (0,2,1)-sorted data is not simply sorted; a full radix re-sort to (2,1,0)
+    # is valid on any order and must see the first call's output
+    qd.transpose_inplace_async(t, [2, 1, 0], qd.SortStrategy.full_radix(), ws)
+    ws.synchronize()
+    c1, v1, _ = ORC.transpose(base.dims, base.coords, base.values, [0, 2, 1])
+    c2, v2, _ = ORC.transpose(base.dims, c1, v1, [2, 1, 0], "radix")
+    assert same(t, c2, v2)
+
+
+def test_async_errors_leave_tensor_untouched(ws):
+    rng = np.random.default_rng(13)
+    big = rand_tensor(rng, [5, 300, 300], 50_000)
+    big.coords[3 * 20_000 + 2] = 300
+    before = big.copy()
+    with pytest.raises(qd.OutOfRange):
+        qd.transpose_inplace_async(big, [2, 1, 0], qd.SortStrategy.quesadilla(), ws)
+    ws.synchronize()
+    assert big == before
+    with pytest.raises(qd.InvalidArgument):
+        qd.transpose_inplace_async(before, [2, 1, 0], qd.SortStrategy.quesadilla(), ws,
+                                   qd.TransposeOptions(boundaries=[]))
+    empty = qd.CooTensor([3, 3], np.zeros(0, np.uint32), np.zeros(0))
+    qd.transpose_inplace_async(empty, [1, 0], qd.SortStrategy.quesadilla(), ws)
+    ws.synchronize()
+    assert empty.nnz() == 0
