@@ -62,6 +62,9 @@ constexpr uint32_t kChunkTiles = 16;  // tiles per scatter chunk
 constexpr double kRunSortMinAvg = 2.5;       // mean run length that pays for a run sort
 constexpr uint64_t kRunSortMinRows = 1u << 20;  // below this, not worth a probe
 constexpr int kMaxRounds = 4096 / kSortThreads;  // 32-row rounds per warp per tile (T <= 4096)
+#ifndef QD_EARLY_ADVANCE
+#define QD_EARLY_ADVANCE 1
+#endif
 
 // ---------------------------------------------------------------------------
 // kernel parameter blocks
@@ -848,6 +851,11 @@ __global__ void __launch_bounds__(kSortThreads, 1024 / kSortThreads) k_scatter(S
       for (int k = threadIdx.x & 31; k < kBins; k += 32) whz[k] = 0;
       __syncwarp();
     }
+#if QD_EARLY_ADVANCE
+    // buffer b^1 was released by the previous tile's closing barrier: start
+    // the next tile's bulk copies before this tile's work
+    if (threadIdx.x >= kAdv) advance(b ^ 1u, ci, ti);
+#endif
     mbar_wait(&s_bar[b], (phases >> b) & 1u);  // each thread observes the TMA completion
     QD_TMARK(2);
     phases ^= 1u << b;
@@ -886,17 +894,36 @@ __global__ void __launch_bounds__(kSortThreads, 1024 / kSortThreads) k_scatter(S
     uint16_t* wh = s_whist + w * kBins;
     const unsigned below = (1u << lane) - 1u;
     uint32_t packed[kMaxRounds];
+    // full rounds (every lane valid: no ballot, no predicates), then at most
+    // one partial round
+    const uint32_t nrow = hi > lo ? hi - lo : 0u;
+    const uint32_t nfull = nrow >> 5;
 #pragma unroll
     for (int r = 0; r < kMaxRounds; ++r) {
+      if ((uint32_t)r >= nfull) break;  // warp-uniform
       const uint32_t p = lo + r * 32 + lane;
-      if (lo + r * 32 >= hi) break;  // warp-uniform
-      const bool valid = p < hi;
+      const uint32_t d = digit_at(p);
+      s_dig[p] = (uint16_t)d;
+      const unsigned peers = warp_peers(d, 0xFFFFFFFFu);
+      const int leader = __ffs(peers) - 1;
+      uint32_t bcount = 0;
+      if (lane == leader) {
+        bcount = wh[d];
+        wh[d] = (uint16_t)(bcount + __popc(peers));
+      }
+      bcount = __shfl_sync(0xFFFFFFFFu, bcount, leader);
+      packed[r] = ((bcount + __popc(peers & below)) << 8) | d;
+    }
+    if (nrow & 31u) {  // warp-uniform
+      const uint32_t r = nfull;
+      const uint32_t p = lo + r * 32 + lane;
+      const bool valid = lane < (nrow & 31u);
       uint32_t d = 0;
       if (valid) {
         d = digit_at(p);
         s_dig[p] = (uint16_t)d;
       }
-      unsigned peers = warp_peers(d, __ballot_sync(0xFFFFFFFFu, valid));
+      unsigned peers = warp_peers(d, (1u << (nrow & 31u)) - 1u);
       if (!valid) peers = 1u << lane;
       const int leader = __ffs(peers) - 1;
       uint32_t bcount = 0;
@@ -905,11 +932,16 @@ __global__ void __launch_bounds__(kSortThreads, 1024 / kSortThreads) k_scatter(S
         wh[d] = (uint16_t)(bcount + __popc(peers));
       }
       bcount = __shfl_sync(0xFFFFFFFFu, bcount, leader);
-      packed[r] = ((bcount + __popc(peers & below)) << 8) | d;
+      const uint32_t v = ((bcount + __popc(peers & below)) << 8) | d;
+#pragma unroll
+      for (int q = 0; q < kMaxRounds; ++q)
+        if ((uint32_t)q == r) packed[q] = v;  // static register index
     }
     __syncthreads();
     QD_TMARK(3);
+#if !QD_EARLY_ADVANCE
     if (threadIdx.x >= kAdv) advance(b ^ 1u, ci, ti);  // warp-wide; overlaps bin_totals
+#endif
     bin_totals<kSortThreads>(s_whist, s_cnt);
     __syncthreads();
     QD_TMARK(4);
@@ -924,14 +956,19 @@ __global__ void __launch_bounds__(kSortThreads, 1024 / kSortThreads) k_scatter(S
     }
     __syncthreads();
     QD_TMARK(5);
+    // sorted position of every row: all lookups first, then the stores (the
+    // compiler cannot hoist a lookup above a possibly aliasing store)
 #pragma unroll
-    for (int r = 0; r < kMaxRounds; ++r) {  // sorted position of every row
+    for (int r = 0; r < kMaxRounds; ++r) {
+      if (lo + r * 32 >= hi) break;
+      const uint32_t d = packed[r] & 0xFFu;
+      packed[r] = s_start[d] + wh[d] + (packed[r] >> 8);
+    }
+#pragma unroll
+    for (int r = 0; r < kMaxRounds; ++r) {
       const uint32_t p = lo + r * 32 + lane;
       if (lo + r * 32 >= hi) break;
-      if (p < hi) {
-        const uint32_t d = packed[r] & 0xFFu;
-        s_sorted[s_start[d] + wh[d] + (packed[r] >> 8)] = (uint16_t)p;
-      }
+      if (p < hi) s_sorted[packed[r]] = (uint16_t)p;
     }
     __syncthreads();
     QD_TMARK(6);
