@@ -942,17 +942,38 @@ __global__ void __launch_bounds__(kSortThreads, 1024 / kSortThreads) k_scatter(S
 #if !QD_EARLY_ADVANCE
     if (threadIdx.x >= kAdv) advance(b ^ 1u, ci, ti);  // warp-wide; overlaps bin_totals
 #endif
-    bin_totals<kSortThreads>(s_whist, s_cnt);
-    __syncthreads();
-    QD_TMARK(4);
-    const bool binthr = threadIdx.x < kBins;
-    const uint32_t cnt = binthr ? s_cnt[threadIdx.x] : 0u;
-    const uint32_t start = block_excl_scan<kSortThreads>(cnt, reinterpret_cast<uint32_t*>(s_tmp));
-    if (binthr) {
-      s_start[threadIdx.x] = start;
-      const unsigned long long r0 = s_run[threadIdx.x];
-      s_gbase[threadIdx.x] = (long long)r0 - (long long)start;
-      s_run[threadIdx.x] = r0 + cnt;
+    // bin totals + bin scan with two barriers: thread b (< kBins) turns the
+    // column of warp counts into warp-exclusive offsets, the first kBins/32
+    // warps scan their 32 bins with shuffles, then combine the warp sums
+    {
+      uint32_t* s_wsum = reinterpret_cast<uint32_t*>(s_tmp);
+      uint32_t cnt = 0, incl = 0;
+      if (threadIdx.x < kBins) {
+#pragma unroll
+        for (int x = 0; x < kSortWarps; ++x) {
+          const uint32_t c = s_whist[x * kBins + threadIdx.x];
+          s_whist[x * kBins + threadIdx.x] = (uint16_t)cnt;
+          cnt += c;
+        }
+        incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+          if (lane >= (uint32_t)o) incl += y;
+        }
+        if (lane == 31) s_wsum[w] = incl;
+      }
+      __syncthreads();
+      QD_TMARK(4);
+      if (threadIdx.x < kBins) {
+        uint32_t base = 0;
+        for (uint32_t x = 0; x < w; ++x) base += s_wsum[x];
+        const uint32_t start = base + incl - cnt;
+        s_start[threadIdx.x] = start;
+        const unsigned long long r0 = s_run[threadIdx.x];
+        s_gbase[threadIdx.x] = (long long)r0 - (long long)start;
+        s_run[threadIdx.x] = r0 + cnt;
+      }
     }
     __syncthreads();
     QD_TMARK(5);
