@@ -194,8 +194,6 @@ def bench_sharded(args, cfg, dist, rank, world, local):
     torch.cuda.synchronize()
     dist.barrier()
     import bench as B  # the driver-side helpers (clock sampler, peaks)
-    be.ws.profile(True)
-    be.ws.profile_reset()
     l0 = be.ws.launches()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with B.ClockSampler(local) as clk:
@@ -206,8 +204,15 @@ def bench_sharded(args, cfg, dist, rank, world, local):
         torch.cuda.synchronize()
     dist.barrier()
     launches = be.ws.launches() - l0
+    # roofline: a second region with the library's per-kernel events
+    be.ws.profile(True)
+    be.ws.profile_reset()
+    for _ in range(args.steps):
+        step()
+    torch.cuda.synchronize()
     prof = be.ws.profile_stats()
     be.ws.profile(False)
+    dist.barrier()
     ms = torch.tensor([e0.elapsed_time(e1)], device="cuda")
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     total = torch.tensor([n_local], device="cuda", dtype=torch.int64)
