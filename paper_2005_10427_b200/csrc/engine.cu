@@ -573,10 +573,7 @@ __global__ void __launch_bounds__(kThreads) k_chunk_hist(ChunkHistArgs a) {
     }
     if (a.in.fmt == kAoS && R == 3 && fast_dig) {
       // AoS rank-3 rows (the common first pass): coordinates in registers,
-      // range + pack checks from them, run-aggregated counting
-      // Each warp takes 128 rows at a time: the loads of its four 32-row
-      // rounds are issued together (enough bytes in flight per SM to cover
-      // HBM latency), then the rounds are counted.
+      // range + pack checks from them
       const uint32_t dm0 = dg.m0, dm1 = dg.m1;
       // per-mode limits: range check (dim for key modes) and pack check
       // (2^width) folded into one compare per coordinate
@@ -589,41 +586,79 @@ __global__ void __launch_bounds__(kThreads) k_chunk_hist(ChunkHistArgs a) {
             if (a.key.mode[k] == m) lim[m] = a.key.dim[k];
         if (a.check_pack && a.pack.width[m] < 32) lim[m] = min(lim[m], 1u << a.pack.width[m]);
       }
-      constexpr int kQ = 4;
-      for (uint32_t g = w * 32 * kQ; g < cd.len; g += kThreads * kQ) {  // warp-uniform
-        uint32_t c[kQ][3];
+      uint32_t* wh = s_h + w * kBins;
+      auto digit3 = [&](uint32_t c0, uint32_t c1, uint32_t c2) {
+        const uint32_t x0 = dm0 == 0 ? c0 : (dm0 == 1 ? c1 : c2);
+        uint32_t d = ((x0 >> dg.r0) & dg.k0) << dg.l0;
+        if (dg.two) {
+          const uint32_t x1 = dm1 == 0 ? c0 : (dm1 == 1 ? c1 : c2);
+          d |= ((x1 >> dg.r1) & dg.k1) << dg.l1;
+        }
+        return d;
+      };
+      auto check3 = [&](unsigned long long grow, uint32_t c0, uint32_t c1, uint32_t c2) {
+        if (c0 >= lim[0] || c1 >= lim[1] || c2 >= lim[2]) {
+          // rare: the exact checks (range: first (row, mode); pack: flag)
+          if (a.do_check) check_row(a.in.c + grow * 3, a.key, grow, a.err);
+          if (a.check_pack &&
+              ((c0 >> a.pack.width[0]) | (c1 >> a.pack.width[1]) | (c2 >> a.pack.width[2])))
+            atomicOr(&a.err->flags, 4u);
+        }
+      };
+      auto scalar_rows = [&](uint32_t from, uint32_t to) {  // rows [from, to) of the chunk
+        for (uint32_t i = from + threadIdx.x; i < to; i += kThreads) {
+          const unsigned long long gr = cd.row_begin + i;
+          const uint32_t* row = a.in.c + gr * 3;
+          const uint32_t c0 = __ldcs(row), c1 = __ldcs(row + 1), c2 = __ldcs(row + 2);
+          check3(gr, c0, c1, c2);
+          atomicAdd(wh + digit3(c0, c1, c2), 1u);
+        }
+      };
+      // Four rows (48 bytes = three 16-byte loads) per thread and two such
+      // quads in flight; equal neighbouring digits add once.
+      const uint32_t head = (uint32_t)min((unsigned long long)cd.len, (4ull - (cd.row_begin & 3ull)) & 3ull);
+      const bool vec = ((uintptr_t)a.in.c & 15u) == 0;
+      const uint32_t nquad = vec ? (cd.len - head) >> 2 : 0u;
+      scalar_rows(0, vec ? head : cd.len);
+      const uint4* q4 = reinterpret_cast<const uint4*>(a.in.c + (cd.row_begin + head) * 3);
+      for (uint32_t q0 = threadIdx.x; q0 < nquad; q0 += 2 * kThreads) {
+        uint4 x[2][3];
 #pragma unroll
-        for (int q = 0; q < kQ; ++q) {
-          const uint32_t i = g + q * 32 + lane;
-          const uint32_t* row = a.in.c + (cd.row_begin + (i < cd.len ? i : 0u)) * 3;
-          c[q][0] = __ldcs(row);
-          c[q][1] = __ldcs(row + 1);
-          c[q][2] = __ldcs(row + 2);
+        for (int u = 0; u < 2; ++u) {
+          const uint32_t q = q0 + u * kThreads;
+          if (q < nquad) {
+            x[u][0] = __ldcs(q4 + 3 * q);
+            x[u][1] = __ldcs(q4 + 3 * q + 1);
+            x[u][2] = __ldcs(q4 + 3 * q + 2);
+          }
         }
 #pragma unroll
-        for (int q = 0; q < kQ; ++q) {
-          if (g + q * 32 >= cd.len) break;  // warp-uniform
-          const uint32_t i = g + q * 32 + lane;
-          const bool valid = i < cd.len;
-          const uint32_t nvalid = min(32u, cd.len - (g + q * 32));
-          const uint32_t x0 = dm0 == 0 ? c[q][0] : (dm0 == 1 ? c[q][1] : c[q][2]);
-          uint32_t d = ((x0 >> dg.r0) & dg.k0) << dg.l0;
-          if (dg.two) {
-            const uint32_t x1 = dm1 == 0 ? c[q][0] : (dm1 == 1 ? c[q][1] : c[q][2]);
-            d |= ((x1 >> dg.r1) & dg.k1) << dg.l1;
+        for (int u = 0; u < 2; ++u) {
+          const uint32_t q = q0 + u * kThreads;
+          if (q >= nquad) break;
+          const uint32_t wv[12] = {x[u][0].x, x[u][0].y, x[u][0].z, x[u][0].w,
+                                   x[u][1].x, x[u][1].y, x[u][1].z, x[u][1].w,
+                                   x[u][2].x, x[u][2].y, x[u][2].z, x[u][2].w};
+          const unsigned long long gr = cd.row_begin + head + 4ull * q;
+          uint32_t d[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            check3(gr + k, wv[3 * k], wv[3 * k + 1], wv[3 * k + 2]);
+            d[k] = digit3(wv[3 * k], wv[3 * k + 1], wv[3 * k + 2]);
           }
-          if (valid && (c[q][0] >= lim[0] || c[q][1] >= lim[1] || c[q][2] >= lim[2])) {
-            // rare: the exact checks (range: first (row, mode); pack: flag)
-            const uint32_t* row = a.in.c + (cd.row_begin + i) * 3;
-            if (a.do_check) check_row(row, a.key, cd.row_begin + i, a.err);
-            if (a.check_pack && ((c[q][0] >> a.pack.width[0]) | (c[q][1] >> a.pack.width[1]) |
-                                 (c[q][2] >> a.pack.width[2])))
-              atomicOr(&a.err->flags, 4u);
+          uint32_t run = 1;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            if (k < 3 && d[k] == d[k + 1]) {
+              ++run;
+            } else {
+              atomicAdd(wh + d[k], run);
+              run = 1;
+            }
           }
-          if (!valid) d = 0;
-          add_runs(s_h + w * kBins, d, valid, nvalid);
         }
       }
+      if (vec) scalar_rows(head + 4 * nquad, cd.len);
       __syncthreads();
       goto flush;
     }
