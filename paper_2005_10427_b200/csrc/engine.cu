@@ -187,8 +187,9 @@ struct ScatterArgs {
   DigitSpec dig;
   uint32_t pk_shift, pk_mask;  // digit of a PK row
   PackSpec pack;
-  uint8_t* next_dig;           // PK output: next pass's digit per row (side channel)
-  uint32_t nd_shift, nd_mask;
+  uint8_t* next_dig;           // next pass's digit per row (side channel for its histogram)
+  uint32_t nd_shift, nd_mask;  // PK output: next digit = (packed >> nd_shift) & nd_mask
+  DigitSpec ndig;              // unpacked output: next digit of the coordinates
 };
 
 // ---------------------------------------------------------------------------
@@ -1088,6 +1089,8 @@ __global__ void __launch_bounds__(kSortThreads, 1024 / kSortThreads) k_scatter(S
           __stcs(OUT == kSoA ? a.out.c + (size_t)m * N + dst : a.out.c + dst * R + m, coord(i, m));
       }
       __stcs(a.out.v + dst, v);
+      if (a.next_dig)  // next pass's digit (unpacked rows: from the coordinates)
+        __stcs(a.next_dig + dst, (uint8_t)digit_by([&](uint32_t m) { return coord(i, m); }, a.ndig));
     }
     __syncthreads();  // buffer b and the scratch are free again
     QD_TMARK(7);
@@ -2004,7 +2007,8 @@ void run_pass(Ctx& c, uint32_t R, uint64_t N, uint32_t T, Rows in, RowsOut out,
               const unsigned long long* run_start, const DigitSpec& dig, const KeySpec& key,
               bool check, unsigned long long** offs_out = nullptr, const PackSpec* pack = nullptr,
               uint32_t pk_shift = 0, uint32_t pk_mask = 0, const uint8_t* digits_in = nullptr,
-              uint8_t* digits_out = nullptr, uint32_t nd_shift = 0, uint32_t nd_mask = 0) {
+              uint8_t* digits_out = nullptr, uint32_t nd_shift = 0, uint32_t nd_mask = 0,
+              const DigitSpec* next_dig = nullptr) {
   Workspace& ws = c.ws;
   const uint64_t nflat = num_chunks * kBins;
   auto* flat = ws.get<uint32_t>("chunk_flat", nflat);
@@ -2052,6 +2056,7 @@ void run_pass(Ctx& c, uint32_t R, uint64_t N, uint32_t T, Rows in, RowsOut out,
   a.next_dig = digits_out;
   a.nd_shift = nd_shift;
   a.nd_mask = nd_mask;
+  if (next_dig) a.ndig = *next_dig;
   if (const char* e = getenv("QD_SCATTER_DBG")) a.dbg = atoi(e);
   if (a.dbg & 2) {
     a.dbg_t = ws.get<unsigned long long>("dbg_t", 16);
@@ -2234,28 +2239,36 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
     }
     // packed intermediates ping-pong in workspace buffers of 16 bytes/row
     uint32_t* pk[2] = {nullptr, nullptr};
-    uint8_t* digbuf = nullptr;
     if (packed) {
       pk[0] = ws.get<uint32_t>("pkA", N * 4);
       if (D > 2) pk[1] = ws.get<uint32_t>("pkB", N * 4);
-      digbuf = ws.get<uint8_t>("digits", N + 16);
     }
+    // unpacked intermediates: AoS rows (two streams) and the digit side
+    // channel, or (QD_SOA_INTERMEDIATES=1) SoA columns whose histogram reads
+    // the key column
+    static const bool unpacked_soa = [] {
+      const char* e = getenv("QD_SOA_INTERMEDIATES");
+      return e && atoi(e) == 1;
+    }();
+    const bool side = packed || !unpacked_soa;
+    uint8_t* digbuf = side && D > 1 ? ws.get<uint8_t>("digits", N + 16) : nullptr;
     Rows in{src_c, src_v, kAoS};
     for (uint32_t q = 0; q < D; ++q) {
       const bool last = q + 1 == D;
       const bool to_dst = ((D - 1 - q) % 2) == 0;
-      const int ofmt = last ? kAoS : (packed ? kPK : kSoA);
+      const int ofmt = last ? kAoS : (packed ? kPK : (unpacked_soa ? kSoA : kAoS));
       RowsOut out{to_dst ? dst_c : tmp_c, to_dst ? dst_v : tmp_v, ofmt};
       if (ofmt == kPK) out = RowsOut{pk[q % 2], nullptr, kPK};
       const uint32_t lo = q * per, hi = std::min(bits, lo + per);
       // packed passes hand the next pass its digit bytes (1 B/row instead of
       // re-reading 16 B rows for the next histogram)
-      const uint8_t* dig_in = (packed && q > 0) ? digbuf : nullptr;
-      uint8_t* dig_out = (packed && !last) ? digbuf : nullptr;
+      const uint8_t* dig_in = (side && q > 0) ? digbuf : nullptr;
+      uint8_t* dig_out = (side && !last) ? digbuf : nullptr;
       const uint32_t nlo = (q + 1) * per, nhi = std::min(bits, nlo + per);
       run_pass(c, R, N, T, in, out, chunks, num_chunks, run_start, digs[q], key,
                q == 0 && key.check, nullptr, packed ? &pack : nullptr, lo,
-               (1u << (hi - lo)) - 1u, dig_in, dig_out, nlo, last ? 0u : (1u << (nhi - nlo)) - 1u);
+               (1u << (hi - lo)) - 1u, dig_in, dig_out, nlo, last ? 0u : (1u << (nhi - nlo)) - 1u,
+               last ? nullptr : &digs[q + 1]);
       in = Rows{out.c, out.v, out.fmt};
     }
   }
