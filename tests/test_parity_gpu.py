@@ -466,3 +466,108 @@ def test_async_errors_leave_tensor_untouched(ws):
     qd.transpose_inplace_async(empty, [1, 0], qd.SortStrategy.quesadilla(), ws)
     ws.synchronize()
     assert empty.nnz() == 0
+
+
+# --- the sharded (multi-GPU) path with the GPU backend, W ranks emulated ----
+# as host threads of one process on one GPU.  Collectives are host-side
+# (barrier + tensor copies); no kernel ever waits on another rank's kernel.
+
+class _Hub:
+    def __init__(self, world):
+        import threading
+        self.world = world
+        self.barrier = threading.Barrier(world)
+        self.slots = {}
+
+
+class _ThreadDist:
+    """The torch.distributed calls shard.py makes, over threads."""
+
+    def __init__(self, hub, rank):
+        self.hub, self.rank, self.calls = hub, rank, 0
+
+    def get_world_size(self):
+        return self.hub.world
+
+    def get_rank(self):
+        return self.rank
+
+    def _post(self, value):
+        key = self.calls
+        self.calls += 1
+        self.hub.slots[(key, self.rank)] = value
+        self.hub.barrier.wait()
+        return key
+
+    def all_reduce(self, t):
+        import torch
+        key = self._post(t.clone())
+        total = torch.stack([self.hub.slots[(key, r)] for r in range(self.hub.world)]).sum(0)
+        self.hub.barrier.wait()
+        t.copy_(total)
+
+    def all_to_all_single(self, out, inp, output_split_sizes=None, input_split_sizes=None):
+        import torch
+        w = self.hub.world
+        sizes = input_split_sizes or [inp.numel() // w] * w
+        parts = list(torch.split(inp, list(sizes)))
+        key = self._post(parts)
+        got = [self.hub.slots[(key, src)][self.rank] for src in range(w)]
+        if output_split_sizes is not None:
+            assert [g.numel() for g in got] == list(output_split_sizes)
+        if got:
+            out.copy_(torch.cat(got))
+        self.hub.barrier.wait()
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_sharded_gpu_backend_emulated_ranks(world):
+    import threading
+    import torch
+    from paper_2005_10427_b200 import shard
+    rng = np.random.default_rng(100 + world)
+    dims = [60, 700, 900]
+    cols = []
+    for d in dims:
+        p = 1.0 / np.arange(1, d + 1) ** 1.1
+        cols.append(rng.choice(d, 300_000, p=p / p.sum()))
+    c = np.unique(np.stack(cols, 1).astype(np.uint32), axis=0)  # unique, simply sorted
+    v = rng.random(len(c))
+    for target in ([1, 0, 2], [2, 1, 0], [1, 2, 0], [0, 2, 1], [2, 0, 1]):
+        if target[0] == 0:
+            b = shard.aligned_bounds(c[:, 0], world)
+        else:
+            b = [len(c) * p // world for p in range(world)] + [len(c)]
+        hub = _Hub(world)
+        outs, errs = [None] * world, []
+
+        def run(rank):
+            try:
+                be = shard.GpuBackend(0)
+                lo, hi = b[rank], b[rank + 1]
+                rows = shard.LocalRows(
+                    torch.from_numpy(np.ascontiguousarray(c[lo:hi]).view(np.int32).ravel()).cuda(),
+                    torch.from_numpy(v[lo:hi].copy()).cuda())
+                res, exchanged = shard.sharded_transpose(_ThreadDist(hub, rank), be, rows, dims,
+                                                         target)
+                outs[rank] = (res.coords.cpu().numpy().view(np.uint32), res.values.cpu().numpy(),
+                              exchanged)
+            except Exception as e:  # surfaced below
+                errs.append(e)
+                hub.barrier.abort()
+
+        th = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        assert not errs, errs
+        ec, ev, _ = ORC.transpose(dims, c.ravel(), v, target)
+        got_c = np.concatenate([o[0] for o in outs])
+        got_v = np.concatenate([o[1] for o in outs])
+        assert np.array_equal(got_c, ec), (world, target)
+        assert np.array_equal(got_v.view(np.uint64), ev.view(np.uint64))
+        assert all(o[2] == (target[0] != 0) for o in outs)
+        # the exchange balanced the sigma1 ranges (no rank got everything)
+        if target[0] != 0:
+            assert max(len(o[1]) for o in outs) < 0.8 * len(v)
