@@ -1471,6 +1471,91 @@ __global__ void k_scan_down(const uint32_t* in, unsigned long long n, const unsi
   }
 }
 
+// Single-pass exclusive scan with decoupled look-back (one launch instead of
+// reduce / parts / down).  Tiles are taken in ticket order (a monotone
+// counter, so a tile only ever waits on tiles that are already running);
+// each tile publishes its aggregate, then its inclusive prefix, in a status
+// word {tag:24 | flag:2 | value:38} whose tag is the tile's global ticket, so
+// the status array never needs clearing between calls.
+constexpr unsigned long long kLbValBits = 38, kLbValMask = (1ull << kLbValBits) - 1;
+__global__ void __launch_bounds__(kThreads) k_scan_lookback(
+    const uint32_t* in, unsigned long long n, unsigned long long* out, unsigned long long* total,
+    unsigned long long* status, uint32_t nstat, unsigned long long* ticket,
+    unsigned long long ticket_base) {
+  __shared__ unsigned long long s_tile, s_prefix;
+  __shared__ unsigned long long s_tmp[64];
+  if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1ull) - ticket_base;
+  __syncthreads();
+  const unsigned long long t = s_tile;
+  const unsigned long long tag = (ticket_base + t) & 0xFFFFFFull;
+  const unsigned long long b = t * kScanTile;
+  unsigned long long v[kScanItems];
+  unsigned long long sum = 0;
+#pragma unroll
+  for (uint32_t k = 0; k < kScanItems; ++k) {
+    const unsigned long long i = b + threadIdx.x * kScanItems + k;
+    v[k] = i < n ? __ldcs(in + i) : 0ull;
+    sum += v[k];
+  }
+  unsigned long long agg;
+  {
+    // block scan (inclusive total via the last thread)
+    const unsigned long long ex = block_excl_scan64<kThreads>(sum, s_tmp);
+    if (threadIdx.x == kThreads - 1) s_prefix = ex + sum;  // tile aggregate
+    __syncthreads();
+    agg = s_prefix;
+    __syncthreads();
+    sum = ex;  // this thread's exclusive offset inside the tile
+  }
+  volatile unsigned long long* st = status;
+  if (threadIdx.x < 32) {
+    const unsigned long long kA = 1ull << kLbValBits, kP = 2ull << kLbValBits;
+    if (t == 0) {
+      if (threadIdx.x == 0) {
+        st[0] = (tag << 40) | kP | (agg & kLbValMask);
+        s_prefix = 0;
+      }
+    } else {
+      if (threadIdx.x == 0) st[t] = (tag << 40) | kA | (agg & kLbValMask);
+      // lane l inspects tile base - l; stop at the nearest inclusive prefix
+      unsigned long long prefix = 0;
+      long long base = (long long)t - 1;
+      while (true) {
+        const long long j = base - (long long)threadIdx.x;
+        unsigned long long w = 0, f = 2;  // before tile 0: inclusive prefix 0
+        if (j >= 0) {
+          const unsigned long long want = (ticket_base + (unsigned long long)j) & 0xFFFFFFull;
+          do {
+            w = st[j];
+            f = (w >> 40) == want ? ((w >> kLbValBits) & 3ull) : 0ull;
+          } while (f == 0);
+        }
+        const unsigned full = __ballot_sync(0xFFFFFFFFu, f == 2);
+        const unsigned stop = full ? (unsigned)(__ffs(full) - 1) : 31u;
+        unsigned long long val = (j >= 0 && threadIdx.x <= stop) ? (w & kLbValMask) : 0ull;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xFFFFFFFFu, val, o);
+        prefix += val;
+        if (full) break;
+        base -= 32;
+      }
+      if (threadIdx.x == 0) {
+        st[t] = (tag << 40) | kP | ((prefix + agg) & kLbValMask);
+        s_prefix = prefix;
+      }
+    }
+  }
+  __syncthreads();
+  unsigned long long run = s_prefix + sum;
+  if (b + kScanTile >= n && threadIdx.x == kThreads - 1) *total = s_prefix + agg;
+#pragma unroll
+  for (uint32_t k = 0; k < kScanItems; ++k) {
+    const unsigned long long i = b + threadIdx.x * kScanItems + k;
+    if (i < n) out[i] = run;
+    run += v[k];
+  }
+}
+
 // ---------------------------------------------------------------------------
 // small utility kernels
 // ---------------------------------------------------------------------------
@@ -1677,6 +1762,12 @@ struct Workspace {
   cudaStream_t s_in = nullptr, s_comp = nullptr, s_out = nullptr;
   cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_comp[2] = {nullptr, nullptr},
               ev_out[2] = {nullptr, nullptr};
+  // single-pass scan (k_scan_lookback): tile status words and the ticket
+  // counter; lb_base = tickets issued so far (the device counter's value)
+  unsigned long long* lb_status = nullptr;
+  unsigned long long* lb_ticket = nullptr;
+  size_t lb_cap = 0;
+  unsigned long long lb_base = 0, lb_cleared_epoch = ~0ull;
   int slot = 0;
   struct HostSpan {
     const void* c = nullptr;
@@ -1920,15 +2011,44 @@ void scan_exclusive(Ctx& c, const uint32_t* in, uint64_t n, unsigned long long* 
     QD_CUDA(cudaMemsetAsync(d_total, 0, sizeof(unsigned long long), c.st));
     return;
   }
+  Workspace& ws = c.ws;
+  static const bool three_kernel = [] {
+    const char* e = getenv("QD_SCAN3");
+    return e && atoi(e) == 1;
+  }();
+  if (three_kernel) {
+    c.pre();
+    k_scan_reduce<<<nb, kThreads, 0, c.st>>>(in, n, part);
+    c.launched(kSegK);
+    c.pre();
+    k_scan_parts<<<1, kThreads, 0, c.st>>>(part, nb, d_total);
+    c.launched(kSegK);
+    c.pre();
+    k_scan_down<<<nb, kThreads, 0, c.st>>>(in, n, part, out);
+    c.launched(kSegK);
+    return;
+  }
+  if (!ws.lb_ticket) {
+    ws.lb_ticket = ws.get<unsigned long long>("lb_ticket", 1);
+    QD_CUDA(cudaMemsetAsync(ws.lb_ticket, 0, 8, c.st));
+    ws.lb_base = 0;
+  }
+  // status words: cleared when (re)allocated and whenever the ticket count
+  // enters a new 2^23 window, so live tags (ticket mod 2^24) never repeat
+  if (nb > ws.lb_cap || (ws.lb_base >> 23) != ws.lb_cleared_epoch ||
+      ((ws.lb_base + nb) >> 23) != (ws.lb_base >> 23)) {
+    if (nb > ws.lb_cap) {
+      ws.lb_cap = std::max<size_t>(nb, 1024);
+      ws.lb_status = ws.get<unsigned long long>("lb_status", ws.lb_cap);
+    }
+    QD_CUDA(cudaMemsetAsync(ws.lb_status, 0, ws.lb_cap * 8, c.st));
+    ws.lb_cleared_epoch = (ws.lb_base + nb) >> 23;
+  }
   c.pre();
-  k_scan_reduce<<<nb, kThreads, 0, c.st>>>(in, n, part);
+  k_scan_lookback<<<nb, kThreads, 0, c.st>>>(in, n, out, d_total, ws.lb_status,
+                                             (uint32_t)ws.lb_cap, ws.lb_ticket, ws.lb_base);
   c.launched(kSegK);
-  c.pre();
-  k_scan_parts<<<1, kThreads, 0, c.st>>>(part, nb, d_total);
-  c.launched(kSegK);
-  c.pre();
-  k_scan_down<<<nb, kThreads, 0, c.st>>>(in, n, part, out);
-  c.launched(kSegK);
+  ws.lb_base += nb;
 }
 
 // Segment discovery on `coords` with respect to `modes`: fills seg_start[0..S]
