@@ -111,6 +111,11 @@ qd_status qd_required_sort_count(const uint32_t* source, const uint32_t* target,
                                  uint32_t rank, int* out);
 qd_status qd_apply_transition(const uint32_t* current, uint32_t rank,
                               qd_plan_step step, uint32_t* next);
+/* relabel_target (planner.cpp:148-158): for a tensor sorted under `source`,
+ * the target ordering in source-relabelled modes (position of each target
+ * mode within source), written to out[rank]. */
+qd_status qd_relabel_target(const uint32_t* source, const uint32_t* target, uint32_t rank,
+                            uint32_t* out);
 qd_status qd_strategy_pass_cost(qd_strategy_kind kind, uint32_t k,
                                 const uint32_t* target, uint32_t rank,
                                 int* total, int* bucketed);
@@ -144,6 +149,24 @@ qd_status qd_transpose_inplace_async(uint32_t rank, const uint32_t* dims, uint64
                                      qd_workspace* ws);
 /* Wait for every asynchronous call on this workspace. */
 qd_status qd_workspace_synchronize(qd_workspace* ws);
+
+/* sort_rows_by (sort.cpp:203-235): stable sort of rows [row_begin, row_end)
+ * by key_modes in priority order, rows outside the range untouched.  Like the
+ * reference (a comparison sort) it never range-checks coordinates; a key
+ * mode >= rank is invalid_argument (so is a row range outside [0, nnz], which
+ * the reference leaves undefined).  Host buffers, in place; the device form
+ * writes the whole tensor out of place.  This is the canonicalisation
+ * read_tns applies (io.cpp:36-38) when key_modes is the simple ordering. */
+qd_status qd_sort_rows_by(uint32_t rank, const uint32_t* dims, uint64_t nnz,
+                          uint32_t* coords, double* values, uint64_t row_begin,
+                          uint64_t row_end, const uint32_t* key_modes, uint32_t n_keys,
+                          qd_workspace* ws);
+qd_status qd_sort_rows_by_device(uint32_t rank, const uint32_t* dims, uint64_t nnz,
+                                 const uint32_t* d_coords_in, const double* d_values_in,
+                                 uint32_t* d_coords_out, double* d_values_out,
+                                 uint64_t row_begin, uint64_t row_end,
+                                 const uint32_t* key_modes, uint32_t n_keys,
+                                 qd_workspace* ws, void* stream);
 
 /* Device-resident, out of place (in and out must not overlap). */
 qd_status qd_transpose_device(uint32_t rank, const uint32_t* dims, uint64_t nnz,

@@ -16,9 +16,13 @@
 //   partial_sort (sort.hpp:32) / parallel_partial_sort (parallel.hpp:35)
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
+#include <string_view>
+#include <thread>
 #include <utility>
 #include <vector>
 
@@ -60,6 +64,13 @@ class Ordering {
   Mode rank() const { return static_cast<Mode>(modes_.size()); }
   Mode at(std::size_t i) const { return modes_[i]; }
   const std::vector<Mode>& modes() const { return modes_; }
+  auto begin() const { return modes_.begin(); }
+  auto end() const { return modes_.end(); }
+  std::size_t position_of(Mode m) const {
+    for (std::size_t i = 0; i < modes_.size(); ++i)
+      if (modes_[i] == m) return i;
+    throw std::invalid_argument("mode not in ordering");
+  }
   bool is_simple() const {
     for (std::size_t i = 0; i < modes_.size(); ++i)
       if (modes_[i] != i) return false;
@@ -70,6 +81,94 @@ class Ordering {
  private:
   std::vector<Mode> modes_;
 };
+
+// all rank! orderings in lexicographic order (ordering.cpp all_orderings)
+inline std::vector<Ordering> all_orderings(Mode rank) {
+  if (rank < 1 || rank > 8) throw std::invalid_argument("all_orderings supports rank 1..8");
+  std::vector<Mode> m(rank);
+  for (Mode i = 0; i < rank; ++i) m[i] = i;
+  std::vector<Ordering> out;
+  do out.emplace_back(m);
+  while (std::next_permutation(m.begin(), m.end()));
+  return out;
+}
+
+// "2134" (1-based digits) or "10,2,1" (ordering.hpp parse_ordering)
+inline Ordering parse_ordering(std::string_view text) {
+  if (text.empty()) throw std::invalid_argument("empty ordering");
+  std::vector<Mode> m;
+  if (text.find(',') != std::string_view::npos) {
+    std::size_t pos = 0;
+    for (;;) {
+      const std::size_t comma = text.find(',', pos);
+      const std::string_view tok = text.substr(pos, comma == std::string_view::npos
+                                                        ? std::string_view::npos : comma - pos);
+      unsigned v = 0;
+      bool ok = !tok.empty();
+      for (char ch : tok) {
+        if (ch < '0' || ch > '9') { ok = false; break; }
+        v = v * 10 + static_cast<unsigned>(ch - '0');
+      }
+      if (!ok || v == 0) throw std::invalid_argument("bad ordering element '" + std::string(tok) + "'");
+      m.push_back(static_cast<Mode>(v - 1));
+      if (comma == std::string_view::npos) break;
+      pos = comma + 1;
+    }
+  } else {
+    for (char ch : text) {
+      if (ch < '1' || ch > '9')
+        throw std::invalid_argument("ordering digits must be 1-9; use the comma form for larger ranks");
+      m.push_back(static_cast<Mode>(ch - '1'));
+    }
+  }
+  return Ordering(std::move(m));
+}
+
+inline std::string format_ordering(const Ordering& o) {
+  std::string out;
+  for (Mode m : o) {
+    if (o.rank() <= 9) {
+      out.push_back(static_cast<char>('1' + m));
+    } else {
+      if (!out.empty()) out.push_back(',');
+      out += std::to_string(m + 1);
+    }
+  }
+  return out;
+}
+
+// f(ordering, p): the modes placed before p (planner.cpp follow_set), as a bit set
+class ModeSet {
+ public:
+  constexpr ModeSet() = default;
+  constexpr void insert(Mode m) { bits_ |= std::uint64_t{1} << m; }
+  constexpr bool contains(Mode m) const { return (bits_ >> m) & 1u; }
+  constexpr bool subset_of(ModeSet o) const { return (bits_ & ~o.bits_) == 0; }
+  constexpr bool empty() const { return bits_ == 0; }
+  int size() const { return __builtin_popcountll(bits_); }
+  constexpr std::uint64_t bits() const { return bits_; }
+  friend constexpr bool operator==(ModeSet, ModeSet) = default;
+
+ private:
+  std::uint64_t bits_ = 0;
+};
+inline ModeSet follow_set(const Ordering& ord, Mode p) {
+  ModeSet s;
+  for (Mode m : ord) {
+    if (m == p) return s;
+    s.insert(m);
+  }
+  throw std::invalid_argument("mode not in ordering");
+}
+
+// Planning from a non-simple source (planner.hpp relabel_target)
+inline Ordering relabel_target(const Ordering& source, const Ordering& target) {
+  if (source.rank() != target.rank()) throw std::invalid_argument("source and target ranks differ");
+  std::vector<Mode> out(target.rank());
+  detail::check(qd_relabel_target(source.modes().data(), target.modes().data(), target.rank(),
+                                  out.data()));
+  return Ordering(std::move(out));
+}
 
 struct PlanStep {
   Mode prefix_len = 0;
@@ -96,8 +195,38 @@ struct CooTensor {
   Mode rank() const { return static_cast<Mode>(dims.size()); }
   std::size_t nnz() const { return values.size(); }
   std::uint32_t coord(std::size_t row, Mode mode) const { return coords[row * dims.size() + mode]; }
+  // coo.cpp check_valid: shapes, positive dims, every coordinate < its dim
+  void check_valid() const {
+    const std::size_t r = dims.size();
+    if (r == 0) throw std::invalid_argument("tensor rank must be positive");
+    for (std::size_t m = 0; m < r; ++m)
+      if (dims[m] == 0)
+        throw std::invalid_argument("dimension of mode " + std::to_string(m) + " must be positive");
+    if (coords.size() != values.size() * r)
+      throw std::invalid_argument("coordinate storage does not match value count");
+    for (std::size_t j = 0; j < values.size(); ++j)
+      for (std::size_t m = 0; m < r; ++m)
+        if (coords[j * r + m] >= dims[m])
+          throw std::invalid_argument("coordinate out of range in row " + std::to_string(j) +
+                                      ", mode " + std::to_string(m));
+  }
   friend bool operator==(const CooTensor&, const CooTensor&) = default;
 };
+
+// coo.hpp is_sorted_under (host); the device check is qd_is_sorted_device
+inline bool is_sorted_under(const CooTensor& t, const Ordering& ord) {
+  if (ord.rank() != t.rank()) throw std::invalid_argument("ordering rank does not match tensor rank");
+  const std::size_t r = t.rank();
+  for (std::size_t j = 1; j < t.nnz(); ++j)
+    for (Mode m : ord) {
+      const std::uint32_t a = t.coords[(j - 1) * r + m], b = t.coords[j * r + m];
+      if (a != b) {
+        if (a > b) return false;
+        break;
+      }
+    }
+  return true;
+}
 
 namespace detail {
 inline SortPlan plan_call(const Ordering& target, Mode want) {
@@ -173,6 +302,25 @@ struct SortStrategy {
   friend bool operator==(const SortStrategy&, const SortStrategy&) = default;
 };
 
+// transpose.hpp parse_strategy: quesadilla, top<K>, radix, comparison, splatt, qsort
+inline SortStrategy parse_strategy(std::string_view name) {
+  if (name == "quesadilla") return SortStrategy::quesadilla();
+  if (name == "radix") return SortStrategy::full_radix();
+  if (name == "comparison" || name == "qsort") return SortStrategy::comparison_sort();
+  if (name == "splatt") return SortStrategy::splatt_style();
+  if (name.size() > 3 && name.substr(0, 3) == "top") {
+    unsigned k = 0;
+    bool ok = true;
+    for (char ch : name.substr(3)) {
+      if (ch < '0' || ch > '9') { ok = false; break; }
+      k = k * 10 + static_cast<unsigned>(ch - '0');
+    }
+    if (ok && k >= 1) return SortStrategy::top_k(static_cast<Mode>(k));
+  }
+  throw std::invalid_argument("unknown strategy '" + std::string(name) +
+                              "' (expected quesadilla, top<K>, radix, comparison, splatt or qsort)");
+}
+
 inline PlanCost strategy_pass_cost(const SortStrategy& s, const Ordering& target) {
   PlanCost c;
   detail::check(qd_strategy_pass_cost(s.c_kind(), s.k, target.modes().data(), target.rank(),
@@ -184,6 +332,16 @@ struct ParallelConfig {
   unsigned workers = 1;  // accepted for API parity; 0 is rejected like the reference
   static ParallelConfig serial() { return {}; }
   static ParallelConfig with_workers(unsigned p) { return {p}; }
+  // QUESADILLA_WORKERS or the host's hardware threads (parallel.cpp); the
+  // GPU ignores the count, but callers that size CPU work by it keep working
+  static unsigned default_workers() {
+    if (const char* e = std::getenv("QUESADILLA_WORKERS")) {
+      const long v = std::strtol(e, nullptr, 10);
+      if (v >= 1) return static_cast<unsigned>(v);
+    }
+    const unsigned hw = std::thread::hardware_concurrency();
+    return hw ? hw : 1u;
+  }
 };
 
 struct TransposeOptions {
@@ -280,6 +438,14 @@ inline CooTensor comparison_transpose(const CooTensor& t, const Ordering& target
 inline CooTensor topk_transpose(const CooTensor& t, const Ordering& target, Mode k,
                                 const TransposeOptions& opts = {}) {
   return transpose(t, target, SortStrategy::top_k(k), opts);
+}
+
+// sort.hpp sort_rows_by: stable sort of rows [row_begin, row_end) by key_modes
+inline void sort_rows_by(CooTensor& t, std::size_t row_begin, std::size_t row_end,
+                         const std::vector<Mode>& key_modes, Workspace& ws) {
+  detail::check(qd_sort_rows_by(t.rank(), t.dims.data(), t.nnz(), t.coords.data(), t.values.data(),
+                                row_begin, row_end, key_modes.data(),
+                                static_cast<std::uint32_t>(key_modes.size()), ws.get()));
 }
 
 inline void partial_sort(CooTensor& t, const std::vector<Mode>& prefix, Mode mode, Workspace& ws) {

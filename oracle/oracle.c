@@ -208,6 +208,27 @@ static void sort_rows_by(uint32_t r, uint32_t* crd, double* val, uint64_t b,
   free(tv);
 }
 
+/* sort_rows_by as a public entry (sort.cpp:203-211 validates the key modes,
+ * then stable-sorts rows [b, e)). */
+int qo_sort_rows_by(uint32_t r, uint64_t nnz, uint32_t* crd, double* val, uint64_t b,
+                    uint64_t e, const uint32_t* keys, uint32_t nk) {
+  for (uint32_t i = 0; i < nk; ++i)
+    if (keys[i] >= r) return 1;
+  if (b > e || e > nnz) return 1;
+  sort_rows_by(r, crd, val, b, e, keys, nk);
+  return 0;
+}
+
+/* relabel_target, planner.cpp:148-158: position of each target mode within
+ * source. */
+int qo_relabel_target(const uint32_t* source, const uint32_t* target, uint32_t r, uint32_t* out) {
+  if (!valid_ordering(source, r) || !valid_ordering(target, r)) return 1;
+  for (uint32_t i = 0; i < r; ++i)
+    for (uint32_t j = 0; j < r; ++j)
+      if (source[j] == target[i]) out[i] = j;
+  return 0;
+}
+
 /* ---- transpose driver (transpose.cpp:59-112) ----------------------------- */
 
 int qo_is_sorted(uint32_t r, uint64_t nnz, const uint32_t* crd,

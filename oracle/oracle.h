@@ -46,6 +46,15 @@ uint64_t qo_bucket_starts(uint32_t rank, uint64_t nnz, const uint32_t* coords,
                           const uint32_t* modes, uint32_t nmodes,
                           uint64_t* starts_out);
 
+/* sort_rows_by, sort.cpp:203-235: stable comparison sort of rows [b, e) by
+ * `keys` in priority order (no range check). */
+int qo_sort_rows_by(uint32_t rank, uint64_t nnz, uint32_t* coords, double* values,
+                    uint64_t b, uint64_t e, const uint32_t* keys, uint32_t nkeys);
+
+/* relabel_target, planner.cpp:148-158. */
+int qo_relabel_target(const uint32_t* source, const uint32_t* target, uint32_t rank,
+                      uint32_t* out);
+
 /* is_sorted_under, coo.cpp:32-49. */
 int qo_is_sorted(uint32_t rank, uint64_t nnz, const uint32_t* coords,
                  const uint32_t* order);

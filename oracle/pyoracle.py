@@ -53,6 +53,25 @@ class Oracle:
                                        C.c_uint32, _u64p]
         L.qo_bucket_starts.restype = C.c_uint64
         L.qo_is_sorted.argtypes = [C.c_uint32, C.c_uint64, _u32p, _u32p]
+        L.qo_sort_rows_by.argtypes = [C.c_uint32, C.c_uint64, _u32p, _f64p, C.c_uint64,
+                                      C.c_uint64, _u32p, C.c_uint32]
+        L.qo_relabel_target.argtypes = [_u32p, _u32p, C.c_uint32, _u32p]
+
+    def sort_rows_by(self, rank, coords, values, row_begin, row_end, keys):
+        c = _u32(coords).copy()
+        v = np.ascontiguousarray(values, np.float64).copy()
+        k = _u32(keys) if len(keys) else np.zeros(1, np.uint32)
+        s = self.lib.qo_sort_rows_by(rank, len(v), c, v, row_begin, row_end, k, len(keys))
+        if s:
+            raise OracleError(s)
+        return c, v
+
+    def relabel_target(self, source, target):
+        out = np.zeros(len(target), np.uint32)
+        s = self.lib.qo_relabel_target(_u32(source), _u32(target), len(target), out)
+        if s:
+            raise OracleError(s)
+        return [int(x) for x in out]
 
     def plan(self, target, want: int = 0):
         t = _u32(target)
@@ -138,6 +157,23 @@ class Reference:
     def _check(self, s):
         if s:
             raise OracleError(s, self.lib.qref_last_error().decode())
+
+    def sort_rows_by(self, dims, coords, values, row_begin, row_end, keys):
+        dims = _u32(dims)
+        c = _u32(coords).copy()
+        v = np.ascontiguousarray(values, np.float64).copy()
+        k = _u32(keys) if len(keys) else np.zeros(1, np.uint32)
+        self.lib.qref_sort_rows_by.argtypes = [C.c_uint32, _u32p, C.c_uint64, _u32p, _f64p,
+                                               C.c_uint64, C.c_uint64, _u32p, C.c_uint32]
+        self._check(self.lib.qref_sort_rows_by(len(dims), dims, len(v), c, v, row_begin, row_end,
+                                               k, len(keys)))
+        return c, v
+
+    def relabel_target(self, source, target):
+        out = np.zeros(len(target), np.uint32)
+        self.lib.qref_relabel_target.argtypes = [_u32p, _u32p, C.c_uint32, _u32p]
+        self._check(self.lib.qref_relabel_target(_u32(source), _u32(target), len(target), out))
+        return [int(x) for x in out]
 
     def transpose(self, dims, coords, values, target, strategy="quesadilla", k=0,
                   workers=1, verify_input=False):

@@ -161,6 +161,27 @@ int qref_partial_sort(uint32_t rank, const uint32_t* dims, uint64_t nnz,
   });
 }
 
+int qref_sort_rows_by(uint32_t rank, const uint32_t* dims, uint64_t nnz, uint32_t* coords,
+                      double* values, uint64_t row_begin, uint64_t row_end,
+                      const uint32_t* keys, uint32_t nkeys) {
+  return guard([&] {
+    CooTensor t = wrap(rank, dims, nnz, coords, values);
+    std::vector<Mode> k(keys, keys + nkeys);
+    sort_rows_by(t, row_begin, row_end, k);
+    unwrap(t, coords, values);
+  });
+}
+
+int qref_relabel_target(const uint32_t* source, const uint32_t* target, uint32_t rank,
+                        uint32_t* out) {
+  return guard([&] {
+    Ordering s(std::vector<Mode>(source, source + rank));
+    Ordering t(std::vector<Mode>(target, target + rank));
+    Ordering o = relabel_target(s, t);
+    for (uint32_t i = 0; i < rank; ++i) out[i] = o.at(i);
+  });
+}
+
 // want == 0 selects quesadilla_plan, else prefix_plan(target, want).
 int qref_plan(const uint32_t* target, uint32_t rank, uint32_t want,
               uint32_t* steps_out, uint32_t max_steps, uint32_t* nsteps_out) {

@@ -122,6 +122,13 @@ def lib():
                                           C.POINTER(OptionsC), C.c_void_p, C.c_void_p]
         L.qd_partial_sort.argtypes = [C.c_uint32, _u32p, C.c_uint64, _u32p, _f64p, _u32p,
                                       C.c_uint32, C.c_uint32, C.c_void_p]
+        L.qd_sort_rows_by.argtypes = [C.c_uint32, _u32p, C.c_uint64, _u32p, _f64p, C.c_uint64,
+                                      C.c_uint64, _u32p, C.c_uint32, C.c_void_p]
+        L.qd_sort_rows_by_device.argtypes = [C.c_uint32, _u32p, C.c_uint64, C.c_void_p,
+                                             C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64,
+                                             C.c_uint64, _u32p, C.c_uint32, C.c_void_p,
+                                             C.c_void_p]
+        L.qd_relabel_target.argtypes = [_u32p, _u32p, C.c_uint32, _u32p]
         L.qd_partial_sort_device.argtypes = [C.c_uint32, _u32p, C.c_uint64, C.c_void_p, C.c_void_p,
                                              C.c_void_p, C.c_void_p, _u32p, C.c_uint32, C.c_uint32,
                                              C.c_void_p, C.c_void_p]
@@ -610,6 +617,35 @@ def partial_sort(tensor: CooTensor, prefix: Sequence[int], mode: int,
                                  _ptr_u32(p), len(prefix), int(mode), w.handle))
 
 
+def sort_rows_by(tensor: CooTensor, row_begin: int, row_end: int, key_modes: Sequence[int],
+                 ws: Optional[Workspace] = None) -> None:
+    """sort.hpp:38-39 — stable sort of rows [row_begin, row_end) by key_modes
+    (priority order), in place; no range check, like the reference."""
+    w = _ws(ws)
+    k = _arr_u32(list(key_modes) or [0])
+    _check(lib().qd_sort_rows_by(tensor.rank(), _ptr_u32(tensor.dims), tensor.nnz(),
+                                 _ptr_u32(tensor.coords), tensor.values.ctypes.data_as(_f64p),
+                                 int(row_begin), int(row_end), _ptr_u32(k), len(key_modes),
+                                 w.handle))
+
+
+def canonicalize(tensor: CooTensor, ws: Optional[Workspace] = None) -> None:
+    """read_tns's canonicalisation (io.cpp:36-38): stable sort into the simple
+    ordering from any row order."""
+    sort_rows_by(tensor, 0, tensor.nnz(), list(range(tensor.rank())), ws)
+
+
+def relabel_target(source, target) -> Ordering:
+    """planner.hpp:51-55."""
+    s, t = _ord(source), _ord(target)
+    if s.rank() != t.rank():
+        raise InvalidArgument("source and target ranks differ")
+    out = np.zeros(t.rank(), np.uint32)
+    _check(lib().qd_relabel_target(_ptr_u32(_arr_u32(s.modes())), _ptr_u32(_arr_u32(t.modes())),
+                                   t.rank(), _ptr_u32(out)))
+    return Ordering([int(x) for x in out])
+
+
 def parallel_partial_sort(tensor, prefix, mode, ws=None, cfg: ParallelConfig = ParallelConfig()):
     """parallel.hpp:35-37 — identical output; the GPU is the parallelism."""
     if cfg.workers == 0:
@@ -668,6 +704,17 @@ def partial_sort_device(rank, dims, nnz, coords_in, values_in, coords_out, value
                                         C.c_void_p(values_in), C.c_void_p(coords_out),
                                         C.c_void_p(values_out), _ptr_u32(p), len(prefix), mode,
                                         w.handle, C.c_void_p(stream)))
+
+
+def sort_rows_by_device(rank, dims, nnz, coords_in, values_in, coords_out, values_out,
+                        row_begin, row_end, key_modes, ws=None, stream=0):
+    w = _ws(ws)
+    d = _arr_u32(dims)
+    k = _arr_u32(list(key_modes) or [0])
+    _check(lib().qd_sort_rows_by_device(rank, _ptr_u32(d), nnz, C.c_void_p(coords_in),
+                                        C.c_void_p(values_in), C.c_void_p(coords_out),
+                                        C.c_void_p(values_out), int(row_begin), int(row_end),
+                                        _ptr_u32(k), len(key_modes), w.handle, C.c_void_p(stream)))
 
 
 def is_sorted_device(rank, nnz, coords, order, ws=None, stream=0) -> bool:

@@ -85,6 +85,24 @@ std::vector<Group> partial_sort_group(uint32_t rank, const uint32_t* prefix, uin
   return {g};
 }
 
+// sort_rows_by's group: no prefix, the key modes (later repeats of a mode
+// cannot change the order and are dropped), no range check (sort.cpp:203-211)
+std::vector<Group> sort_rows_group(uint32_t rank, const uint32_t* keys, uint32_t nk) {
+  if (nk && !keys) invalid("key_modes is null");
+  Group g;
+  uint64_t seen = 0;
+  for (uint32_t i = 0; i < nk; ++i) {
+    if (keys[i] >= rank) invalid("key mode out of range");
+    if (seen & (uint64_t{1} << keys[i])) continue;
+    seen |= uint64_t{1} << keys[i];
+    g.keys.push_back(keys[i]);
+  }
+  g.check_range = false;
+  g.n_steps = 0;
+  if (g.keys.empty()) return {};
+  return {g};
+}
+
 }  // namespace
 
 extern "C" {
@@ -248,6 +266,60 @@ qd_status qd_partial_sort(uint32_t rank, const uint32_t* dims, uint64_t nnz, uin
     TensorView t{rank, dims, nnz};
     run_groups_host(*reinterpret_cast<Workspace*>(ws), t, coords, values, groups, false, nullptr,
                     nullptr, 0);
+  });
+}
+
+qd_status qd_sort_rows_by(uint32_t rank, const uint32_t* dims, uint64_t nnz, uint32_t* coords,
+                          double* values, uint64_t row_begin, uint64_t row_end,
+                          const uint32_t* key_modes, uint32_t n_keys, qd_workspace* ws) {
+  return guard([&] {
+    if (!ws) invalid("workspace is null");
+    check_tensor(rank, dims, nnz, coords, values);
+    auto groups = sort_rows_group(rank, key_modes, n_keys);
+    if (row_begin > row_end || row_end > nnz) invalid("row range outside [0, nnz]");
+    const uint64_t m = row_end - row_begin;
+    if (m < 2 || groups.empty()) return;
+    TensorView t{rank, dims, m};
+    run_groups_host(*reinterpret_cast<Workspace*>(ws), t, coords + row_begin * rank,
+                    values + row_begin, groups, false, nullptr, nullptr, 0);
+  });
+}
+
+qd_status qd_sort_rows_by_device(uint32_t rank, const uint32_t* dims, uint64_t nnz,
+                                 const uint32_t* d_coords_in, const double* d_values_in,
+                                 uint32_t* d_coords_out, double* d_values_out,
+                                 uint64_t row_begin, uint64_t row_end,
+                                 const uint32_t* key_modes, uint32_t n_keys, qd_workspace* ws,
+                                 void* stream) {
+  return guard([&] {
+    if (!ws) invalid("workspace is null");
+    check_tensor(rank, dims, nnz, d_coords_in, d_values_in);
+    if (nnz && (!d_coords_out || !d_values_out)) invalid("output buffer is null");
+    if (nnz && (d_coords_out == d_coords_in || d_values_out == d_values_in))
+      invalid("device sort is out of place: input and output must differ");
+    auto groups = sort_rows_group(rank, key_modes, n_keys);
+    if (row_begin > row_end || row_end > nnz) invalid("row range outside [0, nnz]");
+    const uint64_t m = row_end - row_begin;
+    copy_rows_device(*reinterpret_cast<Workspace*>(ws), rank, nnz, d_coords_in, d_values_in,
+                     d_coords_out, d_values_out, row_begin, row_end,
+                     m < 2 || groups.empty(), stream);
+    if (m < 2 || groups.empty()) return;
+    TensorView t{rank, dims, m};
+    run_groups(*reinterpret_cast<Workspace*>(ws), t, d_coords_in + row_begin * rank,
+               d_values_in + row_begin, d_coords_out + row_begin * rank, d_values_out + row_begin,
+               groups, false, nullptr, nullptr, 0, stream);
+  });
+}
+
+qd_status qd_relabel_target(const uint32_t* source, const uint32_t* target, uint32_t rank,
+                            uint32_t* out) {
+  return guard([&] {
+    check_ordering(source, rank);
+    check_ordering(target, rank);
+    if (!out) invalid("output is null");
+    for (uint32_t i = 0; i < rank; ++i)
+      for (uint32_t j = 0; j < rank; ++j)
+        if (source[j] == target[i]) out[i] = j;
   });
 }
 

@@ -2737,6 +2737,25 @@ void run_groups_host_async(Workspace& ws, const TensorView& t, uint32_t* coords,
   ws.last_host = cur;
 }
 
+void copy_rows_device(Workspace& ws, uint32_t rank, uint64_t nnz, const uint32_t* c_in,
+                      const double* v_in, uint32_t* c_out, double* v_out, uint64_t row_begin,
+                      uint64_t row_end, bool whole, void* stream) {
+  QD_CUDA(cudaSetDevice(ws.device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  auto cp = [&](uint64_t a, uint64_t b) {
+    if (b <= a) return;
+    QD_CUDA(cudaMemcpyAsync(c_out + a * rank, c_in + a * rank, (b - a) * rank * 4,
+                            cudaMemcpyDeviceToDevice, st));
+    QD_CUDA(cudaMemcpyAsync(v_out + a, v_in + a, (b - a) * 8, cudaMemcpyDeviceToDevice, st));
+  };
+  if (whole) {
+    cp(0, nnz);
+  } else {
+    cp(0, row_begin);
+    cp(row_end, nnz);
+  }
+}
+
 void workspace_synchronize(Workspace* ws) {
   QD_CUDA(cudaSetDevice(ws->device));
   for (cudaStream_t st : {ws->s_in, ws->s_comp, ws->s_out})

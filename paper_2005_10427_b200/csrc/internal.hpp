@@ -85,6 +85,11 @@ void run_groups(Workspace& ws, const TensorView& t, const uint32_t* d_c_in,
                 uint32_t boundary_mode, void* stream);
 
 // Host-buffer convenience: H2D, run_groups, D2H (only on success).
+// Device copies of the rows outside [row_begin, row_end) (all rows when
+// `whole`) from in to out, on `stream`.
+void copy_rows_device(Workspace& ws, uint32_t rank, uint64_t nnz, const uint32_t* c_in,
+                      const double* v_in, uint32_t* c_out, double* v_out, uint64_t row_begin,
+                      uint64_t row_end, bool whole, void* stream);
 void run_groups_host_async(Workspace& ws, const TensorView& t, uint32_t* coords, double* values,
                            const std::vector<Group>& groups, bool verify_input);
 void workspace_synchronize(Workspace* ws);

@@ -13,6 +13,8 @@
 #include <vector>
 
 #include "quesadilla/io.hpp"
+#include "quesadilla/planner.hpp"
+#include "quesadilla/sort.hpp"
 #include "quesadilla/transpose.hpp"
 #include "quesadilla_b200.hpp"
 
@@ -127,6 +129,58 @@ int main() {
     expect(exc_class([&] { Q::topk_transpose(q, Q::Ordering({1, 0}), 0); }) ==
                exc_class([&] { B::topk_transpose(b, B::Ordering({1, 0}), 0); }),
            "exc top-k");
+  }
+  // sort_rows_by over row ranges (sort.cpp:203-235), any key list
+  for (int i = 0; i < 20; ++i) {
+    Q::GenSpec spec;
+    const Q::Mode r = 1 + rng() % 4;
+    for (Q::Mode m = 0; m < r; ++m) spec.dims.push_back(1 + rng() % 500);
+    spec.nnz = rng() % 30000;
+    spec.seed = rng();
+    Q::CooTensor q = Q::generate(spec);
+    B::CooTensor b = to_b(q);
+    std::vector<Q::Mode> keys(rng() % (2 * r + 1));
+    for (auto& k : keys) k = rng() % r;
+    const std::size_t lo = q.nnz() ? rng() % (q.nnz() + 1) : 0;
+    const std::size_t hi = lo + (q.nnz() - lo ? rng() % (q.nnz() - lo + 1) : 0);
+    Q::sort_rows_by(q, lo, hi, keys);
+    B::sort_rows_by(b, lo, hi, keys, ws);
+    expect(same(q, b), "sort_rows_by r=" + std::to_string(r));
+  }
+  // host utilities of the public headers
+  for (Q::Mode r = 1; r <= 4; ++r)
+    for (const Q::Ordering& s : Q::all_orderings(r))
+      for (const Q::Ordering& t : Q::all_orderings(r)) {
+        expect(Q::relabel_target(s, t).modes() ==
+                   B::relabel_target(B::Ordering(s.modes()), B::Ordering(t.modes())).modes(),
+               "relabel_target");
+        expect(Q::format_ordering(t) == B::format_ordering(B::Ordering(t.modes())), "format");
+        expect(Q::parse_ordering(Q::format_ordering(t)).modes() ==
+                   B::parse_ordering(Q::format_ordering(t)).modes(),
+               "parse");
+      }
+  for (const char* name : {"quesadilla", "top2", "radix", "comparison", "splatt", "qsort"})
+    expect(Q::parse_strategy(name).name() == B::parse_strategy(name).name(), "parse_strategy");
+  expect(exc_class([&] { Q::parse_strategy("top0"); }) ==
+             exc_class([&] { B::parse_strategy("top0"); }),
+         "parse_strategy error");
+  {
+    Q::GenSpec spec;
+    spec.dims = {30, 40, 50};
+    spec.nnz = 5000;
+    spec.seed = 7;
+    const Q::CooTensor q = Q::generate(spec);
+    const B::CooTensor b = to_b(q);
+    for (const Q::Ordering& o : Q::all_orderings(3))
+      expect(Q::is_sorted_under(q, o) == B::is_sorted_under(b, B::Ordering(o.modes())),
+             "is_sorted_under");
+    Q::CooTensor qb = q;
+    B::CooTensor bb = b;
+    qb.coords[7] = 99;
+    bb.coords[7] = 99;
+    expect(exc_class([&] { qb.check_valid(); }) == exc_class([&] { bb.check_valid(); }) &&
+               exc_class([&] { bb.check_valid(); }) == 1,
+           "check_valid");
   }
   std::printf("%s %d checks, %d failures\n", failures ? "FAIL" : "PASS", checks, failures);
   return failures ? 1 : 0;

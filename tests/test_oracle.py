@@ -108,3 +108,28 @@ def test_oracle_equals_reference_random():
             assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
             assert np.array_equal(ORC.bucket_starts(r, a[0], pre[:1] or [mode]),
                                   ref.bucket_starts(dims, b[0], b[1], pre[:1] or [mode]))
+
+
+def test_sort_rows_by_and_relabel_match_reference():
+    """The restatement's sort_rows_by / relabel_target equal the reference's."""
+    import itertools
+    from pyoracle import Reference, reference_available
+    if not reference_available():
+        pytest.skip("oracle/_ref not built")
+    ref, orc = Reference(), Oracle()
+    rng = np.random.default_rng(21)
+    for trial in range(20):
+        r = int(rng.integers(1, 5))
+        dims = [int(x) for x in rng.integers(1, 9, r)]
+        n = int(rng.integers(0, 300))
+        c = np.stack([rng.integers(0, d, n) for d in dims], 1).astype(np.uint32).ravel()
+        v = rng.random(n)
+        keys = [int(x) for x in rng.integers(0, r, int(rng.integers(0, 2 * r + 1)))]
+        b = int(rng.integers(0, n + 1)); e = int(rng.integers(b, n + 1))
+        rc, rv = ref.sort_rows_by(dims, c, v, b, e, keys)
+        oc, ov = orc.sort_rows_by(r, c, v, b, e, keys)
+        assert np.array_equal(rc, oc) and np.array_equal(rv.view(np.uint64), ov.view(np.uint64))
+    for r in (1, 2, 3, 4):
+        for s in itertools.permutations(range(r)):
+            for t in itertools.permutations(range(r)):
+                assert ref.relabel_target(list(s), list(t)) == orc.relabel_target(list(s), list(t))

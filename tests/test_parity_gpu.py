@@ -571,3 +571,67 @@ def test_sharded_gpu_backend_emulated_ranks(world):
         # the exchange balanced the sigma1 ranges (no rank got everything)
         if target[0] != 0:
             assert max(len(o[1]) for o in outs) < 0.8 * len(v)
+
+
+# --- sort_rows_by (sort.cpp:203-235), canonicalisation, relabel_target ------
+
+def test_sort_rows_by_matches_oracle(ws):
+    rng = np.random.default_rng(31)
+    for trial in range(25):
+        r = int(rng.integers(1, 6))
+        dims = [int(x) for x in rng.integers(1, 3000, r)]
+        n = int(rng.choice([0, 1, 2, 50, 5000, 120_000]))
+        t = rand_tensor(rng, dims, n, sort=bool(trial % 2))
+        keys = [int(x) for x in rng.integers(0, r, int(rng.integers(0, 2 * r + 1)))]
+        b = int(rng.integers(0, n + 1)) if trial % 3 else 0
+        e = int(rng.integers(b, n + 1)) if trial % 3 else n
+        got = t.copy()
+        qd.sort_rows_by(got, b, e, keys, ws)
+        c, v = ORC.sort_rows_by(r, t.coords, t.values, b, e, keys)
+        assert same(got, c, v), (dims, n, keys, b, e)
+
+
+def test_sort_rows_by_device_and_errors(ws):
+    import torch
+    rng = np.random.default_rng(32)
+    t = rand_tensor(rng, [50, 60, 70], 200_000, sort=False)
+    ci = torch.from_numpy(t.coords.view(np.int32)).cuda()
+    vi = torch.from_numpy(t.values).cuda()
+    co, vo = torch.empty_like(ci), torch.empty_like(vi)
+    for keys, b, e in (([2, 0], 1000, 150_000), ([0, 1, 2], 0, 200_000), ([], 5, 10)):
+        qd.sort_rows_by_device(3, t.dims, t.nnz(), ci.data_ptr(), vi.data_ptr(), co.data_ptr(),
+                               vo.data_ptr(), b, e, keys, ws)
+        c, v = ORC.sort_rows_by(3, t.coords, t.values, b, e, keys)
+        assert np.array_equal(co.cpu().numpy().view(np.uint32), c)
+        assert np.array_equal(vo.cpu().numpy().view(np.uint64), v.view(np.uint64))
+    # coordinates beyond dims are sorted, not rejected (a comparison sort)
+    u = qd.CooTensor([4, 4], [9, 1, 2, 3, 7, 0], [1.0, 2.0, 3.0])
+    qd.sort_rows_by(u, 0, 3, [0], ws)
+    assert u.coords.tolist() == [2, 3, 7, 0, 9, 1]
+    with pytest.raises(qd.InvalidArgument):
+        qd.sort_rows_by(u, 0, 3, [2], ws)
+    with pytest.raises(qd.InvalidArgument):
+        qd.sort_rows_by(u, 2, 4, [0], ws)
+
+
+def test_canonicalize_then_transpose(ws):
+    """read_tns's canonicalisation: any row order -> simple order, then the
+    Quesadilla transpose (the reference's read_tns + transpose path)."""
+    rng = np.random.default_rng(33)
+    t = rand_tensor(rng, [200, 300, 400], 300_000, sort=True, distinct=True)
+    perm = rng.permutation(t.nnz())
+    shuffled = qd.CooTensor(t.dims, t.coords.reshape(-1, 3)[perm].ravel(), t.values[perm])
+    qd.canonicalize(shuffled, ws)
+    assert shuffled == t
+    out = qd.transpose(shuffled, [2, 0, 1], ws=ws)
+    c, v, _ = ORC.transpose(t.dims, t.coords, t.values, [2, 0, 1])
+    assert same(out, c, v)
+
+
+def test_relabel_target_matches_oracle():
+    for r in (1, 2, 3, 4):
+        for s in itertools.permutations(range(r)):
+            for t in itertools.permutations(range(r)):
+                assert qd.relabel_target(list(s), list(t)).modes() == ORC.relabel_target(list(s), list(t))
+    with pytest.raises(qd.InvalidArgument):
+        qd.relabel_target([0, 1], [0, 1, 2])
