@@ -123,6 +123,9 @@ class GpuBackend:
     def to_numpy_i64(self, h):
         return h.cpu().numpy()
 
+    def synchronize(self):
+        self.torch.cuda.synchronize(self.device)
+
     def from_numpy_i64(self, a):
         return self.torch.from_numpy(np.asarray(a, np.int64)).to(self.device)
 
@@ -142,23 +145,41 @@ def exchange(dist, be, rows: LocalRows, counts: Sequence[int], rank_modes: int) 
     return out
 
 
-def sharded_transpose(dist, be, rows: LocalRows, dims: Sequence[int], target: Sequence[int]):
+def sharded_transpose(dist, be, rows: LocalRows, dims: Sequence[int], target: Sequence[int],
+                      stats: dict = None):
     """Transpose the global tensor whose rank-ordered slices are `rows`;
     returns this rank's slice of the global output (and whether an exchange
     was needed).  For target[0] == 0 the input slices must be mode-0 aligned
-    (see aligned_bounds)."""
+    (see aligned_bounds).  `stats` (optional) receives the exchange's bytes
+    sent to other ranks and its host-synchronised duration (SURVEY §8e's
+    NVLink reporting)."""
     r = len(dims)
     target = [int(x) for x in target]
     world = dist.get_world_size()
     if world == 1 or target[0] == 0:
-        return be.transpose(rows, dims, target), False
+        out = be.transpose(rows, dims, target)
+        if stats is not None:
+            stats.update(sent_bytes=0, exchange_s=0.0, rows_out=out.nnz())
+        return out, False
     s1 = target[0]
     h = be.mode_hist(rows, r, s1, dims[s1])
     dist.all_reduce(h)
     lookup = splitters(be.to_numpy_i64(h), world)
     parts, counts = be.partition(rows, r, s1, lookup, world)
+    if stats is not None:
+        import time
+        be.synchronize()
+        t0 = time.perf_counter()
     recv = exchange(dist, be, parts, counts, r)
-    return be.transpose(recv, dims, target), True
+    if stats is not None:
+        be.synchronize()
+        me = dist.get_rank()
+        stats.update(sent_bytes=sum(int(c) for p, c in enumerate(counts) if p != me) * (4 * r + 8),
+                     exchange_s=time.perf_counter() - t0)
+    out = be.transpose(recv, dims, target)
+    if stats is not None:
+        stats["rows_out"] = out.nnz()
+    return out, True
 
 
 def bench_sharded(args, cfg, dist, rank, world, local):
@@ -218,6 +239,23 @@ def bench_sharded(args, cfg, dist, rank, world, local):
     total = torch.tensor([n_local], device="cuda", dtype=torch.int64)
     dist.all_reduce(total)
 
+    # SURVEY §8e reporting: one instrumented step (exchange bytes and time,
+    # output balance), separate from the timed regions
+    ex_bytes = ex_s = 0.0
+    imbalance = []
+    for t in cfg.targets:
+        st = {}
+        sharded_transpose(dist, be, rows, gdims, t, stats=st)
+        vals = torch.tensor([st["sent_bytes"], st["exchange_s"], st["rows_out"], st["rows_out"]],
+                            device="cuda", dtype=torch.float64)
+        mx = vals.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = vals.clone()
+        dist.all_reduce(sm)
+        ex_bytes += sm[0].item()
+        ex_s += mx[1].item()
+        imbalance.append(round(mx[2].item() / max(1.0, sm[3].item() / world), 4))
+
     # end to end: every rank copies its slice in from pinned host memory,
     # runs the sharded transpose and copies its output slice back
     hc = torch.empty(ci.shape, dtype=ci.dtype).pin_memory()
@@ -232,25 +270,40 @@ def bench_sharded(args, cfg, dist, rank, world, local):
     torch.cuda.synchronize()
     dist.barrier()
     k_e2e = max(1, min(args.steps, 3))
-    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # input copies on s_in into two device slots, output copies on s_out: the
+    # output copy of target i overlaps the input copy of target i+1
+    s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+    slots = [(dc, dv), (torch.empty_like(ci), torch.empty_like(vi))]
     h2d = d2h = 0
-    a0.record()
+    keep = []
+    torch.cuda.synchronize()
+    dist.barrier()
+    t0 = time.perf_counter()
+    k = 0
     for _ in range(k_e2e):
         for t in cfg.targets:
-            dc.copy_(hc, non_blocking=True)
-            dv.copy_(hv, non_blocking=True)
-            out, _ = sharded_transpose(dist, be, LocalRows(dc, dv), gdims, t)
+            sc, sv = slots[k % 2]
+            k += 1
+            with torch.cuda.stream(s_in):
+                sc.copy_(hc, non_blocking=True)
+                sv.copy_(hv, non_blocking=True)
+            torch.cuda.current_stream().wait_stream(s_in)
+            out, _ = sharded_transpose(dist, be, LocalRows(sc, sv), gdims, t)
             n_out = out.values.numel()
             if n_out > ov.numel():
                 oc = torch.empty(n_out * r, dtype=ci.dtype).pin_memory()
                 ov = torch.empty(n_out, dtype=vi.dtype).pin_memory()
-            oc[:n_out * r].copy_(out.coords, non_blocking=True)
-            ov[:n_out].copy_(out.values, non_blocking=True)
-            h2d += dc.numel() * 4 + dv.numel() * 8
+            s_out.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s_out):
+                oc[:n_out * r].copy_(out.coords, non_blocking=True)
+                ov[:n_out].copy_(out.values, non_blocking=True)
+            keep.append(out)
+            h2d += sc.numel() * 4 + sv.numel() * 8
             d2h += n_out * (4 * r + 8)
-    a1.record()
     torch.cuda.synchronize()
-    e2e_ms = torch.tensor([a0.elapsed_time(a1)], device="cuda")
+    wall = time.perf_counter() - t0
+    del keep
+    e2e_ms = torch.tensor([wall * 1e3], device="cuda")
     dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
     if rank == 0:
         units = int(total.item()) * len(cfg.targets) * args.steps
@@ -279,8 +332,19 @@ def bench_sharded(args, cfg, dist, rank, world, local):
                          "rank": 0},
             "e2e": {"value": round(e2e_units / (e2e_ms.item() / 1e3) / 1e6, 3), "unit": "Mnnz/s",
                     "h2d_bytes_per_step": h2d // k_e2e, "d2h_bytes_per_step": d2h // k_e2e,
-                    "note": "rank 0's bytes; every rank moves its own slice"},
+                    "note": "rank 0's bytes; every rank moves its own slice; host wall clock, "
+                            "max over ranks; output copy of target i overlaps input copy of i+1"},
             "gpu_launches": launches,
             "clocks": clk.summary(),
+            "exchange": {"note": "one instrumented step: all_to_all bytes to other ranks summed "
+                                 "over ranks and targets; time = max over ranks per target, host-"
+                                 "synchronised around the exchange",
+                         "bytes_sent_total": int(ex_bytes), "exchange_ms": round(ex_s * 1e3, 3),
+                         "nvlink_GBs_per_rank": (round(ex_bytes / world / ex_s / 1e9, 1)
+                                                 if ex_s > 0 else None),
+                         "nvlink_frac": (round(ex_bytes / world / ex_s / 1e9 / 900.0, 4)
+                                         if ex_s > 0 else None),
+                         "imbalance_max_over_mean": dict(zip(
+                             ["".join(str(x) for x in t) for t in cfg.targets], imbalance))},
         }))
     dist.destroy_process_group()

@@ -49,6 +49,9 @@ class CpuBackend:
     def to_numpy_i64(self, h):
         return h.numpy()
 
+    def synchronize(self):
+        pass
+
     def from_numpy_i64(self, a):
         return torch.from_numpy(np.asarray(a, np.int64))
 
@@ -82,7 +85,9 @@ def worker(rank, world, port, cases, results):
         lo, hi = b[rank], b[rank + 1]
         rows = shard.LocalRows(torch.from_numpy(np.ascontiguousarray(c[lo:hi]).view(np.int32).ravel()),
                                torch.from_numpy(v[lo:hi].copy()))
-        res, exchanged = shard.sharded_transpose(dist, be, rows, dims, target)
+        st = {}
+        res, exchanged = shard.sharded_transpose(dist, be, rows, dims, target, stats=st)
+        assert st["rows_out"] == res.nnz() and (st["sent_bytes"] > 0) == exchanged or not exchanged
         out.append((res.coords.numpy().copy(), res.values.numpy().copy(), exchanged))
     results[rank] = out
     dist.destroy_process_group()
