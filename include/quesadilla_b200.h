@@ -133,21 +133,26 @@ qd_status qd_transpose_inplace(uint32_t rank, const uint32_t* dims, uint64_t nnz
                                qd_workspace* ws);
 
 /* Asynchronous form of qd_transpose_inplace for pipelines of host-buffer
- * calls (e.g. the CLI bench's loop over targets, main.cpp:198-213): the
- * host->device copy, the device transpose and the device->host copy of
- * consecutive calls run on the workspace's own streams, so call i's output
- * copy overlaps call i+1's input copy (PCIe is full duplex).  The call
- * returns once its rows are sorted on the device (so out_of_range /
- * invalid_argument are reported by the call itself, host buffers untouched);
- * (coords, values) hold the result after qd_workspace_synchronize.  The
- * buffers must stay valid (and should be pinned) until then; bucket
- * boundaries are not reported by this form. */
+ * calls (e.g. the CLI bench's loop over targets, main.cpp:198-213).  The
+ * call validates its arguments (invalid_argument is returned at once),
+ * enqueues the host->device copy and returns; a worker thread of the
+ * workspace runs the device transpose and enqueues the device->host copy.
+ * Input copies of consecutive calls run back to back while earlier calls
+ * sort and copy out (PCIe is full duplex).  (coords, values) hold the result
+ * after qd_workspace_synchronize, which also returns the FIRST device-side
+ * error (out_of_range, ...) of the calls since the last synchronize; a
+ * failing call leaves its tensor untouched, the others complete.  Buffers
+ * must stay valid (and should be pinned) until then.  Calls that read host
+ * bytes the previous call writes (chained in-place calls) are ordered after
+ * it.  Synchronous calls on the same workspace first wait for its worker.
+ * Bucket boundaries are not reported by this form. */
 qd_status qd_transpose_inplace_async(uint32_t rank, const uint32_t* dims, uint64_t nnz,
                                      uint32_t* coords, double* values,
                                      const uint32_t* target, qd_strategy_kind kind,
                                      uint32_t k, const qd_options* opts,
                                      qd_workspace* ws);
-/* Wait for every asynchronous call on this workspace. */
+/* Wait for every asynchronous call on this workspace; returns the first
+ * device-side error among them (then cleared). */
 qd_status qd_workspace_synchronize(qd_workspace* ws);
 
 /* sort_rows_by (sort.cpp:203-235): stable sort of rows [row_begin, row_end)

@@ -368,10 +368,11 @@ class Workspace {
   qd_workspace* ws_ = nullptr;
 };
 
-// transpose_inplace whose device->host copy completes at ws.synchronize();
-// consecutive calls overlap one's output copy with the next one's input copy.
-// Errors throw from the call itself (tensor untouched); t must outlive the
-// synchronize.  No bucket boundaries in this form.
+// transpose_inplace that returns after enqueueing the input copy; the device
+// work and output copy complete by ws.synchronize(), which throws the first
+// device-side error (that call's tensor untouched).  Consecutive calls
+// overlap copies with device work.  t must outlive the synchronize; no
+// bucket boundaries in this form.
 inline void transpose_inplace_async(CooTensor& t, const Ordering& target, const SortStrategy& s,
                                     Workspace& ws, const TransposeOptions& opts = {}) {
   if (target.rank() != t.rank())

@@ -567,10 +567,11 @@ def transpose_inplace(tensor: CooTensor, target, strategy: SortStrategy = SortSt
 def transpose_inplace_async(tensor: CooTensor, target, strategy: SortStrategy = SortStrategy(),
                             ws: Optional[Workspace] = None,
                             opts: Optional[TransposeOptions] = None) -> None:
-    """transpose_inplace whose device->host copy completes at ws.synchronize();
-    consecutive calls overlap one call's output copy with the next one's input
-    copy.  Errors are raised by the call itself (tensor untouched).  The
-    tensor's arrays must stay alive (and should be pinned) until then."""
+    """transpose_inplace that returns after enqueueing the input copy; the
+    device work and output copy complete by ws.synchronize(), which raises the
+    first device-side error (that call's tensor untouched).  Argument errors
+    raise at once.  The tensor's arrays must stay alive (and should be
+    pinned) until then."""
     target = _ord(target)
     if target.rank() != tensor.rank():
         raise InvalidArgument("target ordering rank does not match tensor")

@@ -103,6 +103,19 @@ std::vector<Group> sort_rows_group(uint32_t rank, const uint32_t* keys, uint32_t
   return {g};
 }
 
+// The workspace for a synchronous call: first wait until its async worker
+// is idle, so the two never touch the workspace's buffers at the same time.
+Workspace& W(qd_workspace* ws) {
+  auto* w = reinterpret_cast<Workspace*>(ws);
+  async_drain(w);
+  return *w;
+}
+const Workspace* Wc(const qd_workspace* ws) {
+  auto* w = const_cast<Workspace*>(reinterpret_cast<const Workspace*>(ws));
+  async_drain(w);
+  return w;
+}
+
 }  // namespace
 
 extern "C" {
@@ -124,23 +137,23 @@ void qd_workspace_destroy(qd_workspace* ws) {
   workspace_destroy(reinterpret_cast<Workspace*>(ws));
 }
 uint64_t qd_workspace_bytes(const qd_workspace* ws) {
-  return ws ? workspace_bytes(reinterpret_cast<const Workspace*>(ws)) : 0;
+  return ws ? workspace_bytes(Wc(ws)) : 0;
 }
 uint64_t qd_workspace_launches(const qd_workspace* ws) {
-  return ws ? workspace_launches(reinterpret_cast<const Workspace*>(ws)) : 0;
+  return ws ? workspace_launches(Wc(ws)) : 0;
 }
 
 void qd_profile_enable(qd_workspace* ws, int enable) {
-  if (ws) workspace_profile(reinterpret_cast<Workspace*>(ws), enable);
+  if (ws) workspace_profile(&W(ws), enable);
 }
 void qd_profile_reset(qd_workspace* ws) {
-  if (ws) workspace_profile_reset(reinterpret_cast<Workspace*>(ws));
+  if (ws) workspace_profile_reset(&W(ws));
 }
 qd_status qd_profile_get(const qd_workspace* ws, int kernel_class, uint64_t* launches,
                          double* total_ms, double* bytes) {
   return guard([&] {
     if (!ws || !launches || !total_ms || !bytes) invalid("null argument");
-    if (!workspace_profile_get(reinterpret_cast<const Workspace*>(ws), kernel_class, launches,
+    if (!workspace_profile_get(Wc(ws), kernel_class, launches,
                                total_ms, bytes))
       invalid("kernel class must be in 0..4");
   });
@@ -198,7 +211,7 @@ qd_status qd_transpose_inplace(uint32_t rank, const uint32_t* dims, uint64_t nnz
     auto groups = strategy_groups(target, rank, kind, k, &steps);
     check_workers(opts, kind, steps);
     TensorView t{rank, dims, nnz};
-    run_groups_host(*reinterpret_cast<Workspace*>(ws), t, coords, values, groups,
+    run_groups_host(W(ws), t, coords, values, groups,
                     opts && opts->verify_input, opts ? opts->boundaries : nullptr,
                     opts ? opts->n_boundaries : nullptr, target[0]);
     log_steps(opts, steps);
@@ -248,7 +261,7 @@ qd_status qd_transpose_device(uint32_t rank, const uint32_t* dims, uint64_t nnz,
     auto groups = strategy_groups(target, rank, kind, k, &steps);
     check_workers(opts, kind, steps);
     TensorView t{rank, dims, nnz};
-    run_groups(*reinterpret_cast<Workspace*>(ws), t, d_coords_in, d_values_in, d_coords_out,
+    run_groups(W(ws), t, d_coords_in, d_values_in, d_coords_out,
                d_values_out, groups, opts && opts->verify_input,
                opts ? opts->boundaries : nullptr, opts ? opts->n_boundaries : nullptr, target[0],
                stream);
@@ -264,7 +277,7 @@ qd_status qd_partial_sort(uint32_t rank, const uint32_t* dims, uint64_t nnz, uin
     check_tensor(rank, dims, nnz, coords, values);
     auto groups = partial_sort_group(rank, prefix, prefix_len, mode);
     TensorView t{rank, dims, nnz};
-    run_groups_host(*reinterpret_cast<Workspace*>(ws), t, coords, values, groups, false, nullptr,
+    run_groups_host(W(ws), t, coords, values, groups, false, nullptr,
                     nullptr, 0);
   });
 }
@@ -280,7 +293,7 @@ qd_status qd_sort_rows_by(uint32_t rank, const uint32_t* dims, uint64_t nnz, uin
     const uint64_t m = row_end - row_begin;
     if (m < 2 || groups.empty()) return;
     TensorView t{rank, dims, m};
-    run_groups_host(*reinterpret_cast<Workspace*>(ws), t, coords + row_begin * rank,
+    run_groups_host(W(ws), t, coords + row_begin * rank,
                     values + row_begin, groups, false, nullptr, nullptr, 0);
   });
 }
@@ -300,12 +313,12 @@ qd_status qd_sort_rows_by_device(uint32_t rank, const uint32_t* dims, uint64_t n
     auto groups = sort_rows_group(rank, key_modes, n_keys);
     if (row_begin > row_end || row_end > nnz) invalid("row range outside [0, nnz]");
     const uint64_t m = row_end - row_begin;
-    copy_rows_device(*reinterpret_cast<Workspace*>(ws), rank, nnz, d_coords_in, d_values_in,
+    copy_rows_device(W(ws), rank, nnz, d_coords_in, d_values_in,
                      d_coords_out, d_values_out, row_begin, row_end,
                      m < 2 || groups.empty(), stream);
     if (m < 2 || groups.empty()) return;
     TensorView t{rank, dims, m};
-    run_groups(*reinterpret_cast<Workspace*>(ws), t, d_coords_in + row_begin * rank,
+    run_groups(W(ws), t, d_coords_in + row_begin * rank,
                d_values_in + row_begin, d_coords_out + row_begin * rank, d_values_out + row_begin,
                groups, false, nullptr, nullptr, 0, stream);
   });
@@ -335,7 +348,7 @@ qd_status qd_partial_sort_device(uint32_t rank, const uint32_t* dims, uint64_t n
       invalid("device partial sort is out of place: input and output must differ");
     auto groups = partial_sort_group(rank, prefix, prefix_len, mode);
     TensorView t{rank, dims, nnz};
-    run_groups(*reinterpret_cast<Workspace*>(ws), t, d_coords_in, d_values_in, d_coords_out,
+    run_groups(W(ws), t, d_coords_in, d_values_in, d_coords_out,
                d_values_out, groups, false, nullptr, nullptr, 0, stream);
   });
 }
@@ -345,7 +358,7 @@ qd_status qd_is_sorted_device(uint32_t rank, uint64_t nnz, const uint32_t* d_coo
   return guard([&] {
     if (!ws || !out) invalid("null argument");
     check_ordering(order, rank);
-    *out = is_sorted_device(*reinterpret_cast<Workspace*>(ws), rank, nnz, d_coords, order, stream);
+    *out = is_sorted_device(W(ws), rank, nnz, d_coords, order, stream);
   });
 }
 
@@ -356,7 +369,7 @@ qd_status qd_bucket_starts_device(uint32_t rank, uint64_t nnz, const uint32_t* d
     if (!ws) invalid("workspace is null");
     for (uint32_t i = 0; i < n_modes; ++i)
       if (modes[i] >= rank) invalid("mode out of range");
-    const uint64_t n = bucket_starts_device(*reinterpret_cast<Workspace*>(ws), rank, nnz,
+    const uint64_t n = bucket_starts_device(W(ws), rank, nnz,
                                             d_coords, modes, n_modes, d_starts, stream);
     if (n_starts) *n_starts = n;
   });
@@ -368,7 +381,7 @@ qd_status qd_mode_histogram_device(uint32_t rank, uint64_t nnz, const uint32_t* 
   return guard([&] {
     if (!ws) invalid("workspace is null");
     if (mode >= rank) invalid("mode out of range");
-    mode_histogram_device(*reinterpret_cast<Workspace*>(ws), rank, nnz, d_coords, mode, dim,
+    mode_histogram_device(W(ws), rank, nnz, d_coords, mode, dim,
                           d_hist, stream);
   });
 }
@@ -380,7 +393,7 @@ qd_status qd_partition_rows_device(uint32_t rank, uint64_t nnz, const uint32_t* 
                                    uint64_t* part_counts, qd_workspace* ws, void* stream) {
   return guard([&] {
     if (!ws) invalid("workspace is null");
-    partition_rows_device(*reinterpret_cast<Workspace*>(ws), rank, nnz, d_coords_in, d_values_in,
+    partition_rows_device(W(ws), rank, nnz, d_coords_in, d_values_in,
                           mode, dim, d_lookup, n_parts, d_coords_out, d_values_out, part_counts,
                           stream);
   });

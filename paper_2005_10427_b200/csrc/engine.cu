@@ -29,11 +29,15 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <condition_variable>
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <deque>
 #include <map>
+#include <mutex>
 #include <string>
+#include <thread>
 
 #include "internal.hpp"
 
@@ -1799,19 +1803,23 @@ struct Workspace {
   ErrBlock* h_err = nullptr;  // pinned
   uint64_t* h_small = nullptr;  // pinned scratch for small D2H reads
   bool allow_pack = true;  // packed intermediates (cleared for a lossy-pack redo)
-  // asynchronous host-buffer transposes (qd_transpose_inplace_async): two
-  // device slots; the H2D, device and D2H work of consecutive calls runs on
-  // separate non-blocking streams so one call's output copy overlaps the
-  // next call's input copy (PCIe is full duplex)
+  // asynchronous host-buffer transposes (qd_transpose_inplace_async): the
+  // caller's thread enqueues each call's host->device copy (s_in) into one of
+  // two device slots and hands the device work to a worker thread, which runs
+  // it on s_comp and enqueues the device->host copy (s_out).  Input copies of
+  // consecutive calls run back to back, overlapping the previous calls'
+  // device work and output copies (PCIe is full duplex).
   cudaStream_t s_in = nullptr, s_comp = nullptr, s_out = nullptr;
   cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_comp[2] = {nullptr, nullptr},
               ev_out[2] = {nullptr, nullptr};
-  // single-pass scan (k_scan_lookback): tile status words and the ticket
-  // counter; lb_base = tickets issued so far (the device counter's value)
-  unsigned long long* lb_status = nullptr;
-  unsigned long long* lb_ticket = nullptr;
-  size_t lb_cap = 0;
-  unsigned long long lb_base = 0, lb_cleared_epoch = ~0ull;
+  struct SlotBuf {
+    uint32_t* ic = nullptr;
+    double* iv = nullptr;
+    uint32_t* oc = nullptr;
+    double* ov = nullptr;
+    size_t rows = 0, rank = 0;
+  } slots[2];
+  bool slot_busy[2] = {false, false};  // job queued / running, output copy not yet issued
   int slot = 0;
   struct HostSpan {
     const void* c = nullptr;
@@ -1819,6 +1827,32 @@ struct Workspace {
     const void* v = nullptr;
     size_t nv = 0;
   } last_host;  // host bytes the latest async call writes back
+  struct AsyncJob {
+    std::vector<uint32_t> dims;
+    uint64_t nnz = 0;
+    uint32_t* coords = nullptr;
+    double* values = nullptr;
+    std::vector<Group> groups;
+    bool verify_input = false;
+    int slot = 0;
+  };
+  std::thread worker;
+  std::mutex mu;
+  std::condition_variable cv;
+  std::deque<AsyncJob> jobs;
+  int running = 0;  // jobs popped and not yet finished by the worker
+  bool stop = false;
+  bool async_failed = false;  // first error of a device job, reported at synchronize
+  qd_status async_code = QD_OK;
+  std::string async_msg;
+  uint64_t async_row = 0;
+  uint32_t async_mode = 0;
+  // single-pass scan (k_scan_lookback): tile status words and the ticket
+  // counter; lb_base = tickets issued so far (the device counter's value)
+  unsigned long long* lb_status = nullptr;
+  unsigned long long* lb_ticket = nullptr;
+  size_t lb_cap = 0;
+  unsigned long long lb_base = 0, lb_cleared_epoch = ~0ull;
   // live per-kernel-class timing (CUDA events on the launch stream)
   bool prof = false;
   struct ProfStat {
@@ -1917,7 +1951,18 @@ Workspace* workspace_create(int device) {
 
 void workspace_destroy(Workspace* ws) {
   if (!ws) return;
+  if (ws->worker.joinable()) {
+    {
+      std::lock_guard<std::mutex> lk(ws->mu);
+      ws->stop = true;
+    }
+    ws->cv.notify_all();
+    ws->worker.join();
+  }
   cudaSetDevice(ws->device);
+  for (auto& sb : ws->slots)
+    for (void* p : {(void*)sb.ic, (void*)sb.iv, (void*)sb.oc, (void*)sb.ov})
+      if (p) cudaFree(p);
   for (cudaStream_t st : {ws->s_in, ws->s_comp, ws->s_out})
     if (st) {
       cudaStreamSynchronize(st);
@@ -2688,6 +2733,65 @@ void run_groups_host(Workspace& ws, const TensorView& t, uint32_t* coords, doubl
   if (n_boundaries) *n_boundaries = nb;
 }
 
+namespace {
+// the worker: device work of each queued call, then its output copy
+void async_worker(Workspace* ws) {
+  cudaSetDevice(ws->device);
+  for (;;) {
+    Workspace::AsyncJob job;
+    {
+      std::unique_lock<std::mutex> lk(ws->mu);
+      ws->cv.wait(lk, [&] { return ws->stop || !ws->jobs.empty(); });
+      if (ws->jobs.empty()) return;  // stop requested, nothing left
+      job = std::move(ws->jobs.front());
+      ws->jobs.pop_front();
+      ++ws->running;
+    }
+    const int sl = job.slot;
+    Workspace::SlotBuf& sb = ws->slots[sl];
+    const uint32_t R = (uint32_t)job.dims.size();
+    const uint64_t N = job.nnz;
+    try {
+      TensorView t{R, job.dims.data(), N};
+      QD_CUDA(cudaStreamWaitEvent(ws->s_comp, ws->ev_in[sl], 0));
+      // its internal host syncs return once this call's rows are sorted (an
+      // out_of_range is found before any host byte is written)
+      run_groups(*ws, t, sb.ic, sb.iv, sb.oc, sb.ov, job.groups, job.verify_input, nullptr,
+                 nullptr, 0, ws->s_comp);
+      QD_CUDA(cudaEventRecord(ws->ev_comp[sl], ws->s_comp));
+      QD_CUDA(cudaStreamWaitEvent(ws->s_out, ws->ev_comp[sl], 0));
+      QD_CUDA(cudaMemcpyAsync(job.coords, sb.oc, N * R * 4, cudaMemcpyDeviceToHost, ws->s_out));
+      QD_CUDA(cudaMemcpyAsync(job.values, sb.ov, N * 8, cudaMemcpyDeviceToHost, ws->s_out));
+      QD_CUDA(cudaEventRecord(ws->ev_out[sl], ws->s_out));
+    } catch (const Error& e) {
+      std::lock_guard<std::mutex> lk(ws->mu);
+      if (!ws->async_failed) {
+        ws->async_failed = true;
+        ws->async_code = e.code;
+        ws->async_msg = e.what();
+        ws->async_row = e.row;
+        ws->async_mode = e.mode;
+      }
+      cudaEventRecord(ws->ev_out[sl], ws->s_comp);  // slot reusable after the failed work
+    } catch (const std::exception& e) {
+      std::lock_guard<std::mutex> lk(ws->mu);
+      if (!ws->async_failed) {
+        ws->async_failed = true;
+        ws->async_code = QD_CUDA_ERROR;
+        ws->async_msg = e.what();
+      }
+      cudaEventRecord(ws->ev_out[sl], ws->s_comp);
+    }
+    {
+      std::lock_guard<std::mutex> lk(ws->mu);
+      ws->slot_busy[sl] = false;
+      --ws->running;
+    }
+    ws->cv.notify_all();
+  }
+}
+}  // namespace
+
 void run_groups_host_async(Workspace& ws, const TensorView& t, uint32_t* coords, double* values,
                            const std::vector<Group>& groups, bool verify_input) {
   QD_CUDA(cudaSetDevice(ws.device));
@@ -2699,42 +2803,87 @@ void run_groups_host_async(Workspace& ws, const TensorView& t, uint32_t* coords,
         QD_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
         QD_CUDA(cudaEventRecord(*e, ws.s_in));  // "done" until first use
       }
+    ws.worker = std::thread(async_worker, &ws);
   }
   const uint64_t N = t.nnz;
   const uint32_t R = t.rank;
   const int sl = ws.slot;
-  const std::string tag = std::to_string(sl);
-  uint32_t* ic = ws.get<uint32_t>("async_in_c" + tag, N * R);
-  double* iv = ws.get<double>("async_in_v" + tag, N);
-  uint32_t* oc = ws.get<uint32_t>("async_out_c" + tag, N * R);
-  double* ov = ws.get<double>("async_out_v" + tag, N);
-  // the slot's buffers are free once its previous output copy has drained;
-  // and if this call reads host bytes the previous call is still writing
-  // (chained in-place calls), its output copy must land first
-  QD_CUDA(cudaStreamWaitEvent(ws.s_in, ws.ev_out[sl], 0));
   auto overlaps = [](const void* a, size_t na, const void* b, size_t nb) {
     const char *x = static_cast<const char*>(a), *y = static_cast<const char*>(b);
     return na && nb && x < y + nb && y < x + na;
   };
   const Workspace::HostSpan cur{coords, N * R * 4, values, N * 8};
   const Workspace::HostSpan& prev = ws.last_host;
-  if (overlaps(cur.c, cur.nc, prev.c, prev.nc) || overlaps(cur.c, cur.nc, prev.v, prev.nv) ||
-      overlaps(cur.v, cur.nv, prev.c, prev.nc) || overlaps(cur.v, cur.nv, prev.v, prev.nv))
-    QD_CUDA(cudaStreamWaitEvent(ws.s_in, ws.ev_out[sl ^ 1], 0));
-  QD_CUDA(cudaMemcpyAsync(ic, coords, N * R * 4, cudaMemcpyHostToDevice, ws.s_in));
-  QD_CUDA(cudaMemcpyAsync(iv, values, N * 8, cudaMemcpyHostToDevice, ws.s_in));
+  const bool chained = overlaps(cur.c, cur.nc, prev.c, prev.nc) ||
+                       overlaps(cur.c, cur.nc, prev.v, prev.nv) ||
+                       overlaps(cur.v, cur.nv, prev.c, prev.nc) ||
+                       overlaps(cur.v, cur.nv, prev.v, prev.nv);
+  {
+    // this slot's previous job must have issued its output copy (so ev_out
+    // is its final record); a chained call also needs the previous one's
+    std::unique_lock<std::mutex> lk(ws.mu);
+    ws.cv.wait(lk, [&] { return !ws.slot_busy[sl] && (!chained || !ws.slot_busy[sl ^ 1]); });
+  }
+  Workspace::SlotBuf& sb = ws.slots[sl];
+  if (sb.rows < N || sb.rank < R) {
+    QD_CUDA(cudaEventSynchronize(ws.ev_out[sl]));  // its buffers are no longer read
+    for (void* p : {(void*)sb.ic, (void*)sb.iv, (void*)sb.oc, (void*)sb.ov})
+      if (p) QD_CUDA(cudaFree(p));
+    sb = Workspace::SlotBuf{};
+    const size_t rows = std::max<size_t>(N + N / 8, 1024), rk = std::max<size_t>(R, 4);
+    QD_CUDA(cudaMalloc(&sb.ic, rows * rk * 4));
+    QD_CUDA(cudaMalloc(&sb.iv, rows * 8));
+    QD_CUDA(cudaMalloc(&sb.oc, rows * rk * 4));
+    QD_CUDA(cudaMalloc(&sb.ov, rows * 8));
+    sb.rows = rows;
+    sb.rank = rk;
+  }
+  // the slot's buffers are free once its previous output copy has drained;
+  // a chained call reads host bytes the previous call's output copy writes
+  QD_CUDA(cudaStreamWaitEvent(ws.s_in, ws.ev_out[sl], 0));
+  if (chained) QD_CUDA(cudaStreamWaitEvent(ws.s_in, ws.ev_out[sl ^ 1], 0));
+  QD_CUDA(cudaMemcpyAsync(sb.ic, coords, N * R * 4, cudaMemcpyHostToDevice, ws.s_in));
+  QD_CUDA(cudaMemcpyAsync(sb.iv, values, N * 8, cudaMemcpyHostToDevice, ws.s_in));
   QD_CUDA(cudaEventRecord(ws.ev_in[sl], ws.s_in));
-  QD_CUDA(cudaStreamWaitEvent(ws.s_comp, ws.ev_in[sl], 0));
-  // device work; its internal host syncs return once this call's rows are
-  // sorted (and report out_of_range before any host byte is written)
-  run_groups(ws, t, ic, iv, oc, ov, groups, verify_input, nullptr, nullptr, 0, ws.s_comp);
-  QD_CUDA(cudaEventRecord(ws.ev_comp[sl], ws.s_comp));
-  QD_CUDA(cudaStreamWaitEvent(ws.s_out, ws.ev_comp[sl], 0));
-  QD_CUDA(cudaMemcpyAsync(coords, oc, N * R * 4, cudaMemcpyDeviceToHost, ws.s_out));
-  QD_CUDA(cudaMemcpyAsync(values, ov, N * 8, cudaMemcpyDeviceToHost, ws.s_out));
-  QD_CUDA(cudaEventRecord(ws.ev_out[sl], ws.s_out));
+  Workspace::AsyncJob job;
+  job.dims.assign(t.dims, t.dims + R);
+  job.nnz = N;
+  job.coords = coords;
+  job.values = values;
+  job.groups = groups;
+  job.verify_input = verify_input;
+  job.slot = sl;
+  {
+    std::lock_guard<std::mutex> lk(ws.mu);
+    ws.slot_busy[sl] = true;
+    ws.jobs.push_back(std::move(job));
+  }
+  ws.cv.notify_all();
   ws.slot = sl ^ 1;
   ws.last_host = cur;
+}
+
+// Wait until the worker has no queued or running job (the calling thread may
+// then use the workspace's buffers).
+void async_drain(Workspace* ws) {
+  if (!ws->worker.joinable()) return;
+  std::unique_lock<std::mutex> lk(ws->mu);
+  ws->cv.wait(lk, [&] { return ws->jobs.empty() && ws->running == 0; });
+}
+
+void workspace_synchronize(Workspace* ws) {
+  async_drain(ws);
+  QD_CUDA(cudaSetDevice(ws->device));
+  for (cudaStream_t st : {ws->s_in, ws->s_comp, ws->s_out})
+    if (st) QD_CUDA(cudaStreamSynchronize(st));
+  std::lock_guard<std::mutex> lk(ws->mu);
+  if (ws->async_failed) {
+    ws->async_failed = false;
+    Error e(ws->async_code, ws->async_msg);
+    e.row = ws->async_row;
+    e.mode = ws->async_mode;
+    throw e;
+  }
 }
 
 void copy_rows_device(Workspace& ws, uint32_t rank, uint64_t nnz, const uint32_t* c_in,
@@ -2754,12 +2903,6 @@ void copy_rows_device(Workspace& ws, uint32_t rank, uint64_t nnz, const uint32_t
     cp(0, row_begin);
     cp(row_end, nnz);
   }
-}
-
-void workspace_synchronize(Workspace* ws) {
-  QD_CUDA(cudaSetDevice(ws->device));
-  for (cudaStream_t st : {ws->s_in, ws->s_comp, ws->s_out})
-    if (st) QD_CUDA(cudaStreamSynchronize(st));
 }
 
 bool is_sorted_device(Workspace& ws, uint32_t rank, uint64_t nnz, const uint32_t* d_coords,

@@ -93,6 +93,7 @@ void copy_rows_device(Workspace& ws, uint32_t rank, uint64_t nnz, const uint32_t
 void run_groups_host_async(Workspace& ws, const TensorView& t, uint32_t* coords, double* values,
                            const std::vector<Group>& groups, bool verify_input);
 void workspace_synchronize(Workspace* ws);
+void async_drain(Workspace* ws);
 void run_groups_host(Workspace& ws, const TensorView& t, uint32_t* coords,
                      double* values, const std::vector<Group>& groups,
                      bool verify_input, uint64_t* h_boundaries,

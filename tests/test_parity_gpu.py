@@ -455,10 +455,18 @@ def test_async_errors_leave_tensor_untouched(ws):
     big = rand_tensor(rng, [5, 300, 300], 50_000)
     big.coords[3 * 20_000 + 2] = 300
     before = big.copy()
+    ok = rand_tensor(rng, [5, 300, 300], 50_000)
+    ok_before = ok.copy()
+    # device errors of queued calls surface at synchronize (the first one);
+    # the failing call's tensor is untouched, the other calls complete
+    qd.transpose_inplace_async(big, [2, 1, 0], qd.SortStrategy.quesadilla(), ws)
+    qd.transpose_inplace_async(ok, [2, 1, 0], qd.SortStrategy.quesadilla(), ws)
     with pytest.raises(qd.OutOfRange):
-        qd.transpose_inplace_async(big, [2, 1, 0], qd.SortStrategy.quesadilla(), ws)
-    ws.synchronize()
+        ws.synchronize()
     assert big == before
+    c, v, _ = ORC.transpose(ok_before.dims, ok_before.coords, ok_before.values, [2, 1, 0])
+    assert same(ok, c, v)
+    ws.synchronize()  # the error was reported once
     with pytest.raises(qd.InvalidArgument):
         qd.transpose_inplace_async(before, [2, 1, 0], qd.SortStrategy.quesadilla(), ws,
                                    qd.TransposeOptions(boundaries=[]))
@@ -635,3 +643,18 @@ def test_relabel_target_matches_oracle():
                 assert qd.relabel_target(list(s), list(t)).modes() == ORC.relabel_target(list(s), list(t))
     with pytest.raises(qd.InvalidArgument):
         qd.relabel_target([0, 1], [0, 1, 2])
+
+
+def test_async_then_sync_calls_on_one_workspace(ws):
+    """A synchronous call on a workspace with queued async calls waits for
+    the worker first; results of both are correct."""
+    rng = np.random.default_rng(14)
+    a = rand_tensor(rng, [80, 90, 100], 300_000)
+    b = rand_tensor(rng, [80, 90, 100], 300_000)
+    a0, b0 = a.copy(), b.copy()
+    qd.transpose_inplace_async(a, [1, 2, 0], qd.SortStrategy.quesadilla(), ws)
+    out = qd.transpose(b, [2, 0, 1], ws=ws)
+    ws.synchronize()
+    ca, va, _ = ORC.transpose(a0.dims, a0.coords, a0.values, [1, 2, 0])
+    cb, vb, _ = ORC.transpose(b0.dims, b0.coords, b0.values, [2, 0, 1])
+    assert same(a, ca, va) and same(out, cb, vb)
