@@ -658,3 +658,46 @@ def test_async_then_sync_calls_on_one_workspace(ws):
     ca, va, _ = ORC.transpose(a0.dims, a0.coords, a0.values, [1, 2, 0])
     cb, vb, _ = ORC.transpose(b0.dims, b0.coords, b0.values, [2, 0, 1])
     assert same(a, ca, va) and same(out, cb, vb)
+
+
+# --- extreme shapes ----------------------------------------------------------
+
+def _np_transpose(dims, coords, values, target):
+    """Stable sort of simply sorted rows by the target key (numpy lexsort)."""
+    r = len(dims)
+    c = np.asarray(coords, np.uint32).reshape(-1, r)
+    order = np.lexsort(tuple(c[:, m] for m in reversed(list(target))))  # stable
+    return c[order].ravel(), np.asarray(values)[order]
+
+
+def test_full_width_dimensions(ws):
+    """Modes of extent up to 2^32 - 1 (32-bit keys, > 64 packed bits: AoS
+    intermediates, no local sort); the reference's count arrays would need
+    16 GB here, so numpy's stable lexsort is the check."""
+    rng = np.random.default_rng(41)
+    dims = [2**32 - 1, 5, 2**31 + 7]
+    n = 400_000
+    c = np.stack([rng.integers(0, d, n, dtype=np.uint64) for d in dims], 1).astype(np.uint32)
+    c[: n // 2, 0] = c[0, 0]  # one huge mode-0 run as well
+    c = c[np.lexsort(c.T[::-1])]
+    v = rng.random(n)
+    t = qd.CooTensor(dims, c.ravel(), v)
+    for target in ([2, 0, 1], [1, 2, 0], [0, 2, 1], [2, 1, 0]):
+        out = qd.transpose(t, target, ws=ws)
+        ec, ev = _np_transpose(dims, t.coords, t.values, target)
+        assert same(out, ec, ev), target
+
+
+def test_high_rank_against_oracle(ws):
+    rng = np.random.default_rng(42)
+    for r in (9, 12, 16):
+        dims = [int(x) for x in rng.integers(2, 5, r)]
+        t = rand_tensor(rng, dims, 30_000)
+        for _ in range(3):
+            target = [int(x) for x in rng.permutation(r)]
+            log = []
+            out = qd.transpose(t, target, qd.SortStrategy.quesadilla(),
+                               qd.TransposeOptions(pass_log=log), ws)
+            c, v, steps = ORC.transpose(t.dims, t.coords, t.values, target)
+            assert same(out, c, v), (r, target)
+            assert [(s.prefix_len, s.mode) for s in log] == [tuple(x) for x in steps]
