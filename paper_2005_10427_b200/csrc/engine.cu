@@ -61,7 +61,6 @@ constexpr int kRadixLog = 8;
 constexpr int kBins = 1 << kRadixLog;
 constexpr int kMaxTerms = 12;
 constexpr int kMaxKeys = QD_MAX_RANK;
-constexpr int kHistPasses = 8;  // passes histogrammed per k_hist launch
 constexpr uint32_t kChunkTiles = 16;  // tiles per scatter chunk
 constexpr double kRunSortMinAvg = 2.5;       // mean run length that pays for a run sort
 constexpr uint64_t kRunSortMinRows = 1u << 20;  // below this, not worth a probe
@@ -805,7 +804,6 @@ __global__ void __launch_bounds__(kSortThreads, 1024 / kSortThreads) k_scatter(S
   uint16_t* s_dig = reinterpret_cast<uint16_t*>(smem + L.dig);
   uint16_t* s_sorted = reinterpret_cast<uint16_t*>(smem + L.sorted);
   uint16_t* s_whist = reinterpret_cast<uint16_t*>(smem + L.whist);
-  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(smem + L.cnt);
   uint32_t* s_start = reinterpret_cast<uint32_t*>(smem + L.start);
   unsigned long long* s_run = reinterpret_cast<unsigned long long*>(smem + L.run);
   long long* s_gbase = reinterpret_cast<long long*>(smem + L.gbase);
@@ -1176,7 +1174,7 @@ __device__ __forceinline__ uint32_t ceil_log2_dev(uint64_t x) {
 }
 
 __global__ void __launch_bounds__(kSortThreads) k_local(LocalArgs a) {
-  extern __shared__ __align__(16) unsigned char smem[];
+  extern __shared__ __align__(128) unsigned char smem[];
   const LocalLayout L(a.cap, a.rank, a.TL);
   uint32_t* s_craw = reinterpret_cast<uint32_t*>(smem + L.c);
   double* s_vraw = reinterpret_cast<double*>(smem + L.v);
@@ -1185,7 +1183,6 @@ __global__ void __launch_bounds__(kSortThreads) k_local(LocalArgs a) {
   uint16_t* s_p1 = reinterpret_cast<uint16_t*>(smem + L.perm1);
   uint16_t* s_rank = reinterpret_cast<uint16_t*>(smem + L.rnk);
   uint16_t* s_whist = reinterpret_cast<uint16_t*>(smem + L.whist);
-  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(smem + L.cnt);
   uint32_t* s_start = reinterpret_cast<uint32_t*>(smem + L.start);
   unsigned long long* s_seg = reinterpret_cast<unsigned long long*>(smem + L.seg);
   uint32_t* s_tmp = reinterpret_cast<uint32_t*>(smem + L.tmp);
@@ -1693,7 +1690,7 @@ constexpr uint32_t kMoveRows = 4096;  // output rows per k_move_runs CTA
 __global__ void __launch_bounds__(kSortThreads, 1) k_move_runs(
     const uint32_t* in_c, const double* in_v, uint32_t* out_c, double* out_v, uint32_t rank,
     uint64_t N, const double* rval, const unsigned long long* dsto, uint64_t S) {
-  extern __shared__ __align__(16) unsigned char smem[];
+  extern __shared__ __align__(128) unsigned char smem[];
   unsigned long long* s_dst = reinterpret_cast<unsigned long long*>(smem);
   unsigned long long* s_src = s_dst + kMoveRows + 1;
   __shared__ unsigned long long s_j0;
