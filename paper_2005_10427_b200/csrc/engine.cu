@@ -810,7 +810,10 @@ __global__ void __launch_bounds__(kSortThreads, 1024 / kSortThreads) k_scatter(S
   unsigned long long* s_tmp = reinterpret_cast<unsigned long long*>(smem + L.tmp);
   uint32_t* s_ofs = reinterpret_cast<uint32_t*>(smem + L.ofs);  // [2][66] byte offsets
   unsigned long long* s_bar = reinterpret_cast<unsigned long long*>(smem + L.bar);
-  __shared__ uint32_t s_chunk, s_tile;  // next (chunk, tile-in-chunk) to process
+  // (chunk, tile-in-chunk) of iteration it, double-buffered by it & 1: the
+  // advancer publishes iteration it+1's during iteration it, and the barrier
+  // ending iteration it orders that before every thread's read
+  __shared__ uint32_t s_chunk[2], s_tile[2];
   __shared__ ChunkDesc s_cd[2];          // descriptor of the chunk staged in buffer b
 
   // spans of a tile: AoS {coords, values}, SoA {column 0..R-1, values},
@@ -872,7 +875,7 @@ __global__ void __launch_bounds__(kSortThreads, 1024 / kSortThreads) k_scatter(S
   };
   // advancer warp: pick the tile after (ci, ti) (whose chunk is in slot b^1),
   // publish it in s_chunk/s_tile and start loading it into buffer b
-  auto advance = [&](uint32_t b, uint32_t ci, uint32_t ti) {
+  auto advance = [&](uint32_t b, uint32_t ci, uint32_t ti, uint32_t pslot) {
     uint32_t nc = ci, nt = ti + 1;
     ChunkDesc cd = s_cd[b ^ 1u];
     if (nt * (unsigned long long)a.T >= cd.len) {
@@ -882,8 +885,8 @@ __global__ void __launch_bounds__(kSortThreads, 1024 / kSortThreads) k_scatter(S
       if (nc + gridDim.x < a.num_chunks) pre = a.chunks[nc + gridDim.x];
     }
     if ((threadIdx.x & 31) == 0) {
-      s_chunk = nc;
-      s_tile = nt;
+      s_chunk[pslot] = nc;
+      s_tile[pslot] = nt;
     }
     if (nc < a.num_chunks) load_tile(b, cd, nt);
   };
@@ -897,8 +900,8 @@ __global__ void __launch_bounds__(kSortThreads, 1024 / kSortThreads) k_scatter(S
   if (threadIdx.x >= kAdv) {  // the advancer warp
     const uint32_t c0 = blockIdx.x;
     if (threadIdx.x == kAdv) {
-      s_chunk = c0;
-      s_tile = 0;
+      s_chunk[0] = c0;
+      s_tile[0] = 0;
     }
     if (c0 < a.num_chunks) {
       if (c0 + gridDim.x < a.num_chunks) pre = a.chunks[c0 + gridDim.x];
@@ -918,9 +921,8 @@ __global__ void __launch_bounds__(kSortThreads, 1024 / kSortThreads) k_scatter(S
   }
   for (uint32_t it = 0;; ++it) {
     const uint32_t b = it & 1u;
-    const uint32_t ci = s_chunk, ti = s_tile;
+    const uint32_t ci = s_chunk[it & 1u], ti = s_tile[it & 1u];
     if (ci >= a.num_chunks) break;
-    __syncthreads();  // everyone has read s_chunk / s_tile
     QD_TMARK(1);
     const ChunkDesc cd = s_cd[b];  // the advancer only refills the other slot
     const unsigned long long rb = cd.row_begin + (unsigned long long)ti * a.T;
@@ -940,7 +942,7 @@ __global__ void __launch_bounds__(kSortThreads, 1024 / kSortThreads) k_scatter(S
 #if QD_EARLY_ADVANCE
     // buffer b^1 was released by the previous tile's closing barrier: start
     // the next tile's bulk copies before this tile's work
-    if (threadIdx.x >= kAdv) advance(b ^ 1u, ci, ti);
+    if (threadIdx.x >= kAdv) advance(b ^ 1u, ci, ti, (it + 1) & 1u);
 #endif
     mbar_wait(&s_bar[b], (phases >> b) & 1u);  // each thread observes the TMA completion
     QD_TMARK(2);
@@ -1026,7 +1028,7 @@ __global__ void __launch_bounds__(kSortThreads, 1024 / kSortThreads) k_scatter(S
     __syncthreads();
     QD_TMARK(3);
 #if !QD_EARLY_ADVANCE
-    if (threadIdx.x >= kAdv) advance(b ^ 1u, ci, ti);  // warp-wide; overlaps bin_totals
+    if (threadIdx.x >= kAdv) advance(b ^ 1u, ci, ti, (it + 1) & 1u);  // overlaps bin_totals
 #endif
     // bin totals + bin scan with two barriers: thread b (< kBins) turns the
     // column of warp counts into warp-exclusive offsets, the first kBins/32
