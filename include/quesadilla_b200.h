@@ -201,6 +201,18 @@ qd_status qd_is_sorted_device(uint32_t rank, uint64_t nnz,
                               int* out, qd_workspace* ws, void* stream);
 /* detail::bucket_starts (sort.cpp:136-147) on device coords, followed by nnz:
  * d_starts (device, capacity nnz + 1) receives the run starts + nnz. */
+/* CSF levels of a tensor sorted under `order` (the emitted
+ * boundaries turned into level pointers; the paper's motivation).  Level k
+ * (0 <= k < rank) has n_fibers[k] fibers = maximal runs of equal
+ * (order[0..k]) coordinates; d_crd[k][f] is coordinate order[k] of fiber f;
+ * d_pos[0] = {0, n_fibers[0]} and for k >= 1 d_pos[k][j] is the first
+ * level-k fiber of level-(k-1) fiber j (n_fibers[k-1] + 1 entries).  The
+ * leaf level is the distinct coordinates (duplicates share a leaf; values
+ * stay per row).  Capacities: d_pos[k] max(nnz + 1, 2), d_crd[k] nnz entries. */
+qd_status qd_csf_device(uint32_t rank, uint64_t nnz, const uint32_t* d_coords,
+                        const uint32_t* order, uint64_t* const* d_pos,
+                        uint32_t* const* d_crd, uint64_t* n_fibers,
+                        qd_workspace* ws, void* stream);
 qd_status qd_bucket_starts_device(uint32_t rank, uint64_t nnz,
                                   const uint32_t* d_coords,
                                   const uint32_t* modes, uint32_t n_modes,

@@ -129,6 +129,9 @@ def lib():
                                              C.c_uint64, _u32p, C.c_uint32, C.c_void_p,
                                              C.c_void_p]
         L.qd_relabel_target.argtypes = [_u32p, _u32p, C.c_uint32, _u32p]
+        L.qd_csf_device.argtypes = [C.c_uint32, C.c_uint64, C.c_void_p, _u32p,
+                                    C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
+                                    C.POINTER(C.c_uint64), C.c_void_p, C.c_void_p]
         L.qd_partial_sort_device.argtypes = [C.c_uint32, _u32p, C.c_uint64, C.c_void_p, C.c_void_p,
                                              C.c_void_p, C.c_void_p, _u32p, C.c_uint32, C.c_uint32,
                                              C.c_void_p, C.c_void_p]
@@ -735,6 +738,28 @@ def bucket_starts_device(rank, nnz, coords, modes, starts_out: int, ws=None, str
                                          C.c_void_p(starts_out), C.byref(n), w.handle,
                                          C.c_void_p(stream)))
     return n.value
+
+
+def csf_device(coords, rank: int, order, ws=None, stream=0):
+    """CSF level arrays of a device tensor sorted under `order` (torch int32
+    coords, nnz*rank): returns (pos, crd) lists of torch tensors, level k =
+    runs of equal order[0..k] (qd_csf_device)."""
+    import torch
+    w = _ws(ws)
+    o = _arr_u32(_ord(order).modes())
+    nnz = coords.numel() // rank
+    pos = [torch.empty(max(nnz + 1, 2), dtype=torch.int64, device=coords.device)
+           for _ in range(rank)]
+    crd = [torch.empty(max(nnz, 1), dtype=torch.int32, device=coords.device) for _ in range(rank)]
+    pp = (C.c_void_p * rank)(*[p.data_ptr() for p in pos])
+    cp = (C.c_void_p * rank)(*[c.data_ptr() for c in crd])
+    nf = (C.c_uint64 * rank)()
+    _check(lib().qd_csf_device(rank, nnz, C.c_void_p(coords.data_ptr()), _ptr_u32(o), pp, cp, nf,
+                               w.handle, C.c_void_p(stream)))
+    n = [int(x) for x in nf]
+    pos = [pos[0][:2]] + [pos[k][: n[k - 1] + 1] for k in range(1, rank)]
+    crd = [crd[k][: n[k]] for k in range(rank)]
+    return pos, crd
 
 
 def mode_histogram_device(rank, nnz, coords, mode, dim, hist_out: int, ws=None, stream=0):

@@ -362,6 +362,22 @@ qd_status qd_is_sorted_device(uint32_t rank, uint64_t nnz, const uint32_t* d_coo
   });
 }
 
+qd_status qd_csf_device(uint32_t rank, uint64_t nnz, const uint32_t* d_coords,
+                        const uint32_t* order, uint64_t* const* d_pos, uint32_t* const* d_crd,
+                        uint64_t* n_fibers, qd_workspace* ws, void* stream) {
+  return guard([&] {
+    if (!ws) invalid("workspace is null");
+    if (rank == 0 || rank > QD_MAX_RANK) invalid("tensor rank must be in 1..64");
+    if (nnz && !d_coords) invalid("coordinate buffer is null");
+    if (nnz >= (uint64_t{1} << 32)) invalid("nnz must be below 2^32");
+    check_ordering(order, rank);
+    if (!d_pos || !d_crd || !n_fibers) invalid("output arrays are null");
+    for (uint32_t k = 0; k < rank; ++k)
+      if (!d_pos[k] || (nnz && !d_crd[k])) invalid("output array of a level is null");
+    csf_device(W(ws), rank, nnz, d_coords, order, d_pos, d_crd, n_fibers, stream);
+  });
+}
+
 qd_status qd_bucket_starts_device(uint32_t rank, uint64_t nnz, const uint32_t* d_coords,
                                   const uint32_t* modes, uint32_t n_modes, uint64_t* d_starts,
                                   uint64_t* n_starts, qd_workspace* ws, void* stream) {

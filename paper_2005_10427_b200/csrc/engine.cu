@@ -1679,6 +1679,30 @@ __global__ void k_run_records(const uint32_t* c, uint32_t rank, uint32_t mode, u
   }
 }
 
+// CSF levels: crd[f] = coordinate `mode` of fiber f's first row
+__global__ void k_fiber_crd(const uint32_t* c, uint32_t rank, uint32_t mode,
+                            const unsigned long long* starts, uint64_t nf, uint32_t* crd) {
+  for (uint64_t f = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; f < nf;
+       f += (uint64_t)gridDim.x * blockDim.x)
+    crd[f] = c[starts[f] * rank + mode];
+}
+// pos[j] = index of parent fiber j's first row among the child fiber starts
+// (parents' starts are a subset of the children's, both sorted), j <= np
+__global__ void k_fiber_pos(const unsigned long long* child, uint64_t nc,
+                            const unsigned long long* parent, uint64_t np, uint64_t nnz,
+                            unsigned long long* pos) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j <= np;
+       j += (uint64_t)gridDim.x * blockDim.x) {
+    const unsigned long long x = j < np ? parent[j] : nnz;
+    uint64_t l = 0, h = nc;  // first child start >= x
+    while (l < h) {
+      const uint64_t m = (l + h) >> 1;
+      if (child[m] < x) l = m + 1; else h = m;
+    }
+    pos[j] = l;
+  }
+}
+
 __global__ void k_run_lens(const double* rval, uint64_t S, uint32_t* lens) {
   for (unsigned long long s = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; s < S;
        s += (unsigned long long)gridDim.x * blockDim.x)
@@ -2932,6 +2956,42 @@ uint64_t bucket_starts_device(Workspace& ws, uint32_t rank, uint64_t nnz, const 
   QD_CUDA(cudaMemcpyAsync(d_starts, seg, (S + 1) * 8, cudaMemcpyDeviceToDevice, c.st));
   QD_CUDA(cudaStreamSynchronize(c.st));
   return S + 1;
+}
+
+void csf_device(Workspace& ws, uint32_t rank, uint64_t nnz, const uint32_t* d_coords,
+                const uint32_t* order, uint64_t* const* d_pos, uint32_t* const* d_crd,
+                uint64_t* n_fibers, void* stream) {
+  Ctx c = make_ctx(ws, stream);
+  uint64_t prev_n = 0;
+  for (uint32_t k = 0; k < rank; ++k) {
+    unsigned long long* seg = nullptr;
+    uint64_t S = 0;
+    if (nnz) S = find_runs(c, d_coords, rank, nnz, std::vector<uint32_t>(order, order + k + 1), &seg);
+    n_fibers[k] = S;
+    // keep this level's starts for the next level's pos (find_runs reuses its buffer)
+    auto* cur = c.ws.get<unsigned long long>(k & 1 ? "csf_starts1" : "csf_starts0", S + 1);
+    const auto* prev = c.ws.get<unsigned long long>(k & 1 ? "csf_starts0" : "csf_starts1", 1);
+    const uint32_t grid = (uint32_t)std::min<uint64_t>((S + kThreads) / kThreads, ws.num_sms * 8);
+    if (S) {
+      QD_CUDA(cudaMemcpyAsync(cur, seg, S * 8, cudaMemcpyDeviceToDevice, c.st));
+      c.pre();
+      k_fiber_crd<<<grid, kThreads, 0, c.st>>>(d_coords, rank, order[k], cur, S, d_crd[k]);
+      c.launched(kOtherK);
+    }
+    if (k == 0) {
+      const unsigned long long h[2] = {0ull, (unsigned long long)S};
+      QD_CUDA(cudaMemcpyAsync(d_pos[0], h, 16, cudaMemcpyHostToDevice, c.st));
+      QD_CUDA(cudaStreamSynchronize(c.st));  // h is on the stack
+    } else {
+      const uint32_t g2 = (uint32_t)std::min<uint64_t>((prev_n + kThreads) / kThreads, ws.num_sms * 8);
+      c.pre();
+      k_fiber_pos<<<g2, kThreads, 0, c.st>>>(cur, S, prev, prev_n, nnz,
+                                              reinterpret_cast<unsigned long long*>(d_pos[k]));
+      c.launched(kOtherK);
+    }
+    prev_n = S;
+  }
+  QD_CUDA(cudaStreamSynchronize(c.st));
 }
 
 void mode_histogram_device(Workspace& ws, uint32_t rank, uint64_t nnz, const uint32_t* d_coords,

@@ -102,6 +102,9 @@ void run_groups_host(Workspace& ws, const TensorView& t, uint32_t* coords,
 bool is_sorted_device(Workspace& ws, uint32_t rank, uint64_t nnz,
                       const uint32_t* d_coords, const uint32_t* order,
                       void* stream);
+void csf_device(Workspace& ws, uint32_t rank, uint64_t nnz, const uint32_t* d_coords,
+                const uint32_t* order, uint64_t* const* d_pos, uint32_t* const* d_crd,
+                uint64_t* n_fibers, void* stream);
 uint64_t bucket_starts_device(Workspace& ws, uint32_t rank, uint64_t nnz,
                               const uint32_t* d_coords, const uint32_t* modes,
                               uint32_t n_modes, uint64_t* d_starts, void* stream);

@@ -701,3 +701,38 @@ def test_high_rank_against_oracle(ws):
             c, v, steps = ORC.transpose(t.dims, t.coords, t.values, target)
             assert same(out, c, v), (r, target)
             assert [(s.prefix_len, s.mode) for s in log] == [tuple(x) for x in steps]
+
+
+def _np_csf(c, r, order):
+    """CSF levels from numpy (rows sorted under `order`)."""
+    c = c.reshape(-1, r)
+    pos, crd, prev_starts = [], [], None
+    n = len(c)
+    for k in range(r):
+        key = c[:, list(order[: k + 1])]
+        head = np.ones(n, bool)
+        if n > 1:
+            head[1:] = (key[1:] != key[:-1]).any(1)
+        starts = np.flatnonzero(head)
+        crd.append(c[starts, order[k]])
+        if k == 0:
+            pos.append(np.array([0, len(starts)]))
+        else:
+            pos.append(np.searchsorted(starts, np.append(prev_starts, n)))
+        prev_starts = starts
+    return pos, crd
+
+
+def test_csf_levels_after_transpose(ws):
+    import torch
+    rng = np.random.default_rng(51)
+    for dims, n, target in (([30, 40, 50], 50_000, [2, 0, 1]), ([7, 9, 11, 13], 20_000, [3, 1, 0, 2]),
+                            ([5, 5], 0, [1, 0]), ([4, 4, 4], 200, [0, 1, 2])):
+        t = rand_tensor(rng, dims, n)
+        out = qd.transpose(t, target, ws=ws)
+        dc = torch.from_numpy(out.coords.view(np.int32)).cuda()
+        pos, crd = qd.csf_device(dc, len(dims), target, ws)
+        epos, ecrd = _np_csf(out.coords, len(dims), target)
+        for k in range(len(dims)):
+            assert np.array_equal(pos[k].cpu().numpy(), epos[k]), (dims, k)
+            assert np.array_equal(crd[k].cpu().numpy().view(np.uint32), ecrd[k]), (dims, k)
