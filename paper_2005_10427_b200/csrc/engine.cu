@@ -1663,6 +1663,23 @@ __global__ void k_mode_hist(const uint32_t* c, uint32_t rank, uint64_t nnz, uint
 // {key, start << 32 | len}, the records are sorted with the same engine, and
 // k_move_runs copies every run to its place.
 // ---------------------------------------------------------------------------
+// Run-length probe for the run-sort decision: heads of mode-`mode` runs in
+// 256 evenly spaced blocks of 1024 consecutive rows.
+constexpr uint32_t kProbeBlocks = 256, kProbeRows = 1024;
+__global__ void __launch_bounds__(kThreads) k_probe_runs(const uint32_t* c, uint32_t rank,
+                                                         uint64_t nnz, uint32_t mode,
+                                                         unsigned long long* heads) {
+  const unsigned long long span = nnz / kProbeBlocks;
+  const unsigned long long b0 = blockIdx.x * span;
+  uint32_t h = 0;
+  for (uint32_t i = 1 + threadIdx.x; i < kProbeRows; i += kThreads) {
+    const unsigned long long r = b0 + i;
+    if (r < nnz && c[r * rank + mode] != c[(r - 1) * rank + mode]) ++h;
+  }
+  for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xFFFFFFFFu, h, o);
+  if ((threadIdx.x & 31) == 0 && h) atomicAdd(heads, (unsigned long long)h);
+}
+
 __global__ void k_run_records(const uint32_t* c, uint32_t rank, uint32_t mode, uint32_t dim,
                               const unsigned long long* seg, uint64_t S, uint32_t* rkey,
                               double* rval, ErrBlock* err) {
@@ -1707,6 +1724,102 @@ __global__ void k_run_lens(const double* rval, uint64_t S, uint32_t* lens) {
   for (unsigned long long s = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; s < S;
        s += (unsigned long long)gridDim.x * blockDim.x)
     lens[s] = (uint32_t)((unsigned long long)__double_as_longlong(rval[s]) & 0xFFFFFFFFull);
+}
+
+// Run move v2: output tiles of kMoveTile rows; thread t resolves the source
+// row of the tile's rows [8t, 8t+8) (one binary search, then a forward walk
+// over the sorted run starts), then the tile's coordinate WORDS and values are
+// copied word-per-thread, so every warp access is 128 contiguous bytes on
+// the write side and contiguous within each run on the read side.
+constexpr uint32_t kMoveTile = 2048;
+constexpr int kMoveThreads = 256;
+constexpr int kMoveRowsPerThread = kMoveTile / kMoveThreads;
+
+// first run of every output tile (upper_bound(dsto, tile * kMoveTile) - 1)
+__global__ void k_tile_first_run(const unsigned long long* dsto, uint64_t S, uint64_t ntiles,
+                                 uint32_t* first) {
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t <= ntiles;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    const unsigned long long p = t * kMoveTile;
+    uint64_t l = 0, h = S;  // first run with dsto > p
+    while (l < h) {
+      const uint64_t m = (l + h) >> 1;
+      if (dsto[m] <= p) l = m + 1; else h = m;
+    }
+    first[t] = (uint32_t)(l ? l - 1 : 0);
+  }
+}
+
+template <int RT>
+__global__ void __launch_bounds__(kMoveThreads) k_move_runs2(
+    const uint32_t* __restrict__ in_c, const double* __restrict__ in_v, uint32_t* __restrict__ out_c,
+    double* __restrict__ out_v, uint32_t rank, uint64_t N, const double* rval,
+    const unsigned long long* dsto, uint64_t S, const uint32_t* first) {
+  __shared__ unsigned long long s_rdst[kMoveTile + 2];
+  __shared__ uint32_t s_rsrc[kMoveTile + 2];
+  __shared__ uint32_t s_rowsrc[kMoveTile];
+  const uint32_t R = RT ? RT : rank;
+  const unsigned long long p0 = (unsigned long long)blockIdx.x * kMoveTile;
+  const uint32_t n = (uint32_t)min((unsigned long long)kMoveTile, N - p0);
+  const uint32_t j0 = first[blockIdx.x];
+  const uint32_t nr = min((uint32_t)(first[blockIdx.x + 1] - j0 + 1), (uint32_t)(S - j0));
+  for (uint32_t k = threadIdx.x; k < nr; k += kMoveThreads) {
+    s_rdst[k] = dsto[j0 + k];
+    s_rsrc[k] = (uint32_t)((unsigned long long)__double_as_longlong(rval[j0 + k]) >> 32);
+  }
+  __syncthreads();
+  {
+    const uint32_t i0 = threadIdx.x * kMoveRowsPerThread;
+    if (i0 < n) {
+      const unsigned long long row0 = p0 + i0;
+      uint32_t l = 0, h = nr;  // last run start <= row0
+      while (h - l > 1) {
+        const uint32_t m = (l + h) >> 1;
+        if (s_rdst[m] <= row0) l = m; else h = m;
+      }
+#pragma unroll
+      for (int q = 0; q < kMoveRowsPerThread; ++q) {
+        const unsigned long long row = row0 + q;
+        while (l + 1 < nr && s_rdst[l + 1] <= row) ++l;
+        if (i0 + q < n) s_rowsrc[i0 + q] = s_rsrc[l] + (uint32_t)(row - s_rdst[l]);
+      }
+    }
+  }
+  __syncthreads();
+  // coordinates: the tile's words, several per thread in flight
+  const uint32_t nw = n * R;
+  const unsigned long long w0 = p0 * R;
+  constexpr int kB = 8;
+  for (uint32_t wb = threadIdx.x; wb < nw; wb += kB * kMoveThreads) {
+    uint32_t x[kB];
+#pragma unroll
+    for (int q = 0; q < kB; ++q) {
+      const uint32_t w = wb + q * kMoveThreads;
+      if (w < nw) {
+        const uint32_t i = w / R, m = w - i * R;
+        x[q] = __ldg(in_c + (unsigned long long)s_rowsrc[i] * R + m);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kB; ++q) {
+      const uint32_t w = wb + q * kMoveThreads;
+      if (w < nw) __stcs(out_c + w0 + w, x[q]);
+    }
+  }
+  // values
+  for (uint32_t ib = threadIdx.x; ib < n; ib += kB * kMoveThreads) {
+    double v[kB];
+#pragma unroll
+    for (int q = 0; q < kB; ++q) {
+      const uint32_t i = ib + q * kMoveThreads;
+      if (i < n) v[q] = __ldg(in_v + s_rowsrc[i]);
+    }
+#pragma unroll
+    for (int q = 0; q < kB; ++q) {
+      const uint32_t i = ib + q * kMoveThreads;
+      if (i < n) __stcs(out_v + p0 + i, v[q]);
+    }
+  }
 }
 
 constexpr uint32_t kMoveRows = 4096;  // output rows per k_move_runs CTA
@@ -2550,10 +2663,22 @@ bool try_run_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const doub
   k_run_lens<<<grid, kThreads, 0, c.st>>>(rv1, S, lens);
   c.launched(kSegK);
   scan_exclusive(c, lens, S, dsto, tot);
-  const size_t smem = (size_t)(kMoveRows + 1) * 16;
+  const uint64_t ntiles = (N + kMoveTile - 1) / kMoveTile;
+  auto* first = ws.get<uint32_t>("run_tile_first", ntiles + 1);
   c.pre();
-  k_move_runs<<<(uint32_t)((N + kMoveRows - 1) / kMoveRows), kSortThreads, smem, c.st>>>(
-      src_c, src_v, dst_c, dst_v, R, N, rv1, dsto, S);
+  k_tile_first_run<<<(uint32_t)std::min<uint64_t>((ntiles + kThreads) / kThreads, ws.num_sms * 8),
+                     kThreads, 0, c.st>>>(dsto, S, ntiles, first);
+  c.launched(kSegK);
+  c.pre();
+  if (R == 3)
+    k_move_runs2<3><<<(uint32_t)ntiles, kMoveThreads, 0, c.st>>>(src_c, src_v, dst_c, dst_v, R, N,
+                                                                 rv1, dsto, S, first);
+  else if (R == 4)
+    k_move_runs2<4><<<(uint32_t)ntiles, kMoveThreads, 0, c.st>>>(src_c, src_v, dst_c, dst_v, R, N,
+                                                                 rv1, dsto, S, first);
+  else
+    k_move_runs2<0><<<(uint32_t)ntiles, kMoveThreads, 0, c.st>>>(src_c, src_v, dst_c, dst_v, R, N,
+                                                                 rv1, dsto, S, first);
   c.launched(kSweep);
   return true;
 }
@@ -2567,9 +2692,11 @@ void exec_group(Ctx& c, const TensorView& t, const uint32_t* src_c, const double
   Workspace& ws = c.ws;
   const uint64_t N = t.nnz;
   const uint32_t R = t.rank;
-  // Off by default: the move of short runs (gather of ~6-row runs) does not
-  // yet beat two chunk passes on the c2 data; QD_RUN_SORT=1 enables it.
-  const bool disabled = getenv("QD_RUN_SORT") == nullptr;
+  // QD_RUN_SORT: unset = decide by the cost model below, 0 = never, 1 = always
+  // (when a candidate's runs are long enough)
+  const char* rs_env = getenv("QD_RUN_SORT");
+  const int rs_mode = rs_env ? atoi(rs_env) : -1;
+  const bool disabled = rs_mode == 0;
   uint64_t min_rows = kRunSortMinRows;
   if (const char* e = getenv("QD_RUN_SORT_MIN_ROWS")) min_rows = strtoull(e, nullptr, 10);
   // candidates: the key mode is not the last mode (its runs would be single
@@ -2581,11 +2708,39 @@ void exec_group(Ctx& c, const TensorView& t, const uint32_t* src_c, const double
     return true;
   };
   const size_t m = g.keys.size();
+  // Cost model (per row / per run, measured on B200 with c2/c3 data): a
+  // chunked digit pass (histogram, scan, scatter) costs ~10.5 ps per row when
+  // the coordinates pack into 64 bits (16-byte rows), ~14.5 ps for wider
+  // rank-3 rows and ~16 ps for wider rank >= 4 rows; a run sort pays ~2.3 ps
+  // per row for run discovery plus ~13.5 ps (rank 3) / 17 ps (rank >= 4)
+  // per row for the run move, and ~(20 + 10 x its digit passes) ps per run.
+  auto worth_it = [&](uint32_t k, const std::vector<uint32_t>& rest_keys) -> bool {
+    if (rs_mode == 1) return true;
+    uint32_t all_bits = 0, key_bits = ceil_log2(t.dims[k]), rest_bits = 0;
+    for (uint32_t q = 0; q < R; ++q) all_bits += ceil_log2(t.dims[q]);
+    for (uint32_t q : rest_keys) rest_bits += ceil_log2(t.dims[q]);
+    const double c_row = all_bits <= 64 ? 10.5 : (R <= 3 ? 14.5 : 16.0);
+    const double c_move = (R <= 3 ? 13.5 : 17.0) + 2.3;
+    const double chunked = (double)((key_bits + rest_bits + 7) / 8) * N * c_row;
+    const double rest = rest_keys.empty() ? 0.0 : (double)((rest_bits + 7) / 8) * N * c_row;
+    // expected runs from a probe of 256 x 1024 rows
+    auto* heads = ws.get<unsigned long long>("probe_heads", 1);
+    QD_CUDA(cudaMemsetAsync(heads, 0, 8, c.st));
+    c.pre();
+    k_probe_runs<<<kProbeBlocks, kThreads, 0, c.st>>>(src_c, R, N, k, heads);
+    c.launched(kSegK);
+    QD_CUDA(cudaMemcpyAsync(ws.h_small, heads, 8, cudaMemcpyDeviceToHost, c.st));
+    QD_CUDA(cudaStreamSynchronize(c.st));
+    const double frac = ((double)ws.h_small[0] + kProbeBlocks) / ((double)kProbeBlocks * kProbeRows);
+    const double S_est = std::min(1.0, frac) * (double)N;
+    const double run = N * c_move + S_est * (20.0 + 10.0 * ((key_bits + 7) / 8)) + rest;
+    return run < 0.9 * chunked;
+  };
   if (!disabled && g.check_range && g.prefix.empty() && m >= 1 && N >= min_rows) {
     auto* xc = m >= 2 ? ws.get<uint32_t>("rowsC_c", N * R) : nullptr;
     auto* xv = m >= 2 ? ws.get<double>("rowsC_v", N) : nullptr;
     const uint32_t k1 = g.keys[0], km = g.keys[m - 1];
-    if (candidate(k1)) {
+    if (candidate(k1) && worth_it(k1, std::vector<uint32_t>(g.keys.begin() + 1, g.keys.end()))) {
       if (try_run_sort(c, t, src_c, src_v, m == 1 ? dst_c : xc, m == 1 ? dst_v : xv, k1)) {
         if (m >= 2) {
           Group rest;
@@ -2596,7 +2751,8 @@ void exec_group(Ctx& c, const TensorView& t, const uint32_t* src_c, const double
         }
         return;
       }
-    } else if (m >= 2 && candidate(km)) {
+    } else if (m >= 2 && candidate(km) &&
+               worth_it(km, std::vector<uint32_t>(g.keys.begin(), g.keys.end() - 1))) {
       if (try_run_sort(c, t, src_c, src_v, xc, xv, km)) {
         Group rest;
         rest.prefix = g.prefix;
