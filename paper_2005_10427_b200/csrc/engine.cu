@@ -1661,7 +1661,7 @@ __global__ void k_mode_hist(const uint32_t* c, uint32_t rank, uint64_t nnz, uint
 // (prefix, key) — the input's existing order (e.g. (i0,i1) fibers when sorting
 // by i1) — a stable sort moves each run as a block.  Runs become records
 // {key, start << 32 | len}, the records are sorted with the same engine, and
-// k_move_runs copies every run to its place.
+// k_move_runs2 copies every run to its place.
 // ---------------------------------------------------------------------------
 // Run-length probe for the run-sort decision: heads of mode-`mode` runs in
 // 256 evenly spaced blocks of 1024 consecutive rows.
@@ -1822,105 +1822,6 @@ __global__ void __launch_bounds__(kMoveThreads) k_move_runs2(
   }
 }
 
-constexpr uint32_t kMoveRows = 4096;  // output rows per k_move_runs CTA
-
-// Output rows [p0, p0 + kMoveRows): each comes from the sorted run that
-// covers it (dsto = run output offsets, rval = {start << 32 | len}).
-__global__ void __launch_bounds__(kSortThreads, 1) k_move_runs(
-    const uint32_t* in_c, const double* in_v, uint32_t* out_c, double* out_v, uint32_t rank,
-    uint64_t N, const double* rval, const unsigned long long* dsto, uint64_t S) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  unsigned long long* s_dst = reinterpret_cast<unsigned long long*>(smem);
-  unsigned long long* s_src = s_dst + kMoveRows + 1;
-  __shared__ unsigned long long s_j0;
-  __shared__ uint32_t s_nr;
-  const unsigned long long p0 = (unsigned long long)blockIdx.x * kMoveRows;
-  const unsigned long long p1 = min((unsigned long long)N, p0 + kMoveRows);
-  if (threadIdx.x == 0) {  // last run starting at or before p0
-    uint64_t l = 0, h = S;
-    while (h - l > 1) {
-      const uint64_t m = (l + h) >> 1;
-      if (dsto[m] <= p0) l = m; else h = m;
-    }
-    s_j0 = l;
-    s_nr = 0xFFFFFFFFu;
-  }
-  __syncthreads();
-  const uint64_t j0 = s_j0;
-  for (uint32_t k = threadIdx.x; k <= kMoveRows; k += blockDim.x) {
-    const uint64_t j = j0 + k;
-    if (j < S && (k == 0 || dsto[j] < p1)) {
-      s_dst[k] = dsto[j];
-      s_src[k] = (unsigned long long)__double_as_longlong(rval[j]) >> 32;
-    } else {
-      atomicMin(&s_nr, k);
-    }
-  }
-  __syncthreads();
-  const uint32_t nr = min(s_nr, kMoveRows + 1);
-  // every thread resolves its kMoveRows/blockDim rows together (independent
-  // binary searches interleaved), then issues all their loads, then stores
-  constexpr int K = kMoveRows / kSortThreads;
-  unsigned long long src[K];
-  uint32_t lo[K], hi[K];
-#pragma unroll
-  for (int q = 0; q < K; ++q) {
-    lo[q] = 0;
-    hi[q] = nr;
-  }
-  for (int it = 0; it < 13; ++it) {  // 2^13 > kMoveRows + 1 entries
-#pragma unroll
-    for (int q = 0; q < K; ++q) {
-      const unsigned long long p = p0 + threadIdx.x + q * kSortThreads;
-      if (hi[q] - lo[q] > 1) {
-        const uint32_t m = (lo[q] + hi[q]) >> 1;
-        if (s_dst[m] <= p) lo[q] = m; else hi[q] = m;
-      }
-    }
-  }
-#pragma unroll
-  for (int q = 0; q < K; ++q) {
-    const unsigned long long p = p0 + threadIdx.x + q * kSortThreads;
-    src[q] = s_src[lo[q]] + (p - s_dst[lo[q]]);
-  }
-  if (rank == 3) {
-    uint32_t x[K][3];
-    double v[K];
-#pragma unroll
-    for (int q = 0; q < K; ++q) {
-      const unsigned long long p = p0 + threadIdx.x + q * kSortThreads;
-      if (p < p1) {
-        const uint32_t* ic = in_c + src[q] * 3;
-        x[q][0] = __ldg(ic);
-        x[q][1] = __ldg(ic + 1);
-        x[q][2] = __ldg(ic + 2);
-        v[q] = __ldg(in_v + src[q]);
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < K; ++q) {
-      const unsigned long long p = p0 + threadIdx.x + q * kSortThreads;
-      if (p < p1) {
-        uint32_t* oc = out_c + p * 3;
-        __stcs(oc, x[q][0]);
-        __stcs(oc + 1, x[q][1]);
-        __stcs(oc + 2, x[q][2]);
-        __stcs(out_v + p, v[q]);
-      }
-    }
-    return;
-  }
-#pragma unroll
-  for (int q = 0; q < K; ++q) {
-    const unsigned long long p = p0 + threadIdx.x + q * kSortThreads;
-    if (p < p1) {
-      const uint32_t* ic = in_c + src[q] * rank;
-      uint32_t* oc = out_c + p * rank;
-      for (uint32_t m = 0; m < rank; ++m) __stcs(oc + m, __ldg(ic + m));
-      __stcs(out_v + p, __ldg(in_v + src[q]));
-    }
-  }
-}
 
 // ---------------------------------------------------------------------------
 // host side
@@ -2080,7 +1981,6 @@ Workspace* workspace_create(int device) {
           if (ScatterFn f = scatter_kernel(rt, dm, in, out))
             allow_smem(reinterpret_cast<const void*>(f));
   allow_smem(reinterpret_cast<const void*>(k_local));
-  allow_smem(reinterpret_cast<const void*>(k_move_runs));
   ws->smem_optin = optin - 1024;  // dynamic budget below the static usage
   return ws;
 }
