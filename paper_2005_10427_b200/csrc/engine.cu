@@ -1786,10 +1786,28 @@ __global__ void __launch_bounds__(kMoveThreads) k_move_runs2(
     }
   }
   __syncthreads();
-  // coordinates: the tile's words, several per thread in flight
-  const uint32_t nw = n * R;
-  const unsigned long long w0 = p0 * R;
   constexpr int kB = 8;
+  if (RT == 4) {
+    // rank 4: a row's coordinates are one aligned 16-byte vector
+    const uint4* ic4 = reinterpret_cast<const uint4*>(in_c);
+    uint4* oc4 = reinterpret_cast<uint4*>(out_c) + p0;
+    for (uint32_t ib = threadIdx.x; ib < n; ib += kB * kMoveThreads) {
+      uint4 x[kB];
+#pragma unroll
+      for (int q = 0; q < kB; ++q) {
+        const uint32_t i = ib + q * kMoveThreads;
+        if (i < n) x[q] = __ldg(ic4 + s_rowsrc[i]);
+      }
+#pragma unroll
+      for (int q = 0; q < kB; ++q) {
+        const uint32_t i = ib + q * kMoveThreads;
+        if (i < n) __stcs(oc4 + i, x[q]);
+      }
+    }
+  }
+  // coordinates: the tile's words, several per thread in flight
+  const uint32_t nw = RT == 4 ? 0u : n * R;
+  const unsigned long long w0 = p0 * R;
   for (uint32_t wb = threadIdx.x; wb < nw; wb += kB * kMoveThreads) {
     uint32_t x[kB];
 #pragma unroll
