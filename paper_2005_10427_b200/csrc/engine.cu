@@ -154,10 +154,62 @@ struct RowsOut {
 };
 
 // Packed coordinate layout: mode m at bits [off[m], off[m] + width[m]).
+// Packed coordinate layout: key mode m at bits [off[m], off[m] + width[m])
+// (the group's combined key in the low key_bits), the other modes above it
+// either as bit fields too or, when those would overflow 64 bits
+// (`mixed`), as one mixed-radix number hi = ((c_a * d_b + c_b) * d_c + c_c)
+// ... over their dimensions, stored at bit key_bits.  lim[m] is the bound
+// a coordinate must respect to pack losslessly (2^width or the dimension).
 struct PackSpec {
   uint32_t rank;
   uint8_t off[kMaxKeys], width[kMaxKeys];
+  uint32_t lim[kMaxKeys];
+  uint32_t mixed, key_bits, nk_n;
+  uint8_t nk_mode[kMaxKeys];
+  uint32_t nk_dim[kMaxKeys];
+  double nk_rcp[kMaxKeys];  // 1 / nk_dim
 };
+
+// x / d for d < 2^32: a double multiply by the precomputed reciprocal when
+// x < 2^53 (then exact after a short fix-up), else the 64-bit hardware path
+__device__ __forceinline__ unsigned long long div_u64_u32(unsigned long long x, uint32_t d,
+                                                          double rcp) {
+  if (x < (1ull << 53)) {
+    // |x * rcp - x / d| < 1 for x < 2^53: one correction either way
+    unsigned long long q = (unsigned long long)((double)x * rcp);
+    if (q * d > x) --q;
+    else if ((q + 1) * d <= x) ++q;
+    return q;
+  }
+  return x / d;
+}
+template <class F>
+__device__ __forceinline__ unsigned long long pack_coords(const PackSpec& p, uint32_t R, F coord) {
+  unsigned long long pk = 0;
+  for (uint32_t m = 0; m < R; ++m)
+    if (p.width[m]) pk |= (unsigned long long)coord(m) << p.off[m];
+  if (p.mixed) {
+    unsigned long long hi = 0;
+    for (uint32_t j = 0; j < p.nk_n; ++j) hi = hi * p.nk_dim[j] + coord(p.nk_mode[j]);
+    pk |= hi << p.key_bits;
+  }
+  return pk;
+}
+// writes the R coordinates of packed word x through put(m, value)
+template <class P>
+__device__ __forceinline__ void unpack_coords(const PackSpec& p, uint32_t R, unsigned long long x,
+                                              P put) {
+  for (uint32_t m = 0; m < R; ++m)
+    if (p.width[m]) put(m, (uint32_t)(x >> p.off[m]) & (uint32_t)((1ull << p.width[m]) - 1ull));
+  if (p.mixed) {
+    unsigned long long hi = p.key_bits < 64 ? x >> p.key_bits : 0ull;
+    for (int j = (int)p.nk_n - 1; j >= 0; --j) {
+      const unsigned long long q = div_u64_u32(hi, p.nk_dim[j], p.nk_rcp[j]);
+      put(p.nk_mode[j], (uint32_t)(hi - q * p.nk_dim[j]));
+      hi = q;
+    }
+  }
+}
 
 struct ChunkHistArgs {
   Rows in;
@@ -636,7 +688,7 @@ __global__ void __launch_bounds__(kThreads) k_chunk_hist(ChunkHistArgs a) {
         if (a.do_check)
           for (uint32_t k = 0; k < a.key.n; ++k)
             if (a.key.mode[k] == m) lim[m] = a.key.dim[k];
-        if (a.check_pack && a.pack.width[m] < 32) lim[m] = min(lim[m], 1u << a.pack.width[m]);
+        if (a.check_pack) lim[m] = min(lim[m], a.pack.lim[m]);
       }
       uint32_t* wh = s_h + w * kBins;
       auto digit3 = [&](uint32_t c0, uint32_t c1, uint32_t c2) {
@@ -653,7 +705,7 @@ __global__ void __launch_bounds__(kThreads) k_chunk_hist(ChunkHistArgs a) {
           // rare: the exact checks (range: first (row, mode); pack: flag)
           if (a.do_check) check_row(a.in.c + grow * 3, a.key, grow, a.err);
           if (a.check_pack &&
-              ((c0 >> a.pack.width[0]) | (c1 >> a.pack.width[1]) | (c2 >> a.pack.width[2])))
+              (c0 >= a.pack.lim[0] || c1 >= a.pack.lim[1] || c2 >= a.pack.lim[2]))
             atomicOr(&a.err->flags, 4u);
         }
       };
@@ -731,7 +783,7 @@ __global__ void __launch_bounds__(kThreads) k_chunk_hist(ChunkHistArgs a) {
           if (a.do_check) check_row(row, a.key, r, a.err);
           if (a.check_pack) {
             uint32_t bad = 0;
-            for (uint32_t m = 0; m < R; ++m) bad |= a.pack.width[m] >= 32 ? 0u : (row[m] >> a.pack.width[m]);
+            for (uint32_t m = 0; m < R; ++m) bad |= row[m] >= a.pack.lim[m];
             if (bad) atomicOr(&a.err->flags, 4u);
           }
           auto get = [&](uint32_t m) { return __ldg(row + m); };
@@ -795,7 +847,7 @@ struct ScatterLayout {
 // RT: compile-time rank (0 = runtime); IN/OUT: row formats (kAoS/kSoA/kPK);
 // DM: digit of an AoS/SoA row inside 1 or 2 key fields (0 = general).
 // ---------------------------------------------------------------------------
-template <int RT, int IN, int OUT, int DM>
+template <int RT, int IN, int OUT, int DM, int MX = 0>
 __global__ void __launch_bounds__(kSortThreads, 1024 / kSortThreads) k_scatter(ScatterArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   const uint32_t R = RT ? RT : a.rank;
@@ -1099,7 +1151,33 @@ __global__ void __launch_bounds__(kSortThreads, 1024 / kSortThreads) k_scatter(S
           if (a.next_dig) __stcs(a.next_dig + dst, (uint8_t)((row.x >> a.nd_shift) & a.nd_mask));
         } else {  // unpack into AoS
           uint32_t* o = a.out.c + dst * R;
-          if (RT) {
+          if (MX && RT) {
+            // key fields, then the mixed-radix part from its last mode down;
+            // unrolled with static indices so cv stays in registers
+            uint32_t cv[RT > 0 ? RT : 1];
+#pragma unroll
+            for (int m = 0; m < (RT > 0 ? RT : 1); ++m)
+              cv[m] = (uint32_t)(row.x >> a.pack.off[m]) &
+                      (uint32_t)((1ull << a.pack.width[m]) - 1ull);
+            unsigned long long hi = row.x >> a.pack.key_bits;
+#pragma unroll
+            for (int jj = (RT > 0 ? RT : 1) - 1; jj >= 0; --jj) {
+              if ((uint32_t)jj < a.pack.nk_n) {
+                const uint32_t d = a.pack.nk_dim[jj];
+                const unsigned long long q = div_u64_u32(hi, d, a.pack.nk_rcp[jj]);
+                const uint32_t v = (uint32_t)(hi - q * d);
+                const uint32_t mj = a.pack.nk_mode[jj];
+#pragma unroll
+                for (int m = 0; m < (RT > 0 ? RT : 1); ++m)
+                  if (mj == (uint32_t)m) cv[m] = v;
+                hi = q;
+              }
+            }
+#pragma unroll
+            for (int m = 0; m < (RT > 0 ? RT : 1); ++m) __stcs(o + m, cv[m]);
+          } else if (MX) {
+            unpack_coords(a.pack, R, row.x, [&](uint32_t m, uint32_t v) { __stcs(o + m, v); });
+          } else if (RT) {
 #pragma unroll
             for (int m = 0; m < (RT > 0 ? RT : 1); ++m)
               __stcs(o + m, (uint32_t)(row.x >> a.pack.off[m]) &
@@ -1116,7 +1194,29 @@ __global__ void __launch_bounds__(kSortThreads, 1024 / kSortThreads) k_scatter(S
       const double v = *reinterpret_cast<const double*>(scb + vbase + i * 8u);
       if (OUT == kPK) {  // pack (first pass)
         unsigned long long pk = 0;
-        if (RT) {
+        if (MX && RT) {
+          uint32_t cv[RT > 0 ? RT : 1];
+#pragma unroll
+          for (int m = 0; m < (RT > 0 ? RT : 1); ++m) {
+            cv[m] = *reinterpret_cast<const uint32_t*>(scb + cb[m] + i * rstride);
+            if (a.pack.width[m]) pk |= (unsigned long long)cv[m] << a.pack.off[m];
+          }
+          // fully unrolled so cv stays in registers (static indices only)
+          unsigned long long hi = 0;
+#pragma unroll
+          for (int j = 0; j < (RT > 0 ? RT : 1); ++j) {
+            if ((uint32_t)j < a.pack.nk_n) {
+              const uint32_t mj = a.pack.nk_mode[j];
+              uint32_t x = cv[0];
+#pragma unroll
+              for (int m = 1; m < (RT > 0 ? RT : 1); ++m) x = mj == (uint32_t)m ? cv[m] : x;
+              hi = hi * a.pack.nk_dim[j] + x;
+            }
+          }
+          pk |= hi << a.pack.key_bits;
+        } else if (MX) {
+          pk = pack_coords(a.pack, R, [&](uint32_t m) { return coord(i, m); });
+        } else if (RT) {
 #pragma unroll
           for (int m = 0; m < (RT > 0 ? RT : 1); ++m)
             pk |= (unsigned long long)*reinterpret_cast<const uint32_t*>(scb + cb[m] + i * rstride)
@@ -1946,29 +2046,34 @@ using ScatterFn = void (*)(ScatterArgs);
 // (in, out) format pairs used: AoS->AoS, AoS->SoA, SoA->SoA, SoA->AoS (any
 // group), AoS->PK, PK->PK, PK->AoS (packed groups)
 template <int RT, int DM>
-ScatterFn scatter_kernel_fmt(int in, int out) {
+ScatterFn scatter_kernel_fmt(int in, int out, int mx) {
   if (in == kAoS && out == kAoS) return k_scatter<RT, kAoS, kAoS, DM>;
   if (in == kAoS && out == kSoA) return k_scatter<RT, kAoS, kSoA, DM>;
   if (in == kSoA && out == kSoA) return k_scatter<RT, kSoA, kSoA, DM>;
   if (in == kSoA && out == kAoS) return k_scatter<RT, kSoA, kAoS, DM>;
-  if (in == kAoS && out == kPK) return k_scatter<RT, kAoS, kPK, DM>;
+  if (in == kAoS && out == kPK)
+    return mx ? k_scatter<RT, kAoS, kPK, DM, 1> : k_scatter<RT, kAoS, kPK, DM>;
   return nullptr;
 }
 template <int RT>
-ScatterFn scatter_kernel_rt(int dm, int in, int out) {
-  if (in == kPK) return out == kPK ? k_scatter<RT, kPK, kPK, 0> : k_scatter<RT, kPK, kAoS, 0>;
+ScatterFn scatter_kernel_rt(int dm, int in, int out, int mx) {
+  if (in == kPK) {
+    if (out == kPK) return k_scatter<RT, kPK, kPK, 0>;
+    return mx ? k_scatter<RT, kPK, kAoS, 0, 1> : k_scatter<RT, kPK, kAoS, 0>;
+  }
   switch (dm) {
-    case 1: return scatter_kernel_fmt<RT, 1>(in, out);
-    case 2: return scatter_kernel_fmt<RT, 2>(in, out);
-    default: return scatter_kernel_fmt<RT, 0>(in, out);
+    case 1: return scatter_kernel_fmt<RT, 1>(in, out, mx);
+    case 2: return scatter_kernel_fmt<RT, 2>(in, out, mx);
+    default: return scatter_kernel_fmt<RT, 0>(in, out, mx);
   }
 }
-// rt: compile-time rank (3, 4 or 0 = runtime); dm: digit mode; in/out formats
-ScatterFn scatter_kernel(int rt, int dm, int in, int out) {
+// rt: compile-time rank (3, 4 or 0 = runtime); dm: digit mode; in/out
+// formats; mx: mixed-radix packed rows (PackSpec::mixed)
+ScatterFn scatter_kernel(int rt, int dm, int in, int out, int mx = 0) {
   switch (rt) {
-    case 3: return scatter_kernel_rt<3>(dm, in, out);
-    case 4: return scatter_kernel_rt<4>(dm, in, out);
-    default: return scatter_kernel_rt<0>(dm, in, out);
+    case 3: return scatter_kernel_rt<3>(dm, in, out, mx);
+    case 4: return scatter_kernel_rt<4>(dm, in, out, mx);
+    default: return scatter_kernel_rt<0>(dm, in, out, mx);
   }
 }
 
@@ -1996,8 +2101,9 @@ Workspace* workspace_create(int device) {
     for (int dm = 0; dm < 3; ++dm)
       for (int in = 0; in < 3; ++in)
         for (int out = 0; out < 3; ++out)
-          if (ScatterFn f = scatter_kernel(rt, dm, in, out))
-            allow_smem(reinterpret_cast<const void*>(f));
+          for (int mx = 0; mx < 2; ++mx)
+            if (ScatterFn f = scatter_kernel(rt, dm, in, out, mx))
+              allow_smem(reinterpret_cast<const void*>(f));
   allow_smem(reinterpret_cast<const void*>(k_local));
   ws->smem_optin = optin - 1024;  // dynamic budget below the static usage
   return ws;
@@ -2254,6 +2360,61 @@ DigitSpec make_digit(const KeySpec& k, uint32_t lo, uint32_t hi) {
   return d;
 }
 
+// Packed row layout of a group (PackSpec): key fields at their key offsets,
+// the other modes as bit fields above when everything fits 64 bits, else as
+// one mixed-radix number when THAT fits; false if neither does.
+bool make_pack(const KeySpec& key, uint32_t R, const uint32_t* dims, PackSpec* out) {
+  PackSpec p{};
+  p.rank = R;
+  p.key_bits = key.total_bits;
+  for (uint32_t m = 0; m < R; ++m) p.lim[m] = 0xFFFFFFFFu;
+  std::vector<uint32_t> nonkey;
+  for (uint32_t m = 0; m < R; ++m) {
+    bool is_key = false;
+    for (uint32_t k = 0; k < key.n; ++k) is_key |= key.mode[k] == m;
+    if (!is_key) nonkey.push_back(m);
+  }
+  for (uint32_t k = 0; k < key.n; ++k) {
+    p.off[key.mode[k]] = (uint8_t)key.off[k];
+    p.width[key.mode[k]] = key.width[k];
+    if (key.width[k] < 32) p.lim[key.mode[k]] = 1u << key.width[k];
+  }
+  uint32_t bits = key.total_bits;
+  for (uint32_t m : nonkey) bits += ceil_log2(dims[m]);
+  if (bits <= 64) {
+    uint32_t o = key.total_bits;
+    for (uint32_t m : nonkey) {
+      const uint32_t w = ceil_log2(dims[m]);
+      p.off[m] = (uint8_t)o;
+      p.width[m] = (uint8_t)w;
+      p.lim[m] = w < 32 ? (1u << w) : 0xFFFFFFFFu;
+      o += w;
+    }
+    *out = p;
+    return true;
+  }
+  // mixed radix: the product of the non-key dimensions must fit the bits
+  // left above the key
+  if (key.total_bits >= 64) return false;
+  const unsigned __int128 room = (unsigned __int128)1 << (64 - key.total_bits);
+  unsigned __int128 prod = 1;
+  for (uint32_t m : nonkey) {
+    prod *= dims[m];
+    if (prod > room) return false;
+  }
+  p.mixed = 1;
+  p.nk_n = (uint32_t)nonkey.size();
+  for (uint32_t j = 0; j < p.nk_n; ++j) {
+    p.nk_mode[j] = (uint8_t)nonkey[j];
+    p.nk_dim[j] = dims[nonkey[j]];
+    p.nk_rcp[j] = 1.0 / (double)dims[nonkey[j]];
+    p.lim[nonkey[j]] = dims[nonkey[j]];
+    p.width[nonkey[j]] = 0;
+  }
+  *out = p;
+  return true;
+}
+
 // Tiles per chunk: chunks are statically dealt to the resident CTAs, so aim
 // for ~8 chunks per CTA (good balance) but at most kChunkTiles tiles each.
 uint32_t chunk_tiles(const Workspace& ws, uint64_t rows, uint32_t T) {
@@ -2333,7 +2494,7 @@ void run_pass(Ctx& c, uint32_t R, uint64_t N, uint32_t T, Rows in, RowsOut out,
   const size_t smem = ScatterLayout(T, R, in.fmt).total;
   const int rt = (R == 3 || R == 4) ? (int)R : 0;
   const int dm = dig.lookup ? 0 : (dig.n == 1 ? 1 : (dig.n == 2 ? 2 : 0));
-  ScatterFn fn = scatter_kernel(rt, dm, in.fmt, out.fmt);
+  ScatterFn fn = scatter_kernel(rt, dm, in.fmt, out.fmt, pack && pack->mixed ? 1 : 0);
   if (!fn) throw Error(QD_CUDA_ERROR, "no scatter kernel for this row format pair");
   int per_sm = 0;
   QD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kSortThreads, smem));
@@ -2481,24 +2642,11 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
     // possible for modes the plan never range-checks) is flagged by the
     // first histogram and the whole call is redone unpacked (run_groups).
     PackSpec pack{};
-    uint32_t pbits = key.total_bits;
     bool packed = ws.allow_pack && g.check_range && D > 1;
-    if (packed) {
-      pack.rank = R;
-      for (uint32_t k = 0; k < key.n; ++k) {
-        pack.off[key.mode[k]] = (uint8_t)key.off[k];
-        pack.width[key.mode[k]] = key.width[k];
-      }
-      for (uint32_t m = 0; m < R && packed; ++m) {
-        bool is_key = false;
-        for (uint32_t k = 0; k < key.n; ++k) is_key |= key.mode[k] == m;
-        if (is_key) continue;
-        const uint32_t wdt = ceil_log2(t.dims[m]);
-        pack.off[m] = (uint8_t)pbits;
-        pack.width[m] = (uint8_t)wdt;
-        pbits += wdt;
-      }
-      packed = pbits <= 64;
+    if (packed) packed = make_pack(key, R, t.dims, &pack);
+    if (!packed && D > 1 && !tmp_c) {
+      tmp_c = ws.get<uint32_t>("rowsA_c", N * R);
+      tmp_v = ws.get<double>("rowsA_v", N);
     }
     // packed intermediates ping-pong in workspace buffers of 16 bytes/row
     uint32_t* pk[2] = {nullptr, nullptr};
@@ -2741,8 +2889,10 @@ static void run_groups_once(Workspace& ws, const TensorView& t, const uint32_t* 
       QD_CUDA(cudaMemcpyAsync(d_v_out, d_v_in, N * 8, cudaMemcpyDeviceToDevice, c.st));
     }
   } else {
-    uint32_t* Ac = ws.get<uint32_t>("rowsA_c", N * R);
-    double* Av = ws.get<double>("rowsA_v", N);
+    // one group: its scratch rows are allocated by segmented_sort only if an
+    // unpacked multi-pass sort needs them (packed passes use pkA/pkB)
+    uint32_t* Ac = G >= 2 ? ws.get<uint32_t>("rowsA_c", N * R) : nullptr;
+    double* Av = G >= 2 ? ws.get<double>("rowsA_v", N) : nullptr;
     uint32_t* Bc = G >= 2 ? ws.get<uint32_t>("rowsB_c", N * R) : nullptr;
     double* Bv = G >= 2 ? ws.get<double>("rowsB_v", N) : nullptr;
     const uint32_t* sc = d_c_in;

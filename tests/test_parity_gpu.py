@@ -736,3 +736,24 @@ def test_csf_levels_after_transpose(ws):
         for k in range(len(dims)):
             assert np.array_equal(pos[k].cpu().numpy(), epos[k]), (dims, k)
             assert np.array_equal(crd[k].cpu().numpy().view(np.uint32), ecrd[k]), (dims, k)
+
+
+def test_mixed_radix_packing(ws):
+    """Coordinates whose bit widths exceed 64 (23+21+21 = 65, config 5's
+    shape) but whose non-key modes fit as one mixed-radix number: packed
+    16-byte rows with a mixed-radix high part; unchecked out-of-range
+    non-key coordinates fall back to unpacked rows."""
+    rng = np.random.default_rng(61)
+    dims = [4821207, 1774269, 1805187]
+    t = rand_tensor(rng, dims, 300_000)
+    for target in ([1, 0, 2], [0, 2, 1], [2, 0, 1], [1, 2, 0]):
+        out = qd.transpose(t, target, ws=ws)
+        c, v, _ = ORC.transpose(t.dims, t.coords, t.values, target)
+        assert same(out, c, v), target
+    # mode 0 is never a key of (1,0,2): a coordinate beyond its dimension is
+    # moved untouched (not range-checked), so the pack must not wrap it
+    u = t.copy()
+    u.coords[3 * 1000] = dims[0] + 12345
+    out = qd.transpose(u, [1, 0, 2], ws=ws)
+    c, v = _np_transpose(dims, u.coords, u.values, [1, 0, 2])
+    assert same(out, c, v)
