@@ -675,6 +675,47 @@ __global__ void __launch_bounds__(kThreads) k_chunk_hist(ChunkHistArgs a) {
       __syncthreads();
       goto flush;
     }
+    if (a.in.fmt == kAoS && R == 4 && fast_dig && ((uintptr_t)a.in.c & 15u) == 0) {
+      // AoS rank-4 rows are aligned 16-byte vectors: one load per row, two
+      // rows in flight per thread, range + pack checks from the registers
+      uint32_t lim[4];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        lim[m] = 0xFFFFFFFFu;
+        if (a.do_check)
+          for (uint32_t k = 0; k < a.key.n; ++k)
+            if (a.key.mode[k] == m) lim[m] = a.key.dim[k];
+        if (a.check_pack) lim[m] = min(lim[m], a.pack.lim[m]);
+      }
+      uint32_t* wh = s_h + w * kBins;
+      const uint4* rows4 = reinterpret_cast<const uint4*>(a.in.c) + cd.row_begin;
+      auto sel = [&](const uint4& x, uint32_t m) {
+        return m == 0 ? x.x : (m == 1 ? x.y : (m == 2 ? x.z : x.w));
+      };
+      for (uint32_t i0 = threadIdx.x; i0 < cd.len; i0 += 2 * kThreads) {
+        uint4 x[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+          if (i0 + u * kThreads < cd.len) x[u] = __ldcs(rows4 + i0 + u * kThreads);
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const uint32_t i = i0 + u * kThreads;
+          if (i >= cd.len) break;
+          if (x[u].x >= lim[0] || x[u].y >= lim[1] || x[u].z >= lim[2] || x[u].w >= lim[3]) {
+            const unsigned long long gr = cd.row_begin + i;
+            if (a.do_check) check_row(a.in.c + gr * 4, a.key, gr, a.err);
+            if (a.check_pack && (x[u].x >= a.pack.lim[0] || x[u].y >= a.pack.lim[1] ||
+                                 x[u].z >= a.pack.lim[2] || x[u].w >= a.pack.lim[3]))
+              atomicOr(&a.err->flags, 4u);
+          }
+          uint32_t d = ((sel(x[u], dg.m0) >> dg.r0) & dg.k0) << dg.l0;
+          if (dg.two) d |= ((sel(x[u], dg.m1) >> dg.r1) & dg.k1) << dg.l1;
+          atomicAdd(wh + d, 1u);
+        }
+      }
+      __syncthreads();
+      goto flush;
+    }
     if (a.in.fmt == kAoS && R == 3 && fast_dig) {
       // AoS rank-3 rows (the common first pass): coordinates in registers,
       // range + pack checks from them
