@@ -168,6 +168,10 @@ struct PackSpec {
   uint8_t nk_mode[kMaxKeys];
   uint32_t nk_dim[kMaxKeys];
   double nk_rcp[kMaxKeys];  // 1 / nk_dim
+  // prefix modes left out of the packed word: constant within a run, so the
+  // last pass restores them from the run (run_prefix[li * n_imp + k])
+  uint32_t n_imp;
+  uint8_t imp_mode[kMaxKeys];
 };
 
 // x / d for d < 2^32: a double multiply by the precomputed reciprocal when
@@ -248,6 +252,7 @@ struct ScatterArgs {
   uint8_t* next_dig;           // next pass's digit per row (side channel for its histogram)
   uint32_t nd_shift, nd_mask;  // PK output: next digit = (packed >> nd_shift) & nd_mask
   DigitSpec ndig;              // unpacked output: next digit of the coordinates
+  const uint32_t* run_prefix;  // implicit prefix modes per large run (PackSpec::n_imp)
 };
 
 // ---------------------------------------------------------------------------
@@ -1200,10 +1205,10 @@ __global__ void __launch_bounds__(kSortThreads, 1024 / kSortThreads) k_scatter(S
             for (int m = 0; m < (RT > 0 ? RT : 1); ++m)
               cv[m] = (uint32_t)(row.x >> a.pack.off[m]) &
                       (uint32_t)((1ull << a.pack.width[m]) - 1ull);
-            unsigned long long hi = row.x >> a.pack.key_bits;
+            unsigned long long hi = a.pack.key_bits < 64 ? row.x >> a.pack.key_bits : 0ull;
 #pragma unroll
             for (int jj = (RT > 0 ? RT : 1) - 1; jj >= 0; --jj) {
-              if ((uint32_t)jj < a.pack.nk_n) {
+              if (a.pack.mixed && (uint32_t)jj < a.pack.nk_n) {
                 const uint32_t d = a.pack.nk_dim[jj];
                 const unsigned long long q = div_u64_u32(hi, d, a.pack.nk_rcp[jj]);
                 const uint32_t v = (uint32_t)(hi - q * d);
@@ -1214,10 +1219,20 @@ __global__ void __launch_bounds__(kSortThreads, 1024 / kSortThreads) k_scatter(S
                 hi = q;
               }
             }
+            for (uint32_t k = 0; k < a.pack.n_imp; ++k) {
+              const uint32_t v = __ldg(a.run_prefix + (size_t)s_cd[b].li * a.pack.n_imp + k);
+              const uint32_t mk = a.pack.imp_mode[k];
+#pragma unroll
+              for (int m = 0; m < (RT > 0 ? RT : 1); ++m)
+                if (mk == (uint32_t)m) cv[m] = v;
+            }
 #pragma unroll
             for (int m = 0; m < (RT > 0 ? RT : 1); ++m) __stcs(o + m, cv[m]);
           } else if (MX) {
             unpack_coords(a.pack, R, row.x, [&](uint32_t m, uint32_t v) { __stcs(o + m, v); });
+            for (uint32_t k = 0; k < a.pack.n_imp; ++k)
+              __stcs(o + a.pack.imp_mode[k],
+                     __ldg(a.run_prefix + (size_t)s_cd[b].li * a.pack.n_imp + k));
           } else if (RT) {
 #pragma unroll
             for (int m = 0; m < (RT > 0 ? RT : 1); ++m)
@@ -1246,7 +1261,7 @@ __global__ void __launch_bounds__(kSortThreads, 1024 / kSortThreads) k_scatter(S
           unsigned long long hi = 0;
 #pragma unroll
           for (int j = 0; j < (RT > 0 ? RT : 1); ++j) {
-            if ((uint32_t)j < a.pack.nk_n) {
+            if (a.pack.mixed && (uint32_t)j < a.pack.nk_n) {
               const uint32_t mj = a.pack.nk_mode[j];
               uint32_t x = cv[0];
 #pragma unroll
@@ -1254,7 +1269,7 @@ __global__ void __launch_bounds__(kSortThreads, 1024 / kSortThreads) k_scatter(S
               hi = hi * a.pack.nk_dim[j] + x;
             }
           }
-          pk |= hi << a.pack.key_bits;
+          if (a.pack.mixed) pk |= hi << a.pack.key_bits;
         } else if (MX) {
           pk = pack_coords(a.pack, R, [&](uint32_t m) { return coord(i, m); });
         } else if (RT) {
@@ -1819,6 +1834,14 @@ __global__ void __launch_bounds__(kThreads) k_probe_runs(const uint32_t* c, uint
   }
   for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xFFFFFFFFu, h, o);
   if ((threadIdx.x & 31) == 0 && h) atomicAdd(heads, (unsigned long long)h);
+}
+
+// implicit prefix coordinates of every large run (PackSpec::n_imp)
+__global__ void k_run_prefix(const uint32_t* c, uint32_t rank, const unsigned long long* run_start,
+                             uint64_t nruns, ModeList modes, uint32_t* out) {
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < nruns;
+       r += (uint64_t)gridDim.x * blockDim.x)
+    for (uint32_t k = 0; k < modes.n; ++k) out[r * modes.n + k] = c[run_start[r] * rank + modes.m[k]];
 }
 
 __global__ void k_run_records(const uint32_t* c, uint32_t rank, uint32_t mode, uint32_t dim,
@@ -2404,7 +2427,8 @@ DigitSpec make_digit(const KeySpec& k, uint32_t lo, uint32_t hi) {
 // Packed row layout of a group (PackSpec): key fields at their key offsets,
 // the other modes as bit fields above when everything fits 64 bits, else as
 // one mixed-radix number when THAT fits; false if neither does.
-bool make_pack(const KeySpec& key, uint32_t R, const uint32_t* dims, PackSpec* out) {
+bool make_pack(const KeySpec& key, uint32_t R, const uint32_t* dims, PackSpec* out,
+               const std::vector<uint32_t>& implicit = {}) {
   PackSpec p{};
   p.rank = R;
   p.key_bits = key.total_bits;
@@ -2413,8 +2437,11 @@ bool make_pack(const KeySpec& key, uint32_t R, const uint32_t* dims, PackSpec* o
   for (uint32_t m = 0; m < R; ++m) {
     bool is_key = false;
     for (uint32_t k = 0; k < key.n; ++k) is_key |= key.mode[k] == m;
+    for (uint32_t q : implicit) is_key |= q == m;  // not stored at all
     if (!is_key) nonkey.push_back(m);
   }
+  p.n_imp = (uint32_t)implicit.size();
+  for (uint32_t k = 0; k < p.n_imp; ++k) p.imp_mode[k] = (uint8_t)implicit[k];
   for (uint32_t k = 0; k < key.n; ++k) {
     p.off[key.mode[k]] = (uint8_t)key.off[k];
     p.width[key.mode[k]] = key.width[k];
@@ -2473,7 +2500,7 @@ void run_pass(Ctx& c, uint32_t R, uint64_t N, uint32_t T, Rows in, RowsOut out,
               bool check, unsigned long long** offs_out = nullptr, const PackSpec* pack = nullptr,
               uint32_t pk_shift = 0, uint32_t pk_mask = 0, const uint8_t* digits_in = nullptr,
               uint8_t* digits_out = nullptr, uint32_t nd_shift = 0, uint32_t nd_mask = 0,
-              const DigitSpec* next_dig = nullptr) {
+              const DigitSpec* next_dig = nullptr, const uint32_t* run_prefix = nullptr) {
   Workspace& ws = c.ws;
   const uint64_t nflat = num_chunks * kBins;
   auto* flat = ws.get<uint32_t>("chunk_flat", nflat);
@@ -2522,6 +2549,7 @@ void run_pass(Ctx& c, uint32_t R, uint64_t N, uint32_t T, Rows in, RowsOut out,
   a.nd_shift = nd_shift;
   a.nd_mask = nd_mask;
   if (next_dig) a.ndig = *next_dig;
+  a.run_prefix = run_prefix;
   if (const char* e = getenv("QD_SCATTER_DBG")) a.dbg = atoi(e);
   if (a.dbg & 2) {
     a.dbg_t = ws.get<unsigned long long>("dbg_t", 16);
@@ -2535,7 +2563,7 @@ void run_pass(Ctx& c, uint32_t R, uint64_t N, uint32_t T, Rows in, RowsOut out,
   const size_t smem = ScatterLayout(T, R, in.fmt).total;
   const int rt = (R == 3 || R == 4) ? (int)R : 0;
   const int dm = dig.lookup ? 0 : (dig.n == 1 ? 1 : (dig.n == 2 ? 2 : 0));
-  ScatterFn fn = scatter_kernel(rt, dm, in.fmt, out.fmt, pack && pack->mixed ? 1 : 0);
+  ScatterFn fn = scatter_kernel(rt, dm, in.fmt, out.fmt, pack && (pack->mixed || pack->n_imp) ? 1 : 0);
   if (!fn) throw Error(QD_CUDA_ERROR, "no scatter kernel for this row format pair");
   int per_sm = 0;
   QD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kSortThreads, smem));
@@ -2684,7 +2712,24 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
     // first histogram and the whole call is redone unpacked (run_groups).
     PackSpec pack{};
     bool packed = ws.allow_pack && g.check_range && D > 1;
-    if (packed) packed = make_pack(key, R, t.dims, &pack);
+    if (packed) {
+      // prefix modes are constant within a run: when the row does not pack
+      // otherwise, leave them out and restore them from the run
+      packed = make_pack(key, R, t.dims, &pack) ||
+               (run_start && make_pack(key, R, t.dims, &pack, g.prefix));
+    }
+    uint32_t* run_prefix = nullptr;
+    if (packed && pack.n_imp) {
+      run_prefix = ws.get<uint32_t>("run_prefix", num_large * pack.n_imp + 1);
+      ModeList pm{};
+      pm.n = pack.n_imp;
+      for (uint32_t k = 0; k < pack.n_imp; ++k) pm.m[k] = pack.imp_mode[k];
+      c.pre();
+      k_run_prefix<<<(uint32_t)std::min<uint64_t>((num_large + kThreads - 1) / kThreads + 1,
+                                                   ws.num_sms * 8),
+                     kThreads, 0, c.st>>>(src_c, R, run_start, num_large, pm, run_prefix);
+      c.launched(kSegK);
+    }
     if (!packed && D > 1 && !tmp_c) {
       tmp_c = ws.get<uint32_t>("rowsA_c", N * R);
       tmp_v = ws.get<double>("rowsA_v", N);
@@ -2720,7 +2765,7 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
       run_pass(c, R, N, T, in, out, chunks, num_chunks, run_start, digs[q], key,
                q == 0 && key.check, nullptr, packed ? &pack : nullptr, lo,
                (1u << (hi - lo)) - 1u, dig_in, dig_out, nlo, last ? 0u : (1u << (nhi - nlo)) - 1u,
-               last ? nullptr : &digs[q + 1]);
+               last ? nullptr : &digs[q + 1], run_prefix);
       in = Rows{out.c, out.v, out.fmt};
     }
   }

@@ -757,3 +757,21 @@ def test_mixed_radix_packing(ws):
     out = qd.transpose(u, [1, 0, 2], ws=ws)
     c, v = _np_transpose(dims, u.coords, u.values, [1, 0, 2])
     assert same(out, c, v)
+
+
+def test_implicit_prefix_packing(ws):
+    """config 3's shape, target (0,3,1,2): the plan sorts mode 3 inside mode-0
+    runs; 11 key bits + modes 1, 2 pack into 64 bits only when mode 0 (the
+    run prefix) is left out of the row and restored from the run."""
+    rng = np.random.default_rng(71)
+    dims = [532924, 17262471, 2480308, 1443]
+    n = 300_000
+    c = np.stack([rng.integers(0, 12, n) * 40000 + rng.integers(0, 3, n),  # few long mode-0 runs
+                  rng.integers(0, dims[1], n), rng.integers(0, dims[2], n),
+                  rng.integers(0, dims[3], n)], 1).astype(np.uint32)
+    c = np.unique(c, axis=0)
+    t = qd.CooTensor(dims, c.ravel(), rng.random(len(c)))
+    for target in ([0, 3, 1, 2], [0, 3, 2, 1], [0, 1, 3, 2]):
+        out = qd.transpose(t, target, ws=ws)
+        ec, ev, _ = ORC.transpose(t.dims, t.coords, t.values, target)
+        assert same(out, ec, ev), target
