@@ -64,7 +64,13 @@ constexpr int kMaxKeys = QD_MAX_RANK;
 constexpr uint32_t kChunkTiles = 16;  // tiles per scatter chunk
 constexpr double kRunSortMinAvg = 2.5;       // mean run length that pays for a run sort
 constexpr uint64_t kRunSortMinRows = 1u << 20;  // below this, not worth a probe
-constexpr int kMaxRounds = 4096 / kSortThreads;  // 32-row rounds per warp per tile (T <= 4096)
+#ifndef QD_MAX_TILE
+#define QD_MAX_TILE 4096
+#endif
+#ifndef QD_SCATTER_CTAS
+#define QD_SCATTER_CTAS 2  // resident k_scatter CTAs per SM (register / shared-memory split)
+#endif
+constexpr int kMaxRounds = QD_MAX_TILE / kSortThreads;  // 32-row rounds per warp per tile
 #ifndef QD_LOCAL_BALLOT
 #define QD_LOCAL_BALLOT 1
 #endif
@@ -894,7 +900,7 @@ struct ScatterLayout {
 // DM: digit of an AoS/SoA row inside 1 or 2 key fields (0 = general).
 // ---------------------------------------------------------------------------
 template <int RT, int IN, int OUT, int DM, int MX = 0>
-__global__ void __launch_bounds__(kSortThreads, 1024 / kSortThreads) k_scatter(ScatterArgs a) {
+__global__ void __launch_bounds__(kSortThreads, QD_SCATTER_CTAS * 512 / kSortThreads) k_scatter(ScatterArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   const uint32_t R = RT ? RT : a.rank;
   const uint64_t N = a.nnz;
@@ -2298,13 +2304,13 @@ constexpr uint32_t kCounters = 4096;
 // Rows per onesweep tile / local chunk for a given rank, from the smem budget.
 uint32_t sweep_tile_rows(const Workspace& ws, uint32_t rank) {
   if (const char* e = getenv("QD_TILE_ROWS")) return (uint32_t)atoi(e);
-  size_t budget = std::min<size_t>(ws.smem_optin, 112 * 1024);  // 2 CTAs/SM
+  size_t budget = std::min<size_t>(ws.smem_optin, (226 / QD_SCATTER_CTAS) * 1024);
   if (const char* e = getenv("QD_SMEM_BUDGET")) budget = (size_t)atoi(e) * 1024;
   auto need = [&](uint32_t T) {
     return std::max({ScatterLayout(T, rank, kAoS).total, ScatterLayout(T, rank, kSoA).total,
                      ScatterLayout(T, rank, kPK).total});
   };
-  uint32_t T = 4096;
+  uint32_t T = QD_MAX_TILE;
   while (T > 512 && need(T) > budget) T -= 512;
   while (T > 32 && need(T) > budget) T -= 32;
   return T;
