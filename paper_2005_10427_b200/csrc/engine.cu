@@ -2302,11 +2302,13 @@ struct Ctx {
 constexpr uint32_t kCounters = 4096;
 
 // Rows per onesweep tile / local chunk for a given rank, from the smem budget.
-uint32_t sweep_tile_rows(const Workspace& ws, uint32_t rank) {
+// fmt < 0: the largest tile every input format fits; else that format's
+uint32_t sweep_tile_rows(const Workspace& ws, uint32_t rank, int fmt = -1) {
   if (const char* e = getenv("QD_TILE_ROWS")) return (uint32_t)atoi(e);
   size_t budget = std::min<size_t>(ws.smem_optin, (226 / QD_SCATTER_CTAS) * 1024);
   if (const char* e = getenv("QD_SMEM_BUDGET")) budget = (size_t)atoi(e) * 1024;
   auto need = [&](uint32_t T) {
+    if (fmt >= 0) return ScatterLayout(T, rank, fmt).total;
     return std::max({ScatterLayout(T, rank, kAoS).total, ScatterLayout(T, rank, kSoA).total,
                      ScatterLayout(T, rank, kPK).total});
   };
@@ -2635,10 +2637,22 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
   for (uint32_t q = 0; q < D; ++q) digs[q] = make_digit(key, q * per, std::min(bits, (q + 1) * per));
 
   const uint32_t T = sweep_tile_rows(ws, R);
+  static const bool per_fmt_tiles = [] {
+    const char* e = getenv("QD_PK_TILES");
+    return !(e && atoi(e) == 0);
+  }();
   uint32_t TL = local_span(ws, R);
   if (bits + ceil_log2(TL) + 1 > 64) TL = 0;  // local key would not fit 64 bits
 
-  const uint32_t CH = T * chunk_tiles(ws, N, T);
+  // chunks hold whole tiles of the passes that dominate: the packed-row
+  // tile when the rows will pack (the first, AoS, pass then ends each chunk
+  // with a partial tile)
+  uint32_t Tch = T;
+  if (per_fmt_tiles && ws.allow_pack && g.check_range && D > 1) {
+    PackSpec probe{};
+    if (make_pack(key, R, t.dims, &probe)) Tch = sweep_tile_rows(ws, R, kPK);
+  }
+  const uint32_t CH = Tch * chunk_tiles(ws, N, Tch);
   ChunkDesc* chunks = ws.get<ChunkDesc>("chunks", 1);
   const unsigned long long* run_start = nullptr;
   uint64_t num_chunks = 0;
@@ -2768,7 +2782,9 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
       const uint8_t* dig_in = (side && q > 0) ? digbuf : nullptr;
       uint8_t* dig_out = (side && !last) ? digbuf : nullptr;
       const uint32_t nlo = (q + 1) * per, nhi = std::min(bits, nlo + per);
-      run_pass(c, R, N, T, in, out, chunks, num_chunks, run_start, digs[q], key,
+      // packed-row passes afford a larger tile (16-byte staged rows)
+      const uint32_t Tq = (per_fmt_tiles && in.fmt == kPK) ? sweep_tile_rows(ws, R, kPK) : T;
+      run_pass(c, R, N, Tq, in, out, chunks, num_chunks, run_start, digs[q], key,
                q == 0 && key.check, nullptr, packed ? &pack : nullptr, lo,
                (1u << (hi - lo)) - 1u, dig_in, dig_out, nlo, last ? 0u : (1u << (nhi - nlo)) - 1u,
                last ? nullptr : &digs[q + 1], run_prefix);
