@@ -874,7 +874,7 @@ struct ScatterLayout {
     }
     c0 = o; o += 2 * cbuf;
     v0 = o; o += 2 * vbuf;
-    dig = o; o += align16(size_t(T) * 2);
+    dig = o; o += align16(size_t(T) + 16);  // u8 digit per row
     rnk = o; o += 0;  // ranks live in registers
     sorted = o; o += align16(size_t(T) * 2);
     whist = o; o += align16(size_t(kSortWarps) * kBins * 2);
@@ -905,7 +905,7 @@ __global__ void __launch_bounds__(kSortThreads, QD_SCATTER_CTAS * 512 / kSortThr
   const uint32_t R = RT ? RT : a.rank;
   const uint64_t N = a.nnz;
   const ScatterLayout L(a.T, R, IN);
-  uint16_t* s_dig = reinterpret_cast<uint16_t*>(smem + L.dig);
+  uint8_t* s_dig = reinterpret_cast<uint8_t*>(smem + L.dig);
   uint16_t* s_sorted = reinterpret_cast<uint16_t*>(smem + L.sorted);
   uint16_t* s_whist = reinterpret_cast<uint16_t*>(smem + L.whist);
   uint32_t* s_start = reinterpret_cast<uint32_t*>(smem + L.start);
@@ -1095,7 +1095,7 @@ __global__ void __launch_bounds__(kSortThreads, QD_SCATTER_CTAS * 512 / kSortThr
       if ((uint32_t)r >= nfull) break;  // warp-uniform
       const uint32_t p = lo + r * 32 + lane;
       const uint32_t d = digit_at(p);
-      s_dig[p] = (uint16_t)d;
+      s_dig[p] = (uint8_t)d;
       const unsigned peers = warp_peers(d, 0xFFFFFFFFu);
       const int leader = __ffs(peers) - 1;
       uint32_t bcount = 0;
@@ -1113,7 +1113,7 @@ __global__ void __launch_bounds__(kSortThreads, QD_SCATTER_CTAS * 512 / kSortThr
       uint32_t d = 0;
       if (valid) {
         d = digit_at(p);
-        s_dig[p] = (uint16_t)d;
+        s_dig[p] = (uint8_t)d;
       }
       unsigned peers = warp_peers(d, (1u << (nrow & 31u)) - 1u);
       if (!valid) peers = 1u << lane;
