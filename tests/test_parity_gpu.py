@@ -775,3 +775,32 @@ def test_implicit_prefix_packing(ws):
         out = qd.transpose(t, target, ws=ws)
         ec, ev, _ = ORC.transpose(t.dims, t.coords, t.values, target)
         assert same(out, ec, ev), target
+
+
+def test_randomised_stress_against_oracle(ws):
+    """Random shapes across the engine's layout choices (bit-field, mixed-
+    radix and implicit-prefix packing, AoS rows, run-level sort, local
+    sorts) and strategies, against the C oracle."""
+    rng = np.random.default_rng(2027)
+    big = [33_554_467, 3_000_017, 1_000_003, 40_000, 5000, 700, 60, 3]
+    for trial in range(40):
+        r = int(rng.integers(2, 6))
+        dims = [int(rng.choice(big)) for _ in range(r)]
+        n = int(rng.choice([1000, 30_000, 150_000]))
+        cols = []
+        for d in dims:
+            if rng.random() < 0.5:
+                k = int(rng.integers(1, 50))  # few distinct values -> long runs
+                vals = rng.integers(0, d, k)
+                cols.append(vals[rng.integers(0, k, n)])
+            else:
+                cols.append(rng.integers(0, d, n, dtype=np.int64))
+        c = np.stack(cols, 1).astype(np.uint32)
+        c = c[np.lexsort(c.T[::-1])]
+        t = qd.CooTensor(dims, c.ravel(), rng.random(n))
+        target = [int(x) for x in rng.permutation(r)]
+        name = ["quesadilla", "radix", "topk", "comparison"][trial % 4]
+        k = int(rng.integers(1, r + 1))
+        out = qd.transpose(t, target, strategy(name, k), ws=ws)
+        ec, ev, _ = ORC.transpose(t.dims, t.coords, t.values, target, name, k)
+        assert same(out, ec, ev), (trial, dims, n, target, name, k)
