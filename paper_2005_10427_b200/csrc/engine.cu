@@ -178,6 +178,7 @@ struct PackSpec {
   // last pass restores them from the run (run_prefix[li * n_imp + k])
   uint32_t n_imp;
   uint8_t imp_mode[kMaxKeys];
+  uint8_t kind[kMaxKeys];  // per mode: 0 bit field (width may be 0), 1 mixed radix, 2 implicit
 };
 
 // x / d for d < 2^32: a double multiply by the precomputed reciprocal when
@@ -209,8 +210,8 @@ __device__ __forceinline__ unsigned long long pack_coords(const PackSpec& p, uin
 template <class P>
 __device__ __forceinline__ void unpack_coords(const PackSpec& p, uint32_t R, unsigned long long x,
                                               P put) {
-  for (uint32_t m = 0; m < R; ++m)
-    if (p.width[m]) put(m, (uint32_t)(x >> p.off[m]) & (uint32_t)((1ull << p.width[m]) - 1ull));
+  for (uint32_t m = 0; m < R; ++m)  // every bit field, including 0-bit ones (extent 1)
+    if (p.kind[m] == 0) put(m, (uint32_t)(x >> p.off[m]) & (uint32_t)((1ull << p.width[m]) - 1ull));
   if (p.mixed) {
     unsigned long long hi = p.key_bits < 64 ? x >> p.key_bits : 0ull;
     for (int j = (int)p.nk_n - 1; j >= 0; --j) {
@@ -2107,6 +2108,15 @@ struct Workspace {
       const size_t want = bytes + bytes / 8;  // headroom against regrowth
       QD_CUDA(cudaMalloc(&b.p, want));
       b.bytes = want;
+      static const int poison = [] {
+        const char* e = getenv("QD_POISON");
+        return e ? atoi(e) : 0;
+      }();
+      static const char* only = getenv("QD_POISON_ONLY");
+      static const char* except = getenv("QD_POISON_EXCEPT");
+      if (poison && (!only || name.find(only) != std::string::npos) &&
+          (!except || name.find(except) == std::string::npos))
+        QD_CUDA(cudaMemset(b.p, poison & 0xFF, want));  // debug: expose reads of unwritten scratch
     }
     return static_cast<T*>(b.p);
   }
@@ -2449,7 +2459,10 @@ bool make_pack(const KeySpec& key, uint32_t R, const uint32_t* dims, PackSpec* o
     if (!is_key) nonkey.push_back(m);
   }
   p.n_imp = (uint32_t)implicit.size();
-  for (uint32_t k = 0; k < p.n_imp; ++k) p.imp_mode[k] = (uint8_t)implicit[k];
+  for (uint32_t k = 0; k < p.n_imp; ++k) {
+    p.imp_mode[k] = (uint8_t)implicit[k];
+    p.kind[implicit[k]] = 2;
+  }
   for (uint32_t k = 0; k < key.n; ++k) {
     p.off[key.mode[k]] = (uint8_t)key.off[k];
     p.width[key.mode[k]] = key.width[k];
@@ -2486,6 +2499,7 @@ bool make_pack(const KeySpec& key, uint32_t R, const uint32_t* dims, PackSpec* o
     p.nk_rcp[j] = 1.0 / (double)dims[nonkey[j]];
     p.lim[nonkey[j]] = dims[nonkey[j]];
     p.width[nonkey[j]] = 0;
+    p.kind[nonkey[j]] = 1;
   }
   *out = p;
   return true;

@@ -804,3 +804,14 @@ def test_randomised_stress_against_oracle(ws):
         out = qd.transpose(t, target, strategy(name, k), ws=ws)
         ec, ev, _ = ORC.transpose(t.dims, t.coords, t.values, target, name, k)
         assert same(out, ec, ev), (trial, dims, n, target, name, k)
+
+
+def test_stress_with_poisoned_scratch():
+    """The randomised stress in a fresh process whose workspace buffers start
+    as garbage (QD_POISON): no kernel may depend on zero-filled scratch."""
+    import subprocess
+    import sys as _sys
+    env = dict(os.environ, QD_POISON="255")
+    r = subprocess.run([_sys.executable, os.path.join(os.path.dirname(__file__), "stress_util.py"),
+                        "8", "60"], env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
