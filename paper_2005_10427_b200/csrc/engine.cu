@@ -126,6 +126,7 @@ struct LocalArgs {
   KeySpec key;
   ErrBlock* err;
   const uint32_t* chunk_list;  // chunk ids holding small runs (blockIdx.x -> chunk)
+  const uint32_t* first_run;   // per chunk: first run starting in it (k_classify_chunks)
 };
 
 // A chunk: a contiguous row range inside one run, processed by one CTA in
@@ -1370,11 +1371,18 @@ __global__ void __launch_bounds__(kSortThreads) k_local(LocalArgs a) {
     const unsigned long long hi = min((unsigned long long)a.nnz, lo + (unsigned long long)a.TL);
     const uint64_t S = a.nseg;  // seg_start has S+1 entries
     if (threadIdx.x == 0) {
-      // first run starting at or after lo
-      uint64_t l = 0, h = S;
-      while (l < h) {
-        const uint64_t m = (l + h) >> 1;
-        if (a.seg_start[m] < lo) l = m + 1; else h = m;
+      // first run starting at or after lo (precomputed per chunk; a binary
+      // search here would be a chain of dependent global loads per CTA)
+      uint64_t l;
+      if (a.first_run) {
+        l = a.first_run[chunk];
+      } else {
+        l = 0;
+        uint64_t h = S;
+        while (l < h) {
+          const uint64_t m = (l + h) >> 1;
+          if (a.seg_start[m] < lo) l = m + 1; else h = m;
+        }
       }
       s_sa = l;
       s_nsl = 0xFFFFFFFFu;
@@ -1557,7 +1565,8 @@ __global__ void __launch_bounds__(kThreads) k_compact(const uint32_t* words, uin
 // Per run: large flag and its chunk count (CH rows per chunk).
 __global__ void k_classify_chunks(const unsigned long long* seg_start,
                                   const unsigned long long* S_ptr, uint32_t TL, uint32_t CH,
-                                  uint32_t* is_large, uint32_t* nchunks, uint32_t* local_flag) {
+                                  uint32_t* is_large, uint32_t* nchunks, uint32_t* local_flag,
+                                  uint32_t* first_run) {
   const unsigned long long S = *S_ptr;
   for (unsigned long long s = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; s < S;
        s += (unsigned long long)gridDim.x * blockDim.x) {
@@ -1565,7 +1574,13 @@ __global__ void k_classify_chunks(const unsigned long long* seg_start,
     const bool large = len > TL;
     is_large[s] = large;
     nchunks[s] = large ? (uint32_t)((len + CH - 1) / CH) : 0u;
-    if (!large && TL) local_flag[seg_start[s] / TL] = 1u;  // a local chunk has work
+    if (TL) {
+      const unsigned long long cl = seg_start[s] / TL;
+      if (!large) local_flag[cl] = 1u;  // a local chunk has work
+      // the first run starting in a chunk records itself (one writer per
+      // chunk; a flagged chunk always starts with a small run)
+      if (s == 0 || seg_start[s - 1] / TL != cl) first_run[cl] = (uint32_t)s;
+    }
   }
 }
 
@@ -2673,12 +2688,13 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
   unsigned long long* seg = nullptr;
   uint64_t S = 0, num_large = 0, local_chunks = 0;
   const uint32_t* local_list = nullptr;
+  const uint32_t* local_first = nullptr;
   bool small_runs = false;
 
   if (g.prefix.empty()) {
     if (TL && N <= TL) {
       LocalArgs la{src_c, src_v, dst_c, dst_v, R, N, TL, (uint32_t)N, nullptr, 1, key, c.err,
-                   nullptr};
+                   nullptr, nullptr};
       const size_t smem = LocalLayout((uint32_t)N, R, TL).total;
       c.pre();
       k_local<<<1, kSortThreads, smem, c.st>>>(la);
@@ -2703,12 +2719,14 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
     auto* lflag = ws.get<uint32_t>("local_flag", nloc + 1);
     auto* lpos = ws.get<unsigned long long>("local_pos", nloc + 1);
     auto* llist = ws.get<uint32_t>("local_list", nloc + 1);
+    auto* lfirst = ws.get<uint32_t>("local_first", nloc + 1);
     if (nloc) QD_CUDA(cudaMemsetAsync(lflag, 0, nloc * 4, c.st));
     ws.h_small[0] = S;
     QD_CUDA(cudaMemcpyAsync(S_dev, ws.h_small, 8, cudaMemcpyHostToDevice, c.st));
     const uint32_t grid = (uint32_t)std::min<uint64_t>((S + kThreads - 1) / kThreads, ws.num_sms * 8);
     c.pre();
-    k_classify_chunks<<<grid, kThreads, 0, c.st>>>(seg, S_dev, TL, CH, is_large, nch, lflag);
+    k_classify_chunks<<<grid, kThreads, 0, c.st>>>(seg, S_dev, TL, CH, is_large, nch, lflag,
+                                                   lfirst);
     c.launched(kSegK);
     scan_exclusive(c, is_large, S, loff, totals);
     scan_exclusive(c, nch, S, coff, totals + 1);
@@ -2727,6 +2745,7 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
     num_chunks = ws.h_small[2];
     local_chunks = ws.h_small[3];
     local_list = llist;
+    local_first = lfirst;
     small_runs = S > num_large;
     if (num_chunks) {
       chunks = ws.get<ChunkDesc>("chunks", num_chunks);
@@ -2809,7 +2828,8 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
     // small runs: chunks of runs starting in [c*TL, (c+1)*TL), only the
     // chunks that hold some (compact list); after the passes, whose
     // intermediates may use dst's storage
-    LocalArgs la{src_c, src_v, dst_c, dst_v, R, N, TL, 2 * TL, seg, S, key, c.err, local_list};
+    LocalArgs la{src_c, src_v, dst_c, dst_v, R, N, TL, 2 * TL, seg, S, key, c.err, local_list,
+                 local_first};
     const size_t smem = LocalLayout(2 * TL, R, TL).total;
     c.pre();
     k_local<<<(uint32_t)local_chunks, kSortThreads, smem, c.st>>>(la);
