@@ -1417,19 +1417,49 @@ __global__ void __launch_bounds__(kSortThreads) k_local(LocalArgs a) {
   const double* s_v = s_vraw + (uint32_t)(r0 & 1ull);
 
   const uint32_t kb = a.key.total_bits;
+  // the key's first (up to) four fields in registers, hoisted out of the row
+  // loop (the general KeySpec walk reloads every field per row)
+  constexpr int kF = 4;
+  const bool few = a.key.n <= (uint32_t)kF;
+  uint32_t fm[kF], fw[kF], fo[kF], fd[kF];
+#pragma unroll
+  for (int f = 0; f < kF; ++f) {
+    const bool on = (uint32_t)f < a.key.n;
+    fm[f] = on ? a.key.mode[f] : 0u;
+    fw[f] = on ? a.key.width[f] : 0u;
+    fo[f] = on ? a.key.off[f] : 0u;
+    fd[f] = on ? a.key.dim[f] : 0xFFFFFFFFu;
+  }
+  // each thread walks its rows in order, so the run index only moves forward
+  uint32_t run = 0;
   for (uint32_t i = threadIdx.x; i < n; i += kSortThreads) {
     const uint32_t* row = s_c + (size_t)i * R;
-    if (a.key.check) check_row(row, a.key, r0 + i, a.err);
-    unsigned long long k = full_key(row, a.key);
-    if (nsl > 1) {
-      // local run index: last run start <= row
-      uint32_t l = 0, h = nsl;  // s_seg[0..nsl]
-      const unsigned long long g = r0 + i;
-      while (h - l > 1) {
-        const uint32_t m = (l + h) >> 1;
-        if (s_seg[m] <= g) l = m; else h = m;
+    unsigned long long k = 0;
+    if (few) {
+      bool bad = false;
+#pragma unroll
+      for (int f = 0; f < kF; ++f) {
+        if ((uint32_t)f < a.key.n) {
+          const uint32_t x = row[fm[f]];
+          bad |= x >= fd[f];
+          if (fw[f]) k |= (unsigned long long)(x & (uint32_t)((1ull << fw[f]) - 1ull)) << fo[f];
+        }
       }
-      k |= (unsigned long long)l << kb;
+      if (a.key.check && bad) check_row(row, a.key, r0 + i, a.err);
+    } else {
+      if (a.key.check) check_row(row, a.key, r0 + i, a.err);
+      k = full_key(row, a.key);
+    }
+    if (nsl > 1) {
+      // local run index: last run start <= row (this thread's rows only move
+      // forward, so the search starts at the previous answer)
+      const unsigned long long g = r0 + i;
+      uint32_t h = nsl;
+      while (h - run > 1) {
+        const uint32_t m = (run + h) >> 1;
+        if (s_seg[m] <= g) run = m; else h = m;
+      }
+      k |= (unsigned long long)run << kb;
     }
     s_key[i] = k;
     s_p0[i] = (uint16_t)i;
