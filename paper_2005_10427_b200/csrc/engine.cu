@@ -77,6 +77,9 @@ constexpr int kMaxRounds = QD_MAX_TILE / kSortThreads;  // 32-row rounds per war
 #ifndef QD_EARLY_ADVANCE
 #define QD_EARLY_ADVANCE 1
 #endif
+#ifndef QD_RANK_BCAST
+#define QD_RANK_BCAST 1
+#endif
 
 // ---------------------------------------------------------------------------
 // kernel parameter blocks
@@ -876,9 +879,9 @@ struct ScatterLayout {
     }
     c0 = o; o += 2 * cbuf;
     v0 = o; o += 2 * vbuf;
-    dig = o; o += align16(size_t(T) + 16);  // u8 digit per row
+    dig = o; o += 0;  // digits travel with the sorted index (s_sorted)
     rnk = o; o += 0;  // ranks live in registers
-    sorted = o; o += align16(size_t(T) * 2);
+    sorted = o; o += align16(size_t(T) * 4);  // (row << 8) | digit by sorted slot
     whist = o; o += align16(size_t(kSortWarps) * kBins * 2);
     cnt = o; o += align16(kBins * 4);
     start = o; o += align16(kBins * 4);
@@ -907,8 +910,7 @@ __global__ void __launch_bounds__(kSortThreads, QD_SCATTER_CTAS * 512 / kSortThr
   const uint32_t R = RT ? RT : a.rank;
   const uint64_t N = a.nnz;
   const ScatterLayout L(a.T, R, IN);
-  uint8_t* s_dig = reinterpret_cast<uint8_t*>(smem + L.dig);
-  uint16_t* s_sorted = reinterpret_cast<uint16_t*>(smem + L.sorted);
+  uint32_t* s_sorted = reinterpret_cast<uint32_t*>(smem + L.sorted);
   uint16_t* s_whist = reinterpret_cast<uint16_t*>(smem + L.whist);
   uint32_t* s_start = reinterpret_cast<uint32_t*>(smem + L.start);
   unsigned long long* s_run = reinterpret_cast<unsigned long long*>(smem + L.run);
@@ -1097,8 +1099,14 @@ __global__ void __launch_bounds__(kSortThreads, QD_SCATTER_CTAS * 512 / kSortThr
       if ((uint32_t)r >= nfull) break;  // warp-uniform
       const uint32_t p = lo + r * 32 + lane;
       const uint32_t d = digit_at(p);
-      s_dig[p] = (uint8_t)d;
       const unsigned peers = warp_peers(d, 0xFFFFFFFFu);
+#if QD_RANK_BCAST
+      // every lane reads its digit's count (equal digits: one broadcast
+      // wavefront), the lowest peer writes it back: no shuffle
+      const uint32_t bcount = wh[d];
+      if ((peers & below) == 0u) wh[d] = (uint16_t)(bcount + __popc(peers));
+      __syncwarp();
+#else
       const int leader = __ffs(peers) - 1;
       uint32_t bcount = 0;
       if (lane == leader) {
@@ -1106,6 +1114,7 @@ __global__ void __launch_bounds__(kSortThreads, QD_SCATTER_CTAS * 512 / kSortThr
         wh[d] = (uint16_t)(bcount + __popc(peers));
       }
       bcount = __shfl_sync(0xFFFFFFFFu, bcount, leader);
+#endif
       packed[r] = ((bcount + __popc(peers & below)) << 8) | d;
     }
     if (nrow & 31u) {  // warp-uniform
@@ -1113,12 +1122,14 @@ __global__ void __launch_bounds__(kSortThreads, QD_SCATTER_CTAS * 512 / kSortThr
       const uint32_t p = lo + r * 32 + lane;
       const bool valid = lane < (nrow & 31u);
       uint32_t d = 0;
-      if (valid) {
-        d = digit_at(p);
-        s_dig[p] = (uint8_t)d;
-      }
+      if (valid) d = digit_at(p);
       unsigned peers = warp_peers(d, (1u << (nrow & 31u)) - 1u);
       if (!valid) peers = 1u << lane;
+#if QD_RANK_BCAST
+      const uint32_t bcount = valid ? wh[d] : 0u;
+      if (valid && (peers & below) == 0u) wh[d] = (uint16_t)(bcount + __popc(peers));
+      __syncwarp();
+#else
       const int leader = __ffs(peers) - 1;
       uint32_t bcount = 0;
       if (valid && lane == leader) {
@@ -1126,6 +1137,7 @@ __global__ void __launch_bounds__(kSortThreads, QD_SCATTER_CTAS * 512 / kSortThr
         wh[d] = (uint16_t)(bcount + __popc(peers));
       }
       bcount = __shfl_sync(0xFFFFFFFFu, bcount, leader);
+#endif
       const uint32_t v = ((bcount + __popc(peers & below)) << 8) | d;
 #pragma unroll
       for (int q = 0; q < kMaxRounds; ++q)
@@ -1172,18 +1184,20 @@ __global__ void __launch_bounds__(kSortThreads, QD_SCATTER_CTAS * 512 / kSortThr
     __syncthreads();
     QD_TMARK(5);
     // sorted position of every row: all lookups first, then the stores (the
-    // compiler cannot hoist a lookup above a possibly aliasing store)
+    // compiler cannot hoist a lookup above a possibly aliasing store); the
+    // row's digit travels with its index, so the store loop reads both
+    // sequentially by sorted slot (no random digit gather)
 #pragma unroll
     for (int r = 0; r < kMaxRounds; ++r) {
       if (lo + r * 32 >= hi) break;
       const uint32_t d = packed[r] & 0xFFu;
-      packed[r] = s_start[d] + wh[d] + (packed[r] >> 8);
+      packed[r] = ((s_start[d] + wh[d] + (packed[r] >> 8)) << 8) | d;
     }
 #pragma unroll
     for (int r = 0; r < kMaxRounds; ++r) {
       const uint32_t p = lo + r * 32 + lane;
       if (lo + r * 32 >= hi) break;
-      if (p < hi) s_sorted[packed[r]] = (uint16_t)p;
+      if (p < hi) s_sorted[packed[r] >> 8] = (p << 8) | (packed[r] & 0xFFu);
     }
     __syncthreads();
     QD_TMARK(6);
@@ -1195,8 +1209,9 @@ __global__ void __launch_bounds__(kSortThreads, QD_SCATTER_CTAS * 512 / kSortThr
     }
     const uint32_t vbase = IN == kPK ? 0u : (uint32_t)(span_dst(b, R) - scb) + s_ofsb[R];
     for (uint32_t j = threadIdx.x; j < n; j += kSortThreads) {
-      const uint32_t i = s_sorted[j];
-      const unsigned long long dst = (unsigned long long)(s_gbase[s_dig[i]] + j);
+      const uint32_t sj = s_sorted[j];
+      const uint32_t i = sj >> 8;
+      const unsigned long long dst = (unsigned long long)(s_gbase[sj & 0xFFu] + j);
       if (a.dbg & 1) continue;
       if (IN == kPK) {
         const ulonglong2 row = s_pk[i];
