@@ -57,6 +57,11 @@ constexpr int kWarps = kThreads / 32;
 #endif
 constexpr int kSortThreads = QD_SORT_THREADS;  // k_scatter / k_local
 constexpr int kSortWarps = kSortThreads / 32;
+#ifndef QD_LOCAL_THREADS
+#define QD_LOCAL_THREADS 512
+#endif
+constexpr int kLocalThreads = QD_LOCAL_THREADS;  // k_local
+constexpr int kLocalWarps = kLocalThreads / 32;
 constexpr int kRadixLog = 8;
 constexpr int kBins = 1 << kRadixLog;
 constexpr int kMaxTerms = 12;
@@ -1341,7 +1346,7 @@ struct LocalLayout {
     perm0 = o; o += align16(size_t(cap) * 2);
     perm1 = o; o += align16(size_t(cap) * 2);
     rnk = o; o += align16(size_t(cap) * 2);
-    whist = o; o += align16(size_t(kSortWarps) * kBins * 2);
+    whist = o; o += align16(size_t(kLocalWarps) * kBins * 2);
     cnt = o; o += align16(kBins * 4);
     start = o; o += align16(kBins * 4);
     seg = o; o += align16((size_t(TL) + 2) * 8);
@@ -1354,7 +1359,7 @@ __device__ __forceinline__ uint32_t ceil_log2_dev(uint64_t x) {
   return x <= 1 ? 0u : 64u - (uint32_t)__clzll((long long)(x - 1));
 }
 
-__global__ void __launch_bounds__(kSortThreads) k_local(LocalArgs a) {
+__global__ void __launch_bounds__(kLocalThreads) k_local(LocalArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   const LocalLayout L(a.cap, a.rank, a.TL);
   uint32_t* s_craw = reinterpret_cast<uint32_t*>(smem + L.c);
@@ -1405,7 +1410,7 @@ __global__ void __launch_bounds__(kSortThreads) k_local(LocalArgs a) {
     __syncthreads();
     const uint64_t sa = s_sa;
     // runs sa .. sa+k starting in [lo, hi) and small; at most TL of them
-    for (uint32_t k = threadIdx.x; k <= a.TL; k += kSortThreads) {
+    for (uint32_t k = threadIdx.x; k <= a.TL; k += kLocalThreads) {
       const uint64_t s = sa + k;
       bool stop = true;
       if (s < S) {
@@ -1425,8 +1430,8 @@ __global__ void __launch_bounds__(kSortThreads) k_local(LocalArgs a) {
   __syncthreads();
   const uint32_t n = (uint32_t)(r1 - r0);
   const uint32_t R = a.rank;
-  load_words<kSortThreads>(s_craw, a.in_c, r0 * R, n * R);
-  load_doubles<kSortThreads>(s_vraw, a.in_v, r0, n);
+  load_words<kLocalThreads>(s_craw, a.in_c, r0 * R, n * R);
+  load_doubles<kLocalThreads>(s_vraw, a.in_v, r0, n);
   __syncthreads();
   const uint32_t* s_c = s_craw + (uint32_t)((r0 * R) & 3ull);
   const double* s_v = s_vraw + (uint32_t)(r0 & 1ull);
@@ -1447,7 +1452,7 @@ __global__ void __launch_bounds__(kSortThreads) k_local(LocalArgs a) {
   }
   // each thread walks its rows in order, so the run index only moves forward
   uint32_t run = 0;
-  for (uint32_t i = threadIdx.x; i < n; i += kSortThreads) {
+  for (uint32_t i = threadIdx.x; i < n; i += kLocalThreads) {
     const uint32_t* row = s_c + (size_t)i * R;
     unsigned long long k = 0;
     if (few) {
@@ -1481,19 +1486,19 @@ __global__ void __launch_bounds__(kSortThreads) k_local(LocalArgs a) {
   }
   const uint32_t nbits = kb + ceil_log2_dev(nsl);
   const uint32_t passes = (nbits + kRadixLog - 1) / kRadixLog;
-  const uint32_t ipw = (n + kSortWarps - 1) / kSortWarps;
+  const uint32_t ipw = (n + kLocalWarps - 1) / kLocalWarps;
   uint16_t* cur = s_p0;
   uint16_t* nxt = s_p1;
   for (uint32_t q = 0; q < passes; ++q) {
     const uint32_t sh = q * kRadixLog;
-    for (int k = threadIdx.x; k < kSortWarps * kBins; k += kSortThreads) s_whist[k] = 0;
+    for (int k = threadIdx.x; k < kLocalWarps * kBins; k += kLocalThreads) s_whist[k] = 0;
     __syncthreads();
     // the local sort's digits are key bits in arbitrary order (high entropy):
     // ballot peers beat MATCH.ANY there (~25 vs ~61 SM cycles per warp round)
     warp_rank<QD_LOCAL_BALLOT>([&](uint32_t p) { return (uint32_t)((s_key[cur[p]] >> sh) & (kBins - 1)); },
                                n, ipw, s_rank, s_whist);
     __syncthreads();
-    bin_offsets<kSortThreads>(s_whist, s_tmp, s_start);
+    bin_offsets<kLocalThreads>(s_whist, s_tmp, s_start);
     __syncthreads();
     {
       const uint32_t w = threadIdx.x >> 5;
@@ -1510,7 +1515,7 @@ __global__ void __launch_bounds__(kSortThreads) k_local(LocalArgs a) {
     cur = nxt;
     nxt = t;
   }
-  for (uint32_t j = threadIdx.x; j < n; j += kSortThreads) {
+  for (uint32_t j = threadIdx.x; j < n; j += kLocalThreads) {
     const uint32_t i = cur[j];
     store_row(a.out_c, a.out_v, R, r0 + j, s_c + (size_t)i * R, s_v[i]);
   }
@@ -2388,7 +2393,8 @@ uint32_t sweep_tile_rows(const Workspace& ws, uint32_t rank, int fmt = -1) {
   return T;
 }
 uint32_t local_span(const Workspace& ws, uint32_t rank) {
-  const size_t budget = std::min<size_t>(ws.smem_optin, 112 * 1024);
+  size_t budget = std::min<size_t>(ws.smem_optin, 112 * 1024);
+  if (const char* e = getenv("QD_LOCAL_KB")) budget = (size_t)atoi(e) * 1024;
   uint32_t TL = 2048;
   while (TL > 32 && LocalLayout(2 * TL, rank, TL).total > budget) TL -= 32;
   return TL;
@@ -2742,7 +2748,7 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
                    nullptr, nullptr};
       const size_t smem = LocalLayout((uint32_t)N, R, TL).total;
       c.pre();
-      k_local<<<1, kSortThreads, smem, c.st>>>(la);
+      k_local<<<1, kLocalThreads, smem, c.st>>>(la);
       c.launched(kLocalK, 1);
       return;
     }
@@ -2877,7 +2883,7 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
                  local_first};
     const size_t smem = LocalLayout(2 * TL, R, TL).total;
     c.pre();
-    k_local<<<(uint32_t)local_chunks, kSortThreads, smem, c.st>>>(la);
+    k_local<<<(uint32_t)local_chunks, kLocalThreads, smem, c.st>>>(la);
     c.launched(kLocalK);
   }
 }
@@ -2885,14 +2891,15 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
 
 // Run-level stable sort by mode k (empty prefix): see k_run_records.  Returns
 // false (nothing written) when the runs are too short to pay off.
+template <class Pays>
 bool try_run_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const double* src_v,
-                  uint32_t* dst_c, double* dst_v, uint32_t k) {
+                  uint32_t* dst_c, double* dst_v, uint32_t k, Pays pays) {
   Workspace& ws = c.ws;
   const uint64_t N = t.nnz;
   const uint32_t R = t.rank;
   unsigned long long* seg = nullptr;
   const uint64_t S = find_runs(c, src_c, R, N, {k}, &seg);
-  if (S == 0 || (double)N / (double)S < kRunSortMinAvg) return false;
+  if (S == 0 || (double)N / (double)S < kRunSortMinAvg || !pays(S)) return false;
   auto* rk0 = ws.get<uint32_t>("run_rk0", S);
   auto* rv0 = ws.get<double>("run_rv0", S);
   auto* rk1 = ws.get<uint32_t>("run_rk1", S);
@@ -2967,15 +2974,28 @@ void exec_group(Ctx& c, const TensorView& t, const uint32_t* src_c, const double
   // rank-3 rows and ~16 ps for wider rank >= 4 rows; a run sort pays ~2.3 ps
   // per row for run discovery plus ~13.5 ps (rank 3) / 17 ps (rank >= 4)
   // per row for the run move, and ~(20 + 10 x its digit passes) ps per run.
-  auto worth_it = [&](uint32_t k, const std::vector<uint32_t>& rest_keys) -> bool {
-    if (rs_mode == 1) return true;
-    uint32_t all_bits = 0, key_bits = ceil_log2(t.dims[k]), rest_bits = 0;
-    for (uint32_t q = 0; q < R; ++q) all_bits += ceil_log2(t.dims[q]);
+  // the chunked passes' per-row cost: 16-byte packed rows whenever the
+  // group's rows pack (plain or mixed-radix, as segmented_sort decides)
+  bool packs = false;
+  if (ws.allow_pack && g.check_range) {
+    std::vector<uint32_t> wd(m);
+    for (size_t i = 0; i < m; ++i) wd[i] = ceil_log2(t.dims[g.keys[i]]);
+    PackSpec probe{};
+    packs = make_pack(make_keyspec(g.keys, wd, t.dims, true), R, t.dims, &probe);
+  }
+  const double c_row = packs ? 10.5 : (R <= 3 ? 14.5 : 16.0);
+  const double c_move = (R <= 3 ? 13.5 : 17.0) + 2.3;
+  // run-sort vs chunked cost (ps) for S runs
+  auto costs = [&](uint32_t k, const std::vector<uint32_t>& rest_keys, double S) {
+    uint32_t key_bits = ceil_log2(t.dims[k]), rest_bits = 0;
     for (uint32_t q : rest_keys) rest_bits += ceil_log2(t.dims[q]);
-    const double c_row = all_bits <= 64 ? 10.5 : (R <= 3 ? 14.5 : 16.0);
-    const double c_move = (R <= 3 ? 13.5 : 17.0) + 2.3;
     const double chunked = (double)((key_bits + rest_bits + 7) / 8) * N * c_row;
     const double rest = rest_keys.empty() ? 0.0 : (double)((rest_bits + 7) / 8) * N * c_row;
+    const double run = N * c_move + S * (20.0 + 10.0 * ((key_bits + 7) / 8)) + rest;
+    return std::make_pair(run, chunked);
+  };
+  auto worth_it = [&](uint32_t k, const std::vector<uint32_t>& rest_keys) -> bool {
+    if (rs_mode == 1) return true;
     // expected runs from a probe of 256 x 1024 rows
     auto* heads = ws.get<unsigned long long>("probe_heads", 1);
     QD_CUDA(cudaMemsetAsync(heads, 0, 8, c.st));
@@ -2986,15 +3006,25 @@ void exec_group(Ctx& c, const TensorView& t, const uint32_t* src_c, const double
     QD_CUDA(cudaStreamSynchronize(c.st));
     const double frac = ((double)ws.h_small[0] + kProbeBlocks) / ((double)kProbeBlocks * kProbeRows);
     const double S_est = std::min(1.0, frac) * (double)N;
-    const double run = N * c_move + S_est * (20.0 + 10.0 * ((key_bits + 7) / 8)) + rest;
-    return run < 0.9 * chunked;
+    const auto rc = costs(k, rest_keys, S_est);
+    return rc.first < 0.9 * rc.second;
+  };
+  // after run discovery: the actual run count must still pay (the probe's
+  // evenly spaced blocks can over-sample a skewed head)
+  auto still_worth = [&](uint32_t k, const std::vector<uint32_t>& rest_keys, uint64_t S) -> bool {
+    if (rs_mode == 1) return true;
+    const auto rc = costs(k, rest_keys, (double)S);
+    return rc.first < rc.second;
   };
   if (!disabled && g.check_range && g.prefix.empty() && m >= 1 && N >= min_rows) {
     auto* xc = m >= 2 ? ws.get<uint32_t>("rowsC_c", N * R) : nullptr;
     auto* xv = m >= 2 ? ws.get<double>("rowsC_v", N) : nullptr;
     const uint32_t k1 = g.keys[0], km = g.keys[m - 1];
-    if (candidate(k1) && worth_it(k1, std::vector<uint32_t>(g.keys.begin() + 1, g.keys.end()))) {
-      if (try_run_sort(c, t, src_c, src_v, m == 1 ? dst_c : xc, m == 1 ? dst_v : xv, k1)) {
+    const std::vector<uint32_t> rest1(g.keys.begin() + 1, g.keys.end());
+    const std::vector<uint32_t> restm(g.keys.begin(), g.keys.end() - 1);
+    if (candidate(k1) && worth_it(k1, rest1)) {
+      if (try_run_sort(c, t, src_c, src_v, m == 1 ? dst_c : xc, m == 1 ? dst_v : xv, k1,
+                       [&](uint64_t S) { return still_worth(k1, rest1, S); })) {
         if (m >= 2) {
           Group rest;
           rest.prefix = g.prefix;
@@ -3004,9 +3034,9 @@ void exec_group(Ctx& c, const TensorView& t, const uint32_t* src_c, const double
         }
         return;
       }
-    } else if (m >= 2 && candidate(km) &&
-               worth_it(km, std::vector<uint32_t>(g.keys.begin(), g.keys.end() - 1))) {
-      if (try_run_sort(c, t, src_c, src_v, xc, xv, km)) {
+    } else if (m >= 2 && candidate(km) && worth_it(km, restm)) {
+      if (try_run_sort(c, t, src_c, src_v, xc, xv, km,
+                       [&](uint64_t S) { return still_worth(km, restm, S); })) {
         Group rest;
         rest.prefix = g.prefix;
         rest.keys.assign(g.keys.begin(), g.keys.end() - 1);

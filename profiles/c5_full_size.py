@@ -1,0 +1,117 @@
+"""Config-5 shape at full size on one GPU: seeded Zipf(1.05) rows over
+4821207x1774269x1805187, canonicalised on the device, deduplicated, exactly N
+unique rows kept by a seeded subset; then each target timed with CUDA events
+plus the library's per-class profile."""
+import faulthandler
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))  # repo root
+sys.path.insert(0, ROOT)
+import paper_2005_10427_b200 as qd  # noqa: E402
+from paper_2005_10427_b200 import synth  # noqa: E402
+
+faulthandler.dump_traceback_later(240, exit=True)
+cfg = synth.CONFIGS["c5"]
+N = int(sys.argv[1]) if len(sys.argv) > 1 else cfg.nnz
+reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+dev = "cuda"
+g = torch.Generator(device=dev)
+g.manual_seed(cfg.seed)
+r = 3
+# Zipf(1.05) draws repeat often in the head values: ~1.4 draws per unique
+# row at this size.  Coordinates are drawn first (values only for the kept
+# rows), canonicalised and deduplicated in three parts split on mode 0 (the
+# parts' outputs concatenate in order), then exactly N of the unique rows
+# are kept by a seeded uniform subset (a subsequence stays sorted).
+M = int(N * 1.5) + 1024
+t0 = time.time()
+raw = torch.empty((M, r), dtype=torch.int32, device=dev)
+for j, d in enumerate(cfg.dims):
+    cdf = torch.from_numpy(synth._zipf_cdf(d, cfg.s)).to(dev)
+    for a in range(0, M, 1 << 28):
+        b = min(M, a + (1 << 28))
+        u = torch.rand(b - a, generator=g, device=dev, dtype=torch.float64)
+        raw[a:b, j] = torch.searchsorted(cdf, u, right=True).clamp_(max=d - 1).to(torch.int32)
+        del u
+    del cdf
+smp = raw[:1 << 24, 0].double().sort().values
+nparts = int(os.environ.get("C5_PARTS", "3"))
+cuts = [0] + [int(smp[k * len(smp) // nparts].item()) + 1 for k in range(1, nparts)] + [(1 << 31) - 1]
+del smp
+print("drawn", M, "cuts", cuts, f"{time.time() - t0:.1f} s", flush=True)
+sp = torch.cuda.current_stream().cuda_stream
+uniq = []
+for lo, hi in zip(cuts[:-1], cuts[1:]):
+    half = (raw[:, 0] >= lo) & (raw[:, 0] < hi)
+    part = raw[half].reshape(-1).contiguous()
+    del half
+    m = part.numel() // r
+    dummy = torch.zeros(m, dtype=torch.float64, device=dev)
+    po = torch.empty_like(part)
+    pv = torch.empty_like(dummy)
+    ws = qd.Workspace(0)
+    qd.sort_rows_by_device(r, cfg.dims, m, part.data_ptr(), dummy.data_ptr(), po.data_ptr(),
+                           pv.data_ptr(), 0, m, [0, 1, 2], ws, sp)
+    torch.cuda.synchronize()
+    ws.close()
+    del part, dummy, pv, ws
+    s = po.view(m, r)
+    head = torch.ones(m, dtype=torch.bool, device=dev)
+    head[1:] = (s[1:] != s[:-1]).any(1)
+    uniq.append(s[head])
+    print("part", lo, hi, m, uniq[-1].shape[0], f"{time.time() - t0:.1f} s", flush=True)
+    del s, po, head
+    torch.cuda.empty_cache()
+del raw
+torch.cuda.empty_cache()
+U = sum(u.shape[0] for u in uniq)
+assert U >= N, (U, N)
+# a seeded uniform N-subset (torch.randperm stalls at this size)
+keep = torch.rand(U, generator=g, device=dev, dtype=torch.float64).argsort()[:N].sort().values
+ci = torch.cat(uniq)[keep].reshape(-1).contiguous()
+del uniq, keep
+vi = torch.rand(N, generator=g, device=dev, dtype=torch.float64)
+torch.cuda.synchronize()
+torch.cuda.empty_cache()
+ws = qd.Workspace(0)
+print(f"generated {N} unique rows (from {M} draws, {U} unique) in {time.time() - t0:.1f} s",
+      flush=True)
+faulthandler.dump_traceback_later(240, exit=True)
+assert qd.is_sorted_device(r, N, ci.data_ptr(), [0, 1, 2], ws, sp)
+co = torch.empty_like(ci)
+vo = torch.empty_like(vi)
+res = {}
+for t in cfg.targets:
+    def once():
+        qd.transpose_device(r, cfg.dims, N, ci.data_ptr(), vi.data_ptr(), co.data_ptr(),
+                            vo.data_ptr(), t, qd.SortStrategy.quesadilla(), ws, sp)
+    once()
+    torch.cuda.synchronize()
+    assert qd.is_sorted_device(r, N, co.data_ptr(), t, ws, sp)
+    ms = []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        once()
+        e1.record()
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    ws.profile(True)
+    ws.profile_reset()
+    once()
+    torch.cuda.synchronize()
+    prof = ws.profile_stats()
+    ws.profile(False)
+    key = "".join(map(str, t))
+    res[key] = {"ms_min": round(min(ms), 3), "Gnnz_s": round(N / min(ms) / 1e6, 2),
+                "classes": {k: {"n": v["launches"], "ms": round(v["ms"], 3),
+                                "GBs": round(v["bytes"] / v["ms"] / 1e6, 1) if v["ms"] else 0}
+                            for k, v in prof.items() if v["launches"]}}
+    print(key, json.dumps(res[key]), flush=True)
+print(json.dumps({"config": "c5 full size, 1 GPU", "nnz": N, "targets": res}))
