@@ -269,11 +269,36 @@ struct ScatterArgs {
   uint32_t nd_shift, nd_mask;  // PK output: next digit = (packed >> nd_shift) & nd_mask
   DigitSpec ndig;              // unpacked output: next digit of the coordinates
   const uint32_t* run_prefix;  // implicit prefix modes per large run (PackSpec::n_imp)
+  int vec_out;                 // AoS output rows may use 16-byte stores (rank 4, aligned base)
 };
 
 // ---------------------------------------------------------------------------
 // device helpers
 // ---------------------------------------------------------------------------
+
+// One AoS row of RT coordinates: rank 4 as one 16-byte access (the caller
+// guarantees 16-byte alignment), other ranks word by word.  (Rank 3 as an
+// 8-byte + 4-byte pair chosen by the row's word parity measured 1.5 % slower
+// on c2: the selects cost more than the saved shared-memory wavefronts.)
+template <int RT>
+__device__ __forceinline__ void load_row_words(const uint32_t* w, uint32_t (&cv)[RT]) {
+  if constexpr (RT == 4) {
+    const uint4 x = *reinterpret_cast<const uint4*>(w);
+    cv[0] = x.x; cv[1] = x.y; cv[2] = x.z; cv[3] = x.w;
+  } else {
+#pragma unroll
+    for (int m = 0; m < RT; ++m) cv[m] = w[m];
+  }
+}
+template <int RT>
+__device__ __forceinline__ void store_row_words(uint32_t* w, const uint32_t (&cv)[RT]) {
+  if constexpr (RT == 4) {
+    __stcs(reinterpret_cast<uint4*>(w), make_uint4(cv[0], cv[1], cv[2], cv[3]));
+  } else {
+#pragma unroll
+    for (int m = 0; m < RT; ++m) __stcs(w + m, cv[m]);
+  }
+}
 
 __device__ __forceinline__ uint32_t digit_of(const uint32_t* row, const DigitSpec& d) {
   if (d.lookup) {
@@ -1212,6 +1237,19 @@ __global__ void __launch_bounds__(kSortThreads, QD_SCATTER_CTAS * 512 / kSortThr
 #pragma unroll
       for (int m = 0; m < (RT > 0 ? RT : 1); ++m) cb[m] = mbase(m);
     }
+    // AoS tiles: a row's coordinates with vector shared loads (rank 4 needs a
+    // 16-byte aligned staging head; tile-uniform)
+    const bool vec_in = IN == kAoS && RT && (RT != 4 || (s_ofsb[0] & 15u) == 0);
+    auto load_cv = [&](uint32_t i, uint32_t (&cv)[RT > 0 ? RT : 1]) {
+      if (vec_in) {
+        load_row_words<(RT > 0 ? RT : 1)>(
+            reinterpret_cast<const uint32_t*>(scb + cb[0] + i * rstride), cv);
+      } else {
+#pragma unroll
+        for (int m = 0; m < (RT > 0 ? RT : 1); ++m)
+          cv[m] = *reinterpret_cast<const uint32_t*>(scb + cb[m] + i * rstride);
+      }
+    };
     const uint32_t vbase = IN == kPK ? 0u : (uint32_t)(span_dst(b, R) - scb) + s_ofsb[R];
     for (uint32_t j = threadIdx.x; j < n; j += kSortThreads) {
       const uint32_t sj = s_sorted[j];
@@ -1254,18 +1292,28 @@ __global__ void __launch_bounds__(kSortThreads, QD_SCATTER_CTAS * 512 / kSortThr
               for (int m = 0; m < (RT > 0 ? RT : 1); ++m)
                 if (mk == (uint32_t)m) cv[m] = v;
             }
+            if (RT != 4 || a.vec_out) {
+              store_row_words<(RT > 0 ? RT : 1)>(o, cv);
+            } else {
 #pragma unroll
-            for (int m = 0; m < (RT > 0 ? RT : 1); ++m) __stcs(o + m, cv[m]);
+              for (int m = 0; m < (RT > 0 ? RT : 1); ++m) __stcs(o + m, cv[m]);
+            }
           } else if (MX) {
             unpack_coords(a.pack, R, row.x, [&](uint32_t m, uint32_t v) { __stcs(o + m, v); });
             for (uint32_t k = 0; k < a.pack.n_imp; ++k)
               __stcs(o + a.pack.imp_mode[k],
                      __ldg(a.run_prefix + (size_t)s_cd[b].li * a.pack.n_imp + k));
           } else if (RT) {
+            uint32_t cv[RT > 0 ? RT : 1];
 #pragma unroll
             for (int m = 0; m < (RT > 0 ? RT : 1); ++m)
-              __stcs(o + m, (uint32_t)(row.x >> a.pack.off[m]) &
-                                (uint32_t)((1ull << a.pack.width[m]) - 1ull));
+              cv[m] = (uint32_t)(row.x >> a.pack.off[m]) & (uint32_t)((1ull << a.pack.width[m]) - 1ull);
+            if (RT != 4 || a.vec_out) {
+              store_row_words<(RT > 0 ? RT : 1)>(o, cv);
+            } else {
+#pragma unroll
+              for (int m = 0; m < (RT > 0 ? RT : 1); ++m) __stcs(o + m, cv[m]);
+            }
           } else {
             for (uint32_t m = 0; m < R; ++m)
               __stcs(o + m, (uint32_t)(row.x >> a.pack.off[m]) &
@@ -1280,11 +1328,10 @@ __global__ void __launch_bounds__(kSortThreads, QD_SCATTER_CTAS * 512 / kSortThr
         unsigned long long pk = 0;
         if (MX && RT) {
           uint32_t cv[RT > 0 ? RT : 1];
+          load_cv(i, cv);
 #pragma unroll
-          for (int m = 0; m < (RT > 0 ? RT : 1); ++m) {
-            cv[m] = *reinterpret_cast<const uint32_t*>(scb + cb[m] + i * rstride);
+          for (int m = 0; m < (RT > 0 ? RT : 1); ++m)
             if (a.pack.width[m]) pk |= (unsigned long long)cv[m] << a.pack.off[m];
-          }
           // fully unrolled so cv stays in registers (static indices only)
           unsigned long long hi = 0;
 #pragma unroll
@@ -1301,10 +1348,10 @@ __global__ void __launch_bounds__(kSortThreads, QD_SCATTER_CTAS * 512 / kSortThr
         } else if (MX) {
           pk = pack_coords(a.pack, R, [&](uint32_t m) { return coord(i, m); });
         } else if (RT) {
+          uint32_t cv[RT > 0 ? RT : 1];
+          load_cv(i, cv);
 #pragma unroll
-          for (int m = 0; m < (RT > 0 ? RT : 1); ++m)
-            pk |= (unsigned long long)*reinterpret_cast<const uint32_t*>(scb + cb[m] + i * rstride)
-                  << a.pack.off[m];
+          for (int m = 0; m < (RT > 0 ? RT : 1); ++m) pk |= (unsigned long long)cv[m] << a.pack.off[m];
         } else {
           for (uint32_t m = 0; m < R; ++m)
             pk |= (unsigned long long)coord(i, m) << a.pack.off[m];
@@ -1314,7 +1361,17 @@ __global__ void __launch_bounds__(kSortThreads, QD_SCATTER_CTAS * 512 / kSortThr
         if (a.next_dig) __stcs(a.next_dig + dst, (uint8_t)((pk >> a.nd_shift) & a.nd_mask));
         continue;
       }
-      if (RT) {
+      if (RT && OUT == kAoS && IN == kAoS) {
+        uint32_t cv[RT > 0 ? RT : 1];
+        load_cv(i, cv);
+        uint32_t* o = a.out.c + dst * (RT > 0 ? RT : 1);
+        if (RT != 4 || a.vec_out) {
+          store_row_words<(RT > 0 ? RT : 1)>(o, cv);
+        } else {
+#pragma unroll
+          for (int m = 0; m < (RT > 0 ? RT : 1); ++m) __stcs(o + m, cv[m]);
+        }
+      } else if (RT) {
 #pragma unroll
         for (int m = 0; m < (RT > 0 ? RT : 1); ++m) {
           const uint32_t x = *reinterpret_cast<const uint32_t*>(scb + cb[m] + i * rstride);
@@ -2580,6 +2637,15 @@ uint32_t chunk_tiles(const Workspace& ws, uint64_t rows, uint32_t T) {
   return (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(kChunkTiles, tiles / (8 * ctas)));
 }
 
+// QD_VEC_ROWS=0: scalar rank-4 row stores in k_scatter's store loop (A/B switch)
+static bool vec_rows_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("QD_VEC_ROWS");
+    return !(e && atoi(e) == 0);
+  }();
+  return on;
+}
+
 // One stable counting pass of digit `dig` over the chunks: chunk histograms,
 // (run, bin, chunk) exclusive scan, chunk-ordered scatter.
 void run_pass(Ctx& c, uint32_t R, uint64_t N, uint32_t T, Rows in, RowsOut out,
@@ -2638,6 +2704,7 @@ void run_pass(Ctx& c, uint32_t R, uint64_t N, uint32_t T, Rows in, RowsOut out,
   a.nd_mask = nd_mask;
   if (next_dig) a.ndig = *next_dig;
   a.run_prefix = run_prefix;
+  a.vec_out = out.fmt == kAoS && (reinterpret_cast<uintptr_t>(out.c) & 15u) == 0 && vec_rows_enabled();
   if (const char* e = getenv("QD_SCATTER_DBG")) a.dbg = atoi(e);
   if (a.dbg & 2) {
     a.dbg_t = ws.get<unsigned long long>("dbg_t", 16);
