@@ -1466,19 +1466,28 @@ __global__ void __launch_bounds__(kLocalThreads) k_local(LocalArgs a) {
     }
     __syncthreads();
     const uint64_t sa = s_sa;
-    // runs sa .. sa+k starting in [lo, hi) and small; at most TL of them
-    for (uint32_t k = threadIdx.x; k <= a.TL; k += kLocalThreads) {
-      const uint64_t s = sa + k;
-      bool stop = true;
-      if (s < S) {
-        const unsigned long long b = a.seg_start[s], e = a.seg_start[s + 1];
-        s_seg[k] = b;
-        stop = b >= hi || (e - b) > a.TL;
-        if (!stop) s_seg[k + 1] = e;
+    // runs sa .. sa+k starting in [lo, hi) and small; at most TL of them.
+    // Read in batches that stop at the first batch holding the end: 64
+    // entries first (chunks of a few hundred-row runs end there), then
+    // kLocalThreads at a time (chunks of tiny runs)
+    for (uint32_t base = 0, width = 64; base <= a.TL; base += width, width = kLocalThreads) {
+      const uint32_t k = base + threadIdx.x;
+      if (threadIdx.x < width && k <= a.TL) {
+        const uint64_t s = sa + k;
+        bool stop = true;
+        if (s < S) {
+          const unsigned long long b = a.seg_start[s], e = a.seg_start[s + 1];
+          s_seg[k] = b;
+          stop = b >= hi || (e - b) > a.TL;
+          if (!stop) s_seg[k + 1] = e;
+        }
+        if (stop) atomicMin(&s_nsl, k);
       }
-      if (stop) atomicMin(&s_nsl, k);
+      __syncthreads();
+      const bool done = s_nsl != 0xFFFFFFFFu;
+      __syncthreads();  // every thread has read s_nsl before the next batch updates it
+      if (done) break;
     }
-    __syncthreads();
     nsl = min(s_nsl, a.TL + 1);
     if (nsl == 0) return;
     r0 = s_seg[0];
