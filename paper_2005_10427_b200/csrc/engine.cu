@@ -82,6 +82,9 @@ constexpr int kMaxRounds = QD_MAX_TILE / kSortThreads;  // 32-row rounds per war
 #ifndef QD_EARLY_ADVANCE
 #define QD_EARLY_ADVANCE 1
 #endif
+#ifndef QD_FULL_ROUNDS
+#define QD_FULL_ROUNDS 1
+#endif
 #ifndef QD_RANK_BCAST
 #define QD_RANK_BCAST 1
 #endif
@@ -1115,7 +1118,13 @@ __global__ void __launch_bounds__(kSortThreads, QD_SCATTER_CTAS * 512 / kSortThr
     // [w*ipw, (w+1)*ipw) and walks them in rounds of 32 (rank order = row
     // order); packed[r] = (rank within the warp's equal digits << 8) | digit.
     const uint32_t w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // rows per warp rounded up to whole 32-row rounds: every round but the
+    // tile's last is full (trailing warps may get fewer rows or none)
+#if QD_FULL_ROUNDS
+    const uint32_t ipw = (((n + kSortWarps - 1) / kSortWarps) + 31u) & ~31u;
+#else
     const uint32_t ipw = (n + kSortWarps - 1) / kSortWarps;
+#endif
     const uint32_t lo = w * ipw, hi = min(n, lo + ipw);
     uint16_t* wh = s_whist + w * kBins;
     const unsigned below = (1u << lane) - 1u;
@@ -1552,7 +1561,11 @@ __global__ void __launch_bounds__(kLocalThreads) k_local(LocalArgs a) {
   }
   const uint32_t nbits = kb + ceil_log2_dev(nsl);
   const uint32_t passes = (nbits + kRadixLog - 1) / kRadixLog;
+#if QD_FULL_ROUNDS
+  const uint32_t ipw = (((n + kLocalWarps - 1) / kLocalWarps) + 31u) & ~31u;  // whole rounds
+#else
   const uint32_t ipw = (n + kLocalWarps - 1) / kLocalWarps;
+#endif
   uint16_t* cur = s_p0;
   uint16_t* nxt = s_p1;
   for (uint32_t q = 0; q < passes; ++q) {
