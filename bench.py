@@ -42,7 +42,7 @@ sys.path.insert(0, ROOT)
 def parse_args():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--steps", type=int, default=30)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--config", default="c2")
@@ -56,6 +56,9 @@ def parse_args():
 # clocks sampled during the timed region
 # ---------------------------------------------------------------------------
 class ClockSampler:
+    """SM clock, max clock and throttle reasons sampled every ~5 ms through NVML
+    on a background thread while the timed region runs (nvidia-smi's query
+    loop as the fallback when NVML is unavailable)."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -64,8 +67,29 @@ class ClockSampler:
         self.device = device
         self.lines = []
         self.proc = None
+        self.nvml = None
+        self.stop = threading.Event()
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            h = None
+            try:
+                import torch
+                pr = torch.cuda.get_device_properties(device)
+                bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+                h = N.nvmlDeviceGetHandleByPciBusId(bus)
+            except Exception:
+                h = N.nvmlDeviceGetHandleByIndex(device)
+            self.nvml, self.h = N, h
+            self.max_mhz = float(N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM))
+        except Exception:
+            self.nvml = None
 
     def __enter__(self):
+        if self.nvml is not None:
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+            return self
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
@@ -77,11 +101,31 @@ class ClockSampler:
             self.proc = None
         return self
 
+    def _poll(self):
+        N, h = self.nvml, self.h
+        bits = [("hw_slowdown", N.nvmlClocksEventReasonHwSlowdown),
+                ("hw_thermal_slowdown", N.nvmlClocksEventReasonHwThermalSlowdown),
+                ("sw_thermal_slowdown", N.nvmlClocksEventReasonSwThermalSlowdown),
+                ("sw_power_cap", N.nvmlClocksEventReasonSwPowerCap)]
+        while not self.stop.is_set():
+            try:
+                sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+                rs = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                flags = ["Active" if rs & b else "Not Active" for _, b in bits]
+                self.lines.append(", ".join([str(self.device), str(sm), str(self.max_mhz), "0",
+                                             hex(rs)] + flags))
+            except Exception:
+                pass
+            self.stop.wait(0.005)
+
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
     def __exit__(self, *a):
+        self.stop.set()
+        if self.nvml is not None:
+            self.t.join(timeout=1)
         if self.proc:
             self.proc.terminate()
             try:
