@@ -503,12 +503,21 @@ __device__ __forceinline__ uint32_t bin_offsets(uint16_t* s_whist, uint32_t* s_w
   return cnt;
 }
 
+// Word offset of g + a inside its 16-byte line (any caller pointer: device
+// buffers need only be 4-byte aligned), and the same for doubles.
+__device__ __forceinline__ uint32_t words_head(const uint32_t* g, unsigned long long a) {
+  return (uint32_t)((reinterpret_cast<uintptr_t>(g + a) >> 2) & 3u);
+}
+__device__ __forceinline__ uint32_t doubles_head(const double* g, unsigned long long a) {
+  return (uint32_t)((reinterpret_cast<uintptr_t>(g + a) >> 3) & 1u);
+}
+
 // Load words [a, a+nw) of g into s_raw so that word a+k lands at
-// s_raw[(a & 3) + k]; 16-byte vector loads for the aligned body.
+// s_raw[words_head(g, a) + k]; 16-byte vector loads for the aligned body.
 template <int NT = kThreads>
 __device__ __forceinline__ void load_words(uint32_t* s_raw, const uint32_t* g,
                                            unsigned long long a, uint32_t nw) {
-  const uint32_t h = (uint32_t)(a & 3ull);
+  const uint32_t h = words_head(g, a);
   const uint32_t* gb = g + (a - h);
   const uint32_t total = h + nw;
   const uint32_t nvec = total >> 2;
@@ -519,11 +528,11 @@ __device__ __forceinline__ void load_words(uint32_t* s_raw, const uint32_t* g,
   for (uint32_t w = (nvec << 2) + threadIdx.x; w < total; w += NT) s_raw[w] = __ldcs(gb + w);
 }
 
-// Same for doubles: element a+k lands at s_raw[(a & 1) + k].
+// Same for doubles: element a+k lands at s_raw[doubles_head(g, a) + k].
 template <int NT = kThreads>
 __device__ __forceinline__ void load_doubles(double* s_raw, const double* g,
                                              unsigned long long a, uint32_t n) {
-  const uint32_t h = (uint32_t)(a & 1ull);
+  const uint32_t h = doubles_head(g, a);
   const double* gb = g + (a - h);
   const uint32_t total = h + n;
   const uint32_t nvec = total >> 1;
@@ -1508,8 +1517,8 @@ __global__ void __launch_bounds__(kLocalThreads) k_local(LocalArgs a) {
   load_words<kLocalThreads>(s_craw, a.in_c, r0 * R, n * R);
   load_doubles<kLocalThreads>(s_vraw, a.in_v, r0, n);
   __syncthreads();
-  const uint32_t* s_c = s_craw + (uint32_t)((r0 * R) & 3ull);
-  const double* s_v = s_vraw + (uint32_t)(r0 & 1ull);
+  const uint32_t* s_c = s_craw + words_head(a.in_c, r0 * R);
+  const double* s_v = s_vraw + doubles_head(a.in_v, r0);
 
   const uint32_t kb = a.key.total_bits;
   // the key's first (up to) four fields in registers, hoisted out of the row
@@ -3022,7 +3031,7 @@ bool try_run_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const doub
   if (R == 3)
     k_move_runs2<3><<<(uint32_t)ntiles, kMoveThreads, 0, c.st>>>(src_c, src_v, dst_c, dst_v, R, N,
                                                                  rv1, dsto, S, first);
-  else if (R == 4)
+  else if (R == 4 && ((reinterpret_cast<uintptr_t>(src_c) | reinterpret_cast<uintptr_t>(dst_c)) & 15u) == 0)
     k_move_runs2<4><<<(uint32_t)ntiles, kMoveThreads, 0, c.st>>>(src_c, src_v, dst_c, dst_v, R, N,
                                                                  rv1, dsto, S, first);
   else

@@ -324,6 +324,43 @@ def test_device_api_with_torch(ws):
     assert not qd.is_sorted_device(3, t.nnz(), co.data_ptr(), [0, 1, 2], ws=ws)
 
 
+@pytest.mark.parametrize("shift", [0, 1, 2, 3])
+def test_device_api_unaligned_rank4_buffers(ws, shift):
+    """Rank-4 rows take 16-byte shared loads / global stores in k_scatter when
+    the staged tile and the output are 16-byte aligned; device buffers that
+    start 4, 8 or 12 bytes off (any caller pointer) must take the word path
+    and give the same bytes.  Multi-pass groups (AoS and packed) on both."""
+    import torch
+    rng = np.random.default_rng(40 + shift)
+    for dims, target, env in (([40, 3000, 900, 70], [3, 2, 1, 0], {}),          # packed rows
+                              ([3000, 2 ** 20, 2 ** 22, 1500], [3, 2, 1, 0], {}),  # AoS
+                              ([3000, 2 ** 20, 2 ** 22, 1500], [0, 3, 1, 2], {}),
+                              ([300, 40, 2 ** 22, 1500], [1, 0, 2, 3],        # run move
+                               {"QD_RUN_SORT": "1", "QD_RUN_SORT_MIN_ROWS": "1"})):
+        old = {k: os.environ.get(k) for k in env}
+        os.environ.update(env)
+        t = rand_tensor(rng, dims, 200_000)
+        n = t.nnz()
+        cbuf = torch.zeros(n * 4 + 8, dtype=torch.int32, device="cuda")
+        obuf = torch.zeros(n * 4 + 8, dtype=torch.int32, device="cuda")
+        ci = cbuf[shift:shift + n * 4]
+        ci.copy_(torch.from_numpy(t.coords.view(np.int32)))
+        co = obuf[(4 - shift) % 4:(4 - shift) % 4 + n * 4]
+        vi = torch.from_numpy(t.values).cuda()
+        vo = torch.empty_like(vi)
+        qd.transpose_device(4, dims, n, ci.data_ptr(), vi.data_ptr(), co.data_ptr(),
+                            vo.data_ptr(), target, qd.SortStrategy.quesadilla(), ws,
+                            torch.cuda.current_stream().cuda_stream)
+        for k, x in old.items():
+            if x is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = x
+        c, v, _ = ORC.transpose(dims, t.coords, t.values, target)
+        assert np.array_equal(co.cpu().numpy().view(np.uint32), c), (dims, target, shift)
+        assert np.array_equal(vo.cpu().numpy().view(np.uint64), v.view(np.uint64))
+
+
 # --- multi-GPU building blocks on one GPU ---------------------------------------
 
 def test_partition_rows_and_mode_hist(ws):
