@@ -325,30 +325,37 @@ def test_device_api_with_torch(ws):
 
 
 @pytest.mark.parametrize("shift", [0, 1, 2, 3])
-def test_device_api_unaligned_rank4_buffers(ws, shift):
+def test_device_api_unaligned_buffers(ws, shift):
     """Rank-4 rows take 16-byte shared loads / global stores in k_scatter when
     the staged tile and the output are 16-byte aligned; device buffers that
-    start 4, 8 or 12 bytes off (any caller pointer) must take the word path
-    and give the same bytes.  Multi-pass groups (AoS and packed) on both."""
+    start 4, 8 or 12 bytes off (any caller pointer; values 8 bytes off) must
+    take the word path and give the same bytes.  Packed, AoS, implicit-prefix,
+    run-move, k_local (small runs) and rank-5 paths."""
     import torch
     rng = np.random.default_rng(40 + shift)
     for dims, target, env in (([40, 3000, 900, 70], [3, 2, 1, 0], {}),          # packed rows
                               ([3000, 2 ** 20, 2 ** 22, 1500], [3, 2, 1, 0], {}),  # AoS
                               ([3000, 2 ** 20, 2 ** 22, 1500], [0, 3, 1, 2], {}),
                               ([300, 40, 2 ** 22, 1500], [1, 0, 2, 3],        # run move
-                               {"QD_RUN_SORT": "1", "QD_RUN_SORT_MIN_ROWS": "1"})):
+                               {"QD_RUN_SORT": "1", "QD_RUN_SORT_MIN_ROWS": "1"}),
+                              ([20000, 300, 5000], [0, 2, 1], {}),              # k_local
+                              ([700, 900, 300, 20, 50], [4, 3, 2, 1, 0], {})):  # rank 5
         old = {k: os.environ.get(k) for k in env}
         os.environ.update(env)
         t = rand_tensor(rng, dims, 200_000)
-        n = t.nnz()
-        cbuf = torch.zeros(n * 4 + 8, dtype=torch.int32, device="cuda")
-        obuf = torch.zeros(n * 4 + 8, dtype=torch.int32, device="cuda")
-        ci = cbuf[shift:shift + n * 4]
+        n, R = t.nnz(), len(dims)
+        cbuf = torch.zeros(n * R + 8, dtype=torch.int32, device="cuda")
+        obuf = torch.zeros(n * R + 8, dtype=torch.int32, device="cuda")
+        ci = cbuf[shift:shift + n * R]
         ci.copy_(torch.from_numpy(t.coords.view(np.int32)))
-        co = obuf[(4 - shift) % 4:(4 - shift) % 4 + n * 4]
-        vi = torch.from_numpy(t.values).cuda()
-        vo = torch.empty_like(vi)
-        qd.transpose_device(4, dims, n, ci.data_ptr(), vi.data_ptr(), co.data_ptr(),
+        co = obuf[(4 - shift) % 4:(4 - shift) % 4 + n * R]
+        # values 8 bytes off a 16-byte line on odd shifts
+        vbuf = torch.zeros(n + 2, dtype=torch.float64, device="cuda")
+        vi = vbuf[shift & 1:(shift & 1) + n]
+        vi.copy_(torch.from_numpy(t.values))
+        vobuf = torch.zeros(n + 2, dtype=torch.float64, device="cuda")
+        vo = vobuf[1 - (shift & 1):1 - (shift & 1) + n]
+        qd.transpose_device(R, dims, n, ci.data_ptr(), vi.data_ptr(), co.data_ptr(),
                             vo.data_ptr(), target, qd.SortStrategy.quesadilla(), ws,
                             torch.cuda.current_stream().cuda_stream)
         for k, x in old.items():
