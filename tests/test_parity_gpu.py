@@ -368,6 +368,37 @@ def test_device_api_unaligned_buffers(ws, shift):
         assert np.array_equal(vo.cpu().numpy().view(np.uint64), v.view(np.uint64))
 
 
+def test_two_workspaces_on_two_threads():
+    """Distinct workspaces may be used concurrently from different host threads
+    (the reference forbids only sharing one Workspace, sort.hpp:12-13): no
+    library-global state may leak between the calls."""
+    import threading
+    rng = np.random.default_rng(77)
+    jobs = [(rand_tensor(rng, [300, 2000, 900], 400_000), [2, 1, 0]),
+            (rand_tensor(rng, [50, 7000, 40, 30], 300_000), [0, 3, 1, 2])]
+    want = [ORC.transpose(t.dims, t.coords, t.values, tg) for t, tg in jobs]
+    errors = []
+
+    def run(k):
+        try:
+            w = qd.Workspace(0)
+            t, tg = jobs[k]
+            for _ in range(4):
+                out = qd.transpose(t, tg, qd.SortStrategy.quesadilla(), None, w)
+                if not same(out, want[k][0], want[k][1]):
+                    errors.append(f"job {k}: output differs")
+            w.close()
+        except Exception as e:  # noqa: BLE001
+            errors.append(f"job {k}: {e!r}")
+
+    th = [threading.Thread(target=run, args=(k,)) for k in range(2)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    assert not errors, errors
+
+
 # --- multi-GPU building blocks on one GPU ---------------------------------------
 
 def test_partition_rows_and_mode_hist(ws):
