@@ -11,8 +11,10 @@ moves 5 x 76.9M nonzeros.
 
   value : whole-job Mnnz/s, inputs resident in HBM, device-timed (CUDA events
           around exactly K steps, max over ranks)
-  e2e   : the same metric through the host C-ABI entry (qd_transpose_inplace on
-          pinned host buffers): H2D + GPU passes + D2H inside the timed region
+  e2e   : the same metric through the host C-ABI entry (qd_transpose_inplace_async
+          + qd_workspace_synchronize on pinned host buffers, one call per target,
+          K steps enqueued back to back): every H2D + GPU pass + D2H inside the
+          timed region; the per-step synchronised figure is reported beside it
   roofline : dominant kernel class, algorithmic bytes / its event-timed
           duration (recorded by the library on its launch stream) vs the
           measured HBM copy peak (MEASURED_PEAKS.json)
