@@ -237,6 +237,24 @@ qd_status qd_partition_rows_device(uint32_t rank, uint64_t nnz,
                                    uint32_t n_parts, uint32_t* d_coords_out,
                                    double* d_values_out, uint64_t* part_counts,
                                    qd_workspace* ws, void* stream);
+/* The same partition fused with the exchange that follows it (SURVEY §8e
+ * steps 3-4): part p's rows are written straight into destination p — device
+ * addresses peer_coords[p] / peer_values[p] (on a multi-GPU box: NVLink peer
+ * mappings of rank p's receive buffer, e.g. torch symmetric memory), starting
+ * at row peer_row_offsets[p] (this rank's place among the senders to p, in
+ * source-rank order) — instead of a local buffer followed by an all-to-all.
+ * Replaces the ncclSend/ncclRecv group of the exchange step; the caller
+ * orders the receivers' reads after every sender's kernel (stream sync +
+ * barrier). */
+qd_status qd_partition_rows_to_peers_device(uint32_t rank, uint64_t nnz,
+                                            const uint32_t* d_coords_in,
+                                            const double* d_values_in, uint32_t mode,
+                                            uint32_t dim, const uint32_t* d_lookup,
+                                            uint32_t n_parts, const uint64_t* peer_coords,
+                                            const uint64_t* peer_values,
+                                            const uint64_t* peer_row_offsets,
+                                            uint64_t* part_counts, qd_workspace* ws,
+                                            void* stream);
 
 #ifdef __cplusplus
 }

@@ -146,6 +146,10 @@ def lib():
                                                C.c_uint32, C.c_uint32, C.c_void_p, C.c_uint32,
                                                C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64),
                                                C.c_void_p, C.c_void_p]
+        _u64p = C.POINTER(C.c_uint64)
+        L.qd_partition_rows_to_peers_device.argtypes = [
+            C.c_uint32, C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p,
+            C.c_uint32, _u64p, _u64p, _u64p, _u64p, C.c_void_p, C.c_void_p]
         _lib = L
     return _lib
 
@@ -776,6 +780,21 @@ def partition_rows_device(rank, nnz, coords_in, values_in, mode, dim, lookup, n_
                                           mode, dim, C.c_void_p(lookup), n_parts,
                                           C.c_void_p(coords_out), C.c_void_p(values_out), counts,
                                           w.handle, C.c_void_p(stream)))
+    return [int(x) for x in counts]
+
+
+def partition_rows_to_peers_device(rank, nnz, coords_in, values_in, mode, dim, lookup, n_parts,
+                                   peer_coords, peer_values, peer_row_offsets, ws=None,
+                                   stream=0) -> List[int]:
+    """qd_partition_rows_to_peers_device: part p's rows written to device
+    addresses peer_coords[p] / peer_values[p] from row peer_row_offsets[p]."""
+    w = _ws(ws)
+    counts = (C.c_uint64 * n_parts)()
+    arr = lambda xs: (C.c_uint64 * n_parts)(*[int(x) for x in xs])  # noqa: E731
+    _check(lib().qd_partition_rows_to_peers_device(
+        rank, nnz, C.c_void_p(coords_in), C.c_void_p(values_in), mode, dim, C.c_void_p(lookup),
+        n_parts, arr(peer_coords), arr(peer_values), arr(peer_row_offsets), counts, w.handle,
+        C.c_void_p(stream)))
     return [int(x) for x in counts]
 
 

@@ -415,4 +415,24 @@ qd_status qd_partition_rows_device(uint32_t rank, uint64_t nnz, const uint32_t* 
   });
 }
 
+qd_status qd_partition_rows_to_peers_device(uint32_t rank, uint64_t nnz,
+                                            const uint32_t* d_coords_in,
+                                            const double* d_values_in, uint32_t mode,
+                                            uint32_t dim, const uint32_t* d_lookup,
+                                            uint32_t n_parts, const uint64_t* peer_coords,
+                                            const uint64_t* peer_values,
+                                            const uint64_t* peer_row_offsets,
+                                            uint64_t* part_counts, qd_workspace* ws,
+                                            void* stream) {
+  return guard([&] {
+    if (!ws) invalid("workspace is null");
+    if (!peer_coords || !peer_values || !peer_row_offsets) invalid("peer tables are null");
+    for (uint32_t p = 0; p < n_parts; ++p)
+      if (!peer_coords[p] || !peer_values[p]) invalid("null peer destination");
+    partition_rows_device(W(ws), rank, nnz, d_coords_in, d_values_in, mode, dim, d_lookup,
+                          n_parts, nullptr, nullptr, part_counts, stream, peer_coords,
+                          peer_values, peer_row_offsets);
+  });
+}
+
 }  // extern "C"

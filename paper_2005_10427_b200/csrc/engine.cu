@@ -252,6 +252,13 @@ struct ChunkHistArgs {
   const uint8_t* digits;       // this pass's digit per row, written by the previous scatter
 };
 
+// One destination of a peer-writing partition pass: part p's rows go to
+// (c, v) (device addresses, typically NVLink peer mappings of another rank's
+// receive buffer) starting at row `off`.
+struct PeerDest {
+  unsigned long long c, v, off;
+};
+
 struct ScatterArgs {
   int dbg;  // experiment switches (QD_SCATTER_DBG): 1 = skip global stores
   unsigned long long* dbg_t;  // QD_SCATTER_DBG & 2: per-phase clock totals
@@ -272,6 +279,7 @@ struct ScatterArgs {
   uint32_t nd_shift, nd_mask;  // PK output: next digit = (packed >> nd_shift) & nd_mask
   DigitSpec ndig;              // unpacked output: next digit of the coordinates
   const uint32_t* run_prefix;  // implicit prefix modes per large run (PackSpec::n_imp)
+  const PeerDest* peers;       // AoS output per bin (partition straight into peer buffers)
   int vec_out;                 // AoS output rows may use 16-byte stores (rank 4, aligned base)
 };
 
@@ -1062,6 +1070,7 @@ __global__ void __launch_bounds__(kSortThreads, QD_SCATTER_CTAS * 512 / kSortThr
 
   const Dig2 dg = dig2_of(a.dig);
   uint32_t phases = 0u;
+  long long peer_shift = 0;  // peers: destination row of this bin's first row minus its part start
   long long t_last = clock64();
 #define QD_TMARK(ph)                                           \
   if (a.dbg_t && threadIdx.x == 0) {                           \
@@ -1083,6 +1092,9 @@ __global__ void __launch_bounds__(kSortThreads, QD_SCATTER_CTAS * 512 / kSortThr
       const unsigned long long rs = a.run_start ? a.run_start[cd.li] : 0ull;
       s_run[threadIdx.x] =
           a.offs[cd.coff * kBins + (size_t)threadIdx.x * cd.nchunks + cd.cidx] - base0 + rs;
+      if (a.peers)  // part start = the bin's cursor in the run's first chunk
+        peer_shift = (long long)a.peers[threadIdx.x].off -
+                     (long long)(a.offs[cd.coff * kBins + (size_t)threadIdx.x * cd.nchunks] - base0 + rs);
     }
     {  // each warp clears its own histogram (no block barrier before ranking)
       uint16_t* whz = s_whist + (threadIdx.x >> 5) * kBins;
@@ -1225,7 +1237,7 @@ __global__ void __launch_bounds__(kSortThreads, QD_SCATTER_CTAS * 512 / kSortThr
         const uint32_t start = base + incl - cnt;
         s_start[threadIdx.x] = start;
         const unsigned long long r0 = s_run[threadIdx.x];
-        s_gbase[threadIdx.x] = (long long)r0 - (long long)start;
+        s_gbase[threadIdx.x] = (long long)r0 - (long long)start + peer_shift;
         s_run[threadIdx.x] = r0 + cnt;
       }
     }
@@ -1342,6 +1354,11 @@ __global__ void __launch_bounds__(kSortThreads, QD_SCATTER_CTAS * 512 / kSortThr
         continue;
       }
       const double v = *reinterpret_cast<const double*>(scb + vbase + i * 8u);
+      // AoS output arrays: the bin's peer destination when partitioning into peers
+      uint32_t* const oc = (OUT == kAoS && a.peers)
+                               ? reinterpret_cast<uint32_t*>(a.peers[sj & 0xFFu].c) : a.out.c;
+      double* const ov = (OUT == kAoS && a.peers)
+                             ? reinterpret_cast<double*>(a.peers[sj & 0xFFu].v) : a.out.v;
       if (OUT == kPK) {  // pack (first pass)
         unsigned long long pk = 0;
         if (MX && RT) {
@@ -1382,7 +1399,7 @@ __global__ void __launch_bounds__(kSortThreads, QD_SCATTER_CTAS * 512 / kSortThr
       if (RT && OUT == kAoS && IN == kAoS) {
         uint32_t cv[RT > 0 ? RT : 1];
         load_cv(i, cv);
-        uint32_t* o = a.out.c + dst * (RT > 0 ? RT : 1);
+        uint32_t* o = oc + dst * (RT > 0 ? RT : 1);
         if (RT != 4 || a.vec_out) {
           store_row_words<(RT > 0 ? RT : 1)>(o, cv);
         } else {
@@ -1393,13 +1410,13 @@ __global__ void __launch_bounds__(kSortThreads, QD_SCATTER_CTAS * 512 / kSortThr
 #pragma unroll
         for (int m = 0; m < (RT > 0 ? RT : 1); ++m) {
           const uint32_t x = *reinterpret_cast<const uint32_t*>(scb + cb[m] + i * rstride);
-          __stcs(OUT == kSoA ? a.out.c + (size_t)m * N + dst : a.out.c + dst * RT + m, x);
+          __stcs(OUT == kSoA ? a.out.c + (size_t)m * N + dst : oc + dst * RT + m, x);
         }
       } else {
         for (uint32_t m = 0; m < R; ++m)
-          __stcs(OUT == kSoA ? a.out.c + (size_t)m * N + dst : a.out.c + dst * R + m, coord(i, m));
+          __stcs(OUT == kSoA ? a.out.c + (size_t)m * N + dst : oc + dst * R + m, coord(i, m));
       }
-      __stcs(a.out.v + dst, v);
+      __stcs(ov + dst, v);
       if (a.next_dig)  // next pass's digit (unpacked rows: from the coordinates)
         __stcs(a.next_dig + dst, (uint8_t)digit_by([&](uint32_t m) { return coord(i, m); }, a.ndig));
     }
@@ -2685,7 +2702,8 @@ void run_pass(Ctx& c, uint32_t R, uint64_t N, uint32_t T, Rows in, RowsOut out,
               bool check, unsigned long long** offs_out = nullptr, const PackSpec* pack = nullptr,
               uint32_t pk_shift = 0, uint32_t pk_mask = 0, const uint8_t* digits_in = nullptr,
               uint8_t* digits_out = nullptr, uint32_t nd_shift = 0, uint32_t nd_mask = 0,
-              const DigitSpec* next_dig = nullptr, const uint32_t* run_prefix = nullptr) {
+              const DigitSpec* next_dig = nullptr, const uint32_t* run_prefix = nullptr,
+              const PeerDest* peers = nullptr, bool peers_aligned = false) {
   Workspace& ws = c.ws;
   const uint64_t nflat = num_chunks * kBins;
   auto* flat = ws.get<uint32_t>("chunk_flat", nflat);
@@ -2735,7 +2753,9 @@ void run_pass(Ctx& c, uint32_t R, uint64_t N, uint32_t T, Rows in, RowsOut out,
   a.nd_mask = nd_mask;
   if (next_dig) a.ndig = *next_dig;
   a.run_prefix = run_prefix;
-  a.vec_out = out.fmt == kAoS && (reinterpret_cast<uintptr_t>(out.c) & 15u) == 0 && vec_rows_enabled();
+  a.peers = peers;
+  a.vec_out = out.fmt == kAoS && vec_rows_enabled() &&
+              (peers ? peers_aligned : (reinterpret_cast<uintptr_t>(out.c) & 15u) == 0);
   if (const char* e = getenv("QD_SCATTER_DBG")) a.dbg = atoi(e);
   if (a.dbg & 2) {
     a.dbg_t = ws.get<unsigned long long>("dbg_t", 16);
@@ -3549,7 +3569,9 @@ void mode_histogram_device(Workspace& ws, uint32_t rank, uint64_t nnz, const uin
 void partition_rows_device(Workspace& ws, uint32_t rank, uint64_t nnz, const uint32_t* d_c_in,
                            const double* d_v_in, uint32_t mode, uint32_t dim,
                            const uint32_t* d_lookup, uint32_t n_parts, uint32_t* d_c_out,
-                           double* d_v_out, uint64_t* part_counts, void* stream) {
+                           double* d_v_out, uint64_t* part_counts, void* stream,
+                           const uint64_t* peer_c, const uint64_t* peer_v,
+                           const uint64_t* peer_off) {
   if (n_parts == 0 || n_parts > (uint32_t)kBins) invalid("n_parts must be in 1..256");
   if (mode >= rank) invalid("partition mode out of range");
   Ctx c = make_ctx(ws, stream);
@@ -3569,8 +3591,23 @@ void partition_rows_device(Workspace& ws, uint32_t rank, uint64_t nnz, const uin
   dig.lookup_dim = dim;
   KeySpec key{};
   unsigned long long* offs = nullptr;
+  // peer destinations: a kBins-entry table on the device (unused bins zero)
+  PeerDest* d_peers = nullptr;
+  bool aligned = true;
+  if (peer_c) {
+    std::vector<PeerDest> hp(kBins, PeerDest{0, 0, 0});
+    for (uint32_t p = 0; p < n_parts; ++p) {
+      hp[p] = PeerDest{peer_c[p], peer_v[p], peer_off[p]};
+      aligned &= ((peer_c[p] + peer_off[p] * 4ull * rank) & 15ull) == 0;
+    }
+    d_peers = ws.get<PeerDest>("peer_table", kBins);
+    QD_CUDA(cudaMemcpyAsync(d_peers, hp.data(), kBins * sizeof(PeerDest), cudaMemcpyHostToDevice,
+                            c.st));
+    QD_CUDA(cudaStreamSynchronize(c.st));  // hp is pageable and goes out of scope
+  }
   run_pass(c, rank, nnz, T, Rows{d_c_in, d_v_in, 0}, RowsOut{d_c_out, d_v_out, 0}, chunks, nc,
-           nullptr, dig, key, false, &offs);
+           nullptr, dig, key, false, &offs, nullptr, 0, 0, nullptr, nullptr, 0, 0, nullptr, nullptr,
+           d_peers, aligned);
   // part p starts at offs[p * nc] (bin-major flat layout of one run)
   const uint32_t nb = std::min<uint32_t>(n_parts + 1, kBins);
   auto* starts = ws.get<unsigned long long>("part_starts", kBins + 1);

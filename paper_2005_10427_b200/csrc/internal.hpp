@@ -115,6 +115,8 @@ void partition_rows_device(Workspace& ws, uint32_t rank, uint64_t nnz,
                            const uint32_t* d_c_in, const double* d_v_in,
                            uint32_t mode, uint32_t dim, const uint32_t* d_lookup,
                            uint32_t n_parts, uint32_t* d_c_out, double* d_v_out,
-                           uint64_t* part_counts, void* stream);
+                           uint64_t* part_counts, void* stream,
+                           const uint64_t* peer_c = nullptr, const uint64_t* peer_v = nullptr,
+                           const uint64_t* peer_off = nullptr);
 
 }  // namespace qb200

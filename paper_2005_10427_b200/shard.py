@@ -18,6 +18,13 @@ transpose of the global tensor:
   all_to_all over NCCL/NVLink, and the received parts concatenated in SOURCE
   RANK order — a subsequence of the simply sorted input, hence still simply
   sorted — then the full local Quesadilla plan.
+  ``QD_EXCHANGE=p2p`` fuses the partition with the exchange instead: the
+  (rank x part) row counts are all-reduced (a world x world matrix), every
+  rank's receive buffer lives in symmetric memory (NVLink peer mappings), and
+  ``qd_partition_rows_to_peers_device`` writes each part straight into its
+  destination rank's buffer at this rank's source-order offset — the same
+  bytes as the all_to_all path, with no local partitioned copy and no NCCL
+  send/recv (``p2p_layout`` is the offset arithmetic).
 
 The local work goes through a backend: ``GpuBackend`` (the CUDA library) in
 the product; tests substitute a CPU backend to check the host logic with
@@ -74,6 +81,18 @@ class LocalRows:
         return int(self.values.shape[0])
 
 
+@dataclass
+class SymRows:
+    """A rank's symmetric receive buffer: local coords/values views and every
+    rank's coords/values base address (valid in this process)."""
+    coords: object
+    values: object
+    peer_c: List[int]
+    peer_v: List[int]
+    cap: int
+    raw: object = None
+
+
 class GpuBackend:
     """Local work on this rank's GPU through the C ABI."""
 
@@ -120,6 +139,37 @@ class GpuBackend:
                                      self.qd.SortStrategy.quesadilla(), self.ws, self.stream())
         return out
 
+    def symmetric_rows(self, cap: int, rank: int, dist):
+        """This rank's receive buffer for `cap` rows and every rank's buffer
+        address in this process: torch symmetric memory (NVLink peer
+        mappings) on a multi-GPU box, or the test hub's emulation
+        (``dist.symmetric_empty``) when ranks are emulated on one GPU.
+        Grow-only and cached (cap is the same on every rank)."""
+        t = self.torch
+        if getattr(self, "_sym", None) is None or self._sym.cap < cap:
+            cap2 = max(cap, int((self._sym.cap if getattr(self, "_sym", None) else 0) * 1.25), 1)
+            voff = ((cap2 * rank * 4 + 255) // 256) * 256
+            nbytes = voff + cap2 * 8
+            if hasattr(dist, "symmetric_empty"):
+                raw, ptrs = dist.symmetric_empty(nbytes, self.device)
+            else:
+                import torch.distributed._symmetric_memory as symm_mem
+                raw = symm_mem.empty(nbytes, dtype=t.uint8, device=self.device)
+                hdl = symm_mem.rendezvous(raw, dist.group.WORLD.group_name)
+                ptrs = [int(p) for p in hdl.buffer_ptrs]
+            self._sym = SymRows(raw[:cap2 * rank * 4].view(t.int32),
+                                raw[voff:voff + cap2 * 8].view(t.float64),
+                                list(ptrs), [p + voff for p in ptrs], cap2, raw)
+        return self._sym
+
+    def partition_to_peers(self, rows: LocalRows, rank: int, mode: int, lookup: np.ndarray,
+                           parts: int, buf, offs):
+        t = self.torch
+        lk = t.from_numpy(np.ascontiguousarray(lookup).view(np.int32)).to(self.device)
+        return self.qd.partition_rows_to_peers_device(
+            rank, rows.nnz(), rows.coords.data_ptr(), rows.values.data_ptr(), mode, len(lookup),
+            lk.data_ptr(), parts, buf.peer_c, buf.peer_v, offs, self.ws, self.stream())
+
     def to_numpy_i64(self, h):
         return h.cpu().numpy()
 
@@ -128,6 +178,39 @@ class GpuBackend:
 
     def from_numpy_i64(self, a):
         return self.torch.from_numpy(np.asarray(a, np.int64)).to(self.device)
+
+
+def p2p_layout(C: np.ndarray, me: int):
+    """C[s, p] = rows source rank s sends to destination p.  Returns the row
+    offset of this rank's part p inside destination p's receive buffer (all
+    lower source ranks first: source-rank order), this rank's receive count
+    and the symmetric buffer capacity (the largest receive count)."""
+    C = np.asarray(C, np.int64)
+    offs = C[:me, :].sum(0) if me else np.zeros(C.shape[1], np.int64)
+    return [int(x) for x in offs], int(C[:, me].sum()), int(C.sum(0).max())
+
+
+def exchange_p2p(dist, be, rows: LocalRows, rank_modes: int, mode: int, lookup: np.ndarray,
+                 local_counts: Sequence[int]) -> LocalRows:
+    """Partition fused with the exchange: part p of this rank's rows is
+    written by the partition kernel directly into rank p's receive buffer."""
+    world, me = dist.get_world_size(), dist.get_rank()
+    M = np.zeros((world, world), np.int64)
+    M[me] = np.asarray(local_counts, np.int64)
+    t = be.from_numpy_i64(M.ravel())
+    dist.all_reduce(t)
+    C = be.to_numpy_i64(t).reshape(world, world)
+    offs, recv, cap = p2p_layout(C, me)
+    # every receiver has finished reading its buffer from the previous call
+    be.synchronize()
+    dist.barrier()
+    buf = be.symmetric_rows(cap, rank_modes, dist)
+    counts = be.partition_to_peers(rows, rank_modes, mode, lookup, world, buf, offs)
+    assert list(counts) == list(M[me]), (counts, M[me])
+    # every sender's writes have landed before this rank reads its buffer
+    be.synchronize()
+    dist.barrier()
+    return LocalRows(buf.coords[:recv * rank_modes], buf.values[:recv])
 
 
 def exchange(dist, be, rows: LocalRows, counts: Sequence[int], rank_modes: int) -> LocalRows:
@@ -143,6 +226,16 @@ def exchange(dist, be, rows: LocalRows, counts: Sequence[int], rank_modes: int) 
                            [int(c) * rank_modes for c in counts])
     dist.all_to_all_single(out.values, rows.values, rc, [int(c) for c in counts])
     return out
+
+
+def exchange_mode() -> str:
+    """QD_EXCHANGE: 'nccl' (default: partition + all_to_all) or 'p2p' (the
+    partition writes into peer receive buffers)."""
+    import os
+    m = os.environ.get("QD_EXCHANGE", "nccl").lower()
+    if m not in ("nccl", "p2p"):
+        raise ValueError(f"QD_EXCHANGE must be nccl or p2p, not {m!r}")
+    return m
 
 
 def sharded_transpose(dist, be, rows: LocalRows, dims: Sequence[int], target: Sequence[int],
@@ -163,14 +256,21 @@ def sharded_transpose(dist, be, rows: LocalRows, dims: Sequence[int], target: Se
         return out, False
     s1 = target[0]
     h = be.mode_hist(rows, r, s1, dims[s1])
+    p2p = exchange_mode() == "p2p"
+    h_local = be.to_numpy_i64(h).copy() if p2p else None
     dist.all_reduce(h)
     lookup = splitters(be.to_numpy_i64(h), world)
-    parts, counts = be.partition(rows, r, s1, lookup, world)
     if stats is not None:
         import time
         be.synchronize()
         t0 = time.perf_counter()
-    recv = exchange(dist, be, parts, counts, r)
+    if p2p:
+        local_counts = np.bincount(lookup, weights=h_local, minlength=world).astype(np.int64)
+        recv = exchange_p2p(dist, be, rows, r, s1, lookup, local_counts)
+        counts = local_counts
+    else:
+        parts, counts = be.partition(rows, r, s1, lookup, world)
+        recv = exchange(dist, be, parts, counts, r)
     if stats is not None:
         be.synchronize()
         me = dist.get_rank()

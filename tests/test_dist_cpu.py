@@ -46,6 +46,33 @@ class CpuBackend:
                                      target)
         return shard.LocalRows(torch.from_numpy(c.view(np.int32)), torch.from_numpy(v))
 
+    # QD_EXCHANGE=p2p: the peer writes are emulated over gloo (each sender
+    # ships its part with the row offset shard.p2p_layout gave it, and the
+    # receiver stores it there), so the offset arithmetic is what is tested
+    def symmetric_rows(self, cap, rank, dist):
+        return shard.SymRows(torch.zeros(cap * rank, dtype=torch.int32),
+                             torch.zeros(cap, dtype=torch.float64), [], [], cap)
+
+    def partition_to_peers(self, rows, rank, mode, lookup, parts, buf, offs):
+        part_rows, counts = self.partition(rows, rank, mode, lookup, parts)
+        send = torch.tensor(list(counts) + list(offs), dtype=torch.int64)
+        got = torch.empty(2 * parts, dtype=torch.int64)
+        dist.all_to_all_single(got, send.view(2, parts).t().contiguous().view(-1))
+        rc = got.view(parts, 2)[:, 0].tolist()  # rows from each source
+        ro = got.view(parts, 2)[:, 1].tolist()  # where each source said they go
+        out_c = torch.empty(sum(rc) * rank, dtype=torch.int32)
+        out_v = torch.empty(sum(rc), dtype=torch.float64)
+        dist.all_to_all_single(out_c, part_rows.coords, [c * rank for c in rc],
+                               [c * rank for c in counts])
+        dist.all_to_all_single(out_v, part_rows.values, rc, list(counts))
+        k = 0
+        for src in range(parts):
+            n, o = rc[src], ro[src]
+            buf.coords[o * rank:(o + n) * rank] = out_c[k * rank:(k + n) * rank]
+            buf.values[o:o + n] = out_v[k:k + n]
+            k += n
+        return counts
+
     def to_numpy_i64(self, h):
         return h.numpy()
 
@@ -112,7 +139,9 @@ CASES = [
 ]
 
 
-def test_sharded_transpose_world2_gloo():
+@pytest.mark.parametrize("exchange", ["nccl", "p2p"])
+def test_sharded_transpose_world2_gloo(exchange, monkeypatch):
+    monkeypatch.setenv("QD_EXCHANGE", exchange)  # inherited by the forked ranks
     world = 2
     mgr = mp.Manager()
     results = mgr.dict()
@@ -136,6 +165,15 @@ def test_splitters_balance_and_monotone():
         assert (np.diff(lk.astype(int)) >= 0).all() and lk.max() < parts
     lk = shard.splitters(np.array([5] * 8), 4)
     assert lk.tolist() == [0, 0, 1, 1, 2, 2, 3, 3]
+
+
+def test_p2p_layout_offsets():
+    C = np.array([[5, 0, 2],
+                  [1, 4, 0],
+                  [3, 3, 3]])
+    assert shard.p2p_layout(C, 0) == ([0, 0, 0], 9, 9)
+    assert shard.p2p_layout(C, 1) == ([5, 0, 2], 7, 9)
+    assert shard.p2p_layout(C, 2) == ([6, 4, 2], 5, 9)
 
 
 def test_aligned_bounds_never_split_runs():

@@ -589,6 +589,19 @@ class _ThreadDist:
         self.hub.barrier.wait()
         t.copy_(total)
 
+    def barrier(self):
+        self.hub.barrier.wait()
+
+    def symmetric_empty(self, nbytes, device):
+        """Emulated symmetric memory: every rank's buffer lives on the one GPU,
+        so the other ranks' base addresses are directly writable."""
+        import torch
+        raw = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        key = self._post(raw)
+        ptrs = [self.hub.slots[(key, r)].data_ptr() for r in range(self.hub.world)]
+        self.hub.barrier.wait()
+        return raw, ptrs
+
     def all_to_all_single(self, out, inp, output_split_sizes=None, input_split_sizes=None):
         import torch
         w = self.hub.world
@@ -603,8 +616,14 @@ class _ThreadDist:
         self.hub.barrier.wait()
 
 
+@pytest.mark.parametrize("exchange", ["nccl", "p2p"])
 @pytest.mark.parametrize("world", [2, 3, 4])
-def test_sharded_gpu_backend_emulated_ranks(world):
+def test_sharded_gpu_backend_emulated_ranks(world, exchange, monkeypatch):
+    """exchange='p2p': the partition kernel writes every part straight into
+    its destination rank's receive buffer (qd_partition_rows_to_peers_device);
+    the emulated ranks' buffers share the one GPU, so the peer addresses are
+    real device addresses and no kernel waits on another."""
+    monkeypatch.setenv("QD_EXCHANGE", exchange)
     import threading
     import torch
     from paper_2005_10427_b200 import shard
