@@ -3336,6 +3336,10 @@ void async_worker(Workspace* ws) {
     try {
       TensorView t{R, job.dims.data(), N};
       QD_CUDA(cudaStreamWaitEvent(ws->s_comp, ws->ev_in[sl], 0));
+      // the slot's OUTPUT buffers are rewritten only after the previous
+      // job's output copy from them has drained (its input buffers were
+      // refilled as soon as that job's sort had read them)
+      QD_CUDA(cudaStreamWaitEvent(ws->s_comp, ws->ev_out[sl], 0));
       // its internal host syncs return once this call's rows are sorted (an
       // out_of_range is found before any host byte is written)
       run_groups(*ws, t, sb.ic, sb.iv, sb.oc, sb.ov, job.groups, job.verify_input, nullptr,
@@ -3354,7 +3358,8 @@ void async_worker(Workspace* ws) {
         ws->async_row = e.row;
         ws->async_mode = e.mode;
       }
-      cudaEventRecord(ws->ev_out[sl], ws->s_comp);  // slot reusable after the failed work
+      cudaEventRecord(ws->ev_comp[sl], ws->s_comp);  // slot reusable after the failed work
+      cudaEventRecord(ws->ev_out[sl], ws->s_comp);
     } catch (const std::exception& e) {
       std::lock_guard<std::mutex> lk(ws->mu);
       if (!ws->async_failed) {
@@ -3362,6 +3367,7 @@ void async_worker(Workspace* ws) {
         ws->async_code = QD_CUDA_ERROR;
         ws->async_msg = e.what();
       }
+      cudaEventRecord(ws->ev_comp[sl], ws->s_comp);
       cudaEventRecord(ws->ev_out[sl], ws->s_comp);
     }
     {
@@ -3420,9 +3426,11 @@ void run_groups_host_async(Workspace& ws, const TensorView& t, uint32_t* coords,
     sb.rows = rows;
     sb.rank = rk;
   }
-  // the slot's buffers are free once its previous output copy has drained;
-  // a chained call reads host bytes the previous call's output copy writes
-  QD_CUDA(cudaStreamWaitEvent(ws.s_in, ws.ev_out[sl], 0));
+  // the slot's input buffers are free once its previous job's sort has read
+  // them (ev_comp; the output buffers wait for their copy-out in the worker),
+  // so input copies run back to back while earlier outputs drain; a chained
+  // call reads host bytes the previous call's output copy writes
+  QD_CUDA(cudaStreamWaitEvent(ws.s_in, ws.ev_comp[sl], 0));
   if (chained) QD_CUDA(cudaStreamWaitEvent(ws.s_in, ws.ev_out[sl ^ 1], 0));
   QD_CUDA(cudaMemcpyAsync(sb.ic, coords, N * R * 4, cudaMemcpyHostToDevice, ws.s_in));
   QD_CUDA(cudaMemcpyAsync(sb.iv, values, N * 8, cudaMemcpyHostToDevice, ws.s_in));
