@@ -82,6 +82,9 @@ constexpr int kMaxRounds = QD_MAX_TILE / kSortThreads;  // 32-row rounds per war
 #ifndef QD_EARLY_ADVANCE
 #define QD_EARLY_ADVANCE 1
 #endif
+#ifndef QD_ASYNC_SLOTS
+#define QD_ASYNC_SLOTS 2
+#endif
 #ifndef QD_FULL_ROUNDS
 #define QD_FULL_ROUNDS 1
 #endif
@@ -2206,16 +2209,16 @@ struct Workspace {
   // consecutive calls run back to back, overlapping the previous calls'
   // device work and output copies (PCIe is full duplex).
   cudaStream_t s_in = nullptr, s_comp = nullptr, s_out = nullptr;
-  cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_comp[2] = {nullptr, nullptr},
-              ev_out[2] = {nullptr, nullptr};
+  static constexpr int kSlots = QD_ASYNC_SLOTS;  // device in/out buffer pairs in flight
+  cudaEvent_t ev_in[kSlots] = {}, ev_comp[kSlots] = {}, ev_out[kSlots] = {};
   struct SlotBuf {
     uint32_t* ic = nullptr;
     double* iv = nullptr;
     uint32_t* oc = nullptr;
     double* ov = nullptr;
     size_t rows = 0, rank = 0;
-  } slots[2];
-  bool slot_busy[2] = {false, false};  // job queued / running, output copy not yet issued
+  } slots[kSlots];
+  bool slot_busy[kSlots] = {};  // job queued / running, output copy not yet issued
   int slot = 0;
   struct HostSpan {
     const void* c = nullptr;
@@ -2378,7 +2381,7 @@ void workspace_destroy(Workspace* ws) {
       cudaStreamSynchronize(st);
       cudaStreamDestroy(st);
     }
-  for (int i = 0; i < 2; ++i)
+  for (int i = 0; i < Workspace::kSlots; ++i)
     for (cudaEvent_t e : {ws->ev_in[i], ws->ev_comp[i], ws->ev_out[i]})
       if (e) cudaEventDestroy(e);
   for (auto& kv : ws->bufs)
@@ -3386,7 +3389,7 @@ void run_groups_host_async(Workspace& ws, const TensorView& t, uint32_t* coords,
   if (!ws.s_in) {
     for (cudaStream_t* st : {&ws.s_in, &ws.s_comp, &ws.s_out})
       QD_CUDA(cudaStreamCreateWithFlags(st, cudaStreamNonBlocking));
-    for (int i = 0; i < 2; ++i)
+    for (int i = 0; i < Workspace::kSlots; ++i)
       for (cudaEvent_t* e : {&ws.ev_in[i], &ws.ev_comp[i], &ws.ev_out[i]}) {
         QD_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
         QD_CUDA(cudaEventRecord(*e, ws.s_in));  // "done" until first use
@@ -3396,6 +3399,7 @@ void run_groups_host_async(Workspace& ws, const TensorView& t, uint32_t* coords,
   const uint64_t N = t.nnz;
   const uint32_t R = t.rank;
   const int sl = ws.slot;
+  const int psl = (sl + Workspace::kSlots - 1) % Workspace::kSlots;  // the previous call's slot
   auto overlaps = [](const void* a, size_t na, const void* b, size_t nb) {
     const char *x = static_cast<const char*>(a), *y = static_cast<const char*>(b);
     return na && nb && x < y + nb && y < x + na;
@@ -3410,7 +3414,7 @@ void run_groups_host_async(Workspace& ws, const TensorView& t, uint32_t* coords,
     // this slot's previous job must have issued its output copy (so ev_out
     // is its final record); a chained call also needs the previous one's
     std::unique_lock<std::mutex> lk(ws.mu);
-    ws.cv.wait(lk, [&] { return !ws.slot_busy[sl] && (!chained || !ws.slot_busy[sl ^ 1]); });
+    ws.cv.wait(lk, [&] { return !ws.slot_busy[sl] && (!chained || !ws.slot_busy[psl]); });
   }
   Workspace::SlotBuf& sb = ws.slots[sl];
   if (sb.rows < N || sb.rank < R) {
@@ -3431,7 +3435,7 @@ void run_groups_host_async(Workspace& ws, const TensorView& t, uint32_t* coords,
   // so input copies run back to back while earlier outputs drain; a chained
   // call reads host bytes the previous call's output copy writes
   QD_CUDA(cudaStreamWaitEvent(ws.s_in, ws.ev_comp[sl], 0));
-  if (chained) QD_CUDA(cudaStreamWaitEvent(ws.s_in, ws.ev_out[sl ^ 1], 0));
+  if (chained) QD_CUDA(cudaStreamWaitEvent(ws.s_in, ws.ev_out[psl], 0));
   QD_CUDA(cudaMemcpyAsync(sb.ic, coords, N * R * 4, cudaMemcpyHostToDevice, ws.s_in));
   QD_CUDA(cudaMemcpyAsync(sb.iv, values, N * 8, cudaMemcpyHostToDevice, ws.s_in));
   QD_CUDA(cudaEventRecord(ws.ev_in[sl], ws.s_in));
@@ -3449,7 +3453,7 @@ void run_groups_host_async(Workspace& ws, const TensorView& t, uint32_t* coords,
     ws.jobs.push_back(std::move(job));
   }
   ws.cv.notify_all();
-  ws.slot = sl ^ 1;
+  ws.slot = (sl + 1) % Workspace::kSlots;
   ws.last_host = cur;
 }
 
