@@ -82,6 +82,9 @@ constexpr int kMaxRounds = QD_MAX_TILE / kSortThreads;  // 32-row rounds per war
 #ifndef QD_EARLY_ADVANCE
 #define QD_EARLY_ADVANCE 1
 #endif
+#ifndef QD_DYNAMIC_CHUNKS
+#define QD_DYNAMIC_CHUNKS 1
+#endif
 #ifndef QD_ASYNC_SLOTS
 #define QD_ASYNC_SLOTS 2
 #endif
@@ -1008,6 +1011,20 @@ __global__ void __launch_bounds__(kSortThreads, QD_SCATTER_CTAS * 512 / kSortThr
   // chunk's descriptor is loaded one chunk ahead.
   constexpr uint32_t kAdv = kSortThreads - 32;
   ChunkDesc pre{};  // advancer only: descriptor of this CTA's next chunk
+  uint32_t pre_idx = 0;  // advancer only: index of that chunk
+  // the chunk after the current one: dynamic (a per-launch atomic counter
+  // deals chunks gridDim.x.. in completion order, so CTAs that drew easy
+  // tiles take more) or static round robin; whole advancer warp
+  auto next_chunk = [&](uint32_t cur) -> uint32_t {
+#if QD_DYNAMIC_CHUNKS
+    uint32_t x = 0;
+    if ((threadIdx.x & 31) == 0) x = gridDim.x + atomicAdd(a.chunk_counter, 1u);
+    (void)cur;
+    return __shfl_sync(0xFFFFFFFFu, x, 0);
+#else
+    return cur + gridDim.x;
+#endif
+  };
   // called by the whole advancer warp: lane j issues span j's bulk copy
   auto load_tile = [&](uint32_t b, const ChunkDesc& cd, uint32_t ti) {
     const uint32_t lane = threadIdx.x & 31;
@@ -1040,10 +1057,13 @@ __global__ void __launch_bounds__(kSortThreads, QD_SCATTER_CTAS * 512 / kSortThr
     uint32_t nc = ci, nt = ti + 1;
     ChunkDesc cd = s_cd[b ^ 1u];
     if (nt * (unsigned long long)a.T >= cd.len) {
-      nc = ci + gridDim.x;
+      nc = pre_idx;
       nt = 0;
       cd = pre;
-      if (nc + gridDim.x < a.num_chunks) pre = a.chunks[nc + gridDim.x];
+      if (nc < a.num_chunks) {
+        pre_idx = next_chunk(nc);
+        if (pre_idx < a.num_chunks) pre = a.chunks[pre_idx];
+      }
     }
     if ((threadIdx.x & 31) == 0) {
       s_chunk[pslot] = nc;
@@ -1064,8 +1084,9 @@ __global__ void __launch_bounds__(kSortThreads, QD_SCATTER_CTAS * 512 / kSortThr
       s_chunk[0] = c0;
       s_tile[0] = 0;
     }
+    pre_idx = c0 < a.num_chunks ? next_chunk(c0) : a.num_chunks;
     if (c0 < a.num_chunks) {
-      if (c0 + gridDim.x < a.num_chunks) pre = a.chunks[c0 + gridDim.x];
+      if (pre_idx < a.num_chunks) pre = a.chunks[pre_idx];
       load_tile(0, a.chunks[c0], 0);
     }
   }
