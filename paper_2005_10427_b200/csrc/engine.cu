@@ -3159,7 +3159,9 @@ void exec_group(Ctx& c, const TensorView& t, const uint32_t* src_c, const double
     const auto rc = costs(k, rest_keys, (double)S);
     return rc.first < rc.second;
   };
-  if (!disabled && g.check_range && g.prefix.empty() && m >= 1 && N >= min_rows) {
+  // run records hold a run's start row in 32 bits (k_run_records)
+  if (!disabled && g.check_range && g.prefix.empty() && m >= 1 && N >= min_rows &&
+      N <= 0xFFFFFFFFull) {
     auto* xc = m >= 2 ? ws.get<uint32_t>("rowsC_c", N * R) : nullptr;
     auto* xv = m >= 2 ? ws.get<double>("rowsC_v", N) : nullptr;
     const uint32_t k1 = g.keys[0], km = g.keys[m - 1];
