@@ -41,7 +41,8 @@ typedef enum qd_status {
   QD_OUT_OF_RANGE = 2,
   QD_CUDA_ERROR = 3,
   QD_NCCL_ERROR = 4,
-  QD_NO_DEVICE = 5
+  QD_NO_DEVICE = 5,
+  QD_PARSE_ERROR = 6 /* quesadilla::ParseError (io.hpp:15-22), .tns reader */
 } qd_status;
 
 /* quesadilla::SortStrategy::Kind, transpose.hpp:22. */
@@ -255,6 +256,46 @@ qd_status qd_partition_rows_to_peers_device(uint32_t rank, uint64_t nnz,
                                             const uint64_t* peer_row_offsets,
                                             uint64_t* part_counts, qd_workspace* ws,
                                             void* stream);
+
+/* ---- .tns text format (io.hpp:24-47, io.cpp:42-126) --------------------- */
+/* A tensor owned by the library (host memory; release with qd_tns_free). */
+typedef struct qd_tns_tensor {
+  uint32_t rank;
+  uint64_t nnz;
+  uint32_t* dims;   /* rank entries */
+  uint32_t* coords; /* AoS, nnz * rank, 0-based */
+  double* values;   /* nnz */
+} qd_tns_tensor;
+
+/* Where a QD_PARSE_ERROR was found: `line` is ParseError::line() (1-based);
+ * kind 1 first data line has < 2 fields, 2 rank != declared rank, 3 field
+ * count differs from the first data line, 4 invalid index token, 5 index 0,
+ * 6 index beyond its declared dimension, 7 invalid value token, 8 empty
+ * file without declared dims.  `field` is the 0-based field, the token is
+ * text[token_offset, +token_len).  qd_last_error() holds the reference's
+ * ParseError::what() text ("line N: ..."). */
+typedef struct qd_tns_error {
+  uint64_t line;
+  uint32_t kind;
+  uint32_t field;
+  uint32_t got;
+  uint32_t expected;
+  uint64_t token_offset;
+  uint64_t token_len;
+} qd_tns_error;
+
+/* read_tns over a file's bytes (the caller reads the file): tokens are split
+ * on ' ', '\t', '\r'; blank lines and lines whose first field starts with
+ * '#' are skipped; indices are 1-based std::from_chars(uint32_t), values
+ * std::from_chars(double) (correctly rounded, out-of-range rejected).
+ * `declared_dims` (has_declared != 0) plays ReadOptions::declared_dims;
+ * canonicalize != 0 stably sorts the rows into the simple ordering
+ * (io.cpp:36-38) on the device.  Parsing runs on the GPU (text copied to
+ * HBM once); `err` (nullable) receives the failure location. */
+qd_status qd_read_tns(const char* text, uint64_t n_bytes, const uint32_t* declared_dims,
+                      uint32_t declared_rank, int has_declared, int canonicalize,
+                      qd_tns_tensor* out, qd_tns_error* err, qd_workspace* ws);
+void qd_tns_free(qd_tns_tensor* t);
 
 #ifdef __cplusplus
 }

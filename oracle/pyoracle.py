@@ -153,10 +153,47 @@ class Reference:
         L.qref_ctx_transpose.argtypes = [C.c_void_p, _u32p, C.c_uint32]
         L.qref_ctx_read.argtypes = [C.c_void_p, _u32p, _f64p]
         L.qref_default_workers.restype = C.c_uint
+        L.qref_read_tns.restype = C.c_void_p
+        L.qref_read_tns.argtypes = [C.c_char_p, C.c_void_p, C.c_uint32, C.c_int, C.c_int,
+                                    C.POINTER(C.c_int)]
+        L.qref_parse_error_line.restype = C.c_uint64
+        L.qref_tensor_info.argtypes = [C.c_void_p, C.POINTER(C.c_uint32),
+                                       C.POINTER(C.c_uint64)]
+        L.qref_tensor_copy.argtypes = [C.c_void_p, _u32p, _u32p, _f64p]
+        L.qref_tensor_free.argtypes = [C.c_void_p]
+        L.qref_write_tns.argtypes = [C.c_uint32, _u32p, C.c_uint64, _u32p, _f64p, C.c_char_p]
 
     def _check(self, s):
         if s:
             raise OracleError(s, self.lib.qref_last_error().decode())
+
+    def read_tns(self, path, declared_dims=None, canonicalize=True):
+        """io.hpp:40-41.  Raises OracleError(4, what) with .line for ParseError."""
+        decl = None if declared_dims is None else _u32(declared_dims)
+        st = C.c_int(0)
+        h = self.lib.qref_read_tns(str(path).encode(),
+                                   None if decl is None or len(decl) == 0 else decl.ctypes.data,
+                                   0 if decl is None else len(decl), int(decl is not None),
+                                   int(bool(canonicalize)), C.byref(st))
+        if st.value:
+            e = OracleError(st.value, self.lib.qref_last_error().decode())
+            e.line = int(self.lib.qref_parse_error_line())
+            raise e
+        r, n = C.c_uint32(0), C.c_uint64(0)
+        self.lib.qref_tensor_info(h, C.byref(r), C.byref(n))
+        dims = np.zeros(max(r.value, 1), np.uint32)
+        coords = np.zeros(max(n.value * r.value, 1), np.uint32)
+        values = np.zeros(max(n.value, 1), np.float64)
+        self.lib.qref_tensor_copy(h, dims, coords, values)
+        self.lib.qref_tensor_free(h)
+        return dims[: r.value], coords[: n.value * r.value], values[: n.value]
+
+    def write_tns(self, dims, coords, values, path):
+        """io.hpp:47 (shortest round-trip values, 1-based indices)."""
+        d = _u32(dims)
+        self._check(self.lib.qref_write_tns(len(d), d, len(values), _u32(coords),
+                                            np.ascontiguousarray(values, np.float64),
+                                            str(path).encode()))
 
     def sort_rows_by(self, dims, coords, values, row_begin, row_end, keys):
         dims = _u32(dims)

@@ -264,4 +264,46 @@ int qref_is_sorted(uint32_t rank, const uint32_t* dims, uint64_t nnz,
 
 unsigned qref_default_workers(void) { return ParallelConfig::default_workers(); }
 
+
+// read_tns / write_tns (io.hpp:24-47).  ParseError -> 4 with its line().
+static uint64_t g_parse_line = 0;
+uint64_t qref_parse_error_line(void) { return g_parse_line; }
+void* qref_read_tns(const char* path, const uint32_t* declared, uint32_t declared_rank,
+                    int has_declared, int canonicalize, int* status) {
+  CooTensor* out = nullptr;
+  g_parse_line = 0;
+  *status = guard([&] {
+    try {
+      ReadOptions o;
+      o.canonicalize = canonicalize != 0;
+      if (has_declared) o.declared_dims = std::vector<uint32_t>(declared, declared + declared_rank);
+      out = new CooTensor(read_tns(path, o));
+    } catch (const ParseError& e) {
+      g_parse_line = e.line();
+      throw std::runtime_error(std::string("PARSE:") + e.what());
+    }
+  });
+  if (*status == 3 && g_msg.rfind("PARSE:", 0) == 0) {
+    g_msg = g_msg.substr(6);
+    *status = 4;
+  }
+  return out;
+}
+void qref_tensor_info(void* h, uint32_t* rank, uint64_t* nnz) {
+  auto* t = static_cast<CooTensor*>(h);
+  *rank = (uint32_t)t->rank();
+  *nnz = t->nnz();
+}
+void qref_tensor_copy(void* h, uint32_t* dims, uint32_t* coords, double* values) {
+  auto* t = static_cast<CooTensor*>(h);
+  std::memcpy(dims, t->dims.data(), t->dims.size() * 4);
+  std::memcpy(coords, t->coords.data(), t->coords.size() * 4);
+  std::memcpy(values, t->values.data(), t->values.size() * 8);
+}
+void qref_tensor_free(void* h) { delete static_cast<CooTensor*>(h); }
+int qref_write_tns(uint32_t rank, const uint32_t* dims, uint64_t nnz, const uint32_t* coords,
+                   const double* values, const char* path) {
+  return guard([&] { write_tns(wrap(rank, dims, nnz, coords, values), path); });
+}
+
 }  // extern "C"

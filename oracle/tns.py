@@ -1,0 +1,129 @@
+"""TEST INFRASTRUCTURE ONLY — CPU restatement of the reference's .tns reader
+(read_tns, /root/reference/proj/src/io.cpp:42-126), the checker for the GPU
+reader (qd_read_tns).  Pinned against the reference's own read_tns through
+oracle/_ref (tests/test_tns.py).  Never imported by the product.
+
+* lines: std::getline on '\\n' (io.cpp:55) — a final line without '\\n' counts,
+  a trailing '\\n' does not start another line;
+* fields: split on ' ', '\\t', '\\r' (io.cpp:22-34); blank lines and lines whose
+  first field starts with '#' are skipped (io.cpp:57);
+* the first data line fixes the field count (io.cpp:59-72);
+* indices: std::from_chars(uint32_t), 1-based (io.cpp:82-100);
+* values: std::from_chars(double) (io.cpp:108-113) — grammar below, correctly
+  rounded (Python float() is), overflow to inf / underflow to 0 rejected
+  (libstdc++ returns result_out_of_range; measured with g++ 13 here);
+* dims: declared, else the per-mode maximum 1-based index (io.cpp:115-124);
+  check_valid (coo.cpp:8-30); canonicalise = stable sort by all modes
+  (io.cpp:36-38).
+"""
+from __future__ import annotations
+
+import re
+import struct
+
+import numpy as np
+
+_DEC = re.compile(rb"-?(?:[0-9]+\.?[0-9]*|\.[0-9]+)(?:[eE][+-]?[0-9]+)?")
+_INF = re.compile(rb"-?(?:inf|infinity)", re.I)
+_NAN = re.compile(rb"-?nan(?:\([A-Za-z0-9_]*\))?", re.I)
+_IDX = re.compile(rb"[0-9]+")
+
+
+class TnsParseError(Exception):
+    def __init__(self, line: int, what: str):
+        super().__init__(f"line {line}: {what}")
+        self.line = line
+
+
+class TnsInvalid(Exception):
+    pass
+
+
+def from_chars_f64(tok: bytes):
+    """std::from_chars(double) over the whole token; None when rejected."""
+    neg = tok.startswith(b"-")
+    if _INF.fullmatch(tok):
+        return -np.inf if neg else np.inf
+    if _NAN.fullmatch(tok):
+        bits = (1 << 63 if neg else 0) | 0x7FF8000000000000
+        return struct.unpack("<d", struct.pack("<Q", bits))[0]
+    if not _DEC.fullmatch(tok):
+        return None
+    v = float(tok.decode())
+    mant = tok.split(b"e")[0].split(b"E")[0]
+    nonzero = any(c in b"123456789" for c in mant)
+    if v in (np.inf, -np.inf) or (v == 0.0 and nonzero):
+        return None
+    return v
+
+
+def from_chars_u32(tok: bytes):
+    if not _IDX.fullmatch(tok):
+        return None
+    v = int(tok)
+    return v if v <= 0xFFFFFFFF else None
+
+
+def read_tns_bytes(text: bytes, declared_dims=None, canonicalize: bool = True):
+    """Returns (dims u32[r], coords u32[N*r], values f64[N]) or raises
+    TnsParseError / TnsInvalid like io.cpp / coo.cpp."""
+    lines = text.split(b"\n")
+    if text.endswith(b"\n") or not text:
+        lines = lines[:-1]
+    decl = None if declared_dims is None else [int(d) for d in declared_dims]
+    F = 0
+    coords, values = [], []
+    max_index = []
+    lineno = 0
+    for raw in lines:
+        lineno += 1
+        fields = [f for f in re.split(rb"[ \t\r]+", raw) if f]
+        if not fields or fields[0].startswith(b"#"):
+            continue
+        if F == 0:
+            if len(fields) < 2:
+                raise TnsParseError(lineno, "expected at least one index and a value, got "
+                                    f"{len(fields)} fields")
+            if decl is not None and len(decl) != len(fields) - 1:
+                raise TnsParseError(lineno, f"file has rank {len(fields) - 1} but {len(decl)} "
+                                    "dimensions were declared")
+            F = len(fields)
+            max_index = [0] * (F - 1)
+        elif len(fields) != F:
+            raise TnsParseError(lineno, f"expected {F} fields, got {len(fields)}")
+        for m in range(F - 1):
+            tok = fields[m]
+            idx = from_chars_u32(tok)
+            t = tok.decode("latin-1")
+            if idx is None:
+                raise TnsParseError(lineno, f"invalid index '{t}'")
+            if idx < 1:
+                raise TnsParseError(lineno, f"indices are 1-based; got {t} in mode {m + 1}")
+            if decl is not None and idx > decl[m]:
+                raise TnsParseError(lineno, f"index {t} exceeds declared dimension {decl[m]} "
+                                    f"of mode {m + 1}")
+            max_index[m] = max(max_index[m], idx)
+            coords.append(idx - 1)
+        v = from_chars_f64(fields[-1])
+        if v is None:
+            raise TnsParseError(lineno, f"invalid value '{fields[-1].decode('latin-1')}'")
+        values.append(v)
+    if F == 0:
+        if decl is None:
+            raise TnsParseError(lineno, "empty file: rank is unknowable without declared "
+                                "dimensions")
+        dims = decl
+    else:
+        dims = decl if decl is not None else max_index
+    r = len(dims)
+    if r == 0:
+        raise TnsInvalid("tensor rank must be positive")
+    for m, d in enumerate(dims):
+        if d == 0:
+            raise TnsInvalid(f"dimension of mode {m} must be positive")
+    c = np.asarray(coords, np.uint32).reshape(-1, r)
+    v = np.asarray(values, np.float64)
+    if canonicalize and len(v) > 1:
+        order = np.lexsort(tuple(c[:, m] for m in reversed(range(r))))  # stable
+        c, v = c[order], v[order]
+    return np.asarray(dims, np.uint32), np.ascontiguousarray(c).reshape(-1), v

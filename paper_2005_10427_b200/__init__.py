@@ -48,6 +48,9 @@ QD_OK, QD_INVALID_ARGUMENT, QD_OUT_OF_RANGE, QD_CUDA_ERROR, QD_NCCL_ERROR, QD_NO
 KINDS = {"quesadilla": 0, "topk": 1, "radix": 2, "comparison": 3}
 
 
+QD_PARSE_ERROR = 6
+
+
 class InvalidArgument(ValueError):
     """std::invalid_argument"""
 
@@ -62,6 +65,28 @@ class OutOfRange(IndexError):
 
 class DeviceError(RuntimeError):
     """CUDA failure or no device (the library has no CPU path)."""
+
+
+class ParseError(RuntimeError):
+    """quesadilla::ParseError (io.hpp:15-22): str() is "line N: ...", .line() is N."""
+
+    def __init__(self, msg, line=0, kind=0, field=0):
+        super().__init__(msg)
+        self._line, self.kind, self.field = line, kind, field
+
+    def line(self) -> int:
+        return self._line
+
+
+class TnsTensorC(C.Structure):
+    _fields_ = [("rank", C.c_uint32), ("nnz", C.c_uint64), ("dims", C.POINTER(C.c_uint32)),
+                ("coords", C.POINTER(C.c_uint32)), ("values", C.POINTER(C.c_double))]
+
+
+class TnsErrorC(C.Structure):
+    _fields_ = [("line", C.c_uint64), ("kind", C.c_uint32), ("field", C.c_uint32),
+                ("got", C.c_uint32), ("expected", C.c_uint32), ("token_offset", C.c_uint64),
+                ("token_len", C.c_uint64)]
 
 
 class PlanStepC(C.Structure):
@@ -150,6 +175,10 @@ def lib():
         L.qd_partition_rows_to_peers_device.argtypes = [
             C.c_uint32, C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p,
             C.c_uint32, _u64p, _u64p, _u64p, _u64p, C.c_void_p, C.c_void_p]
+        L.qd_read_tns.argtypes = [C.c_char_p, C.c_uint64, C.c_void_p, C.c_uint32, C.c_int,
+                                  C.c_int, C.POINTER(TnsTensorC), C.POINTER(TnsErrorC),
+                                  C.c_void_p]
+        L.qd_tns_free.argtypes = [C.POINTER(TnsTensorC)]
         _lib = L
     return _lib
 
@@ -796,6 +825,50 @@ def partition_rows_to_peers_device(rank, nnz, coords_in, values_in, mode, dim, l
         n_parts, arr(peer_coords), arr(peer_values), arr(peer_row_offsets), counts, w.handle,
         C.c_void_p(stream)))
     return [int(x) for x in counts]
+
+
+
+
+# ---- .tns text format (io.hpp:24-47) ------------------------------------------
+
+def read_tns_text(text: bytes, declared_dims=None, canonicalize: bool = True,
+                  ws: Optional[Workspace] = None) -> CooTensor:
+    """read_tns (io.cpp:42-126) over a file's bytes, parsed on the GPU
+    (qd_read_tns).  Raises ParseError exactly where and with the text the
+    reference would; InvalidArgument for check_valid failures (coo.cpp:8-16)."""
+    L = lib()
+    w = _ws(ws)
+    decl = None if declared_dims is None else _arr_u32(declared_dims)
+    out, err = TnsTensorC(), TnsErrorC()
+    st = L.qd_read_tns(bytes(text), len(text),
+                       None if decl is None or len(decl) == 0 else decl.ctypes.data,
+                       0 if decl is None else len(decl), int(decl is not None),
+                       int(bool(canonicalize)), C.byref(out), C.byref(err), w.handle)
+    if st == QD_PARSE_ERROR:
+        raise ParseError(L.qd_last_error().decode(), err.line, err.kind, err.field)
+    _check(st)
+    try:
+        r, n = out.rank, out.nnz
+        dims = np.ctypeslib.as_array(out.dims, (r,)).copy() if r else np.zeros(0, np.uint32)
+        coords = (np.ctypeslib.as_array(out.coords, (n * r,)).copy() if n
+                  else np.zeros(0, np.uint32))
+        values = (np.ctypeslib.as_array(out.values, (n,)).copy() if n
+                  else np.zeros(0, np.float64))
+    finally:
+        L.qd_tns_free(C.byref(out))
+    return CooTensor(dims, coords, values)
+
+
+def read_tns(path, declared_dims=None, canonicalize: bool = True,
+             ws: Optional[Workspace] = None) -> CooTensor:
+    """read_tns(path, ReadOptions) (io.hpp:40-41); the file is read on the host,
+    everything after that runs on the GPU."""
+    try:
+        with open(path, "rb") as f:
+            text = f.read()
+    except OSError:
+        raise RuntimeError(f"cannot open '{path}' for reading")
+    return read_tns_text(text, declared_dims, canonicalize, ws)
 
 
 __all__ = [n for n in dir() if not n.startswith("_")]

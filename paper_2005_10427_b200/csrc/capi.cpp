@@ -3,6 +3,8 @@
 // with the same exception class (mapped to qd_status):
 //   transpose.cpp:83-89 (rank, verify_input), transpose.cpp:101-103 (top-K),
 //   sort.cpp:153-166 (partial_sort args), parallel.cpp:161-163 (workers).
+#include <cstdlib>
+#include <cuda_runtime.h>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -322,6 +324,87 @@ qd_status qd_sort_rows_by_device(uint32_t rank, const uint32_t* dims, uint64_t n
                d_values_in + row_begin, d_coords_out + row_begin * rank, d_values_out + row_begin,
                groups, false, nullptr, nullptr, 0, stream);
   });
+}
+
+// read_tns (io.cpp:42-126): parse on the device (tns.cu), canonicalise with
+// the engine's sort_rows_by group (io.cpp:36-38), copy the rows out.
+qd_status qd_read_tns(const char* text, uint64_t n_bytes, const uint32_t* declared_dims,
+                      uint32_t declared_rank, int has_declared, int canonicalize,
+                      qd_tns_tensor* out, qd_tns_error* err, qd_workspace* ws) {
+  return guard([&] {
+    if (!ws) invalid("workspace is null");
+    if (!out) invalid("output is null");
+    *out = qd_tns_tensor{};
+    struct Scope {
+      cudaStream_t st = nullptr;
+      std::vector<void*> dev;
+      ~Scope() {
+        if (st) cudaStreamSynchronize(st);
+        for (void* p : dev) cudaFree(p);
+        if (st) cudaStreamDestroy(st);
+      }
+    } sc;
+    auto ck = [](cudaError_t e) {
+      if (e != cudaSuccess) throw Error(QD_CUDA_ERROR, cudaGetErrorString(e));
+    };
+    ck(cudaStreamCreateWithFlags(&sc.st, cudaStreamNonBlocking));
+    TnsParsed p;
+    parse_tns_device(text, n_bytes, declared_dims, declared_rank, has_declared != 0, &p, err,
+                     sc.st);
+    sc.dev.push_back(p.d_coords);
+    sc.dev.push_back(p.d_values);
+    const uint32_t R = p.rank;
+    const uint64_t N = p.nnz;
+    qd_tns_tensor t{R, N, nullptr, nullptr, nullptr};
+    t.dims = static_cast<uint32_t*>(std::malloc(std::max<size_t>(R, 1) * 4));
+    t.coords = static_cast<uint32_t*>(std::malloc(std::max<uint64_t>(N * R, 1) * 4));
+    t.values = static_cast<double*>(std::malloc(std::max<uint64_t>(N, 1) * 8));
+    if (!t.dims || !t.coords || !t.values) {
+      qd_tns_free(&t);
+      throw std::bad_alloc();
+    }
+    std::copy(p.dims.begin(), p.dims.end(), t.dims);
+    const uint32_t* c_src = p.d_coords;
+    const double* v_src = p.d_values;
+    try {
+      if (canonicalize && N >= 2) {
+        std::vector<uint32_t> simple(R);
+        for (uint32_t m = 0; m < R; ++m) simple[m] = m;
+        auto groups = sort_rows_group(R, simple.data(), R);
+        uint32_t* c2 = nullptr;
+        double* v2 = nullptr;
+        ck(cudaMalloc(&c2, N * R * 4));
+        sc.dev.push_back(c2);
+        ck(cudaMalloc(&v2, N * 8));
+        sc.dev.push_back(v2);
+        TensorView tv{R, p.dims.data(), N};
+        run_groups(W(ws), tv, p.d_coords, p.d_values, c2, v2, groups, false, nullptr, nullptr, 0,
+                   sc.st);
+        c_src = c2;
+        v_src = v2;
+      }
+      if (N) {
+        ck(cudaMemcpyAsync(t.coords, c_src, N * R * 4, cudaMemcpyDeviceToHost, sc.st));
+        ck(cudaMemcpyAsync(t.values, v_src, N * 8, cudaMemcpyDeviceToHost, sc.st));
+      }
+      ck(cudaStreamSynchronize(sc.st));
+    } catch (...) {
+      qd_tns_free(&t);
+      throw;
+    }
+    *out = t;
+  });
+}
+
+void qd_tns_free(qd_tns_tensor* t) {
+  if (!t) return;
+  std::free(t->dims);
+  std::free(t->coords);
+  std::free(t->values);
+  t->dims = nullptr;
+  t->coords = nullptr;
+  t->values = nullptr;
+  t->nnz = 0;
 }
 
 qd_status qd_relabel_target(const uint32_t* source, const uint32_t* target, uint32_t rank,

@@ -119,4 +119,19 @@ void partition_rows_device(Workspace& ws, uint32_t rank, uint64_t nnz,
                            const uint64_t* peer_c = nullptr, const uint64_t* peer_v = nullptr,
                            const uint64_t* peer_off = nullptr);
 
+// .tns reader (tns.cu): io.cpp:42-126 minus canonicalisation.  Parses the
+// host text on the device; on success the rows are in device buffers the
+// caller frees (cudaFree), in file order.  Throws Error(QD_PARSE_ERROR) with
+// the reference's ParseError text and fills *err.
+struct TnsParsed {
+  uint32_t rank = 0;
+  uint64_t nnz = 0;
+  std::vector<uint32_t> dims;
+  uint32_t* d_coords = nullptr;
+  double* d_values = nullptr;
+};
+void parse_tns_device(const char* h_text, uint64_t n, const uint32_t* declared,
+                      uint32_t declared_rank, bool has_declared, TnsParsed* out,
+                      qd_tns_error* err, void* stream);
+
 }  // namespace qb200

@@ -1,0 +1,461 @@
+// GPU .tns reader: the reference's read_tns (io.cpp:42-126) as device passes
+// over the file's bytes ("on-disk format and
+// canonicalisation").  Canonicalisation itself (io.cpp:36-38, sort_rows_by)
+// reuses the transpose engine (capi.cpp, qd_read_tns).
+//
+// Passes (text resident in HBM, padded to 16 bytes):
+//   k_nl_count      per 4 KB tile: newline count (16-byte loads)
+//   k_scan_excl     one-CTA exclusive scan of the tile counts
+//   k_nl_positions  per tile: line starts at the scanned offsets
+//   k_line_classify thread per line: field count, data/blank/comment
+//                   (io.cpp:56-57), per-CTA data-line count, first data line
+//   k_scan_excl     row offsets of the CTAs
+//   k_line_parse    thread per line: std::from_chars of every field
+//                   (tns_parse.cuh), 0-based AoS coords + f64 values at the
+//                   line's row, per-mode maxima (dims, io.cpp:117-124),
+//                   first failing line (atomicMin)
+//   k_line_error    one thread re-parses the first failing line and reports
+//                   what failed, so the host can build the reference's exact
+//                   ParseError text (io.cpp:16-18)
+// All byte work is HBM-bound: ~1 read of the text per pass, plus the row write.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "internal.hpp"
+#include "tns_parse.cuh"
+
+namespace qb200 {
+
+namespace {
+
+constexpr int kTileThreads = 256;
+constexpr uint64_t kTileBytes = kTileThreads * 16;
+constexpr int kLineThreads = 256;
+
+#define TNS_CUDA(x)                                                                  \
+  do {                                                                               \
+    cudaError_t e_ = (x);                                                            \
+    if (e_ != cudaSuccess)                                                           \
+      throw Error(QD_CUDA_ERROR, std::string("CUDA error in .tns reader: ") +       \
+                                     cudaGetErrorString(e_));                        \
+  } while (0)
+
+__device__ __forceinline__ int count_nl16(uint4 v) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+  int c = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    // bytes equal to '\n' (0x0A): zero-byte test on w ^ 0x0A0A0A0A
+    const uint32_t x = w[k] ^ 0x0A0A0A0Au;
+    c += __popc(((x - 0x01010101u) & ~x & 0x80808080u));
+  }
+  return c;
+}
+
+__global__ void k_nl_count(const uint4* __restrict__ text, uint64_t n16,
+                           uint32_t* __restrict__ tile_counts) {
+  const uint64_t i = (uint64_t)blockIdx.x * kTileThreads + threadIdx.x;
+  int c = 0;
+  if (i < n16) c = count_nl16(text[i]);
+  c = __reduce_add_sync(0xffffffffu, c);
+  __shared__ int ws[kTileThreads / 32];
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int k = 0; k < kTileThreads / 32; ++k) t += ws[k];
+    tile_counts[blockIdx.x] = (uint32_t)t;
+  }
+}
+
+// Exclusive scan of n u32 counts into u64 offsets (out[n] = total); one CTA.
+__global__ void k_scan_excl(const uint32_t* __restrict__ in, uint64_t n,
+                            uint64_t* __restrict__ out) {
+  __shared__ uint64_t wsum[32];
+  __shared__ uint64_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (uint64_t base = 0; base < n; base += blockDim.x) {
+    const uint64_t i = base + threadIdx.x;
+    const uint64_t v = i < n ? in[i] : 0;
+    uint64_t s = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint64_t t = __shfl_up_sync(0xffffffffu, s, d);
+      if (lane >= d) s += t;
+    }
+    if (lane == 31) wsum[warp] = s;
+    __syncthreads();
+    if (warp == 0) {
+      const int nw = blockDim.x >> 5;
+      uint64_t x = lane < nw ? wsum[lane] : 0;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint64_t t = __shfl_up_sync(0xffffffffu, x, d);
+        if (lane >= d) x += t;
+      }
+      if (lane < nw) wsum[lane] = x;
+    }
+    __syncthreads();
+    const uint64_t before = carry + (warp ? wsum[warp - 1] : 0) + s - v;
+    if (i < n) out[i] = before;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = before + v;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[n] = carry;
+}
+
+// line_start[0] = 0; the line after the j-th newline starts at its byte + 1.
+__global__ void k_nl_positions(const uint4* __restrict__ text, uint64_t n16,
+                               const uint64_t* __restrict__ tile_off,
+                               uint64_t* __restrict__ line_start) {
+  const uint64_t i = (uint64_t)blockIdx.x * kTileThreads + threadIdx.x;
+  uint4 v = make_uint4(0, 0, 0, 0);
+  if (i < n16) v = text[i];
+  const int c = count_nl16(v);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int s = c;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, s, d);
+    if (lane >= d) s += t;
+  }
+  __shared__ int ws[kTileThreads / 32];
+  if (lane == 31) ws[warp] = s;
+  __syncthreads();
+  int before = s - c;
+  for (int k = 0; k < warp; ++k) before += ws[k];
+  uint64_t out = tile_off[blockIdx.x] + before + 1;
+  if (blockIdx.x == 0 && threadIdx.x == 0) line_start[0] = 0;
+  if (c) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int b = 0; b < 16; ++b) {
+      if (((w[b >> 2] >> ((b & 3) * 8)) & 0xFF) == '\n') line_start[out++] = i * 16 + b + 1;
+    }
+  }
+}
+
+// Bytes [begin, end) of line k (the newline excluded).
+__device__ __forceinline__ void line_span(const uint64_t* line_start, uint64_t n_nl, uint64_t n,
+                                          uint64_t k, uint64_t* b, uint64_t* e) {
+  *b = line_start[k];
+  *e = k < n_nl ? line_start[k + 1] - 1 : n;
+}
+
+// Field count of a line (split_fields, io.cpp:24-34); 0 for blank and
+// comment lines (io.cpp:57).
+__device__ uint32_t line_fields(const char* t, uint64_t b, uint64_t e) {
+  uint32_t nf = 0;
+  bool in = false, comment = false;
+  for (uint64_t p = b; p < e; ++p) {
+    const bool sp = tns::is_space(t[p]);
+    if (!sp && !in) {
+      if (nf == 0 && t[p] == '#') comment = true;
+      ++nf;
+    }
+    in = !sp;
+  }
+  return comment ? 0 : nf;
+}
+
+__global__ void k_line_classify(const char* __restrict__ text, uint64_t n,
+                                const uint64_t* __restrict__ line_start, uint64_t n_nl,
+                                uint64_t n_lines, uint32_t* __restrict__ nf_out,
+                                uint32_t* __restrict__ cta_rows,
+                                unsigned long long* __restrict__ first_data) {
+  const uint64_t k = (uint64_t)blockIdx.x * kLineThreads + threadIdx.x;
+  uint32_t nf = 0;
+  if (k < n_lines) {
+    uint64_t b, e;
+    line_span(line_start, n_nl, n, k, &b, &e);
+    nf = line_fields(text, b, e);
+    nf_out[k] = nf;
+  }
+  const unsigned bal = __ballot_sync(0xffffffffu, nf != 0);  // one atomic per warp
+  if (bal && (threadIdx.x & 31) == __ffs(bal) - 1) atomicMin(first_data, (unsigned long long)k);
+  const int c = __syncthreads_count(nf != 0);
+  if (threadIdx.x == 0) cta_rows[blockIdx.x] = (uint32_t)c;
+}
+
+struct ParseArgs {
+  const char* text;
+  uint64_t n;
+  const uint64_t* line_start;
+  uint64_t n_nl, n_lines;
+  const uint32_t* nf;
+  const uint64_t* cta_row_off;
+  uint32_t fields;           // rank + 1 (from the first data line)
+  const uint32_t* declared;  // device, or null
+  uint32_t* coords;
+  double* values;
+  uint32_t* max_index;       // [rank]
+  unsigned long long* err_line;
+};
+
+// Error kinds (the reference's ParseError texts, io.cpp:60-113).
+enum : uint32_t {
+  kErrNone = 0,
+  kErrFieldCount = 3,
+  kErrIndex = 4,
+  kErrZeroIndex = 5,
+  kErrExceeds = 6,
+  kErrValue = 7,
+};
+
+struct LineError {
+  uint32_t kind, field, got;
+  uint64_t tok_begin, tok_len;
+};
+
+// Parses line [b, e) with nf fields; writes the row when row_out is set.
+// Returns the first failure in the reference's check order.
+__device__ LineError parse_line(const ParseArgs& a, uint64_t b, uint64_t e, uint32_t nf,
+                                uint64_t row, bool write, uint32_t* smax) {
+  LineError err{kErrNone, 0, nf, 0, 0};
+  if (nf != a.fields) {
+    err.kind = kErrFieldCount;
+    return err;
+  }
+  const uint32_t rank = a.fields - 1;
+  uint64_t p = b;
+  for (uint32_t m = 0; m < a.fields; ++m) {
+    while (p < e && tns::is_space(a.text[p])) ++p;
+    const uint64_t tb = p;
+    while (p < e && !tns::is_space(a.text[p])) ++p;
+    const uint32_t tl = (uint32_t)(p - tb);
+    if (m < rank) {
+      uint32_t idx = 0;
+      if (!tns::parse_u32(a.text + tb, tl, &idx)) return LineError{kErrIndex, m, nf, tb, tl};
+      if (idx < 1) return LineError{kErrZeroIndex, m, nf, tb, tl};
+      if (a.declared && idx > a.declared[m]) return LineError{kErrExceeds, m, nf, tb, tl};
+      if (write) {
+        a.coords[row * rank + m] = idx - 1;
+        if (smax) atomicMax(&smax[m], idx);
+      }
+    } else {
+      double v = 0;
+      if (!tns::parse_f64(a.text + tb, tl, &v)) return LineError{kErrValue, m, nf, tb, tl};
+      if (write) a.values[row] = v;
+    }
+  }
+  return err;
+}
+
+__global__ void __launch_bounds__(kLineThreads) k_line_parse(ParseArgs a) {
+  __shared__ uint32_t smax[QD_MAX_RANK];
+  __shared__ int wcount[kLineThreads / 32];
+  const uint32_t rank = a.fields - 1;
+  for (uint32_t m = threadIdx.x; m < rank; m += blockDim.x) smax[m] = 0;
+  const uint64_t k = (uint64_t)blockIdx.x * kLineThreads + threadIdx.x;
+  const uint32_t nf = k < a.n_lines ? a.nf[k] : 0;
+  // row = the CTA's offset + data lines before this one in the CTA
+  const unsigned bal = __ballot_sync(0xffffffffu, nf != 0);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) wcount[warp] = __popc(bal);
+  __syncthreads();
+  uint64_t row = a.cta_row_off[blockIdx.x] + __popc(bal & ((1u << lane) - 1));
+  for (int w = 0; w < warp; ++w) row += wcount[w];
+  if (nf) {
+    uint64_t b, e;
+    line_span(a.line_start, a.n_nl, a.n, k, &b, &e);
+    const LineError err = parse_line(a, b, e, nf, row, true, smax);
+    if (err.kind != kErrNone) atomicMin(a.err_line, (unsigned long long)k);
+  }
+  __syncthreads();
+  for (uint32_t m = threadIdx.x; m < rank; m += blockDim.x)
+    if (smax[m]) atomicMax(&a.max_index[m], smax[m]);
+}
+
+__global__ void k_line_error(ParseArgs a, uint64_t k, LineError* out) {
+  uint64_t b, e;
+  line_span(a.line_start, a.n_nl, a.n, k, &b, &e);
+  *out = parse_line(a, b, e, a.nf[k], 0, false, nullptr);
+}
+
+struct DevBuf {
+  void* p = nullptr;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  template <class T>
+  T* alloc(uint64_t bytes) {
+    TNS_CUDA(cudaMalloc(&p, std::max<uint64_t>(bytes, 16)));
+    return static_cast<T*>(p);
+  }
+};
+
+[[noreturn]] void parse_error(qd_tns_error* err, uint64_t line, uint32_t kind, uint32_t field,
+                              uint32_t got, uint32_t expected, uint64_t tb, uint64_t tl,
+                              const std::string& what) {
+  if (err) {
+    err->line = line;
+    err->kind = kind;
+    err->field = field;
+    err->got = got;
+    err->expected = expected;
+    err->token_offset = tb;
+    err->token_len = tl;
+  }
+  Error e(QD_PARSE_ERROR, "line " + std::to_string(line) + ": " + what);
+  e.row = line;
+  e.mode = field;
+  throw e;
+}
+
+}  // namespace
+
+void parse_tns_device(const char* h_text, uint64_t n, const uint32_t* declared,
+                      uint32_t declared_rank, bool has_declared, TnsParsed* out,
+                      qd_tns_error* err, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  out->rank = 0;
+  out->nnz = 0;
+  out->dims.clear();
+  out->d_coords = nullptr;
+  out->d_values = nullptr;
+  if (err) *err = qd_tns_error{};
+  if (n && !h_text) invalid("text is null");
+  if (has_declared && declared_rank && !declared) invalid("declared dims are null");
+
+  // text in HBM, zero-padded to whole 16-byte words (and one more word)
+  const uint64_t n16 = (n + 15) / 16 + 1;
+  DevBuf b_text;
+  char* d_text = b_text.alloc<char>(n16 * 16);
+  const uint64_t pad_from = n & ~15ull;  // zero the partial last word and the extra one
+  TNS_CUDA(cudaMemsetAsync(d_text + pad_from, 0, n16 * 16 - pad_from, st));
+  if (n) TNS_CUDA(cudaMemcpyAsync(d_text, h_text, n, cudaMemcpyHostToDevice, st));
+
+  // newlines -> line starts
+  const uint64_t n_tiles = (n16 + kTileThreads - 1) / kTileThreads;
+  DevBuf b_tc, b_to;
+  uint32_t* d_tc = b_tc.alloc<uint32_t>(n_tiles * 4);
+  uint64_t* d_to = b_to.alloc<uint64_t>((n_tiles + 1) * 8);
+  k_nl_count<<<(unsigned)n_tiles, kTileThreads, 0, st>>>((const uint4*)d_text, n16, d_tc);
+  k_scan_excl<<<1, 1024, 0, st>>>(d_tc, n_tiles, d_to);
+  uint64_t n_nl = 0;
+  TNS_CUDA(cudaMemcpyAsync(&n_nl, d_to + n_tiles, 8, cudaMemcpyDeviceToHost, st));
+  TNS_CUDA(cudaStreamSynchronize(st));
+  // getline semantics: a final line without '\n' still counts
+  const bool tail = n > 0 && h_text[n - 1] != '\n';
+  const uint64_t n_lines = n_nl + (tail ? 1 : 0);
+  DevBuf b_ls;
+  uint64_t* d_ls = b_ls.alloc<uint64_t>((n_nl + 2) * 8);
+  k_nl_positions<<<(unsigned)n_tiles, kTileThreads, 0, st>>>((const uint4*)d_text, n16, d_to,
+                                                            d_ls);
+
+  // classify lines
+  const uint64_t n_ctas = std::max<uint64_t>(1, (n_lines + kLineThreads - 1) / kLineThreads);
+  DevBuf b_nf, b_cr, b_co, b_small;
+  uint32_t* d_nf = b_nf.alloc<uint32_t>(n_lines * 4);
+  uint32_t* d_cr = b_cr.alloc<uint32_t>(n_ctas * 4);
+  uint64_t* d_co = b_co.alloc<uint64_t>((n_ctas + 1) * 8);
+  // small: [0] first data line, [1] error line, [2..] LineError, max_index
+  unsigned long long* d_small = b_small.alloc<unsigned long long>(64 + QD_MAX_RANK * 4 + 64);
+  TNS_CUDA(cudaMemsetAsync(d_small, 0xFF, 16, st));
+  uint32_t* d_max = reinterpret_cast<uint32_t*>(d_small + 8);
+  TNS_CUDA(cudaMemsetAsync(d_max, 0, QD_MAX_RANK * 4, st));
+  LineError* d_lerr = reinterpret_cast<LineError*>(d_small + 2);
+  if (n_lines) {
+    k_line_classify<<<(unsigned)n_ctas, kLineThreads, 0, st>>>(d_text, n, d_ls, n_nl, n_lines,
+                                                               d_nf, d_cr, d_small);
+    k_scan_excl<<<1, 1024, 0, st>>>(d_cr, n_ctas, d_co);
+  } else {
+    TNS_CUDA(cudaMemsetAsync(d_co, 0, (n_ctas + 1) * 8, st));
+  }
+  uint64_t h2[2] = {0, 0};  // first data line, data rows
+  TNS_CUDA(cudaMemcpyAsync(&h2[0], d_small, 8, cudaMemcpyDeviceToHost, st));
+  TNS_CUDA(cudaMemcpyAsync(&h2[1], d_co + n_ctas, 8, cudaMemcpyDeviceToHost, st));
+  TNS_CUDA(cudaStreamSynchronize(st));
+  const uint64_t rows = h2[1];
+
+  if (rows == 0) {  // io.cpp:115-119, then check_valid (coo.cpp:8-16)
+    if (!has_declared)
+      parse_error(err, n_lines, 8, 0, 0, 0, 0, 0,
+                  "empty file: rank is unknowable without declared dimensions");
+    if (declared_rank == 0) invalid("tensor rank must be positive");
+    for (uint32_t m = 0; m < declared_rank; ++m)
+      if (declared[m] == 0) invalid("dimension of mode " + std::to_string(m) + " must be positive");
+    out->rank = declared_rank;
+    out->dims.assign(declared, declared + declared_rank);
+    return;
+  }
+  const uint64_t first = h2[0];
+  uint32_t nf_first = 0;
+  TNS_CUDA(cudaMemcpy(&nf_first, d_nf + first, 4, cudaMemcpyDeviceToHost));
+  if (nf_first < 2)  // io.cpp:60-64
+    parse_error(err, first + 1, 1, 0, nf_first, 0, 0, 0,
+                "expected at least one index and a value, got " + std::to_string(nf_first) +
+                    " fields");
+  if (has_declared && declared_rank != nf_first - 1)  // io.cpp:65-72
+    parse_error(err, first + 1, 2, 0, nf_first, declared_rank, 0, 0,
+                "file has rank " + std::to_string(nf_first - 1) + " but " +
+                    std::to_string(declared_rank) + " dimensions were declared");
+  const uint32_t rank = nf_first - 1;
+  if (rank > QD_MAX_RANK) invalid("tensor rank must be in 1..64");
+
+  DevBuf b_decl;
+  uint32_t* d_decl = nullptr;
+  if (has_declared) {
+    d_decl = b_decl.alloc<uint32_t>(rank * 4);
+    TNS_CUDA(cudaMemcpyAsync(d_decl, declared, rank * 4, cudaMemcpyHostToDevice, st));
+  }
+  uint32_t* d_coords = nullptr;
+  double* d_values = nullptr;
+  TNS_CUDA(cudaMalloc(&d_coords, rows * rank * 4));
+  if (cudaMalloc(&d_values, rows * 8) != cudaSuccess) {
+    cudaFree(d_coords);
+    throw Error(QD_CUDA_ERROR, "device allocation failed in .tns reader");
+  }
+  out->d_coords = d_coords;
+  out->d_values = d_values;
+  ParseArgs a{d_text, n, d_ls, n_nl, n_lines, d_nf, d_co, nf_first, d_decl,
+              d_coords, d_values, d_max, d_small + 1};
+  k_line_parse<<<(unsigned)n_ctas, kLineThreads, 0, st>>>(a);
+  uint64_t eline = ~0ull;
+  TNS_CUDA(cudaMemcpyAsync(&eline, d_small + 1, 8, cudaMemcpyDeviceToHost, st));
+  TNS_CUDA(cudaStreamSynchronize(st));
+  TNS_CUDA(cudaGetLastError());
+  if (eline != ~0ull) {
+    k_line_error<<<1, 1, 0, st>>>(a, eline, d_lerr);
+    LineError le{};
+    TNS_CUDA(cudaMemcpyAsync(&le, d_lerr, sizeof le, cudaMemcpyDeviceToHost, st));
+    TNS_CUDA(cudaStreamSynchronize(st));
+    const std::string tok(h_text + le.tok_begin, le.tok_len);
+    const std::string mode = std::to_string(le.field + 1);
+    std::string what;
+    switch (le.kind) {  // io.cpp:73-113
+      case kErrFieldCount:
+        what = "expected " + std::to_string(nf_first) + " fields, got " + std::to_string(le.got);
+        break;
+      case kErrIndex: what = "invalid index '" + tok + "'"; break;
+      case kErrZeroIndex: what = "indices are 1-based; got " + tok + " in mode " + mode; break;
+      case kErrExceeds:
+        what = "index " + tok + " exceeds declared dimension " +
+               std::to_string(declared[le.field]) + " of mode " + mode;
+        break;
+      default: what = "invalid value '" + tok + "'"; break;
+    }
+    cudaFree(d_coords);
+    cudaFree(d_values);
+    out->d_coords = nullptr;
+    out->d_values = nullptr;
+    parse_error(err, eline + 1, le.kind, le.field, le.got, nf_first, le.tok_begin, le.tok_len,
+                what);
+  }
+  out->rank = rank;
+  out->nnz = rows;
+  if (has_declared) {
+    out->dims.assign(declared, declared + rank);
+  } else {
+    out->dims.resize(rank);
+    TNS_CUDA(cudaMemcpy(out->dims.data(), d_max, rank * 4, cudaMemcpyDeviceToHost));
+  }
+}
+
+}  // namespace qb200
