@@ -847,16 +847,33 @@ def read_tns_text(text: bytes, declared_dims=None, canonicalize: bool = True,
     if st == QD_PARSE_ERROR:
         raise ParseError(L.qd_last_error().decode(), err.line, err.kind, err.field)
     _check(st)
-    try:
-        r, n = out.rank, out.nnz
-        dims = np.ctypeslib.as_array(out.dims, (r,)).copy() if r else np.zeros(0, np.uint32)
-        coords = (np.ctypeslib.as_array(out.coords, (n * r,)).copy() if n
-                  else np.zeros(0, np.uint32))
-        values = (np.ctypeslib.as_array(out.values, (n,)).copy() if n
-                  else np.zeros(0, np.float64))
-    finally:
-        L.qd_tns_free(C.byref(out))
+    # the rows stay in the library's buffers (no copy); freed with the arrays
+    owner = _TnsOwner(out)
+    r, n = out.rank, out.nnz
+    dims = np.ctypeslib.as_array(out.dims, (r,)).copy() if r else np.zeros(0, np.uint32)
+    coords = owner.view(out.coords, C.c_uint32, n * r, np.uint32)
+    values = owner.view(out.values, C.c_double, n, np.float64)
     return CooTensor(dims, coords, values)
+
+
+class _TnsOwner:
+    """Owns a qd_tns_tensor; numpy views keep it alive, qd_tns_free on collection."""
+
+    def __init__(self, t):
+        self.t = t
+
+    def view(self, ptr, ctype, count, dtype):
+        if count == 0:
+            return np.zeros(0, dtype)
+        buf = (ctype * count).from_address(C.addressof(ptr.contents))
+        buf._owner = self
+        return np.frombuffer(buf, dtype=dtype)
+
+    def __del__(self):
+        try:
+            lib().qd_tns_free(C.byref(self.t))
+        except Exception:
+            pass
 
 
 def read_tns(path, declared_dims=None, canonicalize: bool = True,

@@ -3,6 +3,10 @@
 // with the same exception class (mapped to qd_status):
 //   transpose.cpp:83-89 (rank, verify_input), transpose.cpp:101-103 (top-K),
 //   sort.cpp:153-166 (partial_sort args), parallel.cpp:161-163 (workers).
+#include <sys/mman.h>
+
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cuda_runtime.h>
 #include <cstring>
@@ -348,22 +352,45 @@ qd_status qd_read_tns(const char* text, uint64_t n_bytes, const uint32_t* declar
       if (e != cudaSuccess) throw Error(QD_CUDA_ERROR, cudaGetErrorString(e));
     };
     ck(cudaStreamCreateWithFlags(&sc.st, cudaStreamNonBlocking));
+    // QD_TNS_TIMING=1: phase times on stderr (diagnostics; adds stream syncs)
+    static const bool timing = std::getenv("QD_TNS_TIMING") != nullptr;
+    auto t_last = std::chrono::steady_clock::now();
+    auto mark = [&](const char* what) {
+      if (!timing) return;
+      cudaStreamSynchronize(sc.st);
+      const auto now = std::chrono::steady_clock::now();
+      std::fprintf(stderr, "qd_read_tns %-12s %8.2f ms\n", what,
+                   std::chrono::duration<double, std::milli>(now - t_last).count());
+      t_last = now;
+    };
     TnsParsed p;
     parse_tns_device(text, n_bytes, declared_dims, declared_rank, has_declared != 0, &p, err,
                      sc.st);
     sc.dev.push_back(p.d_coords);
     sc.dev.push_back(p.d_values);
+    mark("parse");
     const uint32_t R = p.rank;
     const uint64_t N = p.nnz;
     qd_tns_tensor t{R, N, nullptr, nullptr, nullptr};
+    // rows in 2 MB-aligned, huge-page-advised memory: first touch costs one
+    // fault per 2 MB instead of per 4 KB page
+    auto big = [](uint64_t bytes) -> void* {
+      const uint64_t a = 2ull << 20;
+      bytes = std::max<uint64_t>(bytes, 1);
+      if (bytes < a) return std::malloc(bytes);
+      void* p = std::aligned_alloc(a, (bytes + a - 1) / a * a);
+      if (p) madvise(p, (bytes + a - 1) / a * a, MADV_HUGEPAGE);
+      return p;
+    };
     t.dims = static_cast<uint32_t*>(std::malloc(std::max<size_t>(R, 1) * 4));
-    t.coords = static_cast<uint32_t*>(std::malloc(std::max<uint64_t>(N * R, 1) * 4));
-    t.values = static_cast<double*>(std::malloc(std::max<uint64_t>(N, 1) * 8));
+    t.coords = static_cast<uint32_t*>(big(N * R * 4));
+    t.values = static_cast<double*>(big(N * 8));
     if (!t.dims || !t.coords || !t.values) {
       qd_tns_free(&t);
       throw std::bad_alloc();
     }
     std::copy(p.dims.begin(), p.dims.end(), t.dims);
+    mark("host alloc");
     const uint32_t* c_src = p.d_coords;
     const double* v_src = p.d_values;
     try {
@@ -382,12 +409,14 @@ qd_status qd_read_tns(const char* text, uint64_t n_bytes, const uint32_t* declar
                    sc.st);
         c_src = c2;
         v_src = v2;
+        mark("canonicalise");
       }
       if (N) {
-        ck(cudaMemcpyAsync(t.coords, c_src, N * R * 4, cudaMemcpyDeviceToHost, sc.st));
-        ck(cudaMemcpyAsync(t.values, v_src, N * 8, cudaMemcpyDeviceToHost, sc.st));
+        staged_d2h(t.coords, c_src, N * R * 4, sc.st);
+        staged_d2h(t.values, v_src, N * 8, sc.st);
       }
       ck(cudaStreamSynchronize(sc.st));
+      mark("copy out");
     } catch (...) {
       qd_tns_free(&t);
       throw;

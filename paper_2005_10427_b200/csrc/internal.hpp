@@ -123,6 +123,11 @@ void partition_rows_device(Workspace& ws, uint32_t rank, uint64_t nnz,
 // host text on the device; on success the rows are in device buffers the
 // caller frees (cudaFree), in file order.  Throws Error(QD_PARSE_ERROR) with
 // the reference's ParseError text and fills *err.
+// Large host<->device copies through a pinned chunk ring with parallel host
+// memcpy (tns.cu); synchronous with respect to the host buffer.
+void staged_h2d(void* d_dst, const void* h_src, uint64_t n, void* stream);
+void staged_d2h(void* h_dst, const void* d_src, uint64_t n, void* stream);
+
 struct TnsParsed {
   uint32_t rank = 0;
   uint64_t nnz = 0;

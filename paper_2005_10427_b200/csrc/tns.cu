@@ -21,6 +21,11 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstring>
+#include <thread>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -278,6 +283,99 @@ __global__ void k_line_error(ParseArgs a, uint64_t k, LineError* out) {
   *out = parse_line(a, b, e, a.nf[k], 0, false, nullptr);
 }
 
+
+// ---- host <-> device copies of the large buffers ---------------------------
+// Pageable cudaMemcpy runs at ~11 GB/s here (driver staging, one thread).
+// Instead: a ring of pinned chunks; host threads fill (or drain) a chunk with
+// a parallel memcpy while the copy engine moves the previous one.
+constexpr uint64_t kStageChunk = 32ull << 20;
+constexpr int kStageSlots = 4;
+constexpr int kCopyThreads = 4;
+
+struct StageRing {
+  char* buf[kStageSlots] = {};
+  cudaEvent_t ev[kStageSlots] = {};
+  int device = -1;
+  ~StageRing() {
+    for (int i = 0; i < kStageSlots; ++i) {
+      if (buf[i]) cudaFreeHost(buf[i]);
+      if (ev[i]) cudaEventDestroy(ev[i]);
+    }
+  }
+  void init() {
+    int dev = 0;
+    TNS_CUDA(cudaGetDevice(&dev));
+    if (device == dev) return;
+    for (int i = 0; i < kStageSlots; ++i) {
+      if (buf[i]) cudaFreeHost(buf[i]);
+      if (ev[i]) cudaEventDestroy(ev[i]);
+      TNS_CUDA(cudaMallocHost(&buf[i], kStageChunk));
+      TNS_CUDA(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+    }
+    device = dev;
+  }
+};
+
+void parallel_memcpy(char* dst, const char* src, uint64_t n) {
+  if (n < (4ull << 20)) {
+    std::memcpy(dst, src, n);
+    return;
+  }
+  std::thread th[kCopyThreads - 1];
+  const uint64_t part = (n / kCopyThreads + 4095) & ~4095ull;
+  for (int t = 1; t < kCopyThreads; ++t) {
+    const uint64_t a = std::min(n, t * part), b = std::min(n, (t + 1) * part);
+    th[t - 1] = std::thread([=] { std::memcpy(dst + a, src + a, b - a); });
+  }
+  std::memcpy(dst, src, std::min(n, part));
+  for (auto& x : th) x.join();
+}
+
+StageRing& stage_ring() {
+  static thread_local StageRing r;
+  r.init();
+  return r;
+}
+
+}  // namespace
+
+void staged_h2d(void* d_dst, const void* h_src, uint64_t n, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  StageRing& r = stage_ring();
+  for (uint64_t off = 0, i = 0; off < n; off += kStageChunk, ++i) {
+    const int k = (int)(i % kStageSlots);
+    const uint64_t len = std::min(kStageChunk, n - off);
+    TNS_CUDA(cudaEventSynchronize(r.ev[k]));  // the slot's previous copy is done
+    parallel_memcpy(r.buf[k], static_cast<const char*>(h_src) + off, len);
+    TNS_CUDA(cudaMemcpyAsync(static_cast<char*>(d_dst) + off, r.buf[k], len,
+                             cudaMemcpyHostToDevice, st));
+    TNS_CUDA(cudaEventRecord(r.ev[k], st));
+  }
+}
+
+void staged_d2h(void* h_dst, const void* d_src, uint64_t n, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  StageRing& r = stage_ring();
+  const uint64_t chunks = (n + kStageChunk - 1) / kStageChunk;
+  auto issue = [&](uint64_t i) {
+    const int k = (int)(i % kStageSlots);
+    const uint64_t off = i * kStageChunk, len = std::min(kStageChunk, n - off);
+    TNS_CUDA(cudaMemcpyAsync(r.buf[k], static_cast<const char*>(d_src) + off, len,
+                             cudaMemcpyDeviceToHost, st));
+    TNS_CUDA(cudaEventRecord(r.ev[k], st));
+  };
+  for (uint64_t i = 0; i < std::min<uint64_t>(chunks, kStageSlots); ++i) issue(i);
+  for (uint64_t i = 0; i < chunks; ++i) {
+    const int k = (int)(i % kStageSlots);
+    const uint64_t off = i * kStageChunk, len = std::min(kStageChunk, n - off);
+    TNS_CUDA(cudaEventSynchronize(r.ev[k]));
+    parallel_memcpy(static_cast<char*>(h_dst) + off, r.buf[k], len);
+    if (i + kStageSlots < chunks) issue(i + kStageSlots);
+  }
+}
+
+namespace {
+
 struct DevBuf {
   void* p = nullptr;
   ~DevBuf() {
@@ -314,6 +412,7 @@ void parse_tns_device(const char* h_text, uint64_t n, const uint32_t* declared,
                       uint32_t declared_rank, bool has_declared, TnsParsed* out,
                       qd_tns_error* err, void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const auto t0 = std::chrono::steady_clock::now();
   out->rank = 0;
   out->nnz = 0;
   out->dims.clear();
@@ -329,7 +428,14 @@ void parse_tns_device(const char* h_text, uint64_t n, const uint32_t* declared,
   char* d_text = b_text.alloc<char>(n16 * 16);
   const uint64_t pad_from = n & ~15ull;  // zero the partial last word and the extra one
   TNS_CUDA(cudaMemsetAsync(d_text + pad_from, 0, n16 * 16 - pad_from, st));
-  if (n) TNS_CUDA(cudaMemcpyAsync(d_text, h_text, n, cudaMemcpyHostToDevice, st));
+  if (n) staged_h2d(d_text, h_text, n, st);
+  static const bool timing = getenv("QD_TNS_TIMING") != nullptr;
+  if (timing) {
+    TNS_CUDA(cudaStreamSynchronize(st));
+    fprintf(stderr, "qd_read_tns   (text H2D + alloc %8.2f ms)\n",
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
+                .count());
+  }
 
   // newlines -> line starts
   const uint64_t n_tiles = (n16 + kTileThreads - 1) / kTileThreads;
