@@ -14,11 +14,16 @@
 //   Workspace (sort.hpp:14)                    device workspace (one GPU)
 //   transpose_inplace / transpose (transpose.hpp:59-66)
 //   partial_sort (sort.hpp:32) / parallel_partial_sort (parallel.hpp:35)
+//   read_tns / ParseError / ReadOptions (io.hpp:15-41)
 #pragma once
 
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
+#include <filesystem>
+#include <fstream>
+#include <iterator>
+#include <optional>
 #include <stdexcept>
 #include <string>
 #include <string_view>
@@ -458,6 +463,49 @@ inline void parallel_partial_sort(CooTensor& t, const std::vector<Mode>& prefix,
                                   Workspace& ws, const ParallelConfig& cfg) {
   if (cfg.workers == 0) throw std::invalid_argument("worker count must be at least 1");
   partial_sort(t, prefix, mode, ws);
+}
+
+// ---- io.hpp: the .tns text format -------------------------------------------
+class ParseError : public std::runtime_error {  // io.hpp:15-22
+ public:
+  ParseError(std::size_t line, const std::string& what_text)
+      : std::runtime_error(what_text), line_(line) {}
+  std::size_t line() const { return line_; }
+
+ private:
+  std::size_t line_;
+};
+
+struct ReadOptions {  // io.hpp:24-35
+  bool canonicalize = true;
+  std::optional<std::vector<std::uint32_t>> declared_dims;
+};
+
+// read_tns over bytes already in memory; parsing and canonicalisation on the GPU.
+inline CooTensor read_tns_text(std::string_view text, const ReadOptions& opts, Workspace& ws) {
+  qd_tns_tensor t{};
+  qd_tns_error e{};
+  const auto& d = opts.declared_dims;
+  const qd_status s = qd_read_tns(text.data(), text.size(), d ? d->data() : nullptr,
+                                  d ? static_cast<std::uint32_t>(d->size()) : 0, d ? 1 : 0,
+                                  opts.canonicalize ? 1 : 0, &t, &e, ws.get());
+  if (s == QD_PARSE_ERROR) throw ParseError(e.line, qd_last_error());
+  detail::check(s);
+  CooTensor out;
+  out.dims.assign(t.dims, t.dims + t.rank);
+  out.coords.assign(t.coords, t.coords + t.nnz * t.rank);
+  out.values.assign(t.values, t.values + t.nnz);
+  qd_tns_free(&t);
+  return out;
+}
+
+// io.hpp:40-41 read_tns(path, opts): the file is read on the host.
+inline CooTensor read_tns(const std::filesystem::path& path, const ReadOptions& opts = {}) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) throw std::runtime_error("cannot open '" + path.string() + "' for reading");
+  std::string text((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+  Workspace ws;
+  return read_tns_text(text, opts, ws);
 }
 
 }  // namespace quesadilla_b200

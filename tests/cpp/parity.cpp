@@ -5,6 +5,10 @@
 // for bit, pass logs and exception classes too.  Built by oracle/Makefile
 // (test infrastructure), run by tests/test_cpp_gpu.py on the GPU box.
 #include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <fstream>
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <random>
@@ -181,6 +185,37 @@ int main() {
     expect(exc_class([&] { qb.check_valid(); }) == exc_class([&] { bb.check_valid(); }) &&
                exc_class([&] { bb.check_valid(); }) == 1,
            "check_valid");
+  }
+  {  // io.hpp read_tns: reference reader vs the GPU reader on the same files
+    Q::GenSpec spec;
+    spec.dims = {300, 20, 4000};
+    spec.nnz = 20000;
+    spec.seed = 11;
+    Q::CooTensor q = Q::generate(spec);
+    std::shuffle(q.values.begin(), q.values.end(), rng);
+    for (auto& v : q.values) v = std::ldexp(v, (int)(rng() % 400) - 200);
+    const std::string path = "/tmp/qd_parity_read.tns";
+    Q::write_tns(q, path);
+    for (int canon = 0; canon < 2; ++canon) {
+      Q::ReadOptions qo;
+      qo.canonicalize = canon;
+      B::ReadOptions bo;
+      bo.canonicalize = canon;
+      expect(same(Q::read_tns(path, qo), B::read_tns(path, bo)), "read_tns rows");
+      qo.declared_dims = std::vector<std::uint32_t>{300, 25, 4000};
+      bo.declared_dims = qo.declared_dims;
+      expect(same(Q::read_tns(path, qo), B::read_tns(path, bo)), "read_tns declared");
+    }
+    {
+      std::ofstream f(path, std::ios::trunc);
+      f << "1 1 1 1.0\n# c\n2 2 2 2.0\n3 0 3 3.0\n";
+    }
+    std::string qw, bw;
+    std::size_t ql = 0, bl = 0;
+    try { Q::read_tns(path); } catch (const Q::ParseError& e) { qw = e.what(); ql = e.line(); }
+    try { B::read_tns(path); } catch (const B::ParseError& e) { bw = e.what(); bl = e.line(); }
+    expect(!qw.empty() && qw == bw && ql == bl && ql == 4, "read_tns ParseError");
+    std::remove(path.c_str());
   }
   std::printf("%s %d checks, %d failures\n", failures ? "FAIL" : "PASS", checks, failures);
   return failures ? 1 : 0;
