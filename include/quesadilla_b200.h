@@ -297,6 +297,16 @@ qd_status qd_read_tns(const char* text, uint64_t n_bytes, const uint32_t* declar
                       qd_tns_tensor* out, qd_tns_error* err, qd_workspace* ws);
 void qd_tns_free(qd_tns_tensor* t);
 
+/* write_tns's text (io.cpp:128-152): per row the 1-based indices and the
+ * value (std::to_chars shortest round-trip, fixed or scientific) separated by
+ * ' ', '\n'-terminated, in storage order; formatted on the GPU.  *text is
+ * library-owned (qd_text_free); the caller writes it to the file.  Like the
+ * reference, the tensor is not validated. */
+qd_status qd_write_tns(uint32_t rank, uint64_t nnz, const uint32_t* coords,
+                       const double* values, char** text, uint64_t* n_bytes,
+                       qd_workspace* ws);
+void qd_text_free(char* text);
+
 #ifdef __cplusplus
 }
 #endif

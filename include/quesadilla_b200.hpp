@@ -14,7 +14,7 @@
 //   Workspace (sort.hpp:14)                    device workspace (one GPU)
 //   transpose_inplace / transpose (transpose.hpp:59-66)
 //   partial_sort (sort.hpp:32) / parallel_partial_sort (parallel.hpp:35)
-//   read_tns / ParseError / ReadOptions (io.hpp:15-41)
+//   read_tns / write_tns / ParseError / ReadOptions (io.hpp:15-47)
 #pragma once
 
 #include <algorithm>
@@ -506,6 +506,20 @@ inline CooTensor read_tns(const std::filesystem::path& path, const ReadOptions& 
   std::string text((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
   Workspace ws;
   return read_tns_text(text, opts, ws);
+}
+
+// io.hpp:47 write_tns: the text is formatted on the GPU, then written here.
+inline void write_tns(const CooTensor& tensor, const std::filesystem::path& path) {
+  std::ofstream out(path, std::ios::trunc | std::ios::binary);
+  if (!out) throw std::runtime_error("cannot open '" + path.string() + "' for writing");
+  Workspace ws;
+  char* text = nullptr;
+  std::uint64_t n = 0;
+  detail::check(qd_write_tns(tensor.rank(), tensor.nnz(), tensor.coords.data(),
+                             tensor.values.data(), &text, &n, ws.get()));
+  out.write(text, static_cast<std::streamsize>(n));
+  qd_text_free(text);
+  if (!out) throw std::runtime_error("failed writing '" + path.string() + "'");
 }
 
 }  // namespace quesadilla_b200

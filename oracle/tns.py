@@ -127,3 +127,59 @@ def read_tns_bytes(text: bytes, declared_dims=None, canonicalize: bool = True):
         order = np.lexsort(tuple(c[:, m] for m in reversed(range(r))))  # stable
         c, v = c[order], v[order]
     return np.asarray(dims, np.uint32), np.ascontiguousarray(c).reshape(-1), v
+
+
+def _fmt_value(x: float) -> str:
+    """std::to_chars(double), shortest round-trip (io.cpp:145): Python's repr
+    gives the same shortest digits; the layout (fixed vs scientific, the
+    shorter, fixed on a tie; exact digits for integer values; 2-digit
+    exponents) is restated here."""
+    if x != x:
+        neg = struct.unpack("<Q", struct.pack("<d", x))[0] >> 63
+        return "-nan" if neg else "nan"
+    if x in (np.inf, -np.inf):
+        return "inf" if x > 0 else "-inf"
+    sign = "-" if struct.unpack("<Q", struct.pack("<d", x))[0] >> 63 else ""
+    x = abs(x)
+    if x == 0.0:
+        return sign + "0"
+    r = repr(x)  # shortest round-trip digits
+    mant, _, exp = r.partition("e")
+    e = int(exp) if exp else 0
+    if "." in mant:
+        ip, fp = mant.split(".")
+    else:
+        ip, fp = mant, ""
+    digits = (ip + fp).lstrip("0")
+    lead_zeros = len(ip + fp) - len((ip + fp).lstrip("0"))
+    X = len(ip) - 1 + e - lead_zeros  # scientific exponent of the first digit
+    digits = digits.rstrip("0") or "0"
+    n = len(digits)
+    ax = abs(X)
+    sci = n + (1 if n > 1 else 0) + 2 + (3 if ax >= 100 else 2)
+    if X >= n - 1:
+        fix = X + 1
+    elif X >= 0:
+        fix = n + 1
+    else:
+        fix = n + 1 - X
+    if fix <= sci:
+        if X >= n - 1:
+            return sign + str(int(x))  # exact integer digits
+        if X >= 0:
+            return sign + digits[:X + 1] + "." + digits[X + 1:]
+        return sign + "0." + "0" * (-X - 1) + digits
+    s = digits[0] + ("." + digits[1:] if n > 1 else "")
+    return f"{sign}{s}e{'-' if X < 0 else '+'}{ax:02d}"
+
+
+def write_tns_bytes(dims, coords, values) -> bytes:
+    """write_tns (io.cpp:128-152): storage order, 1-based indices (u32
+    arithmetic, so 2^32-1 + 1 wraps to 0), ' '-separated, '\n' per row."""
+    r = len(dims)
+    c = np.asarray(coords, np.uint32).reshape(-1, r) if r else np.zeros((0, 0), np.uint32)
+    out = []
+    for row, v in zip(c, np.asarray(values, np.float64)):
+        idx = " ".join(str((int(x) + 1) & 0xFFFFFFFF) for x in row)
+        out.append(f"{idx} {_fmt_value(float(v))}\n")
+    return "".join(out).encode()

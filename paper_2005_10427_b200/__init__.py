@@ -179,6 +179,9 @@ def lib():
                                   C.c_int, C.POINTER(TnsTensorC), C.POINTER(TnsErrorC),
                                   C.c_void_p]
         L.qd_tns_free.argtypes = [C.POINTER(TnsTensorC)]
+        L.qd_write_tns.argtypes = [C.c_uint32, C.c_uint64, _u32p, _f64p,
+                                   C.POINTER(C.c_void_p), C.POINTER(C.c_uint64), C.c_void_p]
+        L.qd_text_free.argtypes = [C.c_void_p]
         _lib = L
     return _lib
 
@@ -886,6 +889,33 @@ def read_tns(path, declared_dims=None, canonicalize: bool = True,
     except OSError:
         raise RuntimeError(f"cannot open '{path}' for reading")
     return read_tns_text(text, declared_dims, canonicalize, ws)
+
+
+def write_tns_text(tensor: CooTensor, ws: Optional[Workspace] = None) -> bytes:
+    """write_tns's file contents (io.cpp:128-152), formatted on the GPU
+    (qd_write_tns): 1-based indices, shortest round-trip values."""
+    L = lib()
+    w = _ws(ws)
+    t = tensor
+    p, n = C.c_void_p(), C.c_uint64(0)
+    c = np.ascontiguousarray(t.coords, np.uint32)
+    v = np.ascontiguousarray(t.values, np.float64)
+    _check(L.qd_write_tns(t.rank(), t.nnz(), c.ctypes.data_as(_u32p), v.ctypes.data_as(_f64p),
+                          C.byref(p), C.byref(n), w.handle))
+    try:
+        return C.string_at(p.value, n.value) if n.value else b""
+    finally:
+        L.qd_text_free(p)
+
+
+def write_tns(tensor: CooTensor, path, ws: Optional[Workspace] = None) -> None:
+    """write_tns(tensor, path) (io.hpp:47)."""
+    text = write_tns_text(tensor, ws)
+    try:
+        with open(path, "wb") as f:
+            f.write(text)
+    except OSError:
+        raise RuntimeError(f"cannot open '{path}' for writing")
 
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -436,6 +436,32 @@ void qd_tns_free(qd_tns_tensor* t) {
   t->nnz = 0;
 }
 
+qd_status qd_write_tns(uint32_t rank, uint64_t nnz, const uint32_t* coords,
+                       const double* values, char** text, uint64_t* n_bytes,
+                       qd_workspace* ws) {
+  return guard([&] {
+    if (!ws) invalid("workspace is null");
+    if (!text || !n_bytes) invalid("output is null");
+    *text = nullptr;
+    *n_bytes = 0;
+    if (rank == 0 && nnz) invalid("tensor rank must be positive");
+    if (nnz && (!coords || !values)) invalid("coordinate or value buffer is null");
+    cudaStream_t st = nullptr;
+    if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess)
+      throw Error(QD_CUDA_ERROR, "stream creation failed");
+    try {
+      format_tns_device(rank, nnz, coords, values, text, n_bytes, st);
+    } catch (...) {
+      cudaStreamSynchronize(st);
+      cudaStreamDestroy(st);
+      throw;
+    }
+    cudaStreamDestroy(st);
+  });
+}
+
+void qd_text_free(char* text) { std::free(text); }
+
 qd_status qd_relabel_target(const uint32_t* source, const uint32_t* target, uint32_t rank,
                             uint32_t* out) {
   return guard([&] {

@@ -128,6 +128,11 @@ void partition_rows_device(Workspace& ws, uint32_t rank, uint64_t nnz,
 void staged_h2d(void* d_dst, const void* h_src, uint64_t n, void* stream);
 void staged_d2h(void* h_dst, const void* d_src, uint64_t n, void* stream);
 
+// write_tns's text (io.cpp:128-152) formatted on the device from host rows;
+// *h_text is malloc-family memory (free()), null when nnz == 0.
+void format_tns_device(uint32_t rank, uint64_t nnz, const uint32_t* h_coords,
+                       const double* h_values, char** h_text, uint64_t* n_text, void* stream);
+
 struct TnsParsed {
   uint32_t rank = 0;
   uint64_t nnz = 0;

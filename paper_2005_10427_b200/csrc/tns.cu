@@ -19,6 +19,7 @@
 //                   ParseError text (io.cpp:16-18)
 // All byte work is HBM-bound: ~1 read of the text per pass, plus the row write.
 #include <cuda_runtime.h>
+#include <sys/mman.h>
 
 #include <algorithm>
 #include <cstring>
@@ -30,6 +31,7 @@
 #include <vector>
 
 #include "internal.hpp"
+#include "tns_format.cuh"
 #include "tns_parse.cuh"
 
 namespace qb200 {
@@ -562,6 +564,118 @@ void parse_tns_device(const char* h_text, uint64_t n, const uint32_t* declared,
     out->dims.resize(rank);
     TNS_CUDA(cudaMemcpy(out->dims.data(), d_max, rank * 4, cudaMemcpyDeviceToHost));
   }
+}
+
+// ---- writer: write_tns (io.cpp:128-152) --------------------------------------
+namespace {
+
+constexpr int kFmtThreads = 256;
+constexpr uint32_t kFmtStage = 40 * 1024;  // CTA text staged in shared memory
+
+__device__ __forceinline__ uint32_t row_text(const uint32_t* coords, const double* values,
+                                             uint32_t rank, uint64_t row, char* out) {
+  uint32_t p = 0;
+  for (uint32_t m = 0; m < rank; ++m) {
+    const uint32_t c = coords[row * rank + m] + 1u;  // u32 arithmetic, as io.cpp:141
+    p += tns::format_u64(c, out ? out + p : nullptr);
+    if (out) out[p] = ' ';
+    ++p;
+  }
+  p += tns::format_f64(values[row], out ? out + p : nullptr);
+  if (out) out[p] = '\n';
+  return p + 1;
+}
+
+__global__ void __launch_bounds__(kFmtThreads)
+k_fmt_len(const uint32_t* __restrict__ coords, const double* __restrict__ values, uint32_t rank,
+          uint64_t nnz, uint32_t* __restrict__ row_len, uint32_t* __restrict__ cta_len) {
+  const uint64_t row = (uint64_t)blockIdx.x * kFmtThreads + threadIdx.x;
+  uint32_t len = 0;
+  if (row < nnz) {
+    len = row_text(coords, values, rank, row, nullptr);
+    row_len[row] = len;
+  }
+  len = __reduce_add_sync(0xffffffffu, len);
+  __shared__ uint32_t ws[kFmtThreads / 32];
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = len;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+    for (int k = 0; k < kFmtThreads / 32; ++k) t += ws[k];
+    cta_len[blockIdx.x] = t;
+  }
+}
+
+__global__ void __launch_bounds__(kFmtThreads)
+k_fmt_write(const uint32_t* __restrict__ coords, const double* __restrict__ values,
+            uint32_t rank, uint64_t nnz, const uint32_t* __restrict__ row_len,
+            const uint64_t* __restrict__ cta_off, char* __restrict__ text) {
+  __shared__ uint32_t wsum[kFmtThreads / 32];
+  __shared__ __align__(16) char stage[kFmtStage];
+  const uint64_t row = (uint64_t)blockIdx.x * kFmtThreads + threadIdx.x;
+  const uint32_t len = row < nnz ? row_len[row] : 0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t s = len;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, s, d);
+    if (lane >= d) s += t;
+  }
+  if (lane == 31) wsum[warp] = s;
+  __syncthreads();
+  uint32_t before = s - len, total = 0;
+  for (int w = 0; w < kFmtThreads / 32; ++w) {
+    if (w < warp) before += wsum[w];
+    total += wsum[w];
+  }
+  const uint64_t base = cta_off[blockIdx.x];
+  if (total <= kFmtStage) {
+    if (row < nnz) row_text(coords, values, rank, row, stage + before);
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < total; i += kFmtThreads) text[base + i] = stage[i];
+  } else if (row < nnz) {
+    row_text(coords, values, rank, row, text + base + before);
+  }
+}
+
+}  // namespace
+
+void format_tns_device(uint32_t rank, uint64_t nnz, const uint32_t* h_coords,
+                       const double* h_values, char** h_text, uint64_t* n_text, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  *h_text = nullptr;
+  *n_text = 0;
+  if (nnz == 0) return;
+  DevBuf b_c, b_v, b_len, b_cl, b_co, b_t;
+  uint32_t* d_c = b_c.alloc<uint32_t>(nnz * rank * 4);
+  double* d_v = b_v.alloc<double>(nnz * 8);
+  staged_h2d(d_c, h_coords, nnz * rank * 4, st);
+  staged_h2d(d_v, h_values, nnz * 8, st);
+  const uint64_t n_ctas = (nnz + kFmtThreads - 1) / kFmtThreads;
+  uint32_t* d_len = b_len.alloc<uint32_t>(nnz * 4);
+  uint32_t* d_cl = b_cl.alloc<uint32_t>(n_ctas * 4);
+  uint64_t* d_co = b_co.alloc<uint64_t>((n_ctas + 1) * 8);
+  k_fmt_len<<<(unsigned)n_ctas, kFmtThreads, 0, st>>>(d_c, d_v, rank, nnz, d_len, d_cl);
+  k_scan_excl<<<1, 1024, 0, st>>>(d_cl, n_ctas, d_co);
+  uint64_t total = 0;
+  TNS_CUDA(cudaMemcpyAsync(&total, d_co + n_ctas, 8, cudaMemcpyDeviceToHost, st));
+  TNS_CUDA(cudaStreamSynchronize(st));
+  char* d_t = b_t.alloc<char>(total);
+  k_fmt_write<<<(unsigned)n_ctas, kFmtThreads, 0, st>>>(d_c, d_v, rank, nnz, d_len, d_co, d_t);
+  TNS_CUDA(cudaGetLastError());
+  const uint64_t a = 2ull << 20, cap = (total + a - 1) / a * a;
+  char* h = static_cast<char*>(std::aligned_alloc(a, cap));
+  if (!h) throw std::bad_alloc();
+  madvise(h, cap, MADV_HUGEPAGE);
+  try {
+    staged_d2h(h, d_t, total, st);
+    TNS_CUDA(cudaStreamSynchronize(st));
+  } catch (...) {
+    std::free(h);
+    throw;
+  }
+  *h_text = h;
+  *n_text = total;
 }
 
 }  // namespace qb200

@@ -59,6 +59,24 @@ def main():
                     "ref_cores": 1, "speedup_call": round(ref_s / gpu_s, 1),
                     "bit_exact_vs_ref": bool(np.array_equal(c, t.coords) and
                                              np.array_equal(v.view(np.uint64), t.values.view(np.uint64)))})
+    # writer: write_tns of the tensor just read (text formatted on the GPU)
+    ts = []
+    for _ in range(5):
+        t0 = time.perf_counter()
+        wtext = qb.write_tns_text(t, ws=ws)
+        ts.append(time.perf_counter() - t0)
+    out.update({"write_gpu_text_s": round(min(ts), 4),
+                "write_gpu_mrows_s": round(n / min(ts) / 1e6, 1)})
+    if reference_available():
+        path = os.path.join(tempfile.gettempdir(), "qd_tns_bench_w.tns")
+        t0 = time.perf_counter()
+        Reference().write_tns(t.dims, t.coords, t.values, path)
+        ref_w = time.perf_counter() - t0
+        with open(path, "rb") as f:
+            same = f.read() == wtext
+        os.unlink(path)
+        out.update({"write_ref_s": round(ref_w, 3), "write_ref_mrows_s": round(n / ref_w / 1e6, 2),
+                    "write_speedup": round(ref_w / min(ts), 1), "write_bytes_equal": same})
     print(json.dumps(out))
 
 

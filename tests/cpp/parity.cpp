@@ -215,6 +215,18 @@ int main() {
     try { Q::read_tns(path); } catch (const Q::ParseError& e) { qw = e.what(); ql = e.line(); }
     try { B::read_tns(path); } catch (const B::ParseError& e) { bw = e.what(); bl = e.line(); }
     expect(!qw.empty() && qw == bw && ql == bl && ql == 4, "read_tns ParseError");
+    // write_tns: the GPU writer's bytes equal the reference writer's
+    {
+      const std::string p1 = "/tmp/qd_parity_w1.tns", p2 = "/tmp/qd_parity_w2.tns";
+      Q::write_tns(q, p1);
+      B::write_tns(to_b(q), p2);
+      std::ifstream f1(p1, std::ios::binary), f2(p2, std::ios::binary);
+      const std::string s1((std::istreambuf_iterator<char>(f1)), std::istreambuf_iterator<char>());
+      const std::string s2((std::istreambuf_iterator<char>(f2)), std::istreambuf_iterator<char>());
+      expect(!s1.empty() && s1 == s2, "write_tns bytes");
+      std::remove(p1.c_str());
+      std::remove(p2.c_str());
+    }
     std::remove(path.c_str());
   }
   std::printf("%s %d checks, %d failures\n", failures ? "FAIL" : "PASS", checks, failures);

@@ -205,3 +205,79 @@ def test_gpu_read_tns_large(tmp_path):
     with pytest.raises(otns.TnsParseError) as eo:
         otns.read_tns_bytes(bad)
     assert str(ei.value) == str(eo.value) and ei.value.line() == eo.value.line
+
+
+# ---- writer (write_tns, io.cpp:128-152) --------------------------------------
+
+def _writer_cases():
+    rng = np.random.default_rng(21)
+    out = []
+    n = 5000
+    c = np.stack([rng.integers(0, d, n) for d in (70, 5, 900)], 1).astype(np.uint32)
+    v = rng.random(n) * 10.0 ** rng.integers(-30, 30, n)
+    out.append(("random", np.array([70, 5, 900], np.uint32), c.reshape(-1), v))
+    bits = rng.integers(0, 2 ** 63, 20000, dtype=np.uint64) | (
+        rng.integers(0, 2, 20000, dtype=np.uint64) << np.uint64(63))
+    vb = bits.view(np.float64)
+    out.append(("bit_patterns", np.array([20000], np.uint32),
+                np.arange(20000, dtype=np.uint32), vb))
+    special = np.array([0.0, -0.0, np.inf, -np.inf, np.nan, 1.0, 0.1, 1e-4, 1e-3, 1e16, 1e21,
+                        1.2345678901234567e21, 12300000.0, 5e-324, 1.7976931348623157e308,
+                        2.0 ** 70, 2.0 ** -1074, 123456.0, 0.5, 2.0 / 3.0])
+    out.append(("special", np.array([4294967295, 2], np.uint32),
+                np.stack([np.arange(len(special)) * 200000000, np.arange(len(special)) % 2], 1)
+                .astype(np.uint32).reshape(-1), special))
+    out.append(("max_coord", np.array([4294967295], np.uint32),
+                np.array([4294967294, 0], np.uint32), np.array([1.5, 2.5])))
+    out.append(("empty", np.array([3, 3], np.uint32), np.zeros(0, np.uint32), np.zeros(0)))
+    return out
+
+
+WCASES = _writer_cases()
+
+
+@pytest.mark.skipif(shutil.which("g++") is None, reason="no g++")
+def test_device_formatter_matches_to_chars(tmp_path):
+    exe = tmp_path / "tfc"
+    subprocess.run(["g++", "-O2", "-std=c++20", "-I",
+                    os.path.join(ROOT, "paper_2005_10427_b200", "csrc"),
+                    os.path.join(ROOT, "tests", "cpp", "tns_format_check.cpp"), "-o", str(exe)],
+                   check=True)
+    r = subprocess.run([str(exe), "200000"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout[-2000:]
+    assert " 0 mismatches" in r.stdout
+
+
+@pytest.mark.skipif(not reference_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("name,dims,coords,values", WCASES, ids=[w[0] for w in WCASES])
+def test_oracle_writer_matches_reference(tmp_path, name, dims, coords, values):
+    p = tmp_path / "w.tns"
+    Reference().write_tns(dims, coords, values, p)
+    assert p.read_bytes() == otns.write_tns_bytes(dims, coords, values)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,dims,coords,values", WCASES, ids=[w[0] for w in WCASES])
+def test_gpu_write_tns_matches_oracle(tmp_path, name, dims, coords, values):
+    import paper_2005_10427_b200 as qb
+    t = qb.CooTensor(dims, coords, values)
+    want = otns.write_tns_bytes(dims, coords, values)
+    assert qb.write_tns_text(t) == want
+    p = tmp_path / "g.tns"
+    qb.write_tns(t, p)
+    assert p.read_bytes() == want
+
+
+@pytest.mark.gpu
+def test_gpu_write_read_round_trip():
+    """write_tns -> read_tns returns the tensor (io.hpp:43-46), 200K rows."""
+    import paper_2005_10427_b200 as qb
+    rng = np.random.default_rng(3)
+    dims = np.array([500, 40, 3000], np.uint32)
+    n = 200_000
+    c = np.stack([rng.integers(0, d, n) for d in dims], 1).astype(np.uint32)
+    c[0] = dims - 1  # every dim reached, so the read-back dims match
+    v = rng.standard_normal(n) * 10.0 ** rng.integers(-300, 300, n)
+    t = qb.CooTensor(dims, c.reshape(-1), v)
+    back = qb.read_tns_text(qb.write_tns_text(t), canonicalize=False)
+    assert back == t
