@@ -891,9 +891,10 @@ def read_tns(path, declared_dims=None, canonicalize: bool = True,
     return read_tns_text(text, declared_dims, canonicalize, ws)
 
 
-def write_tns_text(tensor: CooTensor, ws: Optional[Workspace] = None) -> bytes:
+def write_tns_text(tensor: CooTensor, ws: Optional[Workspace] = None) -> memoryview:
     """write_tns's file contents (io.cpp:128-152), formatted on the GPU
-    (qd_write_tns): 1-based indices, shortest round-trip values."""
+    (qd_write_tns): 1-based indices, shortest round-trip values.  Returns a
+    read-only view of the library's buffer (no copy; bytes(...) copies)."""
     L = lib()
     w = _ws(ws)
     t = tensor
@@ -902,20 +903,34 @@ def write_tns_text(tensor: CooTensor, ws: Optional[Workspace] = None) -> bytes:
     v = np.ascontiguousarray(t.values, np.float64)
     _check(L.qd_write_tns(t.rank(), t.nnz(), c.ctypes.data_as(_u32p), v.ctypes.data_as(_f64p),
                           C.byref(p), C.byref(n), w.handle))
-    try:
-        return C.string_at(p.value, n.value) if n.value else b""
-    finally:
+    if not n.value:
         L.qd_text_free(p)
+        return memoryview(b"")
+    buf = (C.c_char * n.value).from_address(p.value)
+    buf._owner = _TextOwner(p.value)
+    return memoryview(buf).cast("B").toreadonly()
+
+
+class _TextOwner:
+    def __init__(self, addr):
+        self.addr = addr
+
+    def __del__(self):
+        try:
+            lib().qd_text_free(C.c_void_p(self.addr))
+        except Exception:
+            pass
 
 
 def write_tns(tensor: CooTensor, path, ws: Optional[Workspace] = None) -> None:
-    """write_tns(tensor, path) (io.hpp:47)."""
-    text = write_tns_text(tensor, ws)
+    """write_tns(tensor, path) (io.hpp:47): text formatted on the GPU, written
+    to the file straight from the library's buffer."""
     try:
-        with open(path, "wb") as f:
-            f.write(text)
+        f = open(path, "wb")
     except OSError:
         raise RuntimeError(f"cannot open '{path}' for writing")
+    with f:
+        f.write(write_tns_text(tensor, ws))
 
 
 __all__ = [n for n in dir() if not n.startswith("_")]

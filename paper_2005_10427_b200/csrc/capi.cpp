@@ -344,7 +344,8 @@ qd_status qd_read_tns(const char* text, uint64_t n_bytes, const uint32_t* declar
       std::vector<void*> dev;
       ~Scope() {
         if (st) cudaStreamSynchronize(st);
-        for (void* p : dev) cudaFree(p);
+        for (void* p : dev) tns_dev_free(p, st);
+        if (st) cudaStreamSynchronize(st);
         if (st) cudaStreamDestroy(st);
       }
     } sc;
@@ -400,9 +401,9 @@ qd_status qd_read_tns(const char* text, uint64_t n_bytes, const uint32_t* declar
         auto groups = sort_rows_group(R, simple.data(), R);
         uint32_t* c2 = nullptr;
         double* v2 = nullptr;
-        ck(cudaMalloc(&c2, N * R * 4));
+        c2 = static_cast<uint32_t*>(tns_dev_alloc(N * R * 4, sc.st));
         sc.dev.push_back(c2);
-        ck(cudaMalloc(&v2, N * 8));
+        v2 = static_cast<double*>(tns_dev_alloc(N * 8, sc.st));
         sc.dev.push_back(v2);
         TensorView tv{R, p.dims.data(), N};
         run_groups(W(ws), tv, p.d_coords, p.d_values, c2, v2, groups, false, nullptr, nullptr, 0,

@@ -121,10 +121,12 @@ void partition_rows_device(Workspace& ws, uint32_t rank, uint64_t nnz,
 
 // .tns reader (tns.cu): io.cpp:42-126 minus canonicalisation.  Parses the
 // host text on the device; on success the rows are in device buffers the
-// caller frees (cudaFree), in file order.  Throws Error(QD_PARSE_ERROR) with
+// caller frees (tns_dev_free on the same stream), in file order.  Throws Error(QD_PARSE_ERROR) with
 // the reference's ParseError text and fills *err.
 // Large host<->device copies through a pinned chunk ring with parallel host
 // memcpy (tns.cu); synchronous with respect to the host buffer.
+void* tns_dev_alloc(uint64_t bytes, void* stream);  // stream-ordered, pooled
+void tns_dev_free(void* p, void* stream);
 void staged_h2d(void* d_dst, const void* h_src, uint64_t n, void* stream);
 void staged_d2h(void* h_dst, const void* d_src, uint64_t n, void* stream);
 

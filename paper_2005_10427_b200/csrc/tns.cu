@@ -341,6 +341,27 @@ StageRing& stage_ring() {
 
 }  // namespace
 
+// Device buffers of the text paths come from the stream-ordered pool, kept
+// cached across calls (a 348 MB text buffer costs ~ms through cudaMalloc).
+void* tns_dev_alloc(uint64_t bytes, void* stream) {
+  static thread_local int pooled_device = -1;
+  int dev = 0;
+  TNS_CUDA(cudaGetDevice(&dev));
+  if (pooled_device != dev) {
+    cudaMemPool_t pool;
+    TNS_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t keep = ~0ull;
+    TNS_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    pooled_device = dev;
+  }
+  void* p = nullptr;
+  TNS_CUDA(cudaMallocAsync(&p, bytes, static_cast<cudaStream_t>(stream)));
+  return p;
+}
+void tns_dev_free(void* p, void* stream) {
+  if (p) cudaFreeAsync(p, static_cast<cudaStream_t>(stream));
+}
+
 void staged_h2d(void* d_dst, const void* h_src, uint64_t n, void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   StageRing& r = stage_ring();
@@ -380,12 +401,14 @@ namespace {
 
 struct DevBuf {
   void* p = nullptr;
+  cudaStream_t st = nullptr;
   ~DevBuf() {
-    if (p) cudaFree(p);
+    if (p) tns_dev_free(p, st);
   }
   template <class T>
-  T* alloc(uint64_t bytes) {
-    TNS_CUDA(cudaMalloc(&p, std::max<uint64_t>(bytes, 16)));
+  T* alloc(uint64_t bytes, cudaStream_t stream) {
+    st = stream;
+    p = tns_dev_alloc(std::max<uint64_t>(bytes, 16), stream);
     return static_cast<T*>(p);
   }
 };
@@ -427,7 +450,7 @@ void parse_tns_device(const char* h_text, uint64_t n, const uint32_t* declared,
   // text in HBM, zero-padded to whole 16-byte words (and one more word)
   const uint64_t n16 = (n + 15) / 16 + 1;
   DevBuf b_text;
-  char* d_text = b_text.alloc<char>(n16 * 16);
+  char* d_text = b_text.alloc<char>(n16 * 16, st);
   const uint64_t pad_from = n & ~15ull;  // zero the partial last word and the extra one
   TNS_CUDA(cudaMemsetAsync(d_text + pad_from, 0, n16 * 16 - pad_from, st));
   if (n) staged_h2d(d_text, h_text, n, st);
@@ -442,8 +465,8 @@ void parse_tns_device(const char* h_text, uint64_t n, const uint32_t* declared,
   // newlines -> line starts
   const uint64_t n_tiles = (n16 + kTileThreads - 1) / kTileThreads;
   DevBuf b_tc, b_to;
-  uint32_t* d_tc = b_tc.alloc<uint32_t>(n_tiles * 4);
-  uint64_t* d_to = b_to.alloc<uint64_t>((n_tiles + 1) * 8);
+  uint32_t* d_tc = b_tc.alloc<uint32_t>(n_tiles * 4, st);
+  uint64_t* d_to = b_to.alloc<uint64_t>((n_tiles + 1) * 8, st);
   k_nl_count<<<(unsigned)n_tiles, kTileThreads, 0, st>>>((const uint4*)d_text, n16, d_tc);
   k_scan_excl<<<1, 1024, 0, st>>>(d_tc, n_tiles, d_to);
   uint64_t n_nl = 0;
@@ -453,18 +476,18 @@ void parse_tns_device(const char* h_text, uint64_t n, const uint32_t* declared,
   const bool tail = n > 0 && h_text[n - 1] != '\n';
   const uint64_t n_lines = n_nl + (tail ? 1 : 0);
   DevBuf b_ls;
-  uint64_t* d_ls = b_ls.alloc<uint64_t>((n_nl + 2) * 8);
+  uint64_t* d_ls = b_ls.alloc<uint64_t>((n_nl + 2) * 8, st);
   k_nl_positions<<<(unsigned)n_tiles, kTileThreads, 0, st>>>((const uint4*)d_text, n16, d_to,
                                                             d_ls);
 
   // classify lines
   const uint64_t n_ctas = std::max<uint64_t>(1, (n_lines + kLineThreads - 1) / kLineThreads);
   DevBuf b_nf, b_cr, b_co, b_small;
-  uint32_t* d_nf = b_nf.alloc<uint32_t>(n_lines * 4);
-  uint32_t* d_cr = b_cr.alloc<uint32_t>(n_ctas * 4);
-  uint64_t* d_co = b_co.alloc<uint64_t>((n_ctas + 1) * 8);
+  uint32_t* d_nf = b_nf.alloc<uint32_t>(n_lines * 4, st);
+  uint32_t* d_cr = b_cr.alloc<uint32_t>(n_ctas * 4, st);
+  uint64_t* d_co = b_co.alloc<uint64_t>((n_ctas + 1) * 8, st);
   // small: [0] first data line, [1] error line, [2..] LineError, max_index
-  unsigned long long* d_small = b_small.alloc<unsigned long long>(64 + QD_MAX_RANK * 4 + 64);
+  unsigned long long* d_small = b_small.alloc<unsigned long long>(64 + QD_MAX_RANK * 4 + 64, st);
   TNS_CUDA(cudaMemsetAsync(d_small, 0xFF, 16, st));
   uint32_t* d_max = reinterpret_cast<uint32_t*>(d_small + 8);
   TNS_CUDA(cudaMemsetAsync(d_max, 0, QD_MAX_RANK * 4, st));
@@ -510,15 +533,17 @@ void parse_tns_device(const char* h_text, uint64_t n, const uint32_t* declared,
   DevBuf b_decl;
   uint32_t* d_decl = nullptr;
   if (has_declared) {
-    d_decl = b_decl.alloc<uint32_t>(rank * 4);
+    d_decl = b_decl.alloc<uint32_t>(rank * 4, st);
     TNS_CUDA(cudaMemcpyAsync(d_decl, declared, rank * 4, cudaMemcpyHostToDevice, st));
   }
   uint32_t* d_coords = nullptr;
   double* d_values = nullptr;
-  TNS_CUDA(cudaMalloc(&d_coords, rows * rank * 4));
-  if (cudaMalloc(&d_values, rows * 8) != cudaSuccess) {
-    cudaFree(d_coords);
-    throw Error(QD_CUDA_ERROR, "device allocation failed in .tns reader");
+  d_coords = static_cast<uint32_t*>(tns_dev_alloc(rows * rank * 4, st));
+  try {
+    d_values = static_cast<double*>(tns_dev_alloc(rows * 8, st));
+  } catch (...) {
+    tns_dev_free(d_coords, st);
+    throw;
   }
   out->d_coords = d_coords;
   out->d_values = d_values;
@@ -549,8 +574,8 @@ void parse_tns_device(const char* h_text, uint64_t n, const uint32_t* declared,
         break;
       default: what = "invalid value '" + tok + "'"; break;
     }
-    cudaFree(d_coords);
-    cudaFree(d_values);
+    tns_dev_free(d_coords, st);
+    tns_dev_free(d_values, st);
     out->d_coords = nullptr;
     out->d_values = nullptr;
     parse_error(err, eline + 1, le.kind, le.field, le.got, nf_first, le.tok_begin, le.tok_len,
@@ -643,33 +668,47 @@ k_fmt_write(const uint32_t* __restrict__ coords, const double* __restrict__ valu
 void format_tns_device(uint32_t rank, uint64_t nnz, const uint32_t* h_coords,
                        const double* h_values, char** h_text, uint64_t* n_text, void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  static const bool timing = getenv("QD_TNS_TIMING") != nullptr;
+  auto t_last = std::chrono::steady_clock::now();
+  auto mark = [&](const char* what) {
+    if (!timing) return;
+    cudaStreamSynchronize(st);
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "qd_write_tns %-12s %8.2f ms\n", what,
+            std::chrono::duration<double, std::milli>(now - t_last).count());
+    t_last = now;
+  };
   *h_text = nullptr;
   *n_text = 0;
   if (nnz == 0) return;
   DevBuf b_c, b_v, b_len, b_cl, b_co, b_t;
-  uint32_t* d_c = b_c.alloc<uint32_t>(nnz * rank * 4);
-  double* d_v = b_v.alloc<double>(nnz * 8);
+  uint32_t* d_c = b_c.alloc<uint32_t>(nnz * rank * 4, st);
+  double* d_v = b_v.alloc<double>(nnz * 8, st);
   staged_h2d(d_c, h_coords, nnz * rank * 4, st);
   staged_h2d(d_v, h_values, nnz * 8, st);
+  mark("rows H2D");
   const uint64_t n_ctas = (nnz + kFmtThreads - 1) / kFmtThreads;
-  uint32_t* d_len = b_len.alloc<uint32_t>(nnz * 4);
-  uint32_t* d_cl = b_cl.alloc<uint32_t>(n_ctas * 4);
-  uint64_t* d_co = b_co.alloc<uint64_t>((n_ctas + 1) * 8);
+  uint32_t* d_len = b_len.alloc<uint32_t>(nnz * 4, st);
+  uint32_t* d_cl = b_cl.alloc<uint32_t>(n_ctas * 4, st);
+  uint64_t* d_co = b_co.alloc<uint64_t>((n_ctas + 1) * 8, st);
   k_fmt_len<<<(unsigned)n_ctas, kFmtThreads, 0, st>>>(d_c, d_v, rank, nnz, d_len, d_cl);
   k_scan_excl<<<1, 1024, 0, st>>>(d_cl, n_ctas, d_co);
   uint64_t total = 0;
   TNS_CUDA(cudaMemcpyAsync(&total, d_co + n_ctas, 8, cudaMemcpyDeviceToHost, st));
   TNS_CUDA(cudaStreamSynchronize(st));
-  char* d_t = b_t.alloc<char>(total);
+  mark("lengths");
+  char* d_t = b_t.alloc<char>(total, st);
   k_fmt_write<<<(unsigned)n_ctas, kFmtThreads, 0, st>>>(d_c, d_v, rank, nnz, d_len, d_co, d_t);
   TNS_CUDA(cudaGetLastError());
   const uint64_t a = 2ull << 20, cap = (total + a - 1) / a * a;
   char* h = static_cast<char*>(std::aligned_alloc(a, cap));
   if (!h) throw std::bad_alloc();
   madvise(h, cap, MADV_HUGEPAGE);
+  mark("format");
   try {
     staged_d2h(h, d_t, total, st);
     TNS_CUDA(cudaStreamSynchronize(st));
+    mark("text D2H");
   } catch (...) {
     std::free(h);
     throw;
