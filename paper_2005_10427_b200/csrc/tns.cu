@@ -292,7 +292,16 @@ __global__ void k_line_error(ParseArgs a, uint64_t k, LineError* out) {
 // a parallel memcpy while the copy engine moves the previous one.
 constexpr uint64_t kStageChunk = 32ull << 20;
 constexpr int kStageSlots = 4;
-constexpr int kCopyThreads = 4;
+constexpr int kMaxCopyThreads = 8;
+
+int copy_threads() {
+  static const int n = [] {
+    if (const char* e = getenv("QD_COPY_THREADS")) return std::max(1, std::min(kMaxCopyThreads, atoi(e)));
+    const unsigned hc = std::thread::hardware_concurrency();
+    return (int)std::max(1u, std::min<unsigned>(kMaxCopyThreads, hc ? hc / 2 : 4));
+  }();
+  return n;
+}
 
 struct StageRing {
   char* buf[kStageSlots] = {};
@@ -323,14 +332,15 @@ void parallel_memcpy(char* dst, const char* src, uint64_t n) {
     std::memcpy(dst, src, n);
     return;
   }
-  std::thread th[kCopyThreads - 1];
-  const uint64_t part = (n / kCopyThreads + 4095) & ~4095ull;
-  for (int t = 1; t < kCopyThreads; ++t) {
+  const int nt = copy_threads();
+  std::thread th[kMaxCopyThreads - 1];
+  const uint64_t part = (n / nt + 4095) & ~4095ull;
+  for (int t = 1; t < nt; ++t) {
     const uint64_t a = std::min(n, t * part), b = std::min(n, (t + 1) * part);
     th[t - 1] = std::thread([=] { std::memcpy(dst + a, src + a, b - a); });
   }
   std::memcpy(dst, src, std::min(n, part));
-  for (auto& x : th) x.join();
+  for (int t = 1; t < nt; ++t) th[t - 1].join();
 }
 
 StageRing& stage_ring() {
