@@ -3327,15 +3327,36 @@ void run_groups_host(Workspace& ws, const TensorView& t, uint32_t* coords, doubl
   double* ov = ws.get<double>("host_out_v", N);
   uint64_t* db = h_boundaries ? ws.get<uint64_t>("host_bounds", N + 1) : nullptr;
   cudaStream_t st = nullptr;
-  if (N) {
+  // Pageable caller buffers (a std::vector in the C++ drop-in) go through the
+  // pinned chunk ring with a parallel host memcpy (tns.cu): the driver's own
+  // pageable path runs at ~11 GB/s.  Pinned buffers are copied directly.
+  auto pinned = [](const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+  };
+  static const bool no_stage = getenv("QD_NO_STAGE") != nullptr;
+  const bool stage = N && !no_stage && !(pinned(coords) && pinned(values));
+  if (N && stage) {
+    staged_h2d(ic, coords, N * R * 4, st);
+    staged_h2d(iv, values, N * 8, st);
+  } else if (N) {
     QD_CUDA(cudaMemcpyAsync(ic, coords, N * R * 4, cudaMemcpyHostToDevice, st));
     QD_CUDA(cudaMemcpyAsync(iv, values, N * 8, cudaMemcpyHostToDevice, st));
   }
   uint64_t nb = 0;
   run_groups(ws, t, ic, iv, oc, ov, groups, verify_input, db, &nb, boundary_mode, st);
-  if (N) {
+  if (N && stage) {
+    staged_d2h(coords, oc, N * R * 4, st);
+    staged_d2h(values, ov, N * 8, st);
+  } else if (N) {
     QD_CUDA(cudaMemcpyAsync(coords, oc, N * R * 4, cudaMemcpyDeviceToHost, st));
     QD_CUDA(cudaMemcpyAsync(values, ov, N * 8, cudaMemcpyDeviceToHost, st));
+  }
+  if (N) {
     if (db && nb) QD_CUDA(cudaMemcpyAsync(h_boundaries, db, nb * 8, cudaMemcpyDeviceToHost, st));
     QD_CUDA(cudaStreamSynchronize(st));
   }
