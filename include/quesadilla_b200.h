@@ -291,7 +291,9 @@ typedef struct qd_tns_error {
  * `declared_dims` (has_declared != 0) plays ReadOptions::declared_dims;
  * canonicalize != 0 stably sorts the rows into the simple ordering
  * (io.cpp:36-38) on the device.  Parsing runs on the GPU (text copied to
- * HBM once); `err` (nullable) receives the failure location. */
+ * HBM once); `err` (nullable) receives the failure location.  Differences
+ * from the reference: a file of rank > QD_MAX_RANK is QD_INVALID_ARGUMENT
+ * (the reference reads it, but no transpose accepts it). */
 qd_status qd_read_tns(const char* text, uint64_t n_bytes, const uint32_t* declared_dims,
                       uint32_t declared_rank, int has_declared, int canonicalize,
                       qd_tns_tensor* out, qd_tns_error* err, qd_workspace* ws);
