@@ -203,6 +203,10 @@ struct ParseArgs {
   double* values;
   uint32_t* max_index;       // [rank]
   unsigned long long* err_line;
+  // lines whose value needs the big-integer slow path (k_line_slow)
+  unsigned long long* slow_count;
+  uint64_t* slow_line;  // pairs {line, row}
+  uint64_t slow_cap;
 };
 
 // Error kinds (the reference's ParseError texts, io.cpp:60-113).
@@ -222,8 +226,9 @@ struct LineError {
 
 // Parses line [b, e) with nf fields; writes the row when row_out is set.
 // Returns the first failure in the reference's check order.
+template <bool kSlow>
 __device__ LineError parse_line(const ParseArgs& a, uint64_t b, uint64_t e, uint32_t nf,
-                                uint64_t row, bool write, uint32_t* smax) {
+                                uint64_t row, bool write, uint32_t* smax, uint64_t line) {
   LineError err{kErrNone, 0, nf, 0, 0};
   if (nf != a.fields) {
     err.kind = kErrFieldCount;
@@ -247,13 +252,23 @@ __device__ LineError parse_line(const ParseArgs& a, uint64_t b, uint64_t e, uint
       }
     } else {
       double v = 0;
-      if (!tns::parse_f64(a.text + tb, tl, &v)) return LineError{kErrValue, m, nf, tb, tl};
+      const int r = tns::parse_f64_impl<kSlow>(a.text + tb, tl, &v);
+      if (r == 2) {  // rare: finished by k_line_slow (or a full slow re-run)
+        const unsigned long long i = atomicAdd(a.slow_count, 1ull);
+        if (i < a.slow_cap) {
+          a.slow_line[2 * i] = line;
+          a.slow_line[2 * i + 1] = row;
+        }
+        return err;
+      }
+      if (!r) return LineError{kErrValue, m, nf, tb, tl};
       if (write) a.values[row] = v;
     }
   }
   return err;
 }
 
+template <bool kSlow>
 __global__ void __launch_bounds__(kLineThreads) k_line_parse(ParseArgs a) {
   __shared__ uint32_t smax[QD_MAX_RANK];
   __shared__ int wcount[kLineThreads / 32];
@@ -271,7 +286,7 @@ __global__ void __launch_bounds__(kLineThreads) k_line_parse(ParseArgs a) {
   if (nf) {
     uint64_t b, e;
     line_span(a.line_start, a.n_nl, a.n, k, &b, &e);
-    const LineError err = parse_line(a, b, e, nf, row, true, smax);
+    const LineError err = parse_line<kSlow>(a, b, e, nf, row, true, smax, k);
     if (err.kind != kErrNone) atomicMin(a.err_line, (unsigned long long)k);
   }
   __syncthreads();
@@ -282,7 +297,24 @@ __global__ void __launch_bounds__(kLineThreads) k_line_parse(ParseArgs a) {
 __global__ void k_line_error(ParseArgs a, uint64_t k, LineError* out) {
   uint64_t b, e;
   line_span(a.line_start, a.n_nl, a.n, k, &b, &e);
-  *out = parse_line(a, b, e, a.nf[k], 0, false, nullptr);
+  *out = parse_line<true>(a, b, e, a.nf[k], 0, false, nullptr, k);
+}
+
+// The listed lines' values through the exact slow path (their indices were
+// written by k_line_parse).
+__global__ void k_line_slow(ParseArgs a, uint64_t count) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const uint64_t k = a.slow_line[2 * i], row = a.slow_line[2 * i + 1];
+  uint64_t b, e;
+  line_span(a.line_start, a.n_nl, a.n, k, &b, &e);
+  // the value is the last field: skip trailing blanks, then back to its start
+  while (e > b && tns::is_space(a.text[e - 1])) --e;
+  uint64_t tb = e;
+  while (tb > b && !tns::is_space(a.text[tb - 1])) --tb;
+  double v = 0;
+  if (tns::parse_f64_impl<true>(a.text + tb, (uint32_t)(e - tb), &v) == 1) a.values[row] = v;
+  else atomicMin(a.err_line, (unsigned long long)k);
 }
 
 
@@ -557,9 +589,26 @@ void parse_tns_device(const char* h_text, uint64_t n, const uint32_t* declared,
   }
   out->d_coords = d_coords;
   out->d_values = d_values;
+  // slow-path list: {line, row} pairs; QD_TNS_SLOW_CAP overrides the capacity
+  uint64_t slow_cap = std::min<uint64_t>(rows, 1ull << 20);
+  if (const char* ev = getenv("QD_TNS_SLOW_CAP")) slow_cap = strtoull(ev, nullptr, 10);
+  DevBuf b_slow;
+  uint64_t* d_slow = b_slow.alloc<uint64_t>(std::max<uint64_t>(slow_cap, 1) * 16, st);
+  unsigned long long* d_slow_count = d_small + 7;
+  TNS_CUDA(cudaMemsetAsync(d_slow_count, 0, 8, st));
   ParseArgs a{d_text, n, d_ls, n_nl, n_lines, d_nf, d_co, nf_first, d_decl,
-              d_coords, d_values, d_max, d_small + 1};
-  k_line_parse<<<(unsigned)n_ctas, kLineThreads, 0, st>>>(a);
+              d_coords, d_values, d_max, d_small + 1, d_slow_count, d_slow, slow_cap};
+  k_line_parse<false><<<(unsigned)n_ctas, kLineThreads, 0, st>>>(a);
+  uint64_t slow = 0;
+  TNS_CUDA(cudaMemcpyAsync(&slow, d_slow_count, 8, cudaMemcpyDeviceToHost, st));
+  TNS_CUDA(cudaStreamSynchronize(st));
+  TNS_CUDA(cudaGetLastError());
+  if (slow > slow_cap) {  // list overflow: every line again with the slow path inline
+    a.slow_cap = 0;
+    k_line_parse<true><<<(unsigned)n_ctas, kLineThreads, 0, st>>>(a);
+  } else if (slow) {
+    k_line_slow<<<(unsigned)((slow + 127) / 128), 128, 0, st>>>(a, slow);
+  }
   uint64_t eline = ~0ull;
   TNS_CUDA(cudaMemcpyAsync(&eline, d_small + 1, 8, cudaMemcpyDeviceToHost, st));
   TNS_CUDA(cudaStreamSynchronize(st));

@@ -222,7 +222,10 @@ QD_HD int compare_halfway(const Digits& dg, int64_t qd, bool sticky, uint64_t h,
 // ---- std::from_chars(double) over a whole token ------------------------------
 QD_HD bool ieq(char c, char lower) { return c == lower || c == (char)(lower - 32); }
 
-QD_HD bool parse_f64(const char* s, uint32_t n, double* out) {
+// 1 = parsed, 0 = rejected, 2 = the exact slow path is needed but kSlow is
+// false (kernels without it keep no big-integer stack frame).
+template <bool kSlow>
+QD_HD int parse_f64_impl(const char* s, uint32_t n, double* out) {
   uint32_t i = 0;
   bool neg = false;
   if (i < n && s[i] == '-') {
@@ -239,26 +242,26 @@ QD_HD bool parse_f64(const char* s, uint32_t n, double* out) {
     const uint32_t m = n - i;
     const char* t = s + i;
     if (ieq(t[0], 'i')) {
-      if (m == 3 && ieq(t[1], 'n') && ieq(t[2], 'f')) { r.u = sign | 0x7FF0000000000000ull; *out = r.d; return true; }
+      if (m == 3 && ieq(t[1], 'n') && ieq(t[2], 'f')) { r.u = sign | 0x7FF0000000000000ull; *out = r.d; return 1; }
       if (m == 8 && ieq(t[1], 'n') && ieq(t[2], 'f') && ieq(t[3], 'i') && ieq(t[4], 'n') &&
           ieq(t[5], 'i') && ieq(t[6], 't') && ieq(t[7], 'y')) {
-        r.u = sign | 0x7FF0000000000000ull; *out = r.d; return true;
+        r.u = sign | 0x7FF0000000000000ull; *out = r.d; return 1;
       }
-      return false;
+      return 0;
     }
-    if (m < 3 || !ieq(t[1], 'a') || !ieq(t[2], 'n')) return false;
+    if (m < 3 || !ieq(t[1], 'a') || !ieq(t[2], 'n')) return 0;
     if (m > 3) {
-      if (t[3] != '(' || t[m - 1] != ')') return false;
+      if (t[3] != '(' || t[m - 1] != ')') return 0;
       for (uint32_t k = 4; k + 1 < m; ++k) {
         const char c = t[k];
         const bool ok = (c >= '0' && c <= '9') || (c >= 'a' && c <= 'z') ||
                         (c >= 'A' && c <= 'Z') || c == '_';
-        if (!ok) return false;
+        if (!ok) return 0;
       }
     }
     r.u = sign | 0x7FF8000000000000ull;
     *out = r.d;
-    return true;
+    return 1;
   }
   // digits [. digits]
   const uint32_t num_begin = i;
@@ -290,7 +293,7 @@ QD_HD bool parse_f64(const char* s, uint32_t n, double* out) {
       if (!frac) ++adj;
     }
   }
-  if (ndig == 0) return false;
+  if (ndig == 0) return 0;
   const uint32_t mant_end = i;
   int64_t e10 = 0;
   if (i < n && (s[i] == 'e' || s[i] == 'E')) {
@@ -310,17 +313,18 @@ QD_HD bool parse_f64(const char* s, uint32_t n, double* out) {
       i = j;
     }
   }
-  if (i != n) return false;
+  if (i != n) return 0;
   if (w == 0) {  // every digit is zero
     r.u = sign;
     *out = r.d;
-    return true;
+    return 1;
   }
   const int64_t q = e10 + adj;
   Adjusted a = compute_float(q, w);
   if (sticky) {
     const Adjusted b = compute_float(q, w + 1);
     if (a.mantissa != b.mantissa || a.power2 != b.power2) {
+      if constexpr (!kSlow) return 2;
       // Exact decision between a and its successor: X vs the upper halfway.
       Digits dg{s + num_begin, mant_end - num_begin, first};
       // significant digits all count; D has min(nsig, kMaxBigDigits) digits
@@ -342,8 +346,11 @@ QD_HD bool parse_f64(const char* s, uint32_t n, double* out) {
       int64_t e2;
       if (a.power2 == 0) { m2 = a.mantissa; e2 = -1074; }
       else { m2 = a.mantissa | (1ull << 52); e2 = (int64_t)a.power2 - 1075; }
-      Big A, B;
-      const int c = compare_halfway(dg, qd, st, 2 * m2 + 1, e2 - 1, A, B);
+      int c = 0;
+      if constexpr (kSlow) {
+        Big A, B;
+        c = compare_halfway(dg, qd, st, 2 * m2 + 1, e2 - 1, A, B);
+      }
       if (c > 0 || (c == 0 && (m2 & 1))) {  // round up to the successor
         uint64_t bits = ((uint64_t)a.power2 << 52) | a.mantissa;
         ++bits;
@@ -352,11 +359,15 @@ QD_HD bool parse_f64(const char* s, uint32_t n, double* out) {
       }
     }
   }
-  if (a.power2 >= 0x7FF) return false;              // overflow: out_of_range
-  if (a.power2 == 0 && a.mantissa == 0) return false;  // underflow: out_of_range
+  if (a.power2 >= 0x7FF) return 0;              // overflow: out_of_range
+  if (a.power2 == 0 && a.mantissa == 0) return 0;  // underflow: out_of_range
   r.u = sign | ((uint64_t)a.power2 << 52) | a.mantissa;
   *out = r.d;
-  return true;
+  return 1;
+}
+
+QD_HD bool parse_f64(const char* s, uint32_t n, double* out) {
+  return parse_f64_impl<true>(s, n, out) == 1;
 }
 
 }  // namespace tns

@@ -281,3 +281,25 @@ def test_gpu_write_read_round_trip():
     t = qb.CooTensor(dims, c.reshape(-1), v)
     back = qb.read_tns_text(qb.write_tns_text(t), canonicalize=False)
     assert back == t
+
+
+@pytest.mark.gpu
+def test_gpu_read_tns_slow_path_list_overflow(monkeypatch):
+    """Values that need the big-integer path are finished by k_line_slow from
+    a bounded list; when the list overflows every line is re-parsed with the
+    slow path inline.  Both give the oracle's rows."""
+    import paper_2005_10427_b200 as qb
+    name, text, decl, canon = [c for c in CASES if c[0] == "halfway_values"][0]
+    want = _oracle(text, decl, canon)
+    for cap in ("1000000", "4", "0"):
+        monkeypatch.setenv("QD_TNS_SLOW_CAP", cap)
+        t = qb.read_tns_text(text, decl, canon)
+        assert _same_rows(("ok", t.dims, t.coords, t.values), want), cap
+    # a slow-path value that underflows is still the first failing line
+    bad = b"1 1.0\n2 2.47032822920623272088e-324\n3 x\n"
+    monkeypatch.setenv("QD_TNS_SLOW_CAP", "8")
+    with pytest.raises(qb.ParseError) as ei:
+        qb.read_tns_text(bad)
+    with pytest.raises(otns.TnsParseError) as eo:
+        otns.read_tns_bytes(bad)
+    assert str(ei.value) == str(eo.value) and ei.value.line() == 2
