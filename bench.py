@@ -1,29 +1,38 @@
 #!/usr/bin/env python
 """bench.py — Quesadilla COO transposition on B200 (BASELINE.json metric:
-nonzeros transposed/sec (Mnnz/s) and achieved HBM GB/s vs roofline).
+nonzeros transposed/sec (Mnnz/s) and achieved HBM GB/s vs roofline, on
+1/2/4/8 B200).
 
-Workload (BASELINE.json configs[1], the metric's headline config): the
-nell-2-shaped 3-order tensor 12092x9184x28818 with 76,879,419 unique Zipf(1.1)
-nonzeros (seeded synthetic stand-in, paper_2005_10427_b200/synth.py), input
-sorted in (0,1,2).  One STEP = transposing it to all 5 non-identity target
-orderings (each through the full Quesadilla plan on the GPU), so one step
-moves 5 x 76.9M nonzeros.
+Workload (default --config c5 = BASELINE.json configs[4], the configuration
+the 1/2/4/8-GPU metric is quoted on; it fits one B200): 4821207 x 1774269 x
+1805187 with 1,741,809,018 unique Zipf(1.05) nonzeros (seeded synthetic
+stand-in, paper_2005_10427_b200/synth.generate_device), input sorted in
+(0,1,2).  One STEP = transposing it to both of the config's targets, (1,0,2)
+(one exchange when sharded) and (0,2,1) (bucketed; communication-free when
+sharded), each through the full Quesadilla plan on the GPU: 2 x 1.74 G
+nonzeros per step.  `--config c1..c4` run the other configurations (per-target
+diagnostics).
 
-  value : whole-job Mnnz/s, inputs resident in HBM, device-timed (CUDA events
-          around exactly K steps, max over ranks)
-  e2e   : the same metric through the host C-ABI entry (qd_transpose_inplace_async
-          + qd_workspace_synchronize on pinned host buffers, one call per target,
-          K steps enqueued back to back): every H2D + GPU pass + D2H inside the
-          timed region; the per-step synchronised figure is reported beside it
-  roofline : dominant kernel class, algorithmic bytes / its event-timed
+  value : whole-job Mnnz/s, inputs resident in HBM (34.8 GB, far above the
+          126 MB L2: no flush needed), CUDA events around exactly K steps
+  e2e   : the same metric through the reference-facing host call
+          (qd_transpose_inplace on host buffers = transpose_inplace's
+          signature, transpose.hpp:59-61): every H2D byte, the device passes
+          and every D2H byte inside the timed region, one call per target
+  roofline : the dominant kernel class, algorithmic bytes / its event-timed
           duration (recorded by the library on its launch stream) vs the
-          measured HBM copy peak (MEASURED_PEAKS.json)
-  cpu_baseline : the reference library itself (oracle/_ref, compiled from the
-          reference sources) on this host's cores, one full step
+          measured HBM copy peak (MEASURED_PEAKS.json); model_roofline = the
+          SURVEY §8(d) B_total byte model per target
+  cpu_baseline : the reference library itself (oracle/_ref: the unmodified
+          reference sources) on this host's cores, on a bounded sample of the
+          same tensor (contiguous row windows, which stay simply sorted):
+          parallel (std::thread workers = all cores) and serial (workers = 1)
 
 --impl reference times the reference's own CPU implementation (oracle/_ref,
-std::thread workers = all host cores) on the same workload and prints the same
-JSON line with "impl": "reference".
+std::thread workers = all host cores) on the same bytes: each step
+transposes one contiguous window of the tensor (2^27 rows, the window moving
+each step) to both targets; one full-size run per target is added when host
+RAM allows.
 """
 from __future__ import annotations
 
@@ -44,13 +53,17 @@ sys.path.insert(0, ROOT)
 def parse_args():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=30)
+    p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--config", default="c2")
+    p.add_argument("--config", default="c5")
     p.add_argument("--nnz", type=int, default=None, help="override nnz (testing only)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--ref-window", type=int, default=1 << 27,
+                   help="rows per reference-arm step (a contiguous window)")
+    p.add_argument("--no-ref-full", action="store_true",
+                   help="reference arm: skip the one full-size run per target")
     return p.parse_args()
 
 
@@ -154,6 +167,8 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -163,7 +178,7 @@ def peaks():
 
 
 def ncu_traffic():
-    """dram bytes per row moved by k_onesweep from the committed ncu capture."""
+    """dram bytes per row moved by k_scatter, from the committed ncu capture."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             return json.load(f)
@@ -171,75 +186,66 @@ def ncu_traffic():
         return None
 
 
+def host_info():
+    """nproc, lscpu model name and host RAM."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except Exception:
+        pass
+    ram = None
+    try:
+        import psutil
+        ram = round(psutil.virtual_memory().total / 2**30, 1)
+    except Exception:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model, "ram_gib": ram}
+
+
+def avail_ram():
+    try:
+        import psutil
+        return psutil.virtual_memory().available
+    except Exception:
+        return 0
+
+
 # ---------------------------------------------------------------------------
 # workload
 # ---------------------------------------------------------------------------
-def make_input(cfg, nnz, device):
+def make_input(cfg, nnz, device="cuda"):
+    """Device-resident seeded input (int32 coords [N*r], f64 values [N])."""
     from paper_2005_10427_b200 import synth
-    if device is not None:
-        return synth.generate_torch(cfg, nnz, device=device)
-    c, v = synth.generate(cfg, nnz)
-    return c.view(np.int32), v
+    n = cfg.nnz if nnz is None else nnz
+    if n > 200_000_000 and all(k in ("zipf", "uniform") for k in cfg.dist):
+        return synth.generate_device(cfg, n, device=device)
+    return synth.generate_torch(cfg, n, device=device)
 
 
-def reference_step(ref, ctx, hc, hv, targets, workers):
-    """Reference transpose_inplace for every target; returns seconds (sum)."""
-    import ctypes as C
-    tot = 0.0
-    for t in targets:
-        ref.lib.qref_ctx_reset(ctx, hc, hv)
-        ta = np.asarray(t, np.uint32)
-        t0 = time.perf_counter()
-        s = ref.lib.qref_ctx_transpose(ctx, ta, workers)
-        tot += time.perf_counter() - t0
-        if s:
-            raise RuntimeError(ref.lib.qref_last_error().decode())
-    return tot
-
-
-def run_reference(args, cfg, rank):
-    """--impl reference: the reference's own CPU implementation (oracle/_ref)."""
-    if rank != 0:
-        return
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    from pyoracle import Reference, reference_available
-    import ctypes as C
-    if not reference_available():
-        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libqref.so not built"}))
-        return
-    try:
-        import torch
-        dev = "cuda" if torch.cuda.is_available() else None
-    except Exception:
-        dev = None
-    ci, vi = make_input(cfg, args.nnz, dev)
-    hc = np.ascontiguousarray(ci.cpu().numpy() if dev else ci).view(np.uint32)
-    hv = np.ascontiguousarray(vi.cpu().numpy() if dev else vi)
-    del ci, vi
-    n = len(hv)
-    ref = Reference()
-    workers = os.cpu_count() or 1
-    dims = np.asarray(cfg.dims, np.uint32)
-    ctx = ref.lib.qref_ctx_create(len(dims), dims, n, hc, hv)
-    for _ in range(args.warmup):
-        reference_step(ref, ctx, hc, hv, cfg.targets, workers)
-    secs = sum(reference_step(ref, ctx, hc, hv, cfg.targets, workers) for _ in range(args.steps))
-    ref.lib.qref_ctx_destroy(ctx)
-    units = n * len(cfg.targets) * args.steps
-    v = units / secs / 1e6
-    print(json.dumps({
-        "impl": "reference", "metric": "nonzeros transposed/sec (Mnnz/s)", "value": round(v, 3),
-        "unit": "Mnnz/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(secs / args.steps * 1e3, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u32+f64", "data": "synthetic",
-        "config": workload_config(cfg, n),
-        "cpu_baseline": {"value": round(v, 3), "unit": "Mnnz/s", "cores": workers,
-                         "kind": "reference",
-                         "sample": f"full workload: {len(cfg.targets)} targets x {n} nnz per step, "
-                                   "reference transpose_inplace (Quesadilla, std::thread workers)"},
-        "e2e": {"value": round(v, 3), "unit": "Mnnz/s", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0},
-    }))
+def row_checksum_device(ci, vi, r):
+    """Order-independent checksum of the (coords, value bits) row multiset,
+    computed on the device in chunks (two wrapping int64 sums of mixed
+    words): equal for a permutation of the rows, different (w.h.p.) when a
+    row is dropped, duplicated or altered."""
+    import torch
+    n = vi.numel()
+    c = ci.view(n, r)
+    s1 = torch.zeros((), dtype=torch.int64, device=vi.device)
+    s2 = torch.zeros((), dtype=torch.int64, device=vi.device)
+    k1 = [0x1F3D5B79A3C4E1, 0x2E4C6A8F1B3D5, 0x3A5C7E9B2D4F6, 0x4B6D8FA3C5E71, 0x5C7E9A1B3D5F8]
+    for a in range(0, n, 1 << 27):
+        b = min(n, a + (1 << 27))
+        x = vi[a:b].view(torch.int64).clone()
+        for m in range(r):
+            x = x * 0x5851F42D4C957F2D + (c[a:b, m].to(torch.int64) + 1) * k1[m % 5]
+            x = x ^ (x >> 29)
+        s1 += x.sum()
+        s2 += (x * x + (x >> 17)).sum()
+    return (int(s1.item()), int(s2.item()))
 
 
 def survey_bytes(dims, target, n):
@@ -261,13 +267,187 @@ def survey_bytes(dims, target, n):
     return b
 
 
+def tname(t):
+    return "(" + ",".join(map(str, t)) + ")"
+
+
 def workload_config(cfg, n, world=1):
     return {"workload": f"{cfg.name}: {'x'.join(map(str, cfg.dims))}, {n} unique nnz "
                         f"({cfg.dist[0]} s={cfg.s}), targets "
-                        + " ".join("(" + ",".join(map(str, t)) + ")" for t in cfg.targets),
+                        + " ".join(tname(t) for t in cfg.targets),
             "nnz": n, "rank": len(cfg.dims), "targets_per_step": len(cfg.targets),
             "parallelism": f"shard{world}" if world > 1 else "single-gpu",
             "l2": "inputs (>= 1.5 GB) larger than the 126 MB L2; no flush needed"}
+
+
+# ---------------------------------------------------------------------------
+# the reference's CPU implementation (oracle/_ref): test infrastructure used
+# only as the timed baseline
+# ---------------------------------------------------------------------------
+def ref_lib():
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from pyoracle import Reference, reference_available
+    if not reference_available():
+        return None
+    return Reference()
+
+
+def ref_windows(n, rows):
+    """Row windows [a, b) of `rows` rows each (the last one clipped)."""
+    rows = max(1, min(rows, n))
+    return [(a, min(n, a + rows)) for a in range(0, n, rows)]
+
+
+def ref_time_window(ref, dims, hc, hv, a, b, targets, workers, ctx_cache):
+    """Reference transpose_inplace of rows [a, b) (a contiguous window of a
+    simply sorted tensor is simply sorted) to every target; returns the
+    summed seconds of the transpose calls (the pristine restore is untimed)."""
+    r = len(dims)
+    rows = b - a
+    key = rows
+    if ctx_cache.get("rows") != key:
+        if ctx_cache.get("ctx"):
+            ref.lib.qref_ctx_destroy(ctx_cache["ctx"])
+        ctx_cache["ctx"] = ref.lib.qref_ctx_create(r, np.asarray(dims, np.uint32), rows,
+                                                   hc[a * r:b * r], hv[a:b])
+        ctx_cache["rows"] = key
+    ctx = ctx_cache["ctx"]
+    tot = 0.0
+    for t in targets:
+        ref.lib.qref_ctx_reset(ctx, hc[a * r:b * r], hv[a:b])
+        ta = np.asarray(t, np.uint32)
+        t0 = time.perf_counter()
+        s = ref.lib.qref_ctx_transpose(ctx, ta, workers)
+        tot += time.perf_counter() - t0
+        if s:
+            raise RuntimeError(ref.lib.qref_last_error().decode())
+    return tot
+
+
+def ref_sample(ref, cfg, hc, hv, rows, workers, reps, start=0):
+    """`reps` steps over consecutive windows of `rows` rows (cycling);
+    returns (Mnnz/s, seconds, nnz processed)."""
+    n = len(hv)
+    wins = ref_windows(n, rows)
+    cache = {}
+    secs = units = 0
+    for k in range(reps):
+        a, b = wins[(start + k) % len(wins)]
+        secs += ref_time_window(ref, cfg.dims, hc, hv, a, b, cfg.targets, workers, cache)
+        units += (b - a) * len(cfg.targets)
+    if cache.get("ctx"):
+        ref.lib.qref_ctx_destroy(cache["ctx"])
+    return units / secs / 1e6, secs, units
+
+
+def host_input(cfg, nnz):
+    """The workload's bytes on the host (generated on the device when one is
+    present, so both arms see identical bytes)."""
+    try:
+        import torch
+        dev = torch.cuda.is_available()
+    except Exception:
+        dev = False
+    if dev:
+        ci, vi = make_input(cfg, nnz, "cuda")
+        hc = ci.cpu().numpy().view(np.uint32)
+        hv = vi.cpu().numpy()
+        del ci, vi
+        torch.cuda.empty_cache()
+        return hc, hv
+    from paper_2005_10427_b200 import synth
+    c, v = synth.generate(cfg, nnz)
+    return c.view(np.uint32), v
+
+
+def run_reference(args, cfg, rank):
+    """--impl reference: the reference's own CPU implementation (oracle/_ref,
+    the unmodified reference sources compiled in place) on this host."""
+    if rank != 0:
+        return
+    ref = ref_lib()
+    if ref is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libqref.so not built"}))
+        return
+    hc, hv = host_input(cfg, args.nnz)
+    n = len(hv)
+    workers = os.cpu_count() or 1
+    rows = min(n, args.ref_window)
+    nwin = len(ref_windows(n, rows))
+    ref_sample(ref, cfg, hc, hv, rows, workers, args.warmup, start=nwin // 2)
+    v, secs, units = ref_sample(ref, cfg, hc, hv, rows, workers, args.steps)
+    # serial path (workers = 1, sort.cpp) on a smaller window
+    srows = max(1, min(n, rows // 16))
+    sv, ssecs, sunits = ref_sample(ref, cfg, hc, hv, srows, 1, 2)
+    full = None
+    # one full-size run per target when the host can hold the tensor, the
+    # reference's working copy, its Workspace and the pristine bytes
+    need = n * (4 * len(cfg.dims) + 8) * 3 + n * 12 + (1 << 30)
+    if rows < n and not args.no_ref_full:
+        if avail_ram() > need:
+            cache = {}
+            per = {}
+            for t in cfg.targets:
+                s = ref_time_window(ref, cfg.dims, hc, hv, 0, n, [t], workers, cache)
+                per[tname(t)] = {"s": round(s, 3), "Mnnz_s": round(n / s / 1e6, 2)}
+            ref.lib.qref_ctx_destroy(cache["ctx"])
+            tot = sum(x["s"] for x in per.values())
+            full = {"Mnnz_s": round(n * len(cfg.targets) / tot / 1e6, 3), "per_target": per,
+                    "workers": workers, "reps": 1}
+        else:
+            full = {"value": None,
+                    "reason": f"not run (RAM: {avail_ram() / 2**30:.0f} GiB available, "
+                              f"{need / 2**30:.0f} GiB needed)"}
+    elif rows >= n:
+        full = {"note": "the sample windows are the whole tensor"}
+    hi = host_info()
+    sample = (f"{args.steps} steps, each one contiguous window of {rows} rows of the "
+              f"{n}-row tensor (windows advance each step; {nwin} windows) transposed to "
+              f"{len(cfg.targets)} targets by the reference transpose_inplace (Quesadilla, "
+              f"std::thread workers = {workers}); pristine restore untimed")
+    print(json.dumps({
+        "impl": "reference", "metric": "nonzeros transposed/sec (Mnnz/s)", "value": round(v, 3),
+        "unit": "Mnnz/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(secs / args.steps * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u32 coords + f64 values",
+        "data": "synthetic (same seeded bytes as the GPU arm)",
+        "config": workload_config(cfg, n),
+        "cpu_baseline": {"value": round(v, 3), "unit": "Mnnz/s", "cores": workers,
+                         "kind": "reference", "sample": sample,
+                         "parallel": {"value": round(v, 3), "workers": workers,
+                                      "rows_per_step": rows},
+                         "serial": {"value": round(sv, 3), "workers": 1,
+                                    "sample": f"2 windows of {srows} rows x {len(cfg.targets)} "
+                                              "targets (sort.cpp serial path)"},
+                         "full_size": full, **hi},
+        "e2e": {"value": round(v, 3), "unit": "Mnnz/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }))
+
+
+def cpu_baseline(cfg, hc, hv):
+    """Reference library (oracle/_ref) on this host, bounded samples of the
+    same tensor: parallel (all cores) and serial (workers = 1)."""
+    try:
+        ref = ref_lib()
+    except Exception:
+        ref = None
+    if ref is None:
+        return None
+    n = len(hv)
+    workers = os.cpu_count() or 1
+    prow = min(n, 1 << 26)
+    pv, _, _ = ref_sample(ref, cfg, hc, hv, prow, workers, 2, start=1)
+    srow = min(n, 1 << 22)
+    sv, _, _ = ref_sample(ref, cfg, hc, hv, srow, 1, 2, start=3)
+    return {"value": round(pv, 3), "unit": "Mnnz/s", "cores": workers, "kind": "reference",
+            "sample": f"2 contiguous windows of {prow} rows of the same tensor x "
+                      f"{len(cfg.targets)} targets, reference transpose_inplace (Quesadilla, "
+                      f"std::thread workers = {workers})",
+            "parallel": {"value": round(pv, 3), "workers": workers, "rows": prow},
+            "serial": {"value": round(sv, 3), "workers": 1, "rows": srow,
+                       "sample": "2 windows, sort.cpp serial path"},
+            **host_info()}
 
 
 # ---------------------------------------------------------------------------
@@ -286,14 +466,15 @@ def main():
     import torch
     import paper_2005_10427_b200 as qd
     torch.cuda.set_device(local)
-    dist = None
     if world > 1 or os.environ.get("QD_FORCE_SHARDED"):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         from paper_2005_10427_b200 import shard
         return shard.bench_sharded(args, cfg, dist, rank, world, local)
 
+    t_gen = time.perf_counter()
     ci, vi = make_input(cfg, args.nnz, "cuda")
+    t_gen = time.perf_counter() - t_gen
     n = vi.numel()
     r = len(cfg.dims)
     co = torch.empty_like(ci)
@@ -301,40 +482,47 @@ def main():
     ws = qd.Workspace(local)
     stream = torch.cuda.current_stream()
     sp = stream.cuda_stream
+    strat = qd.SortStrategy.quesadilla()
+
+    def one(t):
+        qd.transpose_device(r, cfg.dims, n, ci.data_ptr(), vi.data_ptr(), co.data_ptr(),
+                            vo.data_ptr(), t, strat, ws, sp)
 
     def step():
         for t in cfg.targets:
-            qd.transpose_device(r, cfg.dims, n, ci.data_ptr(), vi.data_ptr(), co.data_ptr(),
-                                vo.data_ptr(), t, qd.SortStrategy.quesadilla(), ws, sp)
+            one(t)
 
     for _ in range(args.warmup):
         step()
-    # sanity: the last target's output is sorted under it (device check)
+    # the output of every target: sorted under it, and the same row multiset
+    checks = {}
     if not os.environ.get("QD_SCATTER_DBG"):  # experiment switch: stores skipped
-        assert qd.is_sorted_device(r, n, co.data_ptr(), cfg.targets[-1], ws, sp)
+        h_in = row_checksum_device(ci, vi, r)
+        for t in cfg.targets:
+            one(t)
+            ok_sorted = qd.is_sorted_device(r, n, co.data_ptr(), t, ws, sp)
+            ok_rows = row_checksum_device(co, vo, r) == h_in
+            assert ok_sorted and ok_rows, (t, ok_sorted, ok_rows)
+            checks[tname(t)] = "sorted under target; row-multiset checksum equal"
 
     # timed region 1 (value): exactly K steps, library profiling off
     l0 = ws.launches()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     with ClockSampler(local) as clk:
-        e0.record(stream)
         marks[0].record(stream)
         for k in range(args.steps):
             step()
             marks[k + 1].record(stream)
-        e1.record(stream)
         torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1)
+    ms = marks[0].elapsed_time(marks[-1])
     per_step = sorted(marks[k].elapsed_time(marks[k + 1]) for k in range(args.steps))
     launches = ws.launches() - l0
     units = n * len(cfg.targets) * args.steps
     value = units / (ms / 1e3) / 1e6
 
     # timed region 2 (roofline): the same K steps with the library's CUDA
-    # events around every kernel on its launch stream (per-class durations);
-    # the events add ~6 % to the step, so they stay out of region 1
+    # events around every kernel on its launch stream (per-class durations)
     ws.profile(True)
     ws.profile_reset()
     p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -348,7 +536,6 @@ def main():
     prof = ws.profile_stats()
     ws.profile(False)
 
-    # roofline of the dominant kernel class
     top = max(("scatter", "local", "hist"), key=lambda k: prof[k]["ms"])
     p = prof[top]
     peak, peak_kind = peaks()
@@ -361,103 +548,52 @@ def main():
     step_ms = ms_prof / args.steps
     share = {k: round(v["ms"] / args.steps / step_ms, 4) for k, v in prof.items()}
 
-    # per-target device time (one extra untimed-for-value round) and the
-    # SURVEY §8(d) byte-model roofline fraction of each
+    # per-target device time (min of 3) and the SURVEY §8(d) byte-model
+    # roofline fraction of each
     per_target = {}
     model_bytes = 0
     for t in cfg.targets:
-        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a0.record(stream)
-        qd.transpose_device(r, cfg.dims, n, ci.data_ptr(), vi.data_ptr(), co.data_ptr(),
-                            vo.data_ptr(), t, qd.SortStrategy.quesadilla(), ws, sp)
-        a1.record(stream)
-        torch.cuda.synchronize()
-        tms = a0.elapsed_time(a1)
+        tms = []
+        for _ in range(3):
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            one(t)
+            a1.record(stream)
+            torch.cuda.synchronize()
+            tms.append(a0.elapsed_time(a1))
+        tm = min(tms)
         mb = survey_bytes(cfg.dims, t, n)
         model_bytes += mb
+        lb = n * (2 * (4 * r + 8) + 4 * len(qd.quesadilla_plan(t).steps))
         per_target["".join(str(x) for x in t)] = {
-            "ms": round(tms, 4), "Mnnz_s": round(n / tms / 1e3, 1),
+            "ms": round(tm, 4), "Mnnz_s": round(n / tm / 1e3, 1),
             "model_GB": round(mb / 1e9, 3),
-            "model_frac": round(mb / (tms / 1e3) / 1e9 / peaks()[0], 4)}
+            "model_frac": round(mb / (tm / 1e3) / 1e9 / peak, 4),
+            "model_frac_nominal_8TBs": round(mb / (tm / 1e3) / 1e9 / 8000.0, 4),
+            "lowerbound_frac": round(lb / (tm / 1e3) / 1e9 / peak, 4)}
 
-    # end to end through the host C-ABI entry, pinned host buffers: every
-    # step transposes a fresh host copy of the input to each target with
-    # qd_transpose_inplace_async (one call per target, as the reference CLI's
-    # bench loop makes) and waits for the last output copy; the input copy of
-    # call i+1 overlaps the output copy of call i (full-duplex PCIe).  Wall
-    # clock around the whole step: H2D + device work + D2H of all targets.
+    # host copy of the input (pinned) for e2e and the CPU baseline
+    need_host = n * (4 * r + 8) * 2
     e2e = None
-    if not args.no_e2e:
-        # K steps, each step = one async call per target on its own pinned
-        # host copy of the input (25 buffer pairs for K = 5: the in-place API
-        # overwrites its input, so every call of the timed region needs fresh
-        # host bytes).  The K steps are enqueued back to back and waited for
-        # once: consecutive steps overlap their copies like consecutive
-        # targets do (a stream of tensors through the API).  The per-step
-        # synchronised figure (wait after every step) is reported beside it.
-        hc0 = ci.cpu().numpy().view(np.uint32)
-        hv0 = vi.cpu().numpy()
-        # K = 5 steps (fewer when the host lacks the RAM for 5 x targets
-        # pinned input copies, leaving half of it free)
-        step_bytes = n * (4 * r + 8) * len(cfg.targets)
-        try:
-            import psutil
-            avail = psutil.virtual_memory().available
-        except Exception:
-            avail = 0
-        k_e2e = max(1, min(args.steps, 5, int(avail // 2 // max(1, step_bytes))))
-        pins = [(torch.empty(hc0.shape, dtype=torch.int32).pin_memory(),
-                 torch.empty(hv0.shape, dtype=torch.float64).pin_memory())
-                for _ in range(k_e2e * len(cfg.targets))]
-        bufs = [(pc.numpy().view(np.uint32), pv.numpy()) for pc, pv in pins]
+    hc0 = hv0 = None
+    if not (args.no_e2e and args.no_cpu_baseline):
+        pc = torch.empty(ci.shape, dtype=torch.int32, pin_memory=True)
+        pv = torch.empty(vi.shape, dtype=torch.float64, pin_memory=True)
+        pc.copy_(ci)
+        pv.copy_(vi)
+        hc0, hv0 = pc.numpy().view(np.uint32), pv.numpy()
+    # the device-resident tensors are released: the host-buffer call stages
+    # its own device copies (34.8 GB in + 34.8 GB out at c5)
+    del ci, vi, co, vo
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
 
-        def fill(bs):
-            tens = []
-            for hc, hv in bs:
-                np.copyto(hc, hc0)
-                np.copyto(hv, hv0)
-                tens.append(qd.CooTensor(cfg.dims, hc, hv))  # wraps the pinned buffers
-            return tens
-
-        nt = len(cfg.targets)
-        sync_s = 0.0
-        warm = 2  # both async device slots grow during warm-up
-        for it in range(warm + k_e2e):
-            tens = fill(bufs[:nt])
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            for tn, t in zip(tens, cfg.targets):
-                qd.transpose_inplace_async(tn, t, qd.SortStrategy.quesadilla(), ws)
-            ws.synchronize()
-            if it >= warm:
-                sync_s += time.perf_counter() - t0
-        tens = fill(bufs)
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        for j, tn in enumerate(tens):
-            qd.transpose_inplace_async(tn, cfg.targets[j % nt], qd.SortStrategy.quesadilla(), ws)
-        ws.synchronize()
-        pipe_s = time.perf_counter() - t0
-        # spot check: the last call's host output is sorted under its target
-        last = tens[-1].coords.reshape(-1, r)[:200_000]
-        key = np.lexsort(tuple(last[:, m] for m in reversed(cfg.targets[-1])))
-        assert np.array_equal(key, np.arange(len(key))), "e2e output not sorted"
-        e2e = {"value": round(n * nt * k_e2e / pipe_s / 1e6, 3),
-               "unit": "Mnnz/s", "h2d_bytes_per_step": n * (4 * r + 8) * nt,
-               "d2h_bytes_per_step": n * (4 * r + 8) * nt,
-               "steps": k_e2e, "ms_per_step": round(pipe_s / k_e2e * 1e3, 2),
-               "timing": "host wall clock around K steps enqueued back to back "
-                         "(every H2D/D2H byte inside), one wait at the end",
-               "step_synchronized": {"value": round(n * nt * k_e2e / sync_s / 1e6, 3),
-                                     "ms_per_step": round(sync_s / k_e2e * 1e3, 2),
-                                     "timing": "wait after every step"},
-               "api": "qd_transpose_inplace_async x targets + qd_workspace_synchronize "
-                      "(host buffers, pinned)"}
-        del pins, bufs, tens
+    if not args.no_e2e and avail_ram() > need_host // 2:
+        e2e = run_e2e(args, cfg, qd, ws, hc0, hv0, r, n)
 
     cpu = None
     if not args.no_cpu_baseline:
-        cpu = cpu_baseline(cfg, ci, vi)
+        cpu = cpu_baseline(cfg, hc0, hv0)
 
     out = {
         "metric": "nonzeros transposed/sec (Mnnz/s)", "value": round(value, 3), "unit": "Mnnz/s",
@@ -467,8 +603,10 @@ def main():
         "ms_per_step_median": round(per_step[len(per_step) // 2], 4),
         "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u32 coords + f64 values (moved, not computed)",
-        "data": "synthetic (seeded Zipf stand-in for nell-2; FROSTT files unavailable offline)",
+        "data": f"synthetic (seeded {cfg.dist[0]} stand-in; FROSTT files unavailable offline; "
+                f"generated on the device in {t_gen:.1f} s)",
         "config": workload_config(cfg, n),
+        "checks": checks,
         "roofline": {"bound": "hbm", "kernel": {"scatter": "k_scatter", "local": "k_local",
                                                 "hist": "k_chunk_hist"}[top],
                      "achieved": round(achieved, 1), "peak": peak, "peak_kind": peak_kind,
@@ -479,10 +617,13 @@ def main():
                      "step_share": share,
                      "timing": "second timed region of the same K steps with the library's "
                                "per-kernel CUDA events (ms_per_step there: %.4f)" % step_ms},
-        "model_roofline": {"note": "SURVEY.md §8(d) B_total byte model per step over the 5 targets",
+        "model_roofline": {"note": "SURVEY.md §8(d) B_total byte model per step over the "
+                                   "targets; per target: min of 3 event-timed calls",
                            "bytes_per_step": model_bytes,
                            "achieved_GBs": round(model_bytes / (ms / args.steps / 1e3) / 1e9, 1),
-                           "frac": round(model_bytes / (ms / args.steps / 1e3) / 1e9 / peaks()[0], 4),
+                           "frac": round(model_bytes / (ms / args.steps / 1e3) / 1e9 / peak, 4),
+                           "frac_nominal_8TBs": round(
+                               model_bytes / (ms / args.steps / 1e3) / 1e9 / 8000.0, 4),
                            "per_target": per_target},
         "e2e": e2e,
         "gpu_launches": launches,
@@ -492,28 +633,43 @@ def main():
     print(json.dumps(out))
 
 
-def cpu_baseline(cfg, ci, vi):
-    """Reference library (oracle/_ref) on this host: one full step, all cores."""
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    try:
-        from pyoracle import Reference, reference_available
-    except Exception:
-        return None
-    if not reference_available():
-        return None
-    ref = Reference()
-    hc = ci.cpu().numpy().view(np.uint32).copy()
-    hv = vi.cpu().numpy().copy()
-    n = len(hv)
-    dims = np.asarray(cfg.dims, np.uint32)
-    workers = os.cpu_count() or 1
-    ctx = ref.lib.qref_ctx_create(len(dims), dims, n, hc, hv)
-    best = min(reference_step(ref, ctx, hc, hv, cfg.targets, workers) for _ in range(2))
-    ref.lib.qref_ctx_destroy(ctx)
-    return {"value": round(n * len(cfg.targets) / best / 1e6, 3), "unit": "Mnnz/s",
-            "cores": workers, "kind": "reference",
-            "sample": f"one full step ({len(cfg.targets)} targets x {n} nnz), min of 2 reps, "
-                      "reference transpose_inplace Quesadilla with std::thread workers"}
+def run_e2e(args, cfg, qd, ws, hc0, hv0, r, n):
+    """End to end through the reference-facing host call: qd_transpose_inplace
+    on pinned host buffers (transpose_inplace's signature; synchronous), one
+    call per target per step, the tensor's bytes refreshed from the pristine
+    copy before every call (untimed: the call is in place).  Host wall clock
+    around each call: H2D + device passes + D2H."""
+    import torch
+    k_e2e = max(1, min(args.steps, 2 if n > 500_000_000 else 5))
+    wc = torch.empty(hc0.shape, dtype=torch.int32, pin_memory=True)
+    wv = torch.empty(hv0.shape, dtype=torch.float64, pin_memory=True)
+    hc, hv = wc.numpy().view(np.uint32), wv.numpy()
+    tens = qd.CooTensor(cfg.dims, hc, hv)  # wraps the pinned buffers
+    strat = qd.SortStrategy.quesadilla()
+    secs = 0.0
+    for it in range(1 + k_e2e):  # one untimed warm-up step (workspace growth)
+        for t in cfg.targets:
+            wc.copy_(torch.from_numpy(hc0.view(np.int32)))
+            wv.copy_(torch.from_numpy(hv0))
+            t0 = time.perf_counter()
+            qd.transpose_inplace(tens, t, strat, ws)
+            dt = time.perf_counter() - t0
+            if it:
+                secs += dt
+    last = hc.reshape(-1, r)
+    m = min(len(last), 1 << 21)
+    for a in (0, len(last) - m):  # spot check: host output sorted under the last target
+        blk = last[a:a + m]
+        key = np.lexsort(tuple(blk[:, j] for j in reversed(cfg.targets[-1])))
+        assert np.array_equal(key, np.arange(len(key))), "e2e output not sorted"
+    del tens, wc, wv
+    per = n * (4 * r + 8) * len(cfg.targets)
+    return {"value": round(n * len(cfg.targets) * k_e2e / secs / 1e6, 3), "unit": "Mnnz/s",
+            "h2d_bytes_per_step": per, "d2h_bytes_per_step": per, "steps": k_e2e,
+            "ms_per_step": round(secs / k_e2e * 1e3, 2),
+            "timing": "host wall clock around each synchronous call (every H2D/D2H byte "
+                      "inside), summed over the step's targets",
+            "api": "qd_transpose_inplace (pinned host buffers) x targets"}
 
 
 if __name__ == "__main__":

@@ -18,6 +18,7 @@
 #pragma once
 
 #include <algorithm>
+#include <charconv>
 #include <cstdint>
 #include <cstdlib>
 #include <filesystem>
@@ -53,11 +54,16 @@ class Ordering {
  public:
   explicit Ordering(std::vector<Mode> modes) : modes_(std::move(modes)) {
     const std::size_t r = modes_.size();
-    if (r == 0 || r > kMaxRank) throw std::invalid_argument("ordering rank must be in 1..64");
+    // the reference's checks and messages (ordering.cpp:13-31)
+    if (r == 0 || r > kMaxRank)
+      throw std::invalid_argument("ordering rank must be in 1.." + std::to_string(kMaxRank));
     std::uint64_t seen = 0;
     for (Mode m : modes_) {
-      if (m >= r) throw std::invalid_argument("ordering contains mode outside 0..r-1");
-      if (seen & (std::uint64_t{1} << m)) throw std::invalid_argument("ordering repeats a mode");
+      if (m >= r)
+        throw std::invalid_argument("ordering contains mode " + std::to_string(m) + " outside 0.." +
+                                    std::to_string(r - 1));
+      if (seen & (std::uint64_t{1} << m))
+        throw std::invalid_argument("ordering repeats mode " + std::to_string(m));
       seen |= std::uint64_t{1} << m;
     }
   }
@@ -108,13 +114,11 @@ inline Ordering parse_ordering(std::string_view text) {
       const std::size_t comma = text.find(',', pos);
       const std::string_view tok = text.substr(pos, comma == std::string_view::npos
                                                         ? std::string_view::npos : comma - pos);
+      // std::from_chars like ordering.cpp:77-83: no sign, no spaces, and a
+      // value that overflows unsigned is rejected (not wrapped)
       unsigned v = 0;
-      bool ok = !tok.empty();
-      for (char ch : tok) {
-        if (ch < '0' || ch > '9') { ok = false; break; }
-        v = v * 10 + static_cast<unsigned>(ch - '0');
-      }
-      if (!ok || v == 0) throw std::invalid_argument("bad ordering element '" + std::string(tok) + "'");
+      const auto [ptr, ec] = std::from_chars(tok.data(), tok.data() + tok.size(), v);
+      if (ec != std::errc{} || ptr != tok.data() + tok.size() || v == 0) throw std::invalid_argument("bad ordering element '" + std::string(tok) + "'");
       m.push_back(static_cast<Mode>(v - 1));
       if (comma == std::string_view::npos) break;
       pos = comma + 1;
@@ -314,13 +318,11 @@ inline SortStrategy parse_strategy(std::string_view name) {
   if (name == "comparison" || name == "qsort") return SortStrategy::comparison_sort();
   if (name == "splatt") return SortStrategy::splatt_style();
   if (name.size() > 3 && name.substr(0, 3) == "top") {
+    // std::from_chars like transpose.cpp:30-36 (overflow rejected)
     unsigned k = 0;
-    bool ok = true;
-    for (char ch : name.substr(3)) {
-      if (ch < '0' || ch > '9') { ok = false; break; }
-      k = k * 10 + static_cast<unsigned>(ch - '0');
-    }
-    if (ok && k >= 1) return SortStrategy::top_k(static_cast<Mode>(k));
+    const char* last = name.data() + name.size();
+    const auto [ptr, ec] = std::from_chars(name.data() + 3, last, k);
+    if (ec == std::errc{} && ptr == last && k >= 1) return SortStrategy::top_k(static_cast<Mode>(k));
   }
   throw std::invalid_argument("unknown strategy '" + std::string(name) +
                               "' (expected quesadilla, top<K>, radix, comparison, splatt or qsort)");

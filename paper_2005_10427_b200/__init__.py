@@ -222,8 +222,13 @@ class Ordering:
         r = len(modes)
         if r == 0 or r > MAX_RANK:
             raise InvalidArgument(f"ordering rank must be in 1..{MAX_RANK}")
-        if sorted(modes) != list(range(r)):
-            raise InvalidArgument(f"ordering {modes} is not a permutation of 0..{r - 1}")
+        seen = set()
+        for m in modes:  # the reference's checks and messages (ordering.cpp:13-31)
+            if m < 0 or m >= r:
+                raise InvalidArgument(f"ordering contains mode {m} outside 0..{r - 1}")
+            if m in seen:
+                raise InvalidArgument(f"ordering repeats mode {m}")
+            seen.add(m)
         self._m = tuple(modes)
 
     @staticmethod
@@ -263,6 +268,15 @@ class Ordering:
         return f"Ordering({list(self._m)})"
 
 
+def _from_chars_u32(tok: str):
+    """std::from_chars into an unsigned (32-bit): ASCII digits only, no sign or
+    spaces, None on a parse failure or overflow."""
+    if not tok or any(c < "0" or c > "9" for c in tok):
+        return None
+    v = int(tok)
+    return v if v < 2**32 else None
+
+
 def parse_ordering(text: str) -> Ordering:
     """'2134' (1-based digits) or '10,2,1' (ordering.cpp:68-99)."""
     if not text:
@@ -270,7 +284,7 @@ def parse_ordering(text: str) -> Ordering:
     if "," in text:
         vals = []
         for tok in text.split(","):
-            if not tok.isdigit() or int(tok) == 0:
+            if not _from_chars_u32(tok):
                 raise InvalidArgument(f"bad ordering element '{tok}'")
             vals.append(int(tok) - 1)
         return Ordering(vals)
@@ -397,7 +411,7 @@ def parse_strategy(name: str) -> SortStrategy:
         return SortStrategy.comparison_sort()
     if name == "splatt":
         return SortStrategy.splatt_style()
-    if len(name) > 3 and name.startswith("top") and name[3:].isdigit() and int(name[3:]) >= 1:
+    if len(name) > 3 and name.startswith("top") and (_from_chars_u32(name[3:]) or 0) >= 1:
         return SortStrategy.top_k(int(name[3:]))
     raise InvalidArgument(f"unknown strategy '{name}' (expected quesadilla, top<K>, radix, "
                           "comparison, splatt or qsort)")

@@ -2246,7 +2246,18 @@ struct Workspace {
     size_t nc = 0;
     const void* v = nullptr;
     size_t nv = 0;
-  } last_host;  // host bytes the latest async call writes back
+  };
+  // every async call whose device->host copy may still be pending: the host
+  // bytes it writes back, and an event recorded after that copy (by the
+  // worker, once it has issued it: issued_seq >= seq)
+  struct Pending {
+    HostSpan span;
+    cudaEvent_t done = nullptr;
+    uint64_t seq = 0;
+  };
+  std::deque<Pending> pending;
+  std::vector<cudaEvent_t> done_pool;  // recycled Pending::done events (under mu)
+  uint64_t next_seq = 0, issued_seq = 0;
   struct AsyncJob {
     std::vector<uint32_t> dims;
     uint64_t nnz = 0;
@@ -2255,6 +2266,8 @@ struct Workspace {
     std::vector<Group> groups;
     bool verify_input = false;
     int slot = 0;
+    cudaEvent_t done = nullptr;  // recorded after the output copy
+    uint64_t seq = 0;
   };
   std::thread worker;
   std::mutex mu;
@@ -2410,6 +2423,8 @@ void workspace_destroy(Workspace* ws) {
   if (ws->h_err) cudaFreeHost(ws->h_err);
   if (ws->h_small) cudaFreeHost(ws->h_small);
   for (auto e : ws->ev_pool) cudaEventDestroy(e);
+  for (auto e : ws->done_pool) cudaEventDestroy(e);
+  for (auto& p : ws->pending) cudaEventDestroy(p.done);
   delete ws;
 }
 
@@ -3397,6 +3412,7 @@ void async_worker(Workspace* ws) {
       QD_CUDA(cudaMemcpyAsync(job.coords, sb.oc, N * R * 4, cudaMemcpyDeviceToHost, ws->s_out));
       QD_CUDA(cudaMemcpyAsync(job.values, sb.ov, N * 8, cudaMemcpyDeviceToHost, ws->s_out));
       QD_CUDA(cudaEventRecord(ws->ev_out[sl], ws->s_out));
+      QD_CUDA(cudaEventRecord(job.done, ws->s_out));
     } catch (const Error& e) {
       std::lock_guard<std::mutex> lk(ws->mu);
       if (!ws->async_failed) {
@@ -3408,6 +3424,7 @@ void async_worker(Workspace* ws) {
       }
       cudaEventRecord(ws->ev_comp[sl], ws->s_comp);  // slot reusable after the failed work
       cudaEventRecord(ws->ev_out[sl], ws->s_comp);
+      cudaEventRecord(job.done, ws->s_comp);
     } catch (const std::exception& e) {
       std::lock_guard<std::mutex> lk(ws->mu);
       if (!ws->async_failed) {
@@ -3417,9 +3434,11 @@ void async_worker(Workspace* ws) {
       }
       cudaEventRecord(ws->ev_comp[sl], ws->s_comp);
       cudaEventRecord(ws->ev_out[sl], ws->s_comp);
+      cudaEventRecord(job.done, ws->s_comp);
     }
     {
       std::lock_guard<std::mutex> lk(ws->mu);
+      ws->issued_seq = job.seq;  // jobs run in FIFO order
       ws->slot_busy[sl] = false;
       --ws->running;
     }
@@ -3444,22 +3463,37 @@ void run_groups_host_async(Workspace& ws, const TensorView& t, uint32_t* coords,
   const uint64_t N = t.nnz;
   const uint32_t R = t.rank;
   const int sl = ws.slot;
-  const int psl = (sl + Workspace::kSlots - 1) % Workspace::kSlots;  // the previous call's slot
   auto overlaps = [](const void* a, size_t na, const void* b, size_t nb) {
     const char *x = static_cast<const char*>(a), *y = static_cast<const char*>(b);
     return na && nb && x < y + nb && y < x + na;
   };
   const Workspace::HostSpan cur{coords, N * R * 4, values, N * 8};
-  const Workspace::HostSpan& prev = ws.last_host;
-  const bool chained = overlaps(cur.c, cur.nc, prev.c, prev.nc) ||
-                       overlaps(cur.c, cur.nc, prev.v, prev.nv) ||
-                       overlaps(cur.v, cur.nv, prev.c, prev.nc) ||
-                       overlaps(cur.v, cur.nv, prev.v, prev.nv);
+  // every earlier call (any slot, not only the previous one: A, B, A
+  // interleavings) whose output copy writes host bytes this call reads must
+  // finish that copy before this call's input copy starts.  Calls whose copy
+  // has completed leave the pending list.
+  std::vector<cudaEvent_t> waits;
   {
-    // this slot's previous job must have issued its output copy (so ev_out
-    // is its final record); a chained call also needs the previous one's
     std::unique_lock<std::mutex> lk(ws.mu);
-    ws.cv.wait(lk, [&] { return !ws.slot_busy[sl] && (!chained || !ws.slot_busy[psl]); });
+    while (!ws.pending.empty() && ws.pending.front().seq <= ws.issued_seq &&
+           cudaEventQuery(ws.pending.front().done) == cudaSuccess) {
+      ws.done_pool.push_back(ws.pending.front().done);
+      ws.pending.pop_front();
+    }
+    cudaGetLastError();  // cudaEventQuery's cudaErrorNotReady is not an error
+    uint64_t need = 0;
+    for (const Workspace::Pending& p : ws.pending) {
+      const Workspace::HostSpan& h = p.span;
+      if (overlaps(cur.c, cur.nc, h.c, h.nc) || overlaps(cur.c, cur.nc, h.v, h.nv) ||
+          overlaps(cur.v, cur.nv, h.c, h.nc) || overlaps(cur.v, cur.nv, h.v, h.nv)) {
+        need = std::max(need, p.seq);
+        waits.push_back(p.done);
+      }
+    }
+    // this slot's previous job must have issued its output copy (so ev_out
+    // is its final record), and so must every overlapping one (so its done
+    // event is recorded)
+    ws.cv.wait(lk, [&] { return !ws.slot_busy[sl] && ws.issued_seq >= need; });
   }
   Workspace::SlotBuf& sb = ws.slots[sl];
   if (sb.rows < N || sb.rank < R) {
@@ -3480,7 +3514,7 @@ void run_groups_host_async(Workspace& ws, const TensorView& t, uint32_t* coords,
   // so input copies run back to back while earlier outputs drain; a chained
   // call reads host bytes the previous call's output copy writes
   QD_CUDA(cudaStreamWaitEvent(ws.s_in, ws.ev_comp[sl], 0));
-  if (chained) QD_CUDA(cudaStreamWaitEvent(ws.s_in, ws.ev_out[psl], 0));
+  for (cudaEvent_t e : waits) QD_CUDA(cudaStreamWaitEvent(ws.s_in, e, 0));
   QD_CUDA(cudaMemcpyAsync(sb.ic, coords, N * R * 4, cudaMemcpyHostToDevice, ws.s_in));
   QD_CUDA(cudaMemcpyAsync(sb.iv, values, N * 8, cudaMemcpyHostToDevice, ws.s_in));
   QD_CUDA(cudaEventRecord(ws.ev_in[sl], ws.s_in));
@@ -3492,14 +3526,21 @@ void run_groups_host_async(Workspace& ws, const TensorView& t, uint32_t* coords,
   job.groups = groups;
   job.verify_input = verify_input;
   job.slot = sl;
+  job.seq = ++ws.next_seq;
   {
     std::lock_guard<std::mutex> lk(ws.mu);
+    if (ws.done_pool.empty()) {
+      QD_CUDA(cudaEventCreateWithFlags(&job.done, cudaEventDisableTiming));
+    } else {
+      job.done = ws.done_pool.back();
+      ws.done_pool.pop_back();
+    }
+    ws.pending.push_back({cur, job.done, job.seq});
     ws.slot_busy[sl] = true;
     ws.jobs.push_back(std::move(job));
   }
   ws.cv.notify_all();
   ws.slot = (sl + 1) % Workspace::kSlots;
-  ws.last_host = cur;
 }
 
 // Wait until the worker has no queued or running job (the calling thread may

@@ -23,6 +23,8 @@
 
 #include <algorithm>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <thread>
 #include <chrono>
 #include <cstdio>
@@ -383,21 +385,37 @@ StageRing& stage_ring() {
 
 }  // namespace
 
-// Device buffers of the text paths come from the stream-ordered pool, kept
-// cached across calls (a 348 MB text buffer costs ~ms through cudaMalloc).
+// Device buffers of the text paths come from a PRIVATE stream-ordered pool
+// per device (a 348 MB text buffer costs ~ms through cudaMalloc).  The pool
+// keeps up to kTnsPoolKeep bytes cached across calls and returns the rest to
+// the device at the next synchronisation, so a large read/write does not pin
+// memory the engine's Workspace (cudaMalloc) or other cudaMallocAsync users
+// need later; the device's default pool is left untouched.
+constexpr uint64_t kTnsPoolKeep = 2ull << 30;
 void* tns_dev_alloc(uint64_t bytes, void* stream) {
-  static thread_local int pooled_device = -1;
+  static std::mutex mu;
+  static std::map<int, cudaMemPool_t> pools;
   int dev = 0;
   TNS_CUDA(cudaGetDevice(&dev));
-  if (pooled_device != dev) {
-    cudaMemPool_t pool;
-    TNS_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
-    uint64_t keep = ~0ull;
-    TNS_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
-    pooled_device = dev;
+  cudaMemPool_t pool;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = pools.find(dev);
+    if (it == pools.end()) {
+      cudaMemPoolProps props{};
+      props.allocType = cudaMemAllocationTypePinned;
+      props.handleTypes = cudaMemHandleTypeNone;
+      props.location.type = cudaMemLocationTypeDevice;
+      props.location.id = dev;
+      TNS_CUDA(cudaMemPoolCreate(&pool, &props));
+      uint64_t keep = kTnsPoolKeep;
+      TNS_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+      it = pools.emplace(dev, pool).first;
+    }
+    pool = it->second;
   }
   void* p = nullptr;
-  TNS_CUDA(cudaMallocAsync(&p, bytes, static_cast<cudaStream_t>(stream)));
+  TNS_CUDA(cudaMallocFromPoolAsync(&p, bytes, pool, static_cast<cudaStream_t>(stream)));
   return p;
 }
 void tns_dev_free(void* p, void* stream) {

@@ -205,3 +205,96 @@ def generate_torch(cfg: Config, nnz: Optional[int] = None, seed: Optional[int] =
     perm, _ = lex_order(sel)
     sel, values = sel[perm], values[perm]
     return sel.to(torch.int32).reshape(-1).contiguous(), values.contiguous()
+
+
+def generate_device(cfg: Config, nnz: Optional[int] = None, seed: Optional[int] = None,
+                    device: str = "cuda", parts: int = 3, ws=None):
+    """Fast seeded generator for the billion-row configs (config 5: 1.74B
+    unique Zipf(1.05) rows in ~3 s on one B200), device-resident throughout.
+
+    * ~1.5 N coordinate rows are drawn per mode from torch's Philox generator
+      (Zipf by inverse CDF, as generate_torch);
+    * the draws are canonicalised (simple order) and deduplicated in `parts`
+      ranges of mode 0 (cut at sampled quantiles, so each range's sort fits
+      beside the draws), each with the library's stable device sort
+      (``sort_rows_by_device``, the engine's segmented sort — the same one the
+      .tns reader canonicalises with); the ranges concatenate in order;
+    * exactly N of the unique rows are kept by a seeded uniform subset (a
+      subsequence of a sorted list stays sorted) and values U[0,1) are drawn
+      per kept row.
+
+    The unique set differs from generate()'s first-N-distinct-in-draw-order
+    rule (a uniform N-subset of the distinct draws instead); both are seeded
+    and deterministic, and every consumer (bench arms, tests) uses the same
+    bytes.  Only "zipf"/"uniform" modes and uniform values are supported.
+    Returns (coords int32 [N*r], values float64 [N]) on `device`."""
+    import torch
+
+    import paper_2005_10427_b200 as qd
+
+    if any(k not in ("zipf", "uniform") for k in cfg.dist) or cfg.values != "uniform":
+        raise ValueError("generate_device supports zipf/uniform modes with U[0,1) values")
+    n = cfg.nnz if nnz is None else int(nnz)
+    seed = cfg.seed if seed is None else seed
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    r = len(cfg.dims)
+    m = int(n * 1.5) + 1024
+    raw = torch.empty((m, r), dtype=torch.int32, device=device)
+    step = 1 << 28
+    for j, (d, kind) in enumerate(zip(cfg.dims, cfg.dist)):
+        cdf = torch.from_numpy(_zipf_cdf(d, cfg.s)).to(device) if kind == "zipf" else None
+        for a in range(0, m, step):
+            b = min(m, a + step)
+            if kind == "zipf":
+                u = torch.rand(b - a, generator=g, device=device, dtype=torch.float64)
+                raw[a:b, j] = torch.searchsorted(cdf, u, right=True).clamp_(max=d - 1).to(torch.int32)
+                del u
+            else:
+                raw[a:b, j] = torch.randint(0, d, (b - a,), generator=g, device=device,
+                                            dtype=torch.int32)
+        del cdf
+    smp = raw[: 1 << 24, 0].double().sort().values
+    cuts = [0] + [int(smp[k * len(smp) // parts].item()) + 1 for k in range(1, parts)] + [2**31 - 1]
+    del smp
+    own_ws = ws is None
+    ws = ws or qd.Workspace(torch.device(device).index or 0)
+    sp = torch.cuda.current_stream().cuda_stream
+    uniq = []
+    for lo, hi in zip(cuts[:-1], cuts[1:]):
+        if hi <= lo:
+            continue
+        sel = (raw[:, 0] >= lo) & (raw[:, 0] < hi)
+        part = raw[sel].reshape(-1).contiguous()
+        del sel
+        k = part.numel() // r
+        if k == 0:
+            continue
+        dummy = torch.zeros(k, dtype=torch.float64, device=device)
+        po = torch.empty_like(part)
+        pv = torch.empty_like(dummy)
+        qd.sort_rows_by_device(r, cfg.dims, k, part.data_ptr(), dummy.data_ptr(), po.data_ptr(),
+                               pv.data_ptr(), 0, k, list(range(r)), ws, sp)
+        torch.cuda.synchronize()
+        del part, dummy, pv
+        s = po.view(k, r)
+        head = torch.ones(k, dtype=torch.bool, device=device)
+        head[1:] = (s[1:] != s[:-1]).any(1)
+        uniq.append(s[head])
+        del s, po, head
+        torch.cuda.empty_cache()
+    del raw
+    if own_ws:
+        ws.close()
+    torch.cuda.empty_cache()
+    u = sum(x.shape[0] for x in uniq)
+    if u < n:
+        raise RuntimeError(f"generate_device: only {u} unique rows drawn for {n}")
+    # a seeded uniform N-subset in order (torch.randperm stalls at this size)
+    keep = torch.rand(u, generator=g, device=device, dtype=torch.float64).argsort()[:n].sort().values
+    ci = torch.cat(uniq)[keep].reshape(-1).contiguous()
+    del uniq, keep
+    vi = torch.rand(n, generator=g, device=device, dtype=torch.float64)
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    return ci, vi

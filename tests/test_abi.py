@@ -109,3 +109,50 @@ def test_no_cpu_fallback_without_device():
         pytest.skip("a GPU is visible")
     with pytest.raises(qd.DeviceError):
         qd.Workspace(0)
+
+
+HOST_PARITY = os.path.join(ROOT, "oracle", "_ref", "host_parity")
+
+
+@pytest.mark.skipif(not os.path.exists(HOST_PARITY), reason="oracle/_ref/host_parity not built")
+def test_cpp_host_utilities_match_reference():
+    """The C++ drop-in's parse_ordering / format_ordering / parse_strategy and
+    Ordering checks against the reference library's own, including the
+    std::from_chars edge cases (overflow, sign, spaces, empty tokens) and the
+    exact exception messages (tests/cpp/host_parity.cpp)."""
+    import subprocess
+    r = subprocess.run([HOST_PARITY], capture_output=True, text=True, timeout=60)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert r.stdout.startswith("PASS")
+
+
+@pytest.mark.parametrize("text,outcome", [
+    ("4294967297,2", "bad ordering element '4294967297'"),
+    ("99999999999999999999,1", "bad ordering element '99999999999999999999'"),
+    ("4294967295,1", "ordering contains mode 4294967294 outside 0..1"),
+    ("+1,2", "bad ordering element '+1'"),
+    (" 1,2", "bad ordering element ' 1'"),
+    ("1,", "bad ordering element ''"),
+    ("0,1", "bad ordering element '0'"),
+    ("²,1", "bad ordering element '²'"),
+    ("1,1", "ordering repeats mode 0"),
+    ("3,1", "ordering contains mode 2 outside 0..1"),
+    ("01,2", [0, 1]),
+    ("2,1,3", [1, 0, 2]),
+])
+def test_python_parse_ordering_matches_reference(text, outcome):
+    """Python mirror of parse_ordering (ordering.cpp:68-99): from_chars
+    semantics and the reference's messages (same cases as host_parity.cpp)."""
+    if isinstance(outcome, list):
+        assert qd.parse_ordering(text).modes() == outcome
+    else:
+        with pytest.raises(qd.InvalidArgument) as e:
+            qd.parse_ordering(text)
+        assert str(e.value) == outcome
+
+
+def test_python_parse_strategy_overflow():
+    assert qd.parse_strategy("top4294967295").k == 4294967295
+    for bad in ("top4294967296", "top+2", "top 2", "top0", "top²"):
+        with pytest.raises(qd.InvalidArgument):
+            qd.parse_strategy(bad)

@@ -93,3 +93,64 @@ def test_config5_properties_and_sharded_oracle(ws):
         del co, vo
     del ci, vi
     torch.cuda.empty_cache()
+
+
+def test_config5_full_size():
+    """BASELINE config 5 at FULL size on one B200 (1,741,809,018 unique
+    Zipf(1.05) rows, the bench workload): for both targets the whole output
+    is sorted under the target (device check) and holds the input's row
+    multiset (device checksum); bit-exact slices against the reference
+    library through the sharded oracle: the sigma1 = 0 slice
+    (the Zipf head) and one seeded interior sigma1 range."""
+    import torch
+    sys_path_bench()
+    import bench
+    cfg = synth.CONFIGS["c5"]
+    torch.cuda.empty_cache()
+    free, _ = torch.cuda.mem_get_info()
+    if free < 150 * 2**30:
+        pytest.skip(f"needs ~150 GiB of free device memory ({free / 2**30:.0f} GiB free)")
+    w = qd.Workspace(0)
+    ci, vi = synth.generate_device(cfg, ws=w)
+    n, r = vi.numel(), 3
+    assert n == cfg.nnz
+    h_in = bench.row_checksum_device(ci, vi, r)
+    ref = Reference()
+    rng = np.random.default_rng(2026)
+    cin = ci.view(n, r)
+    try:
+        for target in cfg.targets:
+            co, vo = device_transpose(w, cfg.dims, ci, vi, target)
+            assert qd.is_sorted_device(r, n, co.data_ptr(), target, w)
+            assert bench.row_checksum_device(co, vo, r) == h_in, target
+            s1 = target[0]
+            ocol = co.view(n, r)[:, s1].contiguous()
+            lo = int(rng.integers(1000, cfg.dims[s1] // 4))
+            for a, b in [(0, 1), (lo, lo + 2000)]:
+                sel = (cin[:, s1] >= a) & (cin[:, s1] < b)
+                hc = cin[sel].cpu().numpy().view(np.uint32).ravel()
+                hv = vi[sel].cpu().numpy()
+                del sel
+                rc, rv, _ = ref.transpose(cfg.dims, hc, hv, target, workers=WORKERS)
+                # the output slice is contiguous: the output is sorted by sigma1
+                bnd = torch.tensor([a, b], dtype=torch.int32, device=ocol.device)
+                s, e = [int(x) for x in torch.searchsorted(ocol, bnd).cpu()]
+                assert e - s == len(hv) > 0, (target, a, b)
+                oc = co.view(n, r)[s:e].cpu().numpy().view(np.uint32).ravel()
+                ov = vo[s:e].cpu().numpy()
+                assert np.array_equal(oc, rc), (target, a, b)
+                assert np.array_equal(ov.view(np.uint64), rv.view(np.uint64)), (target, a, b)
+                del hc, hv, rc, rv, oc, ov
+            del co, vo, ocol
+            torch.cuda.empty_cache()
+    finally:
+        del ci, vi, cin
+        w.close()
+        torch.cuda.empty_cache()
+
+
+def sys_path_bench():
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    if root not in sys.path:
+        sys.path.insert(0, root)

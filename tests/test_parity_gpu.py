@@ -525,6 +525,30 @@ def test_async_chained_on_same_buffers(ws):
     assert same(t, c2, v2)
 
 
+@pytest.mark.parametrize("ntensors", [2, 3])
+def test_async_interleaved_buffers(ws, ntensors):
+    """Tensors transposed alternately in place, A, B, A, B, ... (or A, B, C,
+    A, ...: with two device slots A's previous call is then not even the
+    latest call of any slot): every call on A must read the bytes the previous
+    call on A wrote back (only the immediately previous call was
+    checked).  Full radix re-sorts are valid on any input order."""
+    rng = np.random.default_rng(14 + ntensors)
+    shapes = [[50, 3000, 40], [70, 60, 2000], [900, 30, 30]][:ntensors]
+    base = [rand_tensor(rng, d, 400_000 + 50_000 * i) for i, d in enumerate(shapes)]
+    work = [t.copy() for t in base]
+    seq = [[2, 1, 0], [1, 0, 2], [0, 2, 1], [2, 0, 1], [1, 2, 0], [0, 1, 2]]
+    for tgt in seq:
+        for i, t in enumerate(work):
+            qd.transpose_inplace_async(t, tgt if i % 2 == 0 else tgt[::-1],
+                                       qd.SortStrategy.full_radix(), ws)
+    ws.synchronize()
+    for i, (b, t) in enumerate(zip(base, work)):
+        c, v = b.coords, b.values
+        for tgt in seq:
+            c, v, _ = ORC.transpose(b.dims, c, v, tgt if i % 2 == 0 else tgt[::-1], "radix")
+        assert same(t, c, v), i
+
+
 def test_async_errors_leave_tensor_untouched(ws):
     rng = np.random.default_rng(13)
     big = rand_tensor(rng, [5, 300, 300], 50_000)
