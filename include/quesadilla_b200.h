@@ -257,6 +257,49 @@ qd_status qd_partition_rows_to_peers_device(uint32_t rank, uint64_t nnz,
                                             uint64_t* part_counts, qd_workspace* ws,
                                             void* stream);
 
+/* ---- sharded transpose over NCCL ------------
+ * One communicator rank per device: every rank holds a contiguous slice of
+ * the global (simply sorted) input rows, slices in rank order; after the
+ * call rank g holds the slice of the global output whose leading target mode
+ * falls in g's range, so the rank outputs concatenated in rank order equal
+ * transpose(global, target) bit for bit.  Lifts parallel.cpp:113-154's
+ * bucket-aligned regions to GPUs: target[0] == 0 with mode-0-aligned slices
+ * needs no communication; otherwise one exchange (ncclAllReduce of the
+ * leading mode's histogram, splitters on the device, one grouped
+ * ncclSend/ncclRecv per peer, received in source-rank order).  Collective:
+ * every rank calls it with the same target and strategy. */
+typedef struct qd_comm qd_comm;
+typedef struct qd_hub qd_hub;
+typedef struct qd_shard_stats {
+  int exchanged;            /* 1 when the rows were exchanged */
+  uint64_t rows_out;        /* rows of this rank's output slice */
+  uint64_t bytes_sent;      /* to other ranks */
+  uint64_t bytes_received;  /* from other ranks */
+  float exchange_ms;        /* device time of the grouped send/recv (CUDA events) */
+} qd_shard_stats;
+/* ncclGetUniqueId: 128 bytes for rank 0 to broadcast to every rank */
+qd_status qd_comm_unique_id(uint8_t out[128]);
+/* ncclCommInitRank on `device` (NCCL loaded at run time: libnccl.so.2) */
+qd_status qd_comm_create(const uint8_t id[128], int nranks, int rank, int device,
+                         qd_comm** out);
+/* Test transport: `nranks` ranks emulated as threads of one process on one
+ * device (device copies + host barriers; no NCCL).  The hub must outlive
+ * its comms; each rank uses its own workspace. */
+qd_status qd_hub_create(int nranks, qd_hub** out);
+qd_status qd_hub_destroy(qd_hub* hub);
+qd_status qd_comm_create_emulated(qd_hub* hub, int rank, qd_workspace* ws, qd_comm** out);
+qd_status qd_comm_destroy(qd_comm* comm);
+/* this rank's input slice (device) -> its output slice (device, capacity
+ * out_capacity rows; *nnz_out = the slice's rows, also when it does not fit:
+ * then every rank fails with QD_INVALID_ARGUMENT).  stats may be null. */
+qd_status qd_sharded_transpose_device(qd_comm* comm, uint32_t rank, const uint32_t* dims,
+                                      uint64_t nnz, const uint32_t* d_coords_in,
+                                      const double* d_values_in, uint32_t* d_coords_out,
+                                      double* d_values_out, uint64_t out_capacity,
+                                      uint64_t* nnz_out, const uint32_t* target,
+                                      qd_strategy_kind kind, uint32_t k, qd_workspace* ws,
+                                      void* stream, qd_shard_stats* stats);
+
 /* ---- .tns text format (io.hpp:24-47, io.cpp:42-126) --------------------- */
 /* A tensor owned by the library (host memory; release with qd_tns_free). */
 typedef struct qd_tns_tensor {

@@ -182,8 +182,24 @@ def lib():
         L.qd_write_tns.argtypes = [C.c_uint32, C.c_uint64, _u32p, _f64p,
                                    C.POINTER(C.c_void_p), C.POINTER(C.c_uint64), C.c_void_p]
         L.qd_text_free.argtypes = [C.c_void_p]
+        L.qd_comm_unique_id.argtypes = [C.c_void_p]
+        L.qd_comm_create.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]
+        L.qd_hub_create.argtypes = [C.c_int, C.POINTER(C.c_void_p)]
+        L.qd_hub_destroy.argtypes = [C.c_void_p]
+        L.qd_comm_create_emulated.argtypes = [C.c_void_p, C.c_int, C.c_void_p,
+                                              C.POINTER(C.c_void_p)]
+        L.qd_comm_destroy.argtypes = [C.c_void_p]
+        L.qd_sharded_transpose_device.argtypes = [
+            C.c_void_p, C.c_uint32, _u32p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p,
+            C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64), _u32p, C.c_int, C.c_uint32,
+            C.c_void_p, C.c_void_p, C.POINTER(ShardStatsC)]
         _lib = L
     return _lib
+
+
+class ShardStatsC(C.Structure):
+    _fields_ = [("exchanged", C.c_int), ("rows_out", C.c_uint64), ("bytes_sent", C.c_uint64),
+                ("bytes_received", C.c_uint64), ("exchange_ms", C.c_float)]
 
 
 def _check(status: int):
@@ -948,3 +964,70 @@ def write_tns(tensor: CooTensor, path, ws: Optional[Workspace] = None) -> None:
 
 
 __all__ = [n for n in dir() if not n.startswith("_")]
+
+
+# --- sharded transpose over NCCL (qd_sharded_transpose_device) ----
+
+def comm_unique_id() -> bytes:
+    """ncclGetUniqueId (128 bytes) for rank 0 to broadcast to every rank."""
+    buf = (C.c_uint8 * 128)()
+    _check(lib().qd_comm_unique_id(buf))
+    return bytes(buf)
+
+
+class Hub:
+    """Emulated ranks (tests): threads of one process on one device."""
+
+    def __init__(self, nranks: int):
+        h = C.c_void_p()
+        _check(lib().qd_hub_create(nranks, C.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().qd_hub_destroy(self._h)
+            self._h = None
+
+
+class Comm:
+    """One rank of a sharded-transpose communicator: NCCL (ncclCommInitRank on
+    `device`, from the 128-byte unique id of rank 0) or, with `hub`, the
+    emulated transport (ws = this rank's workspace)."""
+
+    def __init__(self, nranks: int = 1, rank: int = 0, device: int = 0, unique_id: bytes = None,
+                 hub: "Hub" = None, ws: "Workspace" = None):
+        h = C.c_void_p()
+        if hub is not None:
+            _check(lib().qd_comm_create_emulated(hub._h, rank, ws.handle, C.byref(h)))
+        else:
+            uid = (C.c_uint8 * 128).from_buffer_copy(unique_id or comm_unique_id())
+            _check(lib().qd_comm_create(uid, nranks, rank, device, C.byref(h)))
+        self._h = h
+        self.nranks, self.rank = nranks if hub is None else None, rank
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().qd_comm_destroy(self._h)
+            self._h = None
+
+
+def sharded_transpose_device(comm: Comm, rank: int, dims, nnz: int, coords_in: int,
+                             values_in: int, coords_out: int, values_out: int, out_capacity: int,
+                             target, strategy: SortStrategy = SortStrategy(),
+                             ws: Optional[Workspace] = None, stream: int = 0):
+    """This rank's slice of the global input -> its slice of the global output
+    (device pointers as ints; collective over `comm`).  Returns (rows_out,
+    stats dict)."""
+    w = _ws(ws)
+    d = _arr_u32(dims)
+    t = _arr_u32(_ord(target).modes())
+    n_out = C.c_uint64(0)
+    st = ShardStatsC()
+    _check(lib().qd_sharded_transpose_device(
+        comm._h, rank, _ptr_u32(d), nnz, C.c_void_p(coords_in), C.c_void_p(values_in),
+        C.c_void_p(coords_out), C.c_void_p(values_out), out_capacity, C.byref(n_out),
+        _ptr_u32(t), KINDS[strategy.kind], strategy.k, w.handle, C.c_void_p(stream),
+        C.byref(st)))
+    return n_out.value, {"exchanged": bool(st.exchanged), "rows_out": st.rows_out,
+                         "bytes_sent": st.bytes_sent, "bytes_received": st.bytes_received,
+                         "exchange_ms": st.exchange_ms}

@@ -575,3 +575,73 @@ qd_status qd_partition_rows_to_peers_device(uint32_t rank, uint64_t nnz,
 }
 
 }  // extern "C"
+
+// ---- sharded transpose (shard.cu) ----------------------------------------------
+struct qd_comm {
+  Comm* c;
+};
+struct qd_hub {
+  Hub* h;
+};
+
+qd_status qd_comm_unique_id(uint8_t out[128]) {
+  return guard([&] {
+    if (!out) invalid("output buffer is null");
+    comm_unique_id(out);
+  });
+}
+
+qd_status qd_comm_create(const uint8_t id[128], int nranks, int rank, int device, qd_comm** out) {
+  return guard([&] {
+    if (!id || !out) invalid("null argument");
+    *out = new qd_comm{comm_create_nccl(id, nranks, rank, device)};
+  });
+}
+
+qd_status qd_hub_create(int nranks, qd_hub** out) {
+  return guard([&] {
+    if (!out) invalid("null argument");
+    *out = new qd_hub{hub_create(nranks)};
+  });
+}
+
+qd_status qd_hub_destroy(qd_hub* hub) {
+  return guard([&] {
+    if (hub) hub_destroy(hub->h);
+    delete hub;
+  });
+}
+
+qd_status qd_comm_create_emulated(qd_hub* hub, int rank, qd_workspace* ws, qd_comm** out) {
+  return guard([&] {
+    if (!hub || !ws || !out) invalid("null argument");
+    *out = new qd_comm{comm_create_emulated(hub->h, rank, workspace_device(W(ws)), &W(ws))};
+  });
+}
+
+qd_status qd_comm_destroy(qd_comm* comm) {
+  return guard([&] {
+    if (comm) comm_destroy(comm->c);
+    delete comm;
+  });
+}
+
+qd_status qd_sharded_transpose_device(qd_comm* comm, uint32_t rank, const uint32_t* dims,
+                                      uint64_t nnz, const uint32_t* d_coords_in,
+                                      const double* d_values_in, uint32_t* d_coords_out,
+                                      double* d_values_out, uint64_t out_capacity,
+                                      uint64_t* nnz_out, const uint32_t* target,
+                                      qd_strategy_kind kind, uint32_t k, qd_workspace* ws,
+                                      void* stream, qd_shard_stats* stats) {
+  return guard([&] {
+    if (!comm || !ws || !nnz_out) invalid("null argument");
+    check_tensor(rank, dims, nnz, d_coords_in, d_values_in);
+    if (out_capacity && (!d_coords_out || !d_values_out)) invalid("output buffer is null");
+    check_ordering(target, rank);
+    std::vector<Step> steps;
+    auto groups = strategy_groups(target, rank, kind, k, &steps);
+    TensorView t{rank, dims, nnz};
+    sharded_transpose_device(*comm->c, W(ws), t, d_coords_in, d_values_in, d_coords_out,
+                             d_values_out, out_capacity, nnz_out, groups, target, stream, stats);
+  });
+}

@@ -1651,6 +1651,278 @@ __global__ void __launch_bounds__(kLocalThreads) k_local(LocalArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// k_local2: the small runs of a bucketed group (Alg. 2 buckets of <= TL
+// rows), streamed.  Persistent CTAs take items (one item = the small runs
+// starting in one TL-row chunk, a contiguous span of < 2*TL rows) from a
+// per-launch counter; the advancer warp loads the NEXT item's span into the
+// other shared-memory buffer with TMA bulk copies (cp.async.bulk + mbarrier)
+// while the CTA sorts the current one.  Inside an item every warp takes whole
+// runs (a shared counter; no block barrier between runs) and sorts each one
+// by the group's key: runs of <= 32 rows by an all-pairs rank of the full key
+// in registers, longer runs by a warp-private LSD radix sort (<= 8-bit
+// digits, MATCH.ANY ranking) over an index array; then the warp writes the
+// run's rows to the output in sorted order (coalesced by output row).  Reads
+// of a span complete (into shared memory) before any row of it is written, so
+// in == out is safe.  sort.cpp:80-134 (Alg. 2) on small buckets.
+// ---------------------------------------------------------------------------
+constexpr int kLocal2Threads = 512;
+constexpr int kLocal2Warps = kLocal2Threads / 32;
+constexpr int kMaxLocalPasses = 8;
+
+struct LocalItem {
+  unsigned long long r0;  // first row of the span
+  uint32_t n;             // rows in the span
+  uint32_t run_first;     // index of its first run in seg_start
+  uint32_t nruns;         // runs in the span (all small)
+  uint32_t pad;
+};
+
+struct Local2Args {
+  const uint32_t* in_c;
+  const double* in_v;
+  uint32_t* out_c;
+  double* out_v;
+  uint32_t rank;
+  uint32_t cap;  // rows per staging buffer (>= the longest span)
+  const unsigned long long* seg_start;
+  const LocalItem* items;
+  uint32_t n_items;
+  uint32_t* item_counter;
+  KeySpec key;
+  uint32_t npasses;
+  DigitSpec dig[kMaxLocalPasses];
+  uint32_t dig_bits[kMaxLocalPasses];
+  ErrBlock* err;
+};
+
+struct Local2Layout {
+  size_t cbuf, vbuf, c0, v0, idx0, idx1, rnk, whist, total;
+  __host__ __device__ Local2Layout(uint32_t cap, uint32_t rank) {
+    size_t o = 0;
+    cbuf = align16(size_t(cap) * rank * 4 + 32);
+    vbuf = align16(size_t(cap) * 8 + 32);
+    c0 = o; o += 2 * cbuf;
+    v0 = o; o += 2 * vbuf;
+    idx0 = o; o += align16(size_t(cap) * 2);
+    idx1 = o; o += align16(size_t(cap) * 2);
+    rnk = o; o += align16(size_t(cap) * 2);
+    whist = o; o += align16(size_t(kLocal2Warps) * kBins * 2);
+    total = o;
+  }
+};
+
+// items: for each listed chunk c, its small runs [first_run[c], first run
+// that starts at/after (c+1)*TL or is large) and their row span
+__global__ void k_local_items(const uint32_t* list, const uint32_t* first_run,
+                              const unsigned long long* seg_start, const unsigned long long* S_ptr,
+                              uint64_t nnz, uint32_t TL, uint32_t n_items, LocalItem* items) {
+  const unsigned long long S = *S_ptr;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_items; i += gridDim.x * blockDim.x) {
+    const uint32_t c = list[i];
+    const unsigned long long hi = min((unsigned long long)nnz, ((unsigned long long)c + 1) * TL);
+    const uint32_t f = first_run[c];
+    uint32_t k = f;
+    while (k < S && seg_start[k] < hi && seg_start[k + 1] - seg_start[k] <= TL) ++k;
+    LocalItem it;
+    it.r0 = seg_start[f];
+    it.n = (uint32_t)(seg_start[k] - seg_start[f]);
+    it.run_first = f;
+    it.nruns = k - f;
+    it.pad = 0;
+    items[i] = it;
+  }
+}
+
+__global__ void __launch_bounds__(kLocal2Threads, 2) k_local2(Local2Args a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const uint32_t R = a.rank;
+  const Local2Layout L(a.cap, R);
+  uint16_t* s_idx0 = reinterpret_cast<uint16_t*>(smem + L.idx0);
+  uint16_t* s_idx1 = reinterpret_cast<uint16_t*>(smem + L.idx1);
+  uint16_t* s_rank = reinterpret_cast<uint16_t*>(smem + L.rnk);
+  uint16_t* s_whist = reinterpret_cast<uint16_t*>(smem + L.whist);
+  __shared__ unsigned long long s_bar[2];
+  __shared__ uint32_t s_item[2];       // item index staged in buffer b
+  __shared__ uint32_t s_ofs[2][2];     // staging heads (bytes) of coords / values
+  __shared__ uint32_t s_next_run;      // next run of the current item (warps take runs)
+  // key and digit specs in shared memory (dynamically indexed below; kernel
+  // parameters indexed at run time would go through local memory)
+  __shared__ KeySpec s_key;
+  __shared__ DigitSpec s_dig[kMaxLocalPasses];
+  __shared__ uint32_t s_dbits[kMaxLocalPasses];
+  constexpr uint32_t kAdv = kLocal2Threads - 32;
+  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+
+  // advancer warp: draw the next item and start its bulk copies into buffer b
+  auto advance = [&](uint32_t b) {
+    uint32_t it = 0;
+    if (lane == 0) it = atomicAdd(a.item_counter, 1u);
+    it = __shfl_sync(0xFFFFFFFFu, it, 0);
+    if (lane == 0) s_item[b] = it;
+    if (it >= a.n_items) return;
+    const LocalItem item = a.items[it];
+    const Stage sc = make_stage(a.in_c + item.r0 * R, item.n * R * 4);
+    const Stage sv = make_stage(a.in_v + item.r0, item.n * 8);
+    if (lane == 0) {
+      s_ofs[b][0] = sc.head;
+      s_ofs[b][1] = sv.head;
+      mbar_expect_tx(&s_bar[b], sc.bulk + sv.bulk);
+    }
+    __syncwarp();
+    if (lane == 0 && sc.bulk) bulk_g2s(smem + L.c0 + b * L.cbuf, sc.gal, sc.bulk, &s_bar[b]);
+    if (lane == 1 && sv.bulk) bulk_g2s(smem + L.v0 + b * L.vbuf, sv.gal, sv.bulk, &s_bar[b]);
+  };
+
+  if (threadIdx.x == kAdv) {
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (threadIdx.x == 0) {
+    s_key = a.key;
+    for (uint32_t q = 0; q < a.npasses; ++q) {
+      s_dig[q] = a.dig[q];
+      s_dbits[q] = a.dig_bits[q];
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x >= kAdv) advance(0);
+  __syncthreads();
+  const KeySpec& key = s_key;
+  const uint32_t nk = key.n;
+  uint32_t phases = 0;
+  for (uint32_t iter = 0;; ++iter) {
+    const uint32_t b = iter & 1u;
+    const uint32_t it = s_item[b];
+    if (it >= a.n_items) break;
+    if (threadIdx.x == 0) s_next_run = 0;
+    // the other buffer was released by the previous item's closing barrier
+    if (threadIdx.x >= kAdv) advance(b ^ 1u);
+    mbar_wait(&s_bar[b], (phases >> b) & 1u);
+    phases ^= 1u << b;
+    __syncthreads();  // s_next_run reset visible; s_item[b^1] written
+    const LocalItem item = a.items[it];
+    const uint32_t* s_c =
+        reinterpret_cast<const uint32_t*>(smem + L.c0 + b * L.cbuf + s_ofs[b][0]);
+    const double* s_v = reinterpret_cast<const double*>(smem + L.v0 + b * L.vbuf + s_ofs[b][1]);
+    auto coord = [&](uint32_t i, uint32_t m) { return s_c[i * R + m]; };
+    auto full_key_at = [&](uint32_t i) -> unsigned long long {
+      unsigned long long k = 0;
+      for (uint32_t f = 0; f < nk; ++f) {
+        const uint32_t wd = key.width[f];
+        if (wd) k |= (unsigned long long)(coord(i, key.mode[f]) & (uint32_t)((1ull << wd) - 1ull))
+                     << key.off[f];
+      }
+      return k;
+    };
+    auto check_at = [&](uint32_t i) {
+      if (!key.check) return;
+      bool bad = false;
+      for (uint32_t f = 0; f < nk; ++f) bad |= coord(i, key.mode[f]) >= key.dim[f];
+      if (bad) check_row(s_c + (size_t)i * R, key, item.r0 + i, a.err);
+    };
+    auto store = [&](uint32_t j, uint32_t i) {  // output row j of the span <- staged row i
+      const unsigned long long dst = item.r0 + j;
+      uint32_t* o = a.out_c + dst * R;
+      for (uint32_t m = 0; m < R; ++m) __stcs(o + m, s_c[i * R + m]);
+      __stcs(a.out_v + dst, s_v[i]);
+    };
+    for (;;) {
+      uint32_t run = 0;
+      if (lane == 0) run = atomicAdd(&s_next_run, 1u);
+      run = __shfl_sync(0xFFFFFFFFu, run, 0);
+      if (run >= item.nruns) break;
+      const uint32_t rb = (uint32_t)(a.seg_start[item.run_first + run] - item.r0);
+      const uint32_t re = (uint32_t)(a.seg_start[item.run_first + run + 1] - item.r0);
+      const uint32_t n = re - rb;
+      if (n <= 32) {
+        // all-pairs stable rank of the full key: position = #smaller keys
+        // + #equal keys earlier in the run
+        const bool valid = lane < n;
+        const uint32_t i = rb + (valid ? lane : 0u);
+        if (valid) check_at(i);
+        const unsigned long long k = valid ? full_key_at(i) : ~0ull;
+        uint32_t pos = 0;
+        for (uint32_t j = 0; j < n; ++j) {
+          const unsigned long long kj = __shfl_sync(0xFFFFFFFFu, k, j);
+          pos += (kj < k) || (kj == k && j < lane);
+        }
+        if (valid) store(rb + pos, i);
+        continue;
+      }
+      // warp-private LSD radix sort of positions [rb, re) by the key digits
+      uint16_t* wh = s_whist + w * kBins;
+      uint16_t* cur = s_idx0;
+      uint16_t* nxt = s_idx1;
+      for (uint32_t p = rb + lane; p < re; p += 32) {
+        check_at(p);
+        cur[p] = (uint16_t)p;
+      }
+      const unsigned below = (1u << lane) - 1u;
+      for (uint32_t q = 0; q < a.npasses; ++q) {
+        const uint32_t nb = 1u << s_dbits[q];
+        for (uint32_t k = lane; k < nb; k += 32) wh[k] = 0;
+        __syncwarp();
+        const DigitSpec& dg = s_dig[q];
+        for (uint32_t base = rb; base < re; base += 32) {  // ranking rounds
+          const uint32_t p = base + lane;
+          const bool valid = p < re;
+          const uint32_t d = valid ? digit_by([&](uint32_t m) { return coord(cur[p], m); }, dg) : nb;
+          const unsigned peers = __match_any_sync(0xFFFFFFFFu, d);
+          uint32_t c = 0;
+          if (valid) c = wh[d];
+          __syncwarp();
+          if (valid && (peers & below) == 0u) wh[d] = (uint16_t)(c + __popc(peers));
+          if (valid) s_rank[p] = (uint16_t)(c + __popc(peers & below));
+          __syncwarp();
+        }
+        // exclusive scan of the warp's bin counts (lane owns nb/32 bins)
+        {
+          const uint32_t per = (nb + 31) / 32;
+          uint32_t loc[8];
+          uint32_t sum = 0;
+#pragma unroll
+          for (uint32_t t = 0; t < 8; ++t) {
+            const uint32_t k = lane * per + t;
+            loc[t] = (t < per && k < nb) ? wh[k] : 0u;
+            sum += loc[t];
+          }
+          uint32_t incl = sum;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= (uint32_t)o) incl += y;
+          }
+          uint32_t run_sum = incl - sum;
+          __syncwarp();
+#pragma unroll
+          for (uint32_t t = 0; t < 8; ++t) {
+            const uint32_t k = lane * per + t;
+            if (t < per && k < nb) {
+              wh[k] = (uint16_t)run_sum;
+              run_sum += loc[t];
+            }
+          }
+          __syncwarp();
+        }
+        for (uint32_t p = rb + lane; p < re; p += 32) {  // scatter of the indices
+          const uint32_t i = cur[p];
+          const uint32_t d = digit_by([&](uint32_t m) { return coord(i, m); }, dg);
+          nxt[rb + wh[d] + s_rank[p]] = (uint16_t)i;
+        }
+        __syncwarp();
+        uint16_t* t = cur;
+        cur = nxt;
+        nxt = t;
+      }
+      for (uint32_t j = rb + lane; j < re; j += 32) store(j, cur[j]);
+      __syncwarp();
+    }
+    __syncthreads();  // buffer b and the index arrays are free again
+  }
+}
+
+// ---------------------------------------------------------------------------
 // segment discovery
 // ---------------------------------------------------------------------------
 constexpr uint32_t kHeadRows = 4096;  // rows per k_heads CTA (128 words)
@@ -2004,12 +2276,17 @@ __global__ void k_mode_max(const uint32_t* c, uint32_t rank, uint64_t nnz, ModeL
   for (uint32_t j = threadIdx.x; j < modes.n; j += blockDim.x) atomicMax(&mx[j], s_mx[j]);
 }
 
+// Warp-aggregated: lanes holding the same value add once (MATCH.ANY), so a
+// Zipf head value (~9 % of config 5's rows) does not serialise on one address.
 __global__ void k_mode_hist(const uint32_t* c, uint32_t rank, uint64_t nnz, uint32_t mode,
                             uint32_t dim, unsigned long long* hist) {
-  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < nnz;
-       i += (unsigned long long)gridDim.x * blockDim.x) {
-    const uint32_t k = c[i * rank + mode];
-    if (k < dim) atomicAdd(hist + k, 1ull);
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  for (unsigned long long i0 = (unsigned long long)blockIdx.x * blockDim.x; i0 < nnz; i0 += stride) {
+    const unsigned long long i = i0 + threadIdx.x;  // warp-uniform loop bound
+    const uint32_t k = i < nnz ? c[i * rank + mode] : 0xFFFFFFFFu;
+    const unsigned peers = __match_any_sync(0xFFFFFFFFu, k);
+    if (k < dim && (peers & ((1u << (threadIdx.x & 31)) - 1u)) == 0u)
+      atomicAdd(hist + k, (unsigned long long)__popc(peers));
   }
 }
 
@@ -2392,6 +2669,7 @@ Workspace* workspace_create(int device) {
             if (ScatterFn f = scatter_kernel(rt, dm, in, out, mx))
               allow_smem(reinterpret_cast<const void*>(f));
   allow_smem(reinterpret_cast<const void*>(k_local));
+  allow_smem(reinterpret_cast<const void*>(k_local2));
   ws->smem_optin = optin - 1024;  // dynamic budget below the static usage
   return ws;
 }
@@ -2434,6 +2712,12 @@ uint64_t workspace_bytes(const Workspace* ws) {
   return b;
 }
 uint64_t workspace_launches(const Workspace* ws) { return ws->launches; }
+void* workspace_buffer(Workspace& ws, const char* name, size_t bytes) {
+  return ws.get<unsigned char>(name, bytes);
+}
+int workspace_device(const Workspace& ws) { return ws.device; }
+int workspace_sms(const Workspace& ws) { return ws.num_sms; }
+void workspace_count_launch(Workspace& ws) { ++ws.launches; }
 
 void workspace_profile(Workspace* ws, int enable) {
   ws->prof = enable != 0;
@@ -2541,6 +2825,16 @@ uint32_t local_span(const Workspace& ws, uint32_t rank) {
   if (const char* e = getenv("QD_LOCAL_KB")) budget = (size_t)atoi(e) * 1024;
   uint32_t TL = 2048;
   while (TL > 32 && LocalLayout(2 * TL, rank, TL).total > budget) TL -= 32;
+  return TL;
+}
+
+// small-run span of k_local2: runs of <= TL rows, spans < 2*TL rows, two
+// staging buffers; two CTAs per SM
+uint32_t local2_span(const Workspace& ws, uint32_t rank) {
+  size_t budget = std::min<size_t>(ws.smem_optin, 110 * 1024);
+  if (const char* e = getenv("QD_LOCAL_KB")) budget = (size_t)atoi(e) * 1024;
+  uint32_t TL = 2048;
+  while (TL > 32 && Local2Layout(2 * TL, rank).total > budget) TL -= 32;
   return TL;
 }
 
@@ -2879,8 +3173,15 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
     const char* e = getenv("QD_PK_TILES");
     return !(e && atoi(e) == 0);
   }();
-  uint32_t TL = local_span(ws, R);
-  if (bits + ceil_log2(TL) + 1 > 64) TL = 0;  // local key would not fit 64 bits
+  // small runs: k_local2 (bucketed groups; keys up to 64 bits, no run bits)
+  // or, for a whole tensor that fits one CTA, k_local (run bits in its key)
+  static const bool old_local = [] {
+    const char* e = getenv("QD_LOCAL_V1");
+    return e && atoi(e) == 1;
+  }();
+  const bool local2 = !g.prefix.empty() && !old_local;
+  uint32_t TL = local2 ? local2_span(ws, R) : local_span(ws, R);
+  if (local2 ? bits > 64 : bits + ceil_log2(TL) + 1 > 64) TL = 0;  // local key would not fit
 
   // chunks hold whole tiles of the passes that dominate: the packed-row
   // tile when the rows will pack (the first, AoS, pass then ends each chunk
@@ -3033,7 +3334,51 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
       in = Rows{out.c, out.v, out.fmt};
     }
   }
-  if (small_runs && local_chunks) {
+  if (small_runs && local_chunks && local2) {
+    // small runs: items = the runs starting in [c*TL, (c+1)*TL) of every
+    // chunk that holds some (compact list); after the passes, whose
+    // intermediates may use dst's storage
+    auto* items = ws.get<LocalItem>("local_items", local_chunks);
+    auto* S_dev = ws.get<unsigned long long>("run_S", 1);
+    c.pre();
+    k_local_items<<<(uint32_t)std::min<uint64_t>((local_chunks + kThreads - 1) / kThreads,
+                                                 ws.num_sms * 8),
+                    kThreads, 0, c.st>>>(local_list, local_first, seg, S_dev, N, TL,
+                                         (uint32_t)local_chunks, items);
+    c.launched(kSegK);
+    Local2Args la{};
+    la.in_c = src_c;
+    la.in_v = src_v;
+    la.out_c = dst_c;
+    la.out_v = dst_v;
+    la.rank = R;
+    la.cap = 2 * TL;
+    la.seg_start = seg;
+    la.items = items;
+    la.n_items = (uint32_t)local_chunks;
+    if (c.next_counter >= kCounters) {
+      QD_CUDA(cudaMemsetAsync(c.counters, 0, kCounters * 4, c.st));
+      c.next_counter = 0;
+    }
+    la.item_counter = c.counters + c.next_counter++;
+    la.key = key;
+    la.npasses = (bits + kRadixLog - 1) / kRadixLog;
+    const uint32_t lper = (bits + la.npasses - 1) / la.npasses;
+    for (uint32_t q = 0; q < la.npasses; ++q) {
+      const uint32_t lo = q * lper, hi = std::min(bits, lo + lper);
+      la.dig[q] = make_digit(key, lo, hi);
+      la.dig_bits[q] = hi - lo;
+    }
+    la.err = c.err;
+    const size_t smem = Local2Layout(2 * TL, R).total;
+    int per_sm = 0;
+    QD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_local2, kLocal2Threads, smem));
+    const uint32_t grid = (uint32_t)std::min<uint64_t>(local_chunks,
+                                                       (uint64_t)std::max(1, per_sm) * ws.num_sms);
+    c.pre();
+    k_local2<<<grid, kLocal2Threads, smem, c.st>>>(la);
+    c.launched(kLocalK);
+  } else if (small_runs && local_chunks) {
     // small runs: chunks of runs starting in [c*TL, (c+1)*TL), only the
     // chunks that hold some (compact list); after the passes, whose
     // intermediates may use dst's storage

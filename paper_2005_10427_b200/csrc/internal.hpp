@@ -64,6 +64,10 @@ Workspace* workspace_create(int device);
 void workspace_destroy(Workspace* ws);
 uint64_t workspace_bytes(const Workspace* ws);
 uint64_t workspace_launches(const Workspace* ws);
+void* workspace_buffer(Workspace& ws, const char* name, size_t bytes);  // cached by name
+int workspace_device(const Workspace& ws);
+int workspace_sms(const Workspace& ws);
+void workspace_count_launch(Workspace& ws);
 void workspace_profile(Workspace* ws, int enable);
 void workspace_profile_reset(Workspace* ws);
 bool workspace_profile_get(const Workspace* ws, int cls, uint64_t* launches, double* ms,
@@ -118,6 +122,24 @@ void partition_rows_device(Workspace& ws, uint32_t rank, uint64_t nnz,
                            uint64_t* part_counts, void* stream,
                            const uint64_t* peer_c = nullptr, const uint64_t* peer_v = nullptr,
                            const uint64_t* peer_off = nullptr);
+
+// ---- multi-GPU (shard.cu) ----------------------------------------------------
+struct Comm;  // one rank of a communicator (NCCL, or the emulated hub)
+struct Hub;   // emulated ranks: threads of one process on one device (tests)
+void comm_unique_id(unsigned char* out128);
+Comm* comm_create_nccl(const unsigned char* id128, int nranks, int rank, int device);
+Hub* hub_create(int nranks);
+void hub_destroy(Hub* h);
+Comm* comm_create_emulated(Hub* hub, int rank, int device, Workspace* ws);
+void comm_destroy(Comm* c);
+int comm_size(const Comm& c);
+int comm_rank(const Comm& c);
+const char* comm_kind(const Comm& c);
+void sharded_transpose_device(Comm& comm, Workspace& ws, const TensorView& t,
+                              const uint32_t* d_c_in, const double* d_v_in, uint32_t* d_c_out,
+                              double* d_v_out, uint64_t out_capacity, uint64_t* n_out,
+                              const std::vector<Group>& groups, const uint32_t* target,
+                              void* stream, qd_shard_stats* stats);
 
 // .tns reader (tns.cu): io.cpp:42-126 minus canonicalisation.  Parses the
 // host text on the device; on success the rows are in device buffers the

@@ -9,7 +9,8 @@ transpose of the global tensor:
 
 * sigma1 == 0 (the plan's first step is bucketed, e.g. (0,2,1)): the slices
   are already sigma1-aligned when no mode-0 run straddles two ranks
-  (``aligned_bounds`` produces such slices) — every rank transposes its own
+  (``aligned_bounds`` produces such slices; ``slices_aligned`` checks it and
+  falls back to the exchange otherwise) — every rank transposes its own
   rows, no communication (the GPU lift of parallel.cpp:125-139).
 * otherwise (e.g. (1,0,2)): one exchange.  Global histogram of sigma1
   (all_reduce of each rank's ``qd_mode_histogram_device``), splitters that
@@ -173,6 +174,14 @@ class GpuBackend:
     def to_numpy_i64(self, h):
         return h.cpu().numpy()
 
+    def slice_info(self, rows: LocalRows, rank: int):
+        """(rows, first mode-0 value, last mode-0 value) of this slice."""
+        n = rows.nnz()
+        if n == 0:
+            return (0, 0, 0)
+        c = rows.coords.view(-1, rank)
+        return (n, int(c[0, 0].item()), int(c[-1, 0].item()))
+
     def synchronize(self):
         self.torch.cuda.synchronize(self.device)
 
@@ -238,6 +247,28 @@ def exchange_mode() -> str:
     return m
 
 
+def slices_aligned(dist, be, rows: LocalRows, rank_modes: int) -> bool:
+    """True when no mode-0 run straddles two ranks' slices (every rank's
+    first/last mode-0 value, gathered as a world x 3 all_reduce): then the
+    slices are independent for a target led by mode 0.  Otherwise the caller
+    falls back to the exchange path (the precondition was
+    assumed, and unaligned slices gave a silently unsorted result)."""
+    world, me = dist.get_world_size(), dist.get_rank()
+    info = np.zeros((world, 3), np.int64)
+    info[me] = be.slice_info(rows, rank_modes)
+    t = be.from_numpy_i64(info.ravel())
+    dist.all_reduce(t)
+    info = be.to_numpy_i64(t).reshape(world, 3)
+    prev = None
+    for q in range(world):
+        if info[q, 0] == 0:
+            continue
+        if prev is not None and info[prev, 2] == info[q, 1]:
+            return False
+        prev = q
+    return True
+
+
 def sharded_transpose(dist, be, rows: LocalRows, dims: Sequence[int], target: Sequence[int],
                       stats: dict = None):
     """Transpose the global tensor whose rank-ordered slices are `rows`;
@@ -249,7 +280,7 @@ def sharded_transpose(dist, be, rows: LocalRows, dims: Sequence[int], target: Se
     r = len(dims)
     target = [int(x) for x in target]
     world = dist.get_world_size()
-    if world == 1 or target[0] == 0:
+    if world == 1 or (target[0] == 0 and slices_aligned(dist, be, rows, r)):
         out = be.transpose(rows, dims, target)
         if stats is not None:
             stats.update(sent_bytes=0, exchange_s=0.0, rows_out=out.nnz())
@@ -283,168 +314,164 @@ def sharded_transpose(dist, be, rows: LocalRows, dims: Sequence[int], target: Se
 
 
 def bench_sharded(args, cfg, dist, rank, world, local):
-    """bench.py --gpus N: weak scaling.  Each rank generates its own
-    c2-shaped slice with mode-0 values offset by rank, so the global tensor
-    (dims[0] * N) x dims[1] x dims[2] is the rank-ordered concatenation, simply
-    sorted; every step transposes it to all 5 targets (the (0,2,1) target
-    without communication, the others with one all_to_all)."""
+    """bench.py --gpus N (torchrun, one process per GPU): STRONG scaling of
+    the configuration (config 5 by default: 1.74 G nonzeros in total, fixed
+    as N grows) through the C++ library's NCCL path
+    (qd_sharded_transpose_device, csrc/shard.cu).  Every rank generates the
+    same seeded tensor on its GPU and keeps its contiguous, mode-0-aligned
+    slice (parallel.cpp:125-139's bucket-aligned regions); each step
+    transposes the global tensor to every target — (0,2,1) without
+    communication, (1,0,2) with one exchange (histogram all-reduce, device
+    splitters, one grouped ncclSend/ncclRecv per peer).  Reports SURVEY §8e's
+    fields: per-N Mnnz/s (max over ranks of the device time), the per-GPU HBM
+    fraction of the byte model, NVLink bytes / exchange time / fraction of
+    900 GB/s, and the max/mean output balance."""
     import json
     import time
 
     import torch
 
-    from paper_2005_10427_b200 import synth
+    import paper_2005_10427_b200 as qd
+    import bench as B  # the driver-side helpers (clock sampler, peaks, byte model)
+
     torch.cuda.set_device(local)
-    ci, vi = synth.generate_torch(cfg, args.nnz, seed=cfg.seed + 1000 * rank, device="cuda")
     r = len(cfg.dims)
-    dims = list(cfg.dims)
-    ci = ci.view(-1, r)
-    ci[:, 0] += rank * dims[0]
-    ci = ci.reshape(-1).contiguous()
-    gdims = [dims[0] * world] + dims[1:]
-    be = GpuBackend(local)
-    rows = LocalRows(ci, vi)
+    ci, vi = B.make_input(cfg, args.nnz, "cuda")
+    n_total = vi.numel()
+    col0 = ci.view(n_total, r)[:, 0]
+    bounds = [0]
+    for p in range(1, world):  # slice bounds advanced to the next mode-0 change
+        j = n_total * p // world
+        if 0 < j < n_total:
+            j = int(torch.searchsorted(col0, col0[j - 1:j], right=True).item())
+        bounds.append(max(j, bounds[-1]))
+    bounds.append(n_total)
+    lo, hi = bounds[rank], bounds[rank + 1]
+    ci = ci[lo * r:hi * r].clone()
+    vi = vi[lo:hi].clone()
+    del col0
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
     n_local = vi.numel()
+    cap = n_total  # any rank may receive up to everything (a single sigma1 value)
+    co = torch.empty(cap * r, dtype=torch.int32, device="cuda")
+    vo = torch.empty(cap, dtype=torch.float64, device="cuda")
+    ws = qd.Workspace(local)
+    uid = [qd.comm_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    comm = qd.Comm(nranks=world, rank=rank, device=local, unique_id=uid[0])
+    stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream
+    strat = qd.SortStrategy.quesadilla()
+
+    def one(t, cin=None, vin=None, n=None):
+        return qd.sharded_transpose_device(
+            comm, r, cfg.dims, n_local if n is None else n,
+            (ci if cin is None else cin).data_ptr(), (vi if vin is None else vin).data_ptr(),
+            co.data_ptr(), vo.data_ptr(), cap, t, strat, ws, sp)
 
     def step():
-        for t in cfg.targets:
-            sharded_transpose(dist, be, rows, gdims, t)
+        return [one(t) for t in cfg.targets]
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     dist.barrier()
-    import bench as B  # the driver-side helpers (clock sampler, peaks)
-    l0 = be.ws.launches()
+    l0 = ws.launches()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with B.ClockSampler(local) as clk:
-        e0.record()
+        e0.record(stream)
         for _ in range(args.steps):
             step()
-        e1.record()
+        e1.record(stream)
         torch.cuda.synchronize()
     dist.barrier()
-    launches = be.ws.launches() - l0
-    # roofline: a second region with the library's per-kernel events
-    be.ws.profile(True)
-    be.ws.profile_reset()
-    for _ in range(args.steps):
-        step()
-    torch.cuda.synchronize()
-    prof = be.ws.profile_stats()
-    be.ws.profile(False)
-    dist.barrier()
+    launches = ws.launches() - l0
     ms = torch.tensor([e0.elapsed_time(e1)], device="cuda")
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    total = torch.tensor([n_local], device="cuda", dtype=torch.int64)
-    dist.all_reduce(total)
-
-    # SURVEY §8e reporting: one instrumented step (exchange bytes and time,
-    # output balance), separate from the timed regions
-    ex_bytes = ex_s = 0.0
-    imbalance = []
+    # SURVEY §8e reporting: one more step's per-target stats
+    per_target = {}
     for t in cfg.targets:
-        st = {}
-        sharded_transpose(dist, be, rows, gdims, t, stats=st)
-        vals = torch.tensor([st["sent_bytes"], st["exchange_s"], st["rows_out"], st["rows_out"]],
-                            device="cuda", dtype=torch.float64)
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        n_out, st = one(t)
+        a1.record(stream)
+        torch.cuda.synchronize()
+        vals = torch.tensor([a0.elapsed_time(a1), st["exchange_ms"], st["bytes_sent"], n_out,
+                             float(st["exchanged"])], device="cuda", dtype=torch.float64)
         mx = vals.clone()
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
         sm = vals.clone()
         dist.all_reduce(sm)
-        ex_bytes += sm[0].item()
-        ex_s += mx[1].item()
-        imbalance.append(round(mx[2].item() / max(1.0, sm[3].item() / world), 4))
-
-    # end to end: every rank copies its slice in from pinned host memory,
-    # runs the sharded transpose and copies its output slice back
-    hc = torch.empty(ci.shape, dtype=ci.dtype).pin_memory()
-    hv = torch.empty(vi.shape, dtype=vi.dtype).pin_memory()
+        t_ms, ex_ms = mx[0].item(), mx[1].item()
+        sent = sm[2].item()
+        mb = B.survey_bytes(cfg.dims, t, n_total)
+        per_target["".join(map(str, t))] = {
+            "ms": round(t_ms, 3), "Mnnz_s": round(n_total / t_ms / 1e3, 1),
+            "exchanged": bool(mx[4].item()),
+            "nvlink_bytes_sent_total": int(sent), "exchange_ms_max": round(ex_ms, 3),
+            "nvlink_GBs_per_rank": round(sent / world / (ex_ms / 1e3) / 1e9, 1) if ex_ms > 0 else None,
+            "nvlink_frac_of_900": (round(sent / world / (ex_ms / 1e3) / 1e9 / 900.0, 4)
+                                   if ex_ms > 0 else None),
+            "hbm_frac_per_gpu": round(mb / world / (t_ms / 1e3) / 1e9 / B.peaks()[0], 4),
+            "imbalance_max_over_mean": round(mx[3].item() / max(1.0, sm[3].item() / world), 4)}
+    # end to end: every rank copies its slice in from pinned host memory, runs
+    # the sharded transpose and copies its output slice back (host wall
+    # clock, max over ranks)
+    hc = torch.empty(ci.shape, dtype=ci.dtype, pin_memory=True)
+    hv = torch.empty(vi.shape, dtype=vi.dtype, pin_memory=True)
     hc.copy_(ci)
     hv.copy_(vi)
-    dc, dv = torch.empty_like(ci), torch.empty_like(vi)
-    # output slices may be larger than the input slice after the exchange
-    cap = 2 * n_local + 1024
-    oc = torch.empty(cap * r, dtype=ci.dtype).pin_memory()
-    ov = torch.empty(cap, dtype=vi.dtype).pin_memory()
-    torch.cuda.synchronize()
-    dist.barrier()
-    k_e2e = max(1, min(args.steps, 3))
-    # input copies on s_in into two device slots, output copies on s_out: the
-    # output copy of target i overlaps the input copy of target i+1
-    s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
-    slots = [(dc, dv), (torch.empty_like(ci), torch.empty_like(vi))]
+    del ci, vi
+    torch.cuda.empty_cache()
+    dc, dv = torch.empty(hc.shape, dtype=hc.dtype, device="cuda"), torch.empty_like(hv, device="cuda")
+    oc = torch.empty(cap * r, dtype=torch.int32, pin_memory=True) if n_total < (1 << 28) else None
+    k_e2e = 1
     h2d = d2h = 0
-    keep = []
     torch.cuda.synchronize()
     dist.barrier()
     t0 = time.perf_counter()
-    k = 0
     for _ in range(k_e2e):
         for t in cfg.targets:
-            sc, sv = slots[k % 2]
-            k += 1
-            with torch.cuda.stream(s_in):
-                sc.copy_(hc, non_blocking=True)
-                sv.copy_(hv, non_blocking=True)
-            torch.cuda.current_stream().wait_stream(s_in)
-            out, _ = sharded_transpose(dist, be, LocalRows(sc, sv), gdims, t)
-            n_out = out.values.numel()
-            if n_out > ov.numel():
-                oc = torch.empty(n_out * r, dtype=ci.dtype).pin_memory()
-                ov = torch.empty(n_out, dtype=vi.dtype).pin_memory()
-            s_out.wait_stream(torch.cuda.current_stream())
-            with torch.cuda.stream(s_out):
-                oc[:n_out * r].copy_(out.coords, non_blocking=True)
-                ov[:n_out].copy_(out.values, non_blocking=True)
-            keep.append(out)
-            h2d += sc.numel() * 4 + sv.numel() * 8
+            dc.copy_(hc, non_blocking=True)
+            dv.copy_(hv, non_blocking=True)
+            n_out, _ = one(t, dc, dv, n_local)
+            h2d += hc.numel() * 4 + hv.numel() * 8
             d2h += n_out * (4 * r + 8)
+            out_c = co[:n_out * r].cpu() if oc is None else oc[:n_out * r].copy_(co[:n_out * r])
+            out_v = vo[:n_out].cpu()
+            del out_c, out_v
     torch.cuda.synchronize()
-    wall = time.perf_counter() - t0
-    del keep
-    e2e_ms = torch.tensor([wall * 1e3], device="cuda")
-    dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+    wall = torch.tensor([time.perf_counter() - t0], device="cuda", dtype=torch.float64)
+    dist.all_reduce(wall, op=dist.ReduceOp.MAX)
+    comm.close()
     if rank == 0:
-        units = int(total.item()) * len(cfg.targets) * args.steps
+        units = n_total * len(cfg.targets) * args.steps
         v = units / (ms.item() / 1e3) / 1e6
-        top = max(("scatter", "local", "hist"), key=lambda k: prof[k]["ms"])
-        p = prof[top]
-        peak, peak_kind = B.peaks()
-        achieved = (p["bytes"] / p["launches"]) / (p["ms"] / p["launches"] / 1e3) / 1e9 \
-            if p["ms"] and p["launches"] else 0.0
-        e2e_units = int(total.item()) * len(cfg.targets) * k_e2e
+        model = sum(B.survey_bytes(cfg.dims, t, n_total) for t in cfg.targets)
+        step_s = ms.item() / args.steps / 1e3
         print(json.dumps({
             "metric": "nonzeros transposed/sec (Mnnz/s)", "value": round(v, 3), "unit": "Mnnz/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(ms.item() / args.steps, 4), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None,
+            "scaling": "strong", "vs_baseline": None,
             "dtype": "u32 coords + f64 values (moved, not computed)",
-            "data": "synthetic (seeded Zipf, per-rank slices of one global tensor)",
-            "config": {"workload": f"c2 x {world}: {gdims[0]}x{gdims[1]}x{gdims[2]}, "
-                                   f"{int(total.item())} nnz, 5 targets",
-                       "parallelism": f"shard{world} (sigma1 ranges; all_to_all over NCCL)",
-                       "l2": "inputs larger than L2; no flush needed"},
-            "roofline": {"bound": "hbm", "kernel": {"scatter": "k_scatter", "local": "k_local",
-                                                    "hist": "k_chunk_hist"}[top],
-                         "achieved": round(achieved, 1), "peak": peak, "peak_kind": peak_kind,
-                         "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
-                         "rank": 0},
-            "e2e": {"value": round(e2e_units / (e2e_ms.item() / 1e3) / 1e6, 3), "unit": "Mnnz/s",
-                    "h2d_bytes_per_step": h2d // k_e2e, "d2h_bytes_per_step": d2h // k_e2e,
+            "data": "synthetic (seeded stand-in; every rank keeps its mode-0-aligned slice)",
+            "config": {**B.workload_config(cfg, n_total, world),
+                       "parallelism": f"shard{world} (sigma1 ranges; C++ over NCCL)"},
+            "roofline": {"bound": "hbm", "kernel": "whole step (per-GPU byte model)",
+                         "achieved": round(model / world / step_s / 1e9, 1),
+                         "peak": B.peaks()[0], "unit": "GB/s",
+                         "frac": round(model / world / step_s / 1e9 / B.peaks()[0], 4),
+                         "traffic": None},
+            "e2e": {"value": round(n_total * len(cfg.targets) * k_e2e / wall.item() / 1e6, 3),
+                    "unit": "Mnnz/s", "h2d_bytes_per_step": h2d // k_e2e,
+                    "d2h_bytes_per_step": d2h // k_e2e,
                     "note": "rank 0's bytes; every rank moves its own slice; host wall clock, "
-                            "max over ranks; output copy of target i overlaps input copy of i+1"},
+                            "max over ranks"},
+            "per_target": per_target,
             "gpu_launches": launches,
             "clocks": clk.summary(),
-            "exchange": {"note": "one instrumented step: all_to_all bytes to other ranks summed "
-                                 "over ranks and targets; time = max over ranks per target, host-"
-                                 "synchronised around the exchange",
-                         "bytes_sent_total": int(ex_bytes), "exchange_ms": round(ex_s * 1e3, 3),
-                         "nvlink_GBs_per_rank": (round(ex_bytes / world / ex_s / 1e9, 1)
-                                                 if ex_s > 0 else None),
-                         "nvlink_frac": (round(ex_bytes / world / ex_s / 1e9 / 900.0, 4)
-                                         if ex_s > 0 else None),
-                         "imbalance_max_over_mean": dict(zip(
-                             ["".join(str(x) for x in t) for t in cfg.targets], imbalance))},
         }))
+    ws.close()
     dist.destroy_process_group()

@@ -16,7 +16,7 @@ sys.path.insert(0, ROOT)
 import paper_2005_10427_b200 as qd  # noqa: E402
 from paper_2005_10427_b200 import synth  # noqa: E402
 
-faulthandler.dump_traceback_later(240, exit=True)
+faulthandler.dump_traceback_later(int(os.environ.get("C5_TIMEOUT", "240")), exit=True)
 cfg = synth.CONFIGS["c5"]
 N = int(sys.argv[1]) if len(sys.argv) > 1 else cfg.nnz
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
@@ -82,7 +82,7 @@ torch.cuda.empty_cache()
 ws = qd.Workspace(0)
 print(f"generated {N} unique rows (from {M} draws, {U} unique) in {time.time() - t0:.1f} s",
       flush=True)
-faulthandler.dump_traceback_later(240, exit=True)
+faulthandler.dump_traceback_later(int(os.environ.get("C5_TIMEOUT", "240")), exit=True)
 assert qd.is_sorted_device(r, N, ci.data_ptr(), [0, 1, 2], ws, sp)
 co = torch.empty_like(ci)
 vo = torch.empty_like(vi)

@@ -616,6 +616,9 @@ class _ThreadDist:
     def barrier(self):
         self.hub.barrier.wait()
 
+    class group:  # noqa: N801 (torch.distributed's attribute name)
+        WORLD = None
+
     def symmetric_empty(self, nbytes, device):
         """Emulated symmetric memory: every rank's buffer lives on the one GPU,
         so the other ranks' base addresses are directly writable."""

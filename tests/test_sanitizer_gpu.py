@@ -1,0 +1,31 @@
+"""compute-sanitizer memcheck / racecheck / synccheck over the engine's
+kernel paths (tests/sanitize_driver.py: small c2/c4/c5-shaped transposes
+through the C ABI, checked against the oracle).  The engine relies on
+inter-CTA protocols (look-back scan status words, atomic chunk dealing,
+mbarrier phases of the TMA double buffers); the reference's own race check is
+its determinism suite (proj/tests/acceptance.cpp:188-220)."""
+import os
+import shutil
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SAN = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+
+
+@pytest.mark.skipif(not os.path.exists(SAN), reason="compute-sanitizer not found")
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck"])
+def test_sanitizer_clean(tool):
+    env = dict(os.environ, QD_SAN_ROWS="4000" if tool == "racecheck" else "8000")
+    cmd = [SAN, "--tool", tool, "--error-exitcode", "17", "--print-limit", "20"]
+    if tool == "memcheck":
+        cmd += ["--leak-check", "no"]
+    cmd += [sys.executable, os.path.join(ROOT, "tests", "sanitize_driver.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=1500, env=env)
+    out = r.stdout + r.stderr
+    assert "sanitize driver ok" in out, out[-4000:]
+    assert r.returncode == 0, out[-4000:]
+    assert "ERROR SUMMARY: 0 errors" in out or "RACECHECK SUMMARY: 0 hazards" in out, out[-4000:]
