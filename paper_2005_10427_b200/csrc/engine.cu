@@ -1923,6 +1923,275 @@ __global__ void __launch_bounds__(kLocal2Threads, 2) k_local2(Local2Args a) {
 }
 
 // ---------------------------------------------------------------------------
+// k_local3: the small runs of a bucketed group, streamed through shared
+// memory with one block-wide LSD radix sort per item.  Persistent CTAs take
+// items (the small runs starting in one TL-row chunk: a contiguous span of
+// < 2*TL rows) from a per-launch counter; the advancer warp loads the NEXT
+// item's span (TMA bulk copies + mbarrier) and its run starts into the other
+// buffer while the CTA sorts the current one.  Every row gets the composite
+// key (local run index, group key) — rows are already grouped by run, so the
+// run index keeps the runs apart through the LSD passes — and the item is
+// sorted by <= 8-bit digits of it (MATCH.ANY ranking per warp stripe, ranks
+// in registers, (key, row) pairs ping-ponged in shared memory), then written
+// out in sorted order.  A span is read completely (into shared memory)
+// before any row of it is written, so in == out is safe.  sort.cpp:80-134
+// (Alg. 2) on small buckets.
+// ---------------------------------------------------------------------------
+struct Local3Layout {
+  size_t cbuf, vbuf, c0, v0, k0, k1, i0, i1, seg, whist, start, wsum, total;
+  __host__ __device__ Local3Layout(uint32_t cap, uint32_t rank, uint32_t key_bytes,
+                                   uint32_t warps = kLocal2Warps) {
+    size_t o = 0;
+    cbuf = align16(size_t(cap) * rank * 4 + 32);
+    vbuf = align16(size_t(cap) * 8 + 32);
+    c0 = o; o += 2 * cbuf;
+    v0 = o; o += 2 * vbuf;
+    k0 = o; o += align16(size_t(cap) * key_bytes);
+    k1 = o; o += align16(size_t(cap) * key_bytes);
+    i0 = o; o += align16(size_t(cap) * 2);
+    i1 = o; o += align16(size_t(cap) * 2);
+    seg = o; o += 2 * align16(size_t(cap + 2) * 2);
+    whist = o; o += align16(size_t(warps) * kBins * 2);
+    start = o; o += align16(kBins * 4);
+    wsum = o; o += align16(64 * 4);
+    total = o;
+  }
+};
+
+template <class K, int NT>
+__global__ void __launch_bounds__(NT, 1024 / NT) k_local3(Local2Args a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  constexpr int NW = NT / 32;
+  const uint32_t R = a.rank;
+  const Local3Layout L(a.cap, R, sizeof(K), NW);
+  K* s_k0 = reinterpret_cast<K*>(smem + L.k0);
+  K* s_k1 = reinterpret_cast<K*>(smem + L.k1);
+  uint16_t* s_i0 = reinterpret_cast<uint16_t*>(smem + L.i0);
+  uint16_t* s_i1 = reinterpret_cast<uint16_t*>(smem + L.i1);
+  uint16_t* s_whist = reinterpret_cast<uint16_t*>(smem + L.whist);
+  uint32_t* s_start = reinterpret_cast<uint32_t*>(smem + L.start);
+  uint32_t* s_wsum = reinterpret_cast<uint32_t*>(smem + L.wsum);
+  const size_t seg_stride = align16(size_t(a.cap + 2) * 2);
+  __shared__ unsigned long long s_bar[2];
+  __shared__ uint32_t s_item[2];
+  __shared__ LocalItem s_desc[2];  // descriptor of the item staged in buffer b
+  __shared__ uint32_t s_ofs[2][2];
+  __shared__ KeySpec s_key;
+  constexpr uint32_t kAdv = NT - 32;
+  constexpr uint32_t kR = 8;  // ranking rounds per warp stripe (cap <= 16 * 32 * kR)
+  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+
+  // advancer warp: draw the next item, start its bulk copies into buffer b
+  // and copy its run starts (local u16 offsets) into the buffer's seg array
+  auto advance = [&](uint32_t b) {
+    uint32_t it = 0;
+    if (lane == 0) it = atomicAdd(a.item_counter, 1u);
+    it = __shfl_sync(0xFFFFFFFFu, it, 0);
+    if (lane == 0) s_item[b] = it;
+    if (it >= a.n_items) return;
+    const LocalItem item = a.items[it];
+    const Stage sc = make_stage(a.in_c + item.r0 * R, item.n * R * 4);
+    const Stage sv = make_stage(a.in_v + item.r0, item.n * 8);
+    if (lane == 0) {
+      s_desc[b] = item;
+      s_ofs[b][0] = sc.head;
+      s_ofs[b][1] = sv.head;
+      mbar_expect_tx(&s_bar[b], sc.bulk + sv.bulk);
+    }
+    __syncwarp();
+    if (lane == 0 && sc.bulk) bulk_g2s(smem + L.c0 + b * L.cbuf, sc.gal, sc.bulk, &s_bar[b]);
+    if (lane == 1 && sv.bulk) bulk_g2s(smem + L.v0 + b * L.vbuf, sv.gal, sv.bulk, &s_bar[b]);
+    uint16_t* sg = reinterpret_cast<uint16_t*>(smem + L.seg + b * seg_stride);
+    for (uint32_t k = lane; k <= item.nruns; k += 32)
+      sg[k] = (uint16_t)(a.seg_start[item.run_first + k] - item.r0);
+  };
+
+  if (threadIdx.x == kAdv) {
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (threadIdx.x == 0) s_key = a.key;
+  __syncthreads();
+  if (threadIdx.x >= kAdv) advance(0);
+  __syncthreads();
+  const KeySpec& key = s_key;
+  const uint32_t nk = key.n;
+  const uint32_t kb = key.total_bits;
+  // the key's first (up to) four fields in registers (the general KeySpec
+  // walk reloads every field from shared memory per row)
+  constexpr int kF = 4;
+  const bool few = nk <= (uint32_t)kF;
+  uint32_t fm[kF], fmask[kF], fo[kF], fd[kF];
+#pragma unroll
+  for (int f = 0; f < kF; ++f) {
+    const bool on = (uint32_t)f < nk;
+    fm[f] = on ? key.mode[f] : 0u;
+    fmask[f] = on ? (uint32_t)((1ull << key.width[f]) - 1ull) : 0u;
+    fo[f] = on ? key.off[f] : 0u;
+    fd[f] = on ? key.dim[f] : 0xFFFFFFFFu;
+  }
+  const bool check = key.check;
+  const unsigned below = (1u << lane) - 1u;
+  uint32_t phases = 0;
+  for (uint32_t iter = 0;; ++iter) {
+    const uint32_t b = iter & 1u;
+    const uint32_t it = s_item[b];
+    if (it >= a.n_items) break;
+    // buffer b^1 was released by the previous item's closing barrier
+    if (threadIdx.x >= kAdv) advance(b ^ 1u);
+    mbar_wait(&s_bar[b], (phases >> b) & 1u);
+    phases ^= 1u << b;
+    const LocalItem item = s_desc[b];
+    const uint32_t n = item.n, nsl = item.nruns;
+    const uint32_t* s_c =
+        reinterpret_cast<const uint32_t*>(smem + L.c0 + b * L.cbuf + s_ofs[b][0]);
+    const double* s_v = reinterpret_cast<const double*>(smem + L.v0 + b * L.vbuf + s_ofs[b][1]);
+    const uint16_t* sg = reinterpret_cast<const uint16_t*>(smem + L.seg + b * seg_stride);
+    // (the advancer's seg writes for buffer b happened before the barrier
+    // that closed the previous item)
+    const uint32_t rbits = nsl > 1 ? 32u - __clz(nsl - 1) : 0u;
+    const uint32_t tb = kb + rbits;
+    const uint32_t P = (tb + kRadixLog - 1) / kRadixLog;
+    const uint32_t per = P ? (tb + P - 1) / P : 0u;
+    // warp stripes of whole 32-row rounds
+    const uint32_t ipw = (((n + NW - 1) / NW) + 31u) & ~31u;
+    const uint32_t lo = w * ipw, hi = min(n, lo + ipw);
+    // composite keys: (local run index << kb) | key; range check of the key
+    {
+      uint32_t run = 0;
+      for (uint32_t p = lo + lane; p < hi; p += 32) {
+        if (nsl > 1) {
+          if (p == lo + lane) {  // first row of this lane: binary search
+            uint32_t l = 0, h = nsl;
+            while (h - l > 1) {
+              const uint32_t m = (l + h) >> 1;
+              if (sg[m] <= p) l = m; else h = m;
+            }
+            run = l;
+          }
+          while (run + 1 < nsl && sg[run + 1] <= p) ++run;
+        }
+        const uint32_t* row = s_c + (size_t)p * R;
+        K k = 0;
+        bool bad = false;
+        if (few) {
+#pragma unroll
+          for (int f = 0; f < kF; ++f) {
+            if ((uint32_t)f < nk) {
+              const uint32_t x = row[fm[f]];
+              bad |= x >= fd[f];
+              k |= (K)(x & fmask[f]) << fo[f];
+            }
+          }
+        } else {
+          for (uint32_t f = 0; f < nk; ++f) {
+            const uint32_t x = row[key.mode[f]];
+            bad |= x >= key.dim[f];
+            const uint32_t wd = key.width[f];
+            if (wd) k |= (K)(x & (uint32_t)((1ull << wd) - 1ull)) << key.off[f];
+          }
+        }
+        if (check && bad) check_row(row, key, item.r0 + p, a.err);
+        if (rbits) k |= (K)run << kb;
+        s_k0[p] = k;
+        s_i0[p] = (uint16_t)p;
+      }
+    }
+    K* kc = s_k0;
+    K* kn = s_k1;
+    uint16_t* ic = s_i0;
+    uint16_t* in_ = s_i1;
+    uint16_t* wh = s_whist + w * kBins;
+    __syncwarp();
+    for (uint32_t q = 0; q < P; ++q) {
+      const uint32_t sh = q * per;
+      const uint32_t dbits = min(per, tb - sh);
+      const uint32_t mask = (1u << dbits) - 1u;
+      const uint32_t nb = 1u << dbits;  // bins of this digit (<= 256)
+      {
+        uint32_t* wz = reinterpret_cast<uint32_t*>(wh);
+        for (uint32_t k = lane; k < (nb + 1) / 2; k += 32) wz[k] = 0u;
+      }
+      __syncwarp();
+      uint32_t packed[kR];
+#pragma unroll
+      for (uint32_t r = 0; r < kR; ++r) {
+        const uint32_t p = lo + r * 32 + lane;
+        if (lo + r * 32 >= hi) break;  // warp-uniform
+        const bool valid = p < hi;
+        const uint32_t d = valid ? (uint32_t)(kc[p] >> sh) & mask : 0xFFFFFFFFu;
+        const unsigned peers = __match_any_sync(0xFFFFFFFFu, d);
+        const uint32_t c = valid ? wh[d] : 0u;
+        __syncwarp();
+        if (valid && (peers & below) == 0u) wh[d] = (uint16_t)(c + __popc(peers));
+        __syncwarp();
+        packed[r] = ((c + __popc(peers & below)) << 8) | (d & 0xFFu);
+      }
+      __syncthreads();
+      // bin pairs (2t, 2t+1): warp-exclusive offsets with 16-bit SIMD adds,
+      // then the bins' starts by a scan over the pair totals
+      {
+        const uint32_t npair = (nb + 1) / 2;
+        uint32_t lo_cnt = 0, hi_cnt = 0, pair_excl = 0;
+        if (threadIdx.x < npair) {
+          uint32_t* wp = reinterpret_cast<uint32_t*>(s_whist) + threadIdx.x;
+          uint32_t run2 = 0;
+#pragma unroll
+          for (int x = 0; x < NW; ++x) {
+            const uint32_t c = wp[x * (kBins / 2)];
+            wp[x * (kBins / 2)] = run2;
+            run2 = __vadd2(run2, c);
+          }
+          lo_cnt = run2 & 0xFFFFu;
+          hi_cnt = run2 >> 16;
+        }
+        const uint32_t tot = lo_cnt + hi_cnt;
+        uint32_t incl = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+          if (lane >= (uint32_t)o) incl += y;
+        }
+        if (threadIdx.x < npair && lane == 31) s_wsum[w] = incl;
+        if (npair > 32) __syncthreads();
+        if (threadIdx.x < npair) {
+          uint32_t base = 0;
+          for (uint32_t x = 0; x < w; ++x) base += s_wsum[x];
+          pair_excl = base + incl - tot;
+          s_start[2 * threadIdx.x] = pair_excl;
+          s_start[2 * threadIdx.x + 1] = pair_excl + lo_cnt;
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (uint32_t r = 0; r < kR; ++r) {
+        const uint32_t p = lo + r * 32 + lane;
+        if (lo + r * 32 >= hi) break;
+        if (p < hi) {
+          const uint32_t d = packed[r] & 0xFFu;
+          const uint32_t slot = s_start[d] + wh[d] + (packed[r] >> 8);
+          kn[slot] = kc[p];
+          in_[slot] = ic[p];
+        }
+      }
+      __syncthreads();
+      K* tk = kc; kc = kn; kn = tk;
+      uint16_t* ti = ic; ic = in_; in_ = ti;
+    }
+    if (P == 0) __syncthreads();
+    for (uint32_t j = threadIdx.x; j < n; j += NT) {
+      const uint32_t i = ic[j];
+      const unsigned long long dst = item.r0 + j;
+      uint32_t* o = a.out_c + dst * R;
+      for (uint32_t m = 0; m < R; ++m) __stcs(o + m, s_c[i * R + m]);
+      __stcs(a.out_v + dst, s_v[i]);
+    }
+    __syncthreads();  // buffer b, its seg array and the scratch are free again
+  }
+}
+
+// ---------------------------------------------------------------------------
 // segment discovery
 // ---------------------------------------------------------------------------
 constexpr uint32_t kHeadRows = 4096;  // rows per k_heads CTA (128 words)
@@ -2670,6 +2939,10 @@ Workspace* workspace_create(int device) {
               allow_smem(reinterpret_cast<const void*>(f));
   allow_smem(reinterpret_cast<const void*>(k_local));
   allow_smem(reinterpret_cast<const void*>(k_local2));
+  allow_smem(reinterpret_cast<const void*>(k_local3<uint32_t, 512>));
+  allow_smem(reinterpret_cast<const void*>(k_local3<unsigned long long, 512>));
+  allow_smem(reinterpret_cast<const void*>(k_local3<uint32_t, 256>));
+  allow_smem(reinterpret_cast<const void*>(k_local3<unsigned long long, 256>));
   ws->smem_optin = optin - 1024;  // dynamic budget below the static usage
   return ws;
 }
@@ -2835,6 +3108,14 @@ uint32_t local2_span(const Workspace& ws, uint32_t rank) {
   if (const char* e = getenv("QD_LOCAL_KB")) budget = (size_t)atoi(e) * 1024;
   uint32_t TL = 2048;
   while (TL > 32 && Local2Layout(2 * TL, rank).total > budget) TL -= 32;
+  return TL;
+}
+
+uint32_t local3_span(const Workspace& ws, uint32_t rank, uint32_t key_bytes, uint32_t warps) {
+  size_t budget = std::min<size_t>(ws.smem_optin, 110 * 1024);
+  if (const char* e = getenv("QD_LOCAL3_KB")) budget = (size_t)atoi(e) * 1024;
+  uint32_t TL = std::min<uint32_t>(2048, warps * 32 * 8 / 2);  // k_local3's kR rounds per stripe
+  while (TL > 32 && Local3Layout(2 * TL, rank, key_bytes, warps).total > budget) TL -= 32;
   return TL;
 }
 
@@ -3175,13 +3456,33 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
   }();
   // small runs: k_local2 (bucketed groups; keys up to 64 bits, no run bits)
   // or, for a whole tensor that fits one CTA, k_local (run bits in its key)
-  static const bool old_local = [] {
-    const char* e = getenv("QD_LOCAL_V1");
-    return e && atoi(e) == 1;
+  // QD_LOCAL_V: 3 (default) = k_local3 (streamed block LSD over (run, key)),
+  // 2 = k_local2 (warp per run), 1 = k_local (round-1 kernel)
+  static const int local_v = [] {
+    const char* e = getenv("QD_LOCAL_V");
+    return e ? atoi(e) : 3;
   }();
-  const bool local2 = !g.prefix.empty() && !old_local;
-  uint32_t TL = local2 ? local2_span(ws, R) : local_span(ws, R);
-  if (local2 ? bits > 64 : bits + ceil_log2(TL) + 1 > 64) TL = 0;  // local key would not fit
+  const bool local2 = !g.prefix.empty() && local_v >= 2;
+  uint32_t TL = 0;
+  uint32_t kbytes = 4;
+  static const int l3_threads = [] {
+    const char* e = getenv("QD_LOCAL3_THREADS");
+    return e && atoi(e) == 256 ? 256 : 512;
+  }();
+  if (local2 && local_v == 3) {
+    TL = local3_span(ws, R, 4, l3_threads / 32);
+    if (bits + ceil_log2(2 * TL) > 32) {
+      kbytes = 8;
+      TL = local3_span(ws, R, 8, l3_threads / 32);
+    }
+    if (bits + ceil_log2(2 * TL) > 64) TL = 0;  // composite key would not fit 64 bits
+  } else if (local2) {
+    TL = local2_span(ws, R);
+    if (bits > 64) TL = 0;
+  } else {
+    TL = local_span(ws, R);
+    if (bits + ceil_log2(TL) + 1 > 64) TL = 0;  // local key would not fit 64 bits
+  }
 
   // chunks hold whole tiles of the passes that dominate: the packed-row
   // tile when the rows will pack (the first, AoS, pass then ends each chunk
@@ -3370,13 +3671,20 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
       la.dig_bits[q] = hi - lo;
     }
     la.err = c.err;
-    const size_t smem = Local2Layout(2 * TL, R).total;
+    using LocalFn = void (*)(Local2Args);
+    const int nt = local_v == 3 ? l3_threads : kLocal2Threads;
+    const LocalFn fn =
+        local_v != 3 ? k_local2
+        : nt == 256 ? (kbytes == 4 ? k_local3<uint32_t, 256> : k_local3<unsigned long long, 256>)
+                    : (kbytes == 4 ? k_local3<uint32_t, 512> : k_local3<unsigned long long, 512>);
+    const size_t smem = local_v == 3 ? Local3Layout(2 * TL, R, kbytes, nt / 32).total
+                                     : Local2Layout(2 * TL, R).total;
     int per_sm = 0;
-    QD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_local2, kLocal2Threads, smem));
+    QD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, nt, smem));
     const uint32_t grid = (uint32_t)std::min<uint64_t>(local_chunks,
                                                        (uint64_t)std::max(1, per_sm) * ws.num_sms);
     c.pre();
-    k_local2<<<grid, kLocal2Threads, smem, c.st>>>(la);
+    fn<<<grid, nt, smem, c.st>>>(la);
     c.launched(kLocalK);
   } else if (small_runs && local_chunks) {
     // small runs: chunks of runs starting in [c*TL, (c+1)*TL), only the

@@ -26,6 +26,21 @@ def test_sanitizer_clean(tool):
     cmd += [sys.executable, os.path.join(ROOT, "tests", "sanitize_driver.py")]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=1500, env=env)
     out = r.stdout + r.stderr
+    if "compute-sanitizer is closed" in out:
+        # the GPU pool refuses compute-sanitizer (it has left GPUs needing a
+        # reset); the race/poison stress of tests/stress_util.py and the
+        # determinism checks stand in for it there
+        pytest.skip("compute-sanitizer is closed on this GPU pool")
     assert "sanitize driver ok" in out, out[-4000:]
     assert r.returncode == 0, out[-4000:]
     assert "ERROR SUMMARY: 0 errors" in out or "RACECHECK SUMMARY: 0 hazards" in out, out[-4000:]
+
+
+def test_driver_with_poisoned_scratch():
+    """The same kernel paths with every fresh workspace buffer poisoned
+    (QD_POISON): a kernel reading scratch it never wrote fails the oracle
+    comparison instead of passing on zero-filled memory."""
+    env = dict(os.environ, QD_POISON="165", QD_SAN_ROWS="60000")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "sanitize_driver.py")],
+                       capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 0 and "sanitize driver ok" in r.stdout, (r.stdout + r.stderr)[-4000:]
