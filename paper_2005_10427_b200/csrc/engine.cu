@@ -246,6 +246,7 @@ struct ChunkHistArgs {
   uint64_t nnz;
   const ChunkDesc* chunks;
   uint32_t num_chunks;
+  const unsigned long long* nc_dev;  // device chunk count (latency mode; num_chunks = its bound)
   uint32_t* flat;  // [(coff + c) * kBins layout: coff*kBins + b*nchunks + cidx]
   DigitSpec dig;
   KeySpec key;
@@ -275,6 +276,7 @@ struct ScatterArgs {
   uint32_t T;  // rows per tile
   const ChunkDesc* chunks;
   uint32_t num_chunks;
+  const unsigned long long* nc_dev;     // device chunk count (latency mode; num_chunks = its bound)
   const unsigned long long* offs;       // exclusive scan of the chunk-hist flat array
   const unsigned long long* run_start;  // [li]; nullptr: 0
   uint32_t* chunk_counter;
@@ -683,7 +685,9 @@ __global__ void __launch_bounds__(kThreads) k_chunk_hist(ChunkHistArgs a) {
   const uint64_t N = a.nnz;
   const bool fast_dig = a.dig.lookup == nullptr && a.dig.n <= 2;
   const Dig2 dg = dig2_of(a.dig);
-  for (uint32_t ci = blockIdx.x; ci < a.num_chunks; ci += gridDim.x) {
+  const uint32_t NCH = a.nc_dev ? (uint32_t)min(*a.nc_dev, (unsigned long long)a.num_chunks)
+                                : a.num_chunks;
+  for (uint32_t ci = blockIdx.x; ci < NCH; ci += gridDim.x) {
     for (int k = threadIdx.x; k < kWarps * kBins; k += kThreads) s_h[k] = 0;
     __syncthreads();
     const ChunkDesc cd = a.chunks[ci];
@@ -966,6 +970,8 @@ __global__ void __launch_bounds__(kSortThreads, QD_SCATTER_CTAS * 512 / kSortThr
   const uint32_t R = RT ? RT : a.rank;
   const uint64_t N = a.nnz;
   const ScatterLayout L(a.T, R, IN);
+  const uint32_t NCH = a.nc_dev ? (uint32_t)min(*a.nc_dev, (unsigned long long)a.num_chunks)
+                                : a.num_chunks;
   uint32_t* s_sorted = reinterpret_cast<uint32_t*>(smem + L.sorted);
   uint16_t* s_whist = reinterpret_cast<uint16_t*>(smem + L.whist);
   uint32_t* s_start = reinterpret_cast<uint32_t*>(smem + L.start);
@@ -1060,16 +1066,16 @@ __global__ void __launch_bounds__(kSortThreads, QD_SCATTER_CTAS * 512 / kSortThr
       nc = pre_idx;
       nt = 0;
       cd = pre;
-      if (nc < a.num_chunks) {
+      if (nc < NCH) {
         pre_idx = next_chunk(nc);
-        if (pre_idx < a.num_chunks) pre = a.chunks[pre_idx];
+        if (pre_idx < NCH) pre = a.chunks[pre_idx];
       }
     }
     if ((threadIdx.x & 31) == 0) {
       s_chunk[pslot] = nc;
       s_tile[pslot] = nt;
     }
-    if (nc < a.num_chunks) load_tile(b, cd, nt);
+    if (nc < NCH) load_tile(b, cd, nt);
   };
 
   if (threadIdx.x == kAdv) {
@@ -1084,9 +1090,9 @@ __global__ void __launch_bounds__(kSortThreads, QD_SCATTER_CTAS * 512 / kSortThr
       s_chunk[0] = c0;
       s_tile[0] = 0;
     }
-    pre_idx = c0 < a.num_chunks ? next_chunk(c0) : a.num_chunks;
-    if (c0 < a.num_chunks) {
-      if (pre_idx < a.num_chunks) pre = a.chunks[pre_idx];
+    pre_idx = c0 < NCH ? next_chunk(c0) : NCH;
+    if (c0 < NCH) {
+      if (pre_idx < NCH) pre = a.chunks[pre_idx];
       load_tile(0, a.chunks[c0], 0);
     }
   }
@@ -1105,7 +1111,7 @@ __global__ void __launch_bounds__(kSortThreads, QD_SCATTER_CTAS * 512 / kSortThr
   for (uint32_t it = 0;; ++it) {
     const uint32_t b = it & 1u;
     const uint32_t ci = s_chunk[it & 1u], ti = s_tile[it & 1u];
-    if (ci >= a.num_chunks) break;
+    if (ci >= NCH) break;
     QD_TMARK(1);
     const ChunkDesc cd = s_cd[b];  // the advancer only refills the other slot
     const unsigned long long rb = cd.row_begin + (unsigned long long)ti * a.T;
@@ -1674,7 +1680,7 @@ struct LocalItem {
   uint32_t n;             // rows in the span
   uint32_t run_first;     // index of its first run in seg_start
   uint32_t nruns;         // runs in the span (all small)
-  uint32_t pad;
+  uint32_t maxrun;        // longest of them (<= 32: k_local3 sorts every run within a warp)
 };
 
 struct Local2Args {
@@ -1686,7 +1692,8 @@ struct Local2Args {
   uint32_t cap;  // rows per staging buffer (>= the longest span)
   const unsigned long long* seg_start;
   const LocalItem* items;
-  uint32_t n_items;
+  uint32_t n_items;                        // (bound, when n_items_dev is set)
+  const unsigned long long* n_items_dev;   // device item count (latency mode)
   uint32_t* item_counter;
   KeySpec key;
   uint32_t npasses;
@@ -1715,25 +1722,38 @@ struct Local2Layout {
 // that starts at/after (c+1)*TL or is large) and their row span
 __global__ void k_local_items(const uint32_t* list, const uint32_t* first_run,
                               const unsigned long long* seg_start, const unsigned long long* S_ptr,
-                              uint64_t nnz, uint32_t TL, uint32_t n_items, LocalItem* items) {
+                              uint64_t nnz, uint32_t TL, uint32_t n_items,
+                              const unsigned long long* n_dev, const uint32_t* maxrun,
+                              LocalItem* items) {
   const unsigned long long S = *S_ptr;
+  if (n_dev) n_items = (uint32_t)min(*n_dev, (unsigned long long)n_items);
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_items; i += gridDim.x * blockDim.x) {
     const uint32_t c = list[i];
     const unsigned long long hi = min((unsigned long long)nnz, ((unsigned long long)c + 1) * TL);
     const uint32_t f = first_run[c];
-    uint32_t k = f;
-    while (k < S && seg_start[k] < hi && seg_start[k + 1] - seg_start[k] <= TL) ++k;
+    // the runs starting in [c*TL, hi): binary search for the first run
+    // starting at or after hi; a large run can only be the last of them
+    // (it reaches past hi), and is left out
+    unsigned long long l = f, h = S;
+    while (l < h) {
+      const unsigned long long m = (l + h) >> 1;
+      if (seg_start[m] < hi) l = m + 1; else h = m;
+    }
+    uint32_t k = (uint32_t)l;
+    if (k > f && seg_start[k] - seg_start[k - 1] > TL) --k;
     LocalItem it;
     it.r0 = seg_start[f];
     it.n = (uint32_t)(seg_start[k] - seg_start[f]);
     it.run_first = f;
     it.nruns = k - f;
-    it.pad = 0;
+    it.maxrun = maxrun ? maxrun[c] : TL;
     items[i] = it;
   }
 }
 
 __global__ void __launch_bounds__(kLocal2Threads, 2) k_local2(Local2Args a) {
+  const uint32_t NI = a.n_items_dev ? (uint32_t)min(*a.n_items_dev, (unsigned long long)a.n_items)
+                                    : a.n_items;
   extern __shared__ __align__(128) unsigned char smem[];
   const uint32_t R = a.rank;
   const Local2Layout L(a.cap, R);
@@ -1759,7 +1779,7 @@ __global__ void __launch_bounds__(kLocal2Threads, 2) k_local2(Local2Args a) {
     if (lane == 0) it = atomicAdd(a.item_counter, 1u);
     it = __shfl_sync(0xFFFFFFFFu, it, 0);
     if (lane == 0) s_item[b] = it;
-    if (it >= a.n_items) return;
+    if (it >= NI) return;
     const LocalItem item = a.items[it];
     const Stage sc = make_stage(a.in_c + item.r0 * R, item.n * R * 4);
     const Stage sv = make_stage(a.in_v + item.r0, item.n * 8);
@@ -1794,7 +1814,7 @@ __global__ void __launch_bounds__(kLocal2Threads, 2) k_local2(Local2Args a) {
   for (uint32_t iter = 0;; ++iter) {
     const uint32_t b = iter & 1u;
     const uint32_t it = s_item[b];
-    if (it >= a.n_items) break;
+    if (it >= NI) break;
     if (threadIdx.x == 0) s_next_run = 0;
     // the other buffer was released by the previous item's closing barrier
     if (threadIdx.x >= kAdv) advance(b ^ 1u);
@@ -1960,6 +1980,8 @@ struct Local3Layout {
 
 template <class K, int NT>
 __global__ void __launch_bounds__(NT, 1024 / NT) k_local3(Local2Args a) {
+  const uint32_t NI = a.n_items_dev ? (uint32_t)min(*a.n_items_dev, (unsigned long long)a.n_items)
+                                    : a.n_items;
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int NW = NT / 32;
   const uint32_t R = a.rank;
@@ -1977,6 +1999,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_local3(Local2Args a) {
   __shared__ LocalItem s_desc[2];  // descriptor of the item staged in buffer b
   __shared__ uint32_t s_ofs[2][2];
   __shared__ KeySpec s_key;
+  __shared__ uint32_t s_next_run;  // warp path: next run of the item
   constexpr uint32_t kAdv = NT - 32;
   constexpr uint32_t kR = 8;  // ranking rounds per warp stripe (cap <= 16 * 32 * kR)
   const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -1988,7 +2011,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_local3(Local2Args a) {
     if (lane == 0) it = atomicAdd(a.item_counter, 1u);
     it = __shfl_sync(0xFFFFFFFFu, it, 0);
     if (lane == 0) s_item[b] = it;
-    if (it >= a.n_items) return;
+    if (it >= NI) return;
     const LocalItem item = a.items[it];
     const Stage sc = make_stage(a.in_c + item.r0 * R, item.n * R * 4);
     const Stage sv = make_stage(a.in_v + item.r0, item.n * 8);
@@ -2011,7 +2034,10 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_local3(Local2Args a) {
     mbar_init(&s_bar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (threadIdx.x == 0) s_key = a.key;
+  if (threadIdx.x == 0) {
+    s_key = a.key;
+    s_next_run = 0;
+  }
   __syncthreads();
   if (threadIdx.x >= kAdv) advance(0);
   __syncthreads();
@@ -2037,7 +2063,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_local3(Local2Args a) {
   for (uint32_t iter = 0;; ++iter) {
     const uint32_t b = iter & 1u;
     const uint32_t it = s_item[b];
-    if (it >= a.n_items) break;
+    if (it >= NI) break;
     // buffer b^1 was released by the previous item's closing barrier
     if (threadIdx.x >= kAdv) advance(b ^ 1u);
     mbar_wait(&s_bar[b], (phases >> b) & 1u);
@@ -2050,6 +2076,60 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_local3(Local2Args a) {
     const uint16_t* sg = reinterpret_cast<const uint16_t*>(smem + L.seg + b * seg_stride);
     // (the advancer's seg writes for buffer b happened before the barrier
     // that closed the previous item)
+    if (item.maxrun <= 32) {
+      // every run is at most 32 rows: row-parallel.  Keys go to shared
+      // memory; then each row finds its run (binary search over the run
+      // starts) and its place in it = #rows of the run with a smaller key +
+      // #equal keys before it (stable), and is written there directly.
+      unsigned long long* s_kk = reinterpret_cast<unsigned long long*>(
+          smem + L.k0);  // k0 and k1 together hold cap u64 keys
+      for (uint32_t p = threadIdx.x; p < n; p += NT) {
+        const uint32_t* row = s_c + (size_t)p * R;
+        unsigned long long k = 0;
+        bool bad = false;
+        if (few) {
+#pragma unroll
+          for (int f = 0; f < kF; ++f) {
+            if ((uint32_t)f < nk) {
+              const uint32_t x = row[fm[f]];
+              bad |= x >= fd[f];
+              k |= (unsigned long long)(x & fmask[f]) << fo[f];
+            }
+          }
+        } else {
+          for (uint32_t f = 0; f < nk; ++f) {
+            const uint32_t x = row[key.mode[f]];
+            bad |= x >= key.dim[f];
+            const uint32_t wd = key.width[f];
+            if (wd) k |= (unsigned long long)(x & (uint32_t)((1ull << wd) - 1ull)) << key.off[f];
+          }
+        }
+        if (check && bad) check_row(row, key, item.r0 + p, a.err);
+        s_kk[p] = k;
+      }
+      __syncthreads();
+      for (uint32_t p = threadIdx.x; p < n; p += NT) {
+        uint32_t l = 0, h = nsl;  // run of p: last start <= p
+        while (h - l > 1) {
+          const uint32_t m = (l + h) >> 1;
+          if (sg[m] <= p) l = m; else h = m;
+        }
+        const uint32_t rb = sg[l], re = sg[l + 1];
+        const unsigned long long k = s_kk[p];
+        uint32_t pos = rb;
+        for (uint32_t j = rb; j < re; ++j) {
+          const unsigned long long kj = s_kk[j];
+          pos += (kj < k) || (kj == k && j < p);
+        }
+        const unsigned long long dst = item.r0 + pos;
+        const uint32_t* row = s_c + (size_t)p * R;
+        uint32_t* o = a.out_c + dst * R;
+        for (uint32_t q = 0; q < R; ++q) __stcs(o + q, row[q]);
+        __stcs(a.out_v + dst, s_v[p]);
+      }
+      __syncthreads();  // buffer b and the key scratch are free again
+      continue;
+    }
     const uint32_t rbits = nsl > 1 ? 32u - __clz(nsl - 1) : 0u;
     const uint32_t tb = kb + rbits;
     const uint32_t P = (tb + kRadixLog - 1) / kRadixLog;
@@ -2286,7 +2366,7 @@ __global__ void __launch_bounds__(kThreads) k_compact(const uint32_t* words, uin
 __global__ void k_classify_chunks(const unsigned long long* seg_start,
                                   const unsigned long long* S_ptr, uint32_t TL, uint32_t CH,
                                   uint32_t* is_large, uint32_t* nchunks, uint32_t* local_flag,
-                                  uint32_t* first_run) {
+                                  uint32_t* first_run, uint32_t* local_maxrun) {
   const unsigned long long S = *S_ptr;
   for (unsigned long long s = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; s < S;
        s += (unsigned long long)gridDim.x * blockDim.x) {
@@ -2300,6 +2380,16 @@ __global__ void k_classify_chunks(const unsigned long long* seg_start,
       // the first run starting in a chunk records itself (one writer per
       // chunk; a flagged chunk always starts with a small run)
       if (s == 0 || seg_start[s - 1] / TL != cl) first_run[cl] = (uint32_t)s;
+    }
+    if (TL && local_maxrun) {
+      // longest small run per local chunk; consecutive runs share a chunk,
+      // so lanes of one chunk reduce first and one of them updates it
+      const unsigned long long cl = seg_start[s] / TL;
+      const uint32_t v = large ? 0u : (uint32_t)len;
+      const unsigned act = __activemask();
+      const unsigned peers = __match_any_sync(act, cl);
+      const uint32_t mx = __reduce_max_sync(peers, v);
+      if ((peers & ((1u << (threadIdx.x & 31)) - 1u)) == 0u && mx) atomicMax(local_maxrun + cl, mx);
     }
   }
 }
@@ -2366,7 +2456,9 @@ __global__ void k_gather_stride(const unsigned long long* in, uint64_t stride, u
 constexpr uint32_t kScanItems = 8;
 constexpr uint32_t kScanTile = kThreads * kScanItems;
 
-__global__ void k_scan_reduce(const uint32_t* in, unsigned long long n, unsigned long long* part) {
+__global__ void k_scan_reduce(const uint32_t* in, unsigned long long n, unsigned long long* part,
+                              const unsigned long long* n_dev, uint32_t n_mul) {
+  if (n_dev) n = min(n, *n_dev * n_mul);
   const unsigned long long b = (unsigned long long)blockIdx.x * kScanTile;
   unsigned long long s = 0;
   for (uint32_t k = 0; k < kScanItems; ++k) {
@@ -2397,7 +2489,9 @@ __global__ void k_scan_parts(unsigned long long* part, uint32_t np, unsigned lon
 }
 
 __global__ void k_scan_down(const uint32_t* in, unsigned long long n, const unsigned long long* part,
-                            unsigned long long* out) {
+                            unsigned long long* out, const unsigned long long* n_dev,
+                            uint32_t n_mul) {
+  if (n_dev) n = min(n, *n_dev * n_mul);
   const unsigned long long b = (unsigned long long)blockIdx.x * kScanTile;
   // each thread owns kScanItems consecutive elements
   unsigned long long v[kScanItems];
@@ -2426,7 +2520,8 @@ constexpr unsigned long long kLbValBits = 38, kLbValMask = (1ull << kLbValBits) 
 __global__ void __launch_bounds__(kThreads) k_scan_lookback(
     const uint32_t* in, unsigned long long n, unsigned long long* out, unsigned long long* total,
     unsigned long long* status, uint32_t nstat, unsigned long long* ticket,
-    unsigned long long ticket_base) {
+    unsigned long long ticket_base, const unsigned long long* n_dev, uint32_t n_mul) {
+  if (n_dev) n = min(n, *n_dev * n_mul);  // latency mode: the count is on the device
   __shared__ unsigned long long s_tile, s_prefix;
   __shared__ unsigned long long s_tmp[64];
   if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1ull) - ticket_base;
@@ -2492,7 +2587,8 @@ __global__ void __launch_bounds__(kThreads) k_scan_lookback(
   }
   __syncthreads();
   unsigned long long run = s_prefix + sum;
-  if (b + kScanTile >= n && threadIdx.x == kThreads - 1) *total = s_prefix + agg;
+  if (b + kScanTile >= n && b < n + kScanTile && threadIdx.x == kThreads - 1)
+    *total = s_prefix + agg;
 #pragma unroll
   for (uint32_t k = 0; k < kScanItems; ++k) {
     const unsigned long long i = b + threadIdx.x * kScanItems + k;
@@ -2585,7 +2681,9 @@ __global__ void __launch_bounds__(kThreads) k_probe_runs(const uint32_t* c, uint
 
 // implicit prefix coordinates of every large run (PackSpec::n_imp)
 __global__ void k_run_prefix(const uint32_t* c, uint32_t rank, const unsigned long long* run_start,
-                             uint64_t nruns, ModeList modes, uint32_t* out) {
+                             uint64_t nruns, const unsigned long long* n_dev, ModeList modes,
+                             uint32_t* out) {
+  if (n_dev) nruns = min((unsigned long long)nruns, *n_dev);
   for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < nruns;
        r += (uint64_t)gridDim.x * blockDim.x)
     for (uint32_t k = 0; k < modes.n; ++k) out[r * modes.n + k] = c[run_start[r] * rank + modes.m[k]];
@@ -2776,6 +2874,7 @@ struct Workspace {
   // consecutive calls run back to back, overlapping the previous calls'
   // device work and output copies (PCIe is full duplex).
   cudaStream_t s_in = nullptr, s_comp = nullptr, s_out = nullptr;
+  cudaStream_t s_host = nullptr;  // synchronous host-buffer calls (capturable, unlike stream 0)
   static constexpr int kSlots = QD_ASYNC_SLOTS;  // device in/out buffer pairs in flight
   cudaEvent_t ev_in[kSlots] = {}, ev_comp[kSlots] = {}, ev_out[kSlots] = {};
   struct SlotBuf {
@@ -2832,6 +2931,16 @@ struct Workspace {
   unsigned long long* lb_ticket = nullptr;
   size_t lb_cap = 0;
   unsigned long long lb_base = 0, lb_cleared_epoch = ~0ull;
+  // CUDA graphs of latency-mode calls, keyed by the call's shape and buffers;
+  // a reallocated workspace buffer (buf_epoch) invalidates them all
+  struct GraphEntry {
+    cudaGraphExec_t exec = nullptr;
+    uint64_t launches = 0;
+    uint64_t epoch = 0;
+    int seen = 0;
+  };
+  std::map<std::string, GraphEntry> graphs;
+  uint64_t buf_epoch = 0;
   // live per-kernel-class timing (CUDA events on the launch stream)
   bool prof = false;
   struct ProfStat {
@@ -2855,6 +2964,7 @@ struct Workspace {
     const size_t bytes = std::max<size_t>(count * sizeof(T), 256);
     DevBuf& b = bufs[name];
     if (b.bytes < bytes) {
+      ++buf_epoch;
       if (b.p) QD_CUDA(cudaFree(b.p));
       b.p = nullptr;
       b.bytes = 0;
@@ -2961,7 +3071,7 @@ void workspace_destroy(Workspace* ws) {
   for (auto& sb : ws->slots)
     for (void* p : {(void*)sb.ic, (void*)sb.iv, (void*)sb.oc, (void*)sb.ov})
       if (p) cudaFree(p);
-  for (cudaStream_t st : {ws->s_in, ws->s_comp, ws->s_out})
+  for (cudaStream_t st : {ws->s_in, ws->s_comp, ws->s_out, ws->s_host})
     if (st) {
       cudaStreamSynchronize(st);
       cudaStreamDestroy(st);
@@ -2974,6 +3084,8 @@ void workspace_destroy(Workspace* ws) {
   if (ws->h_err) cudaFreeHost(ws->h_err);
   if (ws->h_small) cudaFreeHost(ws->h_small);
   for (auto e : ws->ev_pool) cudaEventDestroy(e);
+  for (auto& g : ws->graphs)
+    if (g.second.exec) cudaGraphExecDestroy(g.second.exec);
   for (auto e : ws->done_pool) cudaEventDestroy(e);
   for (auto& p : ws->pending) cudaEventDestroy(p.done);
   delete ws;
@@ -3037,6 +3149,11 @@ struct Ctx {
   int group = 0;
   uint64_t nnz = 0;
   uint32_t rank = 0;
+  // latency mode (small tensors): no host synchronisation inside the call —
+  // run counts, chunk counts and item counts stay on the device and the
+  // kernels bound their grid-stride loops by them; buffers are sized for the
+  // worst case; the launch sequence is then capturable as a CUDA graph
+  bool lat = false;
   void pre() {
     if (ws.prof) {
       pending = ws.event();
@@ -3119,8 +3236,13 @@ uint32_t local3_span(const Workspace& ws, uint32_t rank, uint32_t key_bytes, uin
   return TL;
 }
 
+// n_dev (latency mode): the element count is *n_dev * n_mul on the device
+// and n is its bound; tiles past the count see zeros.  (A latency-mode call
+// resets the look-back ticket and status words first, so its launches
+// replay identically from a CUDA graph.)
 void scan_exclusive(Ctx& c, const uint32_t* in, uint64_t n, unsigned long long* out,
-                    unsigned long long* d_total) {
+                    unsigned long long* d_total, const unsigned long long* n_dev = nullptr,
+                    uint32_t n_mul = 1) {
   const uint32_t nb = (uint32_t)((n + kScanTile - 1) / kScanTile);
   auto* part = c.ws.get<unsigned long long>("scan_part", nb + 1);
   if (n == 0) {
@@ -3134,13 +3256,13 @@ void scan_exclusive(Ctx& c, const uint32_t* in, uint64_t n, unsigned long long* 
   }();
   if (three_kernel) {
     c.pre();
-    k_scan_reduce<<<nb, kThreads, 0, c.st>>>(in, n, part);
+    k_scan_reduce<<<nb, kThreads, 0, c.st>>>(in, n, part, n_dev, n_mul);
     c.launched(kSegK);
     c.pre();
     k_scan_parts<<<1, kThreads, 0, c.st>>>(part, nb, d_total);
     c.launched(kSegK);
     c.pre();
-    k_scan_down<<<nb, kThreads, 0, c.st>>>(in, n, part, out);
+    k_scan_down<<<nb, kThreads, 0, c.st>>>(in, n, part, out, n_dev, n_mul);
     c.launched(kSegK);
     return;
   }
@@ -3162,7 +3284,8 @@ void scan_exclusive(Ctx& c, const uint32_t* in, uint64_t n, unsigned long long* 
   }
   c.pre();
   k_scan_lookback<<<nb, kThreads, 0, c.st>>>(in, n, out, d_total, ws.lb_status,
-                                             (uint32_t)ws.lb_cap, ws.lb_ticket, ws.lb_base);
+                                             (uint32_t)ws.lb_cap, ws.lb_ticket, ws.lb_base,
+                                             n_dev, n_mul);
   c.launched(kSegK);
   ws.lb_base += nb;
 }
@@ -3170,7 +3293,8 @@ void scan_exclusive(Ctx& c, const uint32_t* in, uint64_t n, unsigned long long* 
 // Segment discovery on `coords` with respect to `modes`: fills seg_start[0..S]
 // (device, seg_start[S] = nnz) and returns S (host sync).
 uint64_t find_runs(Ctx& c, const uint32_t* coords, uint32_t rank, uint64_t nnz,
-                   const std::vector<uint32_t>& modes, unsigned long long** seg_out) {
+                   const std::vector<uint32_t>& modes, unsigned long long** seg_out,
+                   unsigned long long** S_dev_out = nullptr) {
   ModeList ml{};
   ml.n = (uint32_t)modes.size();
   for (uint32_t i = 0; i < ml.n; ++i) ml.m[i] = (uint8_t)modes[i];
@@ -3183,9 +3307,13 @@ uint64_t find_runs(Ctx& c, const uint32_t* coords, uint32_t rank, uint64_t nnz,
   k_heads<<<nb, kThreads, 0, c.st>>>(coords, rank, nnz, ml, words, bcnt);
   c.launched(kSegK);
   scan_exclusive(c, bcnt, nb, boff, tot);
-  QD_CUDA(cudaMemcpyAsync(c.ws.h_small, tot, 8, cudaMemcpyDeviceToHost, c.st));
-  QD_CUDA(cudaStreamSynchronize(c.st));
-  const uint64_t S = c.ws.h_small[0];
+  if (S_dev_out) *S_dev_out = tot;
+  uint64_t S = nnz;  // latency mode: the run count stays on the device (bound: nnz)
+  if (!c.lat) {
+    QD_CUDA(cudaMemcpyAsync(c.ws.h_small, tot, 8, cudaMemcpyDeviceToHost, c.st));
+    QD_CUDA(cudaStreamSynchronize(c.st));
+    S = c.ws.h_small[0];
+  }
   auto* seg = c.ws.get<unsigned long long>("seg_start", S + 1);
   c.pre();
   k_compact<<<nb, kThreads, 0, c.st>>>(words, nnz, boff, nb, seg, tot);
@@ -3318,7 +3446,8 @@ void run_pass(Ctx& c, uint32_t R, uint64_t N, uint32_t T, Rows in, RowsOut out,
               uint32_t pk_shift = 0, uint32_t pk_mask = 0, const uint8_t* digits_in = nullptr,
               uint8_t* digits_out = nullptr, uint32_t nd_shift = 0, uint32_t nd_mask = 0,
               const DigitSpec* next_dig = nullptr, const uint32_t* run_prefix = nullptr,
-              const PeerDest* peers = nullptr, bool peers_aligned = false) {
+              const PeerDest* peers = nullptr, bool peers_aligned = false,
+              const unsigned long long* nc_dev = nullptr) {
   Workspace& ws = c.ws;
   const uint64_t nflat = num_chunks * kBins;
   auto* flat = ws.get<uint32_t>("chunk_flat", nflat);
@@ -3330,6 +3459,7 @@ void run_pass(Ctx& c, uint32_t R, uint64_t N, uint32_t T, Rows in, RowsOut out,
   h.nnz = N;
   h.chunks = chunks;
   h.num_chunks = (uint32_t)num_chunks;
+  h.nc_dev = nc_dev;
   h.flat = flat;
   h.dig = dig;
   h.key = key;
@@ -3347,7 +3477,7 @@ void run_pass(Ctx& c, uint32_t R, uint64_t N, uint32_t T, Rows in, RowsOut out,
   k_chunk_hist<<<(uint32_t)std::min<uint64_t>(num_chunks, (uint64_t)ws.num_sms * 8), kThreads, 0,
                  c.st>>>(h);
   c.launched(kHistK);
-  scan_exclusive(c, flat, nflat, offs, tot);
+  scan_exclusive(c, flat, nflat, offs, tot, nc_dev, kBins);
 
   ScatterArgs a{};
   a.in = in;
@@ -3357,6 +3487,7 @@ void run_pass(Ctx& c, uint32_t R, uint64_t N, uint32_t T, Rows in, RowsOut out,
   a.T = T;
   a.chunks = chunks;
   a.num_chunks = (uint32_t)num_chunks;
+  a.nc_dev = nc_dev;
   a.offs = offs;
   a.run_start = run_start;
   a.dig = dig;
@@ -3501,6 +3632,8 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
   const uint32_t* local_list = nullptr;
   const uint32_t* local_first = nullptr;
   bool small_runs = false;
+  const unsigned long long* lat_counts = nullptr;  // latency mode: {large runs, chunks, items}
+  const uint32_t* local_maxrun = nullptr;            // per local chunk: its longest small run
 
   if (g.prefix.empty()) {
     if (TL && N <= TL) {
@@ -3519,7 +3652,8 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
         N, CH, (uint32_t)num_chunks, chunks);
     c.launched(kSegK);
   } else {
-    S = find_runs(c, src_c, R, N, g.prefix, &seg);
+    unsigned long long* S_found = nullptr;
+    S = find_runs(c, src_c, R, N, g.prefix, &seg, &S_found);  // latency mode: a bound (N)
     auto* is_large = ws.get<uint32_t>("run_large", S + 1);
     auto* nch = ws.get<uint32_t>("run_nchunks", S + 1);
     auto* loff = ws.get<unsigned long long>("run_loff", S + 1);
@@ -3531,16 +3665,23 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
     auto* lpos = ws.get<unsigned long long>("local_pos", nloc + 1);
     auto* llist = ws.get<uint32_t>("local_list", nloc + 1);
     auto* lfirst = ws.get<uint32_t>("local_first", nloc + 1);
+    auto* lmax = ws.get<uint32_t>("local_maxrun", nloc + 1);
     if (nloc) QD_CUDA(cudaMemsetAsync(lflag, 0, nloc * 4, c.st));
-    ws.h_small[0] = S;
-    QD_CUDA(cudaMemcpyAsync(S_dev, ws.h_small, 8, cudaMemcpyHostToDevice, c.st));
+    if (nloc) QD_CUDA(cudaMemsetAsync(lmax, 0, nloc * 4, c.st));
+    local_maxrun = lmax;
+    if (c.lat) {  // the device's run count; no host round trip
+      QD_CUDA(cudaMemcpyAsync(S_dev, S_found, 8, cudaMemcpyDeviceToDevice, c.st));
+    } else {
+      ws.h_small[0] = S;
+      QD_CUDA(cudaMemcpyAsync(S_dev, ws.h_small, 8, cudaMemcpyHostToDevice, c.st));
+    }
     const uint32_t grid = (uint32_t)std::min<uint64_t>((S + kThreads - 1) / kThreads, ws.num_sms * 8);
     c.pre();
     k_classify_chunks<<<grid, kThreads, 0, c.st>>>(seg, S_dev, TL, CH, is_large, nch, lflag,
-                                                   lfirst);
+                                                   lfirst, lmax);
     c.launched(kSegK);
-    scan_exclusive(c, is_large, S, loff, totals);
-    scan_exclusive(c, nch, S, coff, totals + 1);
+    scan_exclusive(c, is_large, S, loff, totals, c.lat ? S_found : nullptr);
+    scan_exclusive(c, nch, S, coff, totals + 1, c.lat ? S_found : nullptr);
     if (nloc) {
       scan_exclusive(c, lflag, nloc, lpos, totals + 2);
       c.pre();
@@ -3550,14 +3691,23 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
     } else {
       QD_CUDA(cudaMemsetAsync(totals + 2, 0, 8, c.st));
     }
-    QD_CUDA(cudaMemcpyAsync(ws.h_small + 1, totals, 24, cudaMemcpyDeviceToHost, c.st));
-    QD_CUDA(cudaStreamSynchronize(c.st));
-    num_large = ws.h_small[1];
-    num_chunks = ws.h_small[2];
-    local_chunks = ws.h_small[3];
+    if (c.lat) {
+      // bounds only; the counts stay on the device (totals[0..2])
+      num_large = N / (TL + 1) + 1;
+      num_chunks = N / CH + num_large + 1;
+      local_chunks = nloc;
+      small_runs = TL != 0;
+      lat_counts = totals;
+    } else {
+      QD_CUDA(cudaMemcpyAsync(ws.h_small + 1, totals, 24, cudaMemcpyDeviceToHost, c.st));
+      QD_CUDA(cudaStreamSynchronize(c.st));
+      num_large = ws.h_small[1];
+      num_chunks = ws.h_small[2];
+      local_chunks = ws.h_small[3];
+      small_runs = S > num_large;
+    }
     local_list = llist;
     local_first = lfirst;
-    small_runs = S > num_large;
     if (num_chunks) {
       chunks = ws.get<ChunkDesc>("chunks", num_chunks);
       auto* rs = ws.get<unsigned long long>("run_start", num_large);
@@ -3591,7 +3741,8 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
       c.pre();
       k_run_prefix<<<(uint32_t)std::min<uint64_t>((num_large + kThreads - 1) / kThreads + 1,
                                                    ws.num_sms * 8),
-                     kThreads, 0, c.st>>>(src_c, R, run_start, num_large, pm, run_prefix);
+                     kThreads, 0, c.st>>>(src_c, R, run_start, num_large,
+                                          lat_counts ? lat_counts : nullptr, pm, run_prefix);
       c.launched(kSegK);
     }
     if (!packed && D > 1 && !tmp_c) {
@@ -3631,7 +3782,8 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
       run_pass(c, R, N, Tq, in, out, chunks, num_chunks, run_start, digs[q], key,
                q == 0 && key.check, nullptr, packed ? &pack : nullptr, lo,
                (1u << (hi - lo)) - 1u, dig_in, dig_out, nlo, last ? 0u : (1u << (nhi - nlo)) - 1u,
-               last ? nullptr : &digs[q + 1], run_prefix);
+               last ? nullptr : &digs[q + 1], run_prefix, nullptr, false,
+               lat_counts ? lat_counts + 1 : nullptr);
       in = Rows{out.c, out.v, out.fmt};
     }
   }
@@ -3645,7 +3797,9 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
     k_local_items<<<(uint32_t)std::min<uint64_t>((local_chunks + kThreads - 1) / kThreads,
                                                  ws.num_sms * 8),
                     kThreads, 0, c.st>>>(local_list, local_first, seg, S_dev, N, TL,
-                                         (uint32_t)local_chunks, items);
+                                         (uint32_t)local_chunks,
+                                         lat_counts ? lat_counts + 2 : nullptr, local_maxrun,
+                                         items);
     c.launched(kSegK);
     Local2Args la{};
     la.in_c = src_c;
@@ -3657,6 +3811,7 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
     la.seg_start = seg;
     la.items = items;
     la.n_items = (uint32_t)local_chunks;
+    la.n_items_dev = lat_counts ? lat_counts + 2 : nullptr;
     if (c.next_counter >= kCounters) {
       QD_CUDA(cudaMemsetAsync(c.counters, 0, kCounters * 4, c.st));
       c.next_counter = 0;
@@ -3827,8 +3982,40 @@ void exec_group(Ctx& c, const TensorView& t, const uint32_t* src_c, const double
     const auto rc = costs(k, rest_keys, (double)S);
     return rc.first < rc.second;
   };
+  // MSD split: sort by the first key, then by the rest within its runs, when
+  // those runs come out short enough for the in-shared-memory small-run sort
+  // (expected length N / dim(k1) at most half its span) and the rest of the
+  // key would otherwise cost at least two more chunked passes — e.g. config
+  // 4's (4,3,2,1,0): 57 key bits = 8 chunked passes become 3 (mode 4) plus
+  // one small-run pass over its ~2-row runs.  QD_MSD=0 disables it.
+  static const bool msd_on = [] {
+    const char* e = getenv("QD_MSD");
+    return !(e && atoi(e) == 0);
+  }();
+  if (msd_on && g.check_range && m >= 2) {
+    uint32_t rest_bits = 0;
+    for (size_t i = 1; i < m; ++i) rest_bits += ceil_log2(t.dims[g.keys[i]]);
+    const uint32_t TLs = local3_span(ws, R, 8, kLocal2Warps);
+    const double avg_run = (double)N / (double)std::max<uint32_t>(1, t.dims[g.keys[0]]);
+    uint32_t first_bits = ceil_log2(t.dims[g.keys[0]]);
+    if (rest_bits >= 9 && avg_run * 2.0 <= (double)TLs && first_bits > 0 &&
+        (first_bits + rest_bits + 7) / 8 > (first_bits + 7) / 8 + 1) {
+      auto* xc = ws.get<uint32_t>("rowsC_c", N * R);
+      auto* xv = ws.get<double>("rowsC_v", N);
+      Group first;
+      first.prefix = g.prefix;
+      first.keys = {g.keys[0]};
+      segmented_sort(c, t, src_c, src_v, xc, xv, tmp_c, tmp_v, first);
+      Group rest;
+      rest.prefix = g.prefix;
+      rest.prefix.push_back(g.keys[0]);
+      rest.keys.assign(g.keys.begin() + 1, g.keys.end());
+      segmented_sort(c, t, xc, xv, dst_c, dst_v, tmp_c, tmp_v, rest);
+      return;
+    }
+  }
   // run records hold a run's start row in 32 bits (k_run_records)
-  if (!disabled && g.check_range && g.prefix.empty() && m >= 1 && N >= min_rows &&
+  if (!disabled && !c.lat && g.check_range && g.prefix.empty() && m >= 1 && N >= min_rows &&
       N <= 0xFFFFFFFFull) {
     auto* xc = m >= 2 ? ws.get<uint32_t>("rowsC_c", N * R) : nullptr;
     auto* xv = m >= 2 ? ws.get<double>("rowsC_v", N) : nullptr;
@@ -3893,16 +4080,24 @@ static Ctx make_ctx(Workspace& ws, void* stream) {
   return c;
 }
 
-static void run_groups_once(Workspace& ws, const TensorView& t, const uint32_t* d_c_in,
-                            const double* d_v_in, uint32_t* d_c_out, double* d_v_out,
-                            const std::vector<Group>& groups, bool verify_input,
-                            uint64_t* d_boundaries, uint64_t* n_boundaries,
-                            uint32_t boundary_mode, void* stream, unsigned* flags) {
-  Ctx c = make_ctx(ws, stream);
+// Every launch of a call (no final synchronisation): the part a latency-mode
+// call captures into a CUDA graph.
+static void launch_groups(Ctx& c, const TensorView& t, const uint32_t* d_c_in,
+                          const double* d_v_in, uint32_t* d_c_out, double* d_v_out,
+                          const std::vector<Group>& groups, bool verify_input,
+                          uint64_t* d_boundaries, uint64_t* n_boundaries,
+                          uint32_t boundary_mode) {
+  Workspace& ws = c.ws;
   const uint64_t N = t.nnz;
   const uint32_t R = t.rank;
-  c.nnz = N;
-  c.rank = R;
+  if (c.lat) {
+    // look-back scan state from tile 0 each call (graph-replayable)
+    if (!ws.lb_ticket) ws.lb_ticket = ws.get<unsigned long long>("lb_ticket", 1);
+    QD_CUDA(cudaMemsetAsync(ws.lb_ticket, 0, 8, c.st));
+    if (ws.lb_status) QD_CUDA(cudaMemsetAsync(ws.lb_status, 0, ws.lb_cap * 8, c.st));
+    ws.lb_base = 0;
+    ws.lb_cleared_epoch = 0;
+  }
   if (verify_input && N > 1) {
     ModeList ml{};
     ml.n = R;
@@ -3958,6 +4153,113 @@ static void run_groups_once(Workspace& ws, const TensorView& t, const uint32_t* 
   } else if (n_boundaries) {
     *n_boundaries = 0;
   }
+}
+
+// Latency mode applies to tensors up to kLatRows rows whose groups all use
+// range-checked keys (widths known without a device read), without
+// boundary output; QD_LATENCY=0 disables it, QD_GRAPHS=0 keeps it eager.
+constexpr uint64_t kLatRows = 1ull << 24;
+
+static std::string graph_key(const Workspace& ws, const TensorView& t, const void* a,
+                             const void* b, const void* cc, const void* d,
+                             const std::vector<Group>& groups, bool verify) {
+  std::string k;
+  auto put = [&](uint64_t x) { k.append(reinterpret_cast<const char*>(&x), 8); };
+  put(t.nnz);
+  put(t.rank);
+  for (uint32_t m = 0; m < t.rank; ++m) put(t.dims[m]);
+  put(reinterpret_cast<uintptr_t>(a));
+  put(reinterpret_cast<uintptr_t>(b));
+  put(reinterpret_cast<uintptr_t>(cc));
+  put(reinterpret_cast<uintptr_t>(d));
+  put(verify);
+  put(ws.allow_pack);
+  for (const Group& g : groups) {
+    put(0xFFFF0000ull | g.prefix.size());
+    for (uint32_t m : g.prefix) put(m);
+    put(0xEEEE0000ull | g.keys.size());
+    for (uint32_t m : g.keys) put(m);
+    put(g.check_range);
+  }
+  return k;
+}
+
+static void run_groups_once(Workspace& ws, const TensorView& t, const uint32_t* d_c_in,
+                            const double* d_v_in, uint32_t* d_c_out, double* d_v_out,
+                            const std::vector<Group>& groups, bool verify_input,
+                            uint64_t* d_boundaries, uint64_t* n_boundaries,
+                            uint32_t boundary_mode, void* stream, unsigned* flags) {
+  Ctx c = make_ctx(ws, stream);
+  const uint64_t N = t.nnz;
+  c.nnz = N;
+  c.rank = t.rank;
+  static const bool lat_on = [] {
+    const char* e = getenv("QD_LATENCY");
+    return !(e && atoi(e) == 0);
+  }();
+  static const bool graphs_on = [] {
+    const char* e = getenv("QD_GRAPHS");
+    return !(e && atoi(e) == 0);
+  }();
+  static const bool local_v1 = [] {
+    const char* e = getenv("QD_LOCAL_V");
+    return e && atoi(e) == 1;
+  }();
+  bool lat = lat_on && !local_v1 && N > 0 && N <= kLatRows && !d_boundaries;
+  for (const Group& g : groups) lat &= g.check_range;
+  c.lat = lat;
+  auto eager = [&] {
+    launch_groups(c, t, d_c_in, d_v_in, d_c_out, d_v_out, groups, verify_input, d_boundaries,
+                  n_boundaries, boundary_mode);
+  };
+  // the legacy / per-thread default streams cannot be captured
+  const bool capturable = c.st != nullptr && c.st != cudaStreamLegacy && c.st != cudaStreamPerThread;
+  if (lat && graphs_on && !ws.prof && capturable) {
+    const std::string key = graph_key(ws, t, d_c_in, d_v_in, d_c_out, d_v_out, groups, verify_input);
+    Workspace::GraphEntry& e = ws.graphs[key];
+    if (e.exec && e.epoch != ws.buf_epoch) {  // a buffer it uses was reallocated
+      cudaGraphExecDestroy(e.exec);
+      e = Workspace::GraphEntry{};
+    }
+    if (e.exec) {
+      QD_CUDA(cudaGraphLaunch(e.exec, c.st));
+      ws.launches += e.launches;
+    } else if (e.seen == 0) {
+      // first call of this shape: eager (sizes every workspace buffer)
+      e.seen = 1;
+      eager();
+      e.epoch = ws.buf_epoch;
+    } else {
+      // second call: capture the launches (no allocation happens: the
+      // buffers were sized by the first call) and replay them from now on
+      const uint64_t epoch0 = ws.buf_epoch, l0 = ws.launches;
+      QD_CUDA(cudaStreamBeginCapture(c.st, cudaStreamCaptureModeThreadLocal));
+      cudaGraph_t g = nullptr;
+      try {
+        eager();
+      } catch (...) {
+        cudaStreamEndCapture(c.st, &g);
+        if (g) cudaGraphDestroy(g);
+        cudaGetLastError();
+        throw;
+      }
+      QD_CUDA(cudaStreamEndCapture(c.st, &g));
+      if (ws.buf_epoch != epoch0) {
+        // a buffer grew during capture (should not happen): run eagerly
+        cudaGraphDestroy(g);
+        e = Workspace::GraphEntry{};
+        eager();
+      } else {
+        QD_CUDA(cudaGraphInstantiate(&e.exec, g, 0));
+        QD_CUDA(cudaGraphDestroy(g));
+        e.launches = ws.launches - l0;
+        e.epoch = ws.buf_epoch;
+        QD_CUDA(cudaGraphLaunch(e.exec, c.st));
+      }
+    }
+  } else {
+    eager();
+  }
   *flags = check_errors(c);
 }
 
@@ -3994,7 +4296,8 @@ void run_groups_host(Workspace& ws, const TensorView& t, uint32_t* coords, doubl
   uint32_t* oc = ws.get<uint32_t>("host_out_c", N * R);
   double* ov = ws.get<double>("host_out_v", N);
   uint64_t* db = h_boundaries ? ws.get<uint64_t>("host_bounds", N + 1) : nullptr;
-  cudaStream_t st = nullptr;
+  if (!ws.s_host) QD_CUDA(cudaStreamCreateWithFlags(&ws.s_host, cudaStreamNonBlocking));
+  cudaStream_t st = ws.s_host;
   // Pageable caller buffers (a std::vector in the C++ drop-in) go through the
   // pinned chunk ring with a parallel host memcpy (tns.cu): the driver's own
   // pageable path runs at ~11 GB/s.  Pinned buffers are copied directly.

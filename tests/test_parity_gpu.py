@@ -936,3 +936,70 @@ def test_stress_with_poisoned_scratch():
     r = subprocess.run([_sys.executable, os.path.join(os.path.dirname(__file__), "stress_util.py"),
                         "8", "60"], env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+# --- latency mode: no host syncs inside the call, CUDA graph replays ---------
+
+def test_latency_mode_graph_replays(ws):
+    """Small tensors run without host round trips and, from the second call
+    of a shape on the same buffers, as a replayed CUDA graph: new bytes in
+    the same buffers, alternating shapes and targets, a bucketed plan with
+    small and large runs, and a buffer that grows in between (invalidating
+    the captured graphs) must all still match the oracle."""
+    import torch
+    rng = np.random.default_rng(77)
+    shapes = [([40, 300, 500], 120_000, [2, 1, 0]),
+              ([40, 300, 500], 120_000, [0, 2, 1]),
+              ([15, 12, 9, 3000, 700], 90_000, [4, 3, 2, 1, 0]),
+              ([15, 12, 9, 3000, 700], 90_000, [0, 1, 4, 2, 3])]
+    bufs = {}
+    for rep in range(4):
+        for k, (dims, n, target) in enumerate(shapes):
+            t = rand_tensor(rng, dims, n)
+            r = len(dims)
+            nn = t.nnz()
+            if k not in bufs:
+                cap = n + 10
+                bufs[k] = [torch.empty(cap * r, dtype=torch.int32, device="cuda"),
+                           torch.empty(cap, dtype=torch.float64, device="cuda"),
+                           torch.empty(cap * r, dtype=torch.int32, device="cuda"),
+                           torch.empty(cap, dtype=torch.float64, device="cuda")]
+            ci, vi, co, vo = bufs[k]
+            ci[:nn * r].copy_(torch.from_numpy(t.coords.view(np.int32)))
+            vi[:nn].copy_(torch.from_numpy(t.values))
+            qd.transpose_device(r, dims, nn, ci.data_ptr(), vi.data_ptr(), co.data_ptr(),
+                                vo.data_ptr(), target, qd.SortStrategy.quesadilla(), ws,
+                                torch.cuda.current_stream().cuda_stream)
+            torch.cuda.synchronize()
+            c, v, _ = ORC.transpose(dims, t.coords, t.values, target)
+            assert np.array_equal(co[:nn * r].cpu().numpy().view(np.uint32), c), (rep, k)
+            assert np.array_equal(vo[:nn].cpu().numpy().view(np.uint64), v.view(np.uint64))
+        if rep == 1:  # a bigger call grows workspace buffers: graphs recaptured
+            big = rand_tensor(rng, [200, 300, 900], 2_000_000)
+            out = qd.transpose(big, [1, 2, 0], ws=ws)
+            c, v, _ = ORC.transpose(big.dims, big.coords, big.values, [1, 2, 0])
+            assert np.array_equal(out.coords, c)
+
+
+def test_latency_mode_out_of_range_on_replay(ws):
+    """An out-of-range coordinate found by a replayed graph raises
+    OutOfRange with the reference's first (row, mode)."""
+    import torch
+    rng = np.random.default_rng(78)
+    dims = [30, 40, 50]
+    t = rand_tensor(rng, dims, 50_000)
+    n, r = t.nnz(), 3
+    ci = torch.from_numpy(t.coords.view(np.int32).copy()).cuda()
+    vi = torch.from_numpy(t.values.copy()).cuda()
+    co, vo = torch.empty_like(ci), torch.empty_like(vi)
+    sp = torch.cuda.current_stream().cuda_stream
+    for _ in range(3):  # eager, capture, replay
+        qd.transpose_device(r, dims, n, ci.data_ptr(), vi.data_ptr(), co.data_ptr(), vo.data_ptr(),
+                            [1, 0, 2], qd.SortStrategy.quesadilla(), ws, sp)
+    bad = t.coords.copy().reshape(-1, 3)
+    bad[n // 3, 1] = 40
+    ci.copy_(torch.from_numpy(bad.ravel().view(np.int32)))
+    with pytest.raises(qd.OutOfRange) as e:
+        qd.transpose_device(r, dims, n, ci.data_ptr(), vi.data_ptr(), co.data_ptr(),
+                            vo.data_ptr(), [1, 0, 2], qd.SortStrategy.quesadilla(), ws, sp)
+    assert e.value.row == n // 3 and e.value.mode == 1
