@@ -23,6 +23,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <condition_variable>
 #include <map>
 #include <mutex>
 #include <thread>
@@ -326,13 +327,13 @@ __global__ void k_line_slow(ParseArgs a, uint64_t count) {
 // a parallel memcpy while the copy engine moves the previous one.
 constexpr uint64_t kStageChunk = 32ull << 20;
 constexpr int kStageSlots = 4;
-constexpr int kMaxCopyThreads = 8;
+constexpr int kMaxCopyThreads = 16;
 
 int copy_threads() {
   static const int n = [] {
     if (const char* e = getenv("QD_COPY_THREADS")) return std::max(1, std::min(kMaxCopyThreads, atoi(e)));
     const unsigned hc = std::thread::hardware_concurrency();
-    return (int)std::max(1u, std::min<unsigned>(kMaxCopyThreads, hc ? hc / 2 : 4));
+    return (int)std::max(1u, std::min<unsigned>(kMaxCopyThreads, hc ? hc : 4));
   }();
   return n;
 }
@@ -361,20 +362,81 @@ struct StageRing {
   }
 };
 
+// A persistent pool of host copy threads (spawning threads per 32 MB chunk
+// cost a sizeable fraction of the chunk's copy time).  A job is split into
+// page-aligned parts; the caller copies part 0 and waits for the rest.
+class CopyPool {
+ public:
+  static CopyPool& get() {
+    static CopyPool p(copy_threads());
+    return p;
+  }
+  void run(char* dst, const char* src, uint64_t n) {
+    const int nt = (int)workers_.size() + 1;
+    const uint64_t part = (n / nt + 4095) & ~4095ull;
+    std::unique_lock<std::mutex> lk(mu_);
+    dst_ = dst;
+    src_ = src;
+    n_ = n;
+    part_ = part;
+    pending_ = nt - 1;
+    ++gen_;
+    cv_.notify_all();
+    lk.unlock();
+    std::memcpy(dst, src, std::min(n, part));
+    lk.lock();
+    done_cv_.wait(lk, [&] { return pending_ == 0; });
+  }
+  ~CopyPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+      ++gen_;
+    }
+    cv_.notify_all();
+    for (auto& t : workers_) t.join();
+  }
+
+ private:
+  explicit CopyPool(int nt) {
+    for (int t = 1; t < nt; ++t) workers_.emplace_back([this, t] { loop(t); });
+  }
+  void loop(int t) {
+    uint64_t seen = 0;
+    for (;;) {
+      std::unique_lock<std::mutex> lk(mu_);
+      cv_.wait(lk, [&] { return gen_ != seen; });
+      seen = gen_;
+      if (stop_) return;
+      char* dst = dst_;
+      const char* src = src_;
+      const uint64_t a = std::min(n_, t * part_), b = std::min(n_, (t + 1) * part_);
+      lk.unlock();
+      if (b > a) std::memcpy(dst + a, src + a, b - a);
+      lk.lock();
+      if (--pending_ == 0) done_cv_.notify_one();
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex mu_;
+  std::condition_variable cv_, done_cv_;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+  char* dst_ = nullptr;
+  const char* src_ = nullptr;
+  uint64_t n_ = 0, part_ = 0;
+  int pending_ = 0;
+};
+
+std::mutex g_copy_mu;  // one job at a time in the shared pool
+
 void parallel_memcpy(char* dst, const char* src, uint64_t n) {
-  if (n < (4ull << 20)) {
+  if (n < (4ull << 20) || copy_threads() == 1) {
     std::memcpy(dst, src, n);
     return;
   }
-  const int nt = copy_threads();
-  std::thread th[kMaxCopyThreads - 1];
-  const uint64_t part = (n / nt + 4095) & ~4095ull;
-  for (int t = 1; t < nt; ++t) {
-    const uint64_t a = std::min(n, t * part), b = std::min(n, (t + 1) * part);
-    th[t - 1] = std::thread([=] { std::memcpy(dst + a, src + a, b - a); });
-  }
-  std::memcpy(dst, src, std::min(n, part));
-  for (int t = 1; t < nt; ++t) th[t - 1].join();
+  std::lock_guard<std::mutex> lk(g_copy_mu);
+  CopyPool::get().run(dst, src, n);
 }
 
 StageRing& stage_ring() {
