@@ -480,7 +480,11 @@ def main():
     co = torch.empty_like(ci)
     vo = torch.empty_like(vi)
     ws = qd.Workspace(local)
-    stream = torch.cuda.current_stream()
+    # a created (non-default) stream: the library captures latency-mode calls
+    # (tensors up to 2^24 rows) into CUDA graphs, which the legacy default
+    # stream cannot do
+    stream = torch.cuda.Stream(local)
+    torch.cuda.set_stream(stream)
     sp = stream.cuda_stream
     strat = qd.SortStrategy.quesadilla()
 

@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cuda_runtime.h>
 
+template <bool CS>
 __global__ void k_store(const ulonglong2* __restrict__ in, ulonglong2* __restrict__ out,
                         unsigned long long nchunks, unsigned T, unsigned CH, unsigned B) {
   const unsigned per = T / B;  // rows per bin per tile
@@ -20,7 +21,7 @@ __global__ void k_store(const ulonglong2* __restrict__ in, ulonglong2* __restric
         const ulonglong2 v = __ldcs(in + rb + j);
         const unsigned b = j / per, k = t * per + j % per;
         const unsigned long long dst = ((unsigned long long)b * nchunks + c) * (CH * per) + k;
-        __stcs(out + dst, v);
+        if (CS) __stcs(out + dst, v); else out[dst] = v;
       }
     }
   }
@@ -37,21 +38,24 @@ int main() {
   cudaEventCreate(&b);
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  for (unsigned T : {2048u, 4096u}) {
-    for (unsigned B : {1u, 128u, 256u, 512u, 1024u, 2048u}) {
+  for (int cs = 1; cs >= 0; --cs)
+  for (unsigned T : {2048u, 4096u, 8192u}) {
+    for (unsigned B : {1u, 256u, 1024u, 2048u, 4096u}) {
+      if (B > T) continue;  // needs >= 1 row per bin per tile
       const unsigned CH = 16;
       const unsigned long long nchunks = N / ((unsigned long long)T * CH);
       float best = 1e9;
       for (int rep = 0; rep < 5; ++rep) {
         cudaEventRecord(a);
-        k_store<<<sms * 4, 512>>>(in, out, nchunks, T, CH, B);
+        if (cs) k_store<true><<<sms * 4, 512>>>(in, out, nchunks, T, CH, B);
+        else k_store<false><<<sms * 4, 512>>>(in, out, nchunks, T, CH, B);
         cudaEventRecord(b);
         cudaEventSynchronize(b);
         float ms;
         cudaEventElapsedTime(&ms, a, b);
         if (ms < best) best = ms;
       }
-      printf("T=%u bins=%4u rows/bin/tile=%5.1f  %.3f ms  %.0f GB/s (read+write)\n", T, B,
+      printf("%s T=%u bins=%4u rows/bin/tile=%5.1f  %.3f ms  %.0f GB/s (read+write)\n", cs ? "stcs" : "st  ", T, B,
              (double)T / B, best, 2.0 * N * 16 / best / 1e6);
     }
   }
