@@ -240,6 +240,36 @@ __device__ __forceinline__ void unpack_coords(const PackSpec& p, uint32_t R, uns
   }
 }
 
+// PackSpec decoded on the host for the static-rank (RT = 3, 4) scatter paths:
+// per-mode u32/u64 words at fixed offsets, which the compiler reads as
+// constant-bank operands (the byte arrays of PackSpec indexed per row cost
+// extracts and loads: the round-1 c5 profile had the pack and mixed-radix
+// unpack at ~45 % of the unpacking pass's instructions).
+struct PackFast {
+  uint32_t fsh[4], fmask[4];        // bit field of the mode (mask 0: not a field)
+  unsigned long long mul[4];        // mixed-radix weight of the mode (0: not mixed)
+  uint32_t mpos[4];                 // mixed-radix position of the mode (0xFF: none)
+  uint32_t dimj[4];                 // mixed-radix dimension by position
+  unsigned long long magic[4];      // floor((2^64 - 1) / dimj)
+  uint32_t impk[4];                 // implicit prefix mode: its index in run_prefix (0xFF: none)
+  uint32_t key_bits, mixed, nk_n;
+};
+
+// q = x / d, r = x % d for x < 2^63 and d >= 1 with mg = floor((2^64-1)/d):
+// umulhi(x, mg) is q or q - 1 (its error is below x (1 + 1/d) / 2^64 < 1),
+// one correction step
+__device__ __forceinline__ unsigned long long div_magic(unsigned long long x, uint32_t d,
+                                                        unsigned long long mg, uint32_t& r) {
+  unsigned long long q = __umul64hi(x, mg);
+  unsigned long long rem = x - q * d;
+  if (rem >= d) {
+    ++q;
+    rem -= d;
+  }
+  r = (uint32_t)rem;
+  return q;
+}
+
 struct ChunkHistArgs {
   Rows in;
   uint32_t rank;
@@ -289,6 +319,10 @@ struct ScatterArgs {
   const uint32_t* run_prefix;  // implicit prefix modes per large run (PackSpec::n_imp)
   const PeerDest* peers;       // AoS output per bin (partition straight into peer buffers)
   int vec_out;                 // AoS output rows may use 16-byte stores (rank 4, aligned base)
+  PackFast pf;                 // pack decoded for the RT = 3, 4 paths
+  uint32_t dbits;              // bits of this pass's digit (ballot ranking)
+  int rank_mode;               // adaptive_peers mode (QD_RANK_MODE)
+  uint32_t match_max;          // mode 1: MATCH.ANY when a round has <= this many digit runs
 };
 
 // ---------------------------------------------------------------------------
@@ -427,6 +461,40 @@ __device__ __forceinline__ unsigned warp_peers(uint32_t d, unsigned valid) {
     m &= bit ? v : ~v;
   }
   return m;
+}
+
+// Peers of d among the lanes in `valid` for a digit of `nbits` bits (<= 8):
+// MATCH.ANY costs ~2 SM cycles per DISTINCT digit in the warp (61 for 32
+// random 8-bit digits), nbits ballots a flat ~3.2 each
+// (profiles/microbench/match_any_vs_ballot.*).  mode 1 picks per 32-row
+// round from the number of runs of equal digits among the lanes (an upper
+// bound on the distinct count): MATCH for clustered digits, ballots for
+// high-entropy ones; mode 0 = MATCH only, 2 = ballots only.  Measured
+// (B200, c5/c2/c3 steps): MATCH only 104.8 / 11.59 / 21.42 ms, adaptive
+// 109.6 / 12.15 / 21.89, ballots only 112.6 / 12.10 / 21.81: the kernel is
+// issue-bound enough that 7-8 VOTE + LOP pairs per round cost more than the
+// MATCH.ANY they replace, so mode 0 is the default (QD_RANK_MODE).
+__device__ __forceinline__ unsigned ballot_peers(uint32_t d, unsigned valid, uint32_t nbits) {
+  unsigned m = valid;
+#pragma unroll
+  for (uint32_t b = 0; b < 8; ++b) {
+    if (b < nbits) {  // warp-uniform
+      const unsigned bit = (d >> b) & 1u;
+      const unsigned v = __ballot_sync(0xFFFFFFFFu, bit);
+      m &= bit ? v : ~v;
+    }
+  }
+  return m;
+}
+__device__ __forceinline__ unsigned adaptive_peers(uint32_t d, unsigned valid, uint32_t nbits,
+                                                   int mode, uint32_t match_max) {
+  if (mode == 0) return __match_any_sync(0xFFFFFFFFu, d) & valid;
+  if (mode == 2) return ballot_peers(d, valid, nbits);
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t prev = __shfl_up_sync(0xFFFFFFFFu, d, 1);
+  const unsigned heads = __ballot_sync(0xFFFFFFFFu, lane == 0u || prev != d);
+  if ((uint32_t)__popc(heads) <= match_max) return __match_any_sync(0xFFFFFFFFu, d) & valid;
+  return ballot_peers(d, valid, nbits);
 }
 
 // Stable per-warp ranking of positions [0, n): positions are cut into NW
@@ -1189,7 +1257,7 @@ __global__ void __launch_bounds__(kSortThreads, QD_SCATTER_CTAS * 512 / kSortThr
       if ((uint32_t)r >= nfull) break;  // warp-uniform
       const uint32_t p = lo + r * 32 + lane;
       const uint32_t d = digit_at(p);
-      const unsigned peers = warp_peers(d, 0xFFFFFFFFu);
+      const unsigned peers = adaptive_peers(d, 0xFFFFFFFFu, a.dbits, a.rank_mode, a.match_max);
 #if QD_RANK_BCAST
       // every lane reads its digit's count (equal digits: one broadcast
       // wavefront), the lowest peer writes it back: no shuffle
@@ -1213,7 +1281,7 @@ __global__ void __launch_bounds__(kSortThreads, QD_SCATTER_CTAS * 512 / kSortThr
       const bool valid = lane < (nrow & 31u);
       uint32_t d = 0;
       if (valid) d = digit_at(p);
-      unsigned peers = warp_peers(d, (1u << (nrow & 31u)) - 1u);
+      unsigned peers = adaptive_peers(d, (1u << (nrow & 31u)) - 1u, a.dbits, a.rank_mode, a.match_max);
       if (!valid) peers = 1u << lane;
 #if QD_RANK_BCAST
       const uint32_t bcount = valid ? wh[d] : 0u;
@@ -1311,6 +1379,14 @@ __global__ void __launch_bounds__(kSortThreads, QD_SCATTER_CTAS * 512 / kSortThr
       }
     };
     const uint32_t vbase = IN == kPK ? 0u : (uint32_t)(span_dst(b, R) - scb) + s_ofsb[R];
+    // prefix modes left out of the packed rows: constant within the tile's run
+    uint32_t impv[RT > 0 ? RT : 1];
+#pragma unroll
+    for (int m = 0; m < (RT > 0 ? RT : 1); ++m) {
+      impv[m] = 0u;
+      if (MX && IN == kPK && OUT != kPK && a.pf.impk[m] != 0xFFu)
+        impv[m] = __ldg(a.run_prefix + (size_t)cd.li * a.pack.n_imp + a.pf.impk[m]);
+    }
     for (uint32_t j = threadIdx.x; j < n; j += kSortThreads) {
       const uint32_t sj = s_sorted[j];
       const uint32_t i = sj >> 8;
@@ -1324,34 +1400,33 @@ __global__ void __launch_bounds__(kSortThreads, QD_SCATTER_CTAS * 512 / kSortThr
         } else {  // unpack into AoS
           uint32_t* o = a.out.c + dst * R;
           if (MX && RT) {
-            // key fields, then the mixed-radix part from its last mode down;
-            // unrolled with static indices so cv stays in registers
-            uint32_t cv[RT > 0 ? RT : 1];
+            // bit fields, then the mixed-radix part from its last position
+            // down (nk_n - 1 divisions); static indices keep cv in registers
+            constexpr int kR = RT > 0 ? RT : 1;
+            uint32_t cv[kR];
 #pragma unroll
-            for (int m = 0; m < (RT > 0 ? RT : 1); ++m)
-              cv[m] = (uint32_t)(row.x >> a.pack.off[m]) &
-                      (uint32_t)((1ull << a.pack.width[m]) - 1ull);
-            unsigned long long hi = a.pack.key_bits < 64 ? row.x >> a.pack.key_bits : 0ull;
+            for (int m = 0; m < kR; ++m) cv[m] = (uint32_t)(row.x >> a.pf.fsh[m]) & a.pf.fmask[m];
+            if (a.pf.mixed) {
+              unsigned long long hi = row.x >> a.pf.key_bits;
+              uint32_t v[kR];
 #pragma unroll
-            for (int jj = (RT > 0 ? RT : 1) - 1; jj >= 0; --jj) {
-              if (a.pack.mixed && (uint32_t)jj < a.pack.nk_n) {
-                const uint32_t d = a.pack.nk_dim[jj];
-                const unsigned long long q = div_u64_u32(hi, d, a.pack.nk_rcp[jj]);
-                const uint32_t v = (uint32_t)(hi - q * d);
-                const uint32_t mj = a.pack.nk_mode[jj];
+              for (int jj = kR - 1; jj >= 1; --jj) {
+                v[jj] = 0u;
+                if ((uint32_t)jj < a.pf.nk_n) hi = div_magic(hi, a.pf.dimj[jj], a.pf.magic[jj], v[jj]);
+              }
+              v[0] = (uint32_t)hi;
 #pragma unroll
-                for (int m = 0; m < (RT > 0 ? RT : 1); ++m)
-                  if (mj == (uint32_t)m) cv[m] = v;
-                hi = q;
+              for (int m = 0; m < kR; ++m) {
+                const uint32_t pos = a.pf.mpos[m];
+                uint32_t x = v[0];
+#pragma unroll
+                for (int jj = 1; jj < kR; ++jj) x = pos == (uint32_t)jj ? v[jj] : x;
+                if (pos < (uint32_t)kR) cv[m] = x;
               }
             }
-            for (uint32_t k = 0; k < a.pack.n_imp; ++k) {
-              const uint32_t v = __ldg(a.run_prefix + (size_t)s_cd[b].li * a.pack.n_imp + k);
-              const uint32_t mk = a.pack.imp_mode[k];
 #pragma unroll
-              for (int m = 0; m < (RT > 0 ? RT : 1); ++m)
-                if (mk == (uint32_t)m) cv[m] = v;
-            }
+            for (int m = 0; m < (RT > 0 ? RT : 1); ++m)
+              if (a.pf.impk[m] != 0xFFu) cv[m] = impv[m];
             if (RT != 4 || a.vec_out) {
               store_row_words<(RT > 0 ? RT : 1)>(o, cv);
             } else {
@@ -1367,7 +1442,7 @@ __global__ void __launch_bounds__(kSortThreads, QD_SCATTER_CTAS * 512 / kSortThr
             uint32_t cv[RT > 0 ? RT : 1];
 #pragma unroll
             for (int m = 0; m < (RT > 0 ? RT : 1); ++m)
-              cv[m] = (uint32_t)(row.x >> a.pack.off[m]) & (uint32_t)((1ull << a.pack.width[m]) - 1ull);
+              cv[m] = (uint32_t)(row.x >> a.pf.fsh[m]) & a.pf.fmask[m];
             if (RT != 4 || a.vec_out) {
               store_row_words<(RT > 0 ? RT : 1)>(o, cv);
             } else {
@@ -1394,29 +1469,21 @@ __global__ void __launch_bounds__(kSortThreads, QD_SCATTER_CTAS * 512 / kSortThr
         if (MX && RT) {
           uint32_t cv[RT > 0 ? RT : 1];
           load_cv(i, cv);
-#pragma unroll
-          for (int m = 0; m < (RT > 0 ? RT : 1); ++m)
-            if (a.pack.width[m]) pk |= (unsigned long long)cv[m] << a.pack.off[m];
-          // fully unrolled so cv stays in registers (static indices only)
           unsigned long long hi = 0;
 #pragma unroll
-          for (int j = 0; j < (RT > 0 ? RT : 1); ++j) {
-            if (a.pack.mixed && (uint32_t)j < a.pack.nk_n) {
-              const uint32_t mj = a.pack.nk_mode[j];
-              uint32_t x = cv[0];
-#pragma unroll
-              for (int m = 1; m < (RT > 0 ? RT : 1); ++m) x = mj == (uint32_t)m ? cv[m] : x;
-              hi = hi * a.pack.nk_dim[j] + x;
-            }
+          for (int m = 0; m < (RT > 0 ? RT : 1); ++m) {
+            pk |= (unsigned long long)(cv[m] & a.pf.fmask[m]) << a.pf.fsh[m];
+            hi += (unsigned long long)cv[m] * a.pf.mul[m];
           }
-          if (a.pack.mixed) pk |= hi << a.pack.key_bits;
+          if (a.pf.mixed) pk |= hi << a.pf.key_bits;
         } else if (MX) {
           pk = pack_coords(a.pack, R, [&](uint32_t m) { return coord(i, m); });
         } else if (RT) {
           uint32_t cv[RT > 0 ? RT : 1];
           load_cv(i, cv);
 #pragma unroll
-          for (int m = 0; m < (RT > 0 ? RT : 1); ++m) pk |= (unsigned long long)cv[m] << a.pack.off[m];
+          for (int m = 0; m < (RT > 0 ? RT : 1); ++m)
+            pk |= (unsigned long long)(cv[m] & a.pf.fmask[m]) << a.pf.fsh[m];
         } else {
           for (uint32_t m = 0; m < R; ++m)
             pk |= (unsigned long long)coord(i, m) << a.pack.off[m];
@@ -3359,7 +3426,7 @@ DigitSpec make_digit(const KeySpec& k, uint32_t lo, uint32_t hi) {
 // the other modes as bit fields above when everything fits 64 bits, else as
 // one mixed-radix number when THAT fits; false if neither does.
 bool make_pack(const KeySpec& key, uint32_t R, const uint32_t* dims, PackSpec* out,
-               const std::vector<uint32_t>& implicit = {}) {
+               const std::vector<uint32_t>& implicit = {}, bool allow_mixed = true) {
   PackSpec p{};
   p.rank = R;
   p.key_bits = key.total_bits;
@@ -3397,7 +3464,7 @@ bool make_pack(const KeySpec& key, uint32_t R, const uint32_t* dims, PackSpec* o
   }
   // mixed radix: the product of the non-key dimensions must fit the bits
   // left above the key
-  if (key.total_bits >= 64) return false;
+  if (key.total_bits >= 64 || !allow_mixed) return false;
   const unsigned __int128 room = (unsigned __int128)1 << (64 - key.total_bits);
   unsigned __int128 prod = 1;
   for (uint32_t m : nonkey) {
@@ -3493,7 +3560,37 @@ void run_pass(Ctx& c, uint32_t R, uint64_t N, uint32_t T, Rows in, RowsOut out,
   a.dig = dig;
   a.pk_shift = pk_shift;
   a.pk_mask = pk_mask;
-  if (pack) a.pack = *pack;
+  if (pack) {
+    a.pack = *pack;
+    PackFast& f = a.pf;
+    for (uint32_t m = 0; m < 4; ++m) f.mpos[m] = f.impk[m] = 0xFFu;
+    for (uint32_t k = 0; k < pack->n_imp; ++k)
+      if (pack->imp_mode[k] < 4) f.impk[pack->imp_mode[k]] = k;
+    for (uint32_t m = 0; m < R && m < 4; ++m) {
+      if (pack->kind[m] == 0 && pack->width[m]) {
+        f.fsh[m] = pack->off[m];
+        f.fmask[m] = (uint32_t)((1ull << pack->width[m]) - 1ull);
+      }
+    }
+    f.mixed = pack->mixed;
+    f.key_bits = pack->key_bits;
+    f.nk_n = pack->nk_n;
+    if (pack->mixed) {
+      unsigned long long w = 1;
+      for (int j = (int)pack->nk_n - 1; j >= 0; --j) {
+        const uint32_t m = pack->nk_mode[j];
+        if (j < 4) {
+          f.dimj[j] = pack->nk_dim[j];
+          f.magic[j] = ~0ull / pack->nk_dim[j];
+        }
+        if (m < 4) {
+          f.mul[m] = w;
+          f.mpos[m] = (uint32_t)j;
+        }
+        w *= pack->nk_dim[j];
+      }
+    }
+  }
   a.next_dig = digits_out;
   a.nd_shift = nd_shift;
   a.nd_mask = nd_mask;
@@ -3503,6 +3600,26 @@ void run_pass(Ctx& c, uint32_t R, uint64_t N, uint32_t T, Rows in, RowsOut out,
   a.vec_out = out.fmt == kAoS && vec_rows_enabled() &&
               (peers ? peers_aligned : (reinterpret_cast<uintptr_t>(out.c) & 15u) == 0);
   if (const char* e = getenv("QD_SCATTER_DBG")) a.dbg = atoi(e);
+  {
+    static const int rank_mode = [] {
+      const char* e = getenv("QD_RANK_MODE");
+      return e ? atoi(e) : 0;  // MATCH only: ballots measured slower on c2/c3/c5
+    }();
+    static const uint32_t match_max = [] {
+      const char* e = getenv("QD_MATCH_MAX");
+      return e ? (uint32_t)atoi(e) : 8u;
+    }();
+    uint32_t nb = 0;
+    if (dig.lookup) {
+      nb = 8;
+    } else {
+      for (uint32_t i = 0; i < dig.n; ++i) nb += dig.bits[i];
+    }
+    if (in.fmt == kPK) nb = (uint32_t)__builtin_popcount(pk_mask);
+    a.dbits = std::min<uint32_t>(8, std::max<uint32_t>(1, nb));
+    a.rank_mode = rank_mode;
+    a.match_max = match_max;
+  }
   if (a.dbg & 2) {
     a.dbg_t = ws.get<unsigned long long>("dbg_t", 16);
     QD_CUDA(cudaMemsetAsync(a.dbg_t, 0, 128, c.st));
@@ -3729,8 +3846,21 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
     if (packed) {
       // prefix modes are constant within a run: when the row does not pack
       // otherwise, leave them out and restore them from the run
-      packed = make_pack(key, R, t.dims, &pack) ||
-               (run_start && make_pack(key, R, t.dims, &pack, g.prefix));
+      // QD_PACK_ORDER=1 (default): plain bit fields with the prefix restored
+      // from the run before a mixed-radix word (no division in the
+      // unpacking pass; c5 (0,2,1) 59.3 -> 58.6 ms); 0: mixed radix first
+      static const int pack_order = [] {
+        const char* e = getenv("QD_PACK_ORDER");
+        return e ? atoi(e) : 1;
+      }();
+      if (pack_order == 1)
+        packed = make_pack(key, R, t.dims, &pack, {}, false) ||
+                 (run_start && make_pack(key, R, t.dims, &pack, g.prefix, false)) ||
+                 make_pack(key, R, t.dims, &pack) ||
+                 (run_start && make_pack(key, R, t.dims, &pack, g.prefix));
+      else
+        packed = make_pack(key, R, t.dims, &pack) ||
+                 (run_start && make_pack(key, R, t.dims, &pack, g.prefix));
     }
     uint32_t* run_prefix = nullptr;
     if (packed && pack.n_imp) {
