@@ -1818,6 +1818,40 @@ __global__ void k_local_items(const uint32_t* list, const uint32_t* first_run,
   }
 }
 
+// Adjacent items (one per TL-row window of run starts) whose spans touch —
+// no large run between them — are merged while the span fits the staging
+// capacity: kMergeGroup consecutive items per thread, greedily, the merged
+// item written at its first slot and the absorbed ones emptied (n = 0; the
+// sorter skips them).  Items average a few hundred rows otherwise (c5's
+// (0,2,1): runs of ~66-900 rows), and k_local3's per-item cost (histogram
+// clears, bin offsets, barriers per digit pass) dominated its time.
+constexpr uint32_t kMergeGroup = 16;
+__global__ void k_merge_items(LocalItem* items, uint32_t n_items, const unsigned long long* n_dev,
+                              uint32_t cap) {
+  if (n_dev) n_items = (uint32_t)min(*n_dev, (unsigned long long)n_items);
+  const uint32_t ng = (n_items + kMergeGroup - 1) / kMergeGroup;
+  for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < ng; g += gridDim.x * blockDim.x) {
+    const uint32_t b = g * kMergeGroup, e = min(n_items, b + kMergeGroup);
+    uint32_t head = b;
+    LocalItem cur = items[b];
+    for (uint32_t i = b + 1; i < e; ++i) {
+      const LocalItem nx = items[i];
+      if (cur.r0 + cur.n == nx.r0 && cur.run_first + cur.nruns == nx.run_first &&
+          cur.n + nx.n <= cap) {
+        cur.n += nx.n;
+        cur.nruns += nx.nruns;
+        cur.maxrun = max(cur.maxrun, nx.maxrun);
+        items[i].n = 0u;
+      } else {
+        items[head] = cur;
+        head = i;
+        cur = nx;
+      }
+    }
+    items[head] = cur;
+  }
+}
+
 __global__ void __launch_bounds__(kLocal2Threads, 2) k_local2(Local2Args a) {
   const uint32_t NI = a.n_items_dev ? (uint32_t)min(*a.n_items_dev, (unsigned long long)a.n_items)
                                     : a.n_items;
@@ -1843,11 +1877,16 @@ __global__ void __launch_bounds__(kLocal2Threads, 2) k_local2(Local2Args a) {
   // advancer warp: draw the next item and start its bulk copies into buffer b
   auto advance = [&](uint32_t b) {
     uint32_t it = 0;
-    if (lane == 0) it = atomicAdd(a.item_counter, 1u);
-    it = __shfl_sync(0xFFFFFFFFu, it, 0);
+    LocalItem item{};
+    for (;;) {  // merged-away items are empty: skip them
+      if (lane == 0) it = atomicAdd(a.item_counter, 1u);
+      it = __shfl_sync(0xFFFFFFFFu, it, 0);
+      if (it >= NI) break;
+      item = a.items[it];
+      if (item.n) break;
+    }
     if (lane == 0) s_item[b] = it;
     if (it >= NI) return;
-    const LocalItem item = a.items[it];
     const Stage sc = make_stage(a.in_c + item.r0 * R, item.n * R * 4);
     const Stage sv = make_stage(a.in_v + item.r0, item.n * 8);
     if (lane == 0) {
@@ -2024,6 +2063,11 @@ __global__ void __launch_bounds__(kLocal2Threads, 2) k_local2(Local2Args a) {
 // before any row of it is written, so in == out is safe.  sort.cpp:80-134
 // (Alg. 2) on small buckets.
 // ---------------------------------------------------------------------------
+// k_local3 digits: up to 9 bits, so composite keys of up to 27 bits (21-bit
+// key + 64 runs) take 3 passes instead of 4
+constexpr int kLocalBitsMax = 9;
+constexpr int kLocalBins = 1 << kLocalBitsMax;
+
 struct Local3Layout {
   size_t cbuf, vbuf, c0, v0, k0, k1, i0, i1, seg, whist, start, wsum, total;
   __host__ __device__ Local3Layout(uint32_t cap, uint32_t rank, uint32_t key_bytes,
@@ -2038,20 +2082,20 @@ struct Local3Layout {
     i0 = o; o += align16(size_t(cap) * 2);
     i1 = o; o += align16(size_t(cap) * 2);
     seg = o; o += 2 * align16(size_t(cap + 2) * 2);
-    whist = o; o += align16(size_t(warps) * kBins * 2);
-    start = o; o += align16(kBins * 4);
+    whist = o; o += align16(size_t(warps) * kLocalBins * 2);
+    start = o; o += align16(kLocalBins * 4);
     wsum = o; o += align16(64 * 4);
     total = o;
   }
 };
 
-template <class K, int NT>
+template <class K, int NT, int RT = 0>
 __global__ void __launch_bounds__(NT, 1024 / NT) k_local3(Local2Args a) {
   const uint32_t NI = a.n_items_dev ? (uint32_t)min(*a.n_items_dev, (unsigned long long)a.n_items)
                                     : a.n_items;
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int NW = NT / 32;
-  const uint32_t R = a.rank;
+  const uint32_t R = RT ? (uint32_t)RT : a.rank;
   const Local3Layout L(a.cap, R, sizeof(K), NW);
   K* s_k0 = reinterpret_cast<K*>(smem + L.k0);
   K* s_k1 = reinterpret_cast<K*>(smem + L.k1);
@@ -2075,11 +2119,16 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_local3(Local2Args a) {
   // and copy its run starts (local u16 offsets) into the buffer's seg array
   auto advance = [&](uint32_t b) {
     uint32_t it = 0;
-    if (lane == 0) it = atomicAdd(a.item_counter, 1u);
-    it = __shfl_sync(0xFFFFFFFFu, it, 0);
+    LocalItem item{};
+    for (;;) {  // merged-away items are empty: skip them
+      if (lane == 0) it = atomicAdd(a.item_counter, 1u);
+      it = __shfl_sync(0xFFFFFFFFu, it, 0);
+      if (it >= NI) break;
+      item = a.items[it];
+      if (item.n) break;
+    }
     if (lane == 0) s_item[b] = it;
     if (it >= NI) return;
-    const LocalItem item = a.items[it];
     const Stage sc = make_stage(a.in_c + item.r0 * R, item.n * R * 4);
     const Stage sv = make_stage(a.in_v + item.r0, item.n * 8);
     if (lane == 0) {
@@ -2199,7 +2248,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_local3(Local2Args a) {
     }
     const uint32_t rbits = nsl > 1 ? 32u - __clz(nsl - 1) : 0u;
     const uint32_t tb = kb + rbits;
-    const uint32_t P = (tb + kRadixLog - 1) / kRadixLog;
+    const uint32_t P = (tb + kLocalBitsMax - 1) / kLocalBitsMax;
     const uint32_t per = P ? (tb + P - 1) / P : 0u;
     // warp stripes of whole 32-row rounds
     const uint32_t ipw = (((n + NW - 1) / NW) + 31u) & ~31u;
@@ -2249,16 +2298,17 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_local3(Local2Args a) {
     K* kn = s_k1;
     uint16_t* ic = s_i0;
     uint16_t* in_ = s_i1;
-    uint16_t* wh = s_whist + w * kBins;
+    uint16_t* wh = s_whist + w * kLocalBins;
     __syncwarp();
     for (uint32_t q = 0; q < P; ++q) {
       const uint32_t sh = q * per;
       const uint32_t dbits = min(per, tb - sh);
       const uint32_t mask = (1u << dbits) - 1u;
-      const uint32_t nb = 1u << dbits;  // bins of this digit (<= 256)
-      {
-        uint32_t* wz = reinterpret_cast<uint32_t*>(wh);
-        for (uint32_t k = lane; k < (nb + 1) / 2; k += 32) wz[k] = 0u;
+      const uint32_t nb = 1u << dbits;  // bins of this digit (<= kLocalBins)
+      if (lo < n) {  // warps past the item's rows keep no counts
+        // 16-byte clears (8 bins each); whist rows are 16-byte aligned
+        uint4* wz = reinterpret_cast<uint4*>(wh);
+        for (uint32_t k = lane; k < (nb + 7) / 8; k += 32) wz[k] = make_uint4(0u, 0u, 0u, 0u);
       }
       __syncwarp();
       uint32_t packed[kR];
@@ -2273,7 +2323,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_local3(Local2Args a) {
         __syncwarp();
         if (valid && (peers & below) == 0u) wh[d] = (uint16_t)(c + __popc(peers));
         __syncwarp();
-        packed[r] = ((c + __popc(peers & below)) << 8) | (d & 0xFFu);
+        packed[r] = ((c + __popc(peers & below)) << kLocalBitsMax) | (d & (kLocalBins - 1u));
       }
       __syncthreads();
       // bin pairs (2t, 2t+1): warp-exclusive offsets with 16-bit SIMD adds,
@@ -2284,10 +2334,12 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_local3(Local2Args a) {
         if (threadIdx.x < npair) {
           uint32_t* wp = reinterpret_cast<uint32_t*>(s_whist) + threadIdx.x;
           uint32_t run2 = 0;
+          const uint32_t nwa = (n + ipw - 1) / ipw;  // warps holding rows
 #pragma unroll
           for (int x = 0; x < NW; ++x) {
-            const uint32_t c = wp[x * (kBins / 2)];
-            wp[x * (kBins / 2)] = run2;
+            if ((uint32_t)x >= nwa) break;
+            const uint32_t c = wp[x * (kLocalBins / 2)];
+            wp[x * (kLocalBins / 2)] = run2;
             run2 = __vadd2(run2, c);
           }
           lo_cnt = run2 & 0xFFFFu;
@@ -2316,8 +2368,8 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_local3(Local2Args a) {
         const uint32_t p = lo + r * 32 + lane;
         if (lo + r * 32 >= hi) break;
         if (p < hi) {
-          const uint32_t d = packed[r] & 0xFFu;
-          const uint32_t slot = s_start[d] + wh[d] + (packed[r] >> 8);
+          const uint32_t d = packed[r] & (kLocalBins - 1u);
+          const uint32_t slot = s_start[d] + wh[d] + (packed[r] >> kLocalBitsMax);
           kn[slot] = kc[p];
           in_[slot] = ic[p];
         }
@@ -2327,12 +2379,24 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_local3(Local2Args a) {
       uint16_t* ti = ic; ic = in_; in_ = ti;
     }
     if (P == 0) __syncthreads();
-    for (uint32_t j = threadIdx.x; j < n; j += NT) {
-      const uint32_t i = ic[j];
-      const unsigned long long dst = item.r0 + j;
-      uint32_t* o = a.out_c + dst * R;
-      for (uint32_t m = 0; m < R; ++m) __stcs(o + m, s_c[i * R + m]);
-      __stcs(a.out_v + dst, s_v[i]);
+    if (RT) {
+      // the item's output rows are contiguous: coordinate WORDS one per
+      // thread (coalesced 128-byte warp stores), word w = row w / RT, mode
+      // w % RT of the sorted order
+      uint32_t* oc = a.out_c + item.r0 * RT;
+      for (uint32_t wd = threadIdx.x; wd < n * RT; wd += NT) {
+        const uint32_t j = wd / RT, m = wd - j * RT;
+        __stcs(oc + wd, s_c[(uint32_t)ic[j] * RT + m]);
+      }
+      for (uint32_t j = threadIdx.x; j < n; j += NT) __stcs(a.out_v + item.r0 + j, s_v[ic[j]]);
+    } else {
+      for (uint32_t j = threadIdx.x; j < n; j += NT) {
+        const uint32_t i = ic[j];
+        const unsigned long long dst = item.r0 + j;
+        uint32_t* o = a.out_c + dst * R;
+        for (uint32_t m = 0; m < R; ++m) __stcs(o + m, s_c[i * R + m]);
+        __stcs(a.out_v + dst, s_v[i]);
+      }
     }
     __syncthreads();  // buffer b, its seg array and the scratch are free again
   }
@@ -3118,6 +3182,10 @@ Workspace* workspace_create(int device) {
   allow_smem(reinterpret_cast<const void*>(k_local2));
   allow_smem(reinterpret_cast<const void*>(k_local3<uint32_t, 512>));
   allow_smem(reinterpret_cast<const void*>(k_local3<unsigned long long, 512>));
+  allow_smem(reinterpret_cast<const void*>(k_local3<uint32_t, 512, 3>));
+  allow_smem(reinterpret_cast<const void*>(k_local3<unsigned long long, 512, 3>));
+  allow_smem(reinterpret_cast<const void*>(k_local3<uint32_t, 512, 4>));
+  allow_smem(reinterpret_cast<const void*>(k_local3<unsigned long long, 512, 4>));
   allow_smem(reinterpret_cast<const void*>(k_local3<uint32_t, 256>));
   allow_smem(reinterpret_cast<const void*>(k_local3<unsigned long long, 256>));
   ws->smem_optin = optin - 1024;  // dynamic budget below the static usage
@@ -3931,6 +3999,18 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
                                          lat_counts ? lat_counts + 2 : nullptr, local_maxrun,
                                          items);
     c.launched(kSegK);
+    static const bool merge_items = [] {
+      const char* e = getenv("QD_MERGE_ITEMS");
+      return !(e && atoi(e) == 0);
+    }();
+    if (local_v == 3 && merge_items) {
+      const uint32_t ng = (uint32_t)((local_chunks + kMergeGroup - 1) / kMergeGroup);
+      c.pre();
+      k_merge_items<<<(uint32_t)std::min<uint64_t>((ng + kThreads - 1) / kThreads + 1, ws.num_sms * 8),
+                      kThreads, 0, c.st>>>(items, (uint32_t)local_chunks,
+                                           lat_counts ? lat_counts + 2 : nullptr, 2 * TL);
+      c.launched(kSegK);
+    }
     Local2Args la{};
     la.in_c = src_c;
     la.in_v = src_v;
@@ -3961,6 +4041,8 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
     const LocalFn fn =
         local_v != 3 ? k_local2
         : nt == 256 ? (kbytes == 4 ? k_local3<uint32_t, 256> : k_local3<unsigned long long, 256>)
+        : R == 3    ? (kbytes == 4 ? k_local3<uint32_t, 512, 3> : k_local3<unsigned long long, 512, 3>)
+        : R == 4    ? (kbytes == 4 ? k_local3<uint32_t, 512, 4> : k_local3<unsigned long long, 512, 4>)
                     : (kbytes == 4 ? k_local3<uint32_t, 512> : k_local3<unsigned long long, 512>);
     const size_t smem = local_v == 3 ? Local3Layout(2 * TL, R, kbytes, nt / 32).total
                                      : Local2Layout(2 * TL, R).total;
@@ -3971,6 +4053,36 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
     c.pre();
     fn<<<grid, nt, smem, c.st>>>(la);
     c.launched(kLocalK);
+    if (getenv("QD_LOCAL_STATS") && !c.lat) {  // debug: the small-run items of this call
+      std::vector<LocalItem> h(local_chunks);
+      QD_CUDA(cudaMemcpyAsync(h.data(), items, local_chunks * sizeof(LocalItem),
+                              cudaMemcpyDeviceToHost, c.st));
+      QD_CUDA(cudaStreamSynchronize(c.st));
+      uint64_t ne = 0, rows = 0, runs = 0, pcnt[8] = {0}, prow[8] = {0}, small32 = 0;
+      for (const LocalItem& it : h) {
+        if (!it.n) continue;
+        ++ne;
+        rows += it.n;
+        runs += it.nruns;
+        const uint32_t rb = it.nruns > 1 ? 32 - __builtin_clz(it.nruns - 1) : 0;
+        const uint32_t P = (bits + rb + kLocalBitsMax - 1) / kLocalBitsMax;
+        if (it.maxrun <= 32) {
+          ++small32;
+        } else {
+          ++pcnt[std::min<uint32_t>(P, 7)];
+          prow[std::min<uint32_t>(P, 7)] += it.n;
+        }
+      }
+      fprintf(stderr, "local: TL %u items %llu non-empty %llu rows %llu runs %llu (avg item %.0f rows, "
+              "%.1f runs) row-parallel items %llu; P:", TL, (unsigned long long)local_chunks,
+              (unsigned long long)ne, (unsigned long long)rows, (unsigned long long)runs,
+              ne ? (double)rows / ne : 0.0, ne ? (double)runs / ne : 0.0,
+              (unsigned long long)small32);
+      for (int q = 0; q < 8; ++q)
+        if (pcnt[q]) fprintf(stderr, " %d:%llu items/%llu rows", q, (unsigned long long)pcnt[q],
+                             (unsigned long long)prow[q]);
+      fprintf(stderr, "\n");
+    }
   } else if (small_runs && local_chunks) {
     // small runs: chunks of runs starting in [c*TL, (c+1)*TL), only the
     // chunks that hold some (compact list); after the passes, whose
