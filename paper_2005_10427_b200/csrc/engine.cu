@@ -26,6 +26,7 @@
 //
 // Rows are always moved whole (the reference's scatter_rows), so there is no
 // separate gather.  No CPU fallback exists: every path here is a kernel.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -1523,6 +1524,298 @@ __global__ void __launch_bounds__(kSortThreads, QD_SCATTER_CTAS * 512 / kSortThr
 }
 
 // ---------------------------------------------------------------------------
+// k_small: the latency regime in ONE cooperative kernel.  A single-group plan
+// (prefix P, keys K; every plan of configs 1 and 4) on a tensor of at most
+// kSmallRows rows is a stable sort by the composite key (P, K) whenever the
+// rows are non-decreasing in P — the group's runs of equal P are then
+// contiguous and in P order, so sorting within them (Alg. 2, sort.cpp:80-134)
+// equals sorting by (P, K).  The kernel checks exactly that (and that every
+// composite coordinate is below its dimension); if either fails it raises a
+// flag and the host reruns the call on the general path, which reproduces the
+// reference's semantics (and errors) for any input.
+//
+// Elements {composite key, source row} (16 bytes) go through ceil(bits/8)
+// stable LSD counting passes, L2-resident at these sizes; grid-wide barriers
+// replace kernel boundaries.  Per pass: (1) one CTA per bin scans that bin's
+// per-CTA counts (the (bin, CTA) order = parallel.cpp:88-100's (key, worker)
+// order), (2) every CTA scatters its own contiguous chunk tile by tile (warp
+// MATCH.ANY ranking, per-warp counts, bin offsets in shared memory), (3) every
+// CTA counts the next digit over its chunk of the output.  The last step
+// gathers the AoS rows by source row (random reads hit L2).
+// ---------------------------------------------------------------------------
+constexpr int kSmallThreads = 512;
+constexpr int kSmallWarps = kSmallThreads / 32;
+constexpr uint32_t kSmallTile = 4096;                      // elements per ranked tile (dynamic smem)
+constexpr int kSmallRounds = kSmallTile / kSmallThreads;  // 32-row rounds per warp
+constexpr uint64_t kSmallRows = 1ull << 22;
+constexpr int kSmallMaxPasses = 8;
+
+constexpr size_t kSmallSmem = kSmallTile * 20 + kSmallWarps * kBins * 2 + 3 * kBins * 4 + 64 * 4 + 16;
+
+struct SmallArgs {
+  const uint32_t* in_c;
+  const double* in_v;
+  uint32_t* out_c;
+  double* out_v;
+  uint32_t rank;
+  uint64_t nnz;
+  uint32_t nc, npre;  // composite modes (prefix first), number of prefix modes
+  uint8_t cmode[kMaxKeys], csh[kMaxKeys];
+  uint32_t cdim[kMaxKeys];
+  uint32_t P;
+  uint32_t dlo[kSmallMaxPasses], dmask[kSmallMaxPasses];
+  ulonglong2* ea;
+  ulonglong2* eb;
+  uint32_t* hist;   // [kBins][gridDim.x]
+  uint32_t* offs;   // [kBins][gridDim.x]
+  uint32_t* total;  // [kBins]
+  ErrBlock* err;
+  unsigned long long* dbg;  // QD_SMALL_DBG: %globaltimer at phase ends (CTA 0, thread 0)
+  int rank_mode;            // 0: MATCH.ANY peers, 1: ballots (QD_SMALL_RANK)
+  uint32_t dbits[kSmallMaxPasses];
+};
+
+__device__ __forceinline__ void small_mark(const SmallArgs& a, int k) {
+  if (a.dbg && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.dbg[k] = t;
+  }
+}
+
+__global__ void __launch_bounds__(kSmallThreads, 2) k_small(SmallArgs a) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) unsigned char smem[];
+  ulonglong2* s_el = reinterpret_cast<ulonglong2*>(smem);                    // [kSmallTile]
+  uint32_t* s_srt = reinterpret_cast<uint32_t*>(s_el + kSmallTile);         // [kSmallTile]
+  uint16_t* s_wh = reinterpret_cast<uint16_t*>(s_srt + kSmallTile);         // [warps][kBins]
+  uint32_t* s_cur = reinterpret_cast<uint32_t*>(s_wh + kSmallWarps * kBins);
+  uint32_t* s_tstart = s_cur + kBins;
+  uint32_t* s_h = s_tstart + kBins;
+  uint32_t* s_tmp = s_h + kBins;  // [64]
+
+  const uint32_t G = gridDim.x, cta = blockIdx.x, t = threadIdx.x;
+  const uint32_t lane = t & 31, w = t >> 5;
+  const uint64_t N = a.nnz;
+  const uint64_t lo = N * cta / G, hi = N * (cta + 1) / G;
+  const uint32_t R = a.rank;
+  small_mark(a, 0);
+  unsigned long long* s_bar = reinterpret_cast<unsigned long long*>(s_tmp + 64);
+  uint32_t phase = 0;
+  // the first tile of this CTA's chunk of `src`, by TMA (issued as soon as
+  // the data is final, so the copy overlaps the barriers and scans after it)
+  auto issue_first = [&](const ulonglong2* src) {
+    if (threadIdx.x == 0 && lo < hi) {
+      const uint32_t n0 = (uint32_t)min((unsigned long long)kSmallTile, (unsigned long long)(hi - lo));
+      mbar_expect_tx(s_bar, n0 * 16u);
+      bulk_g2s(s_el, src + lo, n0 * 16u, s_bar);
+    }
+  };
+  if (threadIdx.x == 0) {
+    mbar_init(s_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+
+  // elements in input order + the first digit's counts of this chunk
+  for (uint32_t b = t; b < kBins; b += kSmallThreads) s_h[b] = 0u;
+  __syncthreads();
+  for (uint64_t i = lo + t; i < hi; i += kSmallThreads) {
+    const uint32_t* row = a.in_c + i * R;
+    unsigned long long key = 0;
+    bool bad = false;
+    for (uint32_t j = 0; j < a.nc; ++j) {
+      const uint32_t x = row[a.cmode[j]];
+      bad |= x >= a.cdim[j];
+      key |= (unsigned long long)x << a.csh[j];
+    }
+    if (a.npre && i > 0) {  // rows non-decreasing in the prefix
+      const uint32_t* pr = row - R;
+      for (uint32_t j = 0; j < a.npre; ++j) {
+        const uint32_t x = row[a.cmode[j]], y = pr[a.cmode[j]];
+        if (x != y) {
+          bad |= x < y;
+          break;
+        }
+      }
+    }
+    if (bad) atomicOr(&a.err->flags, 8u);
+    // the final gather reads the values at random: bring them into L2 now
+    asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(a.in_v + i));
+    a.ea[i] = make_ulonglong2(key, i);
+    atomicAdd(&s_h[(uint32_t)(key >> a.dlo[0]) & a.dmask[0]], 1u);
+  }
+  __syncthreads();
+  for (uint32_t b = t; b < kBins; b += kSmallThreads) a.hist[(size_t)b * G + cta] = s_h[b];
+  small_mark(a, 1);
+  grid.sync();
+  small_mark(a, 2);
+  // (generic-proxy writes of ea by other CTAs, ordered by the grid barrier,
+  // before this CTA's async-proxy reads)
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+  issue_first(a.ea);
+
+  const unsigned below = (1u << lane) - 1u;
+  for (uint32_t q = 0; q < a.P; ++q) {
+    const ulonglong2* src = (q & 1u) ? a.eb : a.ea;
+    ulonglong2* dst = (q & 1u) ? a.ea : a.eb;
+    const uint32_t dlo = a.dlo[q], dmask = a.dmask[q];
+    // (1) one CTA per bin: exclusive scan of the bin's counts over the CTAs
+    for (uint32_t b = cta; b < kBins; b += G) {
+      const uint32_t v = t < G ? a.hist[(size_t)b * G + t] : 0u;
+      uint32_t tot = 0;
+      const uint32_t ex = block_excl_scan<kSmallThreads>(v, s_tmp, &tot);
+      if (t < G) a.offs[(size_t)b * G + t] = ex;
+      if (t == 0) a.total[b] = tot;
+    }
+    small_mark(a, 3 + 6 * q);
+    grid.sync();
+    small_mark(a, 4 + 6 * q);
+    // (2) this CTA's cursor per bin, then its chunk tile by tile
+    {
+      const uint32_t v = t < kBins ? a.total[t] : 0u;
+      const uint32_t ex = block_excl_scan<kSmallThreads>(v, s_tmp);
+      if (t < kBins) s_cur[t] = ex + a.offs[(size_t)t * G + cta];
+    }
+    for (uint64_t base = lo; base < hi; base += kSmallTile) {
+      const uint32_t n = (uint32_t)min((unsigned long long)kSmallTile, (unsigned long long)(hi - base));
+      if (base == lo) {  // issued after the previous pass's barrier
+        mbar_wait(s_bar, phase);
+        phase ^= 1u;
+        if (q == 0) small_mark(a, 50);
+      } else {
+        for (uint32_t k = t; k < n; k += kSmallThreads) s_el[k] = src[base + k];
+      }
+      uint16_t* wh = s_wh + w * kBins;
+      for (uint32_t k = lane; k < kBins / 8; k += 32)
+        reinterpret_cast<uint4*>(wh)[k] = make_uint4(0u, 0u, 0u, 0u);
+      __syncthreads();
+      const uint32_t ipw = (((n + kSmallWarps - 1) / kSmallWarps) + 31u) & ~31u;
+      const uint32_t rlo = w * ipw, rhi = min(n, rlo + ipw);
+      uint32_t packed[kSmallRounds];
+#pragma unroll
+      for (int r = 0; r < kSmallRounds; ++r) {
+        const uint32_t p = rlo + r * 32 + lane;
+        if (rlo + r * 32 >= rhi) break;  // warp-uniform
+        const bool valid = p < rhi;
+        const uint32_t d = valid ? (uint32_t)(s_el[p].x >> dlo) & dmask : 0xFFFFFFFFu;
+        const unsigned vm = __ballot_sync(0xFFFFFFFFu, valid);
+        const unsigned peers = a.rank_mode ? (ballot_peers(d, vm, a.dbits[q]) | (valid ? 0u : 1u << lane))
+                                           : __match_any_sync(0xFFFFFFFFu, d);
+        const uint32_t c0 = valid ? wh[d] : 0u;
+        __syncwarp();
+        if (valid && (peers & below) == 0u) wh[d] = (uint16_t)(c0 + __popc(peers));
+        __syncwarp();
+        packed[r] = ((c0 + __popc(peers & below)) << 8) | (d & 0xFFu);
+      }
+      __syncthreads();
+      if (q == 0 && base == lo) small_mark(a, 51);
+      // warp-exclusive offsets per bin and the bins' starts in the tile
+      uint32_t cnt = 0;
+      {
+        uint32_t incl = 0;
+        if (t < kBins) {
+#pragma unroll
+          for (int x = 0; x < kSmallWarps; ++x) {
+            const uint32_t cx = s_wh[x * kBins + t];
+            s_wh[x * kBins + t] = (uint16_t)cnt;
+            cnt += cx;
+          }
+        }
+        const uint32_t ex = block_excl_scan<kSmallThreads>(t < kBins ? cnt : 0u, s_tmp);
+        (void)incl;
+        if (t < kBins) s_tstart[t] = ex;
+      }
+      __syncthreads();
+      if (q == 0 && base == lo) small_mark(a, 52);
+#pragma unroll
+      for (int r = 0; r < kSmallRounds; ++r) {
+        const uint32_t p = rlo + r * 32 + lane;
+        if (rlo + r * 32 >= rhi) break;
+        if (p < rhi) {
+          const uint32_t d = packed[r] & 0xFFu;
+          s_srt[s_tstart[d] + wh[d] + (packed[r] >> 8)] = (p << 8) | d;
+        }
+      }
+      __syncthreads();
+      if (q == 0 && base == lo) small_mark(a, 53);
+      for (uint32_t j = t; j < n; j += kSmallThreads) {
+        const uint32_t x = s_srt[j];
+        const uint32_t d = x & 0xFFu;
+        dst[s_cur[d] + (j - s_tstart[d])] = s_el[x >> 8];
+      }
+      __syncthreads();
+      if (q == 0 && base == lo) small_mark(a, 54);
+      if (t < kBins) s_cur[t] += cnt;
+      // (the next tile's first barrier orders this before any s_cur read)
+    }
+    small_mark(a, 5 + 6 * q);
+    grid.sync();
+    small_mark(a, 6 + 6 * q);
+    if (q + 1 < a.P) {
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      issue_first(dst);
+    }
+    // (3) the next digit's counts over this CTA's chunk of the output
+    if (q + 1 < a.P) {
+      const uint32_t nlo = a.dlo[q + 1], nmask = a.dmask[q + 1];
+      for (uint32_t b = t; b < kBins; b += kSmallThreads) s_h[b] = 0u;
+      __syncthreads();
+      for (uint64_t i = lo + t; i < hi; i += kSmallThreads)
+        atomicAdd(&s_h[(uint32_t)(dst[i].x >> nlo) & nmask], 1u);
+      __syncthreads();
+      for (uint32_t b = t; b < kBins; b += kSmallThreads) a.hist[(size_t)b * G + cta] = s_h[b];
+      small_mark(a, 7 + 6 * q);
+      grid.sync();
+      small_mark(a, 8 + 6 * q);
+    }
+  }
+  // rows in sorted order, gathered by source row
+  const ulonglong2* fin = (a.P & 1u) ? a.eb : a.ea;
+  // four rows per thread in flight (independent loads before any store)
+  constexpr int kG = 4;
+  for (uint64_t i0 = lo + t; i0 < hi; i0 += (uint64_t)kG * kSmallThreads) {
+    unsigned long long r[kG];
+#pragma unroll
+    for (int u = 0; u < kG; ++u) {
+      const uint64_t i = i0 + (uint64_t)u * kSmallThreads;
+      r[u] = i < hi ? fin[i].y : 0ull;
+    }
+    double v[kG];
+#pragma unroll
+    for (int u = 0; u < kG; ++u) v[u] = __ldg(a.in_v + r[u]);
+    if (R == 3) {
+      uint32_t x[kG][3];
+#pragma unroll
+      for (int u = 0; u < kG; ++u)
+#pragma unroll
+        for (int m = 0; m < 3; ++m) x[u][m] = __ldg(a.in_c + r[u] * 3 + m);
+#pragma unroll
+      for (int u = 0; u < kG; ++u) {
+        const uint64_t i = i0 + (uint64_t)u * kSmallThreads;
+        if (i < hi) {
+#pragma unroll
+          for (int m = 0; m < 3; ++m) a.out_c[i * 3 + m] = x[u][m];
+          a.out_v[i] = v[u];
+        }
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < kG; ++u) {
+        const uint64_t i = i0 + (uint64_t)u * kSmallThreads;
+        if (i < hi) {
+          const uint32_t* sr = a.in_c + r[u] * R;
+          uint32_t* o = a.out_c + i * R;
+          for (uint32_t m = 0; m < R; ++m) o[m] = sr[m];
+          a.out_v[i] = v[u];
+        }
+      }
+    }
+  }
+  small_mark(a, 63);
+}
+
+// ---------------------------------------------------------------------------
 // k_local: small runs, fully sorted inside one CTA
 // ---------------------------------------------------------------------------
 struct LocalLayout {
@@ -2996,8 +3289,10 @@ struct Workspace {
   std::map<std::string, DevBuf> bufs;
   uint64_t launches = 0;
   ErrBlock* h_err = nullptr;  // pinned
+  ErrBlock* h_err_init = nullptr;  // pinned, the reset value (flags 0, rowmode ~0)
   uint64_t* h_small = nullptr;  // pinned scratch for small D2H reads
   bool allow_pack = true;  // packed intermediates (cleared for a lossy-pack redo)
+  bool allow_small = true;  // k_small for latency-mode single-group calls (cleared for a redo)
   // asynchronous host-buffer transposes (qd_transpose_inplace_async): the
   // caller's thread enqueues each call's host->device copy (s_in) into one of
   // two device slots and hands the device work to a worker thread, which runs
@@ -3164,6 +3459,9 @@ Workspace* workspace_create(int device) {
   QD_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
   ws->smem_optin = optin;
   QD_CUDA(cudaMallocHost(&ws->h_err, sizeof(ErrBlock)));
+  QD_CUDA(cudaMallocHost(&ws->h_err_init, sizeof(ErrBlock)));
+  std::memset(ws->h_err_init, 0, sizeof(ErrBlock));
+  ws->h_err_init->rowmode = ~0ull;
   QD_CUDA(cudaMallocHost(&ws->h_small, 512 * sizeof(uint64_t)));
   auto allow_smem = [&](const void* fn) {
     cudaFuncAttributes fa{};
@@ -3182,6 +3480,7 @@ Workspace* workspace_create(int device) {
   allow_smem(reinterpret_cast<const void*>(k_local2));
   allow_smem(reinterpret_cast<const void*>(k_local3<uint32_t, 512>));
   allow_smem(reinterpret_cast<const void*>(k_local3<unsigned long long, 512>));
+  allow_smem(reinterpret_cast<const void*>(k_small));
   allow_smem(reinterpret_cast<const void*>(k_local3<uint32_t, 512, 3>));
   allow_smem(reinterpret_cast<const void*>(k_local3<unsigned long long, 512, 3>));
   allow_smem(reinterpret_cast<const void*>(k_local3<uint32_t, 512, 4>));
@@ -3217,6 +3516,7 @@ void workspace_destroy(Workspace* ws) {
   for (auto& kv : ws->bufs)
     if (kv.second.p) cudaFree(kv.second.p);
   if (ws->h_err) cudaFreeHost(ws->h_err);
+  if (ws->h_err_init) cudaFreeHost(ws->h_err_init);
   if (ws->h_small) cudaFreeHost(ws->h_small);
   for (auto e : ws->ev_pool) cudaEventDestroy(e);
   for (auto& g : ws->graphs)
@@ -3289,6 +3589,8 @@ struct Ctx {
   // kernels bound their grid-stride loops by them; buffers are sized for the
   // worst case; the launch sequence is then capturable as a CUDA graph
   bool lat = false;
+  bool small = false;  // the whole call is one k_small launch (latency mode)
+  SmallArgs sa{};
   void pre() {
     if (ws.prof) {
       pending = ws.event();
@@ -4293,8 +4595,11 @@ void exec_group(Ctx& c, const TensorView& t, const uint32_t* src_c, const double
 
 // Synchronise, fold profiling records, and throw the first error found.
 // Returns the error flags (bit2 = a coordinate did not pack losslessly).
-static unsigned check_errors(Ctx& c) {
-  QD_CUDA(cudaMemcpyAsync(c.ws.h_err, c.err, sizeof(ErrBlock), cudaMemcpyDeviceToHost, c.st));
+// copy = false: the error block's device->host copy is already enqueued
+// (it is the last node of a latency-mode graph)
+static unsigned check_errors(Ctx& c, bool copy = true) {
+  if (copy)
+    QD_CUDA(cudaMemcpyAsync(c.ws.h_err, c.err, sizeof(ErrBlock), cudaMemcpyDeviceToHost, c.st));
   QD_CUDA(cudaStreamSynchronize(c.st));
   const ErrBlock e = *c.ws.h_err;
   c.resolve(e);
@@ -4310,16 +4615,111 @@ static unsigned check_errors(Ctx& c) {
   return e.flags;
 }
 
-static Ctx make_ctx(Workspace& ws, void* stream) {
+// the call's error block and chunk counters back to their initial values
+// (stream-ordered; part of a latency-mode graph when captured)
+static void reset_ctx(Ctx& c, bool counters = true) {
+  QD_CUDA(cudaMemcpyAsync(c.err, c.ws.h_err_init, sizeof(ErrBlock), cudaMemcpyHostToDevice, c.st));
+  if (counters) QD_CUDA(cudaMemsetAsync(c.counters, 0, kCounters * 4, c.st));
+}
+
+static Ctx make_ctx(Workspace& ws, void* stream, bool reset = true) {
   QD_CUDA(cudaSetDevice(ws.device));
   Ctx c{ws, static_cast<cudaStream_t>(stream), nullptr, nullptr};
   c.err = ws.get<ErrBlock>("err", 1);
   c.counters = ws.get<uint32_t>("counters", kCounters);
-  std::memset(ws.h_err, 0, sizeof(ErrBlock));
-  ws.h_err->rowmode = ~0ull;
-  QD_CUDA(cudaMemcpyAsync(c.err, ws.h_err, sizeof(ErrBlock), cudaMemcpyHostToDevice, c.st));
-  QD_CUDA(cudaMemsetAsync(c.counters, 0, kCounters * 4, c.st));
+  if (reset) reset_ctx(c);
   return c;
+}
+
+// k_small's plan for a call, or false: one range-checked group whose
+// composite key (prefix modes, then keys; widths from the dimensions) fits
+// 64 bits in at most kSmallMaxPasses 8-bit digits.
+static bool small_plan(const TensorView& t, const std::vector<Group>& groups, SmallArgs* a) {
+  if (groups.size() != 1 || !groups[0].check_range) return false;
+  const Group& g = groups[0];
+  std::vector<uint32_t> C(g.prefix);
+  C.insert(C.end(), g.keys.begin(), g.keys.end());
+  if (C.empty() || C.size() > (size_t)kMaxKeys) return false;
+  uint32_t bits = 0;
+  for (uint32_t m : C) bits += ceil_log2(t.dims[m]);
+  if (bits == 0 || bits > 64) return false;
+  SmallArgs x{};
+  x.rank = t.rank;
+  x.nnz = t.nnz;
+  x.nc = (uint32_t)C.size();
+  x.npre = (uint32_t)g.prefix.size();
+  uint32_t sh = bits;
+  for (size_t j = 0; j < C.size(); ++j) {
+    sh -= ceil_log2(t.dims[C[j]]);
+    x.cmode[j] = (uint8_t)C[j];
+    x.csh[j] = (uint8_t)sh;
+    x.cdim[j] = t.dims[C[j]];
+  }
+  x.P = (bits + kRadixLog - 1) / kRadixLog;
+  if (x.P > (uint32_t)kSmallMaxPasses) return false;
+  const uint32_t per = (bits + x.P - 1) / x.P;
+  for (uint32_t q = 0; q < x.P; ++q) {
+    x.dlo[q] = q * per;
+    x.dmask[q] = (1u << std::min(per, bits - q * per)) - 1u;
+    x.dbits[q] = std::min(per, bits - q * per);
+  }
+  static const int rank_mode = [] {
+    const char* e = getenv("QD_SMALL_RANK");
+    return e ? atoi(e) : 1;
+  }();
+  x.rank_mode = rank_mode;
+  *a = x;
+  return true;
+}
+
+static void launch_small(Ctx& c, const TensorView& t, const uint32_t* d_c_in, const double* d_v_in,
+                         uint32_t* d_c_out, double* d_v_out) {
+  Workspace& ws = c.ws;
+  const uint64_t N = t.nnz;
+  int per_sm = 0;
+  QD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_small, kSmallThreads, kSmallSmem));
+  uint64_t gmax = (uint64_t)std::max(1, per_sm) * ws.num_sms;
+  if (const char* e = getenv("QD_SMALL_G")) gmax = std::min<uint64_t>(gmax, strtoull(e, nullptr, 10));
+  const uint32_t G = (uint32_t)std::max<uint64_t>(
+      1, std::min<uint64_t>({gmax, (N + 1023) / 1024, (uint64_t)kSmallThreads}));
+  SmallArgs a = c.sa;
+  a.in_c = d_c_in;
+  a.in_v = d_v_in;
+  a.out_c = d_c_out;
+  a.out_v = d_v_out;
+  a.ea = ws.get<ulonglong2>("small_ea", N);
+  a.eb = ws.get<ulonglong2>("small_eb", N);
+  a.hist = ws.get<uint32_t>("small_hist", (size_t)kBins * G);
+  a.offs = ws.get<uint32_t>("small_offs", (size_t)kBins * G);
+  a.total = ws.get<uint32_t>("small_total", kBins);
+  a.err = c.err;
+  static const bool dbg = getenv("QD_SMALL_DBG") != nullptr;
+  if (dbg) {
+    a.dbg = ws.get<unsigned long long>("small_dbg", 64);
+    QD_CUDA(cudaMemsetAsync(a.dbg, 0, 64 * 8, c.st));
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(G);
+  cfg.blockDim = dim3(kSmallThreads);
+  cfg.dynamicSmemBytes = kSmallSmem;
+  cfg.stream = c.st;
+  cudaLaunchAttribute attr{};
+  attr.id = cudaLaunchAttributeCooperative;
+  attr.val.cooperative = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  c.pre();
+  QD_CUDA(cudaLaunchKernelEx(&cfg, k_small, a));
+  c.launched(kSweep);
+  if (dbg) {
+    unsigned long long h[64];
+    QD_CUDA(cudaMemcpyAsync(h, a.dbg, sizeof(h), cudaMemcpyDeviceToHost, c.st));
+    QD_CUDA(cudaStreamSynchronize(c.st));
+    fprintf(stderr, "k_small G=%u P=%u N=%llu (us from start):", G, a.P, (unsigned long long)N);
+    for (int k = 1; k < 64; ++k)
+      if (h[k]) fprintf(stderr, " %d:%.1f", k, (h[k] - h[0]) / 1e3);
+    fprintf(stderr, "\n");
+  }
 }
 
 // Every launch of a call (no final synchronisation): the part a latency-mode
@@ -4350,7 +4750,9 @@ static void launch_groups(Ctx& c, const TensorView& t, const uint32_t* d_c_in,
     c.launched(kOtherK);
   }
   const size_t G = groups.size();
-  if (G == 0 || N == 0) {
+  if (c.small) {
+    launch_small(c, t, d_c_in, d_v_in, d_c_out, d_v_out);
+  } else if (G == 0 || N == 0) {
     if (N && d_c_out != d_c_in) {
       QD_CUDA(cudaMemcpyAsync(d_c_out, d_c_in, N * R * 4, cudaMemcpyDeviceToDevice, c.st));
       QD_CUDA(cudaMemcpyAsync(d_v_out, d_v_in, N * 8, cudaMemcpyDeviceToDevice, c.st));
@@ -4416,6 +4818,7 @@ static std::string graph_key(const Workspace& ws, const TensorView& t, const voi
   put(reinterpret_cast<uintptr_t>(d));
   put(verify);
   put(ws.allow_pack);
+  put(ws.allow_small);
   for (const Group& g : groups) {
     put(0xFFFF0000ull | g.prefix.size());
     for (uint32_t m : g.prefix) put(m);
@@ -4431,7 +4834,7 @@ static void run_groups_once(Workspace& ws, const TensorView& t, const uint32_t* 
                             const std::vector<Group>& groups, bool verify_input,
                             uint64_t* d_boundaries, uint64_t* n_boundaries,
                             uint32_t boundary_mode, void* stream, unsigned* flags) {
-  Ctx c = make_ctx(ws, stream);
+  Ctx c = make_ctx(ws, stream, false);  // reset below: eagerly, or inside the graph
   const uint64_t N = t.nnz;
   c.nnz = N;
   c.rank = t.rank;
@@ -4450,6 +4853,18 @@ static void run_groups_once(Workspace& ws, const TensorView& t, const uint32_t* 
   bool lat = lat_on && !local_v1 && N > 0 && N <= kLatRows && !d_boundaries;
   for (const Group& g : groups) lat &= g.check_range;
   c.lat = lat;
+  // one cooperative kernel for the whole call (QD_SMALL=0 disables it)
+  static const bool small_on = [] {
+    const char* e = getenv("QD_SMALL");
+    return !(e && atoi(e) == 0);
+  }();
+  if (lat && small_on && ws.allow_small && N >= 2 && N <= kSmallRows && small_plan(t, groups, &c.sa)) {
+    const uintptr_t ib = reinterpret_cast<uintptr_t>(d_c_in), ob = reinterpret_cast<uintptr_t>(d_c_out);
+    const uintptr_t vb = reinterpret_cast<uintptr_t>(d_v_in), wb = reinterpret_cast<uintptr_t>(d_v_out);
+    const uint64_t cb = N * t.rank * 4, db = N * 8;
+    // the gather reads the input while writing the output: no overlap
+    c.small = (ib + cb <= ob || ob + cb <= ib) && (vb + db <= wb || wb + db <= vb);
+  }
   auto eager = [&] {
     launch_groups(c, t, d_c_in, d_v_in, d_c_out, d_v_out, groups, verify_input, d_boundaries,
                   n_boundaries, boundary_mode);
@@ -4463,45 +4878,58 @@ static void run_groups_once(Workspace& ws, const TensorView& t, const uint32_t* 
       cudaGraphExecDestroy(e.exec);
       e = Workspace::GraphEntry{};
     }
+    // a graph holds the whole call: error-block reset, launches, and the
+    // error block's copy back to the host (then only a stream sync remains)
     if (e.exec) {
       QD_CUDA(cudaGraphLaunch(e.exec, c.st));
       ws.launches += e.launches;
-    } else if (e.seen == 0) {
+      *flags = check_errors(c, false);
+      return;
+    }
+    if (e.seen == 0) {
       // first call of this shape: eager (sizes every workspace buffer)
       e.seen = 1;
+      reset_ctx(c);
       eager();
       e.epoch = ws.buf_epoch;
-    } else {
-      // second call: capture the launches (no allocation happens: the
-      // buffers were sized by the first call) and replay them from now on
-      const uint64_t epoch0 = ws.buf_epoch, l0 = ws.launches;
-      QD_CUDA(cudaStreamBeginCapture(c.st, cudaStreamCaptureModeThreadLocal));
-      cudaGraph_t g = nullptr;
-      try {
-        eager();
-      } catch (...) {
-        cudaStreamEndCapture(c.st, &g);
-        if (g) cudaGraphDestroy(g);
-        cudaGetLastError();
-        throw;
-      }
-      QD_CUDA(cudaStreamEndCapture(c.st, &g));
-      if (ws.buf_epoch != epoch0) {
-        // a buffer grew during capture (should not happen): run eagerly
-        cudaGraphDestroy(g);
-        e = Workspace::GraphEntry{};
-        eager();
-      } else {
-        QD_CUDA(cudaGraphInstantiate(&e.exec, g, 0));
-        QD_CUDA(cudaGraphDestroy(g));
-        e.launches = ws.launches - l0;
-        e.epoch = ws.buf_epoch;
-        QD_CUDA(cudaGraphLaunch(e.exec, c.st));
-      }
+      *flags = check_errors(c);
+      return;
     }
-  } else {
-    eager();
+    // second call: capture (no allocation happens: the buffers were sized by
+    // the first call) and replay from now on
+    const uint64_t epoch0 = ws.buf_epoch, l0 = ws.launches;
+    QD_CUDA(cudaStreamBeginCapture(c.st, cudaStreamCaptureModeThreadLocal));
+    cudaGraph_t g = nullptr;
+    try {
+      reset_ctx(c, !c.small);
+      eager();
+      QD_CUDA(cudaMemcpyAsync(ws.h_err, c.err, sizeof(ErrBlock), cudaMemcpyDeviceToHost, c.st));
+    } catch (...) {
+      cudaStreamEndCapture(c.st, &g);
+      if (g) cudaGraphDestroy(g);
+      cudaGetLastError();
+      throw;
+    }
+    QD_CUDA(cudaStreamEndCapture(c.st, &g));
+    if (ws.buf_epoch != epoch0) {
+      // a buffer grew during capture (should not happen): run eagerly
+      cudaGraphDestroy(g);
+      e = Workspace::GraphEntry{};
+      reset_ctx(c);
+      eager();
+      *flags = check_errors(c);
+      return;
+    }
+    QD_CUDA(cudaGraphInstantiate(&e.exec, g, 0));
+    QD_CUDA(cudaGraphDestroy(g));
+    e.launches = ws.launches - l0;
+    e.epoch = ws.buf_epoch;
+    QD_CUDA(cudaGraphLaunch(e.exec, c.st));
+    *flags = check_errors(c, false);
+    return;
   }
+  reset_ctx(c);
+  eager();
   *flags = check_errors(c);
 }
 
@@ -4512,6 +4940,19 @@ void run_groups(Workspace& ws, const TensorView& t, const uint32_t* d_c_in, cons
   unsigned flags = 0;
   run_groups_once(ws, t, d_c_in, d_v_in, d_c_out, d_v_out, groups, verify_input, d_boundaries,
                   n_boundaries, boundary_mode, stream, &flags);
+  if (flags & 8u) {
+    // k_small's preconditions failed (rows not ordered by the group prefix,
+    // or a composite coordinate out of range): the general path
+    ws.allow_small = false;
+    try {
+      run_groups_once(ws, t, d_c_in, d_v_in, d_c_out, d_v_out, groups, verify_input,
+                      d_boundaries, n_boundaries, boundary_mode, stream, &flags);
+    } catch (...) {
+      ws.allow_small = true;
+      throw;
+    }
+    ws.allow_small = true;
+  }
   if (flags & 4u) {
     // a coordinate of a mode the plan never range-checks does not fit its
     // packed field: redo the call with unpacked (SoA) intermediates
