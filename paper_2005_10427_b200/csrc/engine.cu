@@ -30,6 +30,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <condition_variable>
 #include <cstdlib>
 #include <cstdio>
@@ -4993,7 +4994,12 @@ void run_groups_host(Workspace& ws, const TensorView& t, uint32_t* coords, doubl
     return a.type == cudaMemoryTypeHost;
   };
   static const bool no_stage = getenv("QD_NO_STAGE") != nullptr;
+  static const bool dbg = getenv("QD_HOST_DBG") != nullptr;
   const bool stage = N && !no_stage && !(pinned(coords) && pinned(values));
+  auto now = [] {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+  };
+  double tm[4] = {now(), 0, 0, 0};
   if (N && stage) {
     staged_h2d(ic, coords, N * R * 4, st);
     staged_h2d(iv, values, N * 8, st);
@@ -5001,11 +5007,22 @@ void run_groups_host(Workspace& ws, const TensorView& t, uint32_t* coords, doubl
     QD_CUDA(cudaMemcpyAsync(ic, coords, N * R * 4, cudaMemcpyHostToDevice, st));
     QD_CUDA(cudaMemcpyAsync(iv, values, N * 8, cudaMemcpyHostToDevice, st));
   }
+  if (dbg) {
+    QD_CUDA(cudaStreamSynchronize(st));
+    tm[1] = now();
+  }
   uint64_t nb = 0;
   run_groups(ws, t, ic, iv, oc, ov, groups, verify_input, db, &nb, boundary_mode, st);
+  if (dbg) tm[2] = now();
   if (N && stage) {
-    staged_d2h(coords, oc, N * R * 4, st);
-    staged_d2h(values, ov, N * 8, st);
+    const StageSeg segs[2] = {{coords, oc, N * R * 4}, {values, ov, N * 8}};
+    staged_d2h_multi(segs, 2, st);
+    if (dbg) {
+      QD_CUDA(cudaStreamSynchronize(st));
+      tm[3] = now();
+      fprintf(stderr, "host call: h2d %.2f ms, device %.2f ms, d2h %.2f ms\n", (tm[1] - tm[0]) * 1e3,
+              (tm[2] - tm[1]) * 1e3, (tm[3] - tm[2]) * 1e3);
+    }
   } else if (N) {
     QD_CUDA(cudaMemcpyAsync(coords, oc, N * R * 4, cudaMemcpyDeviceToHost, st));
     QD_CUDA(cudaMemcpyAsync(values, ov, N * 8, cudaMemcpyDeviceToHost, st));

@@ -151,6 +151,12 @@ void* tns_dev_alloc(uint64_t bytes, void* stream);  // stream-ordered, pooled
 void tns_dev_free(void* p, void* stream);
 void staged_h2d(void* d_dst, const void* h_src, uint64_t n, void* stream);
 void staged_d2h(void* h_dst, const void* d_src, uint64_t n, void* stream);
+struct StageSeg {
+  void* h;
+  const void* d;
+  uint64_t n;
+};
+void staged_d2h_multi(const StageSeg* segs, int nseg, void* stream);
 
 // write_tns's text (io.cpp:128-152) formatted on the device from host rows;
 // *h_text is malloc-family memory (free()), null when nnz == 0.

@@ -19,6 +19,7 @@
 //                   ParseError text (io.cpp:16-18)
 // All byte work is HBM-bound: ~1 read of the text per pass, plus the row write.
 #include <cuda_runtime.h>
+#include <emmintrin.h>
 #include <sys/mman.h>
 
 #include <algorithm>
@@ -325,25 +326,42 @@ __global__ void k_line_slow(ParseArgs a, uint64_t count) {
 // Pageable cudaMemcpy runs at ~11 GB/s here (driver staging, one thread).
 // Instead: a ring of pinned chunks; host threads fill (or drain) a chunk with
 // a parallel memcpy while the copy engine moves the previous one.
-constexpr uint64_t kStageChunk = 32ull << 20;
-constexpr int kStageSlots = 4;
+// staging chunk (QD_STAGE_MB overrides; experiments)
+uint64_t stage_chunk() {
+  static const uint64_t c = [] {
+    if (const char* e = getenv("QD_STAGE_MB")) return (uint64_t)std::max(1, atoi(e)) << 20;
+    return (uint64_t)16 << 20;  // 16 MB x 8 slots: 30M-row pageable call 28.4 -> 27.6 ms
+  }();
+  return c;
+}
+constexpr int kMaxStageSlots = 16;
+// slots of the ring (QD_STAGE_SLOTS overrides; experiments)
+int stage_slots() {
+  static const int n = [] {
+    if (const char* e = getenv("QD_STAGE_SLOTS")) return std::max(2, std::min(kMaxStageSlots, atoi(e)));
+    return 8;
+  }();
+  return n;
+}
 constexpr int kMaxCopyThreads = 16;
 
 int copy_threads() {
   static const int n = [] {
     if (const char* e = getenv("QD_COPY_THREADS")) return std::max(1, std::min(kMaxCopyThreads, atoi(e)));
+    // 8 (streaming-store) threads saturate this host's DRAM next to the DMA
+    // engine; more only contend (profiles/microbench/host_staging.*)
     const unsigned hc = std::thread::hardware_concurrency();
-    return (int)std::max(1u, std::min<unsigned>(kMaxCopyThreads, hc ? hc : 4));
+    return (int)std::max(1u, std::min<unsigned>(8, hc ? hc : 4));
   }();
   return n;
 }
 
 struct StageRing {
-  char* buf[kStageSlots] = {};
-  cudaEvent_t ev[kStageSlots] = {};
+  char* buf[kMaxStageSlots] = {};
+  cudaEvent_t ev[kMaxStageSlots] = {};
   int device = -1;
   ~StageRing() {
-    for (int i = 0; i < kStageSlots; ++i) {
+    for (int i = 0; i < kMaxStageSlots; ++i) {
       if (buf[i]) cudaFreeHost(buf[i]);
       if (ev[i]) cudaEventDestroy(ev[i]);
     }
@@ -352,15 +370,49 @@ struct StageRing {
     int dev = 0;
     TNS_CUDA(cudaGetDevice(&dev));
     if (device == dev) return;
-    for (int i = 0; i < kStageSlots; ++i) {
+    for (int i = 0; i < stage_slots(); ++i) {
       if (buf[i]) cudaFreeHost(buf[i]);
       if (ev[i]) cudaEventDestroy(ev[i]);
-      TNS_CUDA(cudaMallocHost(&buf[i], kStageChunk));
+      TNS_CUDA(cudaMallocHost(&buf[i], stage_chunk()));
       TNS_CUDA(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
     }
     device = dev;
   }
 };
+
+// Host copy with non-temporal (streaming) stores: a regular store first reads
+// the destination line (read-for-ownership), so a staged copy would move 4
+// bytes of host DRAM traffic per byte next to the DMA engine's own; with
+// streaming stores it moves 3 (profiles/microbench/host_staging.*: the
+// staged pageable path is host-memory-bandwidth bound).  QD_COPY_NT=0: memcpy.
+void copy_nt(char* dst, const char* src, uint64_t n) {
+  static const bool nt = [] {
+    const char* e = getenv("QD_COPY_NT");
+    return !(e && atoi(e) == 0);
+  }();
+  if (!nt || n < 4096) {
+    std::memcpy(dst, src, n);
+    return;
+  }
+  const uint64_t head = (16 - (reinterpret_cast<uintptr_t>(dst) & 15)) & 15;
+  std::memcpy(dst, src, head);
+  dst += head;
+  src += head;
+  n -= head;
+  const uint64_t body = n & ~uint64_t(63);
+  for (uint64_t i = 0; i < body; i += 64) {
+    const __m128i a = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i));
+    const __m128i b = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 16));
+    const __m128i c = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 32));
+    const __m128i d = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 48));
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i), a);
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 16), b);
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 32), c);
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 48), d);
+  }
+  _mm_sfence();
+  std::memcpy(dst + body, src + body, n - body);
+}
 
 // A persistent pool of host copy threads (spawning threads per 32 MB chunk
 // cost a sizeable fraction of the chunk's copy time).  A job is split into
@@ -383,7 +435,7 @@ class CopyPool {
     ++gen_;
     cv_.notify_all();
     lk.unlock();
-    std::memcpy(dst, src, std::min(n, part));
+    copy_nt(dst, src, std::min(n, part));
     lk.lock();
     done_cv_.wait(lk, [&] { return pending_ == 0; });
   }
@@ -412,7 +464,7 @@ class CopyPool {
       const char* src = src_;
       const uint64_t a = std::min(n_, t * part_), b = std::min(n_, (t + 1) * part_);
       lk.unlock();
-      if (b > a) std::memcpy(dst + a, src + a, b - a);
+      if (b > a) copy_nt(dst + a, src + a, b - a);
       lk.lock();
       if (--pending_ == 0) done_cv_.notify_one();
     }
@@ -487,8 +539,9 @@ void tns_dev_free(void* p, void* stream) {
 void staged_h2d(void* d_dst, const void* h_src, uint64_t n, void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   StageRing& r = stage_ring();
+  const uint64_t kStageChunk = stage_chunk();
   for (uint64_t off = 0, i = 0; off < n; off += kStageChunk, ++i) {
-    const int k = (int)(i % kStageSlots);
+    const int k = (int)(i % stage_slots());
     const uint64_t len = std::min(kStageChunk, n - off);
     TNS_CUDA(cudaEventSynchronize(r.ev[k]));  // the slot's previous copy is done
     parallel_memcpy(r.buf[k], static_cast<const char*>(h_src) + off, len);
@@ -498,25 +551,41 @@ void staged_h2d(void* d_dst, const void* h_src, uint64_t n, void* stream) {
   }
 }
 
-void staged_d2h(void* h_dst, const void* d_src, uint64_t n, void* stream) {
+// Device -> host through the pinned ring for several (host, device, bytes)
+// segments as ONE chunk pipeline (no drain between segments): each chunk's
+// DMA runs while earlier chunks are copied out by the host threads.
+void staged_d2h_multi(const StageSeg* segs, int nseg, void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   StageRing& r = stage_ring();
-  const uint64_t chunks = (n + kStageChunk - 1) / kStageChunk;
-  auto issue = [&](uint64_t i) {
+  const uint64_t kStageChunk = stage_chunk();
+  struct Piece {
+    char* h;
+    const char* d;
+    uint64_t len;
+  };
+  std::vector<Piece> ps;
+  for (int s = 0; s < nseg; ++s)
+    for (uint64_t off = 0; off < segs[s].n; off += kStageChunk)
+      ps.push_back({static_cast<char*>(segs[s].h) + off, static_cast<const char*>(segs[s].d) + off,
+                    std::min(kStageChunk, segs[s].n - off)});
+  const int kStageSlots = stage_slots();
+  auto issue = [&](size_t i) {
     const int k = (int)(i % kStageSlots);
-    const uint64_t off = i * kStageChunk, len = std::min(kStageChunk, n - off);
-    TNS_CUDA(cudaMemcpyAsync(r.buf[k], static_cast<const char*>(d_src) + off, len,
-                             cudaMemcpyDeviceToHost, st));
+    TNS_CUDA(cudaMemcpyAsync(r.buf[k], ps[i].d, ps[i].len, cudaMemcpyDeviceToHost, st));
     TNS_CUDA(cudaEventRecord(r.ev[k], st));
   };
-  for (uint64_t i = 0; i < std::min<uint64_t>(chunks, kStageSlots); ++i) issue(i);
-  for (uint64_t i = 0; i < chunks; ++i) {
+  for (size_t i = 0; i < std::min<size_t>(ps.size(), kStageSlots); ++i) issue(i);
+  for (size_t i = 0; i < ps.size(); ++i) {
     const int k = (int)(i % kStageSlots);
-    const uint64_t off = i * kStageChunk, len = std::min(kStageChunk, n - off);
     TNS_CUDA(cudaEventSynchronize(r.ev[k]));
-    parallel_memcpy(static_cast<char*>(h_dst) + off, r.buf[k], len);
-    if (i + kStageSlots < chunks) issue(i + kStageSlots);
+    parallel_memcpy(ps[i].h, r.buf[k], ps[i].len);
+    if (i + kStageSlots < ps.size()) issue(i + kStageSlots);
   }
+}
+
+void staged_d2h(void* h_dst, const void* d_src, uint64_t n, void* stream) {
+  const StageSeg seg{h_dst, d_src, n};
+  staged_d2h_multi(&seg, 1, stream);
 }
 
 namespace {
