@@ -1003,3 +1003,73 @@ def test_latency_mode_out_of_range_on_replay(ws):
         qd.transpose_device(r, dims, n, ci.data_ptr(), vi.data_ptr(), co.data_ptr(),
                             vo.data_ptr(), [1, 0, 2], qd.SortStrategy.quesadilla(), ws, sp)
     assert e.value.row == n // 3 and e.value.mode == 1
+
+
+def test_small_engine_preconditions(ws):
+    """k_small (one cooperative kernel for a single-group plan on <= 2^22
+    rows) sorts by the composite (prefix, key): valid only when the rows are
+    ordered by the group prefix and every composite coordinate is in range.
+    On a created stream (graphs on), eager / captured / replayed calls on the
+    same buffers must match the oracle for valid input, for input NOT ordered
+    by the prefix and for an out-of-range PREFIX coordinate (both redone on the
+    general path, reference semantics: no error), raise OutOfRange for a key
+    coordinate, and a composite wider than 64 bits takes the general path."""
+    import torch
+    rng = np.random.default_rng(91)
+    st = torch.cuda.Stream()
+    sp = st.cuda_stream
+
+    def run(dims, coords, values, target, bufs):
+        n, r = len(values), len(dims)
+        ci, vi, co, vo = bufs
+        ci[:n * r].copy_(torch.from_numpy(coords.view(np.int32)))
+        vi[:n].copy_(torch.from_numpy(values))
+        torch.cuda.synchronize()
+        qd.transpose_device(r, dims, n, ci.data_ptr(), vi.data_ptr(), co.data_ptr(), vo.data_ptr(),
+                            target, qd.SortStrategy.quesadilla(), ws, sp)
+        st.synchronize()
+        return (co[:n * r].cpu().numpy().view(np.uint32).copy(),
+                vo[:n].cpu().numpy().view(np.uint64).copy())
+
+    for dims, target in (([40, 300, 500], [0, 2, 1]), ([40, 300, 500], [2, 1, 0]),
+                         ([15, 12, 9, 3000, 700], [0, 1, 4, 2, 3])):
+        n, r = 60_000, len(dims)
+        t = rand_tensor(rng, dims, n)
+        bufs = [torch.empty(n * r, dtype=torch.int32, device="cuda"),
+                torch.empty(n, dtype=torch.float64, device="cuda"),
+                torch.empty(n * r, dtype=torch.int32, device="cuda"),
+                torch.empty(n, dtype=torch.float64, device="cuda")]
+        c0, v0, _ = ORC.transpose(dims, t.coords, t.values, target)
+        for _ in range(3):  # eager, capture, replay
+            c, v = run(dims, t.coords, t.values, target, bufs)
+            assert np.array_equal(c, c0) and np.array_equal(v, v0.view(np.uint64)), target
+        # rows not ordered by the prefix (a shuffled block): general-path redo
+        bad = t.coords.reshape(-1, r).copy()
+        perm = np.arange(n)
+        perm[1000:3000] = rng.permutation(perm[1000:3000])
+        bad = bad[perm]
+        badv = t.values[perm]
+        c1, v1, _ = ORC.transpose(dims, bad.ravel(), badv, target)
+        c, v = run(dims, bad.ravel(), badv, target, bufs)
+        assert np.array_equal(c, c1) and np.array_equal(v, v1.view(np.uint64)), ("unsorted", target)
+        if target[0] == 0:
+            # an out-of-range coordinate in the prefix mode (never range-checked)
+            oor = t.coords.reshape(-1, r).copy()
+            oor[-1, 0] = dims[0] + 3
+            c2, v2, _ = ORC.transpose(dims, oor.ravel(), t.values, target)
+            c, v = run(dims, oor.ravel(), t.values, target, bufs)
+            assert np.array_equal(c, c2) and np.array_equal(v, v2.view(np.uint64)), ("prefix", target)
+        # a key coordinate out of range: the reference's out_of_range
+        key_mode = {(0, 2, 1): 2, (2, 1, 0): 2, (0, 1, 4, 2, 3): 4}[tuple(target)]
+        kb = t.coords.reshape(-1, r).copy()
+        kb[n // 2, key_mode] = dims[key_mode]
+        with pytest.raises(qd.OutOfRange):
+            run(dims, kb.ravel(), t.values, target, bufs)
+        c, v = run(dims, t.coords, t.values, target, bufs)  # and valid again
+        assert np.array_equal(c, c0) and np.array_equal(v, v0.view(np.uint64))
+    # a composite key wider than 64 bits: the general path
+    dims = [1 << 22] * 4
+    t = rand_tensor(rng, dims, 40_000)
+    out = qd.transpose(t, [3, 2, 1, 0], ws=ws)
+    c, v, _ = ORC.transpose(dims, t.coords, t.values, [3, 2, 1, 0])
+    assert same(out, c, v)
