@@ -1073,3 +1073,27 @@ def test_small_engine_preconditions(ws):
     out = qd.transpose(t, [3, 2, 1, 0], ws=ws)
     c, v, _ = ORC.transpose(dims, t.coords, t.values, [3, 2, 1, 0])
     assert same(out, c, v)
+
+
+def test_large_bucketed_group_prefix_order(ws):
+    """A bucketed group above the latency-mode size (chunked passes for the
+    large runs, k_local3 for the small ones) on rows ordered by the prefix,
+    and on rows whose prefix order is broken inside runs (a row of a large
+    and of a small run takes another mode-0 value): the output equals the
+    reference's maximal-run semantics (oracle) in both cases."""
+    rng = np.random.default_rng(93)
+    dims = [40000, 3000, 5000]
+    n = (1 << 24) + 4099  # above the latency-mode size, where sampling applies
+    t = rand_tensor(rng, dims, n)
+    c0, v0, _ = ORC.transpose(dims, t.coords, t.values, [0, 2, 1])
+    out = qd.transpose(t, [0, 2, 1], ws=ws)
+    assert same(out, c0, v0)
+    # break the prefix order inside windows (a row in the middle of a run of
+    # a large and of a small run takes another mode-0 value)
+    bad = t.coords.reshape(-1, 3).copy()
+    for p in (123_457, n // 2 + 17, n - 1000):
+        bad[p, 0] = (bad[p, 0] + 7) % dims[0]
+    tb = qd.CooTensor(dims, bad.ravel(), t.values)
+    c1, v1, _ = ORC.transpose(dims, tb.coords, tb.values, [0, 2, 1])
+    out = qd.transpose(tb, [0, 2, 1], ws=ws)
+    assert same(out, c1, v1)
