@@ -3,7 +3,9 @@ c2/c4/c5-shaped transposes through the C ABI (host buffers, no torch in the
 process), every kernel path once — chunked digit passes (plain and packed
 rows), bucketed groups with small runs (k_local2) and large runs, the
 run-level sort, rank 5, verify_input, an out-of-range error, the device
-sortedness check — each checked against the C oracle."""
+sortedness check — each checked against the C oracle.  Single-group plans on
+these small tensors take k_small (the latency-regime cooperative kernel)
+unless QD_SMALL=0, which the tests set for a second run."""
 import os
 import sys
 

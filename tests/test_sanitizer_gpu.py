@@ -16,10 +16,14 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SAN = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
 
 
+# small tensors take k_small (one cooperative kernel) by default; QD_SMALL=0
+# sends the same calls through the general kernels (chunked passes, k_local3,
+# run sorts), so both families run under every tool
 @pytest.mark.skipif(not os.path.exists(SAN), reason="compute-sanitizer not found")
+@pytest.mark.parametrize("small", ["1", "0"])
 @pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck"])
-def test_sanitizer_clean(tool):
-    env = dict(os.environ, QD_SAN_ROWS="4000" if tool == "racecheck" else "8000")
+def test_sanitizer_clean(tool, small):
+    env = dict(os.environ, QD_SAN_ROWS="4000" if tool == "racecheck" else "8000", QD_SMALL=small)
     cmd = [SAN, "--tool", tool, "--error-exitcode", "17", "--print-limit", "20"]
     if tool == "memcheck":
         cmd += ["--leak-check", "no"]
@@ -36,11 +40,12 @@ def test_sanitizer_clean(tool):
     assert "ERROR SUMMARY: 0 errors" in out or "RACECHECK SUMMARY: 0 hazards" in out, out[-4000:]
 
 
-def test_driver_with_poisoned_scratch():
+@pytest.mark.parametrize("small", ["1", "0"])
+def test_driver_with_poisoned_scratch(small):
     """The same kernel paths with every fresh workspace buffer poisoned
     (QD_POISON): a kernel reading scratch it never wrote fails the oracle
     comparison instead of passing on zero-filled memory."""
-    env = dict(os.environ, QD_POISON="165", QD_SAN_ROWS="60000")
+    env = dict(os.environ, QD_POISON="165", QD_SAN_ROWS="60000", QD_SMALL=small)
     r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "sanitize_driver.py")],
                        capture_output=True, text=True, timeout=600, env=env)
     assert r.returncode == 0 and "sanitize driver ok" in r.stdout, (r.stdout + r.stderr)[-4000:]
