@@ -391,10 +391,12 @@ def bench_sharded(args, cfg, dist, rank, world, local):
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     # SURVEY §8e reporting: one more step's per-target stats
     per_target = {}
+    max_out = 0
     for t in cfg.targets:
         a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a0.record(stream)
         n_out, st = one(t)
+        max_out = max(max_out, n_out)
         a1.record(stream)
         torch.cuda.synchronize()
         vals = torch.tensor([a0.elapsed_time(a1), st["exchange_ms"], st["bytes_sent"], n_out,
@@ -425,7 +427,10 @@ def bench_sharded(args, cfg, dist, rank, world, local):
     del ci, vi
     torch.cuda.empty_cache()
     dc, dv = torch.empty(hc.shape, dtype=hc.dtype, device="cuda"), torch.empty_like(hv, device="cuda")
-    oc = torch.empty(cap * r, dtype=torch.int32, pin_memory=True) if n_total < (1 << 28) else None
+    # pinned output slices sized by the rows this rank received above (the
+    # same input gives the same split); pageable .cpu() copies only beyond
+    oc = torch.empty(max(1, max_out) * r, dtype=torch.int32, pin_memory=True)
+    ov = torch.empty(max(1, max_out), dtype=torch.float64, pin_memory=True)
     k_e2e = 1
     h2d = d2h = 0
     torch.cuda.synchronize()
@@ -438,9 +443,11 @@ def bench_sharded(args, cfg, dist, rank, world, local):
             n_out, _ = one(t, dc, dv, n_local)
             h2d += hc.numel() * 4 + hv.numel() * 8
             d2h += n_out * (4 * r + 8)
-            out_c = co[:n_out * r].cpu() if oc is None else oc[:n_out * r].copy_(co[:n_out * r])
-            out_v = vo[:n_out].cpu()
-            del out_c, out_v
+            if n_out <= max_out:
+                oc[:n_out * r].copy_(co[:n_out * r])
+                ov[:n_out].copy_(vo[:n_out])
+            else:
+                co[:n_out * r].cpu(), vo[:n_out].cpu()
     torch.cuda.synchronize()
     wall = torch.tensor([time.perf_counter() - t0], device="cuda", dtype=torch.float64)
     dist.all_reduce(wall, op=dist.ReduceOp.MAX)
