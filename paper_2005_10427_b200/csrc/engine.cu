@@ -1035,7 +1035,10 @@ struct ScatterLayout {
 // DM: digit of an AoS/SoA row inside 1 or 2 key fields (0 = general).
 // ---------------------------------------------------------------------------
 template <int RT, int IN, int OUT, int DM, int MX = 0>
-__global__ void __launch_bounds__(kSortThreads, QD_SCATTER_CTAS * 512 / kSortThreads) k_scatter(ScatterArgs a) {
+#ifndef QD_SCATTER_MINB
+#define QD_SCATTER_MINB (QD_SCATTER_CTAS * 512 / kSortThreads)
+#endif
+__global__ void __launch_bounds__(kSortThreads, QD_SCATTER_MINB) k_scatter(ScatterArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   const uint32_t R = RT ? RT : a.rank;
   const uint64_t N = a.nnz;
