@@ -41,6 +41,8 @@
 #include <string>
 #include <thread>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "internal.hpp"
 
 namespace qb200 {
@@ -51,6 +53,15 @@ namespace qb200 {
     if (e_ != cudaSuccess)                                                      \
       throw Error(QD_CUDA_ERROR, std::string(#x) + ": " + cudaGetErrorString(e_)); \
   } while (0)
+
+// NVTX ranges (nsys / ncu --nvtx filters): the call, each plan group, each
+// digit pass, run discovery and the small-run sort.  Header-only NVTX v3:
+// without an attached tool a range is a null-pointer check.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  explicit NvtxRange(const std::string& name) { nvtxRangePushA(name.c_str()); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 constexpr int kThreads = 256;       // utility kernels
 constexpr int kWarps = kThreads / 32;
@@ -3736,6 +3747,7 @@ void scan_exclusive(Ctx& c, const uint32_t* in, uint64_t n, unsigned long long* 
 uint64_t find_runs(Ctx& c, const uint32_t* coords, uint32_t rank, uint64_t nnz,
                    const std::vector<uint32_t>& modes, unsigned long long** seg_out,
                    unsigned long long** S_dev_out = nullptr) {
+  NvtxRange r_runs("run discovery");
   ModeList ml{};
   ml.n = (uint32_t)modes.size();
   for (uint32_t i = 0; i < ml.n; ++i) ml.m[i] = (uint8_t)modes[i];
@@ -4283,6 +4295,8 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
       const uint32_t nlo = (q + 1) * per, nhi = std::min(bits, nlo + per);
       // packed-row passes afford a larger tile (16-byte staged rows)
       const uint32_t Tq = (per_fmt_tiles && in.fmt == kPK) ? sweep_tile_rows(ws, R, kPK) : T;
+      NvtxRange r_pass("pass " + std::to_string(q) + " bits [" + std::to_string(lo) + "," +
+                       std::to_string(hi) + ")");
       run_pass(c, R, N, Tq, in, out, chunks, num_chunks, run_start, digs[q], key,
                q == 0 && key.check, nullptr, packed ? &pack : nullptr, lo,
                (1u << (hi - lo)) - 1u, dig_in, dig_out, nlo, last ? 0u : (1u << (nhi - nlo)) - 1u,
@@ -4292,6 +4306,7 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
     }
   }
   if (small_runs && local_chunks && local2) {
+    NvtxRange r_local("small runs (k_local3)");
     // small runs: items = the runs starting in [c*TL, (c+1)*TL) of every
     // chunk that holds some (compact list); after the passes, whose
     // intermediates may use dst's storage
@@ -4733,6 +4748,7 @@ static void launch_groups(Ctx& c, const TensorView& t, const uint32_t* d_c_in,
                           const std::vector<Group>& groups, bool verify_input,
                           uint64_t* d_boundaries, uint64_t* n_boundaries,
                           uint32_t boundary_mode) {
+  NvtxRange r_call(c.small ? "qd call (k_small)" : "qd call");
   Workspace& ws = c.ws;
   const uint64_t N = t.nnz;
   const uint32_t R = t.rank;
@@ -4788,6 +4804,11 @@ static void launch_groups(Ctx& c, const TensorView& t, const uint32_t* d_c_in,
         tv = d_v_out;
       }
       c.group = (int)gi;
+      std::string gname = "group prefix=";
+      for (uint32_t m : groups[gi].prefix) gname += std::to_string(m);
+      gname += " keys=";
+      for (uint32_t m : groups[gi].keys) gname += std::to_string(m);
+      NvtxRange r_group(gname);
       exec_group(c, t, sc, sv, dc, dv, tc, tv, groups[gi]);
       sc = dc;
       sv = dv;
