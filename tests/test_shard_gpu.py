@@ -1,5 +1,5 @@
 """The sharded transpose in the C++ library (qd_sharded_transpose_device,
-csrc/shard.cu): world sizes 2-4 with the emulated transport (ranks as host
+csrc/shard.cu): world sizes 2-4 and 8 with the emulated transport (ranks as host
 threads on one GPU: device copies + host barriers, no kernel waits on another
 rank's), and world size 1 over real NCCL.  Output slices concatenated in rank
 order must equal the oracle's transpose of the global tensor bit for bit
@@ -76,7 +76,7 @@ def run_emulated(world, c, v, dims, target, bounds, strategy=None, capacity=None
     return outs, stats, errs
 
 
-@pytest.mark.parametrize("world", [2, 3, 4])
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
 def test_sharded_cpp_emulated(world):
     rng = np.random.default_rng(200 + world)
     dims = [60, 700, 900]
@@ -163,3 +163,36 @@ def test_sharded_cpp_nccl_world1():
     finally:
         comm.close()
         ws.close()
+
+
+def test_sharded_cpp_emulated_config5_shape():
+    """Config 5's shape and distribution (dimensions / 100, Zipf(1.05)) at
+    ~40 M unique rows over two emulated ranks, so each rank's slice is above the
+    latency-mode size and runs the general kernels (segmented passes, small-run
+    sorts, the exchange's partition pass): (1,0,2) with one exchange, (0,2,1)
+    communication-free on mode-0-aligned slices; concatenated rank outputs
+    against the oracle's transpose of the global tensor."""
+    import torch
+    rng = np.random.default_rng(205)
+    dims = [48212, 17742, 18051]
+    n0 = 60_000_000
+    cols = []
+    for d in dims:
+        cdf = np.cumsum(1.0 / np.arange(1, d + 1) ** 1.05)
+        cols.append(np.searchsorted(cdf / cdf[-1], rng.random(n0), side="right").clip(max=d - 1))
+    c = np.unique(np.stack(cols, 1).astype(np.uint32), axis=0)
+    v = rng.random(len(c))
+    n = len(v)
+    assert n > (1 << 25)
+    j = int(np.searchsorted(c[:, 0], c[n // 2 - 1, 0], side="right"))  # no mode-0 run split
+    bounds = [0, j, n]
+    for target in ([1, 0, 2], [0, 2, 1]):
+        outs, stats, errs = run_emulated(2, c, v, dims, target, bounds)
+        assert not errs, errs
+        ec, ev, _ = ORC.transpose(dims, c.ravel(), v, target)
+        got_c = np.concatenate([o[0] for o in outs])
+        got_v = np.concatenate([o[1] for o in outs])
+        assert np.array_equal(got_c, ec), target
+        assert np.array_equal(got_v.view(np.uint64), ev.view(np.uint64)), target
+        assert all(s["exchanged"] for s in stats) == (target[0] != 0)
+        torch.cuda.empty_cache()
