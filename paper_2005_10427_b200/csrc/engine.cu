@@ -10,22 +10,27 @@
 //   k_heads / scan / k_compact     run discovery (bucket_starts, sort.cpp:136)
 //   k_classify_chunks/k_gen_chunks small runs -> local CTA sorts, large runs ->
 //                                  chunks of contiguous rows
-//   per radix digit (LSD, 8 bits):
+//   per radix digit (LSD, <= 8 bits):
 //     k_chunk_hist                 digit histogram of every chunk (+ range
-//                                  check on the first digit: count_keys)
+//                                  check on the first digit: count_keys);
+//                                  later digits from a 1-byte side channel
 //     scan                         (run, bin, chunk) exclusive scan = every
 //                                  chunk's output cursor per bin: the
 //                                  (key, worker) order of parallel.cpp:88-100
 //     k_scatter                    chunk-ordered stable scatter of whole rows:
-//                                  TMA bulk-copy double buffering, warp-ballot
-//                                  ranking in shared memory, coalesced stores;
-//                                  intermediates in SoA so the next histogram
-//                                  reads only the key column
-//   k_local                        runs that fit one CTA: loaded once, fully
-//                                  sorted in shared memory, written once
+//                                  TMA bulk-copy double buffering, MATCH.ANY
+//                                  warp ranking in shared memory, coalesced
+//                                  stores; intermediates as packed 16-byte
+//                                  rows (bit fields / mixed radix / run prefix)
+//   k_local3                       the small runs: merged items staged by TMA,
+//                                  block-wide LSD over (run, key), written once
+//   k_small                        latency regime (single-group plans, <= 2^22
+//                                  rows): the whole call in one cooperative
+//                                  kernel over {key, row} elements in L2
 //
-// Rows are always moved whole (the reference's scatter_rows), so there is no
-// separate gather.  No CPU fallback exists: every path here is a kernel.
+// Rows are always moved whole (the reference's scatter_rows) or gathered once
+// by k_small, so there is no separate gather pass.  No CPU fallback exists:
+// every path here is a kernel.
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
