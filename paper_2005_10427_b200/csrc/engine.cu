@@ -1759,10 +1759,57 @@ __global__ void __launch_bounds__(kSmallThreads, 2) k_small(SmallArgs a) {
       }
       __syncthreads();
       if (q == 0 && base == lo) small_mark(a, 53);
-      for (uint32_t j = t; j < n; j += kSmallThreads) {
-        const uint32_t x = s_srt[j];
-        const uint32_t d = x & 0xFFu;
-        dst[s_cur[d] + (j - s_tstart[d])] = s_el[x >> 8];
+      if (q + 1 < a.P) {
+        for (uint32_t j = t; j < n; j += kSmallThreads) {
+          const uint32_t x = s_srt[j];
+          const uint32_t d = x & 0xFFu;
+          dst[s_cur[d] + (j - s_tstart[d])] = s_el[x >> 8];
+        }
+      } else {
+        // the last pass writes the rows themselves, gathered by source row
+        // (random reads hit L2), four per thread in flight
+        constexpr int kG = 4;
+        for (uint32_t j0 = t; j0 < n; j0 += kG * kSmallThreads) {
+          unsigned long long pos[kG], src[kG];
+#pragma unroll
+          for (int u = 0; u < kG; ++u) {
+            const uint32_t j = j0 + u * kSmallThreads;
+            pos[u] = ~0ull;
+            src[u] = 0ull;
+            if (j < n) {
+              const uint32_t x = s_srt[j];
+              const uint32_t d = x & 0xFFu;
+              pos[u] = s_cur[d] + (j - s_tstart[d]);
+              src[u] = s_el[x >> 8].y;
+            }
+          }
+          double v[kG];
+#pragma unroll
+          for (int u = 0; u < kG; ++u) v[u] = __ldg(a.in_v + src[u]);
+          if (R == 3) {
+            uint32_t cx[kG][3];
+#pragma unroll
+            for (int u = 0; u < kG; ++u)
+#pragma unroll
+              for (int m = 0; m < 3; ++m) cx[u][m] = __ldg(a.in_c + src[u] * 3 + m);
+#pragma unroll
+            for (int u = 0; u < kG; ++u) {
+              if (pos[u] == ~0ull) continue;
+#pragma unroll
+              for (int m = 0; m < 3; ++m) a.out_c[pos[u] * 3 + m] = cx[u][m];
+              a.out_v[pos[u]] = v[u];
+            }
+          } else {
+#pragma unroll
+            for (int u = 0; u < kG; ++u) {
+              if (pos[u] == ~0ull) continue;
+              const uint32_t* sr = a.in_c + src[u] * R;
+              uint32_t* o = a.out_c + pos[u] * R;
+              for (uint32_t m = 0; m < R; ++m) o[m] = __ldg(sr + m);
+              a.out_v[pos[u]] = v[u];
+            }
+          }
+        }
       }
       __syncthreads();
       if (q == 0 && base == lo) small_mark(a, 54);
@@ -1770,6 +1817,7 @@ __global__ void __launch_bounds__(kSmallThreads, 2) k_small(SmallArgs a) {
       // (the next tile's first barrier orders this before any s_cur read)
     }
     small_mark(a, 5 + 6 * q);
+    if (q + 1 == a.P) break;  // the last pass wrote the output rows
     grid.sync();
     small_mark(a, 6 + 6 * q);
     if (q + 1 < a.P) {
@@ -1788,48 +1836,6 @@ __global__ void __launch_bounds__(kSmallThreads, 2) k_small(SmallArgs a) {
       small_mark(a, 7 + 6 * q);
       grid.sync();
       small_mark(a, 8 + 6 * q);
-    }
-  }
-  // rows in sorted order, gathered by source row
-  const ulonglong2* fin = (a.P & 1u) ? a.eb : a.ea;
-  // four rows per thread in flight (independent loads before any store)
-  constexpr int kG = 4;
-  for (uint64_t i0 = lo + t; i0 < hi; i0 += (uint64_t)kG * kSmallThreads) {
-    unsigned long long r[kG];
-#pragma unroll
-    for (int u = 0; u < kG; ++u) {
-      const uint64_t i = i0 + (uint64_t)u * kSmallThreads;
-      r[u] = i < hi ? fin[i].y : 0ull;
-    }
-    double v[kG];
-#pragma unroll
-    for (int u = 0; u < kG; ++u) v[u] = __ldg(a.in_v + r[u]);
-    if (R == 3) {
-      uint32_t x[kG][3];
-#pragma unroll
-      for (int u = 0; u < kG; ++u)
-#pragma unroll
-        for (int m = 0; m < 3; ++m) x[u][m] = __ldg(a.in_c + r[u] * 3 + m);
-#pragma unroll
-      for (int u = 0; u < kG; ++u) {
-        const uint64_t i = i0 + (uint64_t)u * kSmallThreads;
-        if (i < hi) {
-#pragma unroll
-          for (int m = 0; m < 3; ++m) a.out_c[i * 3 + m] = x[u][m];
-          a.out_v[i] = v[u];
-        }
-      }
-    } else {
-#pragma unroll
-      for (int u = 0; u < kG; ++u) {
-        const uint64_t i = i0 + (uint64_t)u * kSmallThreads;
-        if (i < hi) {
-          const uint32_t* sr = a.in_c + r[u] * R;
-          uint32_t* o = a.out_c + i * R;
-          for (uint32_t m = 0; m < R; ++m) o[m] = sr[m];
-          a.out_v[i] = v[u];
-        }
-      }
     }
   }
   small_mark(a, 63);
