@@ -90,6 +90,12 @@ void qd_workspace_destroy(qd_workspace* ws);
 uint64_t qd_workspace_bytes(const qd_workspace* ws);
 /* Number of CUDA kernels this workspace has launched since creation. */
 uint64_t qd_workspace_launches(const qd_workspace* ws);
+/* Slices the last synchronous host-buffer call (qd_transpose_inplace,
+ * qd_partial_sort, qd_sort_rows_by) was pipelined in: 1 = whole tensor; > 1 when
+ * every pass keeps a common prefix mode (Alg. 2 only, sort.cpp:80-134), so the
+ * tensor is cut where that mode changes and the slices' input copies, passes
+ * and output copies overlap.  QD_SLICE_ROWS=<rows> sets the slice size (0: never). */
+uint64_t qd_workspace_slices(const qd_workspace* ws);
 
 /* Live per-kernel-class timing with CUDA events recorded on the launch
  * stream (off by default).  Classes: 0 chunk-ordered digit scatter, 1 chunk histogram,

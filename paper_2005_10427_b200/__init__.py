@@ -126,6 +126,8 @@ def lib():
         L.qd_workspace_bytes.restype = C.c_uint64
         L.qd_workspace_launches.argtypes = [C.c_void_p]
         L.qd_workspace_launches.restype = C.c_uint64
+        L.qd_workspace_slices.argtypes = [C.c_void_p]
+        L.qd_workspace_slices.restype = C.c_uint64
         L.qd_profile_enable.argtypes = [C.c_void_p, C.c_int]
         L.qd_profile_reset.argtypes = [C.c_void_p]
         L.qd_profile_get.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_uint64),
@@ -535,6 +537,10 @@ class Workspace:
 
     def launches(self) -> int:
         return int(lib().qd_workspace_launches(self._h))
+
+    def slices(self) -> int:
+        """Slices the last synchronous host-buffer call was pipelined in (1: whole)."""
+        return int(lib().qd_workspace_slices(self._h))
 
     PROFILE_CLASSES = ("scatter", "hist", "local", "runs", "other")
 

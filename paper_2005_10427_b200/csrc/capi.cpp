@@ -148,6 +148,9 @@ uint64_t qd_workspace_bytes(const qd_workspace* ws) {
 uint64_t qd_workspace_launches(const qd_workspace* ws) {
   return ws ? workspace_launches(Wc(ws)) : 0;
 }
+uint64_t qd_workspace_slices(const qd_workspace* ws) {
+  return ws ? workspace_slices(Wc(ws)) : 0;
+}
 
 void qd_profile_enable(qd_workspace* ws, int enable) {
   if (ws) workspace_profile(&W(ws), enable);

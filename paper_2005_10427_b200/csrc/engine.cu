@@ -3327,6 +3327,12 @@ struct Workspace {
   // device work and output copies (PCIe is full duplex).
   cudaStream_t s_in = nullptr, s_comp = nullptr, s_out = nullptr;
   cudaStream_t s_host = nullptr;  // synchronous host-buffer calls (capturable, unlike stream 0)
+  // sliced host-buffer calls (run_groups_host): the input and output copy
+  // streams of the slice pipeline, and one "slice arrived" event per slice
+  cudaStream_t s_sl_in = nullptr, s_sl_out = nullptr;
+  std::vector<cudaEvent_t> ev_slices;
+  bool allow_latency = true;  // cleared while a sliced call runs its slices (no per-slice graphs)
+  uint64_t last_slices = 1;
   static constexpr int kSlots = QD_ASYNC_SLOTS;  // device in/out buffer pairs in flight
   cudaEvent_t ev_in[kSlots] = {}, ev_comp[kSlots] = {}, ev_out[kSlots] = {};
   struct SlotBuf {
@@ -3531,7 +3537,8 @@ void workspace_destroy(Workspace* ws) {
   for (auto& sb : ws->slots)
     for (void* p : {(void*)sb.ic, (void*)sb.iv, (void*)sb.oc, (void*)sb.ov})
       if (p) cudaFree(p);
-  for (cudaStream_t st : {ws->s_in, ws->s_comp, ws->s_out, ws->s_host})
+  for (cudaEvent_t e : ws->ev_slices) cudaEventDestroy(e);
+  for (cudaStream_t st : {ws->s_in, ws->s_comp, ws->s_out, ws->s_host, ws->s_sl_in, ws->s_sl_out})
     if (st) {
       cudaStreamSynchronize(st);
       cudaStreamDestroy(st);
@@ -3558,6 +3565,7 @@ uint64_t workspace_bytes(const Workspace* ws) {
   return b;
 }
 uint64_t workspace_launches(const Workspace* ws) { return ws->launches; }
+uint64_t workspace_slices(const Workspace* ws) { return ws->last_slices; }
 void* workspace_buffer(Workspace& ws, const char* name, size_t bytes) {
   return ws.get<unsigned char>(name, bytes);
 }
@@ -3654,6 +3662,28 @@ struct Ctx {
     recs.clear();
   }
 };
+
+// Small device->host reads of counts and of the error block (h: pinned).  A
+// sliced host-buffer call keeps the device->host copy engine busy with the
+// previous slice's rows, and a cudaMemcpyAsync of 8 bytes would queue behind
+// gigabytes of them (measured: every slice's passes started only when the
+// previous slice's output copy had drained); there a one-warp kernel stores
+// the words through the pinned buffer's device mapping instead.
+__global__ void k_readback(uint32_t* __restrict__ h, const uint32_t* __restrict__ d, uint32_t words) {
+  for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) h[i] = d[i];
+  __threadfence_system();
+}
+static void readback(Ctx& c, void* h, const void* d, size_t bytes) {
+  if (!c.ws.allow_latency && bytes % 4 == 0) {  // inside a sliced call
+    k_readback<<<1, 32, 0, c.st>>>(static_cast<uint32_t*>(h), static_cast<const uint32_t*>(d),
+                                   (uint32_t)(bytes / 4));
+    ++c.ws.launches;
+    QD_CUDA(cudaGetLastError());
+    return;
+  }
+  QD_CUDA(cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, c.st));
+}
+
 
 constexpr uint32_t kCounters = 4096;
 
@@ -3774,7 +3804,7 @@ uint64_t find_runs(Ctx& c, const uint32_t* coords, uint32_t rank, uint64_t nnz,
   if (S_dev_out) *S_dev_out = tot;
   uint64_t S = nnz;  // latency mode: the run count stays on the device (bound: nnz)
   if (!c.lat) {
-    QD_CUDA(cudaMemcpyAsync(c.ws.h_small, tot, 8, cudaMemcpyDeviceToHost, c.st));
+    readback(c, c.ws.h_small, tot, 8);
     QD_CUDA(cudaStreamSynchronize(c.st));
     S = c.ws.h_small[0];
   }
@@ -4073,7 +4103,7 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
     k_mode_max<<<grid, kThreads, 0, c.st>>>(src_c, R, N, ml, mx);
     c.launched(kOtherK);
     uint32_t* h = reinterpret_cast<uint32_t*>(ws.h_small);
-    QD_CUDA(cudaMemcpyAsync(h, mx, kMaxKeys * 4, cudaMemcpyDeviceToHost, c.st));
+    readback(c, h, mx, kMaxKeys * 4);
     QD_CUDA(cudaStreamSynchronize(c.st));
     for (size_t i = 0; i < g.keys.size(); ++i) widths[i] = ceil_log2((uint64_t)h[i] + 1);
   }
@@ -4213,7 +4243,7 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
       small_runs = TL != 0;
       lat_counts = totals;
     } else {
-      QD_CUDA(cudaMemcpyAsync(ws.h_small + 1, totals, 24, cudaMemcpyDeviceToHost, c.st));
+      readback(c, ws.h_small + 1, totals, 24);
       QD_CUDA(cudaStreamSynchronize(c.st));
       num_large = ws.h_small[1];
       num_chunks = ws.h_small[2];
@@ -4542,7 +4572,7 @@ void exec_group(Ctx& c, const TensorView& t, const uint32_t* src_c, const double
     c.pre();
     k_probe_runs<<<kProbeBlocks, kThreads, 0, c.st>>>(src_c, R, N, k, heads);
     c.launched(kSegK);
-    QD_CUDA(cudaMemcpyAsync(ws.h_small, heads, 8, cudaMemcpyDeviceToHost, c.st));
+    readback(c, ws.h_small, heads, 8);
     QD_CUDA(cudaStreamSynchronize(c.st));
     const double frac = ((double)ws.h_small[0] + kProbeBlocks) / ((double)kProbeBlocks * kProbeRows);
     const double S_est = std::min(1.0, frac) * (double)N;
@@ -4628,8 +4658,7 @@ void exec_group(Ctx& c, const TensorView& t, const uint32_t* src_c, const double
 // copy = false: the error block's device->host copy is already enqueued
 // (it is the last node of a latency-mode graph)
 static unsigned check_errors(Ctx& c, bool copy = true) {
-  if (copy)
-    QD_CUDA(cudaMemcpyAsync(c.ws.h_err, c.err, sizeof(ErrBlock), cudaMemcpyDeviceToHost, c.st));
+  if (copy) readback(c, c.ws.h_err, c.err, sizeof(ErrBlock));
   QD_CUDA(cudaStreamSynchronize(c.st));
   const ErrBlock e = *c.ws.h_err;
   c.resolve(e);
@@ -4886,7 +4915,7 @@ static void run_groups_once(Workspace& ws, const TensorView& t, const uint32_t* 
     const char* e = getenv("QD_LOCAL_V");
     return e && atoi(e) == 1;
   }();
-  bool lat = lat_on && !local_v1 && N > 0 && N <= kLatRows && !d_boundaries;
+  bool lat = lat_on && ws.allow_latency && !local_v1 && N > 0 && N <= kLatRows && !d_boundaries;
   for (const Group& g : groups) lat &= g.check_range;
   c.lat = lat;
   // one cooperative kernel for the whole call (QD_SMALL=0 disables it)
@@ -5004,6 +5033,167 @@ void run_groups(Workspace& ws, const TensorView& t, const uint32_t* d_c_in, cons
   }
 }
 
+// ---- sliced host-buffer calls ------------------------------------------------
+// When every group of the call sorts within runs of a prefix that contains
+// one common mode m (a target that keeps the leading mode: Alg. 2 all the way,
+// sort.cpp:80-134), rows on different sides of a change of m never meet, so
+// the tensor can be cut at such changes and each slice transposed on its own:
+// slice k's input copy, slice k-1's passes and slice k-2's output copy then
+// overlap (PCIe is full duplex), and the call costs about one direction's
+// copy time instead of both.  The cuts come from the host rows (a gallop and
+// a bisection per cut: any row whose m differs from its predecessor's is a
+// run boundary whether or not the rows are ordered).
+static bool common_prefix_mode(const std::vector<Group>& groups, uint32_t* mode) {
+  if (groups.empty()) return false;
+  for (uint32_t m : groups[0].prefix) {
+    bool all = true;
+    for (const Group& g : groups)
+      all &= std::find(g.prefix.begin(), g.prefix.end(), m) != g.prefix.end();
+    if (all) {
+      *mode = m;
+      return true;
+    }
+  }
+  return false;
+}
+
+// a row index b in [from, N] with coords[b][m] != coords[b-1][m] (N: none found)
+static uint64_t next_cut(const uint32_t* c, uint32_t R, uint32_t m, uint64_t N, uint64_t from) {
+  if (from >= N) return N;
+  const uint32_t a = c[(from - 1) * R + m];
+  if (c[from * R + m] != a) return from;
+  uint64_t lo = from, hi, step = 4096;
+  for (;;) {
+    hi = lo + step;
+    if (hi >= N) {
+      hi = N - 1;
+      if (c[hi * R + m] == a) return N;
+      break;
+    }
+    if (c[hi * R + m] != a) break;
+    lo = hi;
+    step *= 2;
+  }
+  while (hi - lo > 1) {  // c[lo][m] == a, c[hi][m] != a
+    const uint64_t mid = lo + (hi - lo) / 2;
+    if (c[mid * R + m] == a) lo = mid; else hi = mid;
+  }
+  return hi;
+}
+
+constexpr uint64_t kSliceMinRows = 1ull << 25;  // calls below this stay whole
+constexpr uint64_t kSliceRows = (1ull << 24) + 1;  // smallest slice (above the latency regime)
+
+static std::vector<uint64_t> slice_cuts(const TensorView& t, const uint32_t* coords, uint32_t m) {
+  const char* env = getenv("QD_SLICE_ROWS");  // 0: never slice (read per call: tests set it)
+  const int64_t env_rows = env ? atoll(env) : -1;
+  const uint64_t N = t.nnz;
+  std::vector<uint64_t> cuts{0};
+  if (env_rows == 0 || N < (env_rows > 0 ? 2 * (uint64_t)env_rows : kSliceMinRows)) {
+    cuts.push_back(N);
+    return cuts;
+  }
+  const uint64_t S = env_rows > 0 ? (uint64_t)env_rows : std::max<uint64_t>(kSliceRows, N / 24);
+  while (cuts.back() < N) {
+    const uint64_t want = cuts.back() + S;
+    if (want >= N || N - want < S / 2) {
+      cuts.push_back(N);
+      break;
+    }
+    const uint64_t b = next_cut(coords, t.rank, m, N, want);
+    cuts.push_back(N - b < S / 2 ? N : b);
+  }
+  return cuts;
+}
+
+// Pinned host buffers, cuts.size() > 2.  Returns false when a slice raised an
+// error: the caller's rows are then as they were (the slices already copied
+// out are restored from the device's input copy) and the whole-tensor call is
+// redone for the canonical error (the first bad row in PASS order).
+static bool run_slices_pinned(Workspace& ws, const TensorView& t, uint32_t* coords, double* values,
+                              uint32_t* ic, double* iv, uint32_t* oc, double* ov,
+                              const std::vector<Group>& groups, const std::vector<uint64_t>& cuts,
+                              cudaStream_t st) {
+  const uint32_t R = t.rank;
+  const size_t ns = cuts.size() - 1;
+  if (!ws.s_sl_in) {
+    QD_CUDA(cudaStreamCreateWithFlags(&ws.s_sl_in, cudaStreamNonBlocking));
+    QD_CUDA(cudaStreamCreateWithFlags(&ws.s_sl_out, cudaStreamNonBlocking));
+  }
+  while (ws.ev_slices.size() < ns) {
+    cudaEvent_t e;
+    QD_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ws.ev_slices.push_back(e);
+  }
+  static const bool dbg = getenv("QD_HOST_DBG") != nullptr;
+  std::vector<cudaEvent_t> tev;  // QD_HOST_DBG: t0, then per slice {arrived, sorted, out begin, out end}
+  if (dbg) {
+    tev.resize(1 + 4 * ns);
+    for (cudaEvent_t& e : tev) QD_CUDA(cudaEventCreate(&e));
+    QD_CUDA(cudaEventRecord(tev[0], ws.s_sl_in));
+  }
+  for (size_t k = 0; k < ns; ++k) {
+    const uint64_t a = cuts[k], n = cuts[k + 1] - a;
+    QD_CUDA(cudaMemcpyAsync(ic + a * R, coords + a * R, n * R * 4, cudaMemcpyHostToDevice, ws.s_sl_in));
+    QD_CUDA(cudaMemcpyAsync(iv + a, values + a, n * 8, cudaMemcpyHostToDevice, ws.s_sl_in));
+    QD_CUDA(cudaEventRecord(ws.ev_slices[k], ws.s_sl_in));
+    if (dbg) QD_CUDA(cudaEventRecord(tev[1 + 4 * k], ws.s_sl_in));
+  }
+  size_t done = 0;  // slices whose output copy was issued
+  bool ok = true;
+  ws.allow_latency = false;
+  try {
+    for (size_t k = 0; k < ns; ++k) {
+      const uint64_t a = cuts[k], n = cuts[k + 1] - a;
+      const TensorView tv{R, t.dims, n};
+      QD_CUDA(cudaStreamWaitEvent(st, ws.ev_slices[k], 0));
+      // returns with the stream synchronised: the slice's rows are sorted
+      run_groups(ws, tv, ic + a * R, iv + a, oc + a * R, ov + a, groups, false, nullptr, nullptr, 0, st);
+      if (dbg) {
+        QD_CUDA(cudaEventRecord(tev[2 + 4 * k], st));
+        QD_CUDA(cudaEventRecord(tev[3 + 4 * k], ws.s_sl_out));
+      }
+      QD_CUDA(cudaMemcpyAsync(coords + a * R, oc + a * R, n * R * 4, cudaMemcpyDeviceToHost, ws.s_sl_out));
+      QD_CUDA(cudaMemcpyAsync(values + a, ov + a, n * 8, cudaMemcpyDeviceToHost, ws.s_sl_out));
+      if (dbg) QD_CUDA(cudaEventRecord(tev[4 + 4 * k], ws.s_sl_out));
+      done = k + 1;
+    }
+  } catch (const Error& e) {
+    if (e.code != QD_OUT_OF_RANGE && e.code != QD_INVALID_ARGUMENT) {
+      ws.allow_latency = true;
+      cudaStreamSynchronize(ws.s_sl_in);
+      cudaStreamSynchronize(ws.s_sl_out);
+      throw;
+    }
+    ok = false;
+  } catch (...) {
+    ws.allow_latency = true;
+    cudaStreamSynchronize(ws.s_sl_in);
+    cudaStreamSynchronize(ws.s_sl_out);
+    throw;
+  }
+  ws.allow_latency = true;
+  QD_CUDA(cudaStreamSynchronize(ws.s_sl_in));
+  QD_CUDA(cudaStreamSynchronize(ws.s_sl_out));
+  if (dbg) {
+    if (ok)
+      for (size_t k = 0; k < ns; ++k) {
+        float t[4];
+        for (int j = 0; j < 4; ++j) cudaEventElapsedTime(&t[j], tev[0], tev[1 + 4 * k + j]);
+        fprintf(stderr, "  slice %2zu: %10llu rows  arrived %7.1f  sorted %7.1f  out %7.1f .. %7.1f ms\n", k,
+                (unsigned long long)(cuts[k + 1] - cuts[k]), t[0], t[1], t[2], t[3]);
+      }
+    for (cudaEvent_t e : tev) cudaEventDestroy(e);
+  }
+  if (!ok && done) {
+    const uint64_t n = cuts[done];
+    QD_CUDA(cudaMemcpyAsync(coords, ic, n * R * 4, cudaMemcpyDeviceToHost, st));
+    QD_CUDA(cudaMemcpyAsync(values, iv, n * 8, cudaMemcpyDeviceToHost, st));
+    QD_CUDA(cudaStreamSynchronize(st));
+  }
+  return ok;
+}
+
 void run_groups_host(Workspace& ws, const TensorView& t, uint32_t* coords, double* values,
                      const std::vector<Group>& groups, bool verify_input, uint64_t* h_boundaries,
                      uint64_t* n_boundaries, uint32_t boundary_mode) {
@@ -5035,7 +5225,23 @@ void run_groups_host(Workspace& ws, const TensorView& t, uint32_t* coords, doubl
     return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
   };
   double tm[4] = {now(), 0, 0, 0};
-  if (N && stage) {
+  ws.last_slices = 1;
+  bool input_on_device = false;
+  uint32_t cut_mode = 0;
+  if (N && !stage && !verify_input && !h_boundaries && common_prefix_mode(groups, &cut_mode)) {
+    const std::vector<uint64_t> cuts = slice_cuts(t, coords, cut_mode);
+    if (cuts.size() > 2) {
+      ws.last_slices = cuts.size() - 1;
+      if (run_slices_pinned(ws, t, coords, values, ic, iv, oc, ov, groups, cuts, st)) {
+        if (dbg) fprintf(stderr, "host call: %zu slices, %.2f ms\n", cuts.size() - 1, (now() - tm[0]) * 1e3);
+        if (n_boundaries) *n_boundaries = 0;
+        return;
+      }
+      input_on_device = true;  // the whole-tensor call below raises the canonical error
+    }
+  }
+  if (input_on_device) {
+  } else if (N && stage) {
     staged_h2d(ic, coords, N * R * 4, st);
     staged_h2d(iv, values, N * 8, st);
   } else if (N) {

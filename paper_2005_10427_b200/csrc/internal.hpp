@@ -64,6 +64,7 @@ Workspace* workspace_create(int device);
 void workspace_destroy(Workspace* ws);
 uint64_t workspace_bytes(const Workspace* ws);
 uint64_t workspace_launches(const Workspace* ws);
+uint64_t workspace_slices(const Workspace* ws);  // of the last synchronous host-buffer call
 void* workspace_buffer(Workspace& ws, const char* name, size_t bytes);  // cached by name
 int workspace_device(const Workspace& ws);
 int workspace_sms(const Workspace& ws);
