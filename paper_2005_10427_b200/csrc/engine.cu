@@ -41,6 +41,7 @@
 #include <cstdio>
 #include <cstring>
 #include <deque>
+#include <exception>
 #include <map>
 #include <mutex>
 #include <string>
@@ -5106,14 +5107,18 @@ static std::vector<uint64_t> slice_cuts(const TensorView& t, const uint32_t* coo
   return cuts;
 }
 
-// Pinned host buffers, cuts.size() > 2.  Returns false when a slice raised an
-// error: the caller's rows are then as they were (the slices already copied
-// out are restored from the device's input copy) and the whole-tensor call is
-// redone for the canonical error (the first bad row in PASS order).
-static bool run_slices_pinned(Workspace& ws, const TensorView& t, uint32_t* coords, double* values,
-                              uint32_t* ic, double* iv, uint32_t* oc, double* ov,
-                              const std::vector<Group>& groups, const std::vector<uint64_t>& cuts,
-                              cudaStream_t st) {
+// cuts.size() > 2.  Pinned host buffers (stage = false): every slice's input
+// copy is enqueued up front and each output copy as soon as its slice is
+// sorted.  Pageable buffers (stage = true): a feeder thread stages the input
+// slices through its pinned chunk ring (tns.cu) while this thread runs each
+// arrived slice's passes and stages its rows out.  Returns false when a slice
+// raised an error: the caller's rows are then as they were (the slices already
+// copied out are restored from the device's input copy) and the whole-tensor
+// call is redone for the canonical error (the first bad row in PASS order).
+static bool run_slices(Workspace& ws, const TensorView& t, uint32_t* coords, double* values,
+                       uint32_t* ic, double* iv, uint32_t* oc, double* ov,
+                       const std::vector<Group>& groups, const std::vector<uint64_t>& cuts,
+                       cudaStream_t st, bool stage) {
   const uint32_t R = t.rank;
   const size_t ns = cuts.size() - 1;
   if (!ws.s_sl_in) {
@@ -5132,13 +5137,54 @@ static bool run_slices_pinned(Workspace& ws, const TensorView& t, uint32_t* coor
     for (cudaEvent_t& e : tev) QD_CUDA(cudaEventCreate(&e));
     QD_CUDA(cudaEventRecord(tev[0], ws.s_sl_in));
   }
-  for (size_t k = 0; k < ns; ++k) {
+  // slices whose input copy has been enqueued (staged: by the feeder thread)
+  std::mutex fmu;
+  std::condition_variable fcv;
+  size_t fed = 0;
+  std::exception_ptr feed_err;
+  auto feed = [&](size_t k) {
     const uint64_t a = cuts[k], n = cuts[k + 1] - a;
-    QD_CUDA(cudaMemcpyAsync(ic + a * R, coords + a * R, n * R * 4, cudaMemcpyHostToDevice, ws.s_sl_in));
-    QD_CUDA(cudaMemcpyAsync(iv + a, values + a, n * 8, cudaMemcpyHostToDevice, ws.s_sl_in));
+    if (stage) {
+      staged_h2d(ic + a * R, coords + a * R, n * R * 4, ws.s_sl_in);
+      staged_h2d(iv + a, values + a, n * 8, ws.s_sl_in);
+    } else {
+      QD_CUDA(cudaMemcpyAsync(ic + a * R, coords + a * R, n * R * 4, cudaMemcpyHostToDevice, ws.s_sl_in));
+      QD_CUDA(cudaMemcpyAsync(iv + a, values + a, n * 8, cudaMemcpyHostToDevice, ws.s_sl_in));
+    }
     QD_CUDA(cudaEventRecord(ws.ev_slices[k], ws.s_sl_in));
     if (dbg) QD_CUDA(cudaEventRecord(tev[1 + 4 * k], ws.s_sl_in));
+  };
+  std::thread feeder;
+  if (stage) {
+    feeder = std::thread([&] {
+      try {
+        QD_CUDA(cudaSetDevice(ws.device));
+        for (size_t k = 0; k < ns; ++k) {
+          feed(k);
+          {
+            std::lock_guard<std::mutex> lk(fmu);
+            fed = k + 1;
+          }
+          fcv.notify_all();
+        }
+      } catch (...) {
+        std::lock_guard<std::mutex> lk(fmu);
+        feed_err = std::current_exception();
+        fcv.notify_all();
+      }
+    });
+  } else {
+    for (size_t k = 0; k < ns; ++k) feed(k);
+    fed = ns;
   }
+  // every exit joins the feeder (it always feeds all slices: the whole-tensor
+  // redo after an error needs the full input on the device)
+  struct Join {
+    std::thread& t;
+    ~Join() {
+      if (t.joinable()) t.join();
+    }
+  } join_feeder{feeder};
   size_t done = 0;  // slices whose output copy was issued
   bool ok = true;
   ws.allow_latency = false;
@@ -5146,6 +5192,11 @@ static bool run_slices_pinned(Workspace& ws, const TensorView& t, uint32_t* coor
     for (size_t k = 0; k < ns; ++k) {
       const uint64_t a = cuts[k], n = cuts[k + 1] - a;
       const TensorView tv{R, t.dims, n};
+      if (stage) {
+        std::unique_lock<std::mutex> lk(fmu);
+        fcv.wait(lk, [&] { return fed > k || feed_err; });
+        if (feed_err) std::rethrow_exception(feed_err);
+      }
       QD_CUDA(cudaStreamWaitEvent(st, ws.ev_slices[k], 0));
       // returns with the stream synchronised: the slice's rows are sorted
       run_groups(ws, tv, ic + a * R, iv + a, oc + a * R, ov + a, groups, false, nullptr, nullptr, 0, st);
@@ -5153,12 +5204,18 @@ static bool run_slices_pinned(Workspace& ws, const TensorView& t, uint32_t* coor
         QD_CUDA(cudaEventRecord(tev[2 + 4 * k], st));
         QD_CUDA(cudaEventRecord(tev[3 + 4 * k], ws.s_sl_out));
       }
-      QD_CUDA(cudaMemcpyAsync(coords + a * R, oc + a * R, n * R * 4, cudaMemcpyDeviceToHost, ws.s_sl_out));
-      QD_CUDA(cudaMemcpyAsync(values + a, ov + a, n * 8, cudaMemcpyDeviceToHost, ws.s_sl_out));
+      done = k + 1;  // (a staged copy-out that fails part-way is restored too)
+      if (stage) {
+        const StageSeg segs[2] = {{coords + a * R, oc + a * R, n * R * 4}, {values + a, ov + a, n * 8}};
+        staged_d2h_multi(segs, 2, ws.s_sl_out);
+      } else {
+        QD_CUDA(cudaMemcpyAsync(coords + a * R, oc + a * R, n * R * 4, cudaMemcpyDeviceToHost, ws.s_sl_out));
+        QD_CUDA(cudaMemcpyAsync(values + a, ov + a, n * 8, cudaMemcpyDeviceToHost, ws.s_sl_out));
+      }
       if (dbg) QD_CUDA(cudaEventRecord(tev[4 + 4 * k], ws.s_sl_out));
-      done = k + 1;
     }
   } catch (const Error& e) {
+    if (feeder.joinable()) feeder.join();
     if (e.code != QD_OUT_OF_RANGE && e.code != QD_INVALID_ARGUMENT) {
       ws.allow_latency = true;
       cudaStreamSynchronize(ws.s_sl_in);
@@ -5167,10 +5224,16 @@ static bool run_slices_pinned(Workspace& ws, const TensorView& t, uint32_t* coor
     }
     ok = false;
   } catch (...) {
+    if (feeder.joinable()) feeder.join();
     ws.allow_latency = true;
     cudaStreamSynchronize(ws.s_sl_in);
     cudaStreamSynchronize(ws.s_sl_out);
     throw;
+  }
+  if (feeder.joinable()) feeder.join();
+  if (feed_err) {
+    ws.allow_latency = true;
+    std::rethrow_exception(feed_err);
   }
   ws.allow_latency = true;
   QD_CUDA(cudaStreamSynchronize(ws.s_sl_in));
@@ -5187,8 +5250,13 @@ static bool run_slices_pinned(Workspace& ws, const TensorView& t, uint32_t* coor
   }
   if (!ok && done) {
     const uint64_t n = cuts[done];
-    QD_CUDA(cudaMemcpyAsync(coords, ic, n * R * 4, cudaMemcpyDeviceToHost, st));
-    QD_CUDA(cudaMemcpyAsync(values, iv, n * 8, cudaMemcpyDeviceToHost, st));
+    if (stage) {
+      const StageSeg segs[2] = {{coords, ic, n * R * 4}, {values, iv, n * 8}};
+      staged_d2h_multi(segs, 2, st);
+    } else {
+      QD_CUDA(cudaMemcpyAsync(coords, ic, n * R * 4, cudaMemcpyDeviceToHost, st));
+      QD_CUDA(cudaMemcpyAsync(values, iv, n * 8, cudaMemcpyDeviceToHost, st));
+    }
     QD_CUDA(cudaStreamSynchronize(st));
   }
   return ok;
@@ -5228,11 +5296,15 @@ void run_groups_host(Workspace& ws, const TensorView& t, uint32_t* coords, doubl
   ws.last_slices = 1;
   bool input_on_device = false;
   uint32_t cut_mode = 0;
-  if (N && !stage && !verify_input && !h_boundaries && common_prefix_mode(groups, &cut_mode)) {
+  // (pageable buffers: measured no gain — the staged copies are bound by the
+  // host's copy threads, 1598 vs 1548 ms on c5 (0,2,1) — so QD_SLICE_PAGEABLE=1 only)
+  const char* sp_env = getenv("QD_SLICE_PAGEABLE");
+  const bool slice_ok = !stage || (sp_env && atoi(sp_env) != 0);
+  if (N && slice_ok && !verify_input && !h_boundaries && common_prefix_mode(groups, &cut_mode)) {
     const std::vector<uint64_t> cuts = slice_cuts(t, coords, cut_mode);
     if (cuts.size() > 2) {
       ws.last_slices = cuts.size() - 1;
-      if (run_slices_pinned(ws, t, coords, values, ic, iv, oc, ov, groups, cuts, st)) {
+      if (run_slices(ws, t, coords, values, ic, iv, oc, ov, groups, cuts, st, stage)) {
         if (dbg) fprintf(stderr, "host call: %zu slices, %.2f ms\n", cuts.size() - 1, (now() - tm[0]) * 1e3);
         if (n_boundaries) *n_boundaries = 0;
         return;

@@ -1,9 +1,9 @@
-"""Sliced host-buffer calls (engine.cu run_groups_host / run_slices_pinned):
+"""Sliced host-buffer calls (engine.cu run_groups_host / run_slices):
 when every pass of a call keeps a common prefix mode (Alg. 2 only,
-sort.cpp:80-134), qd_transpose_inplace on pinned host buffers cuts the tensor
-where that mode changes and pipelines the slices' input copies, passes and
-output copies.  The rows must be the oracle's, bit for bit, however the
-tensor is cut; an error must leave the caller's rows untouched and be the
+sort.cpp:80-134), qd_transpose_inplace on host buffers (pinned: direct copies;
+pageable: staged by a feeder thread) cuts the tensor where that mode changes
+and pipelines the slices' input copies, passes and output copies.  The rows
+must be the oracle's, bit for bit, however the tensor is cut; an error must leave the caller's rows untouched and be the
 whole-tensor call's error."""
 import os
 
@@ -13,8 +13,10 @@ import pytest
 from pyoracle import Oracle
 
 
-def _pinned_tensor(qb, dims, c, v):
+def _pinned_tensor(qb, dims, c, v, pinned=True):
     import torch
+    if not pinned:  # pageable buffers: staged through the pinned chunk ring by a feeder thread
+        return qb.CooTensor(dims, c.copy(), v.copy())
     tc = torch.empty(len(c), dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
     tv = torch.empty(len(v), dtype=torch.float64, pin_memory=True).numpy()
     tc[:] = c
@@ -36,10 +38,12 @@ def _rows(n, dims, seed, head=0.0):
 @pytest.fixture
 def slice_rows():
     old = os.environ.get("QD_SLICE_ROWS")
+    os.environ["QD_SLICE_PAGEABLE"] = "1"  # pageable buffers are sliced on request only
 
     def set_(v):
         os.environ["QD_SLICE_ROWS"] = str(v)
     yield set_
+    os.environ.pop("QD_SLICE_PAGEABLE", None)
     if old is None:
         os.environ.pop("QD_SLICE_ROWS", None)
     else:
@@ -54,7 +58,8 @@ def slice_rows():
     ([40, 50, 60, 70], [0, 1, 3, 2], 0.1),
     ([7, 9, 50, 60, 70], [0, 1, 4, 2, 3], 0.0),
 ])
-def test_sliced_matches_oracle(slice_rows, dims, target, head):
+@pytest.mark.parametrize("pinned", [True, False])
+def test_sliced_matches_oracle(slice_rows, dims, target, head, pinned):
     import paper_2005_10427_b200 as qb
     n = 400_000
     c, v = _rows(n, dims, 11, head)
@@ -62,7 +67,7 @@ def test_sliced_matches_oracle(slice_rows, dims, target, head):
     rc, rv, _ = Oracle().transpose(dims, c, v, target)
     for rows in (30_000, 7_001, 150_000):
         slice_rows(rows)
-        t = _pinned_tensor(qb, dims, c, v)
+        t = _pinned_tensor(qb, dims, c, v, pinned)
         qb.transpose_inplace(t, target, qb.SortStrategy.quesadilla(), ws)
         assert ws.slices() > 1, "the call was not sliced"
         assert np.array_equal(t.coords, rc)
@@ -115,7 +120,8 @@ def test_sliced_unordered_rows(slice_rows):
 
 
 @pytest.mark.gpu
-def test_sliced_error_leaves_rows_untouched(slice_rows):
+@pytest.mark.parametrize("pinned", [True, False])
+def test_sliced_error_leaves_rows_untouched(slice_rows, pinned):
     import paper_2005_10427_b200 as qb
     dims = [300, 2000, 4000]
     n = 300_000
@@ -128,7 +134,7 @@ def test_sliced_error_leaves_rows_untouched(slice_rows):
     errs = []
     for rows in (0, 25_000):
         slice_rows(rows)
-        t = _pinned_tensor(qb, dims, bad, v)
+        t = _pinned_tensor(qb, dims, bad, v, pinned)
         with pytest.raises(qb.OutOfRange) as ei:
             qb.transpose_inplace(t, [0, 2, 1], qb.SortStrategy.quesadilla(), ws)
         assert np.array_equal(t.coords, bad), "rows changed by a failed call"
