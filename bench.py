@@ -655,6 +655,7 @@ def run_e2e(args, cfg, qd, ws, hc0, hv0, r, n):
     tens = qd.CooTensor(cfg.dims, hc, hv)  # wraps the pinned buffers
     strat = qd.SortStrategy.quesadilla()
     secs = 0.0
+    per_t = {tname(t): {"ms": 0.0, "slices": 1} for t in cfg.targets}
     for it in range(1 + k_e2e):  # one untimed warm-up step (workspace growth)
         for t in cfg.targets:
             wc.copy_(torch.from_numpy(hc0.view(np.int32)))
@@ -664,6 +665,12 @@ def run_e2e(args, cfg, qd, ws, hc0, hv0, r, n):
             dt = time.perf_counter() - t0
             if it:
                 secs += dt
+                per_t[tname(t)]["ms"] += dt * 1e3 / k_e2e
+                # > 1: the call kept the leading mode, so the library cut the tensor
+                # where it changes and pipelined H2D / passes / D2H per slice
+                per_t[tname(t)]["slices"] = ws.slices()
+    for v in per_t.values():
+        v["ms"] = round(v["ms"], 2)
     last = hc.reshape(-1, r)
     m = min(len(last), 1 << 21)
     for a in (0, len(last) - m):  # spot check: host output sorted under the last target
@@ -696,6 +703,7 @@ def run_e2e(args, cfg, qd, ws, hc0, hv0, r, n):
             "timing": "host wall clock around each synchronous call (every H2D/D2H byte "
                       "inside), summed over the step's targets",
             "api": "qd_transpose_inplace (pinned host buffers) x targets",
+            "per_target": per_t,
             "pageable": pageable}
 
 

@@ -4793,7 +4793,7 @@ static void launch_groups(Ctx& c, const TensorView& t, const uint32_t* d_c_in,
   Workspace& ws = c.ws;
   const uint64_t N = t.nnz;
   const uint32_t R = t.rank;
-  if (c.lat) {
+  if (c.lat && !c.small) {
     // look-back scan state from tile 0 each call (graph-replayable)
     if (!ws.lb_ticket) ws.lb_ticket = ws.get<unsigned long long>("lb_ticket", 1);
     QD_CUDA(cudaMemsetAsync(ws.lb_ticket, 0, 8, c.st));
@@ -4935,6 +4935,21 @@ static void run_groups_once(Workspace& ws, const TensorView& t, const uint32_t* 
     launch_groups(c, t, d_c_in, d_v_in, d_c_out, d_v_out, groups, verify_input, d_boundaries,
                   n_boundaries, boundary_mode);
   };
+  // k_small alone: no graph and no copy nodes around the kernel — the error
+  // block lives in the pinned host block (reset by a host store; the kernel
+  // only ever raises its redo flag there, through the device mapping), so the
+  // call is one cooperative launch and one stream synchronisation
+  static const bool small_direct = [] {
+    const char* e = getenv("QD_SMALL_DIRECT");
+    return !(e && atoi(e) == 0);
+  }();
+  if (c.small && small_direct && !verify_input && !ws.prof && !getenv("QD_SMALL_DBG")) {
+    *ws.h_err = *ws.h_err_init;
+    c.err = ws.h_err;
+    eager();
+    *flags = check_errors(c, false);
+    return;
+  }
   // the legacy / per-thread default streams cannot be captured
   const bool capturable = c.st != nullptr && c.st != cudaStreamLegacy && c.st != cudaStreamPerThread;
   if (lat && graphs_on && !ws.prof && capturable) {

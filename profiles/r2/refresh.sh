@@ -14,6 +14,8 @@ for c in c2 c3 c4 c1; do
 done
 python profiles/r2/latency.py --config c1 > gpurun_out/r2_latency_c1.log 2>&1
 python profiles/r2/latency.py --config c4 > gpurun_out/r2_latency_c4.log 2>&1
+# the sliced host-buffer call on c5 (0,2,1) with its per-slice timeline, whole-tensor call beside it
+QD_HOST_DBG=1 python profiles/r2/e2e_sliced.py 2 > gpurun_out/r2_e2e_sliced.log 2>&1
 # launch list of one transposition per target of the bench workload (c5, full size)
 python profiles/r2/prof_targets.py --config c5 > /dev/null 2>&1 || exit 1
 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \

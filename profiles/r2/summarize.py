@@ -9,6 +9,7 @@ tracked round-2 files:
   profiles/r2/launches_summary.txt   per-target time by kernel from that list (cold, serialised)
   profiles/r2/ncu_full_summary.txt   ncu --set full metrics per launch (c5 shape, 200M rows)
   profiles/ncu_traffic.json          k_scatter DRAM bytes per row (bench.py's roofline.traffic)
+  profiles/r2/e2e_sliced.txt         sliced vs whole host-buffer call on c5 (0,2,1), per-slice timeline
 """
 import collections
 import csv
@@ -51,6 +52,15 @@ def main():
             p = os.path.join(RAW, f"r2_latency_{c}.log")
             if os.path.exists(p):
                 f.write(f"latency {c}: " + open(p).read().strip().splitlines()[-1] + "\n")
+    p = os.path.join(RAW, "r2_e2e_sliced.log")
+    if os.path.exists(p):
+        lines = open(p).read().splitlines()
+        last = max(i for i, l in enumerate(lines) if l.startswith("  slice  0:"))
+        keep = [l for l in lines if l.startswith("QD_SLICE_ROWS")] + ["# per-slice timeline of the last sliced call "
+                "(ms from the first input copy; CUDA events)"] + [l for l in lines[last:] if l.startswith("  slice")]
+        with open(os.path.join(OUT, "e2e_sliced.txt"), "w") as f:
+            f.write("# profiles/r2/e2e_sliced.py: qd_transpose_inplace on pinned host buffers, c5 (0,2,1) at full size; "
+                    "QD_SLICE_ROWS=0 = the whole-tensor call\n" + "\n".join(keep) + "\n")
     # launch list
     shutil.copy(os.path.join(RAW, "r2_launches_c5.csv"), os.path.join(OUT, "launches_c5.csv"))
     with open(os.path.join(OUT, "launches_c5.csv")) as f:
