@@ -370,6 +370,8 @@ class Workspace {
   qd_workspace* get() const { return ws_; }
   // wait for every transpose_inplace_async on this workspace
   void synchronize() { detail::check(qd_workspace_synchronize(ws_)); }
+  // slices the last synchronous host-buffer call was pipelined in (1: whole tensor)
+  std::uint64_t slices() const { return qd_workspace_slices(ws_); }
 
  private:
   qd_workspace* ws_ = nullptr;
