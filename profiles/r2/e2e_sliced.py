@@ -32,7 +32,7 @@ PAGEABLE = os.environ.get("PAGEABLE")
 if PAGEABLE:
     wc, wv = torch.empty(wc.shape, dtype=torch.int32), torch.empty(wv.shape, dtype=torch.float64)
     tens = qd.CooTensor(cfg.dims, wc.numpy().view(np.uint32), wv.numpy())
-for env in ("0", None, "0", None):
+for env in ((None, "0", None) if os.environ.get("FIRST_SLICED") else ("0", None, "0", None)):
     if env is None:
         os.environ.pop("QD_SLICE_ROWS", None)
     else:
