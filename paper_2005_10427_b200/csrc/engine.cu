@@ -2733,11 +2733,49 @@ struct ModeList {
 };
 
 // head bit of row i = 1 iff i == 0 or row i differs from row i-1 on `modes`.
+// Optional second job of k_heads for a bucketed group's first digit pass: the
+// rows stream through this kernel anyway (the prefix column's sectors hold the
+// whole AoS row), so it also range-checks the key coordinates (count_keys,
+// sort.cpp:54-64), checks that the row packs, and leaves the first digit of
+// every row as a byte — the first k_chunk_hist then reads 1 byte per row
+// instead of the coordinates again (c5 (0,2,1): 20.9 GB less to read).
+struct HeadsExtra {
+  uint8_t* digits;  // nullptr: run discovery only
+  ErrBlock* err;
+  int do_check, check_pack;
+  uint32_t pack_lim[kMaxKeys];
+  DigitSpec dig;
+  KeySpec key;
+};
+
+__device__ __forceinline__ void heads_extra_row(const HeadsExtra& x, const Dig2& dg, bool fast,
+                                                const uint32_t* c, uint32_t rank,
+                                                unsigned long long i) {
+  const uint32_t* row = c + i * rank;
+  if (x.do_check) {
+    bool bad = false;
+#pragma unroll 1
+    for (uint32_t k = 0; k < x.key.n; ++k) bad |= __ldg(row + x.key.mode[k]) >= x.key.dim[k];
+    if (bad) check_row(row, x.key, i, x.err);
+  }
+  if (x.check_pack) {
+    uint32_t bad = 0;
+#pragma unroll 1
+    for (uint32_t m = 0; m < rank; ++m) bad |= __ldg(row + m) >= x.pack_lim[m];
+    if (bad) atomicOr(&x.err->flags, 4u);
+  }
+  auto get = [&](uint32_t m) { return __ldg(row + m); };
+  x.digits[i] = (uint8_t)(fast ? digit2(get, dg) : digit_by(get, x.dig));
+}
+
 __global__ void __launch_bounds__(kThreads) k_heads(const uint32_t* c, uint32_t rank,
                                                     uint64_t nnz, ModeList modes,
-                                                    uint32_t* words, uint32_t* block_cnt) {
+                                                    uint32_t* words, uint32_t* block_cnt,
+                                                    HeadsExtra ex) {
   const unsigned long long r0 = (unsigned long long)blockIdx.x * kHeadRows;
   uint32_t cnt = 0;
+  const bool ex_fast = ex.dig.lookup == nullptr && ex.dig.n <= 2;
+  const Dig2 ex_dg = dig2_of(ex.dig);
   if (modes.n == 1) {
     // one prefix mode: each row's coordinate is loaded once (all rounds'
     // loads in flight together); the previous row's comes from lane - 1
@@ -2762,6 +2800,7 @@ __global__ void __launch_bounds__(kThreads) k_heads(const uint32_t* c, uint32_t 
         const unsigned bits = __ballot_sync(0xFFFFFFFFu, head);
         if (lane == 0 && i < nnz) words[i >> 5] = bits;
         cnt += head;
+        if (ex.digits && i < nnz) heads_extra_row(ex, ex_dg, ex_fast, c, rank, i);
       }
     }
   } else
@@ -2782,6 +2821,7 @@ __global__ void __launch_bounds__(kThreads) k_heads(const uint32_t* c, uint32_t 
     if ((threadIdx.x & 31) == 0 && r0 + k * kThreads + threadIdx.x < nnz)
       words[(r0 + k * kThreads + threadIdx.x) >> 5] = bits;
     cnt += head;
+    if (ex.digits && i < nnz) heads_extra_row(ex, ex_dg, ex_fast, c, rank, i);
   }
   __shared__ uint32_t s_tmp[64];
   uint32_t tot;
@@ -3800,7 +3840,7 @@ void scan_exclusive(Ctx& c, const uint32_t* in, uint64_t n, unsigned long long* 
 // (device, seg_start[S] = nnz) and returns S (host sync).
 uint64_t find_runs(Ctx& c, const uint32_t* coords, uint32_t rank, uint64_t nnz,
                    const std::vector<uint32_t>& modes, unsigned long long** seg_out,
-                   unsigned long long** S_dev_out = nullptr) {
+                   unsigned long long** S_dev_out = nullptr, const HeadsExtra* extra = nullptr) {
   NvtxRange r_runs("run discovery");
   ModeList ml{};
   ml.n = (uint32_t)modes.size();
@@ -3811,7 +3851,7 @@ uint64_t find_runs(Ctx& c, const uint32_t* coords, uint32_t rank, uint64_t nnz,
   auto* boff = c.ws.get<unsigned long long>("head_boff", nb + 1);
   auto* tot = c.ws.get<unsigned long long>("head_total", 1);
   c.pre();
-  k_heads<<<nb, kThreads, 0, c.st>>>(coords, rank, nnz, ml, words, bcnt);
+  k_heads<<<nb, kThreads, 0, c.st>>>(coords, rank, nnz, ml, words, bcnt, extra ? *extra : HeadsExtra{});
   c.launched(kSegK);
   scan_exclusive(c, bcnt, nb, boff, tot);
   if (S_dev_out) *S_dev_out = tot;
@@ -4192,6 +4232,45 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
   const unsigned long long* lat_counts = nullptr;  // latency mode: {large runs, chunks, items}
   const uint32_t* local_maxrun = nullptr;            // per local chunk: its longest small run
 
+  // Intermediate rows: packed 16-byte rows when every coordinate packs into
+  // one u64 (key fields at their key offsets, so a digit is shift + mask),
+  // else AoS rows.  A coordinate that would not pack losslessly (only
+  // possible for modes the plan never range-checks) is flagged by the first
+  // pass over the rows and the whole call is redone unpacked (run_groups).
+  // (Decided before run discovery, which does that first pass's checks for a
+  // bucketed group; a bucketed group's passes always have their runs' table.)
+  PackSpec pack{};
+  bool packed = ws.allow_pack && g.check_range && D > 1;
+  const bool have_runs = !g.prefix.empty();
+  if (packed) {
+    // prefix modes are constant within a run: when the row does not pack
+    // otherwise, leave them out and restore them from the run
+    // QD_PACK_ORDER=1 (default): plain bit fields with the prefix restored
+    // from the run before a mixed-radix word (no division in the
+    // unpacking pass; c5 (0,2,1) 59.3 -> 58.6 ms); 0: mixed radix first
+    static const int pack_order = [] {
+      const char* e = getenv("QD_PACK_ORDER");
+      return e ? atoi(e) : 1;
+    }();
+    if (pack_order == 1)
+      packed = make_pack(key, R, t.dims, &pack, {}, false) ||
+               (have_runs && make_pack(key, R, t.dims, &pack, g.prefix, false)) ||
+               make_pack(key, R, t.dims, &pack) ||
+               (have_runs && make_pack(key, R, t.dims, &pack, g.prefix));
+    else
+      packed = make_pack(key, R, t.dims, &pack) ||
+               (have_runs && make_pack(key, R, t.dims, &pack, g.prefix));
+  }
+  // unpacked intermediates: AoS rows (two streams) and the digit side
+  // channel, or (QD_SOA_INTERMEDIATES=1) SoA columns whose histogram reads
+  // the key column
+  static const bool unpacked_soa = [] {
+    const char* e = getenv("QD_SOA_INTERMEDIATES");
+    return e && atoi(e) == 1;
+  }();
+  const bool side = packed || !unpacked_soa;
+  bool fused_first = false;  // the first digit bytes were written by run discovery
+
   if (g.prefix.empty()) {
     if (TL && N <= TL) {
       LocalArgs la{src_c, src_v, dst_c, dst_v, R, N, TL, (uint32_t)N, nullptr, 1, key, c.err,
@@ -4210,7 +4289,28 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
     c.launched(kSegK);
   } else {
     unsigned long long* S_found = nullptr;
-    S = find_runs(c, src_c, R, N, g.prefix, &seg, &S_found);  // latency mode: a bound (N)
+    // QD_FUSE_HEADS=1: run discovery also range-checks, pack-checks and
+    // leaves every row's first digit as a byte, so the first histogram reads
+    // 1 byte per row instead of the coordinates again (HeadsExtra).  Measured
+    // SLOWER and off by default: the per-row strided loads and byte stores
+    // cost k_heads more than the histogram saves (c5 (0,2,1) 58.4 -> 62.3 ms,
+    // c2 (0,2,1) 2.17 -> 2.33 ms, c3 (0,3,1,2) 4.03 -> 4.24 ms).
+    static const bool fuse_heads = [] {
+      const char* e = getenv("QD_FUSE_HEADS");
+      return e && atoi(e) == 1;
+    }();
+    HeadsExtra hx{};
+    if (fuse_heads && side) {
+      hx.digits = ws.get<uint8_t>("digits", N + 16);
+      hx.err = c.err;
+      hx.do_check = key.check;
+      hx.check_pack = packed;
+      for (uint32_t m = 0; m < R; ++m) hx.pack_lim[m] = packed ? pack.lim[m] : 0xFFFFFFFFu;
+      hx.dig = digs[0];
+      hx.key = key;
+      fused_first = true;
+    }
+    S = find_runs(c, src_c, R, N, g.prefix, &seg, &S_found, hx.digits ? &hx : nullptr);  // latency mode: a bound (N)
     auto* is_large = ws.get<uint32_t>("run_large", S + 1);
     auto* nch = ws.get<uint32_t>("run_nchunks", S + 1);
     auto* loff = ws.get<unsigned long long>("run_loff", S + 1);
@@ -4276,32 +4376,6 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
   }
 
   if (num_chunks) {
-    // Intermediate rows: packed 16-byte rows when every coordinate packs into
-    // one u64 (key fields at their key offsets, so a digit is shift + mask),
-    // else SoA columns.  A coordinate that would not pack losslessly (only
-    // possible for modes the plan never range-checks) is flagged by the
-    // first histogram and the whole call is redone unpacked (run_groups).
-    PackSpec pack{};
-    bool packed = ws.allow_pack && g.check_range && D > 1;
-    if (packed) {
-      // prefix modes are constant within a run: when the row does not pack
-      // otherwise, leave them out and restore them from the run
-      // QD_PACK_ORDER=1 (default): plain bit fields with the prefix restored
-      // from the run before a mixed-radix word (no division in the
-      // unpacking pass; c5 (0,2,1) 59.3 -> 58.6 ms); 0: mixed radix first
-      static const int pack_order = [] {
-        const char* e = getenv("QD_PACK_ORDER");
-        return e ? atoi(e) : 1;
-      }();
-      if (pack_order == 1)
-        packed = make_pack(key, R, t.dims, &pack, {}, false) ||
-                 (run_start && make_pack(key, R, t.dims, &pack, g.prefix, false)) ||
-                 make_pack(key, R, t.dims, &pack) ||
-                 (run_start && make_pack(key, R, t.dims, &pack, g.prefix));
-      else
-        packed = make_pack(key, R, t.dims, &pack) ||
-                 (run_start && make_pack(key, R, t.dims, &pack, g.prefix));
-    }
     uint32_t* run_prefix = nullptr;
     if (packed && pack.n_imp) {
       run_prefix = ws.get<uint32_t>("run_prefix", num_large * pack.n_imp + 1);
@@ -4325,15 +4399,7 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
       pk[0] = ws.get<uint32_t>("pkA", N * 4);
       if (D > 2) pk[1] = ws.get<uint32_t>("pkB", N * 4);
     }
-    // unpacked intermediates: AoS rows (two streams) and the digit side
-    // channel, or (QD_SOA_INTERMEDIATES=1) SoA columns whose histogram reads
-    // the key column
-    static const bool unpacked_soa = [] {
-      const char* e = getenv("QD_SOA_INTERMEDIATES");
-      return e && atoi(e) == 1;
-    }();
-    const bool side = packed || !unpacked_soa;
-    uint8_t* digbuf = side && D > 1 ? ws.get<uint8_t>("digits", N + 16) : nullptr;
+    uint8_t* digbuf = (side && D > 1) || fused_first ? ws.get<uint8_t>("digits", N + 16) : nullptr;
     Rows in{src_c, src_v, kAoS};
     for (uint32_t q = 0; q < D; ++q) {
       const bool last = q + 1 == D;
@@ -4344,7 +4410,7 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
       const uint32_t lo = q * per, hi = std::min(bits, lo + per);
       // packed passes hand the next pass its digit bytes (1 B/row instead of
       // re-reading 16 B rows for the next histogram)
-      const uint8_t* dig_in = (side && q > 0) ? digbuf : nullptr;
+      const uint8_t* dig_in = (side && (q > 0 || fused_first)) ? digbuf : nullptr;
       uint8_t* dig_out = (side && !last) ? digbuf : nullptr;
       const uint32_t nlo = (q + 1) * per, nhi = std::min(bits, nlo + per);
       // packed-row passes afford a larger tile (16-byte staged rows)
@@ -5033,31 +5099,29 @@ void run_groups(Workspace& ws, const TensorView& t, const uint32_t* d_c_in, cons
   unsigned flags = 0;
   run_groups_once(ws, t, d_c_in, d_v_in, d_c_out, d_v_out, groups, verify_input, d_boundaries,
                   n_boundaries, boundary_mode, stream, &flags);
+  // both switches are restored on every exit; a call whose k_small attempt
+  // failed keeps k_small off for its unpacked redo too (the second redo used
+  // to try k_small again and ignore its flag)
+  struct Restore {
+    Workspace& ws;
+    ~Restore() {
+      ws.allow_small = true;
+      ws.allow_pack = true;
+    }
+  } restore{ws};
   if (flags & 8u) {
     // k_small's preconditions failed (rows not ordered by the group prefix,
     // or a composite coordinate out of range): the general path
     ws.allow_small = false;
-    try {
-      run_groups_once(ws, t, d_c_in, d_v_in, d_c_out, d_v_out, groups, verify_input,
-                      d_boundaries, n_boundaries, boundary_mode, stream, &flags);
-    } catch (...) {
-      ws.allow_small = true;
-      throw;
-    }
-    ws.allow_small = true;
+    run_groups_once(ws, t, d_c_in, d_v_in, d_c_out, d_v_out, groups, verify_input, d_boundaries,
+                    n_boundaries, boundary_mode, stream, &flags);
   }
   if (flags & 4u) {
     // a coordinate of a mode the plan never range-checks does not fit its
-    // packed field: redo the call with unpacked (SoA) intermediates
+    // packed field: redo the call with unpacked intermediates
     ws.allow_pack = false;
-    try {
-      run_groups_once(ws, t, d_c_in, d_v_in, d_c_out, d_v_out, groups, verify_input,
-                      d_boundaries, n_boundaries, boundary_mode, stream, &flags);
-    } catch (...) {
-      ws.allow_pack = true;
-      throw;
-    }
-    ws.allow_pack = true;
+    run_groups_once(ws, t, d_c_in, d_v_in, d_c_out, d_v_out, groups, verify_input, d_boundaries,
+                    n_boundaries, boundary_mode, stream, &flags);
   }
 }
 
@@ -5370,12 +5434,6 @@ void run_groups_host(Workspace& ws, const TensorView& t, uint32_t* coords, doubl
   if (N && stage) {
     const StageSeg segs[2] = {{coords, oc, N * R * 4}, {values, ov, N * 8}};
     staged_d2h_multi(segs, 2, st);
-    if (dbg) {
-      QD_CUDA(cudaStreamSynchronize(st));
-      tm[3] = now();
-      fprintf(stderr, "host call: h2d %.2f ms, device %.2f ms, d2h %.2f ms\n", (tm[1] - tm[0]) * 1e3,
-              (tm[2] - tm[1]) * 1e3, (tm[3] - tm[2]) * 1e3);
-    }
   } else if (N) {
     QD_CUDA(cudaMemcpyAsync(coords, oc, N * R * 4, cudaMemcpyDeviceToHost, st));
     QD_CUDA(cudaMemcpyAsync(values, ov, N * 8, cudaMemcpyDeviceToHost, st));
@@ -5383,6 +5441,12 @@ void run_groups_host(Workspace& ws, const TensorView& t, uint32_t* coords, doubl
   if (N) {
     if (db && nb) QD_CUDA(cudaMemcpyAsync(h_boundaries, db, nb * 8, cudaMemcpyDeviceToHost, st));
     QD_CUDA(cudaStreamSynchronize(st));
+    if (dbg) {
+      tm[3] = now();
+      fprintf(stderr, "host call (%s): h2d %.2f ms, device %.2f ms, d2h %.2f ms\n",
+              stage ? "staged" : "pinned", (tm[1] - tm[0]) * 1e3, (tm[2] - tm[1]) * 1e3,
+              (tm[3] - tm[2]) * 1e3);
+    }
   }
   if (n_boundaries) *n_boundaries = nb;
 }

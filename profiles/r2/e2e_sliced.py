@@ -41,7 +41,7 @@ for env in ((None, "0", None) if os.environ.get("FIRST_SLICED") else ("0", None,
         wc.copy_(pc)
         wv.copy_(pv)
         t0 = time.perf_counter()
-        qd.transpose_inplace(tens, [0, 2, 1], qd.SortStrategy.quesadilla(), ws)
+        qd.transpose_inplace(tens, [int(ch) for ch in os.environ.get("TARGET", "021")], qd.SortStrategy.quesadilla(), ws)
         dt = time.perf_counter() - t0
         print(f"QD_SLICE_ROWS={env}: {ws.slices()} slices, {dt * 1e3:.1f} ms, "
               f"{n / dt / 1e6:.1f} Mnnz/s", flush=True)

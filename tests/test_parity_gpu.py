@@ -1059,6 +1059,14 @@ def test_small_engine_preconditions(ws):
             c2, v2, _ = ORC.transpose(dims, oor.ravel(), t.values, target)
             c, v = run(dims, oor.ravel(), t.values, target, bufs)
             assert np.array_equal(c, c2) and np.array_equal(v, v2.view(np.uint64)), ("prefix", target)
+            # the same in a LARGE run and too wide for its packed field: k_small's
+            # redo takes the general path, whose packed attempt is redone unpacked
+            # (that second redo must not go back to k_small)
+            big = t.coords.reshape(-1, r).copy()
+            big[-5000:, 0] = 4 * dims[0] + 3
+            c3, v3, _ = ORC.transpose(dims, big.ravel(), t.values, target)
+            c, v = run(dims, big.ravel(), t.values, target, bufs)
+            assert np.array_equal(c, c3) and np.array_equal(v, v3.view(np.uint64)), ("wide prefix", target)
         # a key coordinate out of range: the reference's out_of_range
         key_mode = {(0, 2, 1): 2, (2, 1, 0): 2, (0, 1, 4, 2, 3): 4}[tuple(target)]
         kb = t.coords.reshape(-1, r).copy()
