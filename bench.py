@@ -19,6 +19,8 @@ diagnostics).
           (qd_transpose_inplace on host buffers = transpose_inplace's
           signature, transpose.hpp:59-61): every H2D byte, the device passes
           and every D2H byte inside the timed region, one call per target
+          (the library pipelines a target that keeps the leading mode,
+          (0,2,1), slice by slice: e2e.per_target reports the slice count)
   roofline : the dominant kernel class, algorithmic bytes / its event-timed
           duration (recorded by the library on its launch stream) vs the
           measured HBM copy peak (MEASURED_PEAKS.json); model_roofline = the
