@@ -2741,6 +2741,7 @@ struct ModeList {
 // instead of the coordinates again (c5 (0,2,1): 20.9 GB less to read).
 struct HeadsExtra {
   uint8_t* digits;  // nullptr: run discovery only
+  int quad;         // k_heads_quad (rank 3/4, one prefix mode, aligned rows, <= 2 digit fields)
   ErrBlock* err;
   int do_check, check_pack;
   uint32_t pack_lim[kMaxKeys];
@@ -2823,6 +2824,125 @@ __global__ void __launch_bounds__(kThreads) k_heads(const uint32_t* c, uint32_t 
     cnt += head;
     if (ex.digits && i < nnz) heads_extra_row(ex, ex_dg, ex_fast, c, rank, i);
   }
+  __shared__ uint32_t s_tmp[64];
+  uint32_t tot;
+  block_excl_scan(cnt, s_tmp, &tot);
+  if (threadIdx.x == 0) block_cnt[blockIdx.x] = tot;
+}
+
+// k_heads + HeadsExtra for rank-3 / rank-4 AoS rows with ONE prefix mode, four
+// consecutive rows per thread from 16-byte loads (rank 3: three loads hold four
+// rows; rank 4: one load per row): head flags, range/pack checks and the first
+// digit all come from the registers, the four digit bytes leave as one word and
+// the head bits of a 32-row word are assembled from eight lanes' nibbles.
+// `c` must be 16-byte aligned.
+template <int RT>
+struct QuadRows {
+  uint32_t w[4][RT];
+};
+template <int RT>
+__device__ __forceinline__ QuadRows<RT> load_quad(const uint32_t* __restrict__ c, uint64_t nnz,
+                                                  unsigned long long i0) {
+  QuadRows<RT> r;
+  if (i0 + 3 < nnz) {
+    if constexpr (RT == 3) {
+      const uint4* q = reinterpret_cast<const uint4*>(c + i0 * 3);
+      const uint4 a = __ldcs(q), b = __ldcs(q + 1), d = __ldcs(q + 2);
+      r.w[0][0] = a.x; r.w[0][1] = a.y; r.w[0][2] = a.z;
+      r.w[1][0] = a.w; r.w[1][1] = b.x; r.w[1][2] = b.y;
+      r.w[2][0] = b.z; r.w[2][1] = b.w; r.w[2][2] = d.x;
+      r.w[3][0] = d.y; r.w[3][1] = d.z; r.w[3][2] = d.w;
+    } else {
+      const uint4* q = reinterpret_cast<const uint4*>(c + i0 * 4);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint4 a = __ldcs(q + k);
+        r.w[k][0] = a.x; r.w[k][1] = a.y; r.w[k][2] = a.z; r.w[k][3] = a.w;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int m = 0; m < RT; ++m) r.w[k][m] = i0 + k < nnz ? __ldg(c + (i0 + k) * RT + m) : 0u;
+  }
+  return r;
+}
+
+template <int RT>
+__global__ void __launch_bounds__(kThreads) k_heads_quad(const uint32_t* __restrict__ c, uint64_t nnz,
+                                                         uint32_t pm, uint32_t* words,
+                                                         uint32_t* block_cnt, HeadsExtra ex) {
+  static_assert(RT == 3 || RT == 4, "rank 3 or 4");
+  const unsigned long long r0 = (unsigned long long)blockIdx.x * kHeadRows;
+  const int lane = threadIdx.x & 31;
+  const Dig2 dg = dig2_of(ex.dig);
+  uint32_t lim[RT];
+#pragma unroll
+  for (int m = 0; m < RT; ++m) {
+    lim[m] = 0xFFFFFFFFu;
+    if (ex.do_check)
+      for (uint32_t k = 0; k < ex.key.n; ++k)
+        if (ex.key.mode[k] == m) lim[m] = ex.key.dim[k];
+    if (ex.check_pack) lim[m] = min(lim[m], ex.pack_lim[m]);
+  }
+#define QD_SEL(k, m) \
+  ((m) == 0u ? row.w[k][0] : ((m) == 1u ? row.w[k][1] : ((RT == 3 || (m) == 2u) ? row.w[k][2] : row.w[k][RT - 1])))
+  uint32_t cnt = 0;
+  auto process = [&](const QuadRows<RT> row, const unsigned long long i0) {
+    const bool full = i0 + 3 < nnz;
+    uint32_t pv[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) pv[k] = QD_SEL(k, pm);
+    uint32_t prev = __shfl_up_sync(0xFFFFFFFFu, pv[3], 1);
+    if (lane == 0) prev = (i0 > 0 && i0 < nnz) ? __ldg(c + (i0 - 1) * RT + pm) : 0u;
+    uint32_t nib = 0, dword = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const unsigned long long i = i0 + k;
+      const bool valid = i < nnz;
+      const bool head = valid && (i == 0 || pv[k] != (k ? pv[k - 1] : prev));
+      nib |= (uint32_t)head << k;
+      cnt += head;
+      if (valid) {
+        bool over = false;
+#pragma unroll
+        for (int m = 0; m < RT; ++m) over |= row.w[k][m] >= lim[m];
+        if (over) {  // rare: the exact checks (range: first (row, mode); pack: flag)
+          if (ex.do_check) check_row(c + i * RT, ex.key, i, ex.err);
+          if (ex.check_pack) {
+            bool bad = false;
+#pragma unroll
+            for (int m = 0; m < RT; ++m) bad |= row.w[k][m] >= ex.pack_lim[m];
+            if (bad) atomicOr(&ex.err->flags, 4u);
+          }
+        }
+        uint32_t d = ((QD_SEL(k, dg.m0) >> dg.r0) & dg.k0) << dg.l0;
+        if (dg.two) d |= ((QD_SEL(k, dg.m1) >> dg.r1) & dg.k1) << dg.l1;
+        dword |= (d & 0xFFu) << (8 * k);
+      }
+    }
+    // the 32-row head word = the nibbles of eight consecutive lanes
+    uint32_t x = nib << (4 * (lane & 7));
+    x |= __shfl_xor_sync(0xFFFFFFFFu, x, 1);
+    x |= __shfl_xor_sync(0xFFFFFFFFu, x, 2);
+    x |= __shfl_xor_sync(0xFFFFFFFFu, x, 4);
+    if ((lane & 7) == 0 && i0 < nnz) words[i0 >> 5] = x;
+    if (full) {
+      *reinterpret_cast<uint32_t*>(ex.digits + i0) = dword;
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (i0 + k < nnz) ex.digits[i0 + k] = (uint8_t)(dword >> (8 * k));
+    }
+  };
+  // one quad at a time (two in flight: 63 registers, 0.99 -> 1.15 ms per 400 M rows)
+#pragma unroll 1
+  for (uint32_t it = 0; it < kHeadRows / (4 * kThreads); ++it) {
+    const unsigned long long ia = r0 + 4ull * (it * kThreads + threadIdx.x);
+    process(load_quad<RT>(c, nnz, ia), ia);
+  }
+#undef QD_SEL
   __shared__ uint32_t s_tmp[64];
   uint32_t tot;
   block_excl_scan(cnt, s_tmp, &tot);
@@ -3851,7 +3971,12 @@ uint64_t find_runs(Ctx& c, const uint32_t* coords, uint32_t rank, uint64_t nnz,
   auto* boff = c.ws.get<unsigned long long>("head_boff", nb + 1);
   auto* tot = c.ws.get<unsigned long long>("head_total", 1);
   c.pre();
-  k_heads<<<nb, kThreads, 0, c.st>>>(coords, rank, nnz, ml, words, bcnt, extra ? *extra : HeadsExtra{});
+  if (extra && extra->quad && rank == 3)
+    k_heads_quad<3><<<nb, kThreads, 0, c.st>>>(coords, nnz, ml.m[0], words, bcnt, *extra);
+  else if (extra && extra->quad && rank == 4)
+    k_heads_quad<4><<<nb, kThreads, 0, c.st>>>(coords, nnz, ml.m[0], words, bcnt, *extra);
+  else
+    k_heads<<<nb, kThreads, 0, c.st>>>(coords, rank, nnz, ml, words, bcnt, extra ? *extra : HeadsExtra{});
   c.launched(kSegK);
   scan_exclusive(c, bcnt, nb, boff, tot);
   if (S_dev_out) *S_dev_out = tot;
@@ -4289,19 +4414,24 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
     c.launched(kSegK);
   } else {
     unsigned long long* S_found = nullptr;
-    // QD_FUSE_HEADS=1: run discovery also range-checks, pack-checks and
+    // Run discovery also does the first pass's range and pack checks and
     // leaves every row's first digit as a byte, so the first histogram reads
-    // 1 byte per row instead of the coordinates again (HeadsExtra).  Measured
-    // SLOWER and off by default: the per-row strided loads and byte stores
-    // cost k_heads more than the histogram saves (c5 (0,2,1) 58.4 -> 62.3 ms,
-    // c2 (0,2,1) 2.17 -> 2.33 ms, c3 (0,3,1,2) 4.03 -> 4.24 ms).
-    static const bool fuse_heads = [] {
+    // 1 byte per row instead of the coordinates again (HeadsExtra): for
+    // rank-3/4 rows with one prefix mode through k_heads_quad.  The generic
+    // per-row form (QD_FUSE_HEADS=2: any rank / prefix) measured SLOWER — its
+    // strided loads and byte stores cost k_heads more than the histogram
+    // saves (c5 (0,2,1) 58.4 -> 62.3 ms).  QD_FUSE_HEADS=0: off.
+    static const int fuse_mode = [] {
       const char* e = getenv("QD_FUSE_HEADS");
-      return e && atoi(e) == 1;
+      return e ? atoi(e) : 1;
     }();
+    const bool quad_ok = (R == 3 || R == 4) && g.prefix.size() == 1 && digs[0].lookup == nullptr &&
+                         digs[0].n <= 2 && (reinterpret_cast<uintptr_t>(src_c) & 15u) == 0;
+    const bool fuse_heads = fuse_mode == 2 || (fuse_mode == 1 && quad_ok);
     HeadsExtra hx{};
     if (fuse_heads && side) {
       hx.digits = ws.get<uint8_t>("digits", N + 16);
+      hx.quad = fuse_mode == 1;
       hx.err = c.err;
       hx.do_check = key.check;
       hx.check_pack = packed;

@@ -1105,3 +1105,53 @@ def test_large_bucketed_group_prefix_order(ws):
     c1, v1, _ = ORC.transpose(dims, tb.coords, tb.values, [0, 2, 1])
     out = qd.transpose(tb, [0, 2, 1], ws=ws)
     assert same(out, c1, v1)
+
+
+# --- run discovery fused with the first digit pass (k_heads_quad) -------------
+
+@pytest.mark.parametrize("dims,target", [([50, 700, 3000], [0, 2, 1]), ([30, 40, 900, 70], [0, 3, 1, 2]),
+                                         ([30, 40, 900, 70], [0, 2, 1, 3])])
+def test_fused_run_discovery_sizes(ws, dims, target):
+    """Bucketed groups of rank-3/4 tensors with one prefix mode take
+    k_heads_quad (four rows per thread; head words from eight lanes' nibbles;
+    the first digit as a byte per row; range and pack checks): row counts
+    around the quad / word / CTA boundaries, a giant run beside tiny ones, the
+    reference's out_of_range (first bad row), and device rows that are NOT
+    16-byte aligned (the per-row kernel) must all give the oracle's rows."""
+    import torch
+    rng = np.random.default_rng(123)
+    r = len(dims)
+    for n in (1, 2, 3, 5, 31, 33, 127, 129, 4095, 4097, 8191, 20_001, 131_075):
+        t = rand_tensor(rng, dims, n)
+        co = t.coords.reshape(-1, r).copy()
+        co[: n // 2, 0] = 0  # one long run (large), then short ones
+        co = co[np.lexsort(co.T[::-1])]
+        t = qd.CooTensor(dims, co.ravel(), t.values)
+        out = qd.transpose(t, target, ws=ws)
+        c, v, _ = ORC.transpose(dims, t.coords, t.values, target)
+        assert same(out, c, v), (n, target)
+    # a key coordinate out of range in two rows: the first one is reported
+    n = 50_000
+    t = rand_tensor(rng, dims, n)
+    co = t.coords.reshape(-1, r).copy()
+    km = target[1]  # the mode the plan sorts (the others are never range-checked)
+    co[40_001, km] = dims[km]
+    co[17_003, km] = dims[km] + 5
+    with pytest.raises(qd.OutOfRange) as ei:
+        qd.transpose(qd.CooTensor(dims, co.ravel(), t.values), target, ws=ws)
+    with pytest.raises(OracleError):
+        ORC.transpose(dims, co.ravel(), t.values, target)
+    assert ei.value.row == 17_003 and ei.value.mode == km
+    # misaligned device rows: a view starting at row 1 of a device buffer
+    t = rand_tensor(rng, dims, 30_001)
+    ci = torch.from_numpy(t.coords.view(np.int32)).cuda()
+    vi = torch.from_numpy(t.values).cuda()
+    co_ = torch.empty_like(ci)
+    vo_ = torch.empty_like(vi)
+    m = 30_000
+    qd.transpose_device(r, dims, m, ci.data_ptr() + 4 * r, vi.data_ptr() + 8, co_.data_ptr() + 4 * r,
+                        vo_.data_ptr() + 8, target, qd.SortStrategy.quesadilla(), ws, 0)
+    torch.cuda.synchronize()
+    c, v, _ = ORC.transpose(dims, t.coords[r:], t.values[1:], target)
+    assert np.array_equal(co_[r:].cpu().numpy().view(np.uint32), c)
+    assert np.array_equal(vo_[1:].cpu().numpy().view(np.uint64), v.view(np.uint64))
