@@ -4119,7 +4119,7 @@ void run_pass(Ctx& c, uint32_t R, uint64_t N, uint32_t T, Rows in, RowsOut out,
               uint8_t* digits_out = nullptr, uint32_t nd_shift = 0, uint32_t nd_mask = 0,
               const DigitSpec* next_dig = nullptr, const uint32_t* run_prefix = nullptr,
               const PeerDest* peers = nullptr, bool peers_aligned = false,
-              const unsigned long long* nc_dev = nullptr) {
+              const unsigned long long* nc_dev = nullptr, bool scattered_digits = false) {
   Workspace& ws = c.ws;
   const uint64_t nflat = num_chunks * kBins;
   auto* flat = ws.get<uint32_t>("chunk_flat", nflat);
@@ -4208,7 +4208,7 @@ void run_pass(Ctx& c, uint32_t R, uint64_t N, uint32_t T, Rows in, RowsOut out,
   {
     static const int rank_mode = [] {
       const char* e = getenv("QD_RANK_MODE");
-      return e ? atoi(e) : 0;  // MATCH only: ballots measured slower on c2/c3/c5
+      return e ? atoi(e) : 3;  // 0 MATCH.ANY, 1 adaptive, 2 ballots, 3 (default) by pass
     }();
     static const uint32_t match_max = [] {
       const char* e = getenv("QD_MATCH_MAX");
@@ -4222,7 +4222,17 @@ void run_pass(Ctx& c, uint32_t R, uint64_t N, uint32_t T, Rows in, RowsOut out,
     }
     if (in.fmt == kPK) nb = (uint32_t)__builtin_popcount(pk_mask);
     a.dbits = std::min<uint32_t>(8, std::max<uint32_t>(1, nb));
-    a.rank_mode = rank_mode;
+    // by pass: ballots where the planner expects nearly random digits within
+    // a tile (the first digit of a group whose least significant key mode is
+    // the fastest-varying mode of the rows' order: a warp's 32 digits are then
+    // nearly all distinct and MATCH.ANY costs ~2 cycles per distinct value);
+    // every other pass sees digit runs, where MATCH.ANY wins.  400 M rows of
+    // c5 (0,2,1): first pass 3.05 -> 2.89 ms with ballots, later passes
+    // +3-14 %; c2 (2,0,1) 1.83 -> 1.76 ms, (1,2,0) 3.17 -> 3.11 ms, while
+    // (1,0,2) and (2,1,0) (key mode 1 first) lose 4-9 % with ballots.
+    a.rank_mode = rank_mode == 3 ? (scattered_digits && !dig.lookup ? 2 : 0)
+                  : rank_mode == 4 ? ((pk_shift == 0 && !dig.lookup) ? 2 : 0)  // experiment: every first pass
+                                   : rank_mode;
     a.match_max = match_max;
   }
   if (a.dbg & 2) {
@@ -4551,7 +4561,7 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
                q == 0 && key.check, nullptr, packed ? &pack : nullptr, lo,
                (1u << (hi - lo)) - 1u, dig_in, dig_out, nlo, last ? 0u : (1u << (nhi - nlo)) - 1u,
                last ? nullptr : &digs[q + 1], run_prefix, nullptr, false,
-               lat_counts ? lat_counts + 1 : nullptr);
+               lat_counts ? lat_counts + 1 : nullptr, q == 0 && g.first_digit_scattered);
       in = Rows{out.c, out.v, out.fmt};
     }
   }

@@ -50,6 +50,11 @@ struct Group {
   // comparison phases (sort_rows_by) do not, and then key widths come from
   // the data instead of the dimensions.
   bool check_range = true;
+  // Hint from the planner (a simply sorted source assumed): the least
+  // significant key mode is the fastest-varying mode of the rows' current
+  // order, so the first digit pass sees nearly random digits within a tile
+  // (the engine then ranks that pass with ballots instead of MATCH.ANY).
+  bool first_digit_scattered = false;
 };
 
 // Groups for a whole strategy (transpose.cpp:79-112): the LOGICAL steps go to

@@ -154,6 +154,18 @@ std::vector<Group> strategy_groups(const uint32_t* target, uint32_t rank,
     default:
       invalid("unknown strategy kind");
   }
+  // the rows' ordering before each group, from a simple source (0, 1, ...):
+  // a group leaves its prefix, then its keys, then the other modes as they were
+  std::vector<uint32_t> cur(rank);
+  for (uint32_t m = 0; m < rank; ++m) cur[m] = m;
+  for (Group& g : groups) {
+    g.first_digit_scattered = rank > 1 && !g.keys.empty() && g.keys.back() == cur[rank - 1];
+    std::vector<uint32_t> next(g.prefix);
+    next.insert(next.end(), g.keys.begin(), g.keys.end());
+    for (uint32_t m : cur)
+      if (std::find(next.begin(), next.end(), m) == next.end()) next.push_back(m);
+    cur = next;
+  }
   if (steps_out) *steps_out = steps;
   return groups;
 }
