@@ -4310,7 +4310,13 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
   const uint32_t D = (bits + kRadixLog - 1) / kRadixLog;
   const uint32_t per = (bits + D - 1) / D;
   std::vector<DigitSpec> digs(D);
-  for (uint32_t q = 0; q < D; ++q) digs[q] = make_digit(key, q * per, std::min(bits, (q + 1) * per));
+  // digit q = key bits [cut[q], cut[q+1]): `per` bits each from the bottom,
+  // the last one narrower (the narrower digit FIRST for groups whose first
+  // digit is scattered measured slower: c2 (0,2,1) 2.04 -> 2.12, (2,0,1)
+  // 1.77 -> 1.88, (1,2,0) 3.10 -> 3.29 ms)
+  std::vector<uint32_t> cut(D + 1);
+  for (uint32_t q = 0; q <= D; ++q) cut[q] = std::min(bits, q * per);
+  for (uint32_t q = 0; q < D; ++q) digs[q] = make_digit(key, cut[q], cut[q + 1]);
 
   const uint32_t T = sweep_tile_rows(ws, R);
   static const bool per_fmt_tiles = [] {
@@ -4547,12 +4553,12 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
       const int ofmt = last ? kAoS : (packed ? kPK : (unpacked_soa ? kSoA : kAoS));
       RowsOut out{to_dst ? dst_c : tmp_c, to_dst ? dst_v : tmp_v, ofmt};
       if (ofmt == kPK) out = RowsOut{pk[q % 2], nullptr, kPK};
-      const uint32_t lo = q * per, hi = std::min(bits, lo + per);
+      const uint32_t lo = cut[q], hi = cut[q + 1];
       // packed passes hand the next pass its digit bytes (1 B/row instead of
       // re-reading 16 B rows for the next histogram)
       const uint8_t* dig_in = (side && (q > 0 || fused_first)) ? digbuf : nullptr;
       uint8_t* dig_out = (side && !last) ? digbuf : nullptr;
-      const uint32_t nlo = (q + 1) * per, nhi = std::min(bits, nlo + per);
+      const uint32_t nlo = cut[std::min(q + 1, D)], nhi = cut[std::min(q + 2, D)];
       // packed-row passes afford a larger tile (16-byte staged rows)
       const uint32_t Tq = (per_fmt_tiles && in.fmt == kPK) ? sweep_tile_rows(ws, R, kPK) : T;
       NvtxRange r_pass("pass " + std::to_string(q) + " bits [" + std::to_string(lo) + "," +
