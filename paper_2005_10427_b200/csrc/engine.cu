@@ -4316,6 +4316,18 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
   // 1.77 -> 1.88, (1,2,0) 3.10 -> 3.29 ms)
   std::vector<uint32_t> cut(D + 1);
   for (uint32_t q = 0; q <= D; ++q) cut[q] = std::min(bits, q * per);
+  if (const char* e = getenv("QD_CUTS")) {  // experiment: explicit upper cuts "8,15,21" for keys of that width
+    std::vector<uint32_t> v;
+    for (const char* p = e; *p;) {
+      v.push_back((uint32_t)strtoul(p, const_cast<char**>(&p), 10));
+      if (*p == ',') ++p;
+    }
+    bool ok = v.size() == D && v.back() == bits;
+    for (size_t i = 0; ok && i < v.size(); ++i)
+      ok = v[i] > (i ? v[i - 1] : 0u) && v[i] - (i ? v[i - 1] : 0u) <= (uint32_t)kRadixLog;
+    if (ok)
+      for (uint32_t q = 0; q < D; ++q) cut[q + 1] = v[q];
+  }
   for (uint32_t q = 0; q < D; ++q) digs[q] = make_digit(key, cut[q], cut[q + 1]);
 
   const uint32_t T = sweep_tile_rows(ws, R);
