@@ -2897,11 +2897,12 @@ __global__ void __launch_bounds__(kThreads) k_heads_quad(const uint32_t* __restr
     uint32_t prev = __shfl_up_sync(0xFFFFFFFFu, pv[3], 1);
     if (lane == 0) prev = (i0 > 0 && i0 < nnz) ? __ldg(c + (i0 - 1) * RT + pm) : 0u;
     uint32_t nib = 0, dword = 0;
+    const bool first = i0 == 0;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const unsigned long long i = i0 + k;
-      const bool valid = i < nnz;
-      const bool head = valid && (i == 0 || pv[k] != (k ? pv[k - 1] : prev));
+      const bool valid = full || i < nnz;  // (one test per quad on the common path)
+      const bool head = valid && ((k == 0 && first) || pv[k] != (k ? pv[k - 1] : prev));
       nib |= (uint32_t)head << k;
       cnt += head;
       if (valid) {

@@ -69,8 +69,8 @@ def main():
     ki, mi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
     scale = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}
     seq = [(r[ki].split("(")[0], float(r[mi].replace(",", "")) * scale[r[ui]]) for r in rows]
-    # the two targets: (1,0,2) first (no k_heads), (0,2,1) starts at its first k_heads
-    split = next(i for i, (k, _) in enumerate(seq) if k.startswith("k_heads"))
+    # the two targets: (1,0,2) first (no run discovery), (0,2,1) starts at its k_heads / k_heads_quad
+    split = next(i for i, (k, _) in enumerate(seq) if "k_heads" in k)
     with open(os.path.join(OUT, "launches_summary.txt"), "w") as f:
         f.write("# ncu --metrics gpu__time_duration.sum --clock-control none, profiles/r2/prof_targets.py "
                 "--config c5: one transposition per target at full size (cold cache, serialised)\n")
@@ -106,7 +106,7 @@ def main():
         for row in data:
             d = dict(zip(hh, row))
             name = d["Kernel Name"].split("(")[0]
-            if name.startswith("k_heads"):
+            if "k_heads" in name:
                 tgt = "(0,2,1)"  # its run discovery opens the second target
             rd = float(d["dram__bytes_read.sum"].replace(",", ""))
             wr = float(d["dram__bytes_write.sum"].replace(",", ""))
