@@ -304,6 +304,7 @@ struct ChunkHistArgs {
   unsigned long long* rows_counter;
   uint32_t pk_shift, pk_mask;  // digit of a PK row
   int check_pack;              // flag bit2 if a coordinate would not pack losslessly
+  uint32_t lim[4];             // rank <= 4: per mode, min(key dimension if checked, pack limit), host-folded
   PackSpec pack;
   const uint8_t* digits;       // this pass's digit per row, written by the previous scatter
 };
@@ -841,15 +842,7 @@ __global__ void __launch_bounds__(kThreads) k_chunk_hist(ChunkHistArgs a) {
     if (a.in.fmt == kAoS && R == 4 && fast_dig && ((uintptr_t)a.in.c & 15u) == 0) {
       // AoS rank-4 rows are aligned 16-byte vectors: one load per row, two
       // rows in flight per thread, range + pack checks from the registers
-      uint32_t lim[4];
-#pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        lim[m] = 0xFFFFFFFFu;
-        if (a.do_check)
-          for (uint32_t k = 0; k < a.key.n; ++k)
-            if (a.key.mode[k] == m) lim[m] = a.key.dim[k];
-        if (a.check_pack) lim[m] = min(lim[m], a.pack.lim[m]);
-      }
+      const uint32_t lim[4] = {a.lim[0], a.lim[1], a.lim[2], a.lim[3]};
       uint32_t* wh = s_h + w * kBins;
       const uint4* rows4 = reinterpret_cast<const uint4*>(a.in.c) + cd.row_begin;
       auto sel = [&](const uint4& x, uint32_t m) {
@@ -885,15 +878,7 @@ __global__ void __launch_bounds__(kThreads) k_chunk_hist(ChunkHistArgs a) {
       const uint32_t dm0 = dg.m0, dm1 = dg.m1;
       // per-mode limits: range check (dim for key modes) and pack check
       // (2^width) folded into one compare per coordinate
-      uint32_t lim[3];
-#pragma unroll
-      for (int m = 0; m < 3; ++m) {
-        lim[m] = 0xFFFFFFFFu;
-        if (a.do_check)
-          for (uint32_t k = 0; k < a.key.n; ++k)
-            if (a.key.mode[k] == m) lim[m] = a.key.dim[k];
-        if (a.check_pack) lim[m] = min(lim[m], a.pack.lim[m]);
-      }
+      const uint32_t lim[3] = {a.lim[0], a.lim[1], a.lim[2]};
       uint32_t* wh = s_h + w * kBins;
       auto digit3 = [&](uint32_t c0, uint32_t c1, uint32_t c2) {
         const uint32_t x0 = dm0 == 0 ? c0 : (dm0 == 1 ? c1 : c2);
@@ -2742,6 +2727,7 @@ struct ModeList {
 struct HeadsExtra {
   uint8_t* digits;  // nullptr: run discovery only
   int quad;         // k_heads_quad (rank 3/4, one prefix mode, aligned rows, <= 2 digit fields)
+  uint32_t lim[4];  // k_heads_quad: per mode, min(key dimension if range-checked, pack limit)
   ErrBlock* err;
   int do_check, check_pack;
   uint32_t pack_lim[kMaxKeys];
@@ -2877,15 +2863,11 @@ __global__ void __launch_bounds__(kThreads) k_heads_quad(const uint32_t* __restr
   const unsigned long long r0 = (unsigned long long)blockIdx.x * kHeadRows;
   const int lane = threadIdx.x & 31;
   const Dig2 dg = dig2_of(ex.dig);
+  // (per-mode limits folded on the host: building them here from the key
+  // spec cost ~600 instructions per thread, 37 per row at 16 rows per thread)
   uint32_t lim[RT];
 #pragma unroll
-  for (int m = 0; m < RT; ++m) {
-    lim[m] = 0xFFFFFFFFu;
-    if (ex.do_check)
-      for (uint32_t k = 0; k < ex.key.n; ++k)
-        if (ex.key.mode[k] == m) lim[m] = ex.key.dim[k];
-    if (ex.check_pack) lim[m] = min(lim[m], ex.pack_lim[m]);
-  }
+  for (int m = 0; m < RT; ++m) lim[m] = ex.lim[m];
 #define QD_SEL(k, m) \
   ((m) == 0u ? row.w[k][0] : ((m) == 1u ? row.w[k][1] : ((RT == 3 || (m) == 2u) ? row.w[k][2] : row.w[k][RT - 1])))
   uint32_t cnt = 0;
@@ -4146,6 +4128,14 @@ void run_pass(Ctx& c, uint32_t R, uint64_t N, uint32_t T, Rows in, RowsOut out,
     h.pack = *pack;
     h.check_pack = in.fmt == kAoS && out.fmt == kPK;
   }
+  for (uint32_t m = 0; m < 4; ++m) {
+    h.lim[m] = 0xFFFFFFFFu;
+    if (m >= R) continue;
+    if (h.do_check)
+      for (uint32_t k = 0; k < key.n; ++k)
+        if (key.mode[k] == m) h.lim[m] = key.dim[k];
+    if (h.check_pack) h.lim[m] = std::min(h.lim[m], h.pack.lim[m]);
+  }
   c.pre();
   k_chunk_hist<<<(uint32_t)std::min<uint64_t>(num_chunks, (uint64_t)ws.num_sms * 8), kThreads, 0,
                  c.st>>>(h);
@@ -4461,6 +4451,14 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
     if (fuse_heads && side) {
       hx.digits = ws.get<uint8_t>("digits", N + 16);
       hx.quad = fuse_mode == 1;
+      for (uint32_t m = 0; m < 4; ++m) {
+        hx.lim[m] = 0xFFFFFFFFu;
+        if (m >= R) continue;
+        if (key.check)
+          for (uint32_t k = 0; k < key.n; ++k)
+            if (key.mode[k] == m) hx.lim[m] = key.dim[k];
+        if (packed) hx.lim[m] = std::min(hx.lim[m], pack.lim[m]);
+      }
       hx.err = c.err;
       hx.do_check = key.check;
       hx.check_pack = packed;
