@@ -506,6 +506,20 @@ __device__ __forceinline__ unsigned ballot_peers(uint32_t d, unsigned valid, uin
   }
   return m;
 }
+// the same for digits of up to MAXB bits (k_local3's 9-bit digits)
+template <int MAXB>
+__device__ __forceinline__ unsigned ballot_peers_n(uint32_t d, unsigned valid, uint32_t nbits) {
+  unsigned m = valid;
+#pragma unroll
+  for (uint32_t b = 0; b < (uint32_t)MAXB; ++b) {
+    if (b < nbits) {  // warp-uniform
+      const unsigned bit = (d >> b) & 1u;
+      const unsigned v = __ballot_sync(0xFFFFFFFFu, bit);
+      m &= bit ? v : ~v;
+    }
+  }
+  return m;
+}
 __device__ __forceinline__ unsigned adaptive_peers(uint32_t d, unsigned valid, uint32_t nbits,
                                                    int mode, uint32_t match_max) {
   if (mode == 0) return __match_any_sync(0xFFFFFFFFu, d) & valid;
@@ -2072,6 +2086,7 @@ struct Local2Args {
   DigitSpec dig[kMaxLocalPasses];
   uint32_t dig_bits[kMaxLocalPasses];
   ErrBlock* err;
+  uint32_t ballot_passes;  // k_local3: bit q = pass q ranks with ballots instead of MATCH.ANY
 };
 
 struct Local2Layout {
@@ -2623,7 +2638,13 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_local3(Local2Args a) {
         if (lo + r * 32 >= hi) break;  // warp-uniform
         const bool valid = p < hi;
         const uint32_t d = valid ? (uint32_t)(kc[p] >> sh) & mask : 0xFFFFFFFFu;
-        const unsigned peers = __match_any_sync(0xFFFFFFFFu, d);
+        unsigned peers;
+        if ((a.ballot_passes >> q) & 1u) {  // warp-uniform
+          const unsigned vm = __ballot_sync(0xFFFFFFFFu, valid);
+          peers = ballot_peers_n<kLocalBitsMax>(d, vm, dbits);
+        } else {
+          peers = __match_any_sync(0xFFFFFFFFu, d);
+        }
         const uint32_t c = valid ? wh[d] : 0u;
         __syncwarp();
         if (valid && (peers & below) == 0u) wh[d] = (uint16_t)(c + __popc(peers));
@@ -4634,6 +4655,14 @@ void segmented_sort(Ctx& c, const TensorView& t, const uint32_t* src_c, const do
       la.dig_bits[q] = hi - lo;
     }
     la.err = c.err;
+    {
+      // QD_LOCAL3_BALLOT: bit q = pass q of k_local3 ranks with ballots
+      static const int bp = [] {
+        const char* e = getenv("QD_LOCAL3_BALLOT");
+        return e ? atoi(e) : 0;
+      }();
+      la.ballot_passes = (uint32_t)bp;
+    }
     using LocalFn = void (*)(Local2Args);
     const int nt = local_v == 3 ? l3_threads : kLocal2Threads;
     const LocalFn fn =
