@@ -2962,6 +2962,9 @@ __global__ void __launch_bounds__(kThreads) k_compact(const uint32_t* words, uin
                                                       const unsigned long long* total) {
   const unsigned long long w0 = (unsigned long long)blockIdx.x * (kHeadRows / 32);
   const unsigned long long nwords = (nnz + 31) / 32;
+  // a block without heads (most blocks inside long runs) has nothing to write
+  const bool last = blockIdx.x == nblocks - 1;
+  if (!last && block_off[blockIdx.x + 1] == block_off[blockIdx.x]) return;
   __shared__ uint32_t s_tmp[64];
   // kHeadRows/32 = 128 words per CTA; threads 0..127 own one word each
   const unsigned long long wi = w0 + threadIdx.x;
