@@ -2731,7 +2731,11 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_local3(Local2Args a) {
 // ---------------------------------------------------------------------------
 // segment discovery
 // ---------------------------------------------------------------------------
-constexpr uint32_t kHeadRows = 4096;  // rows per k_heads CTA (128 words)
+#ifndef QD_HEAD_ROWS
+#define QD_HEAD_ROWS 4096
+#endif
+constexpr uint32_t kHeadRows = QD_HEAD_ROWS;  // rows per k_heads CTA (words = rows / 32 <= kThreads)
+static_assert(kHeadRows / 32 <= (uint32_t)kThreads && (kHeadRows / kThreads) % 8 == 0, "k_heads/k_compact block shape");
 
 struct ModeList {
   uint32_t n;
