@@ -3790,6 +3790,11 @@ struct Ctx {
     cudaEvent_t a, b;
     int group;
     int all_rows;  // local: 1 = every row of the group, 0 = rows outside large runs
+    // rows and rank of the arrays a digit pass ran over (0: the call's): the
+    // passes over run RECORDS of a run-level sort move far fewer rows than
+    // the tensor has, and must not be credited with the tensor's bytes
+    unsigned long long pass_rows;
+    uint32_t pass_rank;
   };
   std::vector<Rec> recs;
   cudaEvent_t pending = nullptr;
@@ -3809,13 +3814,14 @@ struct Ctx {
       QD_CUDA(cudaEventRecord(pending, st));
     }
   }
-  void launched(int cls = kOtherK, int all_rows = 0) {
+  void launched(int cls = kOtherK, int all_rows = 0, unsigned long long pass_rows = 0,
+                uint32_t pass_rank = 0) {
     ++ws.launches;
     QD_CUDA(cudaGetLastError());
     if (ws.prof && pending) {
       cudaEvent_t b = ws.event();
       QD_CUDA(cudaEventRecord(b, st));
-      recs.push_back({cls, pending, b, std::min(group, kMaxGroups - 1), all_rows});
+      recs.push_back({cls, pending, b, std::min(group, kMaxGroups - 1), all_rows, pass_rows, pass_rank});
       pending = nullptr;
     }
   }
@@ -3825,10 +3831,16 @@ struct Ctx {
     for (auto& r : recs) {
       float ms = 0;
       QD_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
-      const double large = (double)e.rows[r.group];
+      double large = (double)e.rows[r.group];
+      double rb = row_bytes, rk = rank;
+      if (r.pass_rows) {
+        large = std::min(large, (double)r.pass_rows);
+        rb = 4.0 * r.pass_rank + 8.0;
+        rk = r.pass_rank;
+      }
       double bytes = 0;
-      if (r.cls == kSweep) bytes = large * 2 * row_bytes;
-      else if (r.cls == kHistK) bytes = large * 4.0 * rank;
+      if (r.cls == kSweep) bytes = large * 2 * rb;
+      else if (r.cls == kHistK) bytes = large * 4.0 * rk;
       else if (r.cls == kLocalK) bytes = (r.all_rows ? (double)nnz : (double)nnz - large) * 2 * row_bytes;
       auto& p = ws.prof_stats[r.cls];
       ++p.launches;
@@ -4167,7 +4179,7 @@ void run_pass(Ctx& c, uint32_t R, uint64_t N, uint32_t T, Rows in, RowsOut out,
   c.pre();
   k_chunk_hist<<<(uint32_t)std::min<uint64_t>(num_chunks, (uint64_t)ws.num_sms * 8), kThreads, 0,
                  c.st>>>(h);
-  c.launched(kHistK);
+  c.launched(kHistK, 0, N, R);
   scan_exclusive(c, flat, nflat, offs, tot, nc_dev, kBins);
 
   ScatterArgs a{};
@@ -4274,7 +4286,7 @@ void run_pass(Ctx& c, uint32_t R, uint64_t N, uint32_t T, Rows in, RowsOut out,
       (uint32_t)std::min<uint64_t>(num_chunks, (uint64_t)std::max(1, per_sm) * ws.num_sms);
   c.pre();
   fn<<<grid, kSortThreads, smem, c.st>>>(a);
-  c.launched(kSweep);
+  c.launched(kSweep, 0, N, R);
   if (a.dbg & 2) {
     unsigned long long h[16];
     QD_CUDA(cudaMemcpyAsync(h, a.dbg_t, 128, cudaMemcpyDeviceToHost, c.st));
