@@ -658,7 +658,10 @@ def run_e2e(args, cfg, qd, ws, hc0, hv0, r, n):
     strat = qd.SortStrategy.quesadilla()
     secs = 0.0
     per_t = {tname(t): {"ms": 0.0, "slices": 1} for t in cfg.targets}
+    step_ms = []  # each timed step's total (the host link of a shared box is noisy)
     for it in range(1 + k_e2e):  # one untimed warm-up step (workspace growth)
+        if it:
+            step_ms.append(0.0)
         for t in cfg.targets:
             wc.copy_(torch.from_numpy(hc0.view(np.int32)))
             wv.copy_(torch.from_numpy(hv0))
@@ -667,6 +670,7 @@ def run_e2e(args, cfg, qd, ws, hc0, hv0, r, n):
             dt = time.perf_counter() - t0
             if it:
                 secs += dt
+                step_ms[-1] += dt * 1e3
                 per_t[tname(t)]["ms"] += dt * 1e3 / k_e2e
                 # > 1: the call kept the leading mode, so the library cut the tensor
                 # where it changes and pipelined H2D / passes / D2H per slice
@@ -706,6 +710,7 @@ def run_e2e(args, cfg, qd, ws, hc0, hv0, r, n):
                       "inside), summed over the step's targets",
             "api": "qd_transpose_inplace (pinned host buffers) x targets",
             "per_target": per_t,
+            "steps_ms": [round(x, 1) for x in step_ms],
             "pageable": pageable}
 
 
